@@ -1,0 +1,160 @@
+/*
+ * morap_cuda.h -- C ABI of the B200 value-iteration backend (libmorap_cuda.so).
+ *
+ * This is the drop-in boundary for the reference's job engine. The reference runs every
+ * Bellman solve as a move-only Job through
+ *     std::map<long,JobResult> runBatch(std::vector<Job>, const PoolConfig&)
+ *         (/root/reference/proj/include/morap/engine.hpp:370-425; Job/JobResult :40-64)
+ * with CPU worker threads calling
+ *     optimalSchedulerOn   (numerics.hpp:74-122)   -- JobKind::Optimize
+ *     evaluateSchedulerOn  (numerics.hpp:130-168)  -- JobKind::Evaluate
+ * and the "stub accelerator" queues (engine.hpp:111,254-259) are where an accelerator
+ * was meant to plug in. Here the product MDPs are uploaded ONCE (the reference keeps them
+ * alive as shared_ptr<const ProductMdp> for the whole query, instance.hpp:26) and every
+ * batch of jobs runs on the GPU. Plain pointers and sizes only; nothing throws across the
+ * ABI; every function returns a status (0 = ok, otherwise 1 + morap::Errc, common.hpp:12-34).
+ *
+ * Arithmetic contract: fp64 values/probabilities/rewards, int32 indices (model.hpp:19-34).
+ * Each row value is accumulated left to right from rho[r] with separately rounded
+ * multiply and add (no FMA), ties in the argmax go to the lowest row, done states are
+ * pinned to 0, and each job stops at its own sweep -- so values, sweeps, residuals and
+ * policies are BITWISE identical to the reference CPU solver.
+ *
+ * Threading: a context is driven by one host thread at a time (SPEC.md:628 says the same
+ * of runBatch). Results do not depend on the device or on how jobs are batched.
+ */
+#ifndef MORAP_CUDA_H
+#define MORAP_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: 0 ok, else 1 + morap::Errc (common.hpp:12-34). */
+enum {
+  MORAP_OK = 0,
+  MORAP_SYNTAX = 1,
+  MORAP_NOT_CO_SAFE = 2,
+  MORAP_CLOSURE_BLOWUP = 3,
+  MORAP_INVALID_DFA = 4,
+  MORAP_INVALID_MODEL = 5,
+  MORAP_NOT_REWARD_FINITE = 6,
+  MORAP_NON_CONVERGENCE = 7,
+  MORAP_SINGULAR_SYSTEM = 8,
+  MORAP_DIMENSION_MISMATCH = 9,
+  MORAP_NON_SQUARE = 10,
+  MORAP_NOT_BISTOCHASTIC = 11,
+  MORAP_NO_PERFECT_MATCHING = 12,
+  MORAP_NOT_POSITIVE_DEFINITE = 13,
+  MORAP_SOLVER_FAILURE = 14,
+  MORAP_DEGENERATE_DIRECTION = 15,
+  MORAP_SIZE_GUARD = 16,
+  MORAP_CYCLE_GUARD = 17,
+  MORAP_INVALID_CONFIG = 18,
+  MORAP_GENERATION_FAILURE = 19,
+  MORAP_NO_CERTIFICATE = 20,
+  MORAP_IO = 21,
+  MORAP_CUDA_ERROR = 100 /* CUDA runtime failure (no Errc equivalent) */
+};
+
+#define MORAP_MAX_OBJECTIVES 8 /* reward vectors per model (K; the reference has K = 2) */
+#define MORAP_MAX_RHS 4        /* reward vectors evaluated together in one fused sweep */
+
+typedef struct morap_ctx morap_ctx;
+
+/* Host view of one product MDP (ProductMdp, model.hpp:143-157): CSR in the reference
+ * layout. rewards[k] has num_rows entries: rewards[0] = cost, rewards[1] = success
+ * (model.hpp:150-151), further entries are extra objectives (K > 2 extension). */
+typedef struct {
+  int32_t num_states;
+  int32_t num_rows;
+  int32_t nnz;
+  int32_t initial;
+  int32_t reward_finite; /* ProductMdp::rewardFinite (model.hpp:152) */
+  int32_t num_objectives;
+  const int32_t* row_offset; /* num_states + 1 */
+  const int32_t* trn_offset; /* num_rows + 1 */
+  const int32_t* succ;       /* nnz */
+  const double* prob;        /* nnz */
+  const uint8_t* done;       /* num_states, 0/1 */
+  const double* const* rewards;
+} morap_csr_view;
+
+/* Context on CUDA device `device` (replaces the PoolConfig + engine lifetime,
+ * engine.hpp:66-72,370). */
+int morap_cuda_create(int device, morap_ctx** out);
+int morap_cuda_destroy(morap_ctx* ctx);
+/* Launch on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ * NULL restores the context's own stream. */
+int morap_cuda_set_stream(morap_ctx* ctx, void* cuda_stream);
+const char* morap_cuda_last_error(morap_ctx* ctx);
+
+/* Upload models once; device copies are immutable until morap_cuda_release_models.
+ * Replaces the shared_ptr<const ProductMdp> handed to every Job (engine.hpp:43).
+ * Validates CSR structure (offsets monotone, successors in range) -> MORAP_INVALID_MODEL. */
+int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models, int32_t* model_ids_out);
+int morap_cuda_release_models(morap_ctx* ctx);
+int morap_cuda_num_models(morap_ctx* ctx);
+
+/* JobKind::Optimize batch (engine.hpp:126-131 -> numerics.hpp:74). Job k runs on model
+ * model_ids[k] with rho = weightedReward(objectives, weights[k*K .. k*K+K-1])
+ * (numerics.hpp:224, as built by supportingPoint solver.hpp:118-128). Per job: value at
+ * the initial state, sweep count, final residual and status (MORAP_OK,
+ * MORAP_NOT_REWARD_FINITE, MORAP_NON_CONVERGENCE). Returns the first job failure's
+ * status only for whole-batch errors; per-job failures are contained in status_out like
+ * JobResult{ok=false, errc} (engine.hpp:140-150). Final values and policies stay on the
+ * device until the next optimize call. */
+int morap_cuda_optimize(morap_ctx* ctx, int njobs, const int32_t* model_ids, const double* weights, int K,
+                        double eps, int sweep_cap, double* value_out, int32_t* sweeps_out,
+                        double* residual_out, int32_t* status_out);
+
+/* Same, with an explicit per-job reward vector (Job::reward, engine.hpp:44) of num_rows
+ * entries for its model. */
+int morap_cuda_optimize_rho(morap_ctx* ctx, int njobs, const int32_t* model_ids, const double* const* rho,
+                            double eps, int sweep_cap, double* value_out, int32_t* sweeps_out,
+                            double* residual_out, int32_t* status_out);
+
+/* Results of the last optimize batch: final value vector (OptimizeResult::values) and the
+ * argmax scheduler of the final sweep (OptimizeResult::policy as deterministic rows,
+ * done states -> first row, numerics.hpp:114-118). */
+int morap_cuda_fetch_values(morap_ctx* ctx, int job, double* values_out);
+int morap_cuda_fetch_policy(morap_ctx* ctx, int job, int32_t* rows_out);
+
+/* Fused JobKind::Evaluate of optimize jobs' own schedulers (supportingPoint's cost and
+ * success jobs, solver.hpp:148-172): for each listed optimize job, evaluate its final
+ * policy under nrhs of its model's objective vectors (objective[0..nrhs-1]) in ONE
+ * multi-RHS sweep; every RHS stops on its own (delta <= eps) exactly as separate
+ * evaluateSchedulerOn calls would. Outputs are njobs x nrhs, row-major. */
+int morap_cuda_evaluate_optimized(morap_ctx* ctx, int njobs, const int32_t* opt_jobs, int nrhs,
+                                  const int32_t* objective, double eps, int sweep_cap, double* value_out,
+                                  int32_t* sweeps_out, double* residual_out, int32_t* status_out);
+
+/* General JobKind::Evaluate batch: job k evaluates the deterministic scheduler
+ * policies[k] (num_states rows) on model model_ids[k] under the explicit reward rho[k]
+ * (num_rows). A policy row outside its state's rows -> MORAP_INVALID_MODEL for that job
+ * (checkScheduler, numerics.hpp:51-66). */
+int morap_cuda_evaluate(morap_ctx* ctx, int njobs, const int32_t* model_ids, const int32_t* const* policies,
+                        const double* const* rho, double eps, int sweep_cap, double* value_out,
+                        int32_t* sweeps_out, double* residual_out, int32_t* status_out);
+
+/* Value vector of (job, rhs) from the last evaluate call. */
+int morap_cuda_fetch_eval_values(morap_ctx* ctx, int job, int rhs, double* values_out);
+
+/* Instrumentation (SweepStats/bench). Totals since the last reset:
+ *   out[0] sweep-kernel launches (optimize), out[1] their summed device ms (only while
+ *   profiling is on: CUDA events around each launch), out[2] algorithmic bytes those
+ *   launches moved (12*nnz + 12*R + 21*S per active job per sweep),
+ *   out[3] nnz backups performed (sum over jobs of sweeps * nnz), out[4..7] the same four
+ *   for evaluate sweeps, out[8] kernels launched in total. */
+int morap_cuda_set_profiling(morap_ctx* ctx, int on);
+int morap_cuda_stats(morap_ctx* ctx, double* out, int nout);
+int morap_cuda_reset_stats(morap_ctx* ctx);
+int morap_cuda_device_bytes(morap_ctx* ctx, int64_t* bytes_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MORAP_CUDA_H */

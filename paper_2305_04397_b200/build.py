@@ -1,0 +1,75 @@
+"""In-tree build of the native libraries (sm_100a CUDA backend + host C++ library).
+
+Outputs (git-ignored, shipped to the GPU box with the snapshot):
+  paper_2305_04397_b200/libmorap_cuda.so   kernels + C ABI (include/morap_cuda.h)
+  paper_2305_04397_b200/libmorap_host.so   host C++ API + C ABI (include/morap.h),
+                                           links libmorap_cuda.so
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+CUDA_SO = os.path.join(PKG, "libmorap_cuda.so")
+HOST_SO = os.path.join(PKG, "libmorap_host.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+JSON_DIR = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+
+CUDA_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-lineinfo", "-O3", "-std=c++17",
+    "-fmad=false",  # bitwise parity with the reference's no-FMA CPU arithmetic
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+HOST_SOURCES = ["host.cpp"]
+
+
+def _newer(target: str, sources: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _deps(names):
+    out = [os.path.join(CSRC, n) for n in names]
+    out += [os.path.join(CSRC, n) for n in os.listdir(CSRC) if n.endswith((".h", ".hpp", ".cuh"))]
+    out += [os.path.join(ROOT, "include", n) for n in os.listdir(os.path.join(ROOT, "include"))]
+    return out
+
+
+def build_cuda(force: bool = False, verbose: bool = False) -> str:
+    src = os.path.join(CSRC, "morap_cuda.cu")
+    if force or _newer(CUDA_SO, _deps(["morap_cuda.cu"])):
+        cmd = [NVCC, *CUDA_FLAGS, "-o", CUDA_SO, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.run(cmd, check=True)
+    return CUDA_SO
+
+
+def build_host(force: bool = False) -> str:
+    srcs = [os.path.join(CSRC, s) for s in HOST_SOURCES if os.path.exists(os.path.join(CSRC, s))]
+    if not srcs:
+        return ""
+    if force or _newer(HOST_SO, _deps(HOST_SOURCES) + [CUDA_SO]):
+        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-pthread", "-ffp-contract=off",
+               f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}", f"-I{JSON_DIR}",
+               "-o", HOST_SO, *srcs, f"-L{PKG}", "-lmorap_cuda", "-Wl,-rpath,$ORIGIN"]
+        subprocess.run(cmd, check=True)
+    return HOST_SO
+
+
+def build_all(force: bool = False) -> None:
+    build_cuda(force)
+    build_host(force)
+
+
+if __name__ == "__main__":
+    import sys
+    build_all(force="--force" in sys.argv)
+    print("built", CUDA_SO, HOST_SO)

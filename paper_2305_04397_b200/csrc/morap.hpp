@@ -1,0 +1,335 @@
+// morap.hpp -- host C++ API of the B200 MORAP hot path (libmorap_host.so).
+//
+// Same surface as the reference library (/root/reference/proj/include/morap/*.hpp): the
+// model loader (mdpFromJson, buildProduct, buildInstance, generateInstance), the
+// per-model solve (optimalScheduler, evaluateScheduler, runBatch) and the Pareto-point
+// query (supportingPoint, paretoPoint, verifyOnly, synthesize). Names, argument meaning
+// and error codes follow the reference; the implementation is new. Every Bellman solve
+// goes through the C ABI of libmorap_cuda.so (include/morap_cuda.h) -- there is no CPU
+// solver in this library.
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "json.hpp"
+
+struct morap_ctx;
+
+namespace morap {
+
+using Json = nlohmann::json;
+
+// ---- errors (common.hpp:12-45) ----------------------------------------------------------
+enum class Errc {
+  Syntax, NotCoSafe, ClosureBlowup, InvalidDfa, InvalidModel, NotRewardFinite, NonConvergence,
+  SingularSystem, DimensionMismatch, NonSquare, NotBistochastic, NoPerfectMatching, NotPositiveDefinite,
+  SolverFailure, DegenerateDirection, SizeGuard, CycleGuard, InvalidConfig, GenerationFailure,
+  NoCertificate, Io,
+};
+
+class Error : public std::runtime_error {
+ public:
+  Error(Errc c, const std::string& what) : std::runtime_error(what), code_(c) {}
+  Errc code() const noexcept { return code_; }
+
+ private:
+  Errc code_;
+};
+
+[[noreturn]] void fail(Errc c, const std::string& msg);
+inline int statusOf(Errc c) { return static_cast<int>(c) + 1; }
+
+using Vec = std::vector<double>;
+
+struct Mat {
+  int rows = 0, cols = 0;
+  Vec a;
+  Mat() = default;
+  Mat(int r, int c, double v = 0.0) : rows(r), cols(c), a(static_cast<size_t>(r) * c, v) {}
+  double& operator()(int r, int c) { return a[static_cast<size_t>(r) * cols + c]; }
+  double operator()(int r, int c) const { return a[static_cast<size_t>(r) * cols + c]; }
+};
+
+// ---- dense linear algebra (common.hpp:47-125) --------------------------------------------
+double dot(const Vec& x, const Vec& y);
+Vec matVec(const Mat& m, const Vec& x);
+double maxAbs(const Vec& v);
+Vec solveDense(Mat A, Vec b, double pivotTol = 1e-12);
+bool choleskyLower(const Mat& m, Mat& lower);
+
+// ---- task logic (logic.hpp) --------------------------------------------------------------
+enum class FKind : uint8_t { True, False, Atom, NotAtom, And, Or, Next, Until, Eventually };
+
+struct Formula {
+  FKind kind = FKind::True;
+  std::string atom;
+  std::vector<Formula> kids;
+};
+int cmpFormula(const Formula& a, const Formula& b);
+bool operator==(const Formula& a, const Formula& b);
+bool operator<(const Formula& a, const Formula& b);
+Formula fTrue();
+Formula fFalse();
+Formula fAtom(std::string a);
+Formula fNotAtom(std::string a);
+Formula fAnd(std::vector<Formula> kids);
+Formula fOr(std::vector<Formula> kids);
+Formula fNext(Formula f);
+Formula fUntil(Formula l, Formula r);
+Formula fEventually(Formula f);
+Formula negate(const Formula& f);
+Formula parseCoSafe(const std::string& src);
+Formula progressMask(const Formula& f, uint32_t letter, const std::vector<std::string>& atoms);
+
+struct Dfa {
+  std::vector<std::string> atoms;  // sorted; letters are bitmasks over them
+  int numLocations = 0;
+  int initial = 0;
+  std::vector<char> accepting, trap, preSink;
+  std::vector<int> delta;  // numLocations x numLetters
+  int numLetters() const { return 1 << static_cast<int>(atoms.size()); }
+  int step(int q, int letter) const { return delta[static_cast<size_t>(q) * numLetters() + letter]; }
+};
+uint32_t letterMaskFor(const Dfa& d, const std::vector<std::string>& sortedLabels);
+Dfa formulaToDfa(const Formula& phi, size_t locationCap = 1000000);
+Dfa insertPreSinks(const Dfa& d);
+Dfa withDeadline(const Dfa& d, int k);
+bool acceptsWord(const Dfa& d, const std::vector<uint32_t>& word);
+Json dfaToJson(const Dfa& d);
+Dfa dfaFromJson(const Json& j);
+
+// ---- models (model.hpp) ------------------------------------------------------------------
+struct Mdp {
+  int numStates = 0;
+  int initial = 0;
+  std::vector<int> rowOffset, trnOffset, succ;
+  std::vector<double> prob;
+  std::vector<std::string> actionName;
+  std::vector<std::vector<std::string>> labels;
+  int numActions() const { return static_cast<int>(trnOffset.size()) - 1; }
+  int actionsBegin(int s) const { return rowOffset[s]; }
+  int actionsEnd(int s) const { return rowOffset[s + 1]; }
+  int trnBegin(int r) const { return trnOffset[r]; }
+  int trnEnd(int r) const { return trnOffset[r + 1]; }
+};
+using RewardStructure = Vec;
+
+void validateMdp(const Mdp& m, double rowSumTol = 1e-9);
+void renormalizeRows(Mdp& m);
+std::pair<Mdp, RewardStructure> mdpFromJson(const Json& j);
+Json mdpToJson(const Mdp& m, const RewardStructure& reward);
+
+struct ProductMdp {
+  Mdp mdp;
+  std::vector<int> agentState, dfaLocation;
+  std::vector<char> done, accept, preSink;
+  RewardStructure cost, success;
+  std::vector<RewardStructure> extra;  // objectives beyond cost/success (K > 2 extension)
+  bool rewardFinite = false;
+  std::vector<std::string> droppedAtoms;
+  int agentId = -1, taskId = -1;
+  uint64_t structuralHash = 0;
+};
+extern const std::string kInternalAction;
+
+std::vector<int> maximalAvoidSet(const Mdp& m, const std::vector<char>& done);
+bool checkRewardFinite(const Mdp& m, const std::vector<char>& done);
+bool checkRewardFinite(const ProductMdp& p);
+uint64_t productHash(const ProductMdp& p);
+ProductMdp buildProduct(const Mdp& agent, const RewardStructure& agentCost, const Dfa& task, int agentId = -1,
+                        int taskId = -1);
+
+// ---- instance (instance.hpp) -------------------------------------------------------------
+struct MorapInstance {
+  std::vector<Mdp> agents;
+  std::vector<RewardStructure> costs;
+  std::vector<Dfa> tasks;
+  int n = 0;
+  int realTasks = 0;
+  std::vector<std::vector<std::shared_ptr<const ProductMdp>>> products;  // [agent][task]
+  int distinctProducts = 0;
+  int objectives = 2;  // K: cost, success (+ extras)
+};
+MorapInstance buildInstance(std::vector<Mdp> agents, std::vector<RewardStructure> costs, std::vector<Dfa> tasks,
+                            int threads = 0);
+Vec expandThresholds(const MorapInstance& inst, const Vec& user);
+// K-objective extension: attach K-2 extra seeded per-row objectives in
+// [-2, 0] to every product (not in the reference; parity for K > 2 is unpinned).
+void addSyntheticObjectives(MorapInstance& inst, int K, uint64_t seed);
+
+// ---- warehouse generator (warehouse.hpp) --------------------------------------------------
+struct WarehouseConfig {
+  int width = 0, height = 0, agents = 1;
+  double slip = 0.05;
+  std::vector<std::array<int, 2>> racks;
+  std::array<int, 2> feed{0, 0};
+  uint64_t seed = 0;
+  int deadline = -1;
+};
+void validateWarehouseConfig(const WarehouseConfig& cfg);
+std::pair<Mdp, RewardStructure> generateAgent(const WarehouseConfig& cfg, int agentIndex);
+Formula generateTask(const WarehouseConfig& cfg, int rackIndex);
+Dfa taskAutomaton(const WarehouseConfig& cfg, int rackIndex);
+MorapInstance generateInstance(const WarehouseConfig& cfg, int threads = 0);
+WarehouseConfig warehouseConfigFromJson(const Json& j);
+
+// ---- per-model solve on the GPU (numerics.hpp, engine.hpp) --------------------------------
+struct Scheduler {  // deterministic: one action row per state (the solver only produces these)
+  std::vector<int> rows;
+};
+Scheduler makeDeterministic(std::vector<int> rows);
+struct SweepStats {
+  int sweeps = 0;
+  double residual = 0.0;
+};
+struct OptimizeResult {
+  Vec values;
+  Scheduler policy;
+  SweepStats stats;
+  double value = 0.0;
+};
+struct EvaluateResult {
+  Vec values;
+  SweepStats stats;
+  double value = 0.0;
+};
+RewardStructure weightedReward(const std::vector<const RewardStructure*>& parts, const Vec& w);
+
+// Device-resident model store + the CUDA context: the accelerator queue of the engine.
+class GpuBackend {
+ public:
+  explicit GpuBackend(int device = 0);
+  ~GpuBackend();
+  GpuBackend(const GpuBackend&) = delete;
+  GpuBackend& operator=(const GpuBackend&) = delete;
+  int modelId(const ProductMdp* p);           // uploads on first use
+  void uploadInstance(const MorapInstance& inst);  // all distinct products in one batch
+  morap_ctx* ctx() const { return ctx_; }
+  int device() const { return device_; }
+  void release();
+
+ private:
+  morap_ctx* ctx_ = nullptr;
+  int device_ = 0;
+  std::map<const ProductMdp*, int> ids_;
+};
+
+OptimizeResult optimalScheduler(GpuBackend& gpu, const ProductMdp& p, const RewardStructure& rho, double eps = 1e-6,
+                                int sweepCap = 100000);
+EvaluateResult evaluateScheduler(GpuBackend& gpu, const ProductMdp& p, const Scheduler& mu, const RewardStructure& rho,
+                                 double eps = 1e-6, int sweepCap = 100000);
+
+enum class JobKind { Optimize, Evaluate };
+struct Job {
+  long id = 0;
+  JobKind kind = JobKind::Optimize;
+  std::shared_ptr<const ProductMdp> model;
+  RewardStructure reward;
+  Scheduler scheduler;
+  double eps = 1e-6;
+  int sweepCap = 100000;
+};
+struct JobResult {
+  bool ok = false;
+  std::string error;
+  std::optional<Errc> errc;
+  double value = 0.0;
+  Vec values;
+  Scheduler policy;
+  SweepStats stats;
+};
+// engine.hpp:370 on the GPU: all jobs of one kind in one device batch.
+std::map<long, JobResult> runBatch(std::vector<Job> jobs, GpuBackend& gpu);
+
+// ---- assignment (assignment.hpp) ---------------------------------------------------------
+struct Assignment {
+  std::vector<int> agentOf;
+  double value = 0.0;
+};
+Assignment maxAssignment(const Mat& c);
+bool validateBistochastic(const Mat& x, double entryTol = 1e-9, double sumTol = 1e-6);
+
+// ---- geometry (geometry.hpp) -------------------------------------------------------------
+struct NormMatrix {
+  Mat m;
+  explicit NormMatrix(Mat mat);
+  static NormMatrix identity(int dim);
+  int dim() const { return m.rows; }
+};
+double normDistance(const NormMatrix& norm, const Vec& v);
+struct LowerApprox {
+  std::vector<Vec> points;
+};
+struct Halfspace {
+  Vec w, r;
+};
+struct UpperApprox {
+  std::vector<Halfspace> cuts;
+};
+struct ProjectionResult {
+  Vec x, lambda;
+  double distance = 0.0;
+};
+ProjectionResult projectToLowerApprox(const Vec& t, const LowerApprox& phi, const NormMatrix& norm);
+Vec weightVector(const Vec& t, const Vec& tUp, const NormMatrix& norm);
+Vec projectToUpperApprox(const Vec& t, const UpperApprox& upper, const NormMatrix& norm);
+
+// ---- solver (solver.hpp) -----------------------------------------------------------------
+struct SupportingPoint {
+  Vec r;
+  Assignment assignment;
+  std::vector<Scheduler> schedulers;
+};
+struct IterationRecord {
+  Vec w, r;
+  Assignment assignment;
+  std::vector<Scheduler> schedulers;
+  Vec tUp, tDown;
+};
+struct ParetoResult {
+  bool feasible = false, converged = false;
+  Vec thresholds, tUp, tDown;
+  LowerApprox phi;
+  UpperApprox lambda;
+  std::vector<IterationRecord> iterations;
+  Vec lambdaStar;
+  double eps = 0.0;
+};
+struct SynthesisTerm {
+  double p = 0.0;
+  Assignment assignment;
+  std::vector<Scheduler> schedulers;
+};
+struct SynthesisResult {
+  std::vector<SynthesisTerm> terms;
+  Mat marginal;
+};
+struct QueryStats {  // per-query instrumentation (bench)
+  long optimizeJobs = 0, evaluateJobs = 0;
+  double optimizeBackups = 0, evaluateStateBackups = 0;
+  double optimizeSeconds = 0, evaluateSeconds = 0, hostSeconds = 0;
+};
+
+using QueryFn = std::function<SupportingPoint(const Vec& w)>;
+
+SupportingPoint supportingPoint(const MorapInstance& inst, const Vec& w, GpuBackend& gpu, QueryStats* stats = nullptr);
+ParetoResult runParetoCore(Vec expandedThresholds, const NormMatrix& norm, double eps, int iterationCap,
+                           bool verifyMode, bool* verdict, const QueryFn& query);
+ParetoResult paretoPoint(const MorapInstance& inst, const Vec& thresholds, const NormMatrix& norm, double eps,
+                         GpuBackend& gpu, int iterationCap = 500, QueryStats* stats = nullptr);
+bool verifyOnly(const MorapInstance& inst, const Vec& thresholds, const NormMatrix& norm, double eps,
+                GpuBackend& gpu, int iterationCap = 500);
+SynthesisResult synthesize(const ParetoResult& result);
+Json resultToJson(const ParetoResult& result, const SynthesisResult* synthesis = nullptr);
+
+// instance file (cli.hpp:84-117): agents inline or as paths, tasks as LTL strings / DFA JSON.
+MorapInstance instanceFromJson(const Json& j, const std::string& baseDir = ".");
+
+}  // namespace morap

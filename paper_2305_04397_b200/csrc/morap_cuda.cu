@@ -1,0 +1,1245 @@
+// libmorap_cuda.so -- sm_100a value-iteration backend behind include/morap_cuda.h.
+//
+// What runs on the GPU (reference functions replaced, /root/reference/proj/include/morap):
+//   k_weighted_reward  weightedReward               numerics.hpp:224-234 (per optimize job)
+//   k_greedy_sweep     optimalSchedulerOn sweep     numerics.hpp:84-113
+//   k_policy           final argmax scheduler       numerics.hpp:96-102,114-115
+//   k_eval_sweep       evaluateSchedulerOn sweep    numerics.hpp:138-162 (multi-RHS)
+//   k_finalize_*       per-job stop test + compaction of the active set (delta <= eps,
+//                      sweep cap -> NonConvergence, numerics.hpp:105-112)
+//
+// Layout in HBM: every uploaded model keeps the reference CSR verbatim
+// (int32 rowOffset/trnOffset/succ, fp64 prob, u8 done, K fp64 objective vectors) in
+// pooled device buffers, plus a tile table: state ranges of <= 256 states and <= 1024
+// action rows. One optimize job = (model, rho_w fp64[R], x fp64[S] x 2, policy int32[S]).
+//
+// Execution: jobs advance in lock step, one sweep per k_greedy_sweep launch; the launch
+// walks only the tiles of still-active jobs (a compacted job list plus a tile prefix sum
+// that k_finalize rebuilds on the device after every sweep), so converged jobs cost
+// nothing and there is no per-sweep host synchronisation. The host polls the active
+// count once per batch of sweeps.
+//
+// Bitwise parity: every product and sum is an explicitly rounded __dmul_rn/__dadd_rn
+// (no FMA contraction; also built with -fmad=false), rows are accumulated left to right
+// from rho[r], the per-state argmax scans rows in order keeping the first strict max, and
+// delta is a max (order independent). Hence values, sweeps, residuals and policies
+// equal the reference CPU solver bit for bit.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/morap_cuda.h"
+
+namespace {
+
+constexpr int kBlock = 256;     // threads per CTA = max states per tile
+constexpr int kRowCap = 1024;   // max action rows staged in shared memory per tile
+constexpr int kFinBlock = 1024; // finalize kernel block
+
+struct DevModel {
+  const int32_t* rowOffset;
+  const int32_t* trnOffset;
+  const int32_t* succ;
+  const double* prob;
+  const uint8_t* done;
+  const double* obj[MORAP_MAX_OBJECTIVES];
+  const int32_t* tileStart;  // ntiles + 1 state boundaries
+  int32_t S, R, nnz, initial, ntiles, K, rewardFinite, pad;
+  unsigned long long bytesPerSweep;  // algorithmic bytes of one greedy sweep
+  unsigned long long bytesPerEval;   // per evaluate sweep, one RHS
+};
+
+struct OptJob {
+  int32_t model;
+  int32_t pad;
+  double w[MORAP_MAX_OBJECTIVES];
+  double* rho;
+  double* buf[2];
+  int32_t* policy;
+};
+
+struct EvalJob {
+  int32_t model;
+  int32_t nrhs;
+  const int32_t* policy;
+  const double* rho[MORAP_MAX_RHS];
+  double* buf[MORAP_MAX_RHS][2];
+};
+
+// Device control block for one batch loop.
+struct Ctl {
+  int32_t nactive;      // jobs in the active list
+  int32_t totalTiles;   // tiles of active jobs (tilePrefix[nactive])
+  int32_t sweepsDone;   // sweeps completed by every active job
+  int32_t pad;
+  unsigned long long bytes;    // algorithmic bytes of all sweeps so far
+  unsigned long long backups;  // nnz backups of all sweeps so far
+};
+
+// --------------------------------------------------------------------------------------
+// device helpers
+
+__device__ __forceinline__ int find_slot(const int32_t* __restrict__ prefix, int n, int t) {
+  // largest a with prefix[a] <= t  (prefix[0] = 0, prefix[n] = total)
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ double row_value(const int32_t* __restrict__ trn, const int32_t* __restrict__ succ,
+                                            const double* __restrict__ prob, const double* __restrict__ rho,
+                                            const double* __restrict__ x, int r) {
+  // numerics.hpp:94-95: v = rho[r]; v += prob[k] * x[succ[k]] left to right, no FMA.
+  double v = rho[r];
+  const int kb = trn[r], ke = trn[r + 1];
+  for (int k = kb; k < ke; ++k) v = __dadd_rn(v, __dmul_rn(prob[k], __ldg(x + succ[k])));
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int NW>
+__device__ __forceinline__ double block_max(double v, double* red) {
+  v = warp_max(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < 32) {
+    r = lane < NW ? red[lane] : 0.0;
+    r = warp_max(r);
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
+// --------------------------------------------------------------------------------------
+// K3: rho_w[r] = 0 + w0*obj0[r] + w1*obj1[r] + ...  (numerics.hpp:227-231)
+
+__global__ void __launch_bounds__(kBlock) k_weighted_reward(const DevModel* __restrict__ models,
+                                                            const OptJob* __restrict__ jobs,
+                                                            const int32_t* __restrict__ list,
+                                                            const int32_t* __restrict__ prefix, int nlist,
+                                                            int total) {
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int a = find_slot(prefix, nlist + 1, t);
+    const OptJob& J = jobs[list[a]];
+    const DevModel& M = models[J.model];
+    const int lt = t - prefix[a];
+    const int s0 = M.tileStart[lt], s1 = M.tileStart[lt + 1];
+    const int r0 = M.rowOffset[s0], r1 = M.rowOffset[s1];
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+      double acc = 0.0;
+      for (int o = 0; o < M.K; ++o) acc = __dadd_rn(acc, __dmul_rn(J.w[o], M.obj[o][r]));
+      J.rho[r] = acc;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// K1: one greedy Jacobi sweep over the tiles of every active optimize job
+// (numerics.hpp:86-104). Phase 1: threads own action rows (coalesced trnOffset / rho /
+// succ / prob streams), row values land in shared memory. Phase 2: threads own states
+// and scan their rows in order for the first strict maximum.
+// POLICY = true: recompute the argmax of the final sweep from x_{k-1} and store rows.
+
+template <bool POLICY>
+__global__ void __launch_bounds__(kBlock) k_greedy_sweep(const DevModel* __restrict__ models,
+                                                         const OptJob* __restrict__ jobs,
+                                                         const int32_t* __restrict__ list,
+                                                         const int32_t* __restrict__ prefix,
+                                                         const Ctl* __restrict__ ctl,
+                                                         const int32_t* __restrict__ jobSweeps,
+                                                         unsigned long long* __restrict__ deltaBits) {
+  __shared__ int32_t sRow[kBlock + 1];
+  __shared__ double sVal[kRowCap];
+  __shared__ double sRed[kBlock / 32];
+
+  const int nact = ctl->nactive;
+  const int total = ctl->totalTiles;
+  if (total <= 0) return;
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per;
+  const int t1 = min(total, t0 + per);
+  if (t0 >= t1) return;
+  int a = find_slot(prefix, nact + 1, t0);
+  const int k = ctl->sweepsDone;
+
+  for (int t = t0; t < t1; ++t) {
+    while (t >= prefix[a + 1]) ++a;
+    const int job = list[a];
+    const OptJob& J = jobs[job];
+    const DevModel& M = models[J.model];
+    const int lt = t - prefix[a];
+    const int s0 = M.tileStart[lt];
+    const int ns = M.tileStart[lt + 1] - s0;
+    const int32_t* __restrict__ trn = M.trnOffset;
+    const int32_t* __restrict__ succ = M.succ;
+    const double* __restrict__ prob = M.prob;
+    const double* __restrict__ rho = J.rho;
+    int parity = k & 1;
+    if (POLICY) parity = (jobSweeps[job] - 1) & 1;
+    const double* __restrict__ x = J.buf[parity];
+    double* __restrict__ y = J.buf[parity ^ 1];
+
+    for (int i = threadIdx.x; i <= ns; i += kBlock) sRow[i] = M.rowOffset[s0 + i];
+    __syncthreads();
+    const int r0 = sRow[0];
+    const int nr = sRow[ns] - r0;
+    const int nstage = min(nr, kRowCap);
+    for (int i = threadIdx.x; i < nstage; i += kBlock) sVal[i] = row_value(trn, succ, prob, rho, x, r0 + i);
+    __syncthreads();
+
+    double d = 0.0;
+    if (threadIdx.x < ns) {
+      const int s = s0 + threadIdx.x;
+      const int rb = sRow[threadIdx.x] - r0, re = sRow[threadIdx.x + 1] - r0;
+      if (M.done[s]) {
+        if (POLICY) J.policy[s] = r0 + rb;  // numerics.hpp:114-115
+      } else {
+        double best = 0.0;
+        int bestRow = -1;
+        for (int q = rb; q < re; ++q) {
+          const double v = q < kRowCap ? sVal[q] : row_value(trn, succ, prob, rho, x, r0 + q);
+          if (bestRow < 0 || v > best) {
+            best = v;
+            bestRow = q;
+          }
+        }
+        if (POLICY) {
+          J.policy[s] = r0 + bestRow;
+        } else {
+          y[s] = best;
+          d = fabs(__dsub_rn(best, x[s]));
+        }
+      }
+    }
+    if (!POLICY) {
+      d = block_max<kBlock / 32>(d, sRed);
+      if (threadIdx.x == 0 && d > 0.0) atomicMax(deltaBits + job, (unsigned long long)__double_as_longlong(d));
+    } else {
+      __syncthreads();
+    }
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// K2: fused multi-RHS fixed-scheduler sweep (numerics.hpp:140-153 with a deterministic
+// scheduler): y_o(s) = 0 + 1.0 * (rho_o[r] + sum_k P_k x_o[succ_k]), r = policy[s].
+// Each RHS o is skipped once converged (its own stop test), so every RHS reproduces a
+// separate evaluateSchedulerOn run exactly.
+
+__global__ void __launch_bounds__(kBlock) k_eval_sweep(const DevModel* __restrict__ models,
+                                                       const EvalJob* __restrict__ jobs,
+                                                       const int32_t* __restrict__ list,
+                                                       const int32_t* __restrict__ prefix,
+                                                       const Ctl* __restrict__ ctl,
+                                                       const uint32_t* __restrict__ rhsMask,
+                                                       unsigned long long* __restrict__ deltaBits) {
+  __shared__ double sRed[kBlock / 32];
+  const int nact = ctl->nactive;
+  const int total = ctl->totalTiles;
+  if (total <= 0) return;
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per;
+  const int t1 = min(total, t0 + per);
+  if (t0 >= t1) return;
+  int a = find_slot(prefix, nact + 1, t0);
+  const int parity = ctl->sweepsDone & 1;
+
+  for (int t = t0; t < t1; ++t) {
+    while (t >= prefix[a + 1]) ++a;
+    const int job = list[a];
+    const EvalJob& J = jobs[job];
+    const DevModel& M = models[J.model];
+    const int lt = t - prefix[a];
+    const int s0 = M.tileStart[lt];
+    const int ns = M.tileStart[lt + 1] - s0;
+    const uint32_t mask = rhsMask[job];
+    const int nrhs = J.nrhs;
+
+    double d[MORAP_MAX_RHS] = {0.0, 0.0, 0.0, 0.0};
+    if (threadIdx.x < ns) {
+      const int s = s0 + threadIdx.x;
+      if (!M.done[s]) {
+        const int r = J.policy[s];
+        const int kb = M.trnOffset[r], ke = M.trnOffset[r + 1];
+        double acc[MORAP_MAX_RHS];
+#pragma unroll
+        for (int o = 0; o < MORAP_MAX_RHS; ++o)
+          if (o < nrhs && (mask >> o & 1u)) acc[o] = J.rho[o][r];
+        for (int kk = kb; kk < ke; ++kk) {
+          const double p = M.prob[kk];
+          const int c = M.succ[kk];
+#pragma unroll
+          for (int o = 0; o < MORAP_MAX_RHS; ++o)
+            if (o < nrhs && (mask >> o & 1u)) acc[o] = __dadd_rn(acc[o], __dmul_rn(p, __ldg(J.buf[o][parity] + c)));
+        }
+#pragma unroll
+        for (int o = 0; o < MORAP_MAX_RHS; ++o)
+          if (o < nrhs && (mask >> o & 1u)) {
+            const double v = __dadd_rn(0.0, __dmul_rn(1.0, acc[o]));
+            J.buf[o][parity ^ 1][s] = v;
+            d[o] = fabs(__dsub_rn(v, J.buf[o][parity][s]));
+          }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < MORAP_MAX_RHS; ++o) {
+      if (o < nrhs && (mask >> o & 1u)) {  // block-uniform condition
+        const double m = block_max<kBlock / 32>(d[o], sRed);
+        if (threadIdx.x == 0 && m > 0.0)
+          atomicMax(deltaBits + job * MORAP_MAX_RHS + o, (unsigned long long)__double_as_longlong(m));
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// Finalize: stop test per job/RHS (numerics.hpp:105-112), then compact the active list
+// and rebuild the tile prefix for the next sweep. One CTA; jobs in chunks of 1024.
+
+__device__ __forceinline__ void block_scan2(int& a, int& b, int* sa, int* sb, int& totA, int& totB) {
+  // exclusive scan of (a, b) over the block (kFinBlock threads)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int xa = a, xb = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int ya = __shfl_up_sync(0xffffffffu, xa, o), yb = __shfl_up_sync(0xffffffffu, xb, o);
+    if (lane >= o) { xa += ya; xb += yb; }
+  }
+  if (lane == 31) { sa[wid] = xa; sb[wid] = xb; }
+  __syncthreads();
+  if (wid == 0) {
+    int va = sa[lane], vb = sb[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int ya = __shfl_up_sync(0xffffffffu, va, o), yb = __shfl_up_sync(0xffffffffu, vb, o);
+      if (lane >= o) { va += ya; vb += yb; }
+    }
+    sa[lane] = va;
+    sb[lane] = vb;
+  }
+  __syncthreads();
+  const int offA = wid ? sa[wid - 1] : 0, offB = wid ? sb[wid - 1] : 0;
+  totA = sa[31];
+  totB = sb[31];
+  a = offA + xa - a;
+  b = offB + xb - b;
+  __syncthreads();
+}
+
+template <bool EVAL>
+__global__ void __launch_bounds__(kFinBlock) k_finalize(const DevModel* __restrict__ models,
+                                                        const int32_t* __restrict__ jobModel,
+                                                        int32_t* __restrict__ list, int32_t* __restrict__ prefix,
+                                                        Ctl* __restrict__ ctl, unsigned long long* __restrict__ deltaBits,
+                                                        uint32_t* __restrict__ rhsMask, const int32_t* __restrict__ nrhsOf,
+                                                        double eps, int cap, int32_t* __restrict__ sweeps,
+                                                        double* __restrict__ residual, int32_t* __restrict__ status) {
+  __shared__ int sa[32], sb[32];
+  __shared__ unsigned long long sBytes[kFinBlock / 32], sBk[kFinBlock / 32];
+  const int nact = ctl->nactive;
+  const int k = ctl->sweepsDone + 1;  // sweeps completed including the one just run
+  int outBase = 0, tileBase = 0;
+  unsigned long long bytes = 0, backups = 0;
+  for (int base = 0; base < nact; base += kFinBlock) {
+    const int i = base + threadIdx.x;
+    int keep = 0, nt = 0, job = -1;
+    if (i < nact) {
+      job = list[i];
+      const DevModel& M = models[jobModel[job]];
+      if (!EVAL) {
+        const double d = __longlong_as_double((long long)deltaBits[job]);
+        deltaBits[job] = 0ull;
+        sweeps[job] = k;
+        residual[job] = d;
+        bytes += M.bytesPerSweep;
+        backups += (unsigned long long)M.nnz;
+        if (d <= eps) status[job] = MORAP_OK;
+        else if (k >= cap) status[job] = MORAP_NON_CONVERGENCE;
+        else keep = 1;
+      } else {
+        uint32_t mask = rhsMask[job];
+        const int nr = nrhsOf[job];
+        for (int o = 0; o < nr; ++o) {
+          if (!(mask >> o & 1u)) continue;
+          const int slot = job * MORAP_MAX_RHS + o;
+          const double d = __longlong_as_double((long long)deltaBits[slot]);
+          deltaBits[slot] = 0ull;
+          sweeps[slot] = k;
+          residual[slot] = d;
+          bytes += M.bytesPerEval;
+          backups += (unsigned long long)M.S;  // one policy row per state (approx. nnz of chosen rows)
+          if (d <= eps) { status[slot] = MORAP_OK; mask &= ~(1u << o); }
+          else if (k >= cap) { status[slot] = MORAP_NON_CONVERGENCE; mask &= ~(1u << o); }
+        }
+        rhsMask[job] = mask;
+        keep = mask != 0;
+      }
+      if (keep) nt = M.ntiles;
+    }
+    int pa = keep, pb = nt, ta, tb;
+    block_scan2(pa, pb, sa, sb, ta, tb);
+    if (keep) {
+      list[outBase + pa] = job;
+      prefix[outBase + pa] = tileBase + pb;
+    }
+    outBase += ta;
+    tileBase += tb;
+    __syncthreads();
+  }
+  // algorithmic-byte accounting for the sweep just run
+  unsigned long long vb = bytes, vk = backups;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    vb += __shfl_xor_sync(0xffffffffu, vb, o);
+    vk += __shfl_xor_sync(0xffffffffu, vk, o);
+  }
+  if ((threadIdx.x & 31) == 0) { sBytes[threadIdx.x >> 5] = vb; sBk[threadIdx.x >> 5] = vk; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tb = 0, tk = 0;
+    for (int w = 0; w < kFinBlock / 32; ++w) { tb += sBytes[w]; tk += sBk[w]; }
+    prefix[outBase] = tileBase;
+    ctl->nactive = outBase;
+    ctl->totalTiles = tileBase;
+    ctl->sweepsDone = k;
+    ctl->bytes += tb;
+    ctl->backups += tk;
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// value at the initial state of every job's final buffer (OptimizeResult::value,
+// numerics.hpp:120) gathered into one array -> one D2H copy per batch
+
+__global__ void k_gather_opt(const DevModel* __restrict__ models, const OptJob* __restrict__ jobs, int njobs,
+                             const int32_t* __restrict__ sweeps, double* __restrict__ out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < njobs; j += gridDim.x * blockDim.x) {
+    const int sw = sweeps[j];
+    out[j] = sw > 0 ? jobs[j].buf[sw & 1][models[jobs[j].model].initial] : 0.0;
+  }
+}
+
+__global__ void k_gather_eval(const DevModel* __restrict__ models, const EvalJob* __restrict__ jobs, int njobs,
+                              const int32_t* __restrict__ sweeps, double* __restrict__ out) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < njobs * MORAP_MAX_RHS; q += gridDim.x * blockDim.x) {
+    const int j = q / MORAP_MAX_RHS, o = q % MORAP_MAX_RHS;
+    const int sw = sweeps[q];
+    out[q] = (o < jobs[j].nrhs && sw > 0) ? jobs[j].buf[o][sw & 1][models[jobs[j].model].initial] : 0.0;
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// host side
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) return ctx->cudaFail(e_, #call, __LINE__);                 \
+  } while (0)
+
+struct HostModel {
+  int32_t S, R, nnz, initial, ntiles, K, rewardFinite;
+};
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+};
+
+}  // namespace
+
+struct morap_ctx {
+  int device = 0;
+  int numSMs = 148;
+  int sweepBlocks = 0;  // persistent grid of the sweep kernels
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  bool profiling = false;
+  double stats[9] = {0};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  std::vector<HostModel> hm;
+  std::vector<DevModel> dm;
+  std::vector<void*> modelAllocs;
+  DevModel* dModels = nullptr;
+  size_t dModelsCap = 0;
+
+  // optimize batch state
+  int optJobs = 0;
+  std::vector<int32_t> optModel;
+  std::vector<int32_t> optSweeps;
+  std::vector<int32_t> optStatus;
+  std::vector<int32_t> optPolicyReady;
+  void* optArena = nullptr;
+  size_t optArenaBytes = 0;
+  OptJob* dOptJobs = nullptr;
+  std::vector<OptJob> hOptJobs;
+
+  // evaluate batch state
+  int evalJobs = 0;
+  std::vector<EvalJob> hEvalJobs;
+  std::vector<int32_t> evalSweeps;  // njobs * MAX_RHS
+  void* evalArena = nullptr;
+  size_t evalArenaBytes = 0;
+
+  // control arrays (shared by optimize/evaluate loops, sized to max jobs)
+  size_t ctlCap = 0;
+  int32_t* dList = nullptr;
+  int32_t* dPrefix = nullptr;
+  int32_t* dJobModel = nullptr;
+  unsigned long long* dDelta = nullptr;
+  uint32_t* dMask = nullptr;
+  int32_t* dNrhs = nullptr;
+  int32_t* dSweeps = nullptr;
+  double* dResidual = nullptr;
+  double* dGather = nullptr;
+  int32_t* dStatus = nullptr;
+  void* evalStage = nullptr;
+  size_t evalStageBytes = 0;
+  Ctl* dCtl = nullptr;
+  Ctl* hCtl = nullptr;  // pinned mirror
+  void* dEvalJobsRaw = nullptr;
+  size_t dEvalJobsCap = 0;
+  size_t dOptJobsCap = 0;
+
+  int cudaFail(cudaError_t e, const char* what, int line) {
+    err = std::string("CUDA error ") + cudaGetErrorString(e) + " at morap_cuda.cu:" + std::to_string(line) + " (" +
+          what + ")";
+    return MORAP_CUDA_ERROR;
+  }
+  int fail(int code, const std::string& msg) {
+    err = msg;
+    return code;
+  }
+};
+
+namespace {
+
+int ensure_ctl(morap_ctx* ctx, size_t njobs) {
+  if (njobs <= ctx->ctlCap && ctx->dCtl) return MORAP_OK;
+  size_t cap = std::max<size_t>(njobs, 64);
+  cudaFree(ctx->dList);
+  cudaFree(ctx->dPrefix);
+  cudaFree(ctx->dJobModel);
+  cudaFree(ctx->dDelta);
+  cudaFree(ctx->dMask);
+  cudaFree(ctx->dNrhs);
+  cudaFree(ctx->dSweeps);
+  cudaFree(ctx->dResidual);
+  cudaFree(ctx->dStatus);
+  cudaFree(ctx->dGather);
+  CK(cudaMalloc(&ctx->dGather, cap * MORAP_MAX_RHS * sizeof(double)));
+  CK(cudaMalloc(&ctx->dList, cap * sizeof(int32_t)));
+  CK(cudaMalloc(&ctx->dPrefix, (cap + 1) * sizeof(int32_t)));
+  CK(cudaMalloc(&ctx->dJobModel, cap * sizeof(int32_t)));
+  CK(cudaMalloc(&ctx->dDelta, cap * MORAP_MAX_RHS * sizeof(unsigned long long)));
+  CK(cudaMalloc(&ctx->dMask, cap * sizeof(uint32_t)));
+  CK(cudaMalloc(&ctx->dNrhs, cap * sizeof(int32_t)));
+  CK(cudaMalloc(&ctx->dSweeps, cap * MORAP_MAX_RHS * sizeof(int32_t)));
+  CK(cudaMalloc(&ctx->dResidual, cap * MORAP_MAX_RHS * sizeof(double)));
+  CK(cudaMalloc(&ctx->dStatus, cap * MORAP_MAX_RHS * sizeof(int32_t)));
+  if (!ctx->dCtl) {
+    CK(cudaMalloc(&ctx->dCtl, sizeof(Ctl)));
+    CK(cudaMallocHost(&ctx->hCtl, sizeof(Ctl)));
+  }
+  ctx->ctlCap = cap;
+  return MORAP_OK;
+}
+
+// Tile table: consecutive states, <= kBlock states and <= kRowCap rows (a state with
+// more rows than kRowCap gets a tile of its own; its overflow rows are computed from
+// global memory in phase 2).
+void make_tiles(const int32_t* rowOffset, int S, std::vector<int32_t>& out) {
+  out.clear();
+  int s = 0;
+  out.push_back(0);
+  while (s < S) {
+    int e = s + 1;
+    while (e < S && e - s < kBlock && rowOffset[e + 1] - rowOffset[s] <= kRowCap) ++e;
+    out.push_back(e);
+    s = e;
+  }
+}
+
+int validate_view(morap_ctx* ctx, const morap_csr_view& v, int idx) {
+  auto bad = [&](const std::string& why) {
+    return ctx->fail(MORAP_INVALID_MODEL, "model " + std::to_string(idx) + ": " + why);
+  };
+  if (v.num_states <= 0) return bad("model has no states");
+  if (v.num_rows < 0 || v.nnz < 0) return bad("negative sizes");
+  if (v.initial < 0 || v.initial >= v.num_states) return bad("initial state out of range");
+  if (v.num_objectives < 0 || v.num_objectives > MORAP_MAX_OBJECTIVES) return bad("too many objectives");
+  if (!v.row_offset || !v.trn_offset || !v.done || (v.nnz && (!v.succ || !v.prob))) return bad("null array");
+  if (v.row_offset[0] != 0 || v.row_offset[v.num_states] != v.num_rows) return bad("rowOffset does not span the rows");
+  for (int s = 0; s < v.num_states; ++s)
+    if (v.row_offset[s + 1] < v.row_offset[s]) return bad("rowOffset not monotone");
+  if (v.trn_offset[0] != 0 || v.trn_offset[v.num_rows] != v.nnz) return bad("trnOffset does not span nnz");
+  for (int r = 0; r < v.num_rows; ++r)
+    if (v.trn_offset[r + 1] < v.trn_offset[r]) return bad("trnOffset not monotone");
+  for (int k = 0; k < v.nnz; ++k)
+    if (v.succ[k] < 0 || v.succ[k] >= v.num_states) return bad("successor out of range");
+  for (int o = 0; o < v.num_objectives; ++o)
+    if (!v.rewards || !v.rewards[o]) return bad("null reward vector");
+  return MORAP_OK;
+}
+
+int upload_models_table(morap_ctx* ctx) {
+  if (ctx->dm.size() > ctx->dModelsCap) {
+    cudaFree(ctx->dModels);
+    size_t cap = std::max<size_t>(ctx->dm.size() * 2, 16);
+    CK(cudaMalloc(&ctx->dModels, cap * sizeof(DevModel)));
+    ctx->dModelsCap = cap;
+  }
+  CK(cudaMemcpyAsync(ctx->dModels, ctx->dm.data(), ctx->dm.size() * sizeof(DevModel), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  return MORAP_OK;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int ensure_arena(morap_ctx* ctx, void** arena, size_t* have, size_t need) {
+  if (need <= *have) return MORAP_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(*arena);
+  *arena = nullptr;
+  size_t cap = std::max(need, *have + *have / 2);
+  cudaError_t e = cudaMalloc(arena, cap);
+  if (e != cudaSuccess) {
+    cap = need;
+    CK(cudaMalloc(arena, cap));
+  }
+  *have = cap;
+  return MORAP_OK;
+}
+
+void launch_rec(morap_ctx* ctx, bool timed, bool start) {
+  if (!timed) return;
+  cudaEventRecord(start ? ctx->ev0 : ctx->ev1, ctx->stream);
+}
+
+// Runs sweeps (+finalize) until no job is active. kind 0 optimize, 1 evaluate.
+// Untimed: launches batches of sweep/finalize pairs and polls the active count once per
+// batch (converged jobs are already frozen on the device, so overshooting a batch only
+// costs empty launches). Profiling: CUDA events around every sweep launch and a poll
+// after each sweep, so the launch count equals the sweeps that did work.
+int run_loop(morap_ctx* ctx, int kind, double eps, int cap) {
+  const bool timed = ctx->profiling;
+  int batch = timed ? 1 : 4;
+  for (;;) {
+    for (int b = 0; b < batch; ++b) {
+      launch_rec(ctx, timed, true);
+      if (kind == 0) {
+        k_greedy_sweep<false><<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(
+            ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
+      } else {
+        k_eval_sweep<<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw,
+                                                                   ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dMask,
+                                                                   ctx->dDelta);
+      }
+      CK(cudaGetLastError());
+      launch_rec(ctx, timed, false);
+      if (kind == 0)
+        k_finalize<false><<<1, kFinBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dJobModel, ctx->dList, ctx->dPrefix,
+                                                           ctx->dCtl, ctx->dDelta, ctx->dMask, ctx->dNrhs, eps, cap,
+                                                           ctx->dSweeps, ctx->dResidual, ctx->dStatus);
+      else
+        k_finalize<true><<<1, kFinBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dJobModel, ctx->dList, ctx->dPrefix,
+                                                          ctx->dCtl, ctx->dDelta, ctx->dMask, ctx->dNrhs, eps, cap,
+                                                          ctx->dSweeps, ctx->dResidual, ctx->dStatus);
+      CK(cudaGetLastError());
+      ctx->stats[8] += 2;
+      if (timed) {
+        CK(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        ctx->stats[kind == 0 ? 1 : 5] += ms;
+      }
+    }
+    CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->hCtl->nactive == 0) break;
+    if (!timed) batch = std::min(batch * 2, 16);
+  }
+  return MORAP_OK;
+}
+
+// Host-built initial active list: jobs listed in `active` (order kept), tile prefix.
+int init_ctl(morap_ctx* ctx, const std::vector<int32_t>& active, const std::vector<int32_t>& jobModel) {
+  std::vector<int32_t> prefix(active.size() + 1, 0);
+  for (size_t a = 0; a < active.size(); ++a) prefix[a + 1] = prefix[a] + ctx->hm[jobModel[active[a]]].ntiles;
+  if (!active.empty()) CK(cudaMemcpyAsync(ctx->dList, active.data(), active.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dPrefix, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dJobModel, jobModel.data(), jobModel.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  Ctl c{};
+  c.nactive = static_cast<int32_t>(active.size());
+  c.totalTiles = prefix.back();
+  c.sweepsDone = 0;
+  *ctx->hCtl = c;
+  CK(cudaMemcpyAsync(ctx->dCtl, ctx->hCtl, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+  return MORAP_OK;
+}
+
+// Shared body of the two optimize entry points. rhoHost == nullptr -> weights mode.
+int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const double* weights, int K,
+                  const double* const* rhoHost, double eps, int cap, double* value_out, int32_t* sweeps_out,
+                  double* residual_out, int32_t* status_out) {
+  if (njobs < 0) return ctx->fail(MORAP_INVALID_CONFIG, "negative job count");
+  if (!(eps >= 0.0)) return ctx->fail(MORAP_INVALID_CONFIG, "eps must be nonnegative");
+  if (cap < 1) return ctx->fail(MORAP_INVALID_CONFIG, "sweep cap must be positive");
+  if (!rhoHost && (K < 0 || K > MORAP_MAX_OBJECTIVES)) return ctx->fail(MORAP_DIMENSION_MISMATCH, "bad objective count");
+  ctx->optJobs = 0;
+  if (njobs == 0) return MORAP_OK;
+  for (int j = 0; j < njobs; ++j) {
+    if (model_ids[j] < 0 || model_ids[j] >= static_cast<int>(ctx->hm.size()))
+      return ctx->fail(MORAP_INVALID_CONFIG, "job " + std::to_string(j) + ": unknown model id");
+    if (!rhoHost && K != ctx->hm[model_ids[j]].K)
+      return ctx->fail(MORAP_DIMENSION_MISMATCH, "one weight per reward structure (numerics.hpp:225)");
+  }
+  // arena regions: [rho of every job][x0|x1 of every job][policy of every job] so the
+  // x region is zeroed with one memset (x = y = 0 at the start, numerics.hpp:81)
+  size_t rhoBytes = 0, xBytes = 0, polBytes = 0;
+  std::vector<size_t> offRho(njobs), offX(njobs), offPol(njobs);
+  for (int j = 0; j < njobs; ++j) {
+    const HostModel& m = ctx->hm[model_ids[j]];
+    offRho[j] = rhoBytes;
+    rhoBytes += align_up(sizeof(double) * m.R, 256);
+    offX[j] = xBytes;
+    xBytes += 2 * align_up(sizeof(double) * m.S, 256);
+    offPol[j] = polBytes;
+    polBytes += align_up(sizeof(int32_t) * m.S, 256);
+  }
+  const size_t need = rhoBytes + xBytes + polBytes;
+  int rc;
+  if ((rc = ensure_arena(ctx, &ctx->optArena, &ctx->optArenaBytes, need))) return rc;
+  if ((rc = ensure_ctl(ctx, njobs))) return rc;
+  if (static_cast<size_t>(njobs) > ctx->dOptJobsCap) {
+    cudaFree(ctx->dOptJobs);
+    ctx->dOptJobsCap = std::max<size_t>(njobs, 64);
+    CK(cudaMalloc(&ctx->dOptJobs, ctx->dOptJobsCap * sizeof(OptJob)));
+  }
+  ctx->hOptJobs.assign(njobs, OptJob{});
+  ctx->optModel.assign(model_ids, model_ids + njobs);
+  std::vector<int32_t> active, statusInit(njobs, MORAP_OK), zeroI(njobs, 0);
+  char* base = static_cast<char*>(ctx->optArena);
+  for (int j = 0; j < njobs; ++j) {
+    const HostModel& m = ctx->hm[model_ids[j]];
+    OptJob& J = ctx->hOptJobs[j];
+    J.model = model_ids[j];
+    J.rho = reinterpret_cast<double*>(base + offRho[j]);
+    J.buf[0] = reinterpret_cast<double*>(base + rhoBytes + offX[j]);
+    J.buf[1] = reinterpret_cast<double*>(base + rhoBytes + offX[j] + align_up(sizeof(double) * m.S, 256));
+    J.policy = reinterpret_cast<int32_t*>(base + rhoBytes + xBytes + offPol[j]);
+    if (!rhoHost)
+      for (int o = 0; o < K; ++o) J.w[o] = weights[static_cast<size_t>(j) * K + o];
+    if (!m.rewardFinite) statusInit[j] = MORAP_NOT_REWARD_FINITE;  // numerics.hpp:79-80
+    else active.push_back(j);
+  }
+  CK(cudaMemsetAsync(base + rhoBytes, 0, xBytes, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dOptJobs, ctx->hOptJobs.data(), njobs * sizeof(OptJob), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dStatus, statusInit.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dSweeps, zeroI.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->dDelta, 0, njobs * sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->dResidual, 0, njobs * sizeof(double), ctx->stream));
+  if ((rc = init_ctl(ctx, active, ctx->optModel))) return rc;
+
+  // rho: device-side weighted reward, or host-provided vectors
+  if (rhoHost) {
+    for (int j = 0; j < njobs; ++j) {
+      const HostModel& m = ctx->hm[model_ids[j]];
+      if (m.R) CK(cudaMemcpyAsync(ctx->hOptJobs[j].rho, rhoHost[j], sizeof(double) * m.R, cudaMemcpyHostToDevice, ctx->stream));
+    }
+  } else if (!active.empty()) {
+    k_weighted_reward<<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, ctx->dList,
+                                                                    ctx->dPrefix, ctx->hCtl->nactive,
+                                                                    ctx->hCtl->totalTiles);
+    CK(cudaGetLastError());
+    ctx->stats[8] += 1;
+  }
+  if (!active.empty())
+    if ((rc = run_loop(ctx, 0, eps, cap))) return rc;
+
+  // results: one gather kernel + one copy per array, one synchronisation
+  ctx->optSweeps.assign(njobs, 0);
+  ctx->optStatus.assign(njobs, 0);
+  std::vector<double> resid(njobs), vals(njobs);
+  k_gather_opt<<<(njobs + 255) / 256, 256, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, njobs, ctx->dSweeps,
+                                                             ctx->dGather);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(ctx->optSweeps.data(), ctx->dSweeps, njobs * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->optStatus.data(), ctx->dStatus, njobs * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(resid.data(), ctx->dResidual, njobs * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(vals.data(), ctx->dGather, njobs * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double backups = 0;
+  for (int j = 0; j < njobs; ++j) {
+    value_out[j] = vals[j];
+    if (sweeps_out) sweeps_out[j] = ctx->optSweeps[j];
+    if (residual_out) residual_out[j] = resid[j];
+    if (status_out) status_out[j] = ctx->optStatus[j];
+    backups += static_cast<double>(ctx->optSweeps[j]) * ctx->hm[model_ids[j]].nnz;
+  }
+  ctx->stats[0] += ctx->hCtl->sweepsDone;
+  ctx->stats[2] += static_cast<double>(ctx->hCtl->bytes);
+  ctx->stats[3] += backups;
+  ctx->optPolicyReady.assign(njobs, 0);
+  ctx->optJobs = njobs;
+  return MORAP_OK;
+}
+
+// Computes final-sweep argmax policies for the listed optimize jobs (on the device).
+int extract_policies(morap_ctx* ctx, const std::vector<int32_t>& jobsIn) {
+  std::vector<int32_t> jobs;
+  for (int j : jobsIn)
+    if (!ctx->optPolicyReady[j] && ctx->optSweeps[j] > 0) jobs.push_back(j);
+  if (jobs.empty()) return MORAP_OK;
+  int rc;
+  if ((rc = init_ctl(ctx, jobs, ctx->optModel))) return rc;
+  CK(cudaMemcpyAsync(ctx->dSweeps, ctx->optSweeps.data(), ctx->optSweeps.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  k_greedy_sweep<true><<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, ctx->dList,
+                                                                     ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr);
+  CK(cudaGetLastError());
+  ctx->stats[8] += 1;
+  for (int j : jobs) ctx->optPolicyReady[j] = 1;
+  return MORAP_OK;
+}
+
+int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, double eps, int cap,
+                  double* value_out, int32_t* sweeps_out, double* residual_out, int32_t* status_out,
+                  const std::vector<uint32_t>& maskInit, const std::vector<int32_t>& statusInit) {
+  int rc;
+  if ((rc = ensure_ctl(ctx, njobs))) return rc;
+  if (static_cast<size_t>(njobs) > ctx->dEvalJobsCap) {
+    cudaFree(ctx->dEvalJobsRaw);
+    ctx->dEvalJobsCap = std::max<size_t>(njobs, 64);
+    CK(cudaMalloc(&ctx->dEvalJobsRaw, ctx->dEvalJobsCap * sizeof(EvalJob)));
+  }
+  // arena: per job per rhs two x buffers
+  size_t need = 0;
+  for (int j = 0; j < njobs; ++j) need += 2 * proto[j].nrhs * align_up(sizeof(double) * ctx->hm[proto[j].model].S, 256);
+  if ((rc = ensure_arena(ctx, &ctx->evalArena, &ctx->evalArenaBytes, need))) return rc;
+  ctx->hEvalJobs = proto;
+  char* p = static_cast<char*>(ctx->evalArena);
+  std::vector<int32_t> jobModel(njobs), active, nrhs(njobs);
+  for (int j = 0; j < njobs; ++j) {
+    EvalJob& J = ctx->hEvalJobs[j];
+    const size_t sz = align_up(sizeof(double) * ctx->hm[J.model].S, 256);
+    for (int o = 0; o < J.nrhs; ++o) {
+      J.buf[o][0] = reinterpret_cast<double*>(p);
+      p += sz;
+      J.buf[o][1] = reinterpret_cast<double*>(p);
+      p += sz;
+    }
+    jobModel[j] = J.model;
+    nrhs[j] = J.nrhs;
+    if (maskInit[j]) active.push_back(j);
+  }
+  if (need) CK(cudaMemsetAsync(ctx->evalArena, 0, need, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dEvalJobsRaw, ctx->hEvalJobs.data(), njobs * sizeof(EvalJob), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dMask, maskInit.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dNrhs, nrhs.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dStatus, statusInit.data(), njobs * MORAP_MAX_RHS * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->dSweeps, 0, njobs * MORAP_MAX_RHS * 4, ctx->stream));
+  CK(cudaMemsetAsync(ctx->dDelta, 0, njobs * MORAP_MAX_RHS * sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->dResidual, 0, njobs * MORAP_MAX_RHS * sizeof(double), ctx->stream));
+  if ((rc = init_ctl(ctx, active, jobModel))) return rc;
+  if (!active.empty())
+    if ((rc = run_loop(ctx, 1, eps, cap))) return rc;
+
+  ctx->evalSweeps.assign(static_cast<size_t>(njobs) * MORAP_MAX_RHS, 0);
+  std::vector<int32_t> st(static_cast<size_t>(njobs) * MORAP_MAX_RHS);
+  std::vector<double> res(static_cast<size_t>(njobs) * MORAP_MAX_RHS);
+  CK(cudaMemcpyAsync(ctx->evalSweeps.data(), ctx->dSweeps, njobs * MORAP_MAX_RHS * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(st.data(), ctx->dStatus, njobs * MORAP_MAX_RHS * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(res.data(), ctx->dResidual, njobs * MORAP_MAX_RHS * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<double> vals(static_cast<size_t>(njobs) * MORAP_MAX_RHS, 0.0);
+  k_gather_eval<<<(njobs * MORAP_MAX_RHS + 255) / 256, 256, 0, ctx->stream>>>(
+      ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw, njobs, ctx->dSweeps, ctx->dGather);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(vals.data(), ctx->dGather, njobs * MORAP_MAX_RHS * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double backups = 0;
+  for (int j = 0; j < njobs; ++j) {
+    const EvalJob& J = ctx->hEvalJobs[j];
+    for (int o = 0; o < J.nrhs; ++o) {
+      const size_t q = static_cast<size_t>(j) * J.nrhs + o, s = static_cast<size_t>(j) * MORAP_MAX_RHS + o;
+      value_out[q] = vals[s];
+      if (sweeps_out) sweeps_out[q] = ctx->evalSweeps[s];
+      if (residual_out) residual_out[q] = res[s];
+      if (status_out) status_out[q] = st[s];
+      backups += static_cast<double>(ctx->evalSweeps[s]) * ctx->hm[J.model].S;
+    }
+  }
+  ctx->stats[4] += ctx->hCtl->sweepsDone;
+  ctx->stats[6] += static_cast<double>(ctx->hCtl->bytes);
+  ctx->stats[7] += backups;
+  ctx->evalJobs = njobs;
+  return MORAP_OK;
+}
+
+}  // namespace
+
+// ======================================================================================
+// C ABI
+
+extern "C" {
+
+int morap_cuda_create(int device, morap_ctx** out) {
+  if (!out) return MORAP_INVALID_CONFIG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return MORAP_CUDA_ERROR;
+  if (device < 0 || device >= ndev) return MORAP_INVALID_CONFIG;
+  morap_ctx* ctx = new morap_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) { delete ctx; return MORAP_CUDA_ERROR; }
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10) {
+    delete ctx;
+    return MORAP_CUDA_ERROR;  // built for sm_100a only
+  }
+  ctx->numSMs = prop.multiProcessorCount;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_sweep<false>, kBlock, 0);
+  int occE = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occE, k_eval_sweep, kBlock, 0);
+  occ = std::max(1, std::min(occ, occE));
+  ctx->sweepBlocks = ctx->numSMs * occ;
+  if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return MORAP_CUDA_ERROR; }
+  ctx->stream = ctx->own;
+  cudaEventCreate(&ctx->ev0);
+  cudaEventCreate(&ctx->ev1);
+  *out = ctx;
+  return MORAP_OK;
+}
+
+int morap_cuda_destroy(morap_ctx* ctx) {
+  if (!ctx) return MORAP_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (void* p : ctx->modelAllocs) cudaFree(p);
+  cudaFree(ctx->dModels);
+  cudaFree(ctx->optArena);
+  cudaFree(ctx->evalArena);
+  cudaFree(ctx->dOptJobs);
+  cudaFree(ctx->dEvalJobsRaw);
+  cudaFree(ctx->dList);
+  cudaFree(ctx->dPrefix);
+  cudaFree(ctx->dJobModel);
+  cudaFree(ctx->dDelta);
+  cudaFree(ctx->dMask);
+  cudaFree(ctx->dNrhs);
+  cudaFree(ctx->dSweeps);
+  cudaFree(ctx->dResidual);
+  cudaFree(ctx->dStatus);
+  cudaFree(ctx->dGather);
+  cudaFree(ctx->evalStage);
+  cudaFree(ctx->dCtl);
+  cudaFreeHost(ctx->hCtl);
+  cudaEventDestroy(ctx->ev0);
+  cudaEventDestroy(ctx->ev1);
+  cudaStreamDestroy(ctx->own);
+  delete ctx;
+  return MORAP_OK;
+}
+
+int morap_cuda_set_stream(morap_ctx* ctx, void* s) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+  return MORAP_OK;
+}
+
+const char* morap_cuda_last_error(morap_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models, int32_t* ids_out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  if (nmodels < 0 || (nmodels > 0 && !models)) return ctx->fail(MORAP_INVALID_CONFIG, "bad model list");
+  if (nmodels == 0) return MORAP_OK;
+  cudaSetDevice(ctx->device);
+  int rc;
+  for (int m = 0; m < nmodels; ++m)
+    if ((rc = validate_view(ctx, models[m], m))) return rc;
+  // pack every array of the batch into one device allocation
+  std::vector<std::vector<int32_t>> tiles(nmodels);
+  size_t bytes = 0;
+  std::vector<size_t> off(nmodels);
+  for (int m = 0; m < nmodels; ++m) {
+    const morap_csr_view& v = models[m];
+    make_tiles(v.row_offset, v.num_states, tiles[m]);
+    off[m] = bytes;
+    bytes += align_up(4ull * (v.num_states + 1), 256) + align_up(4ull * (v.num_rows + 1), 256) +
+             align_up(4ull * v.nnz, 256) + align_up(8ull * v.nnz, 256) + align_up(1ull * v.num_states, 256) +
+             static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256) +
+             align_up(4ull * tiles[m].size(), 256);
+  }
+  void* dev = nullptr;
+  CK(cudaMalloc(&dev, bytes));
+  ctx->modelAllocs.push_back(dev);
+  char* host = nullptr;
+  CK(cudaMallocHost(&host, bytes));
+  const int first = static_cast<int>(ctx->hm.size());
+  for (int m = 0; m < nmodels; ++m) {
+    const morap_csr_view& v = models[m];
+    char* h = host + off[m];
+    char* d = static_cast<char*>(dev) + off[m];
+    DevModel dmod{};
+    auto put = [&](const void* src, size_t n) {
+      std::memcpy(h, src, n);
+      char* at = d;
+      const size_t a = align_up(n, 256);
+      h += a;
+      d += a;
+      return at;
+    };
+    dmod.rowOffset = reinterpret_cast<const int32_t*>(put(v.row_offset, 4ull * (v.num_states + 1)));
+    dmod.trnOffset = reinterpret_cast<const int32_t*>(put(v.trn_offset, 4ull * (v.num_rows + 1)));
+    dmod.succ = reinterpret_cast<const int32_t*>(put(v.succ, 4ull * v.nnz));
+    dmod.prob = reinterpret_cast<const double*>(put(v.prob, 8ull * v.nnz));
+    dmod.done = reinterpret_cast<const uint8_t*>(put(v.done, v.num_states));
+    for (int o = 0; o < v.num_objectives; ++o)
+      dmod.obj[o] = reinterpret_cast<const double*>(put(v.rewards[o], 8ull * v.num_rows));
+    dmod.tileStart = reinterpret_cast<const int32_t*>(put(tiles[m].data(), 4ull * tiles[m].size()));
+    dmod.S = v.num_states;
+    dmod.R = v.num_rows;
+    dmod.nnz = v.nnz;
+    dmod.initial = v.initial;
+    dmod.ntiles = static_cast<int32_t>(tiles[m].size() - 1);
+    dmod.K = v.num_objectives;
+    dmod.rewardFinite = v.reward_finite ? 1 : 0;
+    // succ 4 + prob 8 per nnz; trnOffset 4 + rho 8 per row;
+    // rowOffset 4 + done 1 + x 8 + y 8 per state.
+    dmod.bytesPerSweep = 12ull * v.nnz + 12ull * v.num_rows + 21ull * v.num_states;
+    dmod.bytesPerEval = 0;  // filled below (needs mean nnz per row)
+    const double nnzPerRow = v.num_rows ? static_cast<double>(v.nnz) / v.num_rows : 0.0;
+    // evaluate, one RHS: policy 4 + trnOffset pair 8 + rho 8 + x 8 + y 8 + done 1 + 12 * nnz(row)
+    dmod.bytesPerEval = static_cast<unsigned long long>(v.num_states * (37.0 + 12.0 * nnzPerRow));
+    ctx->dm.push_back(dmod);
+    ctx->hm.push_back(HostModel{v.num_states, v.num_rows, v.nnz, v.initial, dmod.ntiles, v.num_objectives,
+                                dmod.rewardFinite});
+    if (ids_out) ids_out[m] = first + m;
+  }
+  cudaError_t e = cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFreeHost(host);
+  if (e != cudaSuccess) return ctx->cudaFail(e, "upload copy", __LINE__);
+  if ((rc = upload_models_table(ctx))) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MORAP_OK;
+}
+
+int morap_cuda_release_models(morap_ctx* ctx) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (void* p : ctx->modelAllocs) cudaFree(p);
+  ctx->modelAllocs.clear();
+  ctx->dm.clear();
+  ctx->hm.clear();
+  ctx->optJobs = 0;
+  ctx->evalJobs = 0;
+  return MORAP_OK;
+}
+
+int morap_cuda_num_models(morap_ctx* ctx) { return ctx ? static_cast<int>(ctx->hm.size()) : -1; }
+
+int morap_cuda_optimize(morap_ctx* ctx, int njobs, const int32_t* model_ids, const double* weights, int K, double eps,
+                        int sweep_cap, double* value_out, int32_t* sweeps_out, double* residual_out,
+                        int32_t* status_out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  cudaSetDevice(ctx->device);
+  return optimize_impl(ctx, njobs, model_ids, weights, K, nullptr, eps, sweep_cap, value_out, sweeps_out,
+                       residual_out, status_out);
+}
+
+int morap_cuda_optimize_rho(morap_ctx* ctx, int njobs, const int32_t* model_ids, const double* const* rho, double eps,
+                            int sweep_cap, double* value_out, int32_t* sweeps_out, double* residual_out,
+                            int32_t* status_out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  if (njobs > 0 && !rho) return ctx->fail(MORAP_INVALID_CONFIG, "null reward list");
+  cudaSetDevice(ctx->device);
+  return optimize_impl(ctx, njobs, model_ids, nullptr, 0, rho, eps, sweep_cap, value_out, sweeps_out, residual_out,
+                       status_out);
+}
+
+int morap_cuda_fetch_values(morap_ctx* ctx, int job, double* out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  if (job < 0 || job >= ctx->optJobs) return ctx->fail(MORAP_INVALID_CONFIG, "job out of range");
+  cudaSetDevice(ctx->device);
+  const HostModel& m = ctx->hm[ctx->optModel[job]];
+  if (ctx->optSweeps[job] <= 0) {
+    std::fill(out, out + m.S, 0.0);
+    return MORAP_OK;
+  }
+  CK(cudaMemcpyAsync(out, ctx->hOptJobs[job].buf[ctx->optSweeps[job] & 1], sizeof(double) * m.S,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MORAP_OK;
+}
+
+int morap_cuda_fetch_policy(morap_ctx* ctx, int job, int32_t* out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  if (job < 0 || job >= ctx->optJobs) return ctx->fail(MORAP_INVALID_CONFIG, "job out of range");
+  if (ctx->optSweeps[job] <= 0) return ctx->fail(ctx->optStatus[job] ? ctx->optStatus[job] : MORAP_INVALID_CONFIG, "job has no policy");
+  cudaSetDevice(ctx->device);
+  int rc = extract_policies(ctx, {job});
+  if (rc) return rc;
+  const HostModel& m = ctx->hm[ctx->optModel[job]];
+  CK(cudaMemcpyAsync(out, ctx->hOptJobs[job].policy, sizeof(int32_t) * m.S, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MORAP_OK;
+}
+
+int morap_cuda_evaluate_optimized(morap_ctx* ctx, int njobs, const int32_t* opt_jobs, int nrhs, const int32_t* objective,
+                                  double eps, int sweep_cap, double* value_out, int32_t* sweeps_out,
+                                  double* residual_out, int32_t* status_out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  cudaSetDevice(ctx->device);
+  if (njobs < 0 || nrhs < 1 || nrhs > MORAP_MAX_RHS) return ctx->fail(MORAP_INVALID_CONFIG, "bad evaluate batch");
+  if (!(eps >= 0.0) || sweep_cap < 1) return ctx->fail(MORAP_INVALID_CONFIG, "bad eps / sweep cap");
+  ctx->evalJobs = 0;
+  if (njobs == 0) return MORAP_OK;
+  std::vector<int32_t> jl(opt_jobs, opt_jobs + njobs);
+  for (int j : jl)
+    if (j < 0 || j >= ctx->optJobs) return ctx->fail(MORAP_INVALID_CONFIG, "unknown optimize job");
+  for (int j : jl)
+    if (ctx->optSweeps[j] <= 0 || ctx->optStatus[j] != MORAP_OK)
+      return ctx->fail(ctx->optStatus[j] ? ctx->optStatus[j] : MORAP_SOLVER_FAILURE, "optimize job failed");
+  int rc = extract_policies(ctx, jl);
+  if (rc) return rc;
+  std::vector<EvalJob> proto(njobs);
+  std::vector<uint32_t> mask(njobs, (1u << nrhs) - 1u);
+  std::vector<int32_t> st(static_cast<size_t>(njobs) * MORAP_MAX_RHS, MORAP_OK);
+  for (int q = 0; q < njobs; ++q) {
+    const int j = jl[q];
+    const int model = ctx->optModel[j];
+    EvalJob& E = proto[q];
+    E = EvalJob{};
+    E.model = model;
+    E.nrhs = nrhs;
+    E.policy = ctx->hOptJobs[j].policy;
+    for (int o = 0; o < nrhs; ++o) {
+      if (objective[o] < 0 || objective[o] >= ctx->hm[model].K)
+        return ctx->fail(MORAP_DIMENSION_MISMATCH, "objective index out of range");
+      E.rho[o] = ctx->dm[model].obj[objective[o]];
+    }
+  }
+  return evaluate_impl(ctx, njobs, proto, eps, sweep_cap, value_out, sweeps_out, residual_out, status_out, mask, st);
+}
+
+int morap_cuda_evaluate(morap_ctx* ctx, int njobs, const int32_t* model_ids, const int32_t* const* policies,
+                        const double* const* rho, double eps, int sweep_cap, double* value_out, int32_t* sweeps_out,
+                        double* residual_out, int32_t* status_out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  cudaSetDevice(ctx->device);
+  if (njobs < 0 || (njobs > 0 && (!model_ids || !policies || !rho)))
+    return ctx->fail(MORAP_INVALID_CONFIG, "bad evaluate batch");
+  if (!(eps >= 0.0) || sweep_cap < 1) return ctx->fail(MORAP_INVALID_CONFIG, "bad eps / sweep cap");
+  ctx->evalJobs = 0;
+  if (njobs == 0) return MORAP_OK;
+  // stage policies + rewards in one device block
+  size_t bytes = 0;
+  std::vector<size_t> off(njobs);
+  for (int j = 0; j < njobs; ++j) {
+    if (model_ids[j] < 0 || model_ids[j] >= static_cast<int>(ctx->hm.size()))
+      return ctx->fail(MORAP_INVALID_CONFIG, "unknown model id");
+    const HostModel& m = ctx->hm[model_ids[j]];
+    off[j] = bytes;
+    bytes += align_up(4ull * m.S, 256) + align_up(8ull * m.R, 256);
+  }
+  int rc;
+  if ((rc = ensure_arena(ctx, &ctx->evalStage, &ctx->evalStageBytes, bytes))) return rc;
+  std::vector<EvalJob> proto(njobs);
+  std::vector<uint32_t> mask(njobs, 1u);
+  std::vector<int32_t> st(static_cast<size_t>(njobs) * MORAP_MAX_RHS, MORAP_OK);
+  std::vector<int32_t> rowsHost;
+  for (int j = 0; j < njobs; ++j) {
+    const int model = model_ids[j];
+    const HostModel& m = ctx->hm[model];
+    // checkScheduler (numerics.hpp:51-66) needs rowOffset; validate against host copy
+    std::vector<int32_t> ro(m.S + 1);
+    CK(cudaMemcpy(ro.data(), ctx->dm[model].rowOffset, 4ull * (m.S + 1), cudaMemcpyDeviceToHost));
+    std::vector<uint8_t> dn(m.S);
+    CK(cudaMemcpy(dn.data(), ctx->dm[model].done, m.S, cudaMemcpyDeviceToHost));
+    bool ok = true;
+    for (int s = 0; s < m.S && ok; ++s)
+      if (!dn[s] && (policies[j][s] < ro[s] || policies[j][s] >= ro[s + 1])) ok = false;
+    char* base = static_cast<char*>(ctx->evalStage) + off[j];
+    CK(cudaMemcpyAsync(base, policies[j], 4ull * m.S, cudaMemcpyHostToDevice, ctx->stream));
+    char* rb = base + align_up(4ull * m.S, 256);
+    if (m.R) CK(cudaMemcpyAsync(rb, rho[j], 8ull * m.R, cudaMemcpyHostToDevice, ctx->stream));
+    EvalJob& E = proto[j];
+    E = EvalJob{};
+    E.model = model;
+    E.nrhs = 1;
+    E.policy = reinterpret_cast<const int32_t*>(base);
+    E.rho[0] = reinterpret_cast<const double*>(rb);
+    if (!ok) {
+      mask[j] = 0;
+      st[static_cast<size_t>(j) * MORAP_MAX_RHS] = MORAP_INVALID_MODEL;
+    }
+  }
+  return evaluate_impl(ctx, njobs, proto, eps, sweep_cap, value_out, sweeps_out, residual_out, status_out, mask, st);
+}
+
+int morap_cuda_fetch_eval_values(morap_ctx* ctx, int job, int rhs, double* out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  if (job < 0 || job >= ctx->evalJobs) return ctx->fail(MORAP_INVALID_CONFIG, "job out of range");
+  const EvalJob& J = ctx->hEvalJobs[job];
+  if (rhs < 0 || rhs >= J.nrhs) return ctx->fail(MORAP_INVALID_CONFIG, "rhs out of range");
+  cudaSetDevice(ctx->device);
+  const HostModel& m = ctx->hm[J.model];
+  const int sw = ctx->evalSweeps[job * MORAP_MAX_RHS + rhs];
+  if (sw <= 0) {
+    std::fill(out, out + m.S, 0.0);
+    return MORAP_OK;
+  }
+  CK(cudaMemcpyAsync(out, J.buf[rhs][sw & 1], 8ull * m.S, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MORAP_OK;
+}
+
+int morap_cuda_set_profiling(morap_ctx* ctx, int on) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  ctx->profiling = on != 0;
+  return MORAP_OK;
+}
+
+int morap_cuda_stats(morap_ctx* ctx, double* out, int nout) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  for (int i = 0; i < nout && i < 9; ++i) out[i] = ctx->stats[i];
+  return MORAP_OK;
+}
+
+int morap_cuda_reset_stats(morap_ctx* ctx) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  for (double& s : ctx->stats) s = 0.0;
+  return MORAP_OK;
+}
+
+int morap_cuda_device_bytes(morap_ctx* ctx, int64_t* out) {
+  if (!ctx || !out) return MORAP_INVALID_CONFIG;
+  *out = static_cast<int64_t>(ctx->optArenaBytes + ctx->evalArenaBytes);
+  return MORAP_OK;
+}
+
+}  // extern "C"
