@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the MORAP hot path on B200 (BASELINE.json metric: nnz Bellman backups per
+second + Pareto-query wall time).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2]
+
+A step is one point-oriented Pareto query (paretoPoint, solver.hpp:281) on the workload
+-- default C2 of BASELINE.json configs[1]: 10x10 grid warehouse, 10 agents x 10 tasks,
+2 objectives, thresholds (-20 x10, 0.99 x10), eps 0.01 (infeasible; 13 Alg.-1 iterations
+of 100 optimize + 20 evaluate jobs each). Synthetic instance from the seeded warehouse
+generator (warehouse.hpp:176), built on the host before timing.
+
+  value    nnz backups of the query / device time of the query, products resident in HBM
+  e2e      the same metric through the host API with HOST buffers: every step uploads the
+           instance's product CSR (H2D) and reads back values/policies (D2H)
+  roofline dominant kernel k_greedy_sweep: algorithmic bytes (12 nnz + 12 R + 21 S per
+           active job per sweep) / its CUDA-event time over the timed steps
+  cpu_baseline  the reference's own engine (oracle/_ref, runBatch over all host threads)
+           on one optimize phase of the same instance
+
+Multi-GPU (torchrun, N > 1): products are sharded across ranks (distributed.py); every
+rank runs the host loop, values are exchanged by all_gather over NCCL. Reported "weak":
+the instance grows with N so that per-GPU work stays ~constant (n = round(10 sqrt(N))).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "transitions/sec (nnz Bellman backups) + Pareto-query wall time at 1/2/4/8 B200 vs CPU"
+UNIT = "nnz-backups/s"
+
+
+def workload(name: str, world: int = 1):
+    if name == "c2":
+        n = 10 if world == 1 else int(round(10 * math.sqrt(world)))
+        W = H = 10
+        cfg = {"W": W, "H": H, "n": n, "slip": 0.05,
+               "racks": [[W - 1 - (k % W), H - 1 - (k // W)] for k in range(n)], "feed": [0, 0], "seed": 42}
+        return cfg, [-20.0] * n + [0.99] * n, 0.01, 2
+    if name == "c1":
+        cfg = {"W": 6, "H": 6, "n": 2, "slip": 0.05, "racks": [[5, 5], [0, 5], [5, 0]], "feed": [0, 0], "seed": 42}
+        return cfg, [-30.0, -36.0, 0.95, 0.8], 0.01, 2
+    if name == "c3":  # 50 x 50, 3 objectives, infeasible target
+        n, W = 50, 8
+        cfg = {"W": W, "H": W, "n": n, "slip": 0.05,
+               "racks": [[W - 1 - (k % W), W - 1 - (k // W)] for k in range(n)], "feed": [0, 0], "seed": 42}
+        return cfg, [-20.0] * (2 * n) + [0.99] * n, 0.01, 3
+    raise SystemExit(f"unknown workload {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_launch"), d
+    return None, None
+
+
+def csr_bytes(inst) -> int:
+    """Host->device bytes of one instance upload (distinct products, morap_cuda_upload)."""
+    seen, total = set(), 0
+    for i in range(inst.n):
+        for j in range(inst.n):
+            dims, _ = inst.product_dims(i, j)
+            S, R, nnz, first = int(dims[0]), int(dims[1]), int(dims[2]), int(dims[5])
+            if first in seen:
+                continue
+            seen.add(first)
+            total += 4 * (S + 1) + 4 * (R + 1) + 12 * nnz + S + 8 * R * inst.objectives
+    return total
+
+
+def d2h_bytes(inst, report) -> int:
+    n, K = inst.n, inst.objectives
+    per_iter = 8 * n * n + 8 * K * n + 4 * n
+    pol = 0
+    for it in report["iterations"]:
+        for j, i in enumerate(it["assignment"]):
+            pol += 4 * int(inst.product_dims(i, j)[0][0])
+    return per_iter * len(report["iterations"]) + pol
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_baseline(cfg, n):
+    """The reference engine (oracle/_ref) on this host, one optimize phase at uniform w."""
+    import oracle
+    if not oracle.ref_available():
+        return None
+    ref = oracle.ref()
+    inst = ref.warehouse(cfg)
+    w = np.full(2 * n, 1.0 / (2 * n))
+    sec, backups = inst.optimize_phase(w, 0)
+    threads = ref.hardware_threads()
+    return {"value": backups / sec, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"oracle/_ref runBatch (engine.hpp:370) of the {n * n} optimize jobs of one supportingPoint at "
+                      f"uniform w on the same instance, {threads} worker threads, {sec:.2f} s wall, "
+                      f"{backups:.3e} backups"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg, thr, eps, K = workload(args.workload, world)
+    n = cfg["n"]
+    line = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True}
+    if not oracle.ref_available():
+        line["unavailable"] = "oracle/_ref/libmorap_ref.so was not built (needs /root/reference at build time)"
+        print(json.dumps(line))
+        return
+    ref = oracle.ref()
+    t0 = time.time()
+    inst = ref.warehouse(cfg)
+    gen = time.time() - t0
+    w = np.full(2 * n, 1.0 / (2 * n))
+    for _ in range(args.warmup):
+        inst.optimize_phase(w, 0)
+    secs, bks = [], []
+    for _ in range(args.steps):
+        s, b = inst.optimize_phase(w, 0)
+        secs.append(s)
+        bks.append(b)
+    value = sum(bks) / sum(secs)
+    threads = ref.hardware_threads()
+    line.update({
+        "value": value, "ms_per_step": 1e3 * sum(secs) / len(secs), "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded warehouse generator, warehouse.hpp:176)",
+        "config": {"workload": args.workload, "grid": [cfg["W"], cfg["H"]], "agents": n, "tasks": n, "objectives": 2,
+                   "step": "one optimize phase of supportingPoint (n^2 jobs, runBatch) at uniform w",
+                   "generate_s": gen},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} optimize phases of {n * n} jobs on {threads} host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    })
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        from paper_2305_04397_b200 import distributed
+        return distributed.bench_main(args, rank, world, local)
+    from paper_2305_04397_b200.api import Instance, Solver
+
+    torch.cuda.set_device(local)
+    cfg, thr, eps, K = workload(args.workload, 1)
+    t0 = time.time()
+    inst = Instance.warehouse(cfg)
+    if K > 2:
+        inst.add_objectives(K, seed=7)
+    gen_s = time.time() - t0
+    solver = Solver(local)
+    stream = torch.cuda.current_stream()
+    solver.set_stream(stream.cuda_stream)
+    solver.upload(inst)
+    solver.set_profiling(True)
+
+    # ---- device-resident timed region --------------------------------------------------
+    for _ in range(max(args.warmup, 0)):
+        report = solver.pareto(inst, thr, eps=eps)
+    solver.reset_cuda_stats()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    backups, reports = 0.0, []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            report = solver.pareto(inst, thr, eps=eps)
+            st = report["stats"]
+            backups += st["optimize_backups"] + st["evaluate_state_backups"]
+            reports.append(report)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    cs = solver.cuda_stats()
+    value = backups / (ms * 1e-3)
+
+    # ---- end to end through the host API with host buffers ------------------------------
+    e2e_steps = max(1, min(args.steps, 3))
+    h2d = csr_bytes(inst)
+    solver.set_profiling(False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_backups = 0.0
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        solver.release()
+        solver.upload(inst)
+        rep = solver.pareto(inst, thr, eps=eps)
+        e_backups += rep["stats"]["optimize_backups"] + rep["stats"]["evaluate_state_backups"]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e0.elapsed_time(e1)
+
+    peak, peak_src = peak_hbm()
+    achieved = cs["opt_bytes"] / (cs["opt_ms"] * 1e-3) / 1e9 if cs["opt_ms"] > 0 else None
+    traffic, traffic_src = ncu_traffic()
+    first = reports[0]
+    iters = len(first["iterations"])
+    cpu = None if args.no_cpu_baseline else cpu_baseline(cfg, cfg["n"]) if K == 2 else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded warehouse generator, warehouse.hpp:176; built before timing)",
+        "config": {"workload": args.workload, "grid": [cfg["W"], cfg["H"]], "agents": cfg["n"], "tasks": cfg["n"],
+                   "objectives": K, "eps": eps, "thresholds": f"costs {thr[0]} x{(K - 1) * cfg['n']}, probs {thr[-1]}",
+                   "feasible": first["feasible"], "pareto_iterations": iters,
+                   "products": inst.distinct, "states": inst.total_states, "nnz": inst.total_nnz,
+                   "step": "one paretoPoint query (Alg. 1) with products resident in HBM",
+                   "l2": f"inputs larger than L2 (product CSR {h2d / 1e6:.0f} MB > 126 MB)",
+                   "generate_s": round(gen_s, 3), "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "kernel": "k_greedy_sweep", "launches": cs["opt_launches"],
+                     "avg_launch_us": 1e3 * cs["opt_ms"] / max(cs["opt_launches"], 1),
+                     "algorithmic_bytes_per_launch": cs["opt_bytes"] / max(cs["opt_launches"], 1),
+                     "kernel_backups_per_s": cs["opt_backups"] / (cs["opt_ms"] * 1e-3) if cs["opt_ms"] else None,
+                     "peak_source": peak_src, "traffic_source": traffic_src and traffic_src.get("source")},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e_backups / (e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h_bytes(inst, first), "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps},
+        "clocks": clk.summary(),
+        "gpu_launches": int(cs["kernels"]),
+        "pareto_query_ms": ms / args.steps,
+    }
+    if rank == 0:
+        print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,95 @@
+/*
+ * morap.h -- C ABI of the host library (libmorap_host.so): model loader, per-instance
+ * GPU upload and the Pareto-point query, for FFI callers (ctypes/cffi, another language's
+ * runtime). The C++ API behind it is paper_2305_04397_b200/csrc/morap.hpp, which mirrors
+ * the reference's public functions; each entry below names the reference function it
+ * exposes (/root/reference/proj/include/morap/...). The reference itself has no C ABI:
+ * its front door is the `morap` CLI (cli.hpp:331), whose verbs map onto these calls
+ * (INTEGRATION.md).
+ *
+ * Conventions: every function returns 0 or 1 + morap::Errc (common.hpp:12-34), 100 for a
+ * CUDA failure; the message of the last failure on the calling thread is
+ * morap_last_error(). Nothing throws across the ABI. Pointers are host pointers.
+ */
+#ifndef MORAP_H
+#define MORAP_H
+
+#include <stdint.h>
+
+#include "morap_cuda.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct morap_instance morap_instance;
+typedef struct morap_solver morap_solver;
+
+const char* morap_last_error(void);
+
+/* generateInstance (warehouse.hpp:176) from a warehouseConfigFromJson object
+ * (warehouse.hpp:200): {"W","H","n","slip","racks","feed","seed","deadline"}.
+ * threads <= 0: all host threads build the n^2 products (buildInstance, instance.hpp:42). */
+int morap_instance_warehouse(const char* config_json, int threads, morap_instance** out);
+
+/* instanceFromJson (cli.hpp:93-117): {"agents": [...], "tasks": [...], "norm"?: [[...]]}.
+ * Relative paths resolve against base_dir. If the file carries a norm matrix and
+ * norm_out is non-null, the d x d matrix is written there (norm_cap doubles available)
+ * and *has_norm is set. */
+int morap_instance_from_json(const char* json_text, const char* base_dir, morap_instance** out, double* norm_out,
+                             int norm_cap, int* has_norm);
+void morap_instance_free(morap_instance* inst);
+
+/* out[8] = {n, realTasks, distinctProducts, K, sum states, sum rows, sum nnz over the n^2
+ * (i,j) slots, sum nnz over distinct products}. */
+int morap_instance_info(const morap_instance* inst, int64_t* out);
+
+/* Product (i, j) of the instance (ProductMdp, model.hpp:143-157).
+ * dims[6] = {S, R, nnz, initial, rewardFinite, index of the first (i',j') sharing it}. */
+int morap_instance_product_dims(const morap_instance* inst, int i, int j, int64_t* dims, uint64_t* structural_hash);
+int morap_instance_product_export(const morap_instance* inst, int i, int j, int32_t* row_offset, int32_t* trn_offset,
+                                  int32_t* succ, double* prob, double* cost, double* success, uint8_t* done,
+                                  uint8_t* accept);
+
+/* K-objective extension (not in the reference): K-2 extra seeded objectives
+ * per product. Thresholds then list (K-1)*n cost-type bounds, then the task probabilities. */
+int morap_instance_add_objectives(morap_instance* inst, int K, uint64_t seed);
+
+/* Solver = one CUDA context on `device` with the instance's products resident. */
+int morap_solver_create(int device, morap_solver** out);
+void morap_solver_free(morap_solver* s);
+morap_ctx* morap_solver_cuda(morap_solver* s);
+int morap_solver_upload(morap_solver* s, const morap_instance* inst);
+/* Drop every resident product (device memory freed; next query re-uploads). */
+int morap_solver_release(morap_solver* s);
+
+/* supportingPoint (solver.hpp:103-184): w has K*n entries (unit 1-norm). Writes r (K*n)
+ * and the assignment agent_of[n]. stats_out (nullable, 8 doubles): optimize jobs,
+ * optimize nnz backups, evaluate jobs, evaluate state backups, optimize s, evaluate s,
+ * host s, 0. */
+int morap_supporting_point(morap_solver* s, const morap_instance* inst, const double* w, int nw, double* r_out,
+                           int32_t* agent_of_out, double* stats_out);
+
+/* paretoPoint / verifyOnly (solver.hpp:281-294), iteration cap default 500, identity norm
+ * when norm == NULL. json_out receives resultToJson (solver.hpp:358) plus "converged",
+ * "thresholds", "lambdaStar", per-iteration "records" {tUp, tDown, schedulerHash} and the
+ * synthesis "marginal" (synthesize, solver.hpp:299) when the run converged; in verify mode
+ * {"verdict": bool}. stats_out as in morap_supporting_point, summed over the query. */
+int morap_pareto(morap_solver* s, const morap_instance* inst, const double* thresholds, int nt, const double* norm,
+                 double eps, int iteration_cap, int verify, char* json_out, int json_cap, double* stats_out);
+
+/* runParetoCore (solver.hpp:192-266) over an external supporting-point source, e.g. a
+ * multi-GPU driver that shards the products across ranks: query(user, w, d, r_out,
+ * agent_of_out, n) must fill r_out[d] and agent_of_out[n] and return 0 (or a status). */
+typedef int (*morap_query_fn)(void* user, const double* w, int d, double* r_out, int32_t* agent_of_out, int n);
+int morap_pareto_core(const double* expanded_thresholds, int d, int n, const double* norm, double eps,
+                      int iteration_cap, int verify, morap_query_fn query, void* user, char* json_out, int json_cap);
+
+/* maxAssignment (assignment.hpp:54): agent_of[j] for the n x n row-major value matrix. */
+int morap_max_assignment(int n, const double* c, int32_t* agent_of);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MORAP_H */

@@ -60,7 +60,7 @@ enum {
 };
 
 #define MORAP_MAX_OBJECTIVES 8 /* reward vectors per model (K; the reference has K = 2) */
-#define MORAP_MAX_RHS 4        /* reward vectors evaluated together in one fused sweep */
+#define MORAP_MAX_RHS 8        /* reward vectors evaluated together in one fused sweep */
 
 typedef struct morap_ctx morap_ctx;
 
@@ -144,7 +144,7 @@ int morap_cuda_fetch_eval_values(morap_ctx* ctx, int job, int rhs, double* value
 
 /* Instrumentation (SweepStats/bench). Totals since the last reset:
  *   out[0] sweep-kernel launches (optimize), out[1] their summed device ms (only while
- *   profiling is on: CUDA events around each launch), out[2] algorithmic bytes those
+ *   profiling is on: CUDA events around each launch, no extra synchronisation), out[2] algorithmic bytes those
  *   launches moved (12*nnz + 12*R + 21*S per active job per sweep),
  *   out[3] nnz backups performed (sum over jobs of sweeps * nnz), out[4..7] the same four
  *   for evaluate sweeps, out[8] kernels launched in total. */

@@ -1,0 +1,280 @@
+"""Python face of the host library (libmorap_host.so, include/morap.h).
+
+Mirrors the reference's user-level API (model loader, Pareto-point query):
+
+    inst = Instance.warehouse({"W": 10, "H": 10, "n": 10, ...})   # generateInstance
+    inst = Instance.from_json(text, base_dir)                      # instanceFromJson
+    solver = Solver(device=0); solver.upload(inst)
+    r, agent_of = solver.supporting_point(inst, w)                 # supportingPoint
+    report = solver.pareto(inst, thresholds, eps=0.01)             # paretoPoint
+    verdict = solver.verify(inst, thresholds, eps=0.01)            # verifyOnly
+
+Errors raise MorapError carrying the reference's Errc (common.hpp:12-34).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+import numpy as np
+
+from .cuda import load_library as _load_cuda
+from .errors import MorapError
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+HOST_SO = os.path.join(PKG, "libmorap_host.so")
+
+QUERY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double),
+                       C.POINTER(C.c_int32), C.c_int)
+
+_lib = None
+
+
+def load_host_library() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(HOST_SO):
+        raise FileNotFoundError(f"{HOST_SO} missing: run `python -m paper_2305_04397_b200.build` (no CPU fallback)")
+    _load_cuda()  # libmorap_cuda.so first (rpath also finds it)
+    lib = C.CDLL(HOST_SO)
+    p, i32, f64, u64 = C.c_void_p, C.c_int, C.c_double, C.c_uint64
+    sig = {
+        "morap_last_error": (C.c_char_p, []),
+        "morap_instance_warehouse": (i32, [C.c_char_p, i32, C.POINTER(p)]),
+        "morap_instance_from_json": (i32, [C.c_char_p, C.c_char_p, C.POINTER(p), p, i32, C.POINTER(C.c_int)]),
+        "morap_instance_free": (None, [p]),
+        "morap_instance_info": (i32, [p, p]),
+        "morap_instance_product_dims": (i32, [p, i32, i32, p, C.POINTER(u64)]),
+        "morap_instance_product_export": (i32, [p, i32, i32, p, p, p, p, p, p, p, p]),
+        "morap_instance_add_objectives": (i32, [p, i32, u64]),
+        "morap_solver_create": (i32, [i32, C.POINTER(p)]),
+        "morap_solver_free": (None, [p]),
+        "morap_solver_cuda": (p, [p]),
+        "morap_solver_upload": (i32, [p, p]),
+        "morap_solver_release": (i32, [p]),
+        "morap_supporting_point": (i32, [p, p, p, i32, p, p, p]),
+        "morap_pareto": (i32, [p, p, p, i32, p, f64, i32, i32, C.c_char_p, i32, p]),
+        "morap_pareto_core": (i32, [p, i32, i32, p, f64, i32, i32, QUERY_FN, p, C.c_char_p, i32]),
+        "morap_max_assignment": (i32, [i32, p, p]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise MorapError(rc, f"{what}: {_lib.morap_last_error().decode()}")
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class Product:
+    """Host copy of one product MDP (ProductMdp, model.hpp:143-157)."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+    @property
+    def S(self):
+        return self.rowOffset.shape[0] - 1
+
+    @property
+    def R(self):
+        return self.trnOffset.shape[0] - 1
+
+    @property
+    def nnz(self):
+        return self.succ.shape[0]
+
+
+class Instance:
+    """MorapInstance (instance.hpp:20-28) owned by the host library."""
+
+    def __init__(self, handle, norm=None):
+        self._lib = load_host_library()
+        self.h = handle
+        self.norm = norm
+        info = np.zeros(8, np.int64)
+        _check(self._lib.morap_instance_info(self.h, _ptr(info)), "instance_info")
+        (self.n, self.real_tasks, self.distinct, self.objectives, self.total_states, self.total_rows,
+         self.total_nnz, self.distinct_nnz) = (int(x) for x in info)
+
+    @classmethod
+    def warehouse(cls, config: dict, threads: int = 0) -> "Instance":
+        lib = load_host_library()
+        h = C.c_void_p()
+        _check(lib.morap_instance_warehouse(json.dumps(config).encode(), threads, C.byref(h)), "generateInstance")
+        return cls(h)
+
+    @classmethod
+    def from_json(cls, text: str, base_dir: str = ".") -> "Instance":
+        lib = load_host_library()
+        h = C.c_void_p()
+        norm = np.zeros(4096, np.float64)
+        has = C.c_int(0)
+        _check(lib.morap_instance_from_json(text.encode(), base_dir.encode(), C.byref(h), _ptr(norm), norm.shape[0],
+                                            C.byref(has)), "instanceFromJson")
+        d = has.value
+        return cls(h, norm[: d * d].reshape(d, d).copy() if d else None)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.morap_instance_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def add_objectives(self, K: int, seed: int = 0):
+        _check(self._lib.morap_instance_add_objectives(self.h, K, seed), "add_objectives")
+        self.objectives = K
+
+    def product_dims(self, i, j):
+        dims = np.zeros(6, np.int64)
+        h = C.c_uint64(0)
+        _check(self._lib.morap_instance_product_dims(self.h, i, j, _ptr(dims), C.byref(h)), "product_dims")
+        return dims, h.value
+
+    def product(self, i, j) -> Product:
+        dims, h = self.product_dims(i, j)
+        S, R, nnz, initial, fin, first = (int(x) for x in dims)
+        p = Product(rowOffset=np.zeros(S + 1, np.int32), trnOffset=np.zeros(R + 1, np.int32),
+                    succ=np.zeros(nnz, np.int32), prob=np.zeros(nnz), cost=np.zeros(R), success=np.zeros(R),
+                    done=np.zeros(S, np.uint8), accept=np.zeros(S, np.uint8), initial=initial,
+                    rewardFinite=bool(fin), first_slot=first, structural_hash=h)
+        _check(self._lib.morap_instance_product_export(
+            self.h, i, j, _ptr(p.rowOffset), _ptr(p.trnOffset), _ptr(p.succ), _ptr(p.prob), _ptr(p.cost),
+            _ptr(p.success), _ptr(p.done), _ptr(p.accept)), "product_export")
+        return p
+
+
+class Solver:
+    """One CUDA context with the instance's products resident (GpuBackend)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = load_host_library()
+        h = C.c_void_p()
+        _check(self._lib.morap_solver_create(device, C.byref(h)), "solver_create")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.morap_solver_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def cuda_ctx(self):
+        return self._lib.morap_solver_cuda(self.h)
+
+    def upload(self, inst: Instance):
+        _check(self._lib.morap_solver_upload(self.h, inst.h), "upload")
+
+    def release(self):
+        _check(self._lib.morap_solver_release(self.h), "release")
+
+    def cuda_stats(self) -> dict:
+        from .cuda import load_library
+        lib = load_library()
+        out = np.zeros(9)
+        lib.morap_cuda_stats(self.cuda_ctx, _ptr(out), 9)
+        keys = ["opt_launches", "opt_ms", "opt_bytes", "opt_backups", "eval_launches", "eval_ms", "eval_bytes",
+                "eval_state_backups", "kernels"]
+        return dict(zip(keys, out.tolist()))
+
+    def reset_cuda_stats(self):
+        from .cuda import load_library
+        load_library().morap_cuda_reset_stats(self.cuda_ctx)
+
+    def set_profiling(self, on: bool):
+        from .cuda import load_library
+        load_library().morap_cuda_set_profiling(self.cuda_ctx, int(on))
+
+    def set_stream(self, cuda_stream):
+        from .cuda import load_library
+        load_library().morap_cuda_set_stream(self.cuda_ctx, cuda_stream or None)
+
+    def supporting_point(self, inst: Instance, w):
+        w = np.ascontiguousarray(w, np.float64)
+        r = np.zeros(inst.objectives * inst.n)
+        a = np.zeros(inst.n, np.int32)
+        st = np.zeros(8)
+        _check(self._lib.morap_supporting_point(self.h, inst.h, _ptr(w), w.shape[0], _ptr(r), _ptr(a), _ptr(st)),
+               "supportingPoint")
+        self.last_stats = st
+        return r, a
+
+    def pareto(self, inst: Instance, thresholds, eps=0.01, norm=None, iteration_cap=500, verify=False) -> dict:
+        t = np.ascontiguousarray(thresholds, np.float64)
+        nm = None if norm is None else np.ascontiguousarray(norm, np.float64)
+        buf = C.create_string_buffer(1 << 24)
+        st = np.zeros(8)
+        _check(self._lib.morap_pareto(self.h, inst.h, _ptr(t), t.shape[0], None if nm is None else _ptr(nm), eps,
+                                      iteration_cap, int(verify), buf, len(buf), _ptr(st)), "paretoPoint")
+        out = json.loads(buf.value.decode())
+        out["stats"] = dict(zip(["optimize_jobs", "optimize_backups", "evaluate_jobs", "evaluate_state_backups",
+                                 "optimize_s", "evaluate_s", "host_s"], st[:7].tolist()))
+        return out
+
+    def verify(self, inst: Instance, thresholds, eps=0.01, norm=None, iteration_cap=500) -> bool:
+        return bool(self.pareto(inst, thresholds, eps, norm, iteration_cap, verify=True)["verdict"])
+
+
+def pareto_core(thresholds, n, query, eps=0.01, norm=None, iteration_cap=500, verify=False) -> dict:
+    """runParetoCore (solver.hpp:192) over a Python supporting-point source
+    query(w) -> (r, agent_of). Used by the multi-GPU driver (ranks own product shards)."""
+    lib = load_host_library()
+    t = np.ascontiguousarray(thresholds, np.float64)
+    d = t.shape[0]
+    nm = None if norm is None else np.ascontiguousarray(norm, np.float64)
+    err = []
+
+    def cb(user, wp, dd, rp, ap, nn):
+        try:
+            w = np.ctypeslib.as_array(wp, shape=(dd,)).copy()
+            r, a = query(w)
+            np.ctypeslib.as_array(rp, shape=(dd,))[:] = r
+            np.ctypeslib.as_array(ap, shape=(nn,))[:] = a
+            return 0
+        except MorapError as e:
+            err.append(e)
+            return e.status
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+            return 14
+
+    fn = QUERY_FN(cb)
+    buf = C.create_string_buffer(1 << 24)
+    rc = lib.morap_pareto_core(_ptr(t), d, n, None if nm is None else _ptr(nm), eps, iteration_cap, int(verify), fn,
+                               None, buf, len(buf))
+    if rc != 0 and err and not isinstance(err[0], MorapError):
+        raise err[0]
+    _check(rc, "runParetoCore")
+    return json.loads(buf.value.decode())
+
+
+def max_assignment(c) -> np.ndarray:
+    lib = load_host_library()
+    c = np.ascontiguousarray(c, np.float64)
+    if c.ndim != 2 or c.shape[0] != c.shape[1]:
+        raise MorapError(10, "assignment needs a square value matrix")
+    out = np.zeros(c.shape[0], np.int32)
+    _check(lib.morap_max_assignment(c.shape[0], _ptr(c), _ptr(out)), "maxAssignment")
+    return out

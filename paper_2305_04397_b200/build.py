@@ -25,7 +25,8 @@ CUDA_FLAGS = [
     "-Xcompiler", "-fPIC", "-shared",
 ]
 
-HOST_SOURCES = ["host.cpp"]
+HOST_SOURCES = ["linalg.cpp", "logic.cpp", "model.cpp", "warehouse.cpp", "assignment.cpp", "geometry.cpp",
+                "gpu.cpp", "solver.cpp", "capi.cpp"]
 
 
 def _newer(target: str, sources: list[str]) -> bool:
@@ -53,14 +54,28 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
 
 
 def build_host(force: bool = False) -> str:
+    """Compile each translation unit in parallel into build/host/*.o, then link."""
     srcs = [os.path.join(CSRC, s) for s in HOST_SOURCES if os.path.exists(os.path.join(CSRC, s))]
     if not srcs:
         return ""
-    if force or _newer(HOST_SO, _deps(HOST_SOURCES) + [CUDA_SO]):
-        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-pthread", "-ffp-contract=off",
-               f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}", f"-I{JSON_DIR}",
-               "-o", HOST_SO, *srcs, f"-L{PKG}", "-lmorap_cuda", "-Wl,-rpath,$ORIGIN"]
-        subprocess.run(cmd, check=True)
+    if not (force or _newer(HOST_SO, _deps(HOST_SOURCES) + [CUDA_SO])):
+        return HOST_SO
+    obj_dir = os.path.join(ROOT, "build", "host")
+    os.makedirs(obj_dir, exist_ok=True)
+    flags = ["-std=c++20", "-O2", "-fPIC", "-pthread", "-ffp-contract=off", f"-I{os.path.join(ROOT, 'include')}",
+             f"-I{CSRC}", f"-I{JSON_DIR}"]
+    hdrs = [os.path.join(CSRC, n) for n in os.listdir(CSRC) if n.endswith(".hpp")] + \
+        [os.path.join(ROOT, "include", n) for n in os.listdir(os.path.join(ROOT, "include"))]
+    procs, objs = [], []
+    for src in srcs:
+        obj = os.path.join(obj_dir, os.path.basename(src)[:-4] + ".o")
+        objs.append(obj)
+        if force or _newer(obj, [src] + hdrs):
+            procs.append(subprocess.Popen(["g++", *flags, "-c", "-o", obj, src]))
+    if any(p.wait() != 0 for p in procs):
+        raise RuntimeError("host library compilation failed")
+    subprocess.run(["g++", "-shared", "-pthread", "-o", HOST_SO, *objs, f"-L{PKG}", "-lmorap_cuda",
+                    "-Wl,-rpath,$ORIGIN"], check=True)
     return HOST_SO
 
 

@@ -1,0 +1,306 @@
+// extern "C" face of the host library (include/morap.h).
+#include <cstring>
+#include <fstream>
+#include <sstream>
+
+#include "morap.h"
+#include "morap.hpp"
+
+struct morap_instance {
+  morap::MorapInstance inst;
+};
+
+struct morap_solver {
+  std::unique_ptr<morap::GpuBackend> gpu;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class F>
+int guard(F&& body) {
+  try {
+    body();
+    return MORAP_OK;
+  } catch (const morap::Error& e) {
+    g_error = e.what();
+    return morap::statusOf(e.code());
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return morap::statusOf(morap::Errc::SolverFailure);
+  }
+}
+
+uint64_t rowsHash(const morap::Scheduler& mu) {  // FNV-1a over the int32 rows (test fingerprint)
+  uint64_t h = 1469598103934665603ull;
+  for (int32_t r : mu.rows)
+    for (int b = 0; b < 4; ++b) {
+      h ^= (static_cast<uint32_t>(r) >> (8 * b)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  return h;
+}
+
+void putJson(const morap::Json& j, char* out, int cap) {
+  const std::string s = j.dump();
+  if (!out || static_cast<int>(s.size()) + 1 > cap) morap::fail(morap::Errc::Io, "output buffer too small");
+  std::memcpy(out, s.c_str(), s.size() + 1);
+}
+
+morap::Json reportJson(const morap::ParetoResult& res) {
+  std::unique_ptr<morap::SynthesisResult> syn;
+  int synErr = 0;
+  if (res.converged) {
+    try {
+      syn = std::make_unique<morap::SynthesisResult>(morap::synthesize(res));
+    } catch (const morap::Error& e) {
+      synErr = morap::statusOf(e.code());
+    }
+  }
+  morap::Json j = morap::resultToJson(res, syn.get());
+  j["converged"] = res.converged;
+  j["thresholds"] = res.thresholds;
+  j["lambdaStar"] = res.lambdaStar;
+  morap::Json recs = morap::Json::array();
+  for (const auto& rec : res.iterations) {
+    morap::Json hs = morap::Json::array();
+    for (const auto& mu : rec.schedulers) hs.push_back(std::to_string(rowsHash(mu)));
+    recs.push_back({{"tUp", rec.tUp}, {"tDown", rec.tDown}, {"schedulerHash", hs}});
+  }
+  j["records"] = recs;
+  if (syn) {
+    morap::Json mg = morap::Json::array();
+    for (int a = 0; a < syn->marginal.rows; ++a) {
+      morap::Json row = morap::Json::array();
+      for (int b = 0; b < syn->marginal.cols; ++b) row.push_back(syn->marginal(a, b));
+      mg.push_back(row);
+    }
+    j["marginal"] = mg;
+  }
+  if (synErr) j["synthesisError"] = synErr;
+  return j;
+}
+
+void putStats(const morap::QueryStats& q, double* out) {
+  if (!out) return;
+  out[0] = static_cast<double>(q.optimizeJobs);
+  out[1] = q.optimizeBackups;
+  out[2] = static_cast<double>(q.evaluateJobs);
+  out[3] = q.evaluateStateBackups;
+  out[4] = q.optimizeSeconds;
+  out[5] = q.evaluateSeconds;
+  out[6] = q.hostSeconds;
+  out[7] = 0.0;
+}
+
+morap::NormMatrix normOf(const double* norm, int d) {
+  morap::Mat m(d, d, 0.0);
+  if (norm) std::memcpy(m.a.data(), norm, sizeof(double) * d * d);
+  else
+    for (int k = 0; k < d; ++k) m(k, k) = 1.0;
+  return morap::NormMatrix(std::move(m));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* morap_last_error(void) { return g_error.c_str(); }
+
+int morap_instance_warehouse(const char* config_json, int threads, morap_instance** out) {
+  return guard([&] {
+    if (!out || !config_json) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    morap::WarehouseConfig cfg = morap::warehouseConfigFromJson(morap::Json::parse(config_json));
+    *out = new morap_instance{morap::generateInstance(cfg, threads)};
+  });
+}
+
+int morap_instance_from_json(const char* text, const char* base_dir, morap_instance** out, double* norm_out,
+                             int norm_cap, int* has_norm) {
+  return guard([&] {
+    if (!out || !text) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    morap::Json j;
+    try {
+      j = morap::Json::parse(text);
+    } catch (const morap::Json::exception& e) {
+      morap::fail(morap::Errc::Io, e.what());
+    }
+    const std::string base = base_dir ? base_dir : ".";
+    auto inst = std::make_unique<morap_instance>(morap_instance{morap::instanceFromJson(j, base)});
+    if (has_norm) *has_norm = 0;
+    if (j.contains("norm") && norm_out) {
+      morap::Json nj = j.at("norm");
+      if (nj.is_string()) {
+        std::ifstream in(base + "/" + nj.get<std::string>());
+        if (!in) morap::fail(morap::Errc::Io, "cannot open norm file");
+        nj = morap::Json::parse(in);
+      }
+      if (!nj.is_array() || nj.empty()) morap::fail(morap::Errc::InvalidConfig, "norm matrix must be a nonempty array of rows");
+      const int d = static_cast<int>(nj.size());
+      if (d * d > norm_cap) morap::fail(morap::Errc::DimensionMismatch, "norm buffer too small");
+      morap::Mat m(d, d);
+      for (int r = 0; r < d; ++r) {
+        if (!nj[r].is_array() || static_cast<int>(nj[r].size()) != d)
+          morap::fail(morap::Errc::InvalidConfig, "norm matrix rows must all have the matrix dimension");
+        for (int c = 0; c < d; ++c) m(r, c) = nj[r][c].get<double>();
+      }
+      morap::NormMatrix check(m);  // validates symmetry / definiteness
+      std::memcpy(norm_out, m.a.data(), sizeof(double) * d * d);
+      if (has_norm) *has_norm = d;
+    }
+    *out = inst.release();
+  });
+}
+
+void morap_instance_free(morap_instance* inst) { delete inst; }
+
+int morap_instance_info(const morap_instance* p, int64_t* out) {
+  return guard([&] {
+    const auto& I = p->inst;
+    int64_t S = 0, R = 0, Z = 0, Zd = 0;
+    std::vector<const morap::ProductMdp*> seen;
+    for (const auto& row : I.products)
+      for (const auto& q : row) {
+        S += q->mdp.numStates;
+        R += q->mdp.numActions();
+        Z += static_cast<int64_t>(q->mdp.succ.size());
+        if (std::find(seen.begin(), seen.end(), q.get()) == seen.end()) {
+          seen.push_back(q.get());
+          Zd += static_cast<int64_t>(q->mdp.succ.size());
+        }
+      }
+    const int64_t v[8] = {I.n, I.realTasks, I.distinctProducts, I.objectives, S, R, Z, Zd};
+    std::memcpy(out, v, sizeof v);
+  });
+}
+
+int morap_instance_product_dims(const morap_instance* p, int i, int j, int64_t* dims, uint64_t* hash) {
+  return guard([&] {
+    const auto& I = p->inst;
+    if (i < 0 || j < 0 || i >= I.n || j >= I.n) morap::fail(morap::Errc::InvalidConfig, "product index out of range");
+    const morap::ProductMdp& q = *I.products[i][j];
+    int64_t first = -1;
+    for (int a = 0; a < I.n && first < 0; ++a)
+      for (int b = 0; b < I.n && first < 0; ++b)
+        if (I.products[a][b].get() == &q) first = static_cast<int64_t>(a) * I.n + b;
+    const int64_t v[6] = {q.mdp.numStates, q.mdp.numActions(), static_cast<int64_t>(q.mdp.succ.size()), q.mdp.initial,
+                          q.rewardFinite ? 1 : 0, first};
+    std::memcpy(dims, v, sizeof v);
+    if (hash) *hash = q.structuralHash;
+  });
+}
+
+int morap_instance_product_export(const morap_instance* p, int i, int j, int32_t* ro, int32_t* to, int32_t* succ,
+                                  double* prob, double* cost, double* success, uint8_t* done, uint8_t* accept) {
+  return guard([&] {
+    const auto& I = p->inst;
+    if (i < 0 || j < 0 || i >= I.n || j >= I.n) morap::fail(morap::Errc::InvalidConfig, "product index out of range");
+    const morap::ProductMdp& q = *I.products[i][j];
+    auto cp = [](auto* dst, const auto& v) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(ro, q.mdp.rowOffset);
+    cp(to, q.mdp.trnOffset);
+    cp(succ, q.mdp.succ);
+    cp(prob, q.mdp.prob);
+    cp(cost, q.cost);
+    cp(success, q.success);
+    for (int s = 0; s < q.mdp.numStates; ++s) {
+      if (done) done[s] = q.done[s] ? 1 : 0;
+      if (accept) accept[s] = q.accept[s] ? 1 : 0;
+    }
+  });
+}
+
+int morap_instance_add_objectives(morap_instance* p, int K, uint64_t seed) {
+  return guard([&] { morap::addSyntheticObjectives(p->inst, K, seed); });
+}
+
+int morap_solver_create(int device, morap_solver** out) {
+  return guard([&] {
+    if (!out) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    auto s = std::make_unique<morap_solver>();
+    s->gpu = std::make_unique<morap::GpuBackend>(device);
+    *out = s.release();
+  });
+}
+
+void morap_solver_free(morap_solver* s) { delete s; }
+
+morap_ctx* morap_solver_cuda(morap_solver* s) { return s && s->gpu ? s->gpu->ctx() : nullptr; }
+
+int morap_solver_upload(morap_solver* s, const morap_instance* inst) {
+  return guard([&] { s->gpu->uploadInstance(inst->inst); });
+}
+
+int morap_solver_release(morap_solver* s) {
+  return guard([&] { s->gpu->release(); });
+}
+
+int morap_supporting_point(morap_solver* s, const morap_instance* p, const double* w, int nw, double* r_out,
+                           int32_t* agent_of, double* stats_out) {
+  return guard([&] {
+    morap::QueryStats st;
+    morap::SupportingPoint sp = morap::supportingPoint(p->inst, morap::Vec(w, w + nw), *s->gpu, &st);
+    std::memcpy(r_out, sp.r.data(), sizeof(double) * sp.r.size());
+    for (size_t j = 0; j < sp.assignment.agentOf.size(); ++j) agent_of[j] = sp.assignment.agentOf[j];
+    putStats(st, stats_out);
+  });
+}
+
+int morap_pareto(morap_solver* s, const morap_instance* p, const double* thresholds, int nt, const double* norm,
+                 double eps, int iteration_cap, int verify, char* json_out, int json_cap, double* stats_out) {
+  return guard([&] {
+    const int d = p->inst.objectives * p->inst.n;
+    morap::NormMatrix M = normOf(norm, d);
+    morap::Vec t(thresholds, thresholds + nt);
+    morap::QueryStats st;
+    if (verify) {
+      const bool v = morap::verifyOnly(p->inst, t, M, eps, *s->gpu, iteration_cap);
+      putJson(morap::Json{{"verdict", v}}, json_out, json_cap);
+    } else {
+      morap::ParetoResult res = morap::paretoPoint(p->inst, t, M, eps, *s->gpu, iteration_cap, &st);
+      putJson(reportJson(res), json_out, json_cap);
+    }
+    putStats(st, stats_out);
+  });
+}
+
+int morap_pareto_core(const double* thr, int d, int n, const double* norm, double eps, int iteration_cap, int verify,
+                      morap_query_fn query, void* user, char* json_out, int json_cap) {
+  return guard([&] {
+    if (!query) morap::fail(morap::Errc::InvalidConfig, "null query callback");
+    morap::NormMatrix M = normOf(norm, d);
+    bool verdict = false;
+    auto q = [&](const morap::Vec& w) {
+      morap::SupportingPoint sp;
+      sp.r.assign(static_cast<size_t>(d), 0.0);
+      std::vector<int32_t> a(static_cast<size_t>(n), -1);
+      const int rc = query(user, w.data(), d, sp.r.data(), a.data(), n);
+      if (rc != 0) {
+        const morap::Errc e = rc >= 1 && rc <= 21 ? static_cast<morap::Errc>(rc - 1) : morap::Errc::SolverFailure;
+        morap::fail(e, "external supporting-point query failed");
+      }
+      sp.assignment.agentOf.assign(a.begin(), a.end());
+      sp.schedulers.resize(static_cast<size_t>(n));
+      return sp;
+    };
+    morap::ParetoResult res =
+        morap::runParetoCore(morap::Vec(thr, thr + d), M, eps, iteration_cap, verify != 0, verify ? &verdict : nullptr, q);
+    morap::Json j = reportJson(res);
+    if (verify) j["verdict"] = verdict;
+    putJson(j, json_out, json_cap);
+  });
+}
+
+int morap_max_assignment(int n, const double* c, int32_t* agent_of) {
+  return guard([&] {
+    morap::Mat m(n, n);
+    std::memcpy(m.a.data(), c, sizeof(double) * n * n);
+    morap::Assignment a = morap::maxAssignment(m);
+    for (int j = 0; j < n; ++j) agent_of[j] = a.agentOf[j];
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,400 @@
+// Model loader and product builder (reference: model.hpp, instance.hpp).
+//
+// buildProduct explores (agent state, DFA location) pairs breadth first from
+// (s0, delta(q0, L(s0))) and numbers product states in discovery order, so the CSR it
+// emits -- rowOffset / trnOffset / succ / prob / cost / success / done -- is identical,
+// array for array, to the reference's (tests/test_model_parity.py checks this). The pair
+// index is a flat int32 table instead of a hash map, and buildInstance builds the n^2
+// products on all host threads before deduplicating them in (i, j) order.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <set>
+#include <thread>
+
+#include "morap.hpp"
+
+namespace morap {
+
+const std::string kInternalAction = "!advance";
+
+void validateMdp(const Mdp& m, double tol) {
+  if (m.numStates <= 0) fail(Errc::InvalidModel, "model has no states");
+  if (m.initial < 0 || m.initial >= m.numStates) fail(Errc::InvalidModel, "initial state out of range");
+  for (int s = 0; s < m.numStates; ++s)
+    if (m.actionsEnd(s) <= m.actionsBegin(s)) fail(Errc::InvalidModel, "deadlock: state " + std::to_string(s) + " has no action");
+  for (int r = 0; r < m.numActions(); ++r) {
+    double total = 0.0;
+    for (int k = m.trnBegin(r); k < m.trnEnd(r); ++k) {
+      if (m.prob[k] < 0.0) fail(Errc::InvalidModel, "negative transition probability");
+      if (m.succ[k] < 0 || m.succ[k] >= m.numStates) fail(Errc::InvalidModel, "successor out of range");
+      total += m.prob[k];
+    }
+    if (std::fabs(total - 1.0) > tol)
+      fail(Errc::InvalidModel, "action row " + std::to_string(r) + " sums to " + std::to_string(total));
+  }
+}
+
+void renormalizeRows(Mdp& m) {
+  for (int r = 0; r < m.numActions(); ++r) {
+    double total = 0.0;
+    for (int k = m.trnBegin(r); k < m.trnEnd(r); ++k) total += m.prob[k];
+    if (total > 0.0)
+      for (int k = m.trnBegin(r); k < m.trnEnd(r); ++k) m.prob[k] /= total;
+  }
+}
+
+std::pair<Mdp, RewardStructure> mdpFromJson(const Json& j) {
+  if (!j.is_object() || !j.contains("states") || !j.contains("actions"))
+    fail(Errc::InvalidModel, "model JSON must carry states and actions");
+  Mdp m;
+  m.numStates = j.at("states").get<int>();
+  m.initial = j.value("initial", 0);
+  if (m.numStates <= 0) fail(Errc::InvalidModel, "model has no states");
+  m.labels.assign(static_cast<size_t>(m.numStates), {});
+  if (j.contains("labels"))
+    for (auto it = j.at("labels").begin(); it != j.at("labels").end(); ++it) {
+      const int s = std::stoi(it.key());
+      if (s < 0 || s >= m.numStates) fail(Errc::InvalidModel, "label for unknown state " + it.key());
+      auto& lab = m.labels[s];
+      for (const Json& a : it.value()) lab.push_back(a.get<std::string>());
+      std::sort(lab.begin(), lab.end());
+      lab.erase(std::unique(lab.begin(), lab.end()), lab.end());
+    }
+  // rows grouped by owning state, file order kept inside a state
+  std::vector<std::vector<const Json*>> rowsOf(static_cast<size_t>(m.numStates));
+  for (const Json& a : j.at("actions")) {
+    const int s = a.at("state").get<int>();
+    if (s < 0 || s >= m.numStates) fail(Errc::InvalidModel, "action at unknown state");
+    rowsOf[s].push_back(&a);
+  }
+  RewardStructure reward;
+  m.trnOffset.push_back(0);
+  for (int s = 0; s < m.numStates; ++s) {
+    m.rowOffset.push_back(static_cast<int>(reward.size()));
+    for (const Json* a : rowsOf[s]) {
+      for (const Json& t : a->at("to")) {
+        m.succ.push_back(t.at("s").get<int>());
+        m.prob.push_back(t.at("p").get<double>());
+      }
+      m.trnOffset.push_back(static_cast<int>(m.succ.size()));
+      m.actionName.push_back(a->value("name", ""));
+      reward.push_back(a->value("reward", 0.0));
+    }
+  }
+  m.rowOffset.push_back(static_cast<int>(reward.size()));
+  validateMdp(m);
+  renormalizeRows(m);
+  return {std::move(m), std::move(reward)};
+}
+
+Json mdpToJson(const Mdp& m, const RewardStructure& reward) {
+  Json labels = Json::object(), actions = Json::array();
+  for (int s = 0; s < m.numStates; ++s) {
+    if (!m.labels[s].empty()) labels[std::to_string(s)] = m.labels[s];
+    for (int r = m.actionsBegin(s); r < m.actionsEnd(s); ++r) {
+      Json to = Json::array();
+      for (int k = m.trnBegin(r); k < m.trnEnd(r); ++k) to.push_back({{"s", m.succ[k]}, {"p", m.prob[k]}});
+      actions.push_back({{"state", s}, {"name", m.actionName[r]}, {"to", to}, {"reward", reward[r]}});
+    }
+  }
+  return Json{{"states", m.numStates}, {"initial", m.initial}, {"labels", labels}, {"actions", actions}};
+}
+
+// Greatest set of non-done states that some scheduler can keep away from `done` forever:
+// repeatedly discard states all of whose rows may leave the candidate set.
+std::vector<int> maximalAvoidSet(const Mdp& m, const std::vector<char>& done) {
+  const int S = m.numStates, R = m.numActions();
+  std::vector<int> owner(static_cast<size_t>(R));
+  for (int s = 0; s < S; ++s)
+    for (int r = m.actionsBegin(s); r < m.actionsEnd(s); ++r) owner[r] = s;
+  std::vector<char> in(static_cast<size_t>(S));
+  for (int s = 0; s < S; ++s) in[s] = !done[s];
+  std::vector<int> leaving(static_cast<size_t>(R), 0), closedRows(static_cast<size_t>(S), 0);
+  // reverse edges successor -> rows, as a CSR
+  std::vector<int> head(static_cast<size_t>(S) + 1, 0);
+  for (int r = 0; r < R; ++r)
+    if (in[owner[r]])
+      for (int k = m.trnBegin(r); k < m.trnEnd(r); ++k) ++head[m.succ[k] + 1];
+  for (int s = 0; s < S; ++s) head[s + 1] += head[s];
+  std::vector<int> rev(static_cast<size_t>(head[S])), fill(head.begin(), head.end() - 1);
+  for (int r = 0; r < R; ++r) {
+    if (!in[owner[r]]) continue;
+    for (int k = m.trnBegin(r); k < m.trnEnd(r); ++k) {
+      rev[fill[m.succ[k]]++] = r;
+      if (!in[m.succ[k]]) ++leaving[r];
+    }
+    if (leaving[r] == 0) ++closedRows[owner[r]];
+  }
+  std::vector<int> stack;
+  for (int s = 0; s < S; ++s)
+    if (in[s] && closedRows[s] == 0) stack.push_back(s);
+  while (!stack.empty()) {
+    const int s = stack.back();
+    stack.pop_back();
+    if (!in[s]) continue;
+    in[s] = 0;
+    for (int e = head[s]; e < head[s + 1]; ++e) {
+      const int r = rev[e], o = owner[r];
+      if (!in[o]) continue;
+      if (leaving[r]++ == 0 && --closedRows[o] == 0) stack.push_back(o);
+    }
+  }
+  std::vector<int> out;
+  for (int s = 0; s < S; ++s)
+    if (in[s]) out.push_back(s);
+  return out;
+}
+
+bool checkRewardFinite(const Mdp& m, const std::vector<char>& done) { return maximalAvoidSet(m, done).empty(); }
+bool checkRewardFinite(const ProductMdp& p) { return checkRewardFinite(p.mdp, p.done); }
+
+namespace {
+
+struct Fnv {
+  uint64_t h = 1469598103934665603ull;
+  void bytes(const void* p, size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) {
+      h ^= c[i];
+      h *= 1099511628211ull;
+    }
+  }
+  template <class T>
+  void vec(const std::vector<T>& v) {
+    const uint64_t n = v.size();
+    bytes(&n, sizeof n);
+    if (!v.empty()) bytes(v.data(), v.size() * sizeof(T));
+  }
+};
+
+}  // namespace
+
+uint64_t productHash(const ProductMdp& p) {
+  Fnv f;
+  const int64_t head[2] = {p.mdp.numStates, p.mdp.initial};
+  f.bytes(head, sizeof head);
+  f.vec(p.mdp.rowOffset);
+  f.vec(p.mdp.trnOffset);
+  f.vec(p.mdp.succ);
+  f.vec(p.mdp.prob);
+  f.vec(p.cost);
+  f.vec(p.success);
+  f.vec(p.done);
+  f.vec(p.accept);
+  return f.h;
+}
+
+ProductMdp buildProduct(const Mdp& agent, const RewardStructure& agentCost, const Dfa& task, int agentId, int taskId) {
+  if (static_cast<int>(agentCost.size()) != agent.numActions())
+    fail(Errc::DimensionMismatch, "cost structure does not match the model's action rows");
+  // every acceptance must be entered through a pre-sink step (model.hpp:234-243)
+  if (task.accepting[task.initial]) fail(Errc::InvalidDfa, "task automaton lacks pre-sinks: initial location is accepting");
+  const int L = task.numLetters(), Q = task.numLocations;
+  for (int q = 0; q < Q; ++q) {
+    if (task.accepting[q] || task.preSink[q]) continue;
+    for (int w = 0; w < L; ++w)
+      if (task.accepting[task.step(q, w)])
+        fail(Errc::InvalidDfa, "task automaton lacks pre-sinks: acceptance without a pre-sink step");
+  }
+  ProductMdp p;
+  p.agentId = agentId;
+  p.taskId = taskId;
+  const int SA = agent.numStates;
+  std::vector<int> letter(static_cast<size_t>(SA));
+  std::set<std::string> dropped;
+  for (int s = 0; s < SA; ++s) {
+    letter[s] = static_cast<int>(letterMaskFor(task, agent.labels[s]));
+    for (const std::string& a : agent.labels[s])
+      if (!std::binary_search(task.atoms.begin(), task.atoms.end(), a)) dropped.insert(a);
+  }
+  p.droppedAtoms.assign(dropped.begin(), dropped.end());
+
+  std::vector<int32_t> id(static_cast<size_t>(SA) * Q, -1);
+  std::vector<int> qs, as;  // discovery order: agent state, location
+  auto visit = [&](int s, int q) {
+    int32_t& slot = id[static_cast<size_t>(s) * Q + q];
+    if (slot < 0) {
+      slot = static_cast<int32_t>(as.size());
+      as.push_back(s);
+      qs.push_back(q);
+    }
+    return static_cast<int>(slot);
+  };
+  const int q0 = task.preSink[task.initial] ? task.initial : task.step(task.initial, letter[agent.initial]);
+  Mdp& M = p.mdp;
+  M.initial = visit(agent.initial, q0);
+  M.trnOffset.push_back(0);
+  for (size_t x = 0; x < as.size(); ++x) {
+    const int s = as[x], q = qs[x];
+    M.rowOffset.push_back(M.numActions());
+    if (task.preSink[q]) {
+      M.succ.push_back(visit(s, task.step(q, letter[s])));
+      M.prob.push_back(1.0);
+      M.trnOffset.push_back(static_cast<int>(M.succ.size()));
+      M.actionName.push_back(kInternalAction);
+      p.cost.push_back(0.0);
+      p.success.push_back(1.0);
+      continue;
+    }
+    for (int r = agent.actionsBegin(s); r < agent.actionsEnd(s); ++r) {
+      for (int k = agent.trnBegin(r); k < agent.trnEnd(r); ++k) {
+        const int t = agent.succ[k];
+        M.succ.push_back(visit(t, task.step(q, letter[t])));
+        M.prob.push_back(agent.prob[k]);
+      }
+      M.trnOffset.push_back(static_cast<int>(M.succ.size()));
+      M.actionName.push_back(agent.actionName[r]);
+      p.cost.push_back(agentCost[r]);
+      p.success.push_back(0.0);
+    }
+  }
+  M.numStates = static_cast<int>(as.size());
+  M.rowOffset.push_back(M.numActions());
+  M.labels.assign(static_cast<size_t>(M.numStates), {});
+  p.agentState = as;
+  p.dfaLocation = qs;
+  p.done.resize(as.size());
+  p.accept.resize(as.size());
+  p.preSink.resize(as.size());
+  for (size_t x = 0; x < as.size(); ++x) {
+    const int q = qs[x];
+    p.accept[x] = task.accepting[q];
+    p.done[x] = task.accepting[q] || task.trap[q];
+    p.preSink[x] = task.preSink[q];
+  }
+  p.rewardFinite = checkRewardFinite(p);
+  p.structuralHash = productHash(p);
+  return p;
+}
+
+// ---- instance ----------------------------------------------------------------------------
+namespace {
+
+bool sameProduct(const ProductMdp& a, const ProductMdp& b) {
+  const Mdp &x = a.mdp, &y = b.mdp;
+  return x.numStates == y.numStates && x.initial == y.initial && x.rowOffset == y.rowOffset &&
+         x.trnOffset == y.trnOffset && x.succ == y.succ && x.prob == y.prob && x.actionName == y.actionName &&
+         a.cost == b.cost && a.success == b.success && a.done == b.done && a.accept == b.accept &&
+         a.preSink == b.preSink && a.extra == b.extra;
+}
+
+int hostThreads(int want) {
+  if (want > 0) return want;
+  const unsigned hw = std::thread::hardware_concurrency();
+  return hw ? static_cast<int>(hw) : 1;
+}
+
+}  // namespace
+
+MorapInstance buildInstance(std::vector<Mdp> agents, std::vector<RewardStructure> costs, std::vector<Dfa> tasks,
+                            int threads) {
+  if (agents.empty()) fail(Errc::InvalidModel, "instance needs at least one agent");
+  if (agents.size() != costs.size()) fail(Errc::DimensionMismatch, "one cost structure per agent required");
+  if (tasks.size() > agents.size()) fail(Errc::InvalidModel, "more tasks than agents; drop tasks or add agents");
+  MorapInstance inst;
+  inst.n = static_cast<int>(agents.size());
+  inst.realTasks = static_cast<int>(tasks.size());
+  inst.agents = std::move(agents);
+  inst.costs = std::move(costs);
+  inst.tasks = std::move(tasks);
+  for (int i = 0; i < inst.n; ++i) {
+    validateMdp(inst.agents[i]);
+    if (static_cast<int>(inst.costs[i].size()) != inst.agents[i].numActions())
+      fail(Errc::DimensionMismatch, "cost structure does not match agent action rows");
+  }
+  if (inst.realTasks < inst.n) inst.tasks.resize(static_cast<size_t>(inst.n), insertPreSinks(formulaToDfa(fTrue())));
+
+  const int n = inst.n;
+  const size_t total = static_cast<size_t>(n) * n;
+  std::vector<std::unique_ptr<ProductMdp>> built(total);
+  std::vector<std::optional<Error>> errs(total);
+  std::atomic<size_t> next{0};
+  auto worker = [&] {
+    for (size_t k; (k = next.fetch_add(1)) < total;) {
+      const int i = static_cast<int>(k / n), j = static_cast<int>(k % n);
+      try {
+        built[k] = std::make_unique<ProductMdp>(buildProduct(inst.agents[i], inst.costs[i], inst.tasks[j], i, j));
+      } catch (const Error& e) {
+        errs[k] = e;
+      }
+    }
+  };
+  const int T = std::min<int>(hostThreads(threads), static_cast<int>(total));
+  std::vector<std::thread> pool;
+  for (int t = 1; t < T; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+
+  // reject / deduplicate in (i, j) order, as instance.hpp:445-466 does sequentially
+  std::map<uint64_t, std::vector<std::shared_ptr<const ProductMdp>>> byHash;
+  inst.products.assign(static_cast<size_t>(n), std::vector<std::shared_ptr<const ProductMdp>>(static_cast<size_t>(n)));
+  for (size_t k = 0; k < total; ++k) {
+    const int i = static_cast<int>(k / n), j = static_cast<int>(k % n);
+    if (errs[k]) throw *errs[k];
+    if (!built[k]->rewardFinite)
+      fail(Errc::NotRewardFinite,
+           "product of agent " + std::to_string(i) + " and task " + std::to_string(j) + " can cycle without finishing");
+    auto& bucket = byHash[built[k]->structuralHash];
+    std::shared_ptr<const ProductMdp> share;
+    for (const auto& cand : bucket)
+      if (sameProduct(*cand, *built[k])) {
+        share = cand;
+        break;
+      }
+    if (!share) {
+      share = std::shared_ptr<const ProductMdp>(built[k].release());
+      bucket.push_back(share);
+      ++inst.distinctProducts;
+    }
+    inst.products[i][j] = share;
+  }
+  return inst;
+}
+
+Vec expandThresholds(const MorapInstance& inst, const Vec& user) {
+  const int K = inst.objectives;
+  // costs (and extra per-agent objectives) first, then one probability per real task
+  const int want = (K - 1) * inst.n + inst.realTasks;
+  if (static_cast<int>(user.size()) != want)
+    fail(Errc::DimensionMismatch, "expected " + std::to_string(want) + " thresholds (costs first, then task probabilities)");
+  Vec t(static_cast<size_t>(K) * inst.n, 0.0);
+  for (int i = 0; i < (K - 1) * inst.n; ++i) {
+    if (!std::isfinite(user[i])) fail(Errc::InvalidModel, "cost threshold must be finite");
+    t[i] = user[i];
+  }
+  for (int j = 0; j < inst.realTasks; ++j) {
+    const double p = user[(K - 1) * inst.n + j];
+    if (!(p >= 0.0 && p <= 1.0)) fail(Errc::InvalidModel, "probability threshold outside [0,1]");
+    t[(K - 1) * inst.n + j] = p;
+  }
+  return t;
+}
+
+void addSyntheticObjectives(MorapInstance& inst, int K, uint64_t seed) {
+  if (K < 2 || K > 8) fail(Errc::InvalidConfig, "objective count must lie in [2, 8]");
+  std::map<const ProductMdp*, std::shared_ptr<ProductMdp>> remap;
+  for (int i = 0; i < inst.n; ++i)
+    for (int j = 0; j < inst.n; ++j) {
+      const ProductMdp* key = inst.products[i][j].get();
+      auto it = remap.find(key);
+      if (it == remap.end()) {
+        auto copy = std::make_shared<ProductMdp>(*key);
+        copy->extra.clear();
+        std::mt19937_64 rng(seed ^ (0x9e3779b97f4a7c15ull * (static_cast<uint64_t>(i) * inst.n + j + 1)));
+        std::uniform_real_distribution<double> u(-2.0, 0.0);
+        for (int k = 2; k < K; ++k) {
+          RewardStructure v(copy->cost.size());
+          for (size_t r = 0; r < v.size(); ++r) v[r] = copy->mdp.actionName[r] == kInternalAction ? 0.0 : u(rng);
+          copy->extra.push_back(std::move(v));
+        }
+        it = remap.emplace(key, std::move(copy)).first;
+      }
+      inst.products[i][j] = it->second;
+    }
+  inst.objectives = K;
+}
+
+}  // namespace morap

@@ -9,6 +9,8 @@
 // solver in this library.
 #pragma once
 
+#include <algorithm>
+#include <array>
 #include <cstdint>
 #include <functional>
 #include <map>

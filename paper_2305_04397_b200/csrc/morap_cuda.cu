@@ -271,7 +271,9 @@ __global__ void __launch_bounds__(kBlock) k_eval_sweep(const DevModel* __restric
     const uint32_t mask = rhsMask[job];
     const int nrhs = J.nrhs;
 
-    double d[MORAP_MAX_RHS] = {0.0, 0.0, 0.0, 0.0};
+    double d[MORAP_MAX_RHS];
+#pragma unroll
+    for (int o = 0; o < MORAP_MAX_RHS; ++o) d[o] = 0.0;
     if (threadIdx.x < ns) {
       const int s = s0 + threadIdx.x;
       if (!M.done[s]) {
@@ -468,7 +470,8 @@ struct DevBuf {
 struct morap_ctx {
   int device = 0;
   int numSMs = 148;
-  int sweepBlocks = 0;  // persistent grid of the sweep kernels
+  int sweepBlocks = 0;  // persistent grid of the greedy sweep kernel
+  int evalBlocks = 0;   // persistent grid of the evaluate sweep kernel
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   std::string err;
@@ -514,6 +517,9 @@ struct morap_ctx {
   int32_t* dStatus = nullptr;
   void* evalStage = nullptr;
   size_t evalStageBytes = 0;
+  void* stage = nullptr;  // pinned host staging for uploads
+  size_t stageBytes = 0;
+  std::vector<cudaEvent_t> evPool;  // per-sweep start/stop events (profiling)
   Ctl* dCtl = nullptr;
   Ctl* hCtl = nullptr;  // pinned mirror
   void* dEvalJobsRaw = nullptr;
@@ -630,10 +636,6 @@ int ensure_arena(morap_ctx* ctx, void** arena, size_t* have, size_t need) {
   return MORAP_OK;
 }
 
-void launch_rec(morap_ctx* ctx, bool timed, bool start) {
-  if (!timed) return;
-  cudaEventRecord(start ? ctx->ev0 : ctx->ev1, ctx->stream);
-}
 
 // Runs sweeps (+finalize) until no job is active. kind 0 optimize, 1 evaluate.
 // Untimed: launches batches of sweep/finalize pairs and polls the active count once per
@@ -642,20 +644,29 @@ void launch_rec(morap_ctx* ctx, bool timed, bool start) {
 // after each sweep, so the launch count equals the sweeps that did work.
 int run_loop(morap_ctx* ctx, int kind, double eps, int cap) {
   const bool timed = ctx->profiling;
-  int batch = timed ? 1 : 4;
+  int batch = 4;
+  int launched = 0;
   for (;;) {
     for (int b = 0; b < batch; ++b) {
-      launch_rec(ctx, timed, true);
+      if (timed) {
+        while (ctx->evPool.size() < 2u * (launched + 1)) {
+          cudaEvent_t e;
+          CK(cudaEventCreate(&e));
+          ctx->evPool.push_back(e);
+        }
+        CK(cudaEventRecord(ctx->evPool[2 * launched], ctx->stream));
+      }
       if (kind == 0) {
         k_greedy_sweep<false><<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(
             ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
       } else {
-        k_eval_sweep<<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw,
-                                                                   ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dMask,
-                                                                   ctx->dDelta);
+        k_eval_sweep<<<ctx->evalBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw,
+                                                                  ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dMask,
+                                                                  ctx->dDelta);
       }
       CK(cudaGetLastError());
-      launch_rec(ctx, timed, false);
+      if (timed) CK(cudaEventRecord(ctx->evPool[2 * launched + 1], ctx->stream));
+      ++launched;
       if (kind == 0)
         k_finalize<false><<<1, kFinBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dJobModel, ctx->dList, ctx->dPrefix,
                                                            ctx->dCtl, ctx->dDelta, ctx->dMask, ctx->dNrhs, eps, cap,
@@ -666,17 +677,22 @@ int run_loop(morap_ctx* ctx, int kind, double eps, int cap) {
                                                           ctx->dSweeps, ctx->dResidual, ctx->dStatus);
       CK(cudaGetLastError());
       ctx->stats[8] += 2;
-      if (timed) {
-        CK(cudaEventSynchronize(ctx->ev1));
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
-        ctx->stats[kind == 0 ? 1 : 5] += ms;
-      }
     }
     CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->hCtl->nactive == 0) break;
-    if (!timed) batch = std::min(batch * 2, 16);
+    batch = std::min(batch * 2, 16);
+  }
+  if (timed) {
+    // only the launches that still had active jobs count (later ones were empty)
+    const int worked = std::min(launched, ctx->hCtl->sweepsDone);
+    double ms = 0.0;
+    for (int i = 0; i < worked; ++i) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, ctx->evPool[2 * i], ctx->evPool[2 * i + 1]));
+      ms += t;
+    }
+    ctx->stats[kind == 0 ? 1 : 5] += ms;
   }
   return MORAP_OK;
 }
@@ -923,8 +939,8 @@ int morap_cuda_create(int device, morap_ctx** out) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_greedy_sweep<false>, kBlock, 0);
   int occE = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occE, k_eval_sweep, kBlock, 0);
-  occ = std::max(1, std::min(occ, occE));
-  ctx->sweepBlocks = ctx->numSMs * occ;
+  ctx->sweepBlocks = ctx->numSMs * std::max(1, occ);
+  ctx->evalBlocks = ctx->numSMs * std::max(1, occE);
   if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return MORAP_CUDA_ERROR; }
   ctx->stream = ctx->own;
   cudaEventCreate(&ctx->ev0);
@@ -954,6 +970,8 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   cudaFree(ctx->dStatus);
   cudaFree(ctx->dGather);
   cudaFree(ctx->evalStage);
+  cudaFreeHost(ctx->stage);
+  for (cudaEvent_t e : ctx->evPool) cudaEventDestroy(e);
   cudaFree(ctx->dCtl);
   cudaFreeHost(ctx->hCtl);
   cudaEventDestroy(ctx->ev0);
@@ -995,8 +1013,14 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   void* dev = nullptr;
   CK(cudaMalloc(&dev, bytes));
   ctx->modelAllocs.push_back(dev);
-  char* host = nullptr;
-  CK(cudaMallocHost(&host, bytes));
+  if (bytes > ctx->stageBytes) {  // pinned staging, grow-only (reused by later uploads)
+    cudaFreeHost(ctx->stage);
+    ctx->stage = nullptr;
+    ctx->stageBytes = 0;
+    CK(cudaMallocHost(&ctx->stage, bytes));
+    ctx->stageBytes = bytes;
+  }
+  char* host = static_cast<char*>(ctx->stage);
   const int first = static_cast<int>(ctx->hm.size());
   for (int m = 0; m < nmodels; ++m) {
     const morap_csr_view& v = models[m];
@@ -1040,7 +1064,6 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   }
   cudaError_t e = cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  cudaFreeHost(host);
   if (e != cudaSuccess) return ctx->cudaFail(e, "upload copy", __LINE__);
   if ((rc = upload_models_table(ctx))) return rc;
   CK(cudaStreamSynchronize(ctx->stream));

@@ -17,7 +17,7 @@ from .errors import MorapError, check_status
 PKG = os.path.dirname(os.path.abspath(__file__))
 CUDA_SO = os.path.join(PKG, "libmorap_cuda.so")
 MAX_OBJECTIVES = 8
-MAX_RHS = 4
+MAX_RHS = 8
 
 
 class CsrView(C.Structure):
