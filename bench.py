@@ -242,12 +242,15 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     backups, reports = 0.0, []
+    phase = {"optimize_s": 0.0, "evaluate_s": 0.0, "host_s": 0.0}
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             report = solver.pareto(inst, thr, eps=eps)
             st = report["stats"]
             backups += st["optimize_backups"] + st["evaluate_state_backups"]
+            for k in phase:
+                phase[k] += st[k] / args.steps
             reports.append(report)
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -302,6 +305,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "gpu_launches": int(cs["kernels"]),
         "pareto_query_ms": ms / args.steps,
+        "phase_s_per_query": phase,
     }
     if rank == 0:
         print(json.dumps(line))

@@ -224,7 +224,7 @@ class Solver:
     def pareto(self, inst: Instance, thresholds, eps=0.01, norm=None, iteration_cap=500, verify=False) -> dict:
         t = np.ascontiguousarray(thresholds, np.float64)
         nm = None if norm is None else np.ascontiguousarray(norm, np.float64)
-        buf = C.create_string_buffer(1 << 24)
+        buf = self._json_buffer()
         st = np.zeros(8)
         _check(self._lib.morap_pareto(self.h, inst.h, _ptr(t), t.shape[0], None if nm is None else _ptr(nm), eps,
                                       iteration_cap, int(verify), buf, len(buf), _ptr(st)), "paretoPoint")
@@ -232,6 +232,11 @@ class Solver:
         out["stats"] = dict(zip(["optimize_jobs", "optimize_backups", "evaluate_jobs", "evaluate_state_backups",
                                  "optimize_s", "evaluate_s", "host_s"], st[:7].tolist()))
         return out
+
+    def _json_buffer(self):
+        if getattr(self, "_buf", None) is None:
+            self._buf = C.create_string_buffer(1 << 24)
+        return self._buf
 
     def verify(self, inst: Instance, thresholds, eps=0.01, norm=None, iteration_cap=500) -> bool:
         return bool(self.pareto(inst, thresholds, eps, norm, iteration_cap, verify=True)["verdict"])

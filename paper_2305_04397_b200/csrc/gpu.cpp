@@ -67,14 +67,14 @@ void GpuBackend::release() {
 }
 
 int GpuBackend::modelId(const ProductMdp* p) {
-  auto it = ids_.find(p);
+  auto it = ids_.find(p->uid);
   if (it != ids_.end()) return it->second;
   std::vector<const double*> objs = objectivesOf(*p);
   std::vector<uint8_t> done;
   morap_csr_view v = viewOf(*p, objs, done);
   int32_t id = -1;
   check(ctx_, morap_cuda_upload(ctx_, 1, &v, &id), "upload model");
-  ids_.emplace(p, id);
+  ids_.emplace(p->uid, id);
   return id;
 }
 
@@ -82,7 +82,7 @@ void GpuBackend::uploadInstance(const MorapInstance& inst) {
   std::vector<const ProductMdp*> todo;
   for (const auto& row : inst.products)
     for (const auto& p : row)
-      if (!ids_.count(p.get()) && std::find(todo.begin(), todo.end(), p.get()) == todo.end()) todo.push_back(p.get());
+      if (!ids_.count(p->uid) && std::find(todo.begin(), todo.end(), p.get()) == todo.end()) todo.push_back(p.get());
   if (todo.empty()) return;
   std::vector<std::vector<const double*>> objs(todo.size());
   std::vector<std::vector<uint8_t>> done(todo.size());
@@ -93,7 +93,7 @@ void GpuBackend::uploadInstance(const MorapInstance& inst) {
   }
   std::vector<int32_t> ids(todo.size());
   check(ctx_, morap_cuda_upload(ctx_, static_cast<int>(todo.size()), views.data(), ids.data()), "upload instance");
-  for (size_t k = 0; k < todo.size(); ++k) ids_.emplace(todo[k], ids[k]);
+  for (size_t k = 0; k < todo.size(); ++k) ids_.emplace(todo[k]->uid, ids[k]);
 }
 
 Scheduler makeDeterministic(std::vector<int> rows) { return Scheduler{std::move(rows)}; }

@@ -20,6 +20,11 @@ namespace morap {
 
 const std::string kInternalAction = "!advance";
 
+uint64_t nextProductUid() {
+  static std::atomic<uint64_t> counter{1};
+  return counter.fetch_add(1);
+}
+
 void validateMdp(const Mdp& m, double tol) {
   if (m.numStates <= 0) fail(Errc::InvalidModel, "model has no states");
   if (m.initial < 0 || m.initial >= m.numStates) fail(Errc::InvalidModel, "initial state out of range");
@@ -382,6 +387,7 @@ void addSyntheticObjectives(MorapInstance& inst, int K, uint64_t seed) {
       auto it = remap.find(key);
       if (it == remap.end()) {
         auto copy = std::make_shared<ProductMdp>(*key);
+        copy->uid = nextProductUid();
         copy->extra.clear();
         std::mt19937_64 rng(seed ^ (0x9e3779b97f4a7c15ull * (static_cast<uint64_t>(i) * inst.n + j + 1)));
         std::uniform_real_distribution<double> u(-2.0, 0.0);

@@ -128,6 +128,8 @@ void renormalizeRows(Mdp& m);
 std::pair<Mdp, RewardStructure> mdpFromJson(const Json& j);
 Json mdpToJson(const Mdp& m, const RewardStructure& reward);
 
+uint64_t nextProductUid();  // process-unique identity of a built product
+
 struct ProductMdp {
   Mdp mdp;
   std::vector<int> agentState, dfaLocation;
@@ -138,6 +140,7 @@ struct ProductMdp {
   std::vector<std::string> droppedAtoms;
   int agentId = -1, taskId = -1;
   uint64_t structuralHash = 0;
+  uint64_t uid = nextProductUid();  // device-model key (addresses can be reused after free)
 };
 extern const std::string kInternalAction;
 
@@ -220,7 +223,7 @@ class GpuBackend {
  private:
   morap_ctx* ctx_ = nullptr;
   int device_ = 0;
-  std::map<const ProductMdp*, int> ids_;
+  std::map<uint64_t, int> ids_;  // ProductMdp::uid -> device model id
 };
 
 OptimizeResult optimalScheduler(GpuBackend& gpu, const ProductMdp& p, const RewardStructure& rho, double eps = 1e-6,

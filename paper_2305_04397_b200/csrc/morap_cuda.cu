@@ -30,6 +30,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -39,8 +40,16 @@
 namespace {
 
 constexpr int kBlock = 256;     // threads per CTA = max states per tile
-constexpr int kRowCap = 1024;   // max action rows staged in shared memory per tile
+constexpr int kRowCap = 1024;   // max action rows per tile (staged in shared memory)
+constexpr int kNnzCap = 1280;   // max transitions per multi-state tile (staged)
 constexpr int kFinBlock = 1024; // finalize kernel block
+
+// Tile descriptor: first state / row / transition of the tile; `fits` = the tile's
+// streams fit one shared-memory stage of the TMA pipeline (every multi-state tile does;
+// a single state with more than kRowCap rows or kNnzCap transitions does not).
+struct TileDesc {
+  int32_t s0, r0, k0, fits;
+};
 
 struct DevModel {
   const int32_t* rowOffset;
@@ -49,6 +58,7 @@ struct DevModel {
   const double* prob;
   const uint8_t* done;
   const double* obj[MORAP_MAX_OBJECTIVES];
+  const TileDesc* tiles;     // ntiles + 1 (sentinel {S, R, nnz, 0})
   const int32_t* tileStart;  // ntiles + 1 state boundaries
   int32_t S, R, nnz, initial, ntiles, K, rewardFinite, pad;
   unsigned long long bytesPerSweep;  // algorithmic bytes of one greedy sweep
@@ -237,6 +247,340 @@ __global__ void __launch_bounds__(kBlock) k_greedy_sweep(const DevModel* __restr
 }
 
 // --------------------------------------------------------------------------------------
+// K1 (TMA pipeline): the same sweep with every tile's five CSR streams (rowOffset,
+// trnOffset, rho, succ, prob) and the done bytes brought into shared memory by 1-D bulk
+// async copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier, double-buffered:
+// while the CTA computes tile i from stage i&1, the copies of the next tile are in
+// flight. Streaming copies carry an L2 evict-first policy so the x vectors (gathered
+// through L2) stay resident. Phases per tile:
+//   1a  t_k = prob[k] * x[succ[k]]          thread per transition (independent gathers)
+//   1b  v_r = rho[r] + t_k + t_k' + ...      thread per row, left to right (in place)
+//   2   first strict max over the state's rows, y, |y - x| -> block max -> atomicMax
+// 1a/1b is the same rounded arithmetic as row_value (product rounded, then the sum),
+// so results stay bitwise identical. Tiles that do not fit a stage take the global path.
+
+constexpr int kStRowInts = 264;    // >= kBlock + 1 + 3 (front misalignment), multiple of 4
+constexpr int kStTrnInts = 1032;   // >= kRowCap + 1 + 3
+constexpr int kStRhoDbls = 1026;   // >= kRowCap + 1
+constexpr int kStSuccInts = 1284;  // >= kNnzCap + 3
+constexpr int kStProbDbls = 1282;  // >= kNnzCap + 1
+constexpr int kStDoneBytes = 272;  // >= kBlock + 15
+constexpr int kStXDbls = 258;      // >= kBlock + 1 (own states' x for the residual)
+constexpr int kOffRow = 0;
+constexpr int kOffTrn = kOffRow + 4 * kStRowInts;
+constexpr int kOffRho = kOffTrn + 4 * kStTrnInts;
+constexpr int kOffSucc = kOffRho + 8 * kStRhoDbls;
+constexpr int kOffProb = kOffSucc + 4 * kStSuccInts;
+constexpr int kOffDone = kOffProb + 8 * kStProbDbls;
+constexpr int kOffX = kOffDone + kStDoneBytes;
+constexpr int kStageBytes = kOffX + 8 * kStXDbls;
+static_assert(kStageBytes % 16 == 0 && kOffTrn % 16 == 0 && kOffRho % 16 == 0 && kOffSucc % 16 == 0 &&
+                  kOffProb % 16 == 0 && kOffDone % 16 == 0 && kOffX % 16 == 0,
+              "stage regions must be 16-byte aligned");
+constexpr int kTmaSmemBytes = 2 * kStageBytes;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+
+// Copy elements [b, e) of `base` (element size es) with 16-byte aligned source and size;
+// returns the element offset of `b` inside the staged copy.
+__device__ __forceinline__ int stage_range(unsigned char* dst, const void* base, long long b, long long e, int es,
+                                           uint64_t* bar, uint64_t pol, uint32_t& tx) {
+  const long long lo = (b * es) & ~15ll;
+  const long long hi = (e * es + 15) & ~15ll;
+  if (hi > lo) {
+    bulk_g2s(dst, static_cast<const unsigned char*>(base) + lo, static_cast<uint32_t>(hi - lo), bar, pol);
+    tx += static_cast<uint32_t>(hi - lo);
+  }
+  return static_cast<int>((b * es - lo) / es);
+}
+
+// What the producer warp resolved for one staged tile (consumers never walk the
+// prefix / job / model / tile tables themselves).
+struct StageInfo {
+  int t;  // global tile index, -1 = end of this CTA's range
+  int job, fits;
+  int s0, r0, k0, ns, nr, nz;
+  int offRow, offTrn, offRho, offSucc, offProb, offDone, offX;
+  const double* x;
+  double* y;
+  int32_t* policy;
+  const TileDesc* tiles;  // fallback path only
+  const DevModel* model;
+  const double* rho;
+};
+
+constexpr int kConsumers = kBlock;           // 8 compute warps
+constexpr int kTmaThreads = kBlock + 32;     // + 1 producer warp
+
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// block max over the 256 consumer threads (named barrier 1)
+__device__ __forceinline__ double consumer_max(double v, double* red) {
+  v = warp_max(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = v;
+  consumer_sync();
+  double r = 0.0;
+  if (threadIdx.x < 32) r = warp_max(lane < kConsumers / 32 ? red[lane] : 0.0);
+  consumer_sync();
+  return r;
+}
+
+// row value from the staged products: rho + t_k + t_k' ... (left to right)
+__device__ __forceinline__ double staged_row(const double* rhoS, const int32_t* trnS, const double* prodS, int i,
+                                             int k0) {
+  double acc = rhoS[i];
+  const int kb = trnS[i] - k0, ke = trnS[i + 1] - k0;
+  const int n = ke - kb;
+  if (n == 1) return __dadd_rn(acc, prodS[kb]);
+  if (n == 2) return __dadd_rn(__dadd_rn(acc, prodS[kb]), prodS[kb + 1]);
+  for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, prodS[q]);
+  return acc;
+}
+
+template <bool POLICY>
+__global__ void __launch_bounds__(kTmaThreads, 3) k_greedy_sweep_tma(const DevModel* __restrict__ models,
+                                                                     const OptJob* __restrict__ jobs,
+                                                                     const int32_t* __restrict__ list,
+                                                                     const int32_t* __restrict__ prefix,
+                                                                     const Ctl* __restrict__ ctl,
+                                                                     const int32_t* __restrict__ jobSweeps,
+                                                                     unsigned long long* __restrict__ deltaBits) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[2], empty[2];
+  __shared__ StageInfo info[2];
+  __shared__ int32_t sRow[kBlock + 1];
+  __shared__ double sVal[kRowCap];
+  __shared__ double sRed[kConsumers / 32];
+
+  const int nact = ctl->nactive;
+  const int total = ctl->totalTiles;
+  if (total <= 0) return;
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per;
+  const int t1 = min(total, t0 + per);
+  if (t0 >= t1) return;
+  const int k = ctl->sweepsDone;
+  const int tid = threadIdx.x;
+
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], 1);
+    mbar_init(&empty[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (tid >= kConsumers) {
+    // ---------------- producer warp: resolve tiles, stage them with bulk copies ----------
+    if (tid != kConsumers) return;
+    const uint64_t pol = evict_first_policy(), polKeep = evict_last_policy();
+    int ai = find_slot(prefix, nact + 1, t0);
+    int use = 0;
+    auto acquire = [&](int b) {
+      if (use >= 2) mbar_wait(&empty[b], ((use >> 1) - 1) & 1);
+    };
+    for (int ti = t0; ti < t1; ++ti, ++use) {
+      while (ti >= prefix[ai + 1]) ++ai;
+      const int job = list[ai];
+      const OptJob& J = jobs[job];
+      const DevModel* M = &models[J.model];
+      const int lt = ti - prefix[ai];
+      const TileDesc d = M->tiles[lt], e = M->tiles[lt + 1];
+      const int parity = POLICY ? ((jobSweeps[job] - 1) & 1) : (k & 1);
+      const int b = use & 1;
+      acquire(b);
+      StageInfo v;
+      v.t = ti;
+      v.job = job;
+      v.fits = d.fits;
+      v.s0 = d.s0;
+      v.r0 = d.r0;
+      v.k0 = d.k0;
+      v.ns = e.s0 - d.s0;
+      v.nr = e.r0 - d.r0;
+      v.nz = e.k0 - d.k0;
+      v.x = J.buf[parity];
+      v.y = J.buf[parity ^ 1];
+      v.policy = J.policy;
+      v.tiles = M->tiles;
+      v.model = M;
+      v.rho = J.rho;
+      uint64_t* bar = &full[b];
+      if (!d.fits) {
+        info[b] = v;
+        mbar_arrive(bar);  // no copies: consumers take the global path
+        continue;
+      }
+      auto span = [](long long lo, long long hi, int es) {
+        const long long a0 = (lo * es) & ~15ll, z = (hi * es + 15) & ~15ll;
+        return static_cast<uint32_t>(z - a0);
+      };
+      const uint32_t txBytes = span(d.s0, e.s0 + 1, 4) + span(d.r0, e.r0 + 1, 4) + span(d.r0, e.r0, 8) +
+                               span(d.k0, e.k0, 4) + span(d.k0, e.k0, 8) + span(d.s0, e.s0, 1) +
+                               (POLICY ? 0u : span(d.s0, e.s0, 8));
+      unsigned char* st = smem + b * kStageBytes;
+      uint32_t tx = 0;
+      v.offRow = stage_range(st + kOffRow, M->rowOffset, d.s0, e.s0 + 1, 4, bar, pol, tx);
+      v.offTrn = stage_range(st + kOffTrn, M->trnOffset, d.r0, e.r0 + 1, 4, bar, pol, tx);
+      v.offRho = stage_range(st + kOffRho, J.rho, d.r0, e.r0, 8, bar, pol, tx);
+      v.offSucc = stage_range(st + kOffSucc, M->succ, d.k0, e.k0, 4, bar, pol, tx);
+      v.offProb = stage_range(st + kOffProb, M->prob, d.k0, e.k0, 8, bar, pol, tx);
+      v.offDone = stage_range(st + kOffDone, M->done, d.s0, e.s0, 1, bar, pol, tx);
+      v.offX = POLICY ? 0 : stage_range(st + kOffX, v.x, d.s0, e.s0, 8, bar, polKeep, tx);
+      info[b] = v;
+      mbar_expect_tx(bar, txBytes);  // arrive (release: info[b] is visible to the waiters)
+    }
+    const int b = use & 1;
+    acquire(b);
+    info[b].t = -1;
+    mbar_arrive(&full[b]);
+    return;
+  }
+
+  // ---------------- consumer warps ---------------------------------------------------------
+  for (int use = 0;; ++use) {
+    const int b = use & 1;
+    mbar_wait(&full[b], (use >> 1) & 1);
+    const StageInfo v = info[b];
+    if (v.t < 0) break;
+    double dl = 0.0;
+    if (v.fits) {
+      unsigned char* st = smem + b * kStageBytes;
+      const int32_t* rowS = reinterpret_cast<const int32_t*>(st + kOffRow) + v.offRow;
+      const int32_t* trnS = reinterpret_cast<const int32_t*>(st + kOffTrn) + v.offTrn;
+      double* rhoS = reinterpret_cast<double*>(st + kOffRho) + v.offRho;
+      const int32_t* succS = reinterpret_cast<const int32_t*>(st + kOffSucc) + v.offSucc;
+      double* prodS = reinterpret_cast<double*>(st + kOffProb) + v.offProb;
+      const uint8_t* doneS = st + kOffDone + v.offDone;
+      const double* xS = reinterpret_cast<const double*>(st + kOffX) + v.offX;
+      const double* __restrict__ x = v.x;
+      // 1a: t_k = prob[k] * x[succ[k]] for every transition (independent gathers)
+#pragma unroll 4
+      for (int i = tid; i < v.nz; i += kConsumers) prodS[i] = __dmul_rn(prodS[i], __ldg(x + succS[i]));
+      consumer_sync();
+      // 1b: row values, left to right from rho (numerics.hpp:94-95), written over rho
+      for (int i = tid; i < v.nr; i += kConsumers) rhoS[i] = staged_row(rhoS, trnS, prodS, i, v.k0);
+      consumer_sync();
+      // 2: first strict maximum over the state's rows (numerics.hpp:96-103)
+      if (tid < v.ns) {
+        const int s = v.s0 + tid;
+        const int rb = rowS[tid] - v.r0, re = rowS[tid + 1] - v.r0;
+        if (doneS[tid]) {
+          if (POLICY) v.policy[s] = v.r0 + rb;  // numerics.hpp:114-115
+        } else {
+          double best = rhoS[rb];
+          int bestRow = rb;
+          for (int q = rb + 1; q < re; ++q) {
+            const double val = rhoS[q];
+            if (val > best) {
+              best = val;
+              bestRow = q;
+            }
+          }
+          if (POLICY) {
+            v.policy[s] = v.r0 + bestRow;
+          } else {
+            v.y[s] = best;
+            dl = fabs(__dsub_rn(best, xS[tid]));
+          }
+        }
+      }
+    } else {
+      // oversized single-state tile: rows straight from global memory
+      const DevModel& M = *v.model;
+      const double* __restrict__ x = v.x;
+      for (int i = tid; i <= v.ns; i += kConsumers) sRow[i] = M.rowOffset[v.s0 + i];
+      consumer_sync();
+      const int r0 = sRow[0];
+      const int nr = sRow[v.ns] - r0;
+      const int nstage = min(nr, kRowCap);
+      for (int i = tid; i < nstage; i += kConsumers) sVal[i] = row_value(M.trnOffset, M.succ, M.prob, v.rho, x, r0 + i);
+      consumer_sync();
+      if (tid < v.ns) {
+        const int s = v.s0 + tid;
+        const int rb = sRow[tid] - r0, re = sRow[tid + 1] - r0;
+        if (M.done[s]) {
+          if (POLICY) v.policy[s] = r0 + rb;
+        } else {
+          double best = 0.0;
+          int bestRow = -1;
+          for (int q = rb; q < re; ++q) {
+            const double val = q < kRowCap ? sVal[q] : row_value(M.trnOffset, M.succ, M.prob, v.rho, x, r0 + q);
+            if (bestRow < 0 || val > best) {
+              best = val;
+              bestRow = q;
+            }
+          }
+          if (POLICY) {
+            v.policy[s] = r0 + bestRow;
+          } else {
+            v.y[s] = best;
+            dl = fabs(__dsub_rn(best, x[s]));
+          }
+        }
+      }
+    }
+    if (!POLICY) {
+      dl = consumer_max(dl, sRed);  // both named barriers: every consumer is done with stage b
+      if (tid == 0 && dl > 0.0) atomicMax(deltaBits + v.job, (unsigned long long)__double_as_longlong(dl));
+    } else {
+      consumer_sync();
+    }
+    if (tid == 0) mbar_arrive(&empty[b]);
+  }
+}
+
+// --------------------------------------------------------------------------------------
 // K2: fused multi-RHS fixed-scheduler sweep (numerics.hpp:140-153 with a deterministic
 // scheduler): y_o(s) = 0 + 1.0 * (rho_o[r] + sum_k P_k x_o[succ_k]), r = policy[s].
 // Each RHS o is skipped once converged (its own stop test), so every RHS reproduces a
@@ -355,6 +699,7 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(const DevModel* __restri
   __shared__ int sa[32], sb[32];
   __shared__ unsigned long long sBytes[kFinBlock / 32], sBk[kFinBlock / 32];
   const int nact = ctl->nactive;
+  if (nact == 0) return;  // batch already finished: keep the sweep count exact
   const int k = ctl->sweepsDone + 1;  // sweeps completed including the one just run
   int outBase = 0, tileBase = 0;
   unsigned long long bytes = 0, backups = 0;
@@ -472,6 +817,8 @@ struct morap_ctx {
   int numSMs = 148;
   int sweepBlocks = 0;  // persistent grid of the greedy sweep kernel
   int evalBlocks = 0;   // persistent grid of the evaluate sweep kernel
+  int tmaBlocks = 0;    // persistent grid of the TMA-pipelined sweep kernel
+  bool useTma = true;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   std::string err;
@@ -573,16 +920,23 @@ int ensure_ctl(morap_ctx* ctx, size_t njobs) {
 // Tile table: consecutive states, <= kBlock states and <= kRowCap rows (a state with
 // more rows than kRowCap gets a tile of its own; its overflow rows are computed from
 // global memory in phase 2).
-void make_tiles(const int32_t* rowOffset, int S, std::vector<int32_t>& out) {
+void make_tiles(const morap_csr_view& v, std::vector<int32_t>& out, std::vector<TileDesc>& desc) {
+  const int32_t* ro = v.row_offset;
+  const int32_t* to = v.trn_offset;
   out.clear();
+  desc.clear();
   int s = 0;
   out.push_back(0);
-  while (s < S) {
+  while (s < v.num_states) {
     int e = s + 1;
-    while (e < S && e - s < kBlock && rowOffset[e + 1] - rowOffset[s] <= kRowCap) ++e;
+    while (e < v.num_states && e - s < kBlock && ro[e + 1] - ro[s] <= kRowCap && to[ro[e + 1]] - to[ro[s]] <= kNnzCap)
+      ++e;
+    const int rows = ro[e] - ro[s], nz = to[ro[e]] - to[ro[s]];
+    desc.push_back(TileDesc{s, ro[s], to[ro[s]], rows <= kRowCap && nz <= kNnzCap ? 1 : 0});
     out.push_back(e);
     s = e;
   }
+  desc.push_back(TileDesc{v.num_states, v.num_rows, v.nnz, 0});
 }
 
 int validate_view(morap_ctx* ctx, const morap_csr_view& v, int idx) {
@@ -656,7 +1010,10 @@ int run_loop(morap_ctx* ctx, int kind, double eps, int cap) {
         }
         CK(cudaEventRecord(ctx->evPool[2 * launched], ctx->stream));
       }
-      if (kind == 0) {
+      if (kind == 0 && ctx->useTma) {
+        k_greedy_sweep_tma<false><<<ctx->tmaBlocks, kTmaThreads, kTmaSmemBytes, ctx->stream>>>(
+            ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
+      } else if (kind == 0) {
         k_greedy_sweep<false><<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(
             ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
       } else {
@@ -830,8 +1187,12 @@ int extract_policies(morap_ctx* ctx, const std::vector<int32_t>& jobsIn) {
   int rc;
   if ((rc = init_ctl(ctx, jobs, ctx->optModel))) return rc;
   CK(cudaMemcpyAsync(ctx->dSweeps, ctx->optSweeps.data(), ctx->optSweeps.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-  k_greedy_sweep<true><<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, ctx->dList,
-                                                                     ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr);
+  if (ctx->useTma)
+    k_greedy_sweep_tma<true><<<ctx->tmaBlocks, kTmaThreads, kTmaSmemBytes, ctx->stream>>>(
+        ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr);
+  else
+    k_greedy_sweep<true><<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, ctx->dList,
+                                                                       ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr);
   CK(cudaGetLastError());
   ctx->stats[8] += 1;
   for (int j : jobs) ctx->optPolicyReady[j] = 1;
@@ -941,6 +1302,14 @@ int morap_cuda_create(int device, morap_ctx** out) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occE, k_eval_sweep, kBlock, 0);
   ctx->sweepBlocks = ctx->numSMs * std::max(1, occ);
   ctx->evalBlocks = ctx->numSMs * std::max(1, occE);
+  // TMA-pipelined sweep: two ~28 KB shared-memory stages per CTA
+  cudaFuncSetAttribute(k_greedy_sweep_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemBytes);
+  cudaFuncSetAttribute(k_greedy_sweep_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemBytes);
+  int occT = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occT, k_greedy_sweep_tma<false>, kTmaThreads, kTmaSmemBytes);
+  ctx->tmaBlocks = ctx->numSMs * std::max(1, occT);
+  const char* sel = std::getenv("MORAP_SWEEP_KERNEL");  // "global" selects the non-TMA sweep (A/B)
+  ctx->useTma = !(sel && std::string(sel) == "global") && occT > 0;
   if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return MORAP_CUDA_ERROR; }
   ctx->stream = ctx->own;
   cudaEventCreate(&ctx->ev0);
@@ -999,16 +1368,17 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     if ((rc = validate_view(ctx, models[m], m))) return rc;
   // pack every array of the batch into one device allocation
   std::vector<std::vector<int32_t>> tiles(nmodels);
+  std::vector<std::vector<TileDesc>> descs(nmodels);
   size_t bytes = 0;
   std::vector<size_t> off(nmodels);
   for (int m = 0; m < nmodels; ++m) {
     const morap_csr_view& v = models[m];
-    make_tiles(v.row_offset, v.num_states, tiles[m]);
+    make_tiles(v, tiles[m], descs[m]);
     off[m] = bytes;
     bytes += align_up(4ull * (v.num_states + 1), 256) + align_up(4ull * (v.num_rows + 1), 256) +
              align_up(4ull * v.nnz, 256) + align_up(8ull * v.nnz, 256) + align_up(1ull * v.num_states, 256) +
              static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256) +
-             align_up(4ull * tiles[m].size(), 256);
+             align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
   }
   void* dev = nullptr;
   CK(cudaMalloc(&dev, bytes));
@@ -1043,6 +1413,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     for (int o = 0; o < v.num_objectives; ++o)
       dmod.obj[o] = reinterpret_cast<const double*>(put(v.rewards[o], 8ull * v.num_rows));
     dmod.tileStart = reinterpret_cast<const int32_t*>(put(tiles[m].data(), 4ull * tiles[m].size()));
+    dmod.tiles = reinterpret_cast<const TileDesc*>(put(descs[m].data(), sizeof(TileDesc) * descs[m].size()));
     dmod.S = v.num_states;
     dmod.R = v.num_rows;
     dmod.nnz = v.nnz;
