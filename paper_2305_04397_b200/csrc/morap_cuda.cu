@@ -40,8 +40,8 @@
 namespace {
 
 constexpr int kBlock = 256;     // threads per CTA = max states per tile
-constexpr int kRowCap = 1024;   // max action rows per tile (staged in shared memory)
-constexpr int kNnzCap = 1280;   // max transitions per multi-state tile (staged)
+constexpr int kRowCap = 768;    // max action rows per tile (staged in shared memory)
+constexpr int kNnzCap = 1024;   // max transitions per multi-state tile (staged)
 constexpr int kFinBlock = 1024; // finalize kernel block
 
 // Tile descriptor: first state / row / transition of the tile; `fits` = the tile's
@@ -260,10 +260,10 @@ __global__ void __launch_bounds__(kBlock) k_greedy_sweep(const DevModel* __restr
 // so results stay bitwise identical. Tiles that do not fit a stage take the global path.
 
 constexpr int kStRowInts = 264;    // >= kBlock + 1 + 3 (front misalignment), multiple of 4
-constexpr int kStTrnInts = 1032;   // >= kRowCap + 1 + 3
-constexpr int kStRhoDbls = 1026;   // >= kRowCap + 1
-constexpr int kStSuccInts = 1284;  // >= kNnzCap + 3
-constexpr int kStProbDbls = 1282;  // >= kNnzCap + 1
+constexpr int kStTrnInts = kRowCap + 8;    // >= kRowCap + 1 + 3, multiple of 4
+constexpr int kStRhoDbls = kRowCap + 2;    // >= kRowCap + 1, even
+constexpr int kStSuccInts = kNnzCap + 4;   // >= kNnzCap + 3
+constexpr int kStProbDbls = kNnzCap + 2;   // >= kNnzCap + 1
 constexpr int kStDoneBytes = 272;  // >= kBlock + 15
 constexpr int kStXDbls = 258;      // >= kBlock + 1 (own states' x for the residual)
 constexpr int kOffRow = 0;
@@ -387,7 +387,7 @@ __device__ __forceinline__ double staged_row(const double* rhoS, const int32_t* 
 }
 
 template <bool POLICY>
-__global__ void __launch_bounds__(kTmaThreads, 3) k_greedy_sweep_tma(const DevModel* __restrict__ models,
+__global__ void __launch_bounds__(kTmaThreads, 4) k_greedy_sweep_tma(const DevModel* __restrict__ models,
                                                                      const OptJob* __restrict__ jobs,
                                                                      const int32_t* __restrict__ list,
                                                                      const int32_t* __restrict__ prefix,
@@ -397,8 +397,6 @@ __global__ void __launch_bounds__(kTmaThreads, 3) k_greedy_sweep_tma(const DevMo
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[2], empty[2];
   __shared__ StageInfo info[2];
-  __shared__ int32_t sRow[kBlock + 1];
-  __shared__ double sVal[kRowCap];
   __shared__ double sRed[kConsumers / 32];
 
   const int nact = ctl->nactive;
@@ -536,9 +534,12 @@ __global__ void __launch_bounds__(kTmaThreads, 3) k_greedy_sweep_tma(const DevMo
         }
       }
     } else {
-      // oversized single-state tile: rows straight from global memory
+      // oversized single-state tile: rows straight from global memory (its stage slot
+      // carries no copies, so it holds the row offsets and staged row values instead)
       const DevModel& M = *v.model;
       const double* __restrict__ x = v.x;
+      int32_t* sRow = reinterpret_cast<int32_t*>(smem + b * kStageBytes + kOffRow);
+      double* sVal = reinterpret_cast<double*>(smem + b * kStageBytes + kOffRho);
       for (int i = tid; i <= v.ns; i += kConsumers) sRow[i] = M.rowOffset[v.s0 + i];
       consumer_sync();
       const int r0 = sRow[0];
