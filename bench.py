@@ -306,6 +306,7 @@ def run_ours(args):
         "gpu_launches": int(cs["kernels"]),
         "pareto_query_ms": ms / args.steps,
         "phase_s_per_query": phase,
+        "kernel_stats": cs,
     }
     if rank == 0:
         print(json.dumps(line))

@@ -57,14 +57,12 @@ struct Handle {
   MorapInstance inst;
 };
 
+// Scheduler fingerprint (test-only): FNV-style over 32-bit rows, same as capi.cpp rowsHash.
 uint64_t fnv_rows(const Scheduler& mu) {
   uint64_t h = 1469598103934665603ull;
   for (const auto& c : mu.choice) {
-    int32_t r = c.empty() ? -1 : c[0].first;
-    for (int b = 0; b < 4; ++b) {
-      h ^= (static_cast<uint32_t>(r) >> (8 * b)) & 0xffu;
-      h *= 1099511628211ull;
-    }
+    const uint32_t r = static_cast<uint32_t>(c.empty() ? -1 : c[0].first);
+    h = (h ^ r) * 1099511628211ull;
   }
   return h;
 }

@@ -2,6 +2,7 @@
 #include <cstring>
 #include <fstream>
 #include <sstream>
+#include <thread>
 
 #include "morap.h"
 #include "morap.hpp"
@@ -32,13 +33,9 @@ int guard(F&& body) {
   }
 }
 
-uint64_t rowsHash(const morap::Scheduler& mu) {  // FNV-1a over the int32 rows (test fingerprint)
+uint64_t rowsHash(const morap::Scheduler& mu) {  // FNV-style over the int32 rows (test fingerprint)
   uint64_t h = 1469598103934665603ull;
-  for (int32_t r : mu.rows)
-    for (int b = 0; b < 4; ++b) {
-      h ^= (static_cast<uint32_t>(r) >> (8 * b)) & 0xffu;
-      h *= 1099511628211ull;
-    }
+  for (int32_t r : mu.rows) h = (h ^ static_cast<uint32_t>(r)) * 1099511628211ull;
   return h;
 }
 
@@ -62,10 +59,21 @@ morap::Json reportJson(const morap::ParetoResult& res) {
   j["converged"] = res.converged;
   j["thresholds"] = res.thresholds;
   j["lambdaStar"] = res.lambdaStar;
+  // scheduler fingerprints, one thread per iteration record
+  std::vector<std::vector<uint64_t>> hashes(res.iterations.size());
+  {
+    std::vector<std::thread> pool;
+    for (size_t k = 0; k < res.iterations.size(); ++k)
+      pool.emplace_back([&, k] {
+        for (const auto& mu : res.iterations[k].schedulers) hashes[k].push_back(rowsHash(mu));
+      });
+    for (auto& t : pool) t.join();
+  }
   morap::Json recs = morap::Json::array();
-  for (const auto& rec : res.iterations) {
+  for (size_t k = 0; k < res.iterations.size(); ++k) {
+    const auto& rec = res.iterations[k];
     morap::Json hs = morap::Json::array();
-    for (const auto& mu : rec.schedulers) hs.push_back(std::to_string(rowsHash(mu)));
+    for (uint64_t h : hashes[k]) hs.push_back(std::to_string(h));
     recs.push_back({{"tUp", rec.tUp}, {"tDown", rec.tDown}, {"schedulerHash", hs}});
   }
   j["records"] = recs;

@@ -80,6 +80,11 @@ struct EvalJob {
   const int32_t* policy;
   const double* rho[MORAP_MAX_RHS];
   double* buf[MORAP_MAX_RHS][2];
+  // policy chain (compact CSR of the chosen rows, built once per evaluate call)
+  int32_t* chainOff;   // S + 1
+  int32_t* chainSucc;  // <= nnz
+  double* chainProb;   // <= nnz
+  double* rhoC[MORAP_MAX_RHS];  // rho_o of each state's chosen row
 };
 
 // Device control block for one batch loop.
@@ -582,6 +587,318 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_greedy_sweep_tma(const DevMo
 }
 
 // --------------------------------------------------------------------------------------
+// Policy chain: a fixed deterministic scheduler turns the product into a Markov chain
+// with one row per state. Before the evaluate sweeps start, the chosen row of every state
+// is copied into a compact CSR (chainOff / chainSucc / chainProb) together with that row's
+// reward for each RHS (rhoC_o), so a sweep streams ~70 B per state instead of chasing
+// policy -> trnOffset -> succ/prob per state. Three small passes over the tiles of the
+// evaluate jobs: count, per-job scan of the tile counts, fill.
+
+__device__ __forceinline__ void block_scan2(int& a, int& b, int* sa, int* sb, int& totA, int& totB);
+
+__device__ __forceinline__ int chosen_nnz(const DevModel& M, const EvalJob& J, int s) {
+  if (M.done[s]) return 0;
+  const int r = J.policy[s];
+  return M.trnOffset[r + 1] - M.trnOffset[r];
+}
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int* scratch, int& total) {
+  // kBlock threads; scratch >= kBlock / 32 ints
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scratch[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int w = lane < kBlock / 32 ? scratch[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kBlock / 32) scratch[lane] = w;
+  }
+  __syncthreads();
+  total = scratch[kBlock / 32 - 1];
+  const int base = wid ? scratch[wid - 1] : 0;
+  __syncthreads();
+  return base + x - v;
+}
+
+__global__ void __launch_bounds__(kBlock) k_chain_count(const DevModel* __restrict__ models,
+                                                        const EvalJob* __restrict__ jobs,
+                                                        const int32_t* __restrict__ list,
+                                                        const int32_t* __restrict__ prefix, int nlist, int total,
+                                                        int32_t* __restrict__ tileCount) {
+  __shared__ int scratch[kBlock / 32];
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int a = find_slot(prefix, nlist + 1, t);
+    const EvalJob& J = jobs[list[a]];
+    const DevModel& M = models[J.model];
+    const int lt = t - prefix[a];
+    const int s0 = M.tileStart[lt], ns = M.tileStart[lt + 1] - s0;
+    const int c = threadIdx.x < ns ? chosen_nnz(M, J, s0 + threadIdx.x) : 0;
+    int tot;
+    block_exclusive_scan(c, scratch, tot);
+    if (threadIdx.x == 0) tileCount[t] = tot;
+  }
+}
+
+// one CTA per job: exclusive scan of its tile counts (in place), chainOff[S] = total
+__global__ void __launch_bounds__(1024) k_chain_scan(const DevModel* __restrict__ models,
+                                                     const EvalJob* __restrict__ jobs,
+                                                     const int32_t* __restrict__ list,
+                                                     const int32_t* __restrict__ prefix,
+                                                     int32_t* __restrict__ tileCount) {
+  __shared__ int sa[32], sb[32];
+  const int a = blockIdx.x;
+  const int b0 = prefix[a], b1 = prefix[a + 1];
+  int carry = 0;
+  for (int base = b0; base < b1; base += 1024) {
+    const int i = base + threadIdx.x;
+    int v = i < b1 ? tileCount[i] : 0, dummy = 0, tot, tot2;
+    block_scan2(v, dummy, sa, sb, tot, tot2);
+    if (i < b1) tileCount[i] = carry + v;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const EvalJob& J = jobs[list[a]];
+    J.chainOff[models[J.model].S] = carry;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_chain_fill(const DevModel* __restrict__ models,
+                                                       const EvalJob* __restrict__ jobs,
+                                                       const int32_t* __restrict__ list,
+                                                       const int32_t* __restrict__ prefix, int nlist, int total,
+                                                       const int32_t* __restrict__ tileBase) {
+  __shared__ int scratch[kBlock / 32];
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int a = find_slot(prefix, nlist + 1, t);
+    const EvalJob& J = jobs[list[a]];
+    const DevModel& M = models[J.model];
+    const int lt = t - prefix[a];
+    const int s0 = M.tileStart[lt], ns = M.tileStart[lt + 1] - s0;
+    const int s = s0 + threadIdx.x;
+    const int c = threadIdx.x < ns ? chosen_nnz(M, J, s) : 0;
+    int tot;
+    const int off = tileBase[t] + block_exclusive_scan(c, scratch, tot);
+    if (threadIdx.x < ns) {
+      J.chainOff[s] = off;
+      if (c > 0) {
+        const int r = J.policy[s];
+        const int kb = M.trnOffset[r];
+        for (int q = 0; q < c; ++q) {
+          J.chainSucc[off + q] = M.succ[kb + q];
+          J.chainProb[off + q] = M.prob[kb + q];
+        }
+        for (int o = 0; o < J.nrhs; ++o) J.rhoC[o][s] = J.rho[o][r];
+      } else {
+        for (int o = 0; o < J.nrhs; ++o) J.rhoC[o][s] = 0.0;
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// K2 (TMA pipeline): fused multi-RHS sweep over the policy chain. Same producer /
+// consumer structure as k_greedy_sweep_tma; a stage holds chainOff, the chain's
+// succ/prob, done, and rhoC_o / x_o of the tile's states for every still-active RHS.
+// y_o(s) = 0 + 1.0 * (rhoC_o[s] + sum_k P_k x_o[succ_k])   (numerics.hpp:145-151)
+
+constexpr int kEvRhs = 4;        // RHS handled by the pipelined kernel (more -> k_eval_sweep)
+constexpr int kEvChainCap = 1024;
+constexpr int kEvOffInts = kStRowInts;
+constexpr int kEvSuccInts = kEvChainCap + 4;
+constexpr int kEvProbDbls = kEvChainCap + 2;
+constexpr int kEvVecDbls = 258;  // >= kBlock + 1
+constexpr int kEvOffOff = 0;
+constexpr int kEvOffSucc = kEvOffOff + 4 * kEvOffInts;
+constexpr int kEvOffProb = kEvOffSucc + 4 * kEvSuccInts;
+constexpr int kEvOffDone = kEvOffProb + 8 * kEvProbDbls;
+constexpr int kEvOffRho = kEvOffDone + kStDoneBytes;
+constexpr int kEvOffX = kEvOffRho + 8 * kEvVecDbls * kEvRhs;
+constexpr int kEvStageBytes = kEvOffX + 8 * kEvVecDbls * kEvRhs;
+constexpr int kEvSmemBytes = 2 * kEvStageBytes;
+static_assert(kEvOffSucc % 16 == 0 && kEvOffProb % 16 == 0 && kEvOffDone % 16 == 0 && kEvOffRho % 16 == 0 &&
+                  kEvOffX % 16 == 0 && kEvStageBytes % 16 == 0,
+              "eval stage regions must be 16-byte aligned");
+
+struct EvStageInfo {
+  int t, job, fits, mask;
+  int s0, ns, c0, nc;
+  int offOff, offSucc, offProb, offDone;
+  int offRho[kEvRhs], offX[kEvRhs];
+  const EvalJob* J;
+  const DevModel* model;
+  int parity;
+};
+
+__global__ void __launch_bounds__(kTmaThreads, 3) k_eval_sweep_tma(const DevModel* __restrict__ models,
+                                                                   const EvalJob* __restrict__ jobs,
+                                                                   const int32_t* __restrict__ list,
+                                                                   const int32_t* __restrict__ prefix,
+                                                                   const Ctl* __restrict__ ctl,
+                                                                   const uint32_t* __restrict__ rhsMask,
+                                                                   unsigned long long* __restrict__ deltaBits) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[2], empty[2];
+  __shared__ EvStageInfo info[2];
+  __shared__ double sRed[kConsumers / 32];
+
+  const int nact = ctl->nactive;
+  const int total = ctl->totalTiles;
+  if (total <= 0) return;
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per;
+  const int t1 = min(total, t0 + per);
+  if (t0 >= t1) return;
+  const int parity = ctl->sweepsDone & 1;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], 1);
+    mbar_init(&empty[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (tid >= kConsumers) {
+    if (tid != kConsumers) return;
+    const uint64_t pol = evict_first_policy(), polKeep = evict_last_policy();
+    int ai = find_slot(prefix, nact + 1, t0);
+    int use = 0;
+    auto acquire = [&](int b) {
+      if (use >= 2) mbar_wait(&empty[b], ((use >> 1) - 1) & 1);
+    };
+    auto span = [](long long lo, long long hi, int es) {
+      const long long a0 = (lo * es) & ~15ll, z = (hi * es + 15) & ~15ll;
+      return static_cast<uint32_t>(z - a0);
+    };
+    for (int ti = t0; ti < t1; ++ti, ++use) {
+      while (ti >= prefix[ai + 1]) ++ai;
+      const int job = list[ai];
+      const EvalJob& J = jobs[job];
+      const DevModel* M = &models[J.model];
+      const int lt = ti - prefix[ai];
+      const int s0 = M->tileStart[lt], ns = M->tileStart[lt + 1] - s0;
+      const int c0 = J.chainOff[s0], c1 = J.chainOff[s0 + ns];
+      const int b = use & 1;
+      acquire(b);
+      EvStageInfo v;
+      v.t = ti;
+      v.job = job;
+      v.mask = static_cast<int>(rhsMask[job]);
+      v.s0 = s0;
+      v.ns = ns;
+      v.c0 = c0;
+      v.nc = c1 - c0;
+      v.J = &J;
+      v.model = M;
+      v.parity = parity;
+      v.fits = J.nrhs <= kEvRhs && c1 - c0 <= kEvChainCap;
+      uint64_t* bar = &full[b];
+      if (!v.fits) {
+        info[b] = v;
+        mbar_arrive(bar);
+        continue;
+      }
+      uint32_t txBytes = span(s0, s0 + ns + 1, 4) + span(c0, c1, 4) + span(c0, c1, 8) + span(s0, s0 + ns, 1);
+      for (int o = 0; o < J.nrhs; ++o)
+        if (v.mask >> o & 1) txBytes += 2 * span(s0, s0 + ns, 8);
+      unsigned char* st = smem + b * kEvStageBytes;
+      uint32_t tx = 0;
+      v.offOff = stage_range(st + kEvOffOff, J.chainOff, s0, s0 + ns + 1, 4, bar, pol, tx);
+      v.offSucc = stage_range(st + kEvOffSucc, J.chainSucc, c0, c1, 4, bar, pol, tx);
+      v.offProb = stage_range(st + kEvOffProb, J.chainProb, c0, c1, 8, bar, pol, tx);
+      v.offDone = stage_range(st + kEvOffDone, M->done, s0, s0 + ns, 1, bar, pol, tx);
+      for (int o = 0; o < kEvRhs; ++o) {
+        v.offRho[o] = v.offX[o] = 0;
+        if (o < J.nrhs && (v.mask >> o & 1)) {
+          v.offRho[o] = stage_range(st + kEvOffRho + o * 8 * kEvVecDbls, J.rhoC[o], s0, s0 + ns, 8, bar, pol, tx);
+          v.offX[o] = stage_range(st + kEvOffX + o * 8 * kEvVecDbls, J.buf[o][parity], s0, s0 + ns, 8, bar, polKeep, tx);
+        }
+      }
+      info[b] = v;
+      mbar_expect_tx(bar, txBytes);
+    }
+    const int b = use & 1;
+    acquire(b);
+    info[b].t = -1;
+    mbar_arrive(&full[b]);
+    return;
+  }
+
+  for (int use = 0;; ++use) {
+    const int b = use & 1;
+    mbar_wait(&full[b], (use >> 1) & 1);
+    const EvStageInfo v = info[b];
+    if (v.t < 0) break;
+    const EvalJob& J = *v.J;
+    const int nrhs = J.nrhs;
+    double d[kEvRhs];
+#pragma unroll
+    for (int o = 0; o < kEvRhs; ++o) d[o] = 0.0;
+    if (v.fits) {
+      unsigned char* st = smem + b * kEvStageBytes;
+      const int32_t* offS = reinterpret_cast<const int32_t*>(st + kEvOffOff) + v.offOff;
+      const int32_t* succS = reinterpret_cast<const int32_t*>(st + kEvOffSucc) + v.offSucc;
+      const double* probS = reinterpret_cast<const double*>(st + kEvOffProb) + v.offProb;
+      const uint8_t* doneS = st + kEvOffDone + v.offDone;
+      if (tid < v.ns && !doneS[tid]) {
+        const int s = v.s0 + tid;
+        const int cb = offS[tid] - v.c0, ce = offS[tid + 1] - v.c0;
+#pragma unroll
+        for (int o = 0; o < kEvRhs; ++o) {
+          if (o >= nrhs || !(v.mask >> o & 1)) continue;
+          const double* rhoS = reinterpret_cast<const double*>(st + kEvOffRho + o * 8 * kEvVecDbls) + v.offRho[o];
+          const double* xS = reinterpret_cast<const double*>(st + kEvOffX + o * 8 * kEvVecDbls) + v.offX[o];
+          const double* __restrict__ x = J.buf[o][v.parity];
+          double acc = rhoS[tid];
+          for (int q = cb; q < ce; ++q) acc = __dadd_rn(acc, __dmul_rn(probS[q], __ldg(x + succS[q])));
+          const double val = __dadd_rn(0.0, __dmul_rn(1.0, acc));
+          J.buf[o][v.parity ^ 1][s] = val;
+          d[o] = fabs(__dsub_rn(val, xS[tid]));
+        }
+      }
+    } else {
+      // chain too long for a stage (or more than kEvRhs RHS): straight from global memory
+      const DevModel& M = *v.model;
+      if (tid < v.ns) {
+        const int s = v.s0 + tid;
+        if (!M.done[s]) {
+          const int cb = J.chainOff[s], ce = J.chainOff[s + 1];
+          for (int o = 0; o < nrhs && o < kEvRhs; ++o) {
+            if (!(v.mask >> o & 1)) continue;
+            const double* __restrict__ x = J.buf[o][v.parity];
+            double acc = J.rhoC[o][s];
+            for (int q = cb; q < ce; ++q) acc = __dadd_rn(acc, __dmul_rn(J.chainProb[q], __ldg(x + J.chainSucc[q])));
+            const double val = __dadd_rn(0.0, __dmul_rn(1.0, acc));
+            J.buf[o][v.parity ^ 1][s] = val;
+            d[o] = fabs(__dsub_rn(val, x[s]));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < kEvRhs; ++o) {
+      if (o < nrhs && (v.mask >> o & 1)) {  // uniform over the consumers
+        const double m = consumer_max(d[o], sRed);
+        if (tid == 0 && m > 0.0) atomicMax(deltaBits + v.job * MORAP_MAX_RHS + o, (unsigned long long)__double_as_longlong(m));
+      }
+    }
+    consumer_sync();
+    if (tid == 0) mbar_arrive(&empty[b]);
+  }
+}
+
+// --------------------------------------------------------------------------------------
 // K2: fused multi-RHS fixed-scheduler sweep (numerics.hpp:140-153 with a deterministic
 // scheduler): y_o(s) = 0 + 1.0 * (rho_o[r] + sum_k P_k x_o[succ_k]), r = policy[s].
 // Each RHS o is skipped once converged (its own stop test), so every RHS reproduces a
@@ -819,7 +1136,9 @@ struct morap_ctx {
   int sweepBlocks = 0;  // persistent grid of the greedy sweep kernel
   int evalBlocks = 0;   // persistent grid of the evaluate sweep kernel
   int tmaBlocks = 0;    // persistent grid of the TMA-pipelined sweep kernel
+  int evalTmaBlocks = 0;
   bool useTma = true;
+  bool evalTma = false;  // current evaluate batch runs the pipelined chain kernel
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   std::string err;
@@ -1017,6 +1336,10 @@ int run_loop(morap_ctx* ctx, int kind, double eps, int cap) {
       } else if (kind == 0) {
         k_greedy_sweep<false><<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(
             ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
+      } else if (ctx->evalTma) {
+        k_eval_sweep_tma<<<ctx->evalTmaBlocks, kTmaThreads, kEvSmemBytes, ctx->stream>>>(
+            ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dMask,
+            ctx->dDelta);
       } else {
         k_eval_sweep<<<ctx->evalBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw,
                                                                   ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dMask,
@@ -1210,27 +1533,49 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
     ctx->dEvalJobsCap = std::max<size_t>(njobs, 64);
     CK(cudaMalloc(&ctx->dEvalJobsRaw, ctx->dEvalJobsCap * sizeof(EvalJob)));
   }
-  // arena: per job per rhs two x buffers
-  size_t need = 0;
-  for (int j = 0; j < njobs; ++j) need += 2 * proto[j].nrhs * align_up(sizeof(double) * ctx->hm[proto[j].model].S, 256);
+  // arena: [x/y buffers of every job and RHS][policy chains][tile counts]
+  size_t xBytes = 0, chainBytes = 0, totalTiles = 0;
+  bool tmaOk = ctx->useTma;
+  for (int j = 0; j < njobs; ++j) {
+    const HostModel& m = ctx->hm[proto[j].model];
+    xBytes += 2 * proto[j].nrhs * align_up(sizeof(double) * m.S, 256);
+    chainBytes += align_up(4ull * (m.S + 1), 256) + align_up(4ull * m.nnz, 256) + align_up(8ull * m.nnz, 256) +
+                  proto[j].nrhs * align_up(8ull * m.S, 256);
+    totalTiles += m.ntiles;
+    if (proto[j].nrhs > kEvRhs) tmaOk = false;
+  }
+  const size_t need = xBytes + chainBytes + align_up(4ull * (totalTiles + 1), 256);
   if ((rc = ensure_arena(ctx, &ctx->evalArena, &ctx->evalArenaBytes, need))) return rc;
   ctx->hEvalJobs = proto;
   char* p = static_cast<char*>(ctx->evalArena);
+  char* pc = p + xBytes;
+  int32_t* tileCount = reinterpret_cast<int32_t*>(pc + chainBytes);
   std::vector<int32_t> jobModel(njobs), active, nrhs(njobs);
   for (int j = 0; j < njobs; ++j) {
     EvalJob& J = ctx->hEvalJobs[j];
-    const size_t sz = align_up(sizeof(double) * ctx->hm[J.model].S, 256);
+    const HostModel& m = ctx->hm[J.model];
+    const size_t sz = align_up(sizeof(double) * m.S, 256);
     for (int o = 0; o < J.nrhs; ++o) {
       J.buf[o][0] = reinterpret_cast<double*>(p);
       p += sz;
       J.buf[o][1] = reinterpret_cast<double*>(p);
       p += sz;
     }
+    J.chainOff = reinterpret_cast<int32_t*>(pc);
+    pc += align_up(4ull * (m.S + 1), 256);
+    J.chainSucc = reinterpret_cast<int32_t*>(pc);
+    pc += align_up(4ull * m.nnz, 256);
+    J.chainProb = reinterpret_cast<double*>(pc);
+    pc += align_up(8ull * m.nnz, 256);
+    for (int o = 0; o < J.nrhs; ++o) {
+      J.rhoC[o] = reinterpret_cast<double*>(pc);
+      pc += align_up(8ull * m.S, 256);
+    }
     jobModel[j] = J.model;
     nrhs[j] = J.nrhs;
     if (maskInit[j]) active.push_back(j);
   }
-  if (need) CK(cudaMemsetAsync(ctx->evalArena, 0, need, ctx->stream));
+  if (xBytes) CK(cudaMemsetAsync(ctx->evalArena, 0, xBytes, ctx->stream));
   CK(cudaMemcpyAsync(ctx->dEvalJobsRaw, ctx->hEvalJobs.data(), njobs * sizeof(EvalJob), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->dMask, maskInit.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->dNrhs, nrhs.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
@@ -1238,6 +1583,20 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
   CK(cudaMemsetAsync(ctx->dSweeps, 0, njobs * MORAP_MAX_RHS * 4, ctx->stream));
   CK(cudaMemsetAsync(ctx->dDelta, 0, njobs * MORAP_MAX_RHS * sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->dResidual, 0, njobs * MORAP_MAX_RHS * sizeof(double), ctx->stream));
+  if ((rc = init_ctl(ctx, active, jobModel))) return rc;
+  ctx->evalTma = tmaOk;
+  if (tmaOk && !active.empty()) {
+    // policy chains of the active jobs (count, per-job scan, fill)
+    const int nl = ctx->hCtl->nactive, tt = ctx->hCtl->totalTiles;
+    const EvalJob* ej = static_cast<const EvalJob*>(ctx->dEvalJobsRaw);
+    k_chain_count<<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, ej, ctx->dList, ctx->dPrefix, nl, tt,
+                                                                tileCount);
+    k_chain_scan<<<nl, 1024, 0, ctx->stream>>>(ctx->dModels, ej, ctx->dList, ctx->dPrefix, tileCount);
+    k_chain_fill<<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, ej, ctx->dList, ctx->dPrefix, nl, tt,
+                                                               tileCount);
+    CK(cudaGetLastError());
+    ctx->stats[8] += 3;
+  }
   if ((rc = init_ctl(ctx, active, jobModel))) return rc;
   if (!active.empty())
     if ((rc = run_loop(ctx, 1, eps, cap))) return rc;
@@ -1309,6 +1668,10 @@ int morap_cuda_create(int device, morap_ctx** out) {
   int occT = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occT, k_greedy_sweep_tma<false>, kTmaThreads, kTmaSmemBytes);
   ctx->tmaBlocks = ctx->numSMs * std::max(1, occT);
+  cudaFuncSetAttribute(k_eval_sweep_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kEvSmemBytes);
+  int occV = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occV, k_eval_sweep_tma, kTmaThreads, kEvSmemBytes);
+  ctx->evalTmaBlocks = ctx->numSMs * std::max(1, occV);
   const char* sel = std::getenv("MORAP_SWEEP_KERNEL");  // "global" selects the non-TMA sweep (A/B)
   ctx->useTma = !(sel && std::string(sel) == "global") && occT > 0;
   if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return MORAP_CUDA_ERROR; }
