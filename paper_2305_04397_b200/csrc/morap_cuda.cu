@@ -27,7 +27,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <thread>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -1186,7 +1188,28 @@ struct morap_ctx {
   size_t evalStageBytes = 0;
   void* stage = nullptr;  // pinned host staging for uploads
   size_t stageBytes = 0;
-  std::vector<cudaEvent_t> evPool;  // per-sweep start/stop events (profiling)
+  std::vector<cudaEvent_t> evPool;  // per-sweep start/stop events (profiling, no graphs)
+  static constexpr int kKeyPtrs = 14;
+  struct GraphKey {
+    int kind, B, cap, variant;
+    double eps;
+    bool timed;
+    const void* ptrs[kKeyPtrs];
+    bool operator==(const GraphKey& o) const {
+      if (kind != o.kind || B != o.B || cap != o.cap || variant != o.variant || eps != o.eps || timed != o.timed)
+        return false;
+      for (int i = 0; i < kKeyPtrs; ++i)
+        if (ptrs[i] != o.ptrs[i]) return false;
+      return true;
+    }
+  };
+  struct Graph {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<cudaEvent_t> ev;
+  };
+  std::vector<Graph> graphs;  // cached sweep batches
+  bool useGraphs = true;
   Ctl* dCtl = nullptr;
   Ctl* hCtl = nullptr;  // pinned mirror
   void* dEvalJobsRaw = nullptr;
@@ -1259,6 +1282,23 @@ void make_tiles(const morap_csr_view& v, std::vector<int32_t>& out, std::vector<
   desc.push_back(TileDesc{v.num_states, v.num_rows, v.nnz, 0});
 }
 
+template <class F>
+void parallel_for(int n, F&& fn) {
+  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  const int T = std::min(n, hw);
+  if (T <= 1) {
+    for (int i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::atomic<int> next{0};
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&] {
+      for (int i; (i = next.fetch_add(1)) < n;) fn(i);
+    });
+  for (auto& th : pool) th.join();
+}
+
 int validate_view(morap_ctx* ctx, const morap_csr_view& v, int idx) {
   auto bad = [&](const std::string& why) {
     return ctx->fail(MORAP_INVALID_MODEL, "model " + std::to_string(idx) + ": " + why);
@@ -1311,70 +1351,134 @@ int ensure_arena(morap_ctx* ctx, void** arena, size_t* have, size_t need) {
 }
 
 
+// Enqueues B (sweep, finalize) pairs on the context stream; with `ev` (2B events) every
+// sweep launch is bracketed by CUDA events.
+int enqueue_sweeps(morap_ctx* ctx, int kind, double eps, int cap, int B, const cudaEvent_t* ev, bool capturing) {
+  const unsigned evFlags = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+  for (int i = 0; i < B; ++i) {
+    if (ev) CK(cudaEventRecordWithFlags(ev[2 * i], ctx->stream, evFlags));
+    if (kind == 0 && ctx->useTma) {
+      k_greedy_sweep_tma<false><<<ctx->tmaBlocks, kTmaThreads, kTmaSmemBytes, ctx->stream>>>(
+          ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
+    } else if (kind == 0) {
+      k_greedy_sweep<false><<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, ctx->dList,
+                                                                          ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
+    } else if (ctx->evalTma) {
+      k_eval_sweep_tma<<<ctx->evalTmaBlocks, kTmaThreads, kEvSmemBytes, ctx->stream>>>(
+          ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dMask, ctx->dDelta);
+    } else {
+      k_eval_sweep<<<ctx->evalBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw,
+                                                                ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dMask,
+                                                                ctx->dDelta);
+    }
+    CK(cudaGetLastError());
+    if (ev) CK(cudaEventRecordWithFlags(ev[2 * i + 1], ctx->stream, evFlags));
+    if (kind == 0)
+      k_finalize<false><<<1, kFinBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dJobModel, ctx->dList, ctx->dPrefix,
+                                                         ctx->dCtl, ctx->dDelta, ctx->dMask, ctx->dNrhs, eps, cap,
+                                                         ctx->dSweeps, ctx->dResidual, ctx->dStatus);
+    else
+      k_finalize<true><<<1, kFinBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dJobModel, ctx->dList, ctx->dPrefix,
+                                                        ctx->dCtl, ctx->dDelta, ctx->dMask, ctx->dNrhs, eps, cap,
+                                                        ctx->dSweeps, ctx->dResidual, ctx->dStatus);
+    CK(cudaGetLastError());
+  }
+  return MORAP_OK;
+}
+
+// A batch of B sweep/finalize pairs as one CUDA graph (kernel arguments are the same for
+// every batch of a call: all per-sweep state lives in device memory). Cached per
+// (kind, B, eps, cap, profiling, kernel variant, buffer addresses).
+int batch_graph(morap_ctx* ctx, int kind, double eps, int cap, int B, bool timed, morap_ctx::Graph** out) {
+  morap_ctx::GraphKey key{};
+  key.kind = kind;
+  key.B = B;
+  key.eps = eps;
+  key.cap = cap;
+  key.timed = timed;
+  key.variant = (ctx->useTma ? 1 : 0) | (ctx->evalTma ? 2 : 0);
+  const void* ptrs[] = {ctx->dModels, ctx->dOptJobs, ctx->dList,  ctx->dPrefix,    ctx->dCtl,      ctx->dDelta,
+                        ctx->dMask,   ctx->dNrhs,    ctx->dSweeps, ctx->dResidual, ctx->dStatus,   ctx->dJobModel,
+                        ctx->dEvalJobsRaw, ctx->stream};
+  static_assert(sizeof(ptrs) / sizeof(ptrs[0]) == morap_ctx::kKeyPtrs, "graph key size");
+  for (int i = 0; i < morap_ctx::kKeyPtrs; ++i) key.ptrs[i] = ptrs[i];
+  for (auto& g : ctx->graphs)
+    if (g.key == key) {
+      *out = &g;
+      return MORAP_OK;
+    }
+  if (ctx->graphs.size() >= 24) {
+    for (auto& g : ctx->graphs) {
+      cudaGraphExecDestroy(g.exec);
+      for (cudaEvent_t e : g.ev) cudaEventDestroy(e);
+    }
+    ctx->graphs.clear();
+  }
+  morap_ctx::Graph g;
+  g.key = key;
+  if (timed) {
+    g.ev.resize(2 * B);
+    for (auto& e : g.ev) CK(cudaEventCreate(&e));
+  }
+  cudaGraph_t graph = nullptr;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  const int rc = enqueue_sweeps(ctx, kind, eps, cap, B, timed ? g.ev.data() : nullptr, true);
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  if (rc) return rc;
+  if (e != cudaSuccess) return ctx->cudaFail(e, "graph capture", __LINE__);
+  e = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return ctx->cudaFail(e, "graph instantiate", __LINE__);
+  ctx->graphs.push_back(std::move(g));
+  *out = &ctx->graphs.back();
+  return MORAP_OK;
+}
+
 // Runs sweeps (+finalize) until no job is active. kind 0 optimize, 1 evaluate.
-// Untimed: launches batches of sweep/finalize pairs and polls the active count once per
-// batch (converged jobs are already frozen on the device, so overshooting a batch only
-// costs empty launches). Profiling: CUDA events around every sweep launch and a poll
-// after each sweep, so the launch count equals the sweeps that did work.
+// Batches of 4, 8, 16, 32 sweep/finalize pairs go out as one graph launch each and the
+// 4-byte active count is polled once per batch (converged jobs are already frozen on the
+// device, so overshooting a batch only costs empty launches). With profiling on, every
+// sweep launch inside the graphs is bracketed by CUDA events; only launches that still
+// had active jobs are counted.
 int run_loop(morap_ctx* ctx, int kind, double eps, int cap) {
   const bool timed = ctx->profiling;
   int batch = 4;
-  int launched = 0;
+  int before = ctx->hCtl->sweepsDone;
+  double ms = 0.0;
   for (;;) {
-    for (int b = 0; b < batch; ++b) {
+    morap_ctx::Graph* g = nullptr;
+    int rc = ctx->useGraphs ? batch_graph(ctx, kind, eps, cap, batch, timed, &g) : MORAP_OK;
+    if (rc) return rc;
+    std::vector<cudaEvent_t> direct;
+    if (g) {
+      CK(cudaGraphLaunch(g->exec, ctx->stream));
+    } else {
       if (timed) {
-        while (ctx->evPool.size() < 2u * (launched + 1)) {
+        while (ctx->evPool.size() < 2u * batch) {
           cudaEvent_t e;
           CK(cudaEventCreate(&e));
           ctx->evPool.push_back(e);
         }
-        CK(cudaEventRecord(ctx->evPool[2 * launched], ctx->stream));
       }
-      if (kind == 0 && ctx->useTma) {
-        k_greedy_sweep_tma<false><<<ctx->tmaBlocks, kTmaThreads, kTmaSmemBytes, ctx->stream>>>(
-            ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
-      } else if (kind == 0) {
-        k_greedy_sweep<false><<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(
-            ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
-      } else if (ctx->evalTma) {
-        k_eval_sweep_tma<<<ctx->evalTmaBlocks, kTmaThreads, kEvSmemBytes, ctx->stream>>>(
-            ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dMask,
-            ctx->dDelta);
-      } else {
-        k_eval_sweep<<<ctx->evalBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw,
-                                                                  ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dMask,
-                                                                  ctx->dDelta);
-      }
-      CK(cudaGetLastError());
-      if (timed) CK(cudaEventRecord(ctx->evPool[2 * launched + 1], ctx->stream));
-      ++launched;
-      if (kind == 0)
-        k_finalize<false><<<1, kFinBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dJobModel, ctx->dList, ctx->dPrefix,
-                                                           ctx->dCtl, ctx->dDelta, ctx->dMask, ctx->dNrhs, eps, cap,
-                                                           ctx->dSweeps, ctx->dResidual, ctx->dStatus);
-      else
-        k_finalize<true><<<1, kFinBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dJobModel, ctx->dList, ctx->dPrefix,
-                                                          ctx->dCtl, ctx->dDelta, ctx->dMask, ctx->dNrhs, eps, cap,
-                                                          ctx->dSweeps, ctx->dResidual, ctx->dStatus);
-      CK(cudaGetLastError());
-      ctx->stats[8] += 2;
+      if ((rc = enqueue_sweeps(ctx, kind, eps, cap, batch, timed ? ctx->evPool.data() : nullptr, false))) return rc;
     }
+    ctx->stats[8] += 2 * batch;
     CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (ctx->hCtl->nactive == 0) break;
-    batch = std::min(batch * 2, 16);
-  }
-  if (timed) {
-    // only the launches that still had active jobs count (later ones were empty)
-    const int worked = std::min(launched, ctx->hCtl->sweepsDone);
-    double ms = 0.0;
-    for (int i = 0; i < worked; ++i) {
-      float t = 0.f;
-      CK(cudaEventElapsedTime(&t, ctx->evPool[2 * i], ctx->evPool[2 * i + 1]));
-      ms += t;
+    if (timed) {
+      const int worked = ctx->hCtl->sweepsDone - before;
+      const cudaEvent_t* ev = g ? g->ev.data() : ctx->evPool.data();
+      for (int i = 0; i < worked && i < batch; ++i) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]));
+        ms += t;
+      }
     }
-    ctx->stats[kind == 0 ? 1 : 5] += ms;
+    before = ctx->hCtl->sweepsDone;
+    if (ctx->hCtl->nactive == 0) break;
+    batch = std::min(batch * 2, 32);
   }
+  if (timed) ctx->stats[kind == 0 ? 1 : 5] += ms;
   return MORAP_OK;
 }
 
@@ -1674,6 +1778,8 @@ int morap_cuda_create(int device, morap_ctx** out) {
   ctx->evalTmaBlocks = ctx->numSMs * std::max(1, occV);
   const char* sel = std::getenv("MORAP_SWEEP_KERNEL");  // "global" selects the non-TMA sweep (A/B)
   ctx->useTma = !(sel && std::string(sel) == "global") && occT > 0;
+  const char* gsel = std::getenv("MORAP_GRAPHS");  // "0" launches sweeps one by one (A/B)
+  ctx->useGraphs = !(gsel && std::string(gsel) == "0");
   if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return MORAP_CUDA_ERROR; }
   ctx->stream = ctx->own;
   cudaEventCreate(&ctx->ev0);
@@ -1705,6 +1811,10 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   cudaFree(ctx->evalStage);
   cudaFreeHost(ctx->stage);
   for (cudaEvent_t e : ctx->evPool) cudaEventDestroy(e);
+  for (auto& g : ctx->graphs) {
+    cudaGraphExecDestroy(g.exec);
+    for (cudaEvent_t e : g.ev) cudaEventDestroy(e);
+  }
   cudaFree(ctx->dCtl);
   cudaFreeHost(ctx->hCtl);
   cudaEventDestroy(ctx->ev0);
@@ -1728,16 +1838,24 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   if (nmodels == 0) return MORAP_OK;
   cudaSetDevice(ctx->device);
   int rc;
-  for (int m = 0; m < nmodels; ++m)
-    if ((rc = validate_view(ctx, models[m], m))) return rc;
-  // pack every array of the batch into one device allocation
+  // validation and tiling of every model on all host threads (first failure in model order)
   std::vector<std::vector<int32_t>> tiles(nmodels);
   std::vector<std::vector<TileDesc>> descs(nmodels);
+  std::vector<int> status(nmodels, MORAP_OK);
+  std::vector<std::string> why(nmodels);
+  parallel_for(nmodels, [&](int m) {
+    morap_ctx scratch;  // per-model error text
+    status[m] = validate_view(&scratch, models[m], m);
+    if (status[m]) why[m] = scratch.err;
+    else make_tiles(models[m], tiles[m], descs[m]);
+  });
+  for (int m = 0; m < nmodels; ++m)
+    if (status[m]) return ctx->fail(status[m], why[m]);
+  // pack every array of the batch into one device allocation
   size_t bytes = 0;
   std::vector<size_t> off(nmodels);
   for (int m = 0; m < nmodels; ++m) {
     const morap_csr_view& v = models[m];
-    make_tiles(v, tiles[m], descs[m]);
     off[m] = bytes;
     bytes += align_up(4ull * (v.num_states + 1), 256) + align_up(4ull * (v.num_rows + 1), 256) +
              align_up(4ull * v.nnz, 256) + align_up(8ull * v.nnz, 256) + align_up(1ull * v.num_states, 256) +
@@ -1756,13 +1874,14 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   }
   char* host = static_cast<char*>(ctx->stage);
   const int first = static_cast<int>(ctx->hm.size());
-  for (int m = 0; m < nmodels; ++m) {
+  std::vector<DevModel> built(nmodels);
+  parallel_for(nmodels, [&](int m) {
     const morap_csr_view& v = models[m];
     char* h = host + off[m];
     char* d = static_cast<char*>(dev) + off[m];
     DevModel dmod{};
     auto put = [&](const void* src, size_t n) {
-      std::memcpy(h, src, n);
+      if (n) std::memcpy(h, src, n);
       char* at = d;
       const size_t a = align_up(n, 256);
       h += a;
@@ -1788,13 +1907,16 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     // succ 4 + prob 8 per nnz; trnOffset 4 + rho 8 per row;
     // rowOffset 4 + done 1 + x 8 + y 8 per state.
     dmod.bytesPerSweep = 12ull * v.nnz + 12ull * v.num_rows + 21ull * v.num_states;
-    dmod.bytesPerEval = 0;  // filled below (needs mean nnz per row)
+    // evaluate, one RHS over the policy chain: chainOff 4 + done 1 + rhoC 8 + x 8 + y 8 per
+    // state + 12 per chosen transition (mean nnz per row)
     const double nnzPerRow = v.num_rows ? static_cast<double>(v.nnz) / v.num_rows : 0.0;
-    // evaluate, one RHS: policy 4 + trnOffset pair 8 + rho 8 + x 8 + y 8 + done 1 + 12 * nnz(row)
-    dmod.bytesPerEval = static_cast<unsigned long long>(v.num_states * (37.0 + 12.0 * nnzPerRow));
+    dmod.bytesPerEval = static_cast<unsigned long long>(v.num_states * (29.0 + 12.0 * nnzPerRow));
+    built[m] = dmod;
+  });
+  for (int m = 0; m < nmodels; ++m) {
+    const DevModel& dmod = built[m];
     ctx->dm.push_back(dmod);
-    ctx->hm.push_back(HostModel{v.num_states, v.num_rows, v.nnz, v.initial, dmod.ntiles, v.num_objectives,
-                                dmod.rewardFinite});
+    ctx->hm.push_back(HostModel{dmod.S, dmod.R, dmod.nnz, dmod.initial, dmod.ntiles, dmod.K, dmod.rewardFinite});
     if (ids_out) ids_out[m] = first + m;
   }
   cudaError_t e = cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream);

@@ -1,0 +1,231 @@
+"""Multi-GPU Pareto query: the n^2 agent x task products sharded across ranks.
+
+One process per GPU (torch.distributed; NCCL on GPUs, gloo in the CPU tests). The products
+are independent, so each rank owns a subset -- assigned by LPT on nnz --
+and keeps them resident on its GPU for the whole query. Per Algorithm-1 iteration
+(solver.hpp:103-184, supportingPoint):
+
+  1. every rank optimizes the (deduplicated) jobs of the pairs (i, j) it owns;
+  2. the n^2 initial-state values are exchanged with ONE all_gather (values + ownership
+     mask, so each entry keeps its exact bits);
+  3. every rank runs the same host Hungarian (maxAssignment) -> identical assignment;
+  4. the owner of each assigned pair evaluates its policy under all K objectives (fused
+     multi-RHS device batch) and the K*n results are exchanged with a second all_gather.
+
+The sandwich loop itself (runParetoCore, projections, weight vectors) runs redundantly on
+every rank through morap_pareto_core with this query as the supporting-point source, so
+all ranks see the same w sequence. There is no per-sweep communication.
+"""
+from __future__ import annotations
+
+import struct
+
+import numpy as np
+
+from .api import Instance, max_assignment, pareto_core
+from .errors import MorapError
+
+
+def lpt_partition(weights, world: int):
+    """Longest-processing-time assignment of items (by weight) to `world` bins."""
+    order = sorted(range(len(weights)), key=lambda k: (-weights[k], k))
+    load = [0.0] * world
+    owner = [0] * len(weights)
+    for k in order:
+        r = min(range(world), key=lambda b: (load[b], b))
+        owner[k] = r
+        load[r] += weights[k]
+    return owner
+
+
+class _Exchange:
+    """all_gather of float64 arrays that preserves bits, over the default process group."""
+
+    def __init__(self, world: int, device):
+        import torch
+
+        self.torch = torch
+        self.world = world
+        self.device = device
+
+    def gather(self, values: np.ndarray, mask: np.ndarray) -> np.ndarray:
+        """values/mask: flat arrays; entry k is taken from the (unique) rank whose mask is set."""
+        torch = self.torch
+        import torch.distributed as dist
+
+        packed = np.concatenate([values.astype(np.float64), mask.astype(np.float64)])
+        t = torch.from_numpy(packed).to(self.device)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t)
+        res = np.zeros_like(values, dtype=np.float64)
+        hit = np.zeros(values.shape[0], dtype=bool)
+        m = values.shape[0]
+        for o in out:
+            a = o.cpu().numpy()
+            sel = a[m:] > 0.5
+            res[sel] = a[:m][sel]
+            hit |= sel
+        if not hit.all():
+            raise MorapError(14, "sharded exchange: some entries have no owner")
+        return res
+
+
+def _bits(x: float) -> bytes:
+    return struct.pack("<d", x)
+
+
+class ShardedQuery:
+    """Supporting-point source (w -> (r, agent_of)) over products sharded across ranks."""
+
+    def __init__(self, inst: Instance, rank: int, world: int, device: int = 0, backend=None, exchange=None,
+                 eps: float = 1e-6, sweep_cap: int = 100000):
+        self.inst, self.rank, self.world = inst, rank, world
+        self.n, self.K = inst.n, inst.objectives
+        self.eps, self.cap = eps, sweep_cap
+        n = self.n
+        # distinct products (slot of first occurrence) and their owners
+        self.slot_of = {}
+        firsts, sizes = [], []
+        for i in range(n):
+            for j in range(n):
+                dims, _ = inst.product_dims(i, j)
+                first = int(dims[5])
+                self.slot_of[(i, j)] = first
+                if first == i * n + j:
+                    firsts.append(first)
+                    sizes.append(float(dims[2]))
+        owner = lpt_partition(sizes, world)
+        self.owner = {f: o for f, o in zip(firsts, owner)}
+        self.local = [f for f in firsts if self.owner[f] == rank]
+        if backend is None:
+            from .cuda import CudaBackend
+
+            backend = CudaBackend(device)
+        self.be = backend
+        prods = [inst.product(f // n, f % n) for f in self.local]
+        if self.K > 2:
+            raise MorapError(18, "sharded query supports K = 2 objectives (cost, success)")
+        ids = self.be.upload(prods) if prods else []
+        self.model_of = {f: int(m) for f, m in zip(self.local, ids)}
+        self.slot_of_model = {m: f for f, m in self.model_of.items()}
+        if exchange is None:
+            import torch
+
+            exchange = _Exchange(world, torch.device("cuda", device) if torch.cuda.is_available() else "cpu")
+        self.ex = exchange
+        self.stats = {"optimize_backups": 0.0, "evaluate_state_backups": 0.0, "local_products": len(self.local)}
+        self.nnz = {f: s for f, s in zip(firsts, sizes)}
+
+    def coord(self, k, i, j):
+        return k * self.n + i if k < self.K - 1 else (self.K - 1) * self.n + j
+
+    def __call__(self, w):
+        n, K = self.n, self.K
+        w = np.asarray(w, dtype=np.float64)
+        if w.shape[0] != K * n:
+            raise MorapError(9, "weight vector must have one entry per objective")
+        if not np.all(np.isfinite(w)) or abs(np.abs(w).sum() - 1.0) > 1e-6:
+            raise MorapError(18, "weight vector must be finite with unit 1-norm")
+        # 1. local optimize jobs, deduplicated on (product, weight bits) as solver.hpp:110-131
+        job_of, models, weights, pair_job = {}, [], [], {}
+        for i in range(n):
+            for j in range(n):
+                f = self.slot_of[(i, j)]
+                if self.owner[f] != self.rank:
+                    continue
+                wk = tuple(w[self.coord(k, i, j)] for k in range(K))
+                key = (f,) + tuple(_bits(x) for x in wk)
+                if key not in job_of:
+                    job_of[key] = len(models)
+                    models.append(self.model_of[f])
+                    weights.append(wk)
+                pair_job[(i, j)] = job_of[key]
+        vals = np.zeros(n * n)
+        mask = np.zeros(n * n)
+        if models:
+            v, sw, res, st = self.be.optimize(np.array(models, np.int32), np.array(weights), self.eps, self.cap)
+            for (i, j), q in pair_job.items():
+                if st[q] != 0:
+                    raise MorapError(int(st[q]), "weighted optimization failed")
+                vals[i * n + j] = v[q]
+                mask[i * n + j] = 1.0
+            self.stats["optimize_backups"] += float(np.sum(sw.astype(np.float64) *
+                                                           np.array([self.nnz[self.slot_of_model[m]] for m in models])))
+        # 2. exchange the n^2 values, 3. identical Hungarian everywhere
+        c = self.ex.gather(vals, mask).reshape(n, n)
+        agent_of = max_assignment(c)
+        # 4. owners evaluate their assigned pairs under all K objectives
+        mine = [(j, int(agent_of[j])) for j in range(n) if (int(agent_of[j]), j) in pair_job]
+        r = np.zeros(K * n)
+        rmask = np.zeros(K * n)
+        if mine:
+            ev, esw, eres, est = self.be.evaluate_optimized([pair_job[(i, j)] for j, i in mine], tuple(range(K)),
+                                                            self.eps, self.cap)
+            for q, (j, i) in enumerate(mine):
+                for k in range(K):
+                    if est[q, k] != 0:
+                        raise MorapError(int(est[q, k]), "evaluation failed")
+                    r[self.coord(k, i, j)] = ev[q, k]
+                    rmask[self.coord(k, i, j)] = 1.0
+        r = self.ex.gather(r, rmask)
+        return r, agent_of
+
+
+def pareto_sharded(inst: Instance, thresholds, eps: float, rank: int, world: int, device: int = 0, backend=None,
+                   exchange=None, iteration_cap: int = 500, verify: bool = False):
+    """paretoPoint (solver.hpp:281) over products sharded across ranks."""
+    q = ShardedQuery(inst, rank, world, device, backend, exchange)
+    t = np.asarray(thresholds, np.float64)
+    if inst.real_tasks != inst.n or t.shape[0] != 2 * inst.n:
+        raise MorapError(9, "sharded query expects n real tasks and 2n thresholds (expandThresholds identity)")
+    return pareto_core(t, inst.n, q, eps=eps, iteration_cap=iteration_cap, verify=verify), q
+
+
+# ------------------------------------------------------------------------------------------
+def bench_main(args, rank: int, world: int, local: int):
+    """bench.py --gpus N under torchrun: sharded C2-family query, max-over-ranks timing."""
+    import json
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    import bench as B
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg, thr, eps, K = B.workload(args.workload, world)
+    inst = Instance.warehouse(cfg)
+    q = ShardedQuery(inst, rank, world, local)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 0)):
+        pareto_core(np.array(thr), inst.n, q, eps=eps)
+    q.stats["optimize_backups"] = 0.0
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with B.ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            rep = pareto_core(np.array(thr), inst.n, q, eps=eps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    bk = torch.tensor([q.stats["optimize_backups"]], device="cuda", dtype=torch.float64)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    dist.all_reduce(bk, op=dist.ReduceOp.SUM)
+    ms = float(ms.item())
+    value = float(bk.item()) / (ms * 1e-3)
+    if rank == 0:
+        print(json.dumps({
+            "metric": B.METRIC, "value": value, "unit": B.UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded warehouse generator)",
+            "config": {"workload": args.workload, "grid": [cfg["W"], cfg["H"]], "agents": cfg["n"],
+                       "tasks": cfg["n"], "objectives": K, "parallelism": f"products sharded over {world} GPUs (LPT)",
+                       "pareto_iterations": len(rep["iterations"]), "feasible": rep["feasible"],
+                       "value_counts": "optimize nnz backups summed over ranks / max-over-ranks device time"},
+            "clocks": clk.summary(),
+        }))
+    dist.destroy_process_group()
