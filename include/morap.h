@@ -54,6 +54,9 @@ int morap_instance_product_export(const morap_instance* inst, int i, int j, int3
 /* K-objective extension (not in the reference): K-2 extra seeded objectives
  * per product. Thresholds then list (K-1)*n cost-type bounds, then the task probabilities. */
 int morap_instance_add_objectives(morap_instance* inst, int K, uint64_t seed);
+/* Objective vector k (num_rows entries) of product (i, j) in device order:
+ * 0 = cost, 1..K-2 = extra cost-type objectives, K-1 = success. */
+int morap_instance_product_objective(const morap_instance* inst, int i, int j, int k, double* out);
 
 /* Solver = one CUDA context on `device` with the instance's products resident. */
 int morap_solver_create(int device, morap_solver** out);

@@ -49,6 +49,7 @@ def load_host_library() -> C.CDLL:
         "morap_instance_product_dims": (i32, [p, i32, i32, p, C.POINTER(u64)]),
         "morap_instance_product_export": (i32, [p, i32, i32, p, p, p, p, p, p, p, p]),
         "morap_instance_add_objectives": (i32, [p, i32, u64]),
+        "morap_instance_product_objective": (i32, [p, i32, i32, i32, p]),
         "morap_solver_create": (i32, [i32, C.POINTER(p)]),
         "morap_solver_free": (None, [p]),
         "morap_solver_cuda": (p, [p]),
@@ -139,6 +140,13 @@ class Instance:
     def add_objectives(self, K: int, seed: int = 0):
         _check(self._lib.morap_instance_add_objectives(self.h, K, seed), "add_objectives")
         self.objectives = K
+
+    def objective(self, i, j, k) -> np.ndarray:
+        """Objective vector k of product (i, j): 0 cost, 1..K-2 extras, K-1 success."""
+        dims, _ = self.product_dims(i, j)
+        out = np.zeros(int(dims[1]))
+        _check(self._lib.morap_instance_product_objective(self.h, i, j, k, _ptr(out)), "product_objective")
+        return out
 
     def product_dims(self, i, j):
         dims = np.zeros(6, np.int64)

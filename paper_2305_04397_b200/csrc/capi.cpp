@@ -221,6 +221,17 @@ int morap_instance_product_export(const morap_instance* p, int i, int j, int32_t
   });
 }
 
+int morap_instance_product_objective(const morap_instance* p, int i, int j, int k, double* out) {
+  return guard([&] {
+    const auto& I = p->inst;
+    if (i < 0 || j < 0 || i >= I.n || j >= I.n || k < 0 || k >= I.objectives)
+      morap::fail(morap::Errc::InvalidConfig, "objective index out of range");
+    const morap::ProductMdp& q = *I.products[i][j];
+    const morap::RewardStructure& v = k == 0 ? q.cost : k == I.objectives - 1 ? q.success : q.extra.at(k - 1);
+    std::memcpy(out, v.data(), sizeof(double) * v.size());
+  });
+}
+
 int morap_instance_add_objectives(morap_instance* p, int K, uint64_t seed) {
   return guard([&] { morap::addSyntheticObjectives(p->inst, K, seed); });
 }

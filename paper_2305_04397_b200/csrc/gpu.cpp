@@ -22,9 +22,12 @@ void check(morap_ctx* ctx, int status, const char* what) {
   throw Error(Errc::SolverFailure, msg);
 }
 
+// Device objective order: cost, extra cost-type objectives, success -- objective k < K-1
+// is weighted by the agent's coordinate, the last one by the task's.
 std::vector<const double*> objectivesOf(const ProductMdp& p) {
-  std::vector<const double*> o{p.cost.data(), p.success.data()};
+  std::vector<const double*> o{p.cost.data()};
   for (const auto& e : p.extra) o.push_back(e.data());
+  o.push_back(p.success.data());
   return o;
 }
 
