@@ -34,7 +34,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/morap_cuda.h"
@@ -45,12 +47,18 @@ constexpr int kBlock = 256;     // threads per CTA = max states per tile
 constexpr int kRowCap = 768;    // max action rows per tile (staged in shared memory)
 constexpr int kNnzCap = 1024;   // max transitions per multi-state tile (staged)
 constexpr int kFinBlock = 1024; // finalize kernel block
+constexpr bool kFusedStates = true;  // TMA sweep: thread-per-state single pass (else 3 phases)
+// Diagnostics only (MORAP_DEBUG_DRY=1): consumers skip the arithmetic, so the pipeline's
+// pure streaming rate can be measured. Never set in tests or the benchmark.
+__device__ int g_dryRun = 0;
 
 // Tile descriptor: first state / row / transition of the tile; `fits` = the tile's
 // streams fit one shared-memory stage of the TMA pipeline (every multi-state tile does;
 // a single state with more than kRowCap rows or kNnzCap transitions does not).
 struct TileDesc {
   int32_t s0, r0, k0, fits;
+  int32_t wlo, wn;  // successor window: x[wlo, wlo + wn) is staged with the tile
+  int32_t pad0, pad1;
 };
 
 struct DevModel {
@@ -62,7 +70,15 @@ struct DevModel {
   const double* obj[MORAP_MAX_OBJECTIVES];
   const TileDesc* tiles;     // ntiles + 1 (sentinel {S, R, nnz, 0})
   const int32_t* tileStart;  // ntiles + 1 state boundaries
-  int32_t S, R, nnz, initial, ntiles, K, rewardFinite, pad;
+  // compact stream: when a model has <= 256 distinct transition
+  // probabilities and <= 256 distinct reward tuples, sweeps read a u8 probability index
+  // per transition and a u8 reward class per row instead of fp64 prob and rho_w.
+  const uint8_t* probIdx;     // nnz
+  const double* probDict;     // <= 256 distinct probabilities
+  const uint8_t* rclass;      // R
+  const double* classTable;   // nclass x K objective tuples
+  int32_t S, R, nnz, initial, ntiles, K, rewardFinite, compact;
+  int32_t nclass, pad2;
   unsigned long long bytesPerSweep;  // algorithmic bytes of one greedy sweep
   unsigned long long bytesPerEval;   // per evaluate sweep, one RHS
 };
@@ -72,6 +88,7 @@ struct OptJob {
   int32_t pad;
   double w[MORAP_MAX_OBJECTIVES];
   double* rho;
+  double* classRho;  // compact models: rho_w of each reward class (<= 256)
   double* buf[2];
   int32_t* policy;
 };
@@ -162,6 +179,14 @@ __global__ void __launch_bounds__(kBlock) k_weighted_reward(const DevModel* __re
       double acc = 0.0;
       for (int o = 0; o < M.K; ++o) acc = __dadd_rn(acc, __dmul_rn(J.w[o], M.obj[o][r]));
       J.rho[r] = acc;
+    }
+    if (M.compact && lt == 0) {
+      // the same rounded combination for every reward class: rho_w[r] == classRho[rclass[r]]
+      for (int c = threadIdx.x; c < M.nclass; c += blockDim.x) {
+        double acc = 0.0;
+        for (int o = 0; o < M.K; ++o) acc = __dadd_rn(acc, __dmul_rn(J.w[o], M.classTable[c * M.K + o]));
+        J.classRho[c] = acc;
+      }
     }
   }
 }
@@ -280,11 +305,21 @@ constexpr int kOffSucc = kOffRho + 8 * kStRhoDbls;
 constexpr int kOffProb = kOffSucc + 4 * kStSuccInts;
 constexpr int kOffDone = kOffProb + 8 * kStProbDbls;
 constexpr int kOffX = kOffDone + kStDoneBytes;
-constexpr int kStageBytes = kOffX + 8 * kStXDbls;
+constexpr int kOffIdx = kOffX + 8 * kStXDbls;  // compact models: u8 probability index per transition
+constexpr int kOffCls = kOffIdx + kNnzCap + 16;  // compact models: u8 reward class per row
+constexpr int kXWin = 1024;                        // successor window of x staged per tile
+constexpr int kOffXw = kOffCls + kRowCap + 16;
+constexpr int kStageBytes = kOffXw + 8 * (kXWin + 2);
 static_assert(kStageBytes % 16 == 0 && kOffTrn % 16 == 0 && kOffRho % 16 == 0 && kOffSucc % 16 == 0 &&
-                  kOffProb % 16 == 0 && kOffDone % 16 == 0 && kOffX % 16 == 0,
+                  kOffProb % 16 == 0 && kOffDone % 16 == 0 && kOffX % 16 == 0 && kOffIdx % 16 == 0 &&
+                  kOffXw % 16 == 0 &&
+                  kOffCls % 16 == 0,
               "stage regions must be 16-byte aligned");
-constexpr int kTmaSmemBytes = 2 * kStageBytes;
+#ifndef MORAP_STAGES
+#define MORAP_STAGES 2
+#endif
+constexpr int kStages = MORAP_STAGES;  // TMA pipeline depth of the greedy sweep
+constexpr int kTmaSmemBytes = kStages * kStageBytes;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -349,9 +384,12 @@ __device__ __forceinline__ int stage_range(unsigned char* dst, const void* base,
 // prefix / job / model / tile tables themselves).
 struct StageInfo {
   int t;  // global tile index, -1 = end of this CTA's range
-  int job, fits;
+  int job, fits, compact;
   int s0, r0, k0, ns, nr, nz;
-  int offRow, offTrn, offRho, offSucc, offProb, offDone, offX;
+  int offRow, offTrn, offRho, offSucc, offProb, offDone, offX, offIdx, offCls, offXw;
+  int wlo, wn;
+  const double* dict;      // compact: probability dictionary
+  const double* classRho;  // compact: rho_w per reward class
   const double* x;
   double* y;
   int32_t* policy;
@@ -394,7 +432,7 @@ __device__ __forceinline__ double staged_row(const double* rhoS, const int32_t* 
 }
 
 template <bool POLICY>
-__global__ void __launch_bounds__(kTmaThreads, 4) k_greedy_sweep_tma(const DevModel* __restrict__ models,
+__global__ void __launch_bounds__(kTmaThreads, kStages >= 3 ? 2 : 3) k_greedy_sweep_tma(const DevModel* __restrict__ models,
                                                                      const OptJob* __restrict__ jobs,
                                                                      const int32_t* __restrict__ list,
                                                                      const int32_t* __restrict__ prefix,
@@ -402,8 +440,8 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_greedy_sweep_tma(const DevMo
                                                                      const int32_t* __restrict__ jobSweeps,
                                                                      unsigned long long* __restrict__ deltaBits) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full[2], empty[2];
-  __shared__ StageInfo info[2];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ StageInfo info[kStages];
   __shared__ double sRed[kConsumers / 32];
 
   const int nact = ctl->nactive;
@@ -417,22 +455,24 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_greedy_sweep_tma(const DevMo
   const int tid = threadIdx.x;
 
   if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    mbar_init(&empty[0], 1);
-    mbar_init(&empty[1], 1);
+    for (int q = 0; q < kStages; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
     mbar_fence_init();
   }
   __syncthreads();
 
   if (tid >= kConsumers) {
     // ---------------- producer warp: resolve tiles, stage them with bulk copies ----------
-    if (tid != kConsumers) return;
+    // Every lane resolves the tile (broadcast loads), lane i issues stream i's bulk copy,
+    // so the eight copies of a tile go out in parallel instead of one after another.
+    const int lane = tid & 31;
     const uint64_t pol = evict_first_policy(), polKeep = evict_last_policy();
     int ai = find_slot(prefix, nact + 1, t0);
     int use = 0;
     auto acquire = [&](int b) {
-      if (use >= 2) mbar_wait(&empty[b], ((use >> 1) - 1) & 1);
+      if (use >= kStages) mbar_wait(&empty[b], ((use / kStages) - 1) & 1);
     };
     for (int ti = t0; ti < t1; ++ti, ++use) {
       while (ti >= prefix[ai + 1]) ++ai;
@@ -442,82 +482,188 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_greedy_sweep_tma(const DevMo
       const int lt = ti - prefix[ai];
       const TileDesc d = M->tiles[lt], e = M->tiles[lt + 1];
       const int parity = POLICY ? ((jobSweeps[job] - 1) & 1) : (k & 1);
-      const int b = use & 1;
-      acquire(b);
-      StageInfo v;
-      v.t = ti;
-      v.job = job;
-      v.fits = d.fits;
-      v.s0 = d.s0;
-      v.r0 = d.r0;
-      v.k0 = d.k0;
-      v.ns = e.s0 - d.s0;
-      v.nr = e.r0 - d.r0;
-      v.nz = e.k0 - d.k0;
-      v.x = J.buf[parity];
-      v.y = J.buf[parity ^ 1];
-      v.policy = J.policy;
-      v.tiles = M->tiles;
-      v.model = M;
-      v.rho = J.rho;
-      uint64_t* bar = &full[b];
-      if (!d.fits) {
-        info[b] = v;
-        mbar_arrive(bar);  // no copies: consumers take the global path
-        continue;
+      const int b = use % kStages;
+      const double* xcur = J.buf[parity];
+      const bool cp = M->compact != 0 && J.classRho != nullptr;  // explicit-rho jobs stream fp64 rho
+      // this lane's stream: 0 rowOffset, 1 trnOffset, 2 succ, 3 rho|class, 4 prob|index, 5 done,
+      // 6 own x, 7 successor window of x
+      const void* src = nullptr;
+      long long lo = 0, hi = 0;
+      int es = 1, dstOff = 0;
+      uint64_t lp = pol;
+      switch (lane) {
+        case 0: src = M->rowOffset; lo = d.s0; hi = e.s0 + 1; es = 4; dstOff = kOffRow; break;
+        case 1: src = M->trnOffset; lo = d.r0; hi = e.r0 + 1; es = 4; dstOff = kOffTrn; break;
+        case 2: src = M->succ; lo = d.k0; hi = e.k0; es = 4; dstOff = kOffSucc; break;
+        case 3:
+          if (cp) { src = M->rclass; es = 1; dstOff = kOffCls; }
+          else { src = J.rho; es = 8; dstOff = kOffRho; }
+          lo = d.r0; hi = e.r0;
+          break;
+        case 4:
+          if (cp) { src = M->probIdx; es = 1; dstOff = kOffIdx; }
+          else { src = M->prob; es = 8; dstOff = kOffProb; }
+          lo = d.k0; hi = e.k0;
+          break;
+        case 5: src = M->done; lo = d.s0; hi = e.s0; es = 1; dstOff = kOffDone; break;
+        case 6:
+          if (!POLICY) { src = xcur; lo = d.s0; hi = e.s0; es = 8; dstOff = kOffX; lp = polKeep; }
+          break;
+        case 7: src = xcur; lo = d.wlo; hi = d.wlo + d.wn; es = 8; dstOff = kOffXw; lp = polKeep; break;
+        default: break;
       }
-      auto span = [](long long lo, long long hi, int es) {
-        const long long a0 = (lo * es) & ~15ll, z = (hi * es + 15) & ~15ll;
-        return static_cast<uint32_t>(z - a0);
-      };
-      const uint32_t txBytes = span(d.s0, e.s0 + 1, 4) + span(d.r0, e.r0 + 1, 4) + span(d.r0, e.r0, 8) +
-                               span(d.k0, e.k0, 4) + span(d.k0, e.k0, 8) + span(d.s0, e.s0, 1) +
-                               (POLICY ? 0u : span(d.s0, e.s0, 8));
-      unsigned char* st = smem + b * kStageBytes;
-      uint32_t tx = 0;
-      v.offRow = stage_range(st + kOffRow, M->rowOffset, d.s0, e.s0 + 1, 4, bar, pol, tx);
-      v.offTrn = stage_range(st + kOffTrn, M->trnOffset, d.r0, e.r0 + 1, 4, bar, pol, tx);
-      v.offRho = stage_range(st + kOffRho, J.rho, d.r0, e.r0, 8, bar, pol, tx);
-      v.offSucc = stage_range(st + kOffSucc, M->succ, d.k0, e.k0, 4, bar, pol, tx);
-      v.offProb = stage_range(st + kOffProb, M->prob, d.k0, e.k0, 8, bar, pol, tx);
-      v.offDone = stage_range(st + kOffDone, M->done, d.s0, e.s0, 1, bar, pol, tx);
-      v.offX = POLICY ? 0 : stage_range(st + kOffX, v.x, d.s0, e.s0, 8, bar, polKeep, tx);
-      info[b] = v;
-      mbar_expect_tx(bar, txBytes);  // arrive (release: info[b] is visible to the waiters)
+      const long long a0 = (lo * es) & ~15ll, z0 = (hi * es + 15) & ~15ll;
+      const uint32_t bytes = (src && d.fits && z0 > a0) ? static_cast<uint32_t>(z0 - a0) : 0u;
+      const int off = src ? static_cast<int>((lo * es - a0) / es) : 0;
+      const uint32_t txBytes = __reduce_add_sync(0xffffffffu, bytes);
+      const int o0 = __shfl_sync(0xffffffffu, off, 0), o1 = __shfl_sync(0xffffffffu, off, 1),
+                o2 = __shfl_sync(0xffffffffu, off, 2), o3 = __shfl_sync(0xffffffffu, off, 3),
+                o4 = __shfl_sync(0xffffffffu, off, 4), o5 = __shfl_sync(0xffffffffu, off, 5),
+                o6 = __shfl_sync(0xffffffffu, off, 6), o7 = __shfl_sync(0xffffffffu, off, 7);
+      acquire(b);
+      uint64_t* bar = &full[b];
+      if (lane == 0) {
+        StageInfo v;
+        v.t = ti;
+        v.job = job;
+        v.fits = d.fits;
+        v.compact = cp;
+        v.s0 = d.s0;
+        v.r0 = d.r0;
+        v.k0 = d.k0;
+        v.ns = e.s0 - d.s0;
+        v.nr = e.r0 - d.r0;
+        v.nz = e.k0 - d.k0;
+        v.offRow = o0;
+        v.offTrn = o1;
+        v.offSucc = o2;
+        v.offRho = cp ? 0 : o3;
+        v.offCls = cp ? o3 : 0;
+        v.offProb = cp ? 0 : o4;
+        v.offIdx = cp ? o4 : 0;
+        v.offDone = o5;
+        v.offX = o6;
+        v.offXw = o7;
+        v.wlo = d.wlo;
+        v.wn = d.wn;
+        v.dict = M->probDict;
+        v.classRho = J.classRho;
+        v.x = xcur;
+        v.y = J.buf[parity ^ 1];
+        v.policy = J.policy;
+        v.tiles = M->tiles;
+        v.model = M;
+        v.rho = J.rho;
+        info[b] = v;
+        if (d.fits) mbar_expect_tx(bar, txBytes);  // arrive (release: info[b] visible to waiters)
+        else mbar_arrive(bar);                     // no copies: consumers take the global path
+      }
+      __syncwarp();
+      if (bytes) bulk_g2s(smem + b * kStageBytes + dstOff, static_cast<const unsigned char*>(src) + a0, bytes, bar, lp);
     }
-    const int b = use & 1;
-    acquire(b);
-    info[b].t = -1;
-    mbar_arrive(&full[b]);
+    if (lane == 0) {
+      const int b = use % kStages;
+      acquire(b);
+      info[b].t = -1;
+      mbar_arrive(&full[b]);
+    }
     return;
   }
 
   // ---------------- consumer warps ---------------------------------------------------------
   for (int use = 0;; ++use) {
-    const int b = use & 1;
-    mbar_wait(&full[b], (use >> 1) & 1);
+    const int b = use % kStages;
+    mbar_wait(&full[b], (use / kStages) & 1);
     const StageInfo v = info[b];
     if (v.t < 0) break;
     double dl = 0.0;
-    if (v.fits) {
+    if (v.fits && g_dryRun) {
+      // diagnostics: staged but not computed
+    } else if (v.fits) {
       unsigned char* st = smem + b * kStageBytes;
       const int32_t* rowS = reinterpret_cast<const int32_t*>(st + kOffRow) + v.offRow;
       const int32_t* trnS = reinterpret_cast<const int32_t*>(st + kOffTrn) + v.offTrn;
-      double* rhoS = reinterpret_cast<double*>(st + kOffRho) + v.offRho;
+      double* rhoS = reinterpret_cast<double*>(st + kOffRho) + v.offRho;  // compact: offRho = 0
       const int32_t* succS = reinterpret_cast<const int32_t*>(st + kOffSucc) + v.offSucc;
-      double* prodS = reinterpret_cast<double*>(st + kOffProb) + v.offProb;
+      double* prodS = reinterpret_cast<double*>(st + kOffProb) + v.offProb;  // compact: offProb = 0
       const uint8_t* doneS = st + kOffDone + v.offDone;
       const double* xS = reinterpret_cast<const double*>(st + kOffX) + v.offX;
       const double* __restrict__ x = v.x;
-      // 1a: t_k = prob[k] * x[succ[k]] for every transition (independent gathers)
+      if (kFusedStates) {
+        // thread per state, one pass: a state's rows -- and so its transitions -- are
+        // contiguous, so the thread first forms all its rounded products t_k =
+        // prob_k * x[succ_k] (independent gathers, written to its own slice of the stage),
+        // then accumulates each row left to right from rho and keeps the first strict max
+        // (numerics.hpp:86-103). No barrier between the phases: nothing is shared.
+        if (tid < v.ns) {
+          const int s = v.s0 + tid;
+          const int rb = rowS[tid] - v.r0, re = rowS[tid + 1] - v.r0;
+          if (doneS[tid]) {
+            if (POLICY) v.policy[s] = v.r0 + rb;  // numerics.hpp:114-115
+          } else {
+            const int qb = trnS[rb] - v.k0, qe = trnS[re] - v.k0;
+            const double* xwS = reinterpret_cast<const double*>(st + kOffXw) + v.offXw;
+            auto xAt = [&](int sIdx) {  // staged window, else global (rare long-range successor)
+              const unsigned off = static_cast<unsigned>(sIdx - v.wlo);
+              return off < static_cast<unsigned>(v.wn) ? xwS[off] : __ldg(x + sIdx);
+            };
+            if (v.compact) {
+              const uint8_t* idxS = st + kOffIdx + v.offIdx;
 #pragma unroll 4
-      for (int i = tid; i < v.nz; i += kConsumers) prodS[i] = __dmul_rn(prodS[i], __ldg(x + succS[i]));
-      consumer_sync();
-      // 1b: row values, left to right from rho (numerics.hpp:94-95), written over rho
-      for (int i = tid; i < v.nr; i += kConsumers) rhoS[i] = staged_row(rhoS, trnS, prodS, i, v.k0);
-      consumer_sync();
+              for (int q = qb; q < qe; ++q) prodS[q] = __dmul_rn(__ldg(v.dict + idxS[q]), xAt(succS[q]));
+            } else {
+#pragma unroll 4
+              for (int q = qb; q < qe; ++q) prodS[q] = __dmul_rn(prodS[q], xAt(succS[q]));
+            }
+            const uint8_t* clsS = st + kOffCls + v.offCls;
+            double best = 0.0;
+            int bestRow = -1;
+            int kb = qb;
+            for (int r = rb; r < re; ++r) {
+              const int ke = trnS[r + 1] - v.k0;
+              double acc = v.compact ? __ldg(v.classRho + clsS[r]) : rhoS[r];
+              for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, prodS[q]);
+              kb = ke;
+              if (bestRow < 0 || acc > best) {
+                best = acc;
+                bestRow = r;
+              }
+            }
+            if (POLICY) {
+              v.policy[s] = v.r0 + bestRow;
+            } else {
+              v.y[s] = best;
+              dl = fabs(__dsub_rn(best, xS[tid]));
+            }
+          }
+        }
+      } else if (v.compact) {
+        // compact stream: prob from the model's dictionary, rho_w from the job's class table
+        // (the same fp64 values, so the same rounded products and sums)
+        const uint8_t* idxS = st + kOffIdx + v.offIdx;
+        const uint8_t* clsS = st + kOffCls + v.offCls;
+#pragma unroll 4
+        for (int i = tid; i < v.nz; i += kConsumers)
+          prodS[i] = __dmul_rn(__ldg(v.dict + idxS[i]), __ldg(x + succS[i]));
+        consumer_sync();
+        for (int i = tid; i < v.nr; i += kConsumers) {
+          const int kb = trnS[i] - v.k0, ke = trnS[i + 1] - v.k0;
+          double acc = __ldg(v.classRho + clsS[i]);
+          for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, prodS[q]);
+          rhoS[i] = acc;
+        }
+        consumer_sync();
+      } else {
+        // 1a: t_k = prob[k] * x[succ[k]] for every transition (independent gathers)
+#pragma unroll 4
+        for (int i = tid; i < v.nz; i += kConsumers) prodS[i] = __dmul_rn(prodS[i], __ldg(x + succS[i]));
+        consumer_sync();
+        // 1b: row values, left to right from rho (numerics.hpp:94-95), written over rho
+        for (int i = tid; i < v.nr; i += kConsumers) rhoS[i] = staged_row(rhoS, trnS, prodS, i, v.k0);
+        consumer_sync();
+      }
       // 2: first strict maximum over the state's rows (numerics.hpp:96-103)
-      if (tid < v.ns) {
+      if (!kFusedStates && tid < v.ns) {
         const int s = v.s0 + tid;
         const int rb = rowS[tid] - v.r0, re = rowS[tid + 1] - v.r0;
         if (doneS[tid]) {
@@ -580,6 +726,298 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_greedy_sweep_tma(const DevMo
     }
     if (!POLICY) {
       dl = consumer_max(dl, sRed);  // both named barriers: every consumer is done with stage b
+      if (tid == 0 && dl > 0.0) atomicMax(deltaBits + v.job, (unsigned long long)__double_as_longlong(dl));
+    } else {
+      consumer_sync();
+    }
+    if (tid == 0) mbar_arrive(&empty[b]);
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// K1 on compact streams, deep pipeline. When every job of the batch runs on a compact
+// model (u8 probability index + u8 reward class) a stage shrinks to ~20 KB:
+// rowOffset, trnOffset, succ, index, class, done, own x and the successor window of x.
+// That buys kCmpStages = 5 stages per CTA at 2 CTAs per SM, so ~8 stages (~165 KB) are in
+// flight per SM -- what Little's law asks for at ~4 us of copy latency -- instead of 3.
+// Arithmetic per state as in k_greedy_sweep_tma's single pass: row value =
+// classRho[class] + dict[idx_k] * x[succ_k] + ..., left to right, first strict max.
+
+constexpr int kCmpStages = 5;
+#ifndef MORAP_CMP_FAST
+#define MORAP_CMP_FAST 0  // register-batched products per state (A/B: slower on C2)
+#endif
+constexpr int kCOffRow = 0;
+constexpr int kCOffTrn = kCOffRow + 4 * kStRowInts;
+constexpr int kCOffSucc = kCOffTrn + 4 * kStTrnInts;
+constexpr int kCOffIdx = kCOffSucc + 4 * kStSuccInts;
+constexpr int kCOffCls = kCOffIdx + kNnzCap + 16;
+constexpr int kCOffDone = kCOffCls + kRowCap + 16;
+constexpr int kCOffX = kCOffDone + kStDoneBytes;
+constexpr int kCOffXw = kCOffX + 8 * kStXDbls;
+constexpr int kCStageBytes = kCOffXw + 8 * (kXWin + 2);
+static_assert(kCOffTrn % 16 == 0 && kCOffSucc % 16 == 0 && kCOffIdx % 16 == 0 && kCOffCls % 16 == 0 &&
+                  kCOffDone % 16 == 0 && kCOffX % 16 == 0 && kCOffXw % 16 == 0 && kCStageBytes % 16 == 0,
+              "compact stage regions must be 16-byte aligned");
+static_assert(8 * (kXWin + 2) >= 8 * kRowCap, "fallback row values reuse the window region");
+constexpr int kCmpSmemBytes = kCmpStages * kCStageBytes;
+
+struct CmpInfo {
+  int t, job, fits;
+  int s0, r0, k0, ns;
+  int offRow, offTrn, offSucc, offIdx, offCls, offDone, offX, offXw;
+  int wlo, wn;
+  const double* dict;
+  const double* classRho;
+  const double* x;
+  double* y;
+  int32_t* policy;
+  const DevModel* model;
+  const double* rho;
+};
+
+template <bool POLICY>
+__global__ void __launch_bounds__(kTmaThreads, 2) k_greedy_sweep_cmp(const DevModel* __restrict__ models,
+                                                                     const OptJob* __restrict__ jobs,
+                                                                     const int32_t* __restrict__ list,
+                                                                     const int32_t* __restrict__ prefix,
+                                                                     const Ctl* __restrict__ ctl,
+                                                                     const int32_t* __restrict__ jobSweeps,
+                                                                     unsigned long long* __restrict__ deltaBits) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[kCmpStages], empty[kCmpStages];
+  __shared__ CmpInfo info[kCmpStages];
+  __shared__ double sRed[kConsumers / 32];
+
+  const int nact = ctl->nactive;
+  const int total = ctl->totalTiles;
+  if (total <= 0) return;
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per;
+  const int t1 = min(total, t0 + per);
+  if (t0 >= t1) return;
+  const int k = ctl->sweepsDone;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int q = 0; q < kCmpStages; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (tid >= kConsumers) {
+    // producer warp: lane i stages stream i of the tile
+    const int lane = tid & 31;
+    const uint64_t pol = evict_first_policy(), polKeep = evict_last_policy();
+    int ai = find_slot(prefix, nact + 1, t0);
+    int use = 0;
+    auto acquire = [&](int b) {
+      if (use >= kCmpStages) mbar_wait(&empty[b], ((use / kCmpStages) - 1) & 1);
+    };
+    for (int ti = t0; ti < t1; ++ti, ++use) {
+      while (ti >= prefix[ai + 1]) ++ai;
+      const int job = list[ai];
+      const OptJob& J = jobs[job];
+      const DevModel* M = &models[J.model];
+      const int lt = ti - prefix[ai];
+      const TileDesc d = M->tiles[lt], e = M->tiles[lt + 1];
+      const int parity = POLICY ? ((jobSweeps[job] - 1) & 1) : (k & 1);
+      const int b = use % kCmpStages;
+      const double* xcur = J.buf[parity];
+      const void* src = nullptr;
+      long long lo = 0, hi = 0;
+      int es = 1, dstOff = 0;
+      uint64_t lp = pol;
+      switch (lane) {
+        case 0: src = M->rowOffset; lo = d.s0; hi = e.s0 + 1; es = 4; dstOff = kCOffRow; break;
+        case 1: src = M->trnOffset; lo = d.r0; hi = e.r0 + 1; es = 4; dstOff = kCOffTrn; break;
+        case 2: src = M->succ; lo = d.k0; hi = e.k0; es = 4; dstOff = kCOffSucc; break;
+        case 3: src = M->probIdx; lo = d.k0; hi = e.k0; es = 1; dstOff = kCOffIdx; break;
+        case 4: src = M->rclass; lo = d.r0; hi = e.r0; es = 1; dstOff = kCOffCls; break;
+        case 5: src = M->done; lo = d.s0; hi = e.s0; es = 1; dstOff = kCOffDone; break;
+        case 6:
+          if (!POLICY) { src = xcur; lo = d.s0; hi = e.s0; es = 8; dstOff = kCOffX; lp = polKeep; }
+          break;
+        case 7: src = xcur; lo = d.wlo; hi = d.wlo + d.wn; es = 8; dstOff = kCOffXw; lp = polKeep; break;
+        default: break;
+      }
+      const long long a0 = (lo * es) & ~15ll, z0 = (hi * es + 15) & ~15ll;
+      const uint32_t bytes = (src && d.fits && z0 > a0) ? static_cast<uint32_t>(z0 - a0) : 0u;
+      const int off = src ? static_cast<int>((lo * es - a0) / es) : 0;
+      const uint32_t txBytes = __reduce_add_sync(0xffffffffu, bytes);
+      int offs[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) offs[q] = __shfl_sync(0xffffffffu, off, q);
+      acquire(b);
+      uint64_t* bar = &full[b];
+      if (lane == 0) {
+        CmpInfo v;
+        v.t = ti;
+        v.job = job;
+        v.fits = d.fits;
+        v.s0 = d.s0;
+        v.r0 = d.r0;
+        v.k0 = d.k0;
+        v.ns = e.s0 - d.s0;
+        v.offRow = offs[0];
+        v.offTrn = offs[1];
+        v.offSucc = offs[2];
+        v.offIdx = offs[3];
+        v.offCls = offs[4];
+        v.offDone = offs[5];
+        v.offX = offs[6];
+        v.offXw = offs[7];
+        v.wlo = d.wlo;
+        v.wn = d.wn;
+        v.dict = M->probDict;
+        v.classRho = J.classRho;
+        v.x = xcur;
+        v.y = J.buf[parity ^ 1];
+        v.policy = J.policy;
+        v.model = M;
+        v.rho = J.rho;
+        info[b] = v;
+        if (d.fits) mbar_expect_tx(bar, txBytes);
+        else mbar_arrive(bar);
+      }
+      __syncwarp();
+      if (bytes)
+        bulk_g2s(smem + b * kCStageBytes + dstOff, static_cast<const unsigned char*>(src) + a0, bytes, bar, lp);
+    }
+    if (lane == 0) {
+      const int b = use % kCmpStages;
+      acquire(b);
+      info[b].t = -1;
+      mbar_arrive(&full[b]);
+    }
+    return;
+  }
+
+  for (int use = 0;; ++use) {
+    const int b = use % kCmpStages;
+    mbar_wait(&full[b], (use / kCmpStages) & 1);
+    const CmpInfo v = info[b];
+    if (v.t < 0) break;
+    double dl = 0.0;
+    unsigned char* st = smem + b * kCStageBytes;
+    const double* __restrict__ x = v.x;
+    if (v.fits) {
+      const int32_t* rowS = reinterpret_cast<const int32_t*>(st + kCOffRow) + v.offRow;
+      const int32_t* trnS = reinterpret_cast<const int32_t*>(st + kCOffTrn) + v.offTrn;
+      const int32_t* succS = reinterpret_cast<const int32_t*>(st + kCOffSucc) + v.offSucc;
+      const uint8_t* idxS = st + kCOffIdx + v.offIdx;
+      const uint8_t* clsS = st + kCOffCls + v.offCls;
+      const uint8_t* doneS = st + kCOffDone + v.offDone;
+      const double* xS = reinterpret_cast<const double*>(st + kCOffX) + v.offX;
+      const double* xwS = reinterpret_cast<const double*>(st + kCOffXw) + v.offXw;
+      if (tid < v.ns) {
+        const int s = v.s0 + tid;
+        const int rb = rowS[tid] - v.r0, re = rowS[tid + 1] - v.r0;
+        if (doneS[tid]) {
+          if (POLICY) v.policy[s] = v.r0 + rb;  // numerics.hpp:114-115
+        } else {
+          double best = 0.0;
+          int bestRow = -1;
+          const int qb = trnS[rb] - v.k0, qe = trnS[re] - v.k0;
+          auto xAt = [&](int sIdx) {
+            const unsigned o = static_cast<unsigned>(sIdx - v.wlo);
+            return o < static_cast<unsigned>(v.wn) ? xwS[o] : __ldg(x + sIdx);
+          };
+          constexpr int kFast = 8;  // a warehouse state has <= 5 transitions over its rows
+          if (MORAP_CMP_FAST && qe - qb <= kFast) {
+            // all products of the state first (independent loads, static register slots),
+            // then the rows left to right (numerics.hpp:93-100)
+            double t[kFast];
+#pragma unroll
+            for (int q = 0; q < kFast; ++q)
+              if (q < qe - qb) t[q] = __dmul_rn(__ldg(v.dict + idxS[qb + q]), xAt(succS[qb + q]));
+            int r = rb;
+            int rowEnd = trnS[rb + 1] - v.k0 - qb;
+            double acc = __ldg(v.classRho + clsS[rb]);
+#pragma unroll
+            for (int q = 0; q < kFast; ++q) {
+              if (q < qe - qb) {
+                while (q >= rowEnd) {  // close row r (rows may be empty)
+                  if (bestRow < 0 || acc > best) {
+                    best = acc;
+                    bestRow = r;
+                  }
+                  ++r;
+                  acc = __ldg(v.classRho + clsS[r]);
+                  rowEnd = trnS[r + 1] - v.k0 - qb;
+                }
+                acc = __dadd_rn(acc, t[q]);
+              }
+            }
+            for (;;) {  // close the last non-empty row and any trailing empty rows
+              if (bestRow < 0 || acc > best) {
+                best = acc;
+                bestRow = r;
+              }
+              if (++r >= re) break;
+              acc = __ldg(v.classRho + clsS[r]);
+            }
+          } else {
+            int kb = qb;
+            for (int r = rb; r < re; ++r) {
+              const int ke = trnS[r + 1] - v.k0;
+              double acc = __ldg(v.classRho + clsS[r]);
+              for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(v.dict + idxS[q]), xAt(succS[q])));
+              kb = ke;
+              if (bestRow < 0 || acc > best) {
+                best = acc;
+                bestRow = r;
+              }
+            }
+          }
+          if (POLICY) {
+            v.policy[s] = v.r0 + bestRow;
+          } else {
+            v.y[s] = best;
+            dl = fabs(__dsub_rn(best, xS[tid]));
+          }
+        }
+      }
+    } else {
+      // oversized single-state tile from global memory (stage slot reused as scratch)
+      const DevModel& M = *v.model;
+      int32_t* sRow = reinterpret_cast<int32_t*>(st + kCOffRow);
+      double* sVal = reinterpret_cast<double*>(st + kCOffXw);
+      for (int i = tid; i <= v.ns; i += kConsumers) sRow[i] = M.rowOffset[v.s0 + i];
+      consumer_sync();
+      const int r0 = sRow[0];
+      const int nr = sRow[v.ns] - r0;
+      const int nstage = min(nr, kRowCap);
+      for (int i = tid; i < nstage; i += kConsumers) sVal[i] = row_value(M.trnOffset, M.succ, M.prob, v.rho, x, r0 + i);
+      consumer_sync();
+      if (tid < v.ns) {
+        const int s = v.s0 + tid;
+        const int rb = sRow[tid] - r0, re = sRow[tid + 1] - r0;
+        if (M.done[s]) {
+          if (POLICY) v.policy[s] = r0 + rb;
+        } else {
+          double best = 0.0;
+          int bestRow = -1;
+          for (int q = rb; q < re; ++q) {
+            const double val = q < kRowCap ? sVal[q] : row_value(M.trnOffset, M.succ, M.prob, v.rho, x, r0 + q);
+            if (bestRow < 0 || val > best) {
+              best = val;
+              bestRow = q;
+            }
+          }
+          if (POLICY) {
+            v.policy[s] = r0 + bestRow;
+          } else {
+            v.y[s] = best;
+            dl = fabs(__dsub_rn(best, x[s]));
+          }
+        }
+      }
+    }
+    if (!POLICY) {
+      dl = consumer_max(dl, sRed);
       if (tid == 0 && dl > 0.0) atomicMax(deltaBits + v.job, (unsigned long long)__double_as_longlong(dl));
     } else {
       consumer_sync();
@@ -1210,6 +1648,9 @@ struct morap_ctx {
   };
   std::vector<Graph> graphs;  // cached sweep batches
   bool useGraphs = true;
+  bool useCompact = true;  // compact u8 probability / reward-class streams where possible
+  bool optCompact = false; // current optimize batch runs the deep compact pipeline
+  int cmpBlocks = 0;
   Ctl* dCtl = nullptr;
   Ctl* hCtl = nullptr;  // pinned mirror
   void* dEvalJobsRaw = nullptr;
@@ -1263,6 +1704,44 @@ int ensure_ctl(morap_ctx* ctx, size_t njobs) {
 // Tile table: consecutive states, <= kBlock states and <= kRowCap rows (a state with
 // more rows than kRowCap gets a tile of its own; its overflow rows are computed from
 // global memory in phase 2).
+// The x window staged with a tile: the kXWin consecutive states covering the most of the
+// tile's transitions (two pointers over the sorted successors). On warehouse products
+// successors of a 256-state tile sit within ~1000 states of each other (BFS numbering),
+// so >99% of the gathers are served from shared memory; the rest read global memory.
+void successor_window(const morap_csr_view& v, int k0, int k1, int32_t& wlo, int32_t& wn) {
+  wn = std::min(kXWin, v.num_states);
+  if (k1 <= k0) {
+    wlo = 0;
+    return;
+  }
+  // histogram of successors in 64-state bins over [min, max], then the best run of
+  // (kXWin / 64 - 1) bins -- O(transitions) per tile, within one bin of the optimum
+  int lo = v.succ[k0], hi = lo;
+  for (int k = k0 + 1; k < k1; ++k) {
+    lo = std::min(lo, v.succ[k]);
+    hi = std::max(hi, v.succ[k]);
+  }
+  if (hi - lo < wn) {
+    wlo = std::max(0, std::min(lo, v.num_states - wn));
+    return;
+  }
+  constexpr int kBin = 64;
+  const int nb = (hi - lo) / kBin + 1;
+  std::vector<int> h(static_cast<size_t>(nb), 0);
+  for (int k = k0; k < k1; ++k) ++h[(v.succ[k] - lo) / kBin];
+  const int span = std::max(1, wn / kBin - 1);
+  int run = 0, best = -1, bestBin = 0;
+  for (int i = 0; i < nb; ++i) {
+    run += h[i];
+    if (i >= span) run -= h[i - span];
+    if (run > best) {
+      best = run;
+      bestBin = std::max(0, i - span + 1);
+    }
+  }
+  wlo = std::max(0, std::min(lo + bestBin * kBin, v.num_states - wn));
+}
+
 void make_tiles(const morap_csr_view& v, std::vector<int32_t>& out, std::vector<TileDesc>& desc) {
   const int32_t* ro = v.row_offset;
   const int32_t* to = v.trn_offset;
@@ -1275,11 +1754,88 @@ void make_tiles(const morap_csr_view& v, std::vector<int32_t>& out, std::vector<
     while (e < v.num_states && e - s < kBlock && ro[e + 1] - ro[s] <= kRowCap && to[ro[e + 1]] - to[ro[s]] <= kNnzCap)
       ++e;
     const int rows = ro[e] - ro[s], nz = to[ro[e]] - to[ro[s]];
-    desc.push_back(TileDesc{s, ro[s], to[ro[s]], rows <= kRowCap && nz <= kNnzCap ? 1 : 0});
+    TileDesc td{s, ro[s], to[ro[s]], rows <= kRowCap && nz <= kNnzCap ? 1 : 0, 0, 0, 0, 0};
+    successor_window(v, to[ro[s]], to[ro[e]], td.wlo, td.wn);
+    desc.push_back(td);
     out.push_back(e);
     s = e;
   }
-  desc.push_back(TileDesc{v.num_states, v.num_rows, v.nnz, 0});
+  desc.push_back(TileDesc{v.num_states, v.num_rows, v.nnz, 0, 0, 0, 0, 0});
+}
+
+// Compact stream of one model: u8 index into a dictionary of the distinct transition
+// probabilities and u8 class of each row's objective tuple. Keys are the exact fp64 bit
+// patterns, so the device reads back the very same values. ok = false when either
+// alphabet exceeds 256 entries (the model then streams the plain fp64 arrays).
+struct CompactStream {
+  bool ok = false;
+  std::vector<uint8_t> idx, cls;
+  std::vector<double> dict, table;
+};
+
+// Tiny open-addressing table (<= 256 keys of up to 8 words) for build_compact.
+struct SmallIds {
+  static constexpr int kSlots = 1024;
+  int words = 1, count = 0;
+  std::vector<uint64_t> keys;
+  std::vector<int16_t> ids;
+  explicit SmallIds(int w) : words(w), keys(static_cast<size_t>(kSlots) * w), ids(kSlots, -1) {}
+  // id of `k` (inserted if new); -1 when a 257th key would be needed
+  int find(const uint64_t* k) {
+    uint64_t h = 1469598103934665603ull;
+    for (int i = 0; i < words; ++i) h = (h ^ k[i]) * 1099511628211ull;
+    for (int slot = static_cast<int>(h >> 54) & (kSlots - 1);; slot = (slot + 1) & (kSlots - 1)) {
+      if (ids[slot] < 0) {
+        if (count == 256) return -1;
+        std::memcpy(&keys[static_cast<size_t>(slot) * words], k, 8ull * words);
+        ids[slot] = static_cast<int16_t>(count);
+        return count++;
+      }
+      if (std::memcmp(&keys[static_cast<size_t>(slot) * words], k, 8ull * words) == 0) return ids[slot];
+    }
+  }
+};
+
+void build_compact(const morap_csr_view& v, CompactStream& c) {
+  c = CompactStream{};
+  const int K = v.num_objectives;
+  if (K < 1) return;
+  c.idx.resize(static_cast<size_t>(v.nnz));
+  SmallIds probs(1);
+  uint64_t last = ~0ull;
+  int lastId = -1;
+  for (int k = 0; k < v.nnz; ++k) {
+    uint64_t b;
+    std::memcpy(&b, &v.prob[k], 8);
+    if (b != last) {
+      lastId = probs.find(&b);
+      if (lastId < 0) return;
+      if (lastId == static_cast<int>(c.dict.size())) c.dict.push_back(v.prob[k]);
+      last = b;
+    }
+    c.idx[k] = static_cast<uint8_t>(lastId);
+  }
+  c.cls.resize(static_cast<size_t>(v.num_rows));
+  SmallIds classes(K);
+  uint64_t key[MORAP_MAX_OBJECTIVES];
+  uint64_t prev[MORAP_MAX_OBJECTIVES];
+  int prevId = -1;
+  for (int r = 0; r < v.num_rows; ++r) {
+    for (int o = 0; o < K; ++o) std::memcpy(&key[o], &v.rewards[o][r], 8);
+    if (prevId >= 0 && std::memcmp(key, prev, 8ull * K) == 0) {  // runs of equal rows
+      c.cls[r] = static_cast<uint8_t>(prevId);
+      continue;
+    }
+    const int id = classes.find(key);
+    if (id < 0) return;
+    std::memcpy(prev, key, 8ull * K);
+    prevId = id;
+    if (id == static_cast<int>(c.table.size()) / K)
+      for (int o = 0; o < K; ++o) c.table.push_back(v.rewards[o][r]);
+    c.cls[r] = static_cast<uint8_t>(id);
+  }
+  if (c.table.empty()) c.table.assign(static_cast<size_t>(K), 0.0);
+  c.ok = true;
 }
 
 template <class F>
@@ -1357,7 +1913,10 @@ int enqueue_sweeps(morap_ctx* ctx, int kind, double eps, int cap, int B, const c
   const unsigned evFlags = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
   for (int i = 0; i < B; ++i) {
     if (ev) CK(cudaEventRecordWithFlags(ev[2 * i], ctx->stream, evFlags));
-    if (kind == 0 && ctx->useTma) {
+    if (kind == 0 && ctx->useTma && ctx->optCompact) {
+      k_greedy_sweep_cmp<false><<<ctx->cmpBlocks, kTmaThreads, kCmpSmemBytes, ctx->stream>>>(
+          ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
+    } else if (kind == 0 && ctx->useTma) {
       k_greedy_sweep_tma<false><<<ctx->tmaBlocks, kTmaThreads, kTmaSmemBytes, ctx->stream>>>(
           ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
     } else if (kind == 0) {
@@ -1396,7 +1955,7 @@ int batch_graph(morap_ctx* ctx, int kind, double eps, int cap, int B, bool timed
   key.eps = eps;
   key.cap = cap;
   key.timed = timed;
-  key.variant = (ctx->useTma ? 1 : 0) | (ctx->evalTma ? 2 : 0);
+  key.variant = (ctx->useTma ? 1 : 0) | (ctx->evalTma ? 2 : 0) | (ctx->optCompact ? 4 : 0);
   const void* ptrs[] = {ctx->dModels, ctx->dOptJobs, ctx->dList,  ctx->dPrefix,    ctx->dCtl,      ctx->dDelta,
                         ctx->dMask,   ctx->dNrhs,    ctx->dSweeps, ctx->dResidual, ctx->dStatus,   ctx->dJobModel,
                         ctx->dEvalJobsRaw, ctx->stream};
@@ -1527,7 +2086,8 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     offPol[j] = polBytes;
     polBytes += align_up(sizeof(int32_t) * m.S, 256);
   }
-  const size_t need = rhoBytes + xBytes + polBytes;
+  const size_t classBytes = static_cast<size_t>(njobs) * 256 * sizeof(double);  // rho_w per reward class
+  const size_t need = rhoBytes + xBytes + polBytes + classBytes;
   int rc;
   if ((rc = ensure_arena(ctx, &ctx->optArena, &ctx->optArenaBytes, need))) return rc;
   if ((rc = ensure_ctl(ctx, njobs))) return rc;
@@ -1548,12 +2108,18 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     J.buf[0] = reinterpret_cast<double*>(base + rhoBytes + offX[j]);
     J.buf[1] = reinterpret_cast<double*>(base + rhoBytes + offX[j] + align_up(sizeof(double) * m.S, 256));
     J.policy = reinterpret_cast<int32_t*>(base + rhoBytes + xBytes + offPol[j]);
+    J.classRho = (!rhoHost && ctx->dm[model_ids[j]].compact)
+                     ? reinterpret_cast<double*>(base + rhoBytes + xBytes + polBytes + 256ull * sizeof(double) * j)
+                     : nullptr;
     if (!rhoHost)
       for (int o = 0; o < K; ++o) J.w[o] = weights[static_cast<size_t>(j) * K + o];
     if (!m.rewardFinite) statusInit[j] = MORAP_NOT_REWARD_FINITE;  // numerics.hpp:79-80
     else active.push_back(j);
   }
   CK(cudaMemsetAsync(base + rhoBytes, 0, xBytes, ctx->stream));
+  ctx->optCompact = ctx->useCompact && !rhoHost;
+  for (int j = 0; j < njobs && ctx->optCompact; ++j)
+    if (!ctx->dm[model_ids[j]].compact) ctx->optCompact = false;
   CK(cudaMemcpyAsync(ctx->dOptJobs, ctx->hOptJobs.data(), njobs * sizeof(OptJob), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->dStatus, statusInit.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->dSweeps, zeroI.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
@@ -1615,7 +2181,10 @@ int extract_policies(morap_ctx* ctx, const std::vector<int32_t>& jobsIn) {
   int rc;
   if ((rc = init_ctl(ctx, jobs, ctx->optModel))) return rc;
   CK(cudaMemcpyAsync(ctx->dSweeps, ctx->optSweeps.data(), ctx->optSweeps.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-  if (ctx->useTma)
+  if (ctx->useTma && ctx->optCompact)
+    k_greedy_sweep_cmp<true><<<ctx->cmpBlocks, kTmaThreads, kCmpSmemBytes, ctx->stream>>>(
+        ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr);
+  else if (ctx->useTma)
     k_greedy_sweep_tma<true><<<ctx->tmaBlocks, kTmaThreads, kTmaSmemBytes, ctx->stream>>>(
         ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr);
   else
@@ -1772,6 +2341,11 @@ int morap_cuda_create(int device, morap_ctx** out) {
   int occT = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occT, k_greedy_sweep_tma<false>, kTmaThreads, kTmaSmemBytes);
   ctx->tmaBlocks = ctx->numSMs * std::max(1, occT);
+  cudaFuncSetAttribute(k_greedy_sweep_cmp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCmpSmemBytes);
+  cudaFuncSetAttribute(k_greedy_sweep_cmp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCmpSmemBytes);
+  int occC = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occC, k_greedy_sweep_cmp<false>, kTmaThreads, kCmpSmemBytes);
+  ctx->cmpBlocks = ctx->numSMs * std::max(1, occC);
   cudaFuncSetAttribute(k_eval_sweep_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kEvSmemBytes);
   int occV = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occV, k_eval_sweep_tma, kTmaThreads, kEvSmemBytes);
@@ -1780,6 +2354,12 @@ int morap_cuda_create(int device, morap_ctx** out) {
   ctx->useTma = !(sel && std::string(sel) == "global") && occT > 0;
   const char* gsel = std::getenv("MORAP_GRAPHS");  // "0" launches sweeps one by one (A/B)
   ctx->useGraphs = !(gsel && std::string(gsel) == "0");
+  if (const char* dry = std::getenv("MORAP_DEBUG_DRY")) {
+    const int on = std::atoi(dry);
+    cudaMemcpyToSymbol(g_dryRun, &on, sizeof(int));
+  }
+  const char* csel = std::getenv("MORAP_COMPACT");  // "0" keeps the plain fp64 streams (A/B)
+  ctx->useCompact = !(csel && std::string(csel) == "0");
   if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return MORAP_CUDA_ERROR; }
   ctx->stream = ctx->own;
   cudaEventCreate(&ctx->ev0);
@@ -1843,11 +2423,16 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   std::vector<std::vector<TileDesc>> descs(nmodels);
   std::vector<int> status(nmodels, MORAP_OK);
   std::vector<std::string> why(nmodels);
+  std::vector<CompactStream> compact(nmodels);
   parallel_for(nmodels, [&](int m) {
     morap_ctx scratch;  // per-model error text
     status[m] = validate_view(&scratch, models[m], m);
-    if (status[m]) why[m] = scratch.err;
-    else make_tiles(models[m], tiles[m], descs[m]);
+    if (status[m]) {
+      why[m] = scratch.err;
+      return;
+    }
+    make_tiles(models[m], tiles[m], descs[m]);
+    if (ctx->useCompact) build_compact(models[m], compact[m]);
   });
   for (int m = 0; m < nmodels; ++m)
     if (status[m]) return ctx->fail(status[m], why[m]);
@@ -1861,6 +2446,9 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
              align_up(4ull * v.nnz, 256) + align_up(8ull * v.nnz, 256) + align_up(1ull * v.num_states, 256) +
              static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256) +
              align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
+    if (compact[m].ok)
+      bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(v.num_rows, 256) +
+               align_up(8ull * compact[m].table.size(), 256);
   }
   void* dev = nullptr;
   CK(cudaMalloc(&dev, bytes));
@@ -1907,6 +2495,18 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     // succ 4 + prob 8 per nnz; trnOffset 4 + rho 8 per row;
     // rowOffset 4 + done 1 + x 8 + y 8 per state.
     dmod.bytesPerSweep = 12ull * v.nnz + 12ull * v.num_rows + 21ull * v.num_states;
+    const CompactStream& c = compact[m];
+    if (c.ok) {
+      dmod.compact = 1;
+      dmod.probIdx = reinterpret_cast<const uint8_t*>(put(c.idx.data(), c.idx.size()));
+      dmod.probDict = reinterpret_cast<const double*>(put(c.dict.data(), 8ull * c.dict.size()));
+      dmod.rclass = reinterpret_cast<const uint8_t*>(put(c.cls.data(), c.cls.size()));
+      dmod.classTable = reinterpret_cast<const double*>(put(c.table.data(), 8ull * c.table.size()));
+      dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
+      // compact stream: succ 4 + prob index 1 per nnz; trnOffset 4 + class 1 per row;
+      // rowOffset 4 + done 1 + x 8 + y 8 per state
+      dmod.bytesPerSweep = 5ull * v.nnz + 5ull * v.num_rows + 21ull * v.num_states;
+    }
     // evaluate, one RHS over the policy chain: chainOff 4 + done 1 + rhoC 8 + x 8 + y 8 per
     // state + 12 per chosen transition (mean nnz per row)
     const double nnzPerRow = v.num_rows ? static_cast<double>(v.nnz) / v.num_rows : 0.0;

@@ -37,6 +37,7 @@ def load_library(path: str = CUDA_SO) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("MORAP_CUDA_SO", path)  # kernel-variant experiments (scripts/)
     if not os.path.exists(path):
         raise FileNotFoundError(f"{path} missing: run `python -m paper_2305_04397_b200.build` (no CPU fallback)")
     lib = C.CDLL(path)
