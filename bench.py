@@ -309,7 +309,7 @@ def run_ours(args):
                    "generate_s": round(gen_s, 3), "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "k_greedy_sweep_tma", "launches": cs["opt_launches"],
+                     "kernel": ("k_greedy_sweep_tma" if os.environ.get("MORAP_COMPACT") == "0" else "k_greedy_sweep_cmp"), "launches": cs["opt_launches"],
                      "traffic_over_algorithmic": (traffic_src or {}).get("dram_bytes_per_launch", 0) / (traffic_src or {}).get("algorithmic_bytes_per_launch", 1) if traffic_src else None,
                      "avg_launch_us": 1e3 * cs["opt_ms"] / max(cs["opt_launches"], 1),
                      "algorithmic_bytes_per_launch": cs["opt_bytes"] / max(cs["opt_launches"], 1),
