@@ -121,6 +121,9 @@ int morap_cuda_optimize_rho(morap_ctx* ctx, int njobs, const int32_t* model_ids,
  * done states -> first row, numerics.hpp:114-118). */
 int morap_cuda_fetch_values(morap_ctx* ctx, int job, double* values_out);
 int morap_cuda_fetch_policy(morap_ctx* ctx, int job, int32_t* rows_out);
+/* Policies of several optimize jobs in one batch (one synchronisation): rows_out[q]
+ * receives the num_states rows of job jobs[q]. */
+int morap_cuda_fetch_policies(morap_ctx* ctx, int njobs, const int32_t* jobs, int32_t* const* rows_out);
 
 /* Fused JobKind::Evaluate of optimize jobs' own schedulers (supportingPoint's cost and
  * success jobs, solver.hpp:148-172): for each listed optimize job, evaluate its final

@@ -238,7 +238,7 @@ class Solver:
                                       iteration_cap, int(verify), buf, len(buf), _ptr(st)), "paretoPoint")
         out = json.loads(buf.value.decode())
         out["stats"] = dict(zip(["optimize_jobs", "optimize_backups", "evaluate_jobs", "evaluate_state_backups",
-                                 "optimize_s", "evaluate_s", "host_s"], st[:7].tolist()))
+                                 "optimize_s", "evaluate_s", "host_s", "evaluate_batch_s"], st[:8].tolist()))
         return out
 
     def _json_buffer(self):

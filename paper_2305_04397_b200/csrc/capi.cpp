@@ -99,7 +99,7 @@ void putStats(const morap::QueryStats& q, double* out) {
   out[4] = q.optimizeSeconds;
   out[5] = q.evaluateSeconds;
   out[6] = q.hostSeconds;
-  out[7] = 0.0;
+  out[7] = q.evaluateSweepSeconds;
 }
 
 morap::NormMatrix normOf(const double* norm, int d) {

@@ -320,6 +320,7 @@ struct QueryStats {  // per-query instrumentation (bench)
   long optimizeJobs = 0, evaluateJobs = 0;
   double optimizeBackups = 0, evaluateStateBackups = 0;
   double optimizeSeconds = 0, evaluateSeconds = 0, hostSeconds = 0;
+  double evaluateSweepSeconds = 0;  // inside evaluateSeconds: the fused evaluate batch alone
 };
 
 using QueryFn = std::function<SupportingPoint(const Vec& w)>;

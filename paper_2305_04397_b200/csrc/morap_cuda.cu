@@ -1339,6 +1339,156 @@ __global__ void __launch_bounds__(kTmaThreads, 3) k_eval_sweep_tma(const DevMode
 }
 
 // --------------------------------------------------------------------------------------
+// K2 (persistent): the whole evaluate batch in ONE cooperative launch. Evaluate batches are
+// small (n chains of the assigned pairs, L2-resident), so per-sweep launches, the finalize
+// kernel and host polls dominated them. Here every CTA owns a contiguous range of the
+// batch's states; after each sweep the CTAs meet at a grid barrier, every CTA reads the
+// per-(job, RHS) residuals and takes the same stop decisions (delta <= eps, sweep cap),
+// CTA 0 records them. Residual slots rotate over three buffers so clearing one never races
+// with the sweep writing another. x is read with ld.global.cg (L2): it was written by other
+// SMs in the previous sweep of the same launch.
+
+constexpr int kPersistJobs = 16;   // per-CTA residual accumulators (jobs touched by one CTA)
+constexpr int kPersistMaxJobs = 1024;
+
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vg = gen;
+    const unsigned g = *vg;
+    __threadfence();
+    if (atomicAdd(count, 1u) == nblocks - 1) {
+      *count = 0;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*vg == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct PersistArgs {
+  const DevModel* models;
+  const EvalJob* jobs;
+  const long long* statePrefix;  // njobs + 1
+  int njobs;
+  double eps;
+  int cap;
+  uint32_t* mask;                 // per job, RHS still running
+  unsigned long long* slots;      // 3 x njobs x MORAP_MAX_RHS residual bits
+  int32_t* sweeps;
+  double* residual;
+  int32_t* status;
+  Ctl* ctl;
+  unsigned* barCount;
+  unsigned* barGen;
+};
+
+__global__ void __launch_bounds__(kBlock) k_eval_persistent(PersistArgs A) {
+  __shared__ uint32_t sMask[kPersistMaxJobs];
+  __shared__ unsigned long long sDelta[kPersistJobs * MORAP_MAX_RHS];
+  __shared__ int sActive;
+  const int tid = threadIdx.x;
+  const long long total = A.statePrefix[A.njobs];
+  const long long per = (total + gridDim.x - 1) / gridDim.x;
+  const long long i0 = static_cast<long long>(blockIdx.x) * per;
+  const long long i1 = min(total, i0 + per);
+  for (int j = tid; j < A.njobs; j += blockDim.x) sMask[j] = A.mask[j];
+  // first job touched by this CTA
+  int jBase = 0;
+  if (i0 < total) {
+    int lo = 0, hi = A.njobs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (A.statePrefix[mid] <= i0) lo = mid; else hi = mid - 1;
+    }
+    jBase = lo;
+  }
+  __syncthreads();
+  unsigned long long bytesAcc = 0, backupsAcc = 0;
+  for (int k = 0;; ++k) {
+    const int parity = k & 1;
+    unsigned long long* slot = A.slots + static_cast<size_t>(k % 3) * A.njobs * MORAP_MAX_RHS;
+    for (int q = tid; q < kPersistJobs * MORAP_MAX_RHS; q += blockDim.x) sDelta[q] = 0ull;
+    __syncthreads();
+    int j = jBase;
+    for (long long i = i0 + tid; i < i1; i += blockDim.x) {
+      while (i >= A.statePrefix[j + 1]) ++j;
+      const uint32_t mk = sMask[j];
+      if (!mk) continue;
+      const EvalJob& J = A.jobs[j];
+      const DevModel& M = A.models[J.model];
+      const int s = static_cast<int>(i - A.statePrefix[j]);
+      if (M.done[s]) continue;
+      const int cb = __ldg(J.chainOff + s), ce = __ldg(J.chainOff + s + 1);
+      for (int o = 0; o < J.nrhs; ++o) {
+        if (!(mk >> o & 1u)) continue;
+        const double* x = J.buf[o][parity];
+        double acc = __ldg(J.rhoC[o] + s);
+        for (int q = cb; q < ce; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(J.chainProb + q), __ldcg(x + __ldg(J.chainSucc + q))));
+        const double v = __dadd_rn(0.0, __dmul_rn(1.0, acc));
+        J.buf[o][parity ^ 1][s] = v;
+        const double d = fabs(__dsub_rn(v, __ldcg(x + s)));
+        if (d > 0.0) {
+          const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d));
+          const int rel = j - jBase;
+          if (rel < kPersistJobs) atomicMax(&sDelta[rel * MORAP_MAX_RHS + o], bits);
+          else atomicMax(&slot[j * MORAP_MAX_RHS + o], bits);
+        }
+      }
+    }
+    __syncthreads();
+    for (int q = tid; q < kPersistJobs * MORAP_MAX_RHS; q += blockDim.x) {
+      const int jj = jBase + q / MORAP_MAX_RHS;
+      if (sDelta[q] && jj < A.njobs) atomicMax(&slot[jj * MORAP_MAX_RHS + (q % MORAP_MAX_RHS)], sDelta[q]);
+    }
+    grid_barrier(A.barCount, A.barGen, gridDim.x);
+    // every CTA takes the same decisions (numerics.hpp:105-112)
+    if (tid == 0) sActive = 0;
+    __syncthreads();
+    unsigned long long* nextClear = A.slots + static_cast<size_t>((k + 2) % 3) * A.njobs * MORAP_MAX_RHS;
+    for (int jj = tid; jj < A.njobs; jj += blockDim.x) {
+      uint32_t mk = sMask[jj];
+      const EvalJob& J = A.jobs[jj];
+      for (int o = 0; o < J.nrhs; ++o) {
+        if (!(mk >> o & 1u)) continue;
+        const unsigned long long bits = __ldcg(slot + jj * MORAP_MAX_RHS + o);
+        const double d = __longlong_as_double(static_cast<long long>(bits));
+        int st = -1;
+        if (d <= A.eps) st = MORAP_OK;
+        else if (k + 1 >= A.cap) st = MORAP_NON_CONVERGENCE;
+        if (blockIdx.x == 0) {
+          A.sweeps[jj * MORAP_MAX_RHS + o] = k + 1;
+          A.residual[jj * MORAP_MAX_RHS + o] = d;
+          if (st >= 0) A.status[jj * MORAP_MAX_RHS + o] = st;
+          bytesAcc += A.models[J.model].bytesPerEval;
+          backupsAcc += static_cast<unsigned long long>(A.models[J.model].S);
+        }
+        if (st >= 0) mk &= ~(1u << o);
+      }
+      sMask[jj] = mk;
+      if (mk) sActive = 1;  // benign race: every writer stores 1
+      if (blockIdx.x == 0)
+        for (int o = 0; o < MORAP_MAX_RHS; ++o) nextClear[jj * MORAP_MAX_RHS + o] = 0ull;
+    }
+    __syncthreads();
+    if (!sActive) {
+      if (blockIdx.x == 0) {
+        if (tid == 0) A.ctl->sweepsDone = k + 1;
+        for (int jj = tid; jj < A.njobs; jj += blockDim.x) A.mask[jj] = 0u;
+        atomicAdd(&A.ctl->bytes, bytesAcc);
+        atomicAdd(&A.ctl->backups, backupsAcc);
+      }
+      return;
+    }
+    // the next sweep writes slot (k+1)%3, cleared one round ago; (k+2)%3 is cleared by CTA 0
+    // above and is next written two barriers from now
+  }
+}
+
+// --------------------------------------------------------------------------------------
 // K2: fused multi-RHS fixed-scheduler sweep (numerics.hpp:140-153 with a deterministic
 // scheduler): y_o(s) = 0 + 1.0 * (rho_o[r] + sum_k P_k x_o[succ_k]), r = policy[s].
 // Each RHS o is skipped once converged (its own stop test), so every RHS reproduces a
@@ -1651,6 +1801,13 @@ struct morap_ctx {
   bool useCompact = true;  // compact u8 probability / reward-class streams where possible
   bool optCompact = false; // current optimize batch runs the deep compact pipeline
   int cmpBlocks = 0;
+  bool usePersistent = true;  // evaluate batches as one cooperative launch
+  int persistBlocks = 0;
+  unsigned* dBar = nullptr;   // grid-barrier counter + generation
+  void* persistArena = nullptr;
+  size_t persistArenaBytes = 0;
+  void* polStage = nullptr;  // pinned staging for batched policy reads
+  size_t polStageBytes = 0;
   Ctl* dCtl = nullptr;
   Ctl* hCtl = nullptr;  // pinned mirror
   void* dEvalJobsRaw = nullptr;
@@ -2196,6 +2353,52 @@ int extract_policies(morap_ctx* ctx, const std::vector<int32_t>& jobsIn) {
   return MORAP_OK;
 }
 
+// Whole evaluate batch in one cooperative launch (k_eval_persistent). The policy chains
+// must already be built; dMask / dSweeps / dResidual / dStatus are initialised.
+int run_eval_persistent(morap_ctx* ctx, int njobs, double eps, int cap) {
+  std::vector<long long> prefix(static_cast<size_t>(njobs) + 1, 0);
+  for (int j = 0; j < njobs; ++j) prefix[j + 1] = prefix[j] + ctx->hm[ctx->hEvalJobs[j].model].S;
+  const size_t slotBytes = 3ull * njobs * MORAP_MAX_RHS * sizeof(unsigned long long);
+  const size_t need = align_up(slotBytes, 256) + align_up(8ull * (njobs + 1), 256);
+  int rc;
+  if ((rc = ensure_arena(ctx, &ctx->persistArena, &ctx->persistArenaBytes, need))) return rc;
+  char* base = static_cast<char*>(ctx->persistArena);
+  unsigned long long* slots = reinterpret_cast<unsigned long long*>(base);
+  long long* dPrefix = reinterpret_cast<long long*>(base + align_up(slotBytes, 256));
+  CK(cudaMemsetAsync(slots, 0, slotBytes, ctx->stream));
+  CK(cudaMemcpyAsync(dPrefix, prefix.data(), 8ull * (njobs + 1), cudaMemcpyHostToDevice, ctx->stream));
+  PersistArgs a{};
+  a.models = ctx->dModels;
+  a.jobs = static_cast<const EvalJob*>(ctx->dEvalJobsRaw);
+  a.statePrefix = dPrefix;
+  a.njobs = njobs;
+  a.eps = eps;
+  a.cap = cap;
+  a.mask = ctx->dMask;
+  a.slots = slots;
+  a.sweeps = ctx->dSweeps;
+  a.residual = ctx->dResidual;
+  a.status = ctx->dStatus;
+  a.ctl = ctx->dCtl;
+  a.barCount = ctx->dBar;
+  a.barGen = ctx->dBar + 1;
+  void* args[] = {&a};
+  const bool timed = ctx->profiling;
+  if (timed) CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_eval_persistent), dim3(ctx->persistBlocks), dim3(kBlock),
+                                 args, 0, ctx->stream));
+  if (timed) CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->stats[8] += 1;
+  CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (timed) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    ctx->stats[5] += ms;
+  }
+  return MORAP_OK;
+}
+
 int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, double eps, int cap,
                   double* value_out, int32_t* sweeps_out, double* residual_out, int32_t* status_out,
                   const std::vector<uint32_t>& maskInit, const std::vector<int32_t>& statusInit) {
@@ -2270,9 +2473,13 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
     CK(cudaGetLastError());
     ctx->stats[8] += 3;
   }
-  if ((rc = init_ctl(ctx, active, jobModel))) return rc;
-  if (!active.empty())
-    if ((rc = run_loop(ctx, 1, eps, cap))) return rc;
+  if (!active.empty()) {
+    if (tmaOk && ctx->usePersistent && njobs <= kPersistMaxJobs) {
+      if ((rc = run_eval_persistent(ctx, njobs, eps, cap))) return rc;
+    } else if ((rc = run_loop(ctx, 1, eps, cap))) {
+      return rc;
+    }
+  }
 
   ctx->evalSweeps.assign(static_cast<size_t>(njobs) * MORAP_MAX_RHS, 0);
   std::vector<int32_t> st(static_cast<size_t>(njobs) * MORAP_MAX_RHS);
@@ -2346,6 +2553,15 @@ int morap_cuda_create(int device, morap_ctx** out) {
   int occC = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occC, k_greedy_sweep_cmp<false>, kTmaThreads, kCmpSmemBytes);
   ctx->cmpBlocks = ctx->numSMs * std::max(1, occC);
+  int occP = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occP, k_eval_persistent, kBlock, 0);
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+  ctx->persistBlocks = ctx->numSMs * std::max(1, std::min(occP, 4));
+  const char* psel = std::getenv("MORAP_PERSISTENT");  // "0" keeps per-sweep launches (A/B)
+  ctx->usePersistent = coop && occP > 0 && !(psel && std::string(psel) == "0");
+  if (cudaMalloc(&ctx->dBar, 2 * sizeof(unsigned)) != cudaSuccess || cudaMemset(ctx->dBar, 0, 2 * sizeof(unsigned)) != cudaSuccess)
+    ctx->usePersistent = false;
   cudaFuncSetAttribute(k_eval_sweep_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kEvSmemBytes);
   int occV = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occV, k_eval_sweep_tma, kTmaThreads, kEvSmemBytes);
@@ -2390,6 +2606,9 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   cudaFree(ctx->dGather);
   cudaFree(ctx->evalStage);
   cudaFreeHost(ctx->stage);
+  cudaFree(ctx->dBar);
+  cudaFree(ctx->persistArena);
+  cudaFreeHost(ctx->polStage);
   for (cudaEvent_t e : ctx->evPool) cudaEventDestroy(e);
   for (auto& g : ctx->graphs) {
     cudaGraphExecDestroy(g.exec);
@@ -2586,6 +2805,43 @@ int morap_cuda_fetch_policy(morap_ctx* ctx, int job, int32_t* out) {
   const HostModel& m = ctx->hm[ctx->optModel[job]];
   CK(cudaMemcpyAsync(out, ctx->hOptJobs[job].policy, sizeof(int32_t) * m.S, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  return MORAP_OK;
+}
+
+int morap_cuda_fetch_policies(morap_ctx* ctx, int njobs, const int32_t* jobs, int32_t* const* rows_out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  if (njobs <= 0) return MORAP_OK;
+  std::vector<int32_t> list(jobs, jobs + njobs);
+  size_t bytes = 0;
+  for (int j : list) {
+    if (j < 0 || j >= ctx->optJobs) return ctx->fail(MORAP_INVALID_CONFIG, "job out of range");
+    if (ctx->optSweeps[j] <= 0) return ctx->fail(ctx->optStatus[j] ? ctx->optStatus[j] : MORAP_INVALID_CONFIG, "job has no policy");
+    bytes += align_up(sizeof(int32_t) * ctx->hm[ctx->optModel[j]].S, 256);
+  }
+  cudaSetDevice(ctx->device);
+  int rc = extract_policies(ctx, list);
+  if (rc) return rc;
+  // one pinned staging area, one synchronisation for the whole batch
+  if (bytes > ctx->polStageBytes) {
+    cudaFreeHost(ctx->polStage);
+    ctx->polStage = nullptr;
+    ctx->polStageBytes = 0;
+    CK(cudaMallocHost(&ctx->polStage, bytes));
+    ctx->polStageBytes = bytes;
+  }
+  std::vector<size_t> off(static_cast<size_t>(njobs));
+  size_t o = 0;
+  for (int q = 0; q < njobs; ++q) {
+    const size_t n = sizeof(int32_t) * ctx->hm[ctx->optModel[list[q]]].S;
+    off[q] = o;
+    CK(cudaMemcpyAsync(static_cast<char*>(ctx->polStage) + o, ctx->hOptJobs[list[q]].policy, n, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    o += align_up(n, 256);
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int q = 0; q < njobs; ++q)
+    std::memcpy(rows_out[q], static_cast<char*>(ctx->polStage) + off[q],
+                sizeof(int32_t) * ctx->hm[ctx->optModel[list[q]]].S);
   return MORAP_OK;
 }
 

@@ -114,8 +114,10 @@ SupportingPoint supportingPoint(const MorapInstance& inst, const Vec& w, GpuBack
   ck(ctx, morap_cuda_evaluate_optimized(ctx, n, evalJobs.data(), K, objectives.data(), 1e-6, 100000, ev.data(),
                                         esw.data(), eres.data(), est.data()),
      "evaluate batch");
+  if (stats) stats->evaluateSweepSeconds += seconds(t2);
   out.r.assign(static_cast<size_t>(K) * n, 0.0);
   out.schedulers.resize(static_cast<size_t>(n));
+  std::vector<int32_t*> rowsOut(static_cast<size_t>(n));
   for (int j = 0; j < n; ++j) {
     const int i = out.assignment.agentOf[j];
     for (int k = 0; k < K; ++k) {
@@ -125,8 +127,10 @@ SupportingPoint supportingPoint(const MorapInstance& inst, const Vec& w, GpuBack
     for (int k = 0; k < K; ++k) out.r[coord(k, i, j)] = ev[static_cast<size_t>(j) * K + k];
     const ProductMdp& p = *inst.products[i][j];
     out.schedulers[j].rows.resize(static_cast<size_t>(p.mdp.numStates));
-    ck(ctx, morap_cuda_fetch_policy(ctx, evalJobs[j], out.schedulers[j].rows.data()), "fetch policy");
+    rowsOut[j] = out.schedulers[j].rows.data();
   }
+  // the n schedulers of the assigned pairs (IterationRecord::schedulers, solver.hpp:38-45)
+  ck(ctx, morap_cuda_fetch_policies(ctx, n, evalJobs.data(), rowsOut.data()), "fetch policies");
   if (stats) {
     stats->evaluateJobs += static_cast<long>(n) * K;
     for (int j = 0; j < n; ++j)

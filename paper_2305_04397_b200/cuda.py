@@ -54,6 +54,7 @@ def load_library(path: str = CUDA_SO) -> C.CDLL:
         "morap_cuda_optimize_rho": (i32, [p, i32, p, p, f64, i32, p, p, p, p]),
         "morap_cuda_fetch_values": (i32, [p, i32, p]),
         "morap_cuda_fetch_policy": (i32, [p, i32, p]),
+        "morap_cuda_fetch_policies": (i32, [p, i32, p, p]),
         "morap_cuda_evaluate_optimized": (i32, [p, i32, p, i32, p, f64, i32, p, p, p, p]),
         "morap_cuda_evaluate": (i32, [p, i32, p, p, p, f64, i32, p, p, p, p]),
         "morap_cuda_fetch_eval_values": (i32, [p, i32, i32, p]),

@@ -58,6 +58,7 @@ VARIANTS = {
     "plain_tma": {"MORAP_COMPACT": "0"},
     "global": {"MORAP_SWEEP_KERNEL": "global", "MORAP_COMPACT": "0"},
     "no_graphs": {"MORAP_GRAPHS": "0"},
+    "no_persistent_eval": {"MORAP_PERSISTENT": "0"},
 }
 
 
