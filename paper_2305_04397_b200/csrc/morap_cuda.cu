@@ -77,6 +77,7 @@ struct DevModel {
   const double* probDict;     // <= 256 distinct probabilities
   const uint8_t* rclass;      // R
   const double* classTable;   // nclass x K objective tuples
+  const uint16_t* succW;      // compact: successor as offset into its tile's x window, 0xFFFF outside
   int32_t S, R, nnz, initial, ntiles, K, rewardFinite, compact;
   int32_t nclass, pad2;
   unsigned long long bytesPerSweep;  // algorithmic bytes of one greedy sweep
@@ -763,6 +764,7 @@ static_assert(8 * (kXWin + 2) >= 8 * kRowCap, "fallback row values reuse the win
 constexpr int kCmpSmemBytes = kCmpStages * kCStageBytes;
 
 struct CmpInfo {
+  const int32_t* succG;  // absolute successors (out-of-window transitions)
   int t, job, fits;
   int s0, r0, k0, ns;
   int offRow, offTrn, offSucc, offIdx, offCls, offDone, offX, offXw;
@@ -833,7 +835,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_greedy_sweep_cmp(const DevMo
       switch (lane) {
         case 0: src = M->rowOffset; lo = d.s0; hi = e.s0 + 1; es = 4; dstOff = kCOffRow; break;
         case 1: src = M->trnOffset; lo = d.r0; hi = e.r0 + 1; es = 4; dstOff = kCOffTrn; break;
-        case 2: src = M->succ; lo = d.k0; hi = e.k0; es = 4; dstOff = kCOffSucc; break;
+        case 2: src = M->succW; lo = d.k0; hi = e.k0; es = 2; dstOff = kCOffSucc; break;
         case 3: src = M->probIdx; lo = d.k0; hi = e.k0; es = 1; dstOff = kCOffIdx; break;
         case 4: src = M->rclass; lo = d.r0; hi = e.r0; es = 1; dstOff = kCOffCls; break;
         case 5: src = M->done; lo = d.s0; hi = e.s0; es = 1; dstOff = kCOffDone; break;
@@ -878,6 +880,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_greedy_sweep_cmp(const DevMo
         v.policy = J.policy;
         v.model = M;
         v.rho = J.rho;
+        v.succG = M->succ;
         info[b] = v;
         if (d.fits) mbar_expect_tx(bar, txBytes);
         else mbar_arrive(bar);
@@ -895,18 +898,31 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_greedy_sweep_cmp(const DevMo
     return;
   }
 
+  // The residual max is carried per thread across the consecutive tiles of one job and
+  // reduced over the CTA only when the job changes (a CTA's tiles are contiguous in the
+  // active-tile order, so that is a handful of times per sweep instead of once per tile).
+  double runMax = 0.0;
+  int runJob = -1;
   for (int use = 0;; ++use) {
     const int b = use % kCmpStages;
     mbar_wait(&full[b], (use / kCmpStages) & 1);
     const CmpInfo v = info[b];
     if (v.t < 0) break;
+    if (!POLICY && v.job != runJob) {  // uniform over the consumers
+      if (runJob >= 0) {
+        runMax = consumer_max(runMax, sRed);
+        if (tid == 0 && runMax > 0.0) atomicMax(deltaBits + runJob, (unsigned long long)__double_as_longlong(runMax));
+      }
+      runMax = 0.0;
+      runJob = v.job;
+    }
     double dl = 0.0;
     unsigned char* st = smem + b * kCStageBytes;
     const double* __restrict__ x = v.x;
     if (v.fits) {
       const int32_t* rowS = reinterpret_cast<const int32_t*>(st + kCOffRow) + v.offRow;
       const int32_t* trnS = reinterpret_cast<const int32_t*>(st + kCOffTrn) + v.offTrn;
-      const int32_t* succS = reinterpret_cast<const int32_t*>(st + kCOffSucc) + v.offSucc;
+      const uint16_t* succS = reinterpret_cast<const uint16_t*>(st + kCOffSucc) + v.offSucc;
       const uint8_t* idxS = st + kCOffIdx + v.offIdx;
       const uint8_t* clsS = st + kCOffCls + v.offCls;
       const uint8_t* doneS = st + kCOffDone + v.offDone;
@@ -921,9 +937,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_greedy_sweep_cmp(const DevMo
           double best = 0.0;
           int bestRow = -1;
           const int qb = trnS[rb] - v.k0, qe = trnS[re] - v.k0;
-          auto xAt = [&](int sIdx) {
-            const unsigned o = static_cast<unsigned>(sIdx - v.wlo);
-            return o < static_cast<unsigned>(v.wn) ? xwS[o] : __ldg(x + sIdx);
+          auto xAt = [&](int q) {  // window offset staged; absolute successor only outside it
+            const unsigned o = succS[q];
+            return o != 0xFFFFu ? xwS[o] : __ldg(x + __ldg(v.succG + v.k0 + q));
           };
           constexpr int kFast = 8;  // a warehouse state has <= 5 transitions over its rows
           if (MORAP_CMP_FAST && qe - qb <= kFast) {
@@ -932,7 +948,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_greedy_sweep_cmp(const DevMo
             double t[kFast];
 #pragma unroll
             for (int q = 0; q < kFast; ++q)
-              if (q < qe - qb) t[q] = __dmul_rn(__ldg(v.dict + idxS[qb + q]), xAt(succS[qb + q]));
+              if (q < qe - qb) t[q] = __dmul_rn(__ldg(v.dict + idxS[qb + q]), xAt(qb + q));
             int r = rb;
             int rowEnd = trnS[rb + 1] - v.k0 - qb;
             double acc = __ldg(v.classRho + clsS[rb]);
@@ -964,7 +980,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_greedy_sweep_cmp(const DevMo
             for (int r = rb; r < re; ++r) {
               const int ke = trnS[r + 1] - v.k0;
               double acc = __ldg(v.classRho + clsS[r]);
-              for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(v.dict + idxS[q]), xAt(succS[q])));
+              for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(v.dict + idxS[q]), xAt(q)));
               kb = ke;
               if (bestRow < 0 || acc > best) {
                 best = acc;
@@ -1016,13 +1032,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_greedy_sweep_cmp(const DevMo
         }
       }
     }
-    if (!POLICY) {
-      dl = consumer_max(dl, sRed);
-      if (tid == 0 && dl > 0.0) atomicMax(deltaBits + v.job, (unsigned long long)__double_as_longlong(dl));
-    } else {
-      consumer_sync();
-    }
+    runMax = fmax(runMax, dl);
+    consumer_sync();  // every consumer is done with stage b
     if (tid == 0) mbar_arrive(&empty[b]);
+  }
+  if (!POLICY && runJob >= 0) {  // residual of the last job of this CTA's range
+    runMax = consumer_max(runMax, sRed);
+    if (tid == 0 && runMax > 0.0) atomicMax(deltaBits + runJob, (unsigned long long)__double_as_longlong(runMax));
   }
 }
 
@@ -1739,6 +1755,9 @@ struct morap_ctx {
   std::vector<HostModel> hm;
   std::vector<DevModel> dm;
   std::vector<void*> modelAllocs;
+  std::vector<size_t> modelAllocBytes;
+  // released model blocks kept for reuse: cudaFree of ~1 GB costs up to ~0.8 s on B200
+  std::vector<std::pair<void*, size_t>> freeModelAllocs;
   DevModel* dModels = nullptr;
   size_t dModelsCap = 0;
 
@@ -1928,7 +1947,20 @@ struct CompactStream {
   bool ok = false;
   std::vector<uint8_t> idx, cls;
   std::vector<double> dict, table;
+  std::vector<uint16_t> succW;  // successor window offsets (needs the tile table)
 };
+
+// succW[k] = succ[k] - wlo of k's tile when inside the tile's x window, else 0xFFFF
+void build_window_offsets(const morap_csr_view& v, const std::vector<TileDesc>& desc, CompactStream& c) {
+  c.succW.resize(static_cast<size_t>(v.nnz));
+  for (size_t t = 0; t + 1 < desc.size(); ++t) {
+    const TileDesc& d = desc[t];
+    for (int k = d.k0; k < desc[t + 1].k0; ++k) {
+      const unsigned o = static_cast<unsigned>(v.succ[k] - d.wlo);
+      c.succW[k] = o < static_cast<unsigned>(d.wn) ? static_cast<uint16_t>(o) : static_cast<uint16_t>(0xFFFF);
+    }
+  }
+}
 
 // Tiny open-addressing table (<= 256 keys of up to 8 words) for build_compact.
 struct SmallIds {
@@ -2589,6 +2621,7 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (void* p : ctx->modelAllocs) cudaFree(p);
+  for (auto& f : ctx->freeModelAllocs) cudaFree(f.first);
   cudaFree(ctx->dModels);
   cudaFree(ctx->optArena);
   cudaFree(ctx->evalArena);
@@ -2651,7 +2684,10 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
       return;
     }
     make_tiles(models[m], tiles[m], descs[m]);
-    if (ctx->useCompact) build_compact(models[m], compact[m]);
+    if (ctx->useCompact) {
+      build_compact(models[m], compact[m]);
+      if (compact[m].ok) build_window_offsets(models[m], descs[m], compact[m]);
+    }
   });
   for (int m = 0; m < nmodels; ++m)
     if (status[m]) return ctx->fail(status[m], why[m]);
@@ -2667,11 +2703,31 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
              align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
     if (compact[m].ok)
       bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(v.num_rows, 256) +
-               align_up(8ull * compact[m].table.size(), 256);
+               align_up(8ull * compact[m].table.size(), 256) + align_up(2ull * v.nnz, 256);
   }
   void* dev = nullptr;
-  CK(cudaMalloc(&dev, bytes));
-  ctx->modelAllocs.push_back(dev);
+  {
+    int best = -1;
+    for (int q = 0; q < static_cast<int>(ctx->freeModelAllocs.size()); ++q)
+      if (ctx->freeModelAllocs[q].second >= bytes &&
+          (best < 0 || ctx->freeModelAllocs[q].second < ctx->freeModelAllocs[best].second))
+        best = q;
+    if (best >= 0) {
+      dev = ctx->freeModelAllocs[best].first;
+      ctx->modelAllocs.push_back(dev);
+      ctx->modelAllocBytes.push_back(ctx->freeModelAllocs[best].second);
+      ctx->freeModelAllocs.erase(ctx->freeModelAllocs.begin() + best);
+    } else {
+      if (cudaMalloc(&dev, bytes) != cudaSuccess) {  // give the cached blocks back, retry once
+        cudaGetLastError();
+        for (auto& f : ctx->freeModelAllocs) cudaFree(f.first);
+        ctx->freeModelAllocs.clear();
+        CK(cudaMalloc(&dev, bytes));
+      }
+      ctx->modelAllocs.push_back(dev);
+      ctx->modelAllocBytes.push_back(bytes);
+    }
+  }
   if (bytes > ctx->stageBytes) {  // pinned staging, grow-only (reused by later uploads)
     cudaFreeHost(ctx->stage);
     ctx->stage = nullptr;
@@ -2682,6 +2738,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   char* host = static_cast<char*>(ctx->stage);
   const int first = static_cast<int>(ctx->hm.size());
   std::vector<DevModel> built(nmodels);
+  std::atomic<bool> copyFailed{false};
   parallel_for(nmodels, [&](int m) {
     const morap_csr_view& v = models[m];
     char* h = host + off[m];
@@ -2722,15 +2779,22 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
       dmod.rclass = reinterpret_cast<const uint8_t*>(put(c.cls.data(), c.cls.size()));
       dmod.classTable = reinterpret_cast<const double*>(put(c.table.data(), 8ull * c.table.size()));
       dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
-      // compact stream: succ 4 + prob index 1 per nnz; trnOffset 4 + class 1 per row;
-      // rowOffset 4 + done 1 + x 8 + y 8 per state
-      dmod.bytesPerSweep = 5ull * v.nnz + 5ull * v.num_rows + 21ull * v.num_states;
+      dmod.succW = reinterpret_cast<const uint16_t*>(put(c.succW.data(), 2ull * c.succW.size()));
+      // compact stream: window offset 2 + prob index 1 per nnz; trnOffset 4 + class 1 per
+      // row; rowOffset 4 + done 1 + x 8 + y 8 per state
+      dmod.bytesPerSweep = 3ull * v.nnz + 5ull * v.num_rows + 21ull * v.num_states;
     }
     // evaluate, one RHS over the policy chain: chainOff 4 + done 1 + rhoC 8 + x 8 + y 8 per
     // state + 12 per chosen transition (mean nnz per row)
     const double nnzPerRow = v.num_rows ? static_cast<double>(v.nnz) / v.num_rows : 0.0;
     dmod.bytesPerEval = static_cast<unsigned long long>(v.num_states * (29.0 + 12.0 * nnzPerRow));
     built[m] = dmod;
+    // this model's block goes out as soon as it is packed (copies overlap the packing)
+    const size_t len = static_cast<size_t>(h - (host + off[m]));
+    cudaSetDevice(ctx->device);  // packing runs on pool threads
+    if (cudaMemcpyAsync(static_cast<char*>(dev) + off[m], host + off[m], len, cudaMemcpyHostToDevice, ctx->stream) !=
+        cudaSuccess)
+      copyFailed = true;
   });
   for (int m = 0; m < nmodels; ++m) {
     const DevModel& dmod = built[m];
@@ -2738,8 +2802,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     ctx->hm.push_back(HostModel{dmod.S, dmod.R, dmod.nnz, dmod.initial, dmod.ntiles, dmod.K, dmod.rewardFinite});
     if (ids_out) ids_out[m] = first + m;
   }
-  cudaError_t e = cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaError_t e = copyFailed ? cudaErrorUnknown : cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return ctx->cudaFail(e, "upload copy", __LINE__);
   if ((rc = upload_models_table(ctx))) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
@@ -2750,8 +2813,10 @@ int morap_cuda_release_models(morap_ctx* ctx) {
   if (!ctx) return MORAP_INVALID_CONFIG;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (void* p : ctx->modelAllocs) cudaFree(p);
+  for (size_t q = 0; q < ctx->modelAllocs.size(); ++q)
+    ctx->freeModelAllocs.emplace_back(ctx->modelAllocs[q], ctx->modelAllocBytes[q]);
   ctx->modelAllocs.clear();
+  ctx->modelAllocBytes.clear();
   ctx->dm.clear();
   ctx->hm.clear();
   ctx->optJobs = 0;
