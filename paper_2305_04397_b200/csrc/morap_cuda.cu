@@ -744,14 +744,20 @@ __global__ void __launch_bounds__(kTmaThreads, kStages >= 3 ? 2 : 3) k_greedy_sw
 // Arithmetic per state as in k_greedy_sweep_tma's single pass: row value =
 // classRho[class] + dict[idx_k] * x[succ_k] + ..., left to right, first strict max.
 
-constexpr int kCmpStages = 5;
+#ifndef MORAP_CMP_STAGES
+#define MORAP_CMP_STAGES 3
+#endif
+#ifndef MORAP_CMP_CTAS
+#define MORAP_CMP_CTAS 4
+#endif
+constexpr int kCmpStages = MORAP_CMP_STAGES;
 #ifndef MORAP_CMP_FAST
 #define MORAP_CMP_FAST 0  // register-batched products per state (A/B: slower on C2)
 #endif
 constexpr int kCOffRow = 0;
 constexpr int kCOffTrn = kCOffRow + 4 * kStRowInts;
 constexpr int kCOffSucc = kCOffTrn + 4 * kStTrnInts;
-constexpr int kCOffIdx = kCOffSucc + 4 * kStSuccInts;
+constexpr int kCOffIdx = kCOffSucc + 2 * (kNnzCap + 8);  // u16 window offsets (+7 front misalignment)
 constexpr int kCOffCls = kCOffIdx + kNnzCap + 16;
 constexpr int kCOffDone = kCOffCls + kRowCap + 16;
 constexpr int kCOffX = kCOffDone + kStDoneBytes;
@@ -779,7 +785,7 @@ struct CmpInfo {
 };
 
 template <bool POLICY>
-__global__ void __launch_bounds__(kTmaThreads, 2) k_greedy_sweep_cmp(const DevModel* __restrict__ models,
+__global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cmp(const DevModel* __restrict__ models,
                                                                      const OptJob* __restrict__ jobs,
                                                                      const int32_t* __restrict__ list,
                                                                      const int32_t* __restrict__ prefix,
