@@ -43,6 +43,12 @@ METRIC = "transitions/sec (nnz Bellman backups) + Pareto-query wall time at 1/2/
 UNIT = "nnz-backups/s"
 
 
+# Algorithm-1 iteration cap per workload: C3's 150-dimensional sandwich needs hundreds of
+# iterations to close an eps = 0.01 gap, so it is timed per iteration (the paper's own
+# metric) over the first 10 iterations.
+ITER_CAP = {"c3": 10}
+
+
 def workload(name: str, world: int = 1):
     if name == "c2":
         n = 10 if world == 1 else int(round(10 * math.sqrt(world)))
@@ -217,7 +223,7 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or args.sharded:
         from paper_2305_04397_b200 import distributed
         return distributed.bench_main(args, rank, world, local)
     from paper_2305_04397_b200.api import Instance, Solver
@@ -236,7 +242,7 @@ def run_ours(args):
     solver.upload(inst)
     # ---- device-resident timed region --------------------------------------------------
     for _ in range(max(args.warmup, 0)):
-        report = solver.pareto(inst, thr, eps=eps)
+        report = solver.pareto(inst, thr, eps=eps, iteration_cap=ITER_CAP.get(args.workload, 500))
     solver.set_profiling(False)
     solver.reset_cuda_stats()
     torch.cuda.synchronize()
@@ -246,7 +252,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            report = solver.pareto(inst, thr, eps=eps)
+            report = solver.pareto(inst, thr, eps=eps, iteration_cap=ITER_CAP.get(args.workload, 500))
             st = report["stats"]
             backups += st["optimize_backups"] + st["evaluate_state_backups"]
             for k in phase:
@@ -266,7 +272,7 @@ def run_ours(args):
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
     for _ in range(args.steps):
-        solver.pareto(inst, thr, eps=eps)
+        solver.pareto(inst, thr, eps=eps, iteration_cap=ITER_CAP.get(args.workload, 500))
     p1.record(stream)
     torch.cuda.synchronize()
     prof_ms = p0.elapsed_time(p1)
@@ -284,7 +290,7 @@ def run_ours(args):
     for _ in range(e2e_steps):
         solver.release()
         solver.upload(inst)
-        rep = solver.pareto(inst, thr, eps=eps)
+        rep = solver.pareto(inst, thr, eps=eps, iteration_cap=ITER_CAP.get(args.workload, 500))
         e_backups += rep["stats"]["optimize_backups"] + rep["stats"]["evaluate_state_backups"]
     e1.record(stream)
     torch.cuda.synchronize()
@@ -339,6 +345,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU (sharded, NCCL) path even on one rank (testing)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

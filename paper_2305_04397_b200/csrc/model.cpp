@@ -380,26 +380,39 @@ Vec expandThresholds(const MorapInstance& inst, const Vec& user) {
 
 void addSyntheticObjectives(MorapInstance& inst, int K, uint64_t seed) {
   if (K < 2 || K > 8) fail(Errc::InvalidConfig, "objective count must lie in [2, 8]");
-  std::map<const ProductMdp*, std::shared_ptr<ProductMdp>> remap;
+  // distinct products in (i, j) order of first occurrence; each gets its own seeded stream
+  std::map<const ProductMdp*, size_t> slot;
+  std::vector<std::pair<const ProductMdp*, uint64_t>> todo;
   for (int i = 0; i < inst.n; ++i)
-    for (int j = 0; j < inst.n; ++j) {
-      const ProductMdp* key = inst.products[i][j].get();
-      auto it = remap.find(key);
-      if (it == remap.end()) {
-        auto copy = std::make_shared<ProductMdp>(*key);
-        copy->uid = nextProductUid();
-        copy->extra.clear();
-        std::mt19937_64 rng(seed ^ (0x9e3779b97f4a7c15ull * (static_cast<uint64_t>(i) * inst.n + j + 1)));
-        std::uniform_real_distribution<double> u(-2.0, 0.0);
-        for (int k = 2; k < K; ++k) {
-          RewardStructure v(copy->cost.size());
-          for (size_t r = 0; r < v.size(); ++r) v[r] = copy->mdp.actionName[r] == kInternalAction ? 0.0 : u(rng);
-          copy->extra.push_back(std::move(v));
-        }
-        it = remap.emplace(key, std::move(copy)).first;
+    for (int j = 0; j < inst.n; ++j)
+      if (slot.emplace(inst.products[i][j].get(), todo.size()).second)
+        todo.emplace_back(inst.products[i][j].get(), static_cast<uint64_t>(i) * inst.n + j + 1);
+  std::vector<std::shared_ptr<ProductMdp>> copies(todo.size());
+  std::atomic<size_t> next{0};
+  auto worker = [&] {
+    for (size_t q; (q = next.fetch_add(1)) < todo.size();) {
+      auto copy = std::make_shared<ProductMdp>(*todo[q].first);
+      copy->uid = nextProductUid();
+      copy->extra.clear();
+      std::mt19937_64 rng(seed ^ (0x9e3779b97f4a7c15ull * todo[q].second));
+      // seeded per-row costs in [-2, 0] on a 1/8 grid (17 levels), so K-objective products
+      // keep a small reward-tuple alphabet (compact streams)
+      std::uniform_int_distribution<int> u(0, 16);
+      for (int k = 2; k < K; ++k) {
+        RewardStructure v(copy->cost.size());
+        for (size_t r = 0; r < v.size(); ++r)
+          v[r] = copy->mdp.actionName[r] == kInternalAction ? 0.0 : -0.125 * static_cast<double>(u(rng));
+        copy->extra.push_back(std::move(v));
       }
-      inst.products[i][j] = it->second;
+      copies[q] = std::move(copy);
     }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < hostThreads(0); ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+  for (int i = 0; i < inst.n; ++i)
+    for (int j = 0; j < inst.n; ++j) inst.products[i][j] = copies[slot.at(inst.products[i][j].get())];
   inst.objectives = K;
 }
 

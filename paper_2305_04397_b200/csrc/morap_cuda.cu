@@ -1436,31 +1436,49 @@ __global__ void __launch_bounds__(kBlock) k_eval_persistent(PersistArgs A) {
     for (int q = tid; q < kPersistJobs * MORAP_MAX_RHS; q += blockDim.x) sDelta[q] = 0ull;
     __syncthreads();
     int j = jBase;
+    // per-thread running residual of the current job, flushed when the job changes
+    double run[MORAP_MAX_RHS];
+#pragma unroll
+    for (int o = 0; o < MORAP_MAX_RHS; ++o) run[o] = 0.0;
+    int runJob = -1;
+    auto flush = [&]() {
+      if (runJob < 0) return;
+      const int rel = runJob - jBase;
+#pragma unroll
+      for (int o = 0; o < MORAP_MAX_RHS; ++o) {
+        if (run[o] > 0.0) {
+          const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(run[o]));
+          if (rel < kPersistJobs) atomicMax(&sDelta[rel * MORAP_MAX_RHS + o], bits);
+          else atomicMax(&slot[runJob * MORAP_MAX_RHS + o], bits);
+        }
+        run[o] = 0.0;
+      }
+    };
     for (long long i = i0 + tid; i < i1; i += blockDim.x) {
       while (i >= A.statePrefix[j + 1]) ++j;
       const uint32_t mk = sMask[j];
       if (!mk) continue;
+      if (j != runJob) {
+        flush();
+        runJob = j;
+      }
       const EvalJob& J = A.jobs[j];
       const DevModel& M = A.models[J.model];
       const int s = static_cast<int>(i - A.statePrefix[j]);
       if (M.done[s]) continue;
       const int cb = __ldg(J.chainOff + s), ce = __ldg(J.chainOff + s + 1);
-      for (int o = 0; o < J.nrhs; ++o) {
-        if (!(mk >> o & 1u)) continue;
+#pragma unroll
+      for (int o = 0; o < MORAP_MAX_RHS; ++o) {
+        if (o >= J.nrhs || !(mk >> o & 1u)) continue;
         const double* x = J.buf[o][parity];
         double acc = __ldg(J.rhoC[o] + s);
         for (int q = cb; q < ce; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(J.chainProb + q), __ldcg(x + __ldg(J.chainSucc + q))));
         const double v = __dadd_rn(0.0, __dmul_rn(1.0, acc));
         J.buf[o][parity ^ 1][s] = v;
-        const double d = fabs(__dsub_rn(v, __ldcg(x + s)));
-        if (d > 0.0) {
-          const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d));
-          const int rel = j - jBase;
-          if (rel < kPersistJobs) atomicMax(&sDelta[rel * MORAP_MAX_RHS + o], bits);
-          else atomicMax(&slot[j * MORAP_MAX_RHS + o], bits);
-        }
+        run[o] = fmax(run[o], fabs(__dsub_rn(v, __ldcg(x + s))));
       }
     }
+    flush();
     __syncthreads();
     for (int q = tid; q < kPersistJobs * MORAP_MAX_RHS; q += blockDim.x) {
       const int jj = jBase + q / MORAP_MAX_RHS;

@@ -7,6 +7,8 @@
 // objectives in one fused multi-RHS device batch, using the optimize jobs' policies that
 // never left the GPU. runParetoCore is Algorithm 1 (the sandwich loop) on the host.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -130,7 +132,14 @@ SupportingPoint supportingPoint(const MorapInstance& inst, const Vec& w, GpuBack
     rowsOut[j] = out.schedulers[j].rows.data();
   }
   // the n schedulers of the assigned pairs (IterationRecord::schedulers, solver.hpp:38-45)
+  const auto t3 = std::chrono::steady_clock::now();
   ck(ctx, morap_cuda_fetch_policies(ctx, n, evalJobs.data(), rowsOut.data()), "fetch policies");
+  if (std::getenv("MORAP_TRACE"))
+    std::fprintf(stderr, "[morap] supportingPoint: optimize %.3f ms (%d jobs), assign %.3f ms, evaluate %.3f ms, "
+                         "policies %.3f ms\n",
+                 1e3 * std::chrono::duration<double>(t1 - t0).count(), nj,
+                 1e3 * std::chrono::duration<double>(t2 - t1).count(),
+                 1e3 * std::chrono::duration<double>(t3 - t2).count(), 1e3 * seconds(t3));
   if (stats) {
     stats->evaluateJobs += static_cast<long>(n) * K;
     for (int j = 0; j < n; ++j)
@@ -160,9 +169,14 @@ ParetoResult runParetoCore(Vec t, const NormMatrix& norm, double eps, int iterat
     for (size_t k = 0; k < d.size(); ++k) d[k] -= b[k];
     return d;
   };
+  const bool trace = std::getenv("MORAP_TRACE") != nullptr;
   for (int iter = 0; iter < iterationCap; ++iter) {
     if (!res.phi.points.empty()) {
+      const auto tq = std::chrono::steady_clock::now();
       ProjectionResult low = projectToLowerApprox(thr, res.phi, norm);
+      if (trace)
+        std::fprintf(stderr, "[morap] iteration %d: lower projection %.3f ms, gap %.6g\n", iter, 1e3 * seconds(tq),
+                     normDistance(norm, minus(res.tDown, low.x)));
       res.tUp = low.x;
       res.lambdaStar = low.lambda;
       if (normDistance(norm, minus(res.tDown, res.tUp)) <= eps) {
@@ -193,7 +207,9 @@ ParetoResult runParetoCore(Vec t, const NormMatrix& norm, double eps, int iterat
         res.iterations.push_back(std::move(rec));
         return res;
       }
+      const auto tq = std::chrono::steady_clock::now();
       res.tDown = projectToUpperApprox(thr, res.lambda, norm);
+      if (trace) std::fprintf(stderr, "[morap] iteration %d: upper projection %.3f ms\n", iter, 1e3 * seconds(tq));
     }
     rec.tDown = res.tDown;
     res.iterations.push_back(std::move(rec));
