@@ -65,6 +65,16 @@ morap_ctx* morap_solver_cuda(morap_solver* s);
 int morap_solver_upload(morap_solver* s, const morap_instance* inst);
 /* Drop every resident product (device memory freed; next query re-uploads). */
 int morap_solver_release(morap_solver* s);
+/* morap_cuda_set_lean on the solver's context (applies to later uploads). */
+int morap_solver_set_lean(morap_solver* s, int on);
+
+/* Streamed generateInstance for instances whose host copy would not fit (C4: 100 x 100,
+ * ~1e4 products of ~1e5 states): products are built `chunk` at a time on `threads` host
+ * threads, each chunk's distinct products are uploaded to `s` and their host arrays
+ * dropped. The instance then only answers queries on `s` (product_export fails on it).
+ * Deduplication against dropped products compares (structural hash, S, R, nnz, initial). */
+int morap_instance_warehouse_streamed(const char* config_json, int threads, morap_solver* s, int chunk,
+                                      morap_instance** out);
 
 /* supportingPoint (solver.hpp:103-184): w has K*n entries (unit 1-norm). Writes r (K*n)
  * and the assignment agent_of[n]. stats_out (nullable, 8 doubles): optimize jobs,

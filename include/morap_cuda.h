@@ -96,6 +96,12 @@ const char* morap_cuda_last_error(morap_ctx* ctx);
  * Validates CSR structure (offsets monotone, successors in range) -> MORAP_INVALID_MODEL. */
 int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models, int32_t* model_ids_out);
 int morap_cuda_release_models(morap_ctx* ctx);
+/* Lean uploads (for instances that do not fit otherwise, e.g. 100 x 100): a model with a
+ * compact alphabet (<= 256 distinct probabilities and objective tuples) is stored without
+ * its fp64 prob / objective arrays -- the device reads the exact same values from the
+ * model's dictionary and class table. Lean models take weighted optimize jobs and
+ * policy-chain evaluations (<= 4 objectives), not explicit reward vectors. */
+int morap_cuda_set_lean(morap_ctx* ctx, int on);
 int morap_cuda_num_models(morap_ctx* ctx);
 
 /* JobKind::Optimize batch (engine.hpp:126-131 -> numerics.hpp:74). Job k runs on model

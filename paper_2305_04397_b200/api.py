@@ -55,6 +55,8 @@ def load_host_library() -> C.CDLL:
         "morap_solver_cuda": (p, [p]),
         "morap_solver_upload": (i32, [p, p]),
         "morap_solver_release": (i32, [p]),
+        "morap_solver_set_lean": (i32, [p, i32]),
+        "morap_instance_warehouse_streamed": (i32, [C.c_char_p, i32, p, i32, C.POINTER(p)]),
         "morap_supporting_point": (i32, [p, p, p, i32, p, p, p]),
         "morap_pareto": (i32, [p, p, p, i32, p, f64, i32, i32, C.c_char_p, i32, p]),
         "morap_pareto_core": (i32, [p, i32, i32, p, f64, i32, i32, QUERY_FN, p, C.c_char_p, i32]),
@@ -114,6 +116,19 @@ class Instance:
         h = C.c_void_p()
         _check(lib.morap_instance_warehouse(json.dumps(config).encode(), threads, C.byref(h)), "generateInstance")
         return cls(h)
+
+    @classmethod
+    def warehouse_streamed(cls, config: dict, solver: "Solver", chunk: int = 256, threads: int = 0) -> "Instance":
+        """Streamed generateInstance for instances too large for a host copy (C4): products
+        are built `chunk` at a time, uploaded to `solver` and their host arrays dropped, so
+        the instance only answers queries on that solver (morap.h)."""
+        lib = load_host_library()
+        h = C.c_void_p()
+        _check(lib.morap_instance_warehouse_streamed(json.dumps(config).encode(), threads, solver.h, chunk,
+                                                     C.byref(h)), "generateInstance (streamed)")
+        inst = cls(h)
+        inst.streamed = True
+        return inst
 
     @classmethod
     def from_json(cls, text: str, base_dir: str = ".") -> "Instance":
@@ -197,6 +212,10 @@ class Solver:
 
     def release(self):
         _check(self._lib.morap_solver_release(self.h), "release")
+
+    def set_lean(self, on: bool):
+        """Store compact-alphabet products without fp64 prob/objective arrays (morap_cuda_set_lean)."""
+        _check(self._lib.morap_solver_set_lean(self.h, int(on)), "set_lean")
 
     def cuda_stats(self) -> dict:
         from .cuda import load_library

@@ -1,6 +1,8 @@
 // extern "C" face of the host library (include/morap.h).
 #include <cstring>
 #include <fstream>
+#include <map>
+#include <set>
 #include <sstream>
 #include <thread>
 
@@ -9,6 +11,7 @@
 
 struct morap_instance {
   morap::MorapInstance inst;
+  std::map<const morap::ProductMdp*, int64_t> firstSlot;  // lazily filled (product_dims)
 };
 
 struct morap_solver {
@@ -120,7 +123,7 @@ int morap_instance_warehouse(const char* config_json, int threads, morap_instanc
   return guard([&] {
     if (!out || !config_json) morap::fail(morap::Errc::InvalidConfig, "null argument");
     morap::WarehouseConfig cfg = morap::warehouseConfigFromJson(morap::Json::parse(config_json));
-    *out = new morap_instance{morap::generateInstance(cfg, threads)};
+    *out = new morap_instance{morap::generateInstance(cfg, threads), {}};
   });
 }
 
@@ -135,7 +138,7 @@ int morap_instance_from_json(const char* text, const char* base_dir, morap_insta
       morap::fail(morap::Errc::Io, e.what());
     }
     const std::string base = base_dir ? base_dir : ".";
-    auto inst = std::make_unique<morap_instance>(morap_instance{morap::instanceFromJson(j, base)});
+    auto inst = std::make_unique<morap_instance>(morap_instance{morap::instanceFromJson(j, base), {}});
     if (has_norm) *has_norm = 0;
     if (j.contains("norm") && norm_out) {
       morap::Json nj = j.at("norm");
@@ -167,16 +170,13 @@ int morap_instance_info(const morap_instance* p, int64_t* out) {
   return guard([&] {
     const auto& I = p->inst;
     int64_t S = 0, R = 0, Z = 0, Zd = 0;
-    std::vector<const morap::ProductMdp*> seen;
+    std::set<const morap::ProductMdp*> seen;
     for (const auto& row : I.products)
       for (const auto& q : row) {
         S += q->mdp.numStates;
-        R += q->mdp.numActions();
-        Z += static_cast<int64_t>(q->mdp.succ.size());
-        if (std::find(seen.begin(), seen.end(), q.get()) == seen.end()) {
-          seen.push_back(q.get());
-          Zd += static_cast<int64_t>(q->mdp.succ.size());
-        }
+        R += morap::productRows(*q);
+        Z += morap::productNnz(*q);
+        if (seen.insert(q.get()).second) Zd += morap::productNnz(*q);
       }
     const int64_t v[8] = {I.n, I.realTasks, I.distinctProducts, I.objectives, S, R, Z, Zd};
     std::memcpy(out, v, sizeof v);
@@ -188,12 +188,12 @@ int morap_instance_product_dims(const morap_instance* p, int i, int j, int64_t* 
     const auto& I = p->inst;
     if (i < 0 || j < 0 || i >= I.n || j >= I.n) morap::fail(morap::Errc::InvalidConfig, "product index out of range");
     const morap::ProductMdp& q = *I.products[i][j];
-    int64_t first = -1;
-    for (int a = 0; a < I.n && first < 0; ++a)
-      for (int b = 0; b < I.n && first < 0; ++b)
-        if (I.products[a][b].get() == &q) first = static_cast<int64_t>(a) * I.n + b;
-    const int64_t v[6] = {q.mdp.numStates, q.mdp.numActions(), static_cast<int64_t>(q.mdp.succ.size()), q.mdp.initial,
-                          q.rewardFinite ? 1 : 0, first};
+    auto& firstSlot = const_cast<morap_instance*>(p)->firstSlot;
+    if (firstSlot.empty())
+      for (int a = I.n - 1; a >= 0; --a)
+        for (int b = I.n - 1; b >= 0; --b) firstSlot[I.products[a][b].get()] = static_cast<int64_t>(a) * I.n + b;
+    const int64_t v[6] = {q.mdp.numStates, morap::productRows(q), morap::productNnz(q), q.mdp.initial,
+                          q.rewardFinite ? 1 : 0, firstSlot.at(&q)};
     std::memcpy(dims, v, sizeof v);
     if (hash) *hash = q.structuralHash;
   });
@@ -205,6 +205,7 @@ int morap_instance_product_export(const morap_instance* p, int i, int j, int32_t
     const auto& I = p->inst;
     if (i < 0 || j < 0 || i >= I.n || j >= I.n) morap::fail(morap::Errc::InvalidConfig, "product index out of range");
     const morap::ProductMdp& q = *I.products[i][j];
+    morap::requireFull(q, "product export");
     auto cp = [](auto* dst, const auto& v) {
       if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
     };
@@ -227,13 +228,17 @@ int morap_instance_product_objective(const morap_instance* p, int i, int j, int 
     if (i < 0 || j < 0 || i >= I.n || j >= I.n || k < 0 || k >= I.objectives)
       morap::fail(morap::Errc::InvalidConfig, "objective index out of range");
     const morap::ProductMdp& q = *I.products[i][j];
+    morap::requireFull(q, "product objective");
     const morap::RewardStructure& v = k == 0 ? q.cost : k == I.objectives - 1 ? q.success : q.extra.at(k - 1);
     std::memcpy(out, v.data(), sizeof(double) * v.size());
   });
 }
 
 int morap_instance_add_objectives(morap_instance* p, int K, uint64_t seed) {
-  return guard([&] { morap::addSyntheticObjectives(p->inst, K, seed); });
+  return guard([&] {
+    morap::addSyntheticObjectives(p->inst, K, seed);
+    p->firstSlot.clear();
+  });
 }
 
 int morap_solver_create(int device, morap_solver** out) {
@@ -255,6 +260,32 @@ int morap_solver_upload(morap_solver* s, const morap_instance* inst) {
 
 int morap_solver_release(morap_solver* s) {
   return guard([&] { s->gpu->release(); });
+}
+
+int morap_solver_set_lean(morap_solver* s, int on) {
+  return guard([&] { s->gpu->setLean(on != 0); });
+}
+
+int morap_instance_warehouse_streamed(const char* config_json, int threads, morap_solver* s, int chunk,
+                                      morap_instance** out) {
+  return guard([&] {
+    if (!out || !config_json || !s) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    if (chunk < 1) morap::fail(morap::Errc::InvalidConfig, "chunk must be positive");
+    morap::WarehouseConfig cfg = morap::warehouseConfigFromJson(morap::Json::parse(config_json));
+    morap::GpuBackend& gpu = *s->gpu;
+    const morap::ProductSink sink = [&](const std::vector<morap::ProductMdp*>& fresh) {
+      gpu.uploadProducts(std::vector<const morap::ProductMdp*>(fresh.begin(), fresh.end()));
+      std::vector<std::thread> pool;
+      const size_t T = std::max(1u, std::thread::hardware_concurrency());
+      for (size_t t = 0; t < T; ++t)
+        pool.emplace_back([&, t] {
+          for (size_t k = t; k < fresh.size(); k += T) morap::slimProduct(*fresh[k]);
+        });
+      for (auto& th : pool) th.join();
+    };
+    const std::function<void()> retry = [&] { gpu.release(); };
+    *out = new morap_instance{morap::generateInstance(cfg, threads, static_cast<size_t>(chunk), &sink, &retry), {}};
+  });
 }
 
 int morap_supporting_point(morap_solver* s, const morap_instance* p, const double* w, int nw, double* r_out,

@@ -7,6 +7,7 @@
 // the library error code, results independent of how jobs are batched -- but executes
 // each kind of job as a single device batch instead of a CPU worker pool.
 #include <cstring>
+#include <set>
 
 #include "morap.hpp"
 #include "morap_cuda.h"
@@ -32,6 +33,7 @@ std::vector<const double*> objectivesOf(const ProductMdp& p) {
 }
 
 morap_csr_view viewOf(const ProductMdp& p, const std::vector<const double*>& objs, std::vector<uint8_t>& doneBytes) {
+  requireFull(p, "upload to another device");
   morap_csr_view v{};
   v.num_states = p.mdp.numStates;
   v.num_rows = p.mdp.numActions();
@@ -81,11 +83,22 @@ int GpuBackend::modelId(const ProductMdp* p) {
   return id;
 }
 
+void GpuBackend::setLean(bool on) { check(ctx_, morap_cuda_set_lean(ctx_, on ? 1 : 0), "set lean"); }
+
 void GpuBackend::uploadInstance(const MorapInstance& inst) {
   std::vector<const ProductMdp*> todo;
+  std::set<uint64_t> queued;
   for (const auto& row : inst.products)
     for (const auto& p : row)
-      if (!ids_.count(p->uid) && std::find(todo.begin(), todo.end(), p.get()) == todo.end()) todo.push_back(p.get());
+      if (!ids_.count(p->uid) && queued.insert(p->uid).second) todo.push_back(p.get());
+  uploadProducts(todo);
+}
+
+void GpuBackend::uploadProducts(const std::vector<const ProductMdp*>& products) {
+  std::vector<const ProductMdp*> todo;
+  std::set<uint64_t> queued;
+  for (const ProductMdp* p : products)
+    if (!ids_.count(p->uid) && queued.insert(p->uid).second) todo.push_back(p);
   if (todo.empty()) return;
   std::vector<std::vector<const double*>> objs(todo.size());
   std::vector<std::vector<uint8_t>> done(todo.size());
@@ -114,7 +127,7 @@ RewardStructure weightedReward(const std::vector<const RewardStructure*>& parts,
 
 OptimizeResult optimalScheduler(GpuBackend& gpu, const ProductMdp& p, const RewardStructure& rho, double eps,
                                 int sweepCap) {
-  if (static_cast<int>(rho.size()) != p.mdp.numActions())
+  if (static_cast<int>(rho.size()) != productRows(p))
     fail(Errc::DimensionMismatch, "reward structure does not match action rows");
   const int32_t id = gpu.modelId(&p);
   const double* r = rho.data();
@@ -140,7 +153,7 @@ OptimizeResult optimalScheduler(GpuBackend& gpu, const ProductMdp& p, const Rewa
 
 EvaluateResult evaluateScheduler(GpuBackend& gpu, const ProductMdp& p, const Scheduler& mu, const RewardStructure& rho,
                                  double eps, int sweepCap) {
-  if (static_cast<int>(rho.size()) != p.mdp.numActions())
+  if (static_cast<int>(rho.size()) != productRows(p))
     fail(Errc::DimensionMismatch, "reward structure does not match action rows");
   if (static_cast<int>(mu.rows.size()) != p.mdp.numStates) fail(Errc::InvalidModel, "scheduler does not cover every state");
   const int32_t id = gpu.modelId(&p);
@@ -180,7 +193,7 @@ std::map<long, JobResult> runBatch(std::vector<Job> jobs, GpuBackend& gpu) {
         res.errc = Errc::InvalidModel;
         continue;
       }
-      if (static_cast<int>(j.reward.size()) != j.model->mdp.numActions()) {
+      if (static_cast<int>(j.reward.size()) != productRows(*j.model)) {
         res.error = "reward structure does not match action rows";
         res.errc = Errc::DimensionMismatch;
         continue;

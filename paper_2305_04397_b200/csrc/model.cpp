@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <optional>
 #include <random>
 #include <set>
 #include <thread>
@@ -294,8 +295,48 @@ int hostThreads(int want) {
 
 }  // namespace
 
+void slimProduct(ProductMdp& p) {
+  if (p.slim) return;
+  p.slimRows = p.mdp.numActions();
+  p.slimNnz = static_cast<int64_t>(p.mdp.succ.size());
+  auto drop = [](auto& v) { std::remove_reference_t<decltype(v)>().swap(v); };
+  drop(p.mdp.rowOffset);
+  drop(p.mdp.trnOffset);
+  drop(p.mdp.succ);
+  drop(p.mdp.prob);
+  drop(p.mdp.actionName);
+  drop(p.mdp.labels);
+  drop(p.agentState);
+  drop(p.dfaLocation);
+  drop(p.done);
+  drop(p.accept);
+  drop(p.preSink);
+  drop(p.cost);
+  drop(p.success);
+  drop(p.extra);
+  p.slim = true;
+}
+
+void requireFull(const ProductMdp& p, const char* what) {
+  if (p.slim)
+    fail(Errc::InvalidConfig, std::string(what) +
+                                  ": the product's host arrays were dropped after a streamed upload (its only copy is "
+                                  "on the device)");
+}
+
+namespace {
+
+// Same (S, R, nnz, initial) and structural hash: the identity test used against products
+// whose arrays are gone (streamed builds); full products are compared array by array.
+bool sameSlimKey(const ProductMdp& a, const ProductMdp& b) {
+  return a.structuralHash == b.structuralHash && a.mdp.numStates == b.mdp.numStates &&
+         a.mdp.initial == b.mdp.initial && productRows(a) == productRows(b) && productNnz(a) == productNnz(b);
+}
+
+}  // namespace
+
 MorapInstance buildInstance(std::vector<Mdp> agents, std::vector<RewardStructure> costs, std::vector<Dfa> tasks,
-                            int threads) {
+                            int threads, size_t chunk, const ProductSink* sink) {
   if (agents.empty()) fail(Errc::InvalidModel, "instance needs at least one agent");
   if (agents.size() != costs.size()) fail(Errc::DimensionMismatch, "one cost structure per agent required");
   if (tasks.size() > agents.size()) fail(Errc::InvalidModel, "more tasks than agents; drop tasks or add agents");
@@ -314,47 +355,56 @@ MorapInstance buildInstance(std::vector<Mdp> agents, std::vector<RewardStructure
 
   const int n = inst.n;
   const size_t total = static_cast<size_t>(n) * n;
-  std::vector<std::unique_ptr<ProductMdp>> built(total);
-  std::vector<std::optional<Error>> errs(total);
-  std::atomic<size_t> next{0};
-  auto worker = [&] {
-    for (size_t k; (k = next.fetch_add(1)) < total;) {
-      const int i = static_cast<int>(k / n), j = static_cast<int>(k % n);
-      try {
-        built[k] = std::make_unique<ProductMdp>(buildProduct(inst.agents[i], inst.costs[i], inst.tasks[j], i, j));
-      } catch (const Error& e) {
-        errs[k] = e;
-      }
-    }
-  };
-  const int T = std::min<int>(hostThreads(threads), static_cast<int>(total));
-  std::vector<std::thread> pool;
-  for (int t = 1; t < T; ++t) pool.emplace_back(worker);
-  worker();
-  for (auto& th : pool) th.join();
-
-  // reject / deduplicate in (i, j) order, as instance.hpp:445-466 does sequentially
-  std::map<uint64_t, std::vector<std::shared_ptr<const ProductMdp>>> byHash;
+  if (chunk == 0 || !sink) chunk = total;
+  std::map<uint64_t, std::vector<std::shared_ptr<ProductMdp>>> byHash;
   inst.products.assign(static_cast<size_t>(n), std::vector<std::shared_ptr<const ProductMdp>>(static_cast<size_t>(n)));
-  for (size_t k = 0; k < total; ++k) {
-    const int i = static_cast<int>(k / n), j = static_cast<int>(k % n);
-    if (errs[k]) throw *errs[k];
-    if (!built[k]->rewardFinite)
-      fail(Errc::NotRewardFinite,
-           "product of agent " + std::to_string(i) + " and task " + std::to_string(j) + " can cycle without finishing");
-    auto& bucket = byHash[built[k]->structuralHash];
-    std::shared_ptr<const ProductMdp> share;
-    for (const auto& cand : bucket)
-      if (sameProduct(*cand, *built[k])) {
-        share = cand;
-        break;
+  const int T = std::min<int>(hostThreads(threads), static_cast<int>(std::min(total, chunk)));
+  for (size_t base = 0; base < total; base += chunk) {
+    const size_t m = std::min(chunk, total - base);
+    std::vector<std::unique_ptr<ProductMdp>> built(m);
+    std::vector<std::optional<Error>> errs(m);
+    std::atomic<size_t> next{0};
+    auto worker = [&] {
+      for (size_t q; (q = next.fetch_add(1)) < m;) {
+        const size_t k = base + q;
+        const int i = static_cast<int>(k / n), j = static_cast<int>(k % n);
+        try {
+          built[q] = std::make_unique<ProductMdp>(buildProduct(inst.agents[i], inst.costs[i], inst.tasks[j], i, j));
+        } catch (const Error& e) {
+          errs[q] = e;
+        }
       }
-    if (!share) {
-      share = std::shared_ptr<const ProductMdp>(built[k].release());
-      bucket.push_back(share);
-      ++inst.distinctProducts;
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+
+    // reject / deduplicate in (i, j) order, as instance.hpp:445-466 does sequentially
+    std::vector<ProductMdp*> fresh;
+    for (size_t q = 0; q < m; ++q) {
+      const size_t k = base + q;
+      const int i = static_cast<int>(k / n), j = static_cast<int>(k % n);
+      if (errs[q]) throw *errs[q];
+      if (!built[q]->rewardFinite)
+        fail(Errc::NotRewardFinite,
+             "product of agent " + std::to_string(i) + " and task " + std::to_string(j) + " can cycle without finishing");
+      auto& bucket = byHash[built[q]->structuralHash];
+      std::shared_ptr<ProductMdp> share;
+      for (const auto& cand : bucket)
+        if (cand->slim ? sameSlimKey(*cand, *built[q]) : sameProduct(*cand, *built[q])) {
+          share = cand;
+          break;
+        }
+      if (!share) {
+        share = std::shared_ptr<ProductMdp>(built[q].release());
+        bucket.push_back(share);
+        fresh.push_back(share.get());
+        ++inst.distinctProducts;
+      }
+      inst.products[i][j] = share;
     }
-    inst.products[i][j] = share;
+    if (sink && !fresh.empty()) (*sink)(fresh);
   }
   return inst;
 }
@@ -387,6 +437,7 @@ void addSyntheticObjectives(MorapInstance& inst, int K, uint64_t seed) {
     for (int j = 0; j < inst.n; ++j)
       if (slot.emplace(inst.products[i][j].get(), todo.size()).second)
         todo.emplace_back(inst.products[i][j].get(), static_cast<uint64_t>(i) * inst.n + j + 1);
+  for (const auto& t : todo) requireFull(*t.first, "add objectives");
   std::vector<std::shared_ptr<ProductMdp>> copies(todo.size());
   std::atomic<size_t> next{0};
   auto worker = [&] {

@@ -141,7 +141,16 @@ struct ProductMdp {
   int agentId = -1, taskId = -1;
   uint64_t structuralHash = 0;
   uint64_t uid = nextProductUid();  // device-model key (addresses can be reused after free)
+  // Streamed instances (C4): once a product is resident on the device its host arrays are
+  // dropped; numStates / initial / rewardFinite / hash stay, rows and nnz are kept here.
+  bool slim = false;
+  int slimRows = 0;
+  int64_t slimNnz = 0;
 };
+inline int productRows(const ProductMdp& p) { return p.slim ? p.slimRows : p.mdp.numActions(); }
+inline int64_t productNnz(const ProductMdp& p) { return p.slim ? p.slimNnz : static_cast<int64_t>(p.mdp.succ.size()); }
+void slimProduct(ProductMdp& p);  // drop host arrays (the device copy is the only one left)
+void requireFull(const ProductMdp& p, const char* what);  // InvalidConfig on a slim product
 extern const std::string kInternalAction;
 
 std::vector<int> maximalAvoidSet(const Mdp& m, const std::vector<char>& done);
@@ -162,8 +171,12 @@ struct MorapInstance {
   int distinctProducts = 0;
   int objectives = 2;  // K: cost, success (+ extras)
 };
+// Called with each chunk's newly built distinct products (streamed builds): the sink
+// uploads them and may slim them. Later chunks deduplicate against slim products by
+// (structural hash, S, R, nnz, initial) instead of a full array compare.
+using ProductSink = std::function<void(const std::vector<ProductMdp*>&)>;
 MorapInstance buildInstance(std::vector<Mdp> agents, std::vector<RewardStructure> costs, std::vector<Dfa> tasks,
-                            int threads = 0);
+                            int threads = 0, size_t chunk = 0, const ProductSink* sink = nullptr);
 Vec expandThresholds(const MorapInstance& inst, const Vec& user);
 // K-objective extension: attach K-2 extra seeded per-row objectives in
 // [-2, 0] to every product (not in the reference; parity for K > 2 is unpinned).
@@ -182,7 +195,8 @@ void validateWarehouseConfig(const WarehouseConfig& cfg);
 std::pair<Mdp, RewardStructure> generateAgent(const WarehouseConfig& cfg, int agentIndex);
 Formula generateTask(const WarehouseConfig& cfg, int rackIndex);
 Dfa taskAutomaton(const WarehouseConfig& cfg, int rackIndex);
-MorapInstance generateInstance(const WarehouseConfig& cfg, int threads = 0);
+MorapInstance generateInstance(const WarehouseConfig& cfg, int threads = 0, size_t chunk = 0,
+                               const ProductSink* sink = nullptr, const std::function<void()>* onRetry = nullptr);
 WarehouseConfig warehouseConfigFromJson(const Json& j);
 
 // ---- per-model solve on the GPU (numerics.hpp, engine.hpp) --------------------------------
@@ -216,6 +230,8 @@ class GpuBackend {
   GpuBackend& operator=(const GpuBackend&) = delete;
   int modelId(const ProductMdp* p);           // uploads on first use
   void uploadInstance(const MorapInstance& inst);  // all distinct products in one batch
+  void uploadProducts(const std::vector<const ProductMdp*>& products);  // one batch, skips resident ones
+  void setLean(bool on);  // morap_cuda_set_lean: compact-alphabet models without fp64 arrays
   morap_ctx* ctx() const { return ctx_; }
   int device() const { return device_; }
   void release();

@@ -105,6 +105,7 @@ struct EvalJob {
   int32_t* chainSucc;  // <= nnz
   double* chainProb;   // <= nnz
   double* rhoC[MORAP_MAX_RHS];  // rho_o of each state's chosen row
+  int32_t objIdx[MORAP_MAX_RHS];  // objective of each RHS (lean models read the class table)
 };
 
 // Device control block for one batch loop.
@@ -137,6 +138,23 @@ __device__ __forceinline__ double row_value(const int32_t* __restrict__ trn, con
   double v = rho[r];
   const int kb = trn[r], ke = trn[r + 1];
   for (int k = kb; k < ke; ++k) v = __dadd_rn(v, __dmul_rn(prob[k], __ldg(x + succ[k])));
+  return v;
+}
+
+// Model accessors that work for lean compact models too (no fp64 prob / objective arrays
+// on the device: the values come from the model's dictionary / class table, bit-identical).
+__device__ __forceinline__ double model_prob(const DevModel& M, int k) {
+  return M.prob ? M.prob[k] : M.probDict[M.probIdx[k]];
+}
+__device__ __forceinline__ double model_obj(const DevModel& M, int o, int r) {
+  return M.obj[o] ? M.obj[o][r] : M.classTable[M.rclass[r] * M.K + o];
+}
+// row value of the compact kernel's fallback path: rho_w from the job's class table
+__device__ __forceinline__ double row_value_cmp(const DevModel& M, const double* __restrict__ classRho,
+                                               const double* __restrict__ x, int r) {
+  double v = classRho[M.rclass[r]];
+  const int kb = M.trnOffset[r], ke = M.trnOffset[r + 1];
+  for (int k = kb; k < ke; ++k) v = __dadd_rn(v, __dmul_rn(M.probDict[M.probIdx[k]], __ldg(x + M.succ[k])));
   return v;
 }
 
@@ -176,11 +194,12 @@ __global__ void __launch_bounds__(kBlock) k_weighted_reward(const DevModel* __re
     const int lt = t - prefix[a];
     const int s0 = M.tileStart[lt], s1 = M.tileStart[lt + 1];
     const int r0 = M.rowOffset[s0], r1 = M.rowOffset[s1];
-    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-      double acc = 0.0;
-      for (int o = 0; o < M.K; ++o) acc = __dadd_rn(acc, __dmul_rn(J.w[o], M.obj[o][r]));
-      J.rho[r] = acc;
-    }
+    if (J.rho)  // lean compact jobs keep only the class table below
+      for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        double acc = 0.0;
+        for (int o = 0; o < M.K; ++o) acc = __dadd_rn(acc, __dmul_rn(J.w[o], M.obj[o][r]));
+        J.rho[r] = acc;
+      }
     if (M.compact && lt == 0) {
       // the same rounded combination for every reward class: rho_w[r] == classRho[rclass[r]]
       for (int c = threadIdx.x; c < M.nclass; c += blockDim.x) {
@@ -1012,7 +1031,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
       const int r0 = sRow[0];
       const int nr = sRow[v.ns] - r0;
       const int nstage = min(nr, kRowCap);
-      for (int i = tid; i < nstage; i += kConsumers) sVal[i] = row_value(M.trnOffset, M.succ, M.prob, v.rho, x, r0 + i);
+      for (int i = tid; i < nstage; i += kConsumers) sVal[i] = row_value_cmp(M, v.classRho, x, r0 + i);
       consumer_sync();
       if (tid < v.ns) {
         const int s = v.s0 + tid;
@@ -1023,7 +1042,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           double best = 0.0;
           int bestRow = -1;
           for (int q = rb; q < re; ++q) {
-            const double val = q < kRowCap ? sVal[q] : row_value(M.trnOffset, M.succ, M.prob, v.rho, x, r0 + q);
+            const double val = q < kRowCap ? sVal[q] : row_value_cmp(M, v.classRho, x, r0 + q);
             if (bestRow < 0 || val > best) {
               best = val;
               bestRow = q;
@@ -1157,9 +1176,9 @@ __global__ void __launch_bounds__(kBlock) k_chain_fill(const DevModel* __restric
         const int kb = M.trnOffset[r];
         for (int q = 0; q < c; ++q) {
           J.chainSucc[off + q] = M.succ[kb + q];
-          J.chainProb[off + q] = M.prob[kb + q];
+          J.chainProb[off + q] = model_prob(M, kb + q);
         }
-        for (int o = 0; o < J.nrhs; ++o) J.rhoC[o][s] = J.rho[o][r];
+        for (int o = 0; o < J.nrhs; ++o) J.rhoC[o][s] = J.rho[o] ? J.rho[o][r] : model_obj(M, J.objIdx[o], r);
       } else {
         for (int o = 0; o < J.nrhs; ++o) J.rhoC[o][s] = 0.0;
       }
@@ -1842,6 +1861,7 @@ struct morap_ctx {
   std::vector<Graph> graphs;  // cached sweep batches
   bool useGraphs = true;
   bool useCompact = true;  // compact u8 probability / reward-class streams where possible
+  bool lean = false;       // compact models uploaded without their fp64 prob / objective arrays
   bool optCompact = false; // current optimize batch runs the deep compact pipeline
   int cmpBlocks = 0;
   bool usePersistent = true;  // evaluate batches as one cooperative launch
@@ -2285,6 +2305,8 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
       return ctx->fail(MORAP_INVALID_CONFIG, "job " + std::to_string(j) + ": unknown model id");
     if (!rhoHost && K != ctx->hm[model_ids[j]].K)
       return ctx->fail(MORAP_DIMENSION_MISMATCH, "one weight per reward structure (numerics.hpp:225)");
+    if (rhoHost && !ctx->dm[model_ids[j]].prob)
+      return ctx->fail(MORAP_INVALID_CONFIG, "lean models take weighted jobs only (no explicit reward vectors)");
   }
   // arena regions: [rho of every job][x0|x1 of every job][policy of every job] so the
   // x region is zeroed with one memset (x = y = 0 at the start, numerics.hpp:81)
@@ -2293,7 +2315,8 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   for (int j = 0; j < njobs; ++j) {
     const HostModel& m = ctx->hm[model_ids[j]];
     offRho[j] = rhoBytes;
-    rhoBytes += align_up(sizeof(double) * m.R, 256);
+    const bool lean = !ctx->dm[model_ids[j]].prob;  // lean compact model: class table only
+    if (!lean) rhoBytes += align_up(sizeof(double) * m.R, 256);
     offX[j] = xBytes;
     xBytes += 2 * align_up(sizeof(double) * m.S, 256);
     offPol[j] = polBytes;
@@ -2317,7 +2340,7 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     const HostModel& m = ctx->hm[model_ids[j]];
     OptJob& J = ctx->hOptJobs[j];
     J.model = model_ids[j];
-    J.rho = reinterpret_cast<double*>(base + offRho[j]);
+    J.rho = ctx->dm[model_ids[j]].prob ? reinterpret_cast<double*>(base + offRho[j]) : nullptr;
     J.buf[0] = reinterpret_cast<double*>(base + rhoBytes + offX[j]);
     J.buf[1] = reinterpret_cast<double*>(base + rhoBytes + offX[j] + align_up(sizeof(double) * m.S, 256));
     J.policy = reinterpret_cast<int32_t*>(base + rhoBytes + xBytes + offPol[j]);
@@ -2333,6 +2356,10 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   ctx->optCompact = ctx->useCompact && !rhoHost;
   for (int j = 0; j < njobs && ctx->optCompact; ++j)
     if (!ctx->dm[model_ids[j]].compact) ctx->optCompact = false;
+  if (!ctx->optCompact)
+    for (int j = 0; j < njobs; ++j)
+      if (!ctx->dm[model_ids[j]].prob)
+        return ctx->fail(MORAP_INVALID_CONFIG, "a batch with lean models cannot include non-compact models");
   CK(cudaMemcpyAsync(ctx->dOptJobs, ctx->hOptJobs.data(), njobs * sizeof(OptJob), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->dStatus, statusInit.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->dSweeps, zeroI.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
@@ -2721,9 +2748,10 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   for (int m = 0; m < nmodels; ++m) {
     const morap_csr_view& v = models[m];
     off[m] = bytes;
+    const bool lean = ctx->lean && compact[m].ok;
     bytes += align_up(4ull * (v.num_states + 1), 256) + align_up(4ull * (v.num_rows + 1), 256) +
-             align_up(4ull * v.nnz, 256) + align_up(8ull * v.nnz, 256) + align_up(1ull * v.num_states, 256) +
-             static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256) +
+             align_up(4ull * v.nnz, 256) + (lean ? 0 : align_up(8ull * v.nnz, 256)) + align_up(1ull * v.num_states, 256) +
+             (lean ? 0 : static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256)) +
              align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
     if (compact[m].ok)
       bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(v.num_rows, 256) +
@@ -2779,10 +2807,12 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     dmod.rowOffset = reinterpret_cast<const int32_t*>(put(v.row_offset, 4ull * (v.num_states + 1)));
     dmod.trnOffset = reinterpret_cast<const int32_t*>(put(v.trn_offset, 4ull * (v.num_rows + 1)));
     dmod.succ = reinterpret_cast<const int32_t*>(put(v.succ, 4ull * v.nnz));
-    dmod.prob = reinterpret_cast<const double*>(put(v.prob, 8ull * v.nnz));
+    const bool lean = ctx->lean && compact[m].ok;  // fp64 prob / objectives live in the tables
+    if (!lean) dmod.prob = reinterpret_cast<const double*>(put(v.prob, 8ull * v.nnz));
     dmod.done = reinterpret_cast<const uint8_t*>(put(v.done, v.num_states));
-    for (int o = 0; o < v.num_objectives; ++o)
-      dmod.obj[o] = reinterpret_cast<const double*>(put(v.rewards[o], 8ull * v.num_rows));
+    if (!lean)
+      for (int o = 0; o < v.num_objectives; ++o)
+        dmod.obj[o] = reinterpret_cast<const double*>(put(v.rewards[o], 8ull * v.num_rows));
     dmod.tileStart = reinterpret_cast<const int32_t*>(put(tiles[m].data(), 4ull * tiles[m].size()));
     dmod.tiles = reinterpret_cast<const TileDesc*>(put(descs[m].data(), sizeof(TileDesc) * descs[m].size()));
     dmod.S = v.num_states;
@@ -2965,8 +2995,11 @@ int morap_cuda_evaluate_optimized(morap_ctx* ctx, int njobs, const int32_t* opt_
     for (int o = 0; o < nrhs; ++o) {
       if (objective[o] < 0 || objective[o] >= ctx->hm[model].K)
         return ctx->fail(MORAP_DIMENSION_MISMATCH, "objective index out of range");
-      E.rho[o] = ctx->dm[model].obj[objective[o]];
+      E.rho[o] = ctx->dm[model].obj[objective[o]];  // null for lean models (class table used)
+      E.objIdx[o] = objective[o];
     }
+    if (!ctx->dm[model].obj[0] && (nrhs > kEvRhs || !ctx->useTma))
+      return ctx->fail(MORAP_INVALID_CONFIG, "lean models are evaluated through policy chains (<= 4 objectives)");
   }
   return evaluate_impl(ctx, njobs, proto, eps, sweep_cap, value_out, sweeps_out, residual_out, status_out, mask, st);
 }
@@ -3040,6 +3073,13 @@ int morap_cuda_fetch_eval_values(morap_ctx* ctx, int job, int rhs, double* out) 
   }
   CK(cudaMemcpyAsync(out, J.buf[rhs][sw & 1], 8ull * m.S, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  return MORAP_OK;
+}
+
+int morap_cuda_set_lean(morap_ctx* ctx, int on) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  if (on && !ctx->useCompact) return ctx->fail(MORAP_INVALID_CONFIG, "lean uploads need compact streams");
+  ctx->lean = on != 0;
   return MORAP_OK;
 }
 

@@ -77,7 +77,7 @@ SupportingPoint supportingPoint(const MorapInstance& inst, const Vec& w, GpuBack
       if (fresh) {
         models.push_back(gpu.modelId(p));
         for (int k = 0; k < K; ++k) weights.push_back(w[coord(k, i, j)]);
-        nnzOf.push_back(static_cast<long>(p->mdp.succ.size()));
+        nnzOf.push_back(static_cast<long>(productNnz(*p)));
       }
       jobIJ[static_cast<size_t>(i) * n + j] = it->second;
     }

@@ -59,6 +59,7 @@ def load_library(path: str = CUDA_SO) -> C.CDLL:
         "morap_cuda_evaluate": (i32, [p, i32, p, p, p, f64, i32, p, p, p, p]),
         "morap_cuda_fetch_eval_values": (i32, [p, i32, i32, p]),
         "morap_cuda_set_profiling": (i32, [p, i32]),
+        "morap_cuda_set_lean": (i32, [p, i32]),
         "morap_cuda_stats": (i32, [p, p, i32]),
         "morap_cuda_reset_stats": (i32, [p]),
         "morap_cuda_device_bytes": (i32, [p, p]),
@@ -142,6 +143,10 @@ class CudaBackend:
             self._models.append((int(np.asarray(m.rowOffset).shape[0] - 1), int(np.asarray(m.trnOffset).shape[0] - 1),
                                  len(model_objectives(m))))
         return ids
+
+    def set_lean(self, on: bool):
+        """Store compact-alphabet models without their fp64 prob/objective arrays (morap_cuda.h)."""
+        self._check(self.lib.morap_cuda_set_lean(self.h, int(on)), "set_lean")
 
     def release_models(self):
         self._check(self.lib.morap_cuda_release_models(self.h), "release")
