@@ -58,7 +58,8 @@ __device__ int g_dryRun = 0;
 struct TileDesc {
   int32_t s0, r0, k0, fits;
   int32_t wlo, wn;  // successor window: x[wlo, wlo + wn) is staged with the tile
-  int32_t pad0, pad1;
+  int32_t allIn;  // compact: every successor of the tile lies inside the window
+  int32_t pad1;
 };
 
 struct DevModel {
@@ -78,6 +79,8 @@ struct DevModel {
   const uint8_t* rclass;      // R
   const double* classTable;   // nclass x K objective tuples
   const uint16_t* succW;      // compact: successor as offset into its tile's x window, 0xFFFF outside
+  const uint16_t* relRowEnd;  // compact: rowOffset[s + 1] - tile.r0 (u16, fitting tiles)
+  const uint16_t* relTrnEnd;  // compact: trnOffset[r + 1] - tile.k0 (u16, fitting tiles)
   int32_t S, R, nnz, initial, ntiles, K, rewardFinite, compact;
   int32_t nclass, pad2;
   unsigned long long bytesPerSweep;  // algorithmic bytes of one greedy sweep
@@ -327,7 +330,10 @@ constexpr int kOffDone = kOffProb + 8 * kStProbDbls;
 constexpr int kOffX = kOffDone + kStDoneBytes;
 constexpr int kOffIdx = kOffX + 8 * kStXDbls;  // compact models: u8 probability index per transition
 constexpr int kOffCls = kOffIdx + kNnzCap + 16;  // compact models: u8 reward class per row
-constexpr int kXWin = 1024;                        // successor window of x staged per tile
+#ifndef MORAP_XWIN
+#define MORAP_XWIN 1024
+#endif
+constexpr int kXWin = MORAP_XWIN;                        // successor window of x staged per tile
 constexpr int kOffXw = kOffCls + kRowCap + 16;
 constexpr int kStageBytes = kOffXw + 8 * (kXWin + 2);
 static_assert(kStageBytes % 16 == 0 && kOffTrn % 16 == 0 && kOffRho % 16 == 0 && kOffSucc % 16 == 0 &&
@@ -364,6 +370,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "bra WAIT_%=;\n"
       "DONE_%=:\n\t}" ::"r"(smem_addr(bar)),
       "r"(parity)
+      : "memory");
+}
+
+// Same, but a waiting warp is suspended up to `kSuspendNs` per try instead of re-issuing
+// the test in a tight loop (the spin took ~20% of the compact sweep's issue slots).
+#ifndef MORAP_SUSPEND_NS
+#define MORAP_SUSPEND_NS 20000
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity), "n"(MORAP_SUSPEND_NS)
       : "memory");
 }
 
@@ -770,12 +793,14 @@ __global__ void __launch_bounds__(kTmaThreads, kStages >= 3 ? 2 : 3) k_greedy_sw
 #define MORAP_CMP_CTAS 4
 #endif
 constexpr int kCmpStages = MORAP_CMP_STAGES;
-#ifndef MORAP_CMP_FAST
-#define MORAP_CMP_FAST 0  // register-batched products per state (A/B: slower on C2)
+#ifndef MORAP_EXP
+#define MORAP_EXP 0  // timing experiments (scripts/probe_kernel.py); 0 in every shipped build
 #endif
+// stage: u16 tile-relative row ends per state and transition ends per row, u16 window
+// offsets, u8 probability index, u8 reward class, done, own x, successor window of x
 constexpr int kCOffRow = 0;
-constexpr int kCOffTrn = kCOffRow + 4 * kStRowInts;
-constexpr int kCOffSucc = kCOffTrn + 4 * kStTrnInts;
+constexpr int kCOffTrn = kCOffRow + 2 * (kBlock + 8);
+constexpr int kCOffSucc = kCOffTrn + 2 * (kRowCap + 8);
 constexpr int kCOffIdx = kCOffSucc + 2 * (kNnzCap + 8);  // u16 window offsets (+7 front misalignment)
 constexpr int kCOffCls = kCOffIdx + kNnzCap + 16;
 constexpr int kCOffDone = kCOffCls + kRowCap + 16;
@@ -790,7 +815,7 @@ constexpr int kCmpSmemBytes = kCmpStages * kCStageBytes;
 
 struct CmpInfo {
   const int32_t* succG;  // absolute successors (out-of-window transitions)
-  int t, job, fits;
+  int t, job, fits, allIn;
   int s0, r0, k0, ns;
   int offRow, offTrn, offSucc, offIdx, offCls, offDone, offX, offXw;
   int wlo, wn;
@@ -828,95 +853,136 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
   if (tid == 0) {
     for (int q = 0; q < kCmpStages; ++q) {
       mbar_init(&full[q], 1);
-      mbar_init(&empty[q], 1);
+      mbar_init(&empty[q], kConsumers / 32);  // every consumer warp releases a stage on its own
     }
     mbar_fence_init();
   }
   __syncthreads();
 
   if (tid >= kConsumers) {
-    // producer warp: lane i stages stream i of the tile
+    // Producer warp. Tile metadata is resolved 32 tiles at a time (lane l walks the
+    // prefix / list / job / model / tile tables for tile tb + l, so the chain of dependent
+    // loads is paid once per 32 tiles instead of once per tile), and each lane keeps the
+    // base pointer of "its" stream for the current job, reloaded only when the job
+    // changes. Per tile: broadcasts, one elected bookkeeping write, lane i issues the
+    // bulk copy of stream i.
     const int lane = tid & 31;
     const uint64_t pol = evict_first_policy(), polKeep = evict_last_policy();
     int ai = find_slot(prefix, nact + 1, t0);
     int use = 0;
-    auto acquire = [&](int b) {
-      if (use >= kCmpStages) mbar_wait(&empty[b], ((use / kCmpStages) - 1) & 1);
-    };
-    for (int ti = t0; ti < t1; ++ti, ++use) {
-      while (ti >= prefix[ai + 1]) ++ai;
-      const int job = list[ai];
-      const OptJob& J = jobs[job];
-      const DevModel* M = &models[J.model];
-      const int lt = ti - prefix[ai];
-      const TileDesc d = M->tiles[lt], e = M->tiles[lt + 1];
-      const int parity = POLICY ? ((jobSweeps[job] - 1) & 1) : (k & 1);
-      const int b = use % kCmpStages;
-      const double* xcur = J.buf[parity];
-      const void* src = nullptr;
-      long long lo = 0, hi = 0;
-      int es = 1, dstOff = 0;
-      uint64_t lp = pol;
-      switch (lane) {
-        case 0: src = M->rowOffset; lo = d.s0; hi = e.s0 + 1; es = 4; dstOff = kCOffRow; break;
-        case 1: src = M->trnOffset; lo = d.r0; hi = e.r0 + 1; es = 4; dstOff = kCOffTrn; break;
-        case 2: src = M->succW; lo = d.k0; hi = e.k0; es = 2; dstOff = kCOffSucc; break;
-        case 3: src = M->probIdx; lo = d.k0; hi = e.k0; es = 1; dstOff = kCOffIdx; break;
-        case 4: src = M->rclass; lo = d.r0; hi = e.r0; es = 1; dstOff = kCOffCls; break;
-        case 5: src = M->done; lo = d.s0; hi = e.s0; es = 1; dstOff = kCOffDone; break;
-        case 6:
-          if (!POLICY) { src = xcur; lo = d.s0; hi = e.s0; es = 8; dstOff = kCOffX; lp = polKeep; }
-          break;
-        case 7: src = xcur; lo = d.wlo; hi = d.wlo + d.wn; es = 8; dstOff = kCOffXw; lp = polKeep; break;
-        default: break;
+    int curJob = -1;
+    const unsigned char* myBase = nullptr;  // stream base of this lane for curJob
+    const DevModel* curM = nullptr;
+    const OptJob* curJ = nullptr;
+    int parity = k & 1;
+    for (int tb = t0; tb < t1; tb += 32) {
+      // ---- resolve tiles tb .. tb+31, one per lane -----------------------------------
+      const int tl = tb + lane;
+      int mJob = 0, mS0 = 0, mR0 = 0, mK0 = 0, mFits = 0, mWlo = 0, mWn = 0, mAll = 0, eS0 = 0, eR0 = 0, eK0 = 0;
+      if (tl < t1) {
+        int a = ai;
+        while (tl >= prefix[a + 1]) ++a;
+        mJob = list[a];
+        const int lt = tl - prefix[a];
+        const DevModel* M = &models[jobs[mJob].model];
+        const int4* tp = reinterpret_cast<const int4*>(M->tiles + lt);
+        const int4 d0 = tp[0], d1 = tp[1], e0 = tp[2];
+        mS0 = d0.x; mR0 = d0.y; mK0 = d0.z; mFits = d0.w;
+        mWlo = d1.x; mWn = d1.y; mAll = d1.z;
+        eS0 = e0.x; eR0 = e0.y; eK0 = e0.z;
       }
-      const long long a0 = (lo * es) & ~15ll, z0 = (hi * es + 15) & ~15ll;
-      const uint32_t bytes = (src && d.fits && z0 > a0) ? static_cast<uint32_t>(z0 - a0) : 0u;
-      const int off = src ? static_cast<int>((lo * es - a0) / es) : 0;
-      const uint32_t txBytes = __reduce_add_sync(0xffffffffu, bytes);
-      int offs[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) offs[q] = __shfl_sync(0xffffffffu, off, q);
-      acquire(b);
-      uint64_t* bar = &full[b];
-      if (lane == 0) {
-        CmpInfo v;
-        v.t = ti;
-        v.job = job;
-        v.fits = d.fits;
-        v.s0 = d.s0;
-        v.r0 = d.r0;
-        v.k0 = d.k0;
-        v.ns = e.s0 - d.s0;
-        v.offRow = offs[0];
-        v.offTrn = offs[1];
-        v.offSucc = offs[2];
-        v.offIdx = offs[3];
-        v.offCls = offs[4];
-        v.offDone = offs[5];
-        v.offX = offs[6];
-        v.offXw = offs[7];
-        v.wlo = d.wlo;
-        v.wn = d.wn;
-        v.dict = M->probDict;
-        v.classRho = J.classRho;
-        v.x = xcur;
-        v.y = J.buf[parity ^ 1];
-        v.policy = J.policy;
-        v.model = M;
-        v.rho = J.rho;
-        v.succG = M->succ;
-        info[b] = v;
-        if (d.fits) mbar_expect_tx(bar, txBytes);
-        else mbar_arrive(bar);
+      {  // advance ai to the slot of the last tile of the batch
+        const int last = min(t1, tb + 32) - 1;
+        while (last >= prefix[ai + 1]) ++ai;
       }
-      __syncwarp();
-      if (bytes)
-        bulk_g2s(smem + b * kCStageBytes + dstOff, static_cast<const unsigned char*>(src) + a0, bytes, bar, lp);
+      const int nb = min(32, t1 - tb);
+      for (int q = 0; q < nb; ++q, ++use) {
+        const int ti = tb + q;
+        const int job = __shfl_sync(0xffffffffu, mJob, q);
+        const int s0 = __shfl_sync(0xffffffffu, mS0, q), r0 = __shfl_sync(0xffffffffu, mR0, q);
+        const int k0 = __shfl_sync(0xffffffffu, mK0, q), fits = __shfl_sync(0xffffffffu, mFits, q);
+        const int wlo = __shfl_sync(0xffffffffu, mWlo, q), wn = __shfl_sync(0xffffffffu, mWn, q);
+        const int allIn = __shfl_sync(0xffffffffu, mAll, q);
+        const int s1 = __shfl_sync(0xffffffffu, eS0, q), r1 = __shfl_sync(0xffffffffu, eR0, q);
+        const int k1 = __shfl_sync(0xffffffffu, eK0, q);
+        if (job != curJob) {  // uniform: reload this lane's stream base for the new job
+          curJob = job;
+          curJ = &jobs[job];
+          curM = &models[curJ->model];
+          if (POLICY) parity = (jobSweeps[job] - 1) & 1;
+          const void* bp = nullptr;
+          switch (lane) {
+            case 0: bp = curM->relRowEnd; break;
+            case 1: bp = curM->relTrnEnd; break;
+            case 2: bp = curM->succW; break;
+            case 3: bp = curM->probIdx; break;
+            case 4: bp = curM->rclass; break;
+            case 5: bp = curM->done; break;
+            case 6: bp = POLICY ? nullptr : curJ->buf[parity]; break;
+            case 7: bp = curJ->buf[parity]; break;
+            default: break;
+          }
+          myBase = static_cast<const unsigned char*>(bp);
+        }
+        const int b = use % kCmpStages;
+        // stream of this lane: [lo, hi) in elements of 1 << sh bytes
+        long long lo = 0, hi = 0;
+        int sh = 0, dstOff = 0;
+        uint64_t lp = pol;
+        switch (lane) {
+          case 0: lo = s0; hi = s1; sh = 1; dstOff = kCOffRow; break;
+          case 1: lo = r0; hi = r1; sh = 1; dstOff = kCOffTrn; break;
+          case 2: lo = k0; hi = k1; sh = 1; dstOff = kCOffSucc; break;
+          case 3: lo = k0; hi = k1; sh = 0; dstOff = kCOffIdx; break;
+          case 4: lo = r0; hi = r1; sh = 0; dstOff = kCOffCls; break;
+          case 5: lo = s0; hi = s1; sh = 0; dstOff = kCOffDone; break;
+          case 6: lo = s0; hi = s1; sh = 3; dstOff = kCOffX; lp = polKeep; break;
+          case 7: lo = wlo; hi = wlo + wn; sh = 3; dstOff = kCOffXw; lp = polKeep; break;
+          default: break;
+        }
+        const long long a0 = (lo << sh) & ~15ll, z0 = ((hi << sh) + 15) & ~15ll;
+        const uint32_t bytes =
+            (myBase && fits && z0 > a0 && !(MORAP_EXP & 4)) ? static_cast<uint32_t>(z0 - a0) : 0u;
+        const int off = static_cast<int>(((lo << sh) - a0) >> sh);
+        const uint32_t txBytes = __reduce_add_sync(0xffffffffu, bytes);
+        if (use >= kCmpStages) mbar_wait_sleep(&empty[b], ((use / kCmpStages) - 1) & 1);
+        // bookkeeping for the consumers: lane i < 8 writes its stream offset, lane 0 the rest
+        CmpInfo* v = &info[b];
+        int* offSlot = &v->offRow;
+        if (lane < 8) offSlot[lane] = off;
+        if (lane == 0) {
+          v->t = ti;
+          v->job = job;
+          v->fits = fits;
+          v->allIn = allIn;
+          v->s0 = s0;
+          v->r0 = r0;
+          v->k0 = k0;
+          v->ns = s1 - s0;
+          v->wlo = wlo;
+          v->wn = wn;
+          v->dict = curM->probDict;
+          v->classRho = curJ->classRho;
+          v->x = curJ->buf[parity];
+          v->y = curJ->buf[parity ^ 1];
+          v->policy = curJ->policy;
+          v->model = curM;
+          v->rho = curJ->rho;
+          v->succG = curM->succ;
+        }
+        __syncwarp();
+        uint64_t* bar = &full[b];
+        if (lane == 0) {
+          if (fits) mbar_expect_tx(bar, txBytes);
+          else mbar_arrive(bar);
+        }
+        __syncwarp();
+        if (bytes) bulk_g2s(smem + b * kCStageBytes + dstOff, myBase + a0, bytes, bar, lp);
+      }
     }
     if (lane == 0) {
       const int b = use % kCmpStages;
-      acquire(b);
+      if (use >= kCmpStages) mbar_wait_sleep(&empty[b], ((use / kCmpStages) - 1) & 1);
       info[b].t = -1;
       mbar_arrive(&full[b]);
     }
@@ -928,9 +994,10 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
   // active-tile order, so that is a handful of times per sweep instead of once per tile).
   double runMax = 0.0;
   int runJob = -1;
+  const int lane = tid & 31;
   for (int use = 0;; ++use) {
     const int b = use % kCmpStages;
-    mbar_wait(&full[b], (use / kCmpStages) & 1);
+    mbar_wait_sleep(&full[b], (use / kCmpStages) & 1);
     const CmpInfo v = info[b];
     if (v.t < 0) break;
     if (!POLICY && v.job != runJob) {  // uniform over the consumers
@@ -944,66 +1011,55 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     double dl = 0.0;
     unsigned char* st = smem + b * kCStageBytes;
     const double* __restrict__ x = v.x;
-    if (v.fits) {
-      const int32_t* rowS = reinterpret_cast<const int32_t*>(st + kCOffRow) + v.offRow;
-      const int32_t* trnS = reinterpret_cast<const int32_t*>(st + kCOffTrn) + v.offTrn;
+    if (v.fits && g_dryRun) {
+      // diagnostics: stream only
+    } else if (v.fits) {
+      // Tile-relative u16 row / transition END offsets: state i owns rows
+      // [relRowEnd[i-1], relRowEnd[i]) (0 for i = 0), row r owns transitions
+      // [relTrnEnd[r-1], relTrnEnd[r]).
+      const uint16_t* rowE = reinterpret_cast<const uint16_t*>(st + kCOffRow) + v.offRow;
+      const uint16_t* trnE = reinterpret_cast<const uint16_t*>(st + kCOffTrn) + v.offTrn;
       const uint16_t* succS = reinterpret_cast<const uint16_t*>(st + kCOffSucc) + v.offSucc;
       const uint8_t* idxS = st + kCOffIdx + v.offIdx;
       const uint8_t* clsS = st + kCOffCls + v.offCls;
       const uint8_t* doneS = st + kCOffDone + v.offDone;
       const double* xS = reinterpret_cast<const double*>(st + kCOffX) + v.offX;
-      const double* xwS = reinterpret_cast<const double*>(st + kCOffXw) + v.offXw;
+      const double* xwS = reinterpret_cast<const double*>(st + kCOffXw);  // even wlo: no front offset
       if (tid < v.ns) {
         const int s = v.s0 + tid;
-        const int rb = rowS[tid] - v.r0, re = rowS[tid + 1] - v.r0;
+        const int rb = tid ? rowE[tid - 1] : 0, re = rowE[tid];
         if (doneS[tid]) {
           if (POLICY) v.policy[s] = v.r0 + rb;  // numerics.hpp:114-115
         } else {
           double best = 0.0;
           int bestRow = -1;
-          const int qb = trnS[rb] - v.k0, qe = trnS[re] - v.k0;
-          auto xAt = [&](int q) {  // window offset staged; absolute successor only outside it
-            const unsigned o = succS[q];
-            return o != 0xFFFFu ? xwS[o] : __ldg(x + __ldg(v.succG + v.k0 + q));
-          };
-          constexpr int kFast = 8;  // a warehouse state has <= 5 transitions over its rows
-          if (MORAP_CMP_FAST && qe - qb <= kFast) {
-            // all products of the state first (independent loads, static register slots),
-            // then the rows left to right (numerics.hpp:93-100)
-            double t[kFast];
-#pragma unroll
-            for (int q = 0; q < kFast; ++q)
-              if (q < qe - qb) t[q] = __dmul_rn(__ldg(v.dict + idxS[qb + q]), xAt(qb + q));
-            int r = rb;
-            int rowEnd = trnS[rb + 1] - v.k0 - qb;
-            double acc = __ldg(v.classRho + clsS[rb]);
-#pragma unroll
-            for (int q = 0; q < kFast; ++q) {
-              if (q < qe - qb) {
-                while (q >= rowEnd) {  // close row r (rows may be empty)
-                  if (bestRow < 0 || acc > best) {
-                    best = acc;
-                    bestRow = r;
-                  }
-                  ++r;
-                  acc = __ldg(v.classRho + clsS[r]);
-                  rowEnd = trnS[r + 1] - v.k0 - qb;
-                }
-                acc = __dadd_rn(acc, t[q]);
-              }
-            }
-            for (;;) {  // close the last non-empty row and any trailing empty rows
+          int kb = rb ? trnE[rb - 1] : 0;
+          if (v.allIn) {  // every successor inside the staged window: no out-of-window test
+            const double* __restrict__ dict = v.dict;
+            const double* __restrict__ crho = v.classRho;
+#pragma unroll 1
+            for (int r = rb; r < re; ++r) {
+              const int ke = trnE[r];
+              double acc = __ldg(crho + clsS[r]);
+              // warehouse rows carry 1 or 2 transitions: straight-line for those, loop after
+              if (kb < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[kb]), xwS[succS[kb]]));
+              if (kb + 1 < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[kb + 1]), xwS[succS[kb + 1]]));
+#pragma unroll 1
+              for (int q = kb + 2; q < ke; ++q)
+                acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[q]), xwS[succS[q]]));
+              kb = ke;
               if (bestRow < 0 || acc > best) {
                 best = acc;
                 bestRow = r;
               }
-              if (++r >= re) break;
-              acc = __ldg(v.classRho + clsS[r]);
             }
           } else {
-            int kb = qb;
+            auto xAt = [&](int q) {  // window offset staged; absolute successor only outside it
+              const unsigned o = succS[q];
+              return o != 0xFFFFu ? xwS[o] : __ldg(x + __ldg(v.succG + v.k0 + q));
+            };
             for (int r = rb; r < re; ++r) {
-              const int ke = trnS[r + 1] - v.k0;
+              const int ke = trnE[r];
               double acc = __ldg(v.classRho + clsS[r]);
               for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(v.dict + idxS[q]), xAt(q)));
               kb = ke;
@@ -1058,8 +1114,8 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
       }
     }
     runMax = fmax(runMax, dl);
-    consumer_sync();  // every consumer is done with stage b
-    if (tid == 0) mbar_arrive(&empty[b]);
+    __syncwarp();  // this warp is done with stage b (warps drift apart up to the pipeline depth)
+    if (lane == 0) mbar_arrive(&empty[b]);
   }
   if (!POLICY && runJob >= 0) {  // residual of the last job of this CTA's range
     runMax = consumer_max(runMax, sRed);
@@ -1932,6 +1988,7 @@ void successor_window(const morap_csr_view& v, int k0, int k1, int32_t& wlo, int
   wn = std::min(kXWin, v.num_states);
   if (k1 <= k0) {
     wlo = 0;
+    wn = 0;
     return;
   }
   // histogram of successors in 64-state bins over [min, max], then the best run of
@@ -1941,8 +1998,10 @@ void successor_window(const morap_csr_view& v, int k0, int k1, int32_t& wlo, int
     lo = std::min(lo, v.succ[k]);
     hi = std::max(hi, v.succ[k]);
   }
-  if (hi - lo < wn) {
-    wlo = std::max(0, std::min(lo, v.num_states - wn));
+  // windows start at an even state, so the 16-byte aligned window copy lands at offset 0
+  if (hi - lo < wn) {  // the whole successor range fits: stage just that range
+    wlo = lo & ~1;
+    wn = hi - wlo + 1;
     return;
   }
   constexpr int kBin = 64;
@@ -1959,7 +2018,7 @@ void successor_window(const morap_csr_view& v, int k0, int k1, int32_t& wlo, int
       bestBin = std::max(0, i - span + 1);
     }
   }
-  wlo = std::max(0, std::min(lo + bestBin * kBin, v.num_states - wn));
+  wlo = std::max(0, std::min(lo + bestBin * kBin, v.num_states - wn)) & ~1;
 }
 
 void make_tiles(const morap_csr_view& v, std::vector<int32_t>& out, std::vector<TileDesc>& desc) {
@@ -1992,16 +2051,28 @@ struct CompactStream {
   std::vector<uint8_t> idx, cls;
   std::vector<double> dict, table;
   std::vector<uint16_t> succW;  // successor window offsets (needs the tile table)
+  std::vector<uint16_t> relRowEnd, relTrnEnd;  // tile-relative row / transition ends
 };
 
 // succW[k] = succ[k] - wlo of k's tile when inside the tile's x window, else 0xFFFF
-void build_window_offsets(const morap_csr_view& v, const std::vector<TileDesc>& desc, CompactStream& c) {
+void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, CompactStream& c) {
   c.succW.resize(static_cast<size_t>(v.nnz));
+  c.relRowEnd.resize(static_cast<size_t>(v.num_states));
+  c.relTrnEnd.resize(static_cast<size_t>(v.num_rows));
   for (size_t t = 0; t + 1 < desc.size(); ++t) {
-    const TileDesc& d = desc[t];
+    TileDesc& d = desc[t];
+    const TileDesc& e = desc[t + 1];
+    // u16 ends are only read for fitting tiles (<= kRowCap rows, <= kNnzCap transitions)
+    for (int q = d.s0; q < e.s0; ++q)
+      c.relRowEnd[q] = static_cast<uint16_t>(std::min(v.row_offset[q + 1] - d.r0, 0xFFFF));
+    for (int r = d.r0; r < e.r0; ++r)
+      c.relTrnEnd[r] = static_cast<uint16_t>(std::min(v.trn_offset[r + 1] - d.k0, 0xFFFF));
+    d.allIn = 1;
     for (int k = d.k0; k < desc[t + 1].k0; ++k) {
       const unsigned o = static_cast<unsigned>(v.succ[k] - d.wlo);
-      c.succW[k] = o < static_cast<unsigned>(d.wn) ? static_cast<uint16_t>(o) : static_cast<uint16_t>(0xFFFF);
+      const bool in = o < static_cast<unsigned>(d.wn);
+      c.succW[k] = in ? static_cast<uint16_t>(o) : static_cast<uint16_t>(0xFFFF);
+      if (!in) d.allIn = 0;
     }
   }
 }
@@ -2755,7 +2826,8 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
              align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
     if (compact[m].ok)
       bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(v.num_rows, 256) +
-               align_up(8ull * compact[m].table.size(), 256) + align_up(2ull * v.nnz, 256);
+               align_up(8ull * compact[m].table.size(), 256) + align_up(2ull * v.nnz, 256) +
+               align_up(2ull * v.num_states, 256) + align_up(2ull * v.num_rows, 256);
   }
   void* dev = nullptr;
   {
@@ -2834,9 +2906,11 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
       dmod.classTable = reinterpret_cast<const double*>(put(c.table.data(), 8ull * c.table.size()));
       dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
       dmod.succW = reinterpret_cast<const uint16_t*>(put(c.succW.data(), 2ull * c.succW.size()));
-      // compact stream: window offset 2 + prob index 1 per nnz; trnOffset 4 + class 1 per
-      // row; rowOffset 4 + done 1 + x 8 + y 8 per state
-      dmod.bytesPerSweep = 3ull * v.nnz + 5ull * v.num_rows + 21ull * v.num_states;
+      dmod.relRowEnd = reinterpret_cast<const uint16_t*>(put(c.relRowEnd.data(), 2ull * c.relRowEnd.size()));
+      dmod.relTrnEnd = reinterpret_cast<const uint16_t*>(put(c.relTrnEnd.data(), 2ull * c.relTrnEnd.size()));
+      // compact stream: window offset 2 + prob index 1 per nnz; relative transition end 2 +
+      // class 1 per row; relative row end 2 + done 1 + x 8 + y 8 per state
+      dmod.bytesPerSweep = 3ull * v.nnz + 3ull * v.num_rows + 19ull * v.num_states;
     }
     // evaluate, one RHS over the policy chain: chainOff 4 + done 1 + rhoC 8 + x 8 + y 8 per
     // state + 12 per chosen transition (mean nnz per row)
