@@ -793,6 +793,9 @@ __global__ void __launch_bounds__(kTmaThreads, kStages >= 3 ? 2 : 3) k_greedy_sw
 #define MORAP_CMP_CTAS 4
 #endif
 constexpr int kCmpStages = MORAP_CMP_STAGES;
+#ifndef MORAP_CMP_WAITER
+#define MORAP_CMP_WAITER 0  // A/B: one polling warp + named barrier was 7% slower (C2)
+#endif
 #ifndef MORAP_EXP
 #define MORAP_EXP 0  // timing experiments (scripts/probe_kernel.py); 0 in every shipped build
 #endif
@@ -810,7 +813,7 @@ constexpr int kCStageBytes = kCOffXw + 8 * (kXWin + 2);
 static_assert(kCOffTrn % 16 == 0 && kCOffSucc % 16 == 0 && kCOffIdx % 16 == 0 && kCOffCls % 16 == 0 &&
                   kCOffDone % 16 == 0 && kCOffX % 16 == 0 && kCOffXw % 16 == 0 && kCStageBytes % 16 == 0,
               "compact stage regions must be 16-byte aligned");
-static_assert(8 * (kXWin + 2) >= 8 * kRowCap, "fallback row values reuse the window region");
+constexpr int kCFbRows = kXWin + 2 < kRowCap ? kXWin + 2 : kRowCap;  // fallback row values in the window region
 constexpr int kCmpSmemBytes = kCmpStages * kCStageBytes;
 
 struct CmpInfo {
@@ -997,7 +1000,15 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
   const int lane = tid & 31;
   for (int use = 0;; ++use) {
     const int b = use % kCmpStages;
+#if MORAP_CMP_WAITER
+    // one consumer warp polls the stage barrier, the other seven park on a named barrier
+    // (no issue slots burnt spinning), then observe the completed phase themselves
+    if (tid < 32) mbar_wait(&full[b], (use / kCmpStages) & 1);
+    asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
+    if (tid >= 32) mbar_wait(&full[b], (use / kCmpStages) & 1);
+#else
     mbar_wait_sleep(&full[b], (use / kCmpStages) & 1);
+#endif
     const CmpInfo v = info[b];
     if (v.t < 0) break;
     if (!POLICY && v.job != runJob) {  // uniform over the consumers
@@ -1086,7 +1097,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
       consumer_sync();
       const int r0 = sRow[0];
       const int nr = sRow[v.ns] - r0;
-      const int nstage = min(nr, kRowCap);
+      const int nstage = min(nr, kCFbRows);
       for (int i = tid; i < nstage; i += kConsumers) sVal[i] = row_value_cmp(M, v.classRho, x, r0 + i);
       consumer_sync();
       if (tid < v.ns) {
@@ -1098,7 +1109,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           double best = 0.0;
           int bestRow = -1;
           for (int q = rb; q < re; ++q) {
-            const double val = q < kRowCap ? sVal[q] : row_value_cmp(M, v.classRho, x, r0 + q);
+            const double val = q < kCFbRows ? sVal[q] : row_value_cmp(M, v.classRho, x, r0 + q);
             if (bestRow < 0 || val > best) {
               best = val;
               bestRow = q;
