@@ -7,6 +7,8 @@
 // the library error code, results independent of how jobs are batched -- but executes
 // each kind of job as a single device batch instead of a CPU worker pool.
 #include <cstring>
+#include <malloc.h>
+#include <mutex>
 #include <set>
 
 #include "morap.hpp"
@@ -53,7 +55,22 @@ morap_csr_view viewOf(const ProductMdp& p, const std::vector<const double*>& obj
 
 }  // namespace
 
+namespace {
+// Every Pareto iteration keeps n fresh scheduler vectors (IterationRecord::schedulers,
+// ~0.3 MB each on C2). With glibc's defaults those come from fresh mmaps and are
+// page-faulted in on every iteration (~1 ms per C2 iteration); keeping large blocks on
+// the heap lets later queries reuse the pages.
+void keepLargeBlocksOnHeap() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    mallopt(M_MMAP_THRESHOLD, 256 << 20);
+    mallopt(M_TRIM_THRESHOLD, 1 << 30);
+  });
+}
+}  // namespace
+
 GpuBackend::GpuBackend(int device) : device_(device) {
+  keepLargeBlocksOnHeap();
   const int rc = morap_cuda_create(device, &ctx_);
   if (rc != MORAP_OK) {
     ctx_ = nullptr;

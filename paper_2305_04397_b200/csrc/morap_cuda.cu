@@ -31,6 +31,7 @@
 #include <cmath>
 #include <thread>
 #include <cstdint>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1859,6 +1860,7 @@ struct morap_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
   bool profiling = false;
+  bool trace = std::getenv("MORAP_TRACE") != nullptr;
   double stats[9] = {0};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
@@ -2394,11 +2396,15 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   // x region is zeroed with one memset (x = y = 0 at the start, numerics.hpp:81)
   size_t rhoBytes = 0, xBytes = 0, polBytes = 0;
   std::vector<size_t> offRho(njobs), offX(njobs), offPol(njobs);
+  // compact sweeps read rho_w per reward class only: no per-row rho vector then
+  bool allCompact = ctx->useCompact && ctx->useTma && !rhoHost;
+  for (int j = 0; j < njobs && allCompact; ++j)
+    if (!ctx->dm[model_ids[j]].compact) allCompact = false;
   for (int j = 0; j < njobs; ++j) {
     const HostModel& m = ctx->hm[model_ids[j]];
     offRho[j] = rhoBytes;
     const bool lean = !ctx->dm[model_ids[j]].prob;  // lean compact model: class table only
-    if (!lean) rhoBytes += align_up(sizeof(double) * m.R, 256);
+    if (!lean && !allCompact) rhoBytes += align_up(sizeof(double) * m.R, 256);
     offX[j] = xBytes;
     xBytes += 2 * align_up(sizeof(double) * m.S, 256);
     offPol[j] = polBytes;
@@ -2422,7 +2428,7 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     const HostModel& m = ctx->hm[model_ids[j]];
     OptJob& J = ctx->hOptJobs[j];
     J.model = model_ids[j];
-    J.rho = ctx->dm[model_ids[j]].prob ? reinterpret_cast<double*>(base + offRho[j]) : nullptr;
+    J.rho = (ctx->dm[model_ids[j]].prob && !allCompact) ? reinterpret_cast<double*>(base + offRho[j]) : nullptr;
     J.buf[0] = reinterpret_cast<double*>(base + rhoBytes + offX[j]);
     J.buf[1] = reinterpret_cast<double*>(base + rhoBytes + offX[j] + align_up(sizeof(double) * m.S, 256));
     J.policy = reinterpret_cast<int32_t*>(base + rhoBytes + xBytes + offPol[j]);
@@ -2435,9 +2441,7 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     else active.push_back(j);
   }
   CK(cudaMemsetAsync(base + rhoBytes, 0, xBytes, ctx->stream));
-  ctx->optCompact = ctx->useCompact && !rhoHost;
-  for (int j = 0; j < njobs && ctx->optCompact; ++j)
-    if (!ctx->dm[model_ids[j]].compact) ctx->optCompact = false;
+  ctx->optCompact = allCompact;
   if (!ctx->optCompact)
     for (int j = 0; j < njobs; ++j)
       if (!ctx->dm[model_ids[j]].prob)
@@ -2625,6 +2629,14 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
   CK(cudaMemsetAsync(ctx->dDelta, 0, njobs * MORAP_MAX_RHS * sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->dResidual, 0, njobs * MORAP_MAX_RHS * sizeof(double), ctx->stream));
   if ((rc = init_ctl(ctx, active, jobModel))) return rc;
+  const auto tq0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!ctx->trace) return;
+    cudaStreamSynchronize(ctx->stream);
+    std::fprintf(stderr, "[morap] evaluate_impl: %s at %.3f ms\n", what,
+                 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tq0).count());
+  };
+  lap("setup");
   ctx->evalTma = tmaOk;
   if (tmaOk && !active.empty()) {
     // policy chains of the active jobs (count, per-job scan, fill)
@@ -2638,6 +2650,7 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
     CK(cudaGetLastError());
     ctx->stats[8] += 3;
   }
+  lap("chains");
   if (!active.empty()) {
     if (tmaOk && ctx->usePersistent && njobs <= kPersistMaxJobs) {
       if ((rc = run_eval_persistent(ctx, njobs, eps, cap))) return rc;
@@ -2646,6 +2659,7 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
     }
   }
 
+  lap("sweeps");
   ctx->evalSweeps.assign(static_cast<size_t>(njobs) * MORAP_MAX_RHS, 0);
   std::vector<int32_t> st(static_cast<size_t>(njobs) * MORAP_MAX_RHS);
   std::vector<double> res(static_cast<size_t>(njobs) * MORAP_MAX_RHS);
@@ -3064,8 +3078,15 @@ int morap_cuda_evaluate_optimized(morap_ctx* ctx, int njobs, const int32_t* opt_
   for (int j : jl)
     if (ctx->optSweeps[j] <= 0 || ctx->optStatus[j] != MORAP_OK)
       return ctx->fail(ctx->optStatus[j] ? ctx->optStatus[j] : MORAP_SOLVER_FAILURE, "optimize job failed");
+  const bool trace = ctx->trace;
+  const auto tp0 = std::chrono::steady_clock::now();
   int rc = extract_policies(ctx, jl);
   if (rc) return rc;
+  if (trace) {
+    cudaStreamSynchronize(ctx->stream);
+    std::fprintf(stderr, "[morap] evaluate_optimized: policies %.3f ms\n",
+                 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count());
+  }
   std::vector<EvalJob> proto(njobs);
   std::vector<uint32_t> mask(njobs, (1u << nrhs) - 1u);
   std::vector<int32_t> st(static_cast<size_t>(njobs) * MORAP_MAX_RHS, MORAP_OK);

@@ -116,6 +116,7 @@ SupportingPoint supportingPoint(const MorapInstance& inst, const Vec& w, GpuBack
   ck(ctx, morap_cuda_evaluate_optimized(ctx, n, evalJobs.data(), K, objectives.data(), 1e-6, 100000, ev.data(),
                                         esw.data(), eres.data(), est.data()),
      "evaluate batch");
+  const auto t2b = std::chrono::steady_clock::now();
   if (stats) stats->evaluateSweepSeconds += seconds(t2);
   out.r.assign(static_cast<size_t>(K) * n, 0.0);
   out.schedulers.resize(static_cast<size_t>(n));
@@ -135,11 +136,12 @@ SupportingPoint supportingPoint(const MorapInstance& inst, const Vec& w, GpuBack
   const auto t3 = std::chrono::steady_clock::now();
   ck(ctx, morap_cuda_fetch_policies(ctx, n, evalJobs.data(), rowsOut.data()), "fetch policies");
   if (std::getenv("MORAP_TRACE"))
-    std::fprintf(stderr, "[morap] supportingPoint: optimize %.3f ms (%d jobs), assign %.3f ms, evaluate %.3f ms, "
-                         "policies %.3f ms\n",
+    std::fprintf(stderr, "[morap] supportingPoint: optimize %.3f ms (%d jobs), assign %.3f ms, evaluate %.3f ms "
+                         "(device batch %.3f ms), policies %.3f ms\n",
                  1e3 * std::chrono::duration<double>(t1 - t0).count(), nj,
                  1e3 * std::chrono::duration<double>(t2 - t1).count(),
-                 1e3 * std::chrono::duration<double>(t3 - t2).count(), 1e3 * seconds(t3));
+                 1e3 * std::chrono::duration<double>(t3 - t2).count(),
+                 1e3 * std::chrono::duration<double>(t2b - t2).count(), 1e3 * seconds(t3));
   if (stats) {
     stats->evaluateJobs += static_cast<long>(n) * K;
     for (int j = 0; j < n; ++j)
