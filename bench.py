@@ -13,8 +13,9 @@ generator (warehouse.hpp:176), built on the host before timing.
   value    nnz backups of the query / device time of the query, products resident in HBM
   e2e      the same metric through the host API with HOST buffers: every step uploads the
            instance's product CSR (H2D) and reads back values/policies (D2H)
-  roofline dominant kernel k_greedy_sweep: algorithmic bytes (12 nnz + 12 R + 21 S per
-           active job per sweep) / its CUDA-event time over the timed steps
+  roofline dominant kernel k_greedy_sweep_cmp (compact streams): algorithmic bytes
+           (3 nnz + 3 R + 19 S per active job per sweep) / its CUDA-event time
+           over a second pass of the timed steps; traffic from the committed ncu capture
   cpu_baseline  the reference's own engine (oracle/_ref, runBatch over all host threads)
            on one optimize phase of the same instance
 
@@ -136,10 +137,11 @@ def peak_hbm():
 
 
 def ncu_traffic():
+    """DRAM bytes / algorithmic bytes of one sweep launch from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get("dram_bytes_per_launch"), d
+        return d.get("traffic_over_algorithmic"), d
     return None, None
 
 
@@ -324,7 +326,11 @@ def run_ours(args):
 
     peak, peak_src = peak_hbm()
     achieved = cs["opt_bytes"] / (cs["opt_ms"] * 1e-3) / 1e9 if cs["opt_ms"] > 0 else None
-    traffic, traffic_src = ncu_traffic()
+    ratio, traffic_src = ncu_traffic()
+    alg_per_launch = cs["opt_bytes"] / max(cs["opt_launches"], 1)
+    # ncu's dram bytes of the captured launch, scaled to this run's mean launch by the
+    # captured launch's traffic / algorithmic ratio (the kernel and layout are the same)
+    traffic = ratio * alg_per_launch if ratio else None
     first = reports[0]
     iters = len(first["iterations"])
     cpu = None if args.no_cpu_baseline else cpu_baseline(cfg, cfg["n"]) if K == 2 else None
@@ -342,12 +348,12 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": ("k_greedy_sweep_tma" if os.environ.get("MORAP_COMPACT") == "0" else "k_greedy_sweep_cmp"), "launches": cs["opt_launches"],
-                     "traffic_over_algorithmic": (traffic_src or {}).get("dram_bytes_per_launch", 0) / (traffic_src or {}).get("algorithmic_bytes_per_launch", 1) if traffic_src else None,
+                     "traffic_over_algorithmic": ratio,
                      "avg_launch_us": 1e3 * cs["opt_ms"] / max(cs["opt_launches"], 1),
-                     "algorithmic_bytes_per_launch": cs["opt_bytes"] / max(cs["opt_launches"], 1),
+                     "algorithmic_bytes_per_launch": alg_per_launch,
                      "kernel_backups_per_s": cs["opt_backups"] / (cs["opt_ms"] * 1e-3) if cs["opt_ms"] else None,
                      "peak_source": peak_src, "traffic_source": traffic_src and traffic_src.get("source"),
-                     "timing": f"CUDA events around every k_greedy_sweep_tma launch over a second pass of the "
+                     "timing": f"CUDA events around every sweep launch over a second pass of the "
                                f"{args.steps} timed steps ({prof_ms / args.steps:.1f} ms per query with the events)",
                      "share_of_step": cs["opt_ms"] / prof_ms if prof_ms else None},
         "cpu_baseline": cpu,

@@ -2823,6 +2823,12 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   std::vector<int> status(nmodels, MORAP_OK);
   std::vector<std::string> why(nmodels);
   std::vector<CompactStream> compact(nmodels);
+  const auto tu0 = std::chrono::steady_clock::now();
+  auto lapU = [&](const char* what) {
+    if (ctx->trace)
+      std::fprintf(stderr, "[morap] upload %d models: %s at %.3f ms\n", nmodels, what,
+                   1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tu0).count());
+  };
   parallel_for(nmodels, [&](int m) {
     morap_ctx scratch;  // per-model error text
     status[m] = validate_view(&scratch, models[m], m);
@@ -2838,6 +2844,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   });
   for (int m = 0; m < nmodels; ++m)
     if (status[m]) return ctx->fail(status[m], why[m]);
+  lapU("validated, tiled, compacted");
   // pack every array of the batch into one device allocation
   size_t bytes = 0;
   std::vector<size_t> off(nmodels);
@@ -2955,8 +2962,10 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     ctx->hm.push_back(HostModel{dmod.S, dmod.R, dmod.nnz, dmod.initial, dmod.ntiles, dmod.K, dmod.rewardFinite});
     if (ids_out) ids_out[m] = first + m;
   }
+  lapU("packed, copies queued");
   cudaError_t e = copyFailed ? cudaErrorUnknown : cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return ctx->cudaFail(e, "upload copy", __LINE__);
+  lapU("copied");
   if ((rc = upload_models_table(ctx))) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
   return MORAP_OK;

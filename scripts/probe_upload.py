@@ -5,6 +5,8 @@ from paper_2305_04397_b200.api import Instance, Solver
 from tests.helpers import warehouse_config
 inst = Instance.warehouse(warehouse_config(10, 10, 10))
 s = Solver(0)
+if len(sys.argv) > 1 and sys.argv[1] == "lean":
+    s.set_lean(True)
 thr = [-20.0] * 10 + [0.99] * 10
 for rep in range(4):
     t0 = time.perf_counter(); s.release(); t1 = time.perf_counter(); s.upload(inst); t2 = time.perf_counter()
