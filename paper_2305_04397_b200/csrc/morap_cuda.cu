@@ -1495,7 +1495,17 @@ struct PersistArgs {
   unsigned* barGen;
 };
 
-__global__ void __launch_bounds__(kBlock) k_eval_persistent(PersistArgs A) {
+#ifndef MORAP_PERSIST_THREADS
+#define MORAP_PERSIST_THREADS 1024
+#endif
+#ifndef MORAP_PERSIST_MINB
+#define MORAP_PERSIST_MINB (1024 / MORAP_PERSIST_THREADS)  // 64 registers: 1024 threads per SM
+#endif
+constexpr int kPersistThreads = MORAP_PERSIST_THREADS;
+// Only reached with <= kEvRhs RHS per job (the policy-chain path), so the per-thread
+// residual accumulators are kEvRhs wide; done states carry an empty chain and rhoC = 0,
+// so they compute y = 0 + 1.0 * 0 = +0.0, the pinned value, without a branch.
+__global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_persistent(PersistArgs A) {
   __shared__ uint32_t sMask[kPersistMaxJobs];
   __shared__ unsigned long long sDelta[kPersistJobs * MORAP_MAX_RHS];
   __shared__ int sActive;
@@ -1524,15 +1534,15 @@ __global__ void __launch_bounds__(kBlock) k_eval_persistent(PersistArgs A) {
     __syncthreads();
     int j = jBase;
     // per-thread running residual of the current job, flushed when the job changes
-    double run[MORAP_MAX_RHS];
+    double run[kEvRhs];
 #pragma unroll
-    for (int o = 0; o < MORAP_MAX_RHS; ++o) run[o] = 0.0;
+    for (int o = 0; o < kEvRhs; ++o) run[o] = 0.0;
     int runJob = -1;
     auto flush = [&]() {
       if (runJob < 0) return;
       const int rel = runJob - jBase;
 #pragma unroll
-      for (int o = 0; o < MORAP_MAX_RHS; ++o) {
+      for (int o = 0; o < kEvRhs; ++o) {
         if (run[o] > 0.0) {
           const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(run[o]));
           if (rel < kPersistJobs) atomicMax(&sDelta[rel * MORAP_MAX_RHS + o], bits);
@@ -1541,28 +1551,78 @@ __global__ void __launch_bounds__(kBlock) k_eval_persistent(PersistArgs A) {
         run[o] = 0.0;
       }
     };
-    for (long long i = i0 + tid; i < i1; i += blockDim.x) {
-      while (i >= A.statePrefix[j + 1]) ++j;
-      const uint32_t mk = sMask[j];
-      if (!mk) continue;
-      if (j != runJob) {
-        flush();
-        runJob = j;
-      }
-      const EvalJob& J = A.jobs[j];
-      const DevModel& M = A.models[J.model];
-      const int s = static_cast<int>(i - A.statePrefix[j]);
-      if (M.done[s]) continue;
-      const int cb = __ldg(J.chainOff + s), ce = __ldg(J.chainOff + s + 1);
+    // two states per thread per step, their loads issued together (the chain is
+    // chainOff -> chainSucc -> x: three dependent L2 round trips per state)
+    const long long bd = blockDim.x;
+    for (long long ib = i0 + tid; ib < i1; ib += 2 * bd) {
+      int jj[2], sv[2], cb[2], n[2];
+      uint32_t mk[2];
+      int sc0[2], sc1[2];
+      double p0[2], p1[2];
 #pragma unroll
-      for (int o = 0; o < MORAP_MAX_RHS; ++o) {
-        if (o >= J.nrhs || !(mk >> o & 1u)) continue;
-        const double* x = J.buf[o][parity];
-        double acc = __ldg(J.rhoC[o] + s);
-        for (int q = cb; q < ce; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(J.chainProb + q), __ldcg(x + __ldg(J.chainSucc + q))));
-        const double v = __dadd_rn(0.0, __dmul_rn(1.0, acc));
-        J.buf[o][parity ^ 1][s] = v;
-        run[o] = fmax(run[o], fabs(__dsub_rn(v, __ldcg(x + s))));
+      for (int u = 0; u < 2; ++u) {
+        const long long i = ib + u * bd;
+        mk[u] = 0u;
+        jj[u] = j;
+        sv[u] = 0;
+        if (i < i1) {
+          while (i >= A.statePrefix[j + 1]) ++j;
+          jj[u] = j;
+          mk[u] = sMask[j];
+          sv[u] = static_cast<int>(i - A.statePrefix[j]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        cb[u] = 0;
+        n[u] = 0;
+        if (mk[u]) {
+          const EvalJob& J = A.jobs[jj[u]];
+          cb[u] = __ldg(J.chainOff + sv[u]);
+          n[u] = __ldg(J.chainOff + sv[u] + 1) - cb[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        sc0[u] = sc1[u] = 0;
+        p0[u] = p1[u] = 0.0;
+        if (mk[u]) {
+          const EvalJob& J = A.jobs[jj[u]];
+          if (n[u] > 0) {
+            sc0[u] = __ldg(J.chainSucc + cb[u]);
+            p0[u] = __ldg(J.chainProb + cb[u]);
+          }
+          if (n[u] > 1) {
+            sc1[u] = __ldg(J.chainSucc + cb[u] + 1);
+            p1[u] = __ldg(J.chainProb + cb[u] + 1);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!mk[u]) continue;
+        if (jj[u] != runJob) {
+          flush();
+          runJob = jj[u];
+        }
+        const EvalJob& J = A.jobs[jj[u]];
+        const int st = sv[u];
+#pragma unroll
+        for (int o = 0; o < kEvRhs; ++o) {
+          if (o >= J.nrhs || !(mk[u] >> o & 1u)) continue;
+          const double* x = J.buf[o][parity];
+          double acc = __ldg(J.rhoC[o] + st);
+          const double x0 = n[u] > 0 ? __ldcg(x + sc0[u]) : 0.0;
+          const double x1 = n[u] > 1 ? __ldcg(x + sc1[u]) : 0.0;
+          const double xs = __ldcg(x + st);
+          if (n[u] > 0) acc = __dadd_rn(acc, __dmul_rn(p0[u], x0));
+          if (n[u] > 1) acc = __dadd_rn(acc, __dmul_rn(p1[u], x1));
+          for (int q = cb[u] + 2; q < cb[u] + n[u]; ++q)
+            acc = __dadd_rn(acc, __dmul_rn(__ldg(J.chainProb + q), __ldcg(x + __ldg(J.chainSucc + q))));
+          const double v = __dadd_rn(0.0, __dmul_rn(1.0, acc));
+          J.buf[o][parity ^ 1][st] = v;
+          run[o] = fmax(run[o], fabs(__dsub_rn(v, xs)));
+        }
       }
     }
     flush();
@@ -2554,7 +2614,7 @@ int run_eval_persistent(morap_ctx* ctx, int njobs, double eps, int cap) {
   void* args[] = {&a};
   const bool timed = ctx->profiling;
   if (timed) CK(cudaEventRecord(ctx->ev0, ctx->stream));
-  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_eval_persistent), dim3(ctx->persistBlocks), dim3(kBlock),
+  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_eval_persistent), dim3(ctx->persistBlocks), dim3(kPersistThreads),
                                  args, 0, ctx->stream));
   if (timed) CK(cudaEventRecord(ctx->ev1, ctx->stream));
   ctx->stats[8] += 1;
@@ -2733,10 +2793,12 @@ int morap_cuda_create(int device, morap_ctx** out) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occC, k_greedy_sweep_cmp<false>, kTmaThreads, kCmpSmemBytes);
   ctx->cmpBlocks = ctx->numSMs * std::max(1, occC);
   int occP = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occP, k_eval_persistent, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occP, k_eval_persistent, kPersistThreads, 0);
   int coop = 0;
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
-  ctx->persistBlocks = ctx->numSMs * std::max(1, std::min(occP, 4));
+  int persistPerSm = std::max(1, occP);
+  if (const char* pc = std::getenv("MORAP_PERSIST_CTAS")) persistPerSm = std::max(1, std::min(occP, std::atoi(pc)));
+  ctx->persistBlocks = ctx->numSMs * persistPerSm;
   const char* psel = std::getenv("MORAP_PERSISTENT");  // "0" keeps per-sweep launches (A/B)
   ctx->usePersistent = coop && occP > 0 && !(psel && std::string(psel) == "0");
   if (cudaMalloc(&ctx->dBar, 2 * sizeof(unsigned)) != cudaSuccess || cudaMemset(ctx->dBar, 0, 2 * sizeof(unsigned)) != cudaSuccess)
