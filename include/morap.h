@@ -98,6 +98,23 @@ typedef int (*morap_query_fn)(void* user, const double* w, int d, double* r_out,
 int morap_pareto_core(const double* expanded_thresholds, int d, int n, const double* norm, double eps,
                       int iteration_cap, int verify, morap_query_fn query, void* user, char* json_out, int json_cap);
 
+/* Centralised model (centralised.hpp): buildCentralised (:54-179) with its state guard
+ * (MORAP_SIZE_GUARD beyond it), the model's arrays, and centralisedParetoPoint (:216-222)
+ * -- one weighted optimize job on the whole model per iteration plus the fused evaluation
+ * of its scheduler under the 2n objectives, on the solver's GPU. Thresholds as for
+ * morap_pareto (n costs, then the real tasks' probabilities); the report has the same
+ * fields (records carry the single centralised scheduler's hash). */
+typedef struct morap_centralised morap_centralised;
+int morap_centralised_build(const morap_instance* inst, int64_t state_guard, morap_centralised** out);
+void morap_centralised_free(morap_centralised* c);
+/* out[6] = {S, R, nnz, initial, rewardFinite, number of objectives (2n)} */
+int morap_centralised_info(const morap_centralised* c, int64_t* out);
+int morap_centralised_export(const morap_centralised* c, int32_t* row_offset, int32_t* trn_offset, int32_t* succ,
+                             double* prob, uint8_t* done, double* const* rewards);
+int morap_centralised_pareto(morap_solver* s, const morap_centralised* c, const double* thresholds, int nt,
+                             const double* norm, double eps, int iteration_cap, char* json_out, int json_cap,
+                             double* stats_out);
+
 /* maxAssignment (assignment.hpp:54): agent_of[j] for the n x n row-major value matrix. */
 int morap_max_assignment(int n, const double* c, int32_t* agent_of);
 

@@ -231,6 +231,35 @@ class RefInstance:
         return out
 
 
+    # ---- centralised model (centralised.hpp) ------------------------------------------
+    def centralised_dims(self, guard=10000000):
+        dims = np.zeros(6, np.int64)
+        self._check(self._lib.ref_centralised_dims(self._h, guard, dims.ctypes.data_as(C.c_void_p)))
+        return dims
+
+    def centralised(self, guard=10000000) -> dict:
+        S, R, nnz, initial, fin, K = (int(x) for x in self.centralised_dims(guard))
+        out = {"rowOffset": np.zeros(S + 1, np.int32), "trnOffset": np.zeros(R + 1, np.int32),
+               "succ": np.zeros(nnz, np.int32), "prob": np.zeros(nnz), "done": np.zeros(S, np.uint8),
+               "rewards": np.zeros((K, R)), "initial": initial, "rewardFinite": bool(fin)}
+        v = C.c_void_p
+        self._check(self._lib.ref_centralised_export(
+            self._h, guard, out["rowOffset"].ctypes.data_as(v), out["trnOffset"].ctypes.data_as(v),
+            out["succ"].ctypes.data_as(v), out["prob"].ctypes.data_as(v), out["done"].ctypes.data_as(v),
+            out["rewards"].ctypes.data_as(v)))
+        return out
+
+    def centralised_pareto(self, thresholds, eps=0.01, iter_cap=500, guard=10000000):
+        t = np.ascontiguousarray(thresholds, dtype=np.float64)
+        buf = C.create_string_buffer(1 << 24)
+        sec = C.c_double(0)
+        self._check(self._lib.ref_centralised_pareto(self._h, guard, t.ctypes.data_as(C.c_void_p), t.shape[0],
+                                                     C.c_double(eps), iter_cap, buf, len(buf), C.byref(sec)))
+        out = json.loads(buf.value.decode())
+        out["seconds"] = sec.value
+        return out
+
+
 class RefError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"reference error {code}: {msg}")
@@ -265,6 +294,10 @@ class _Ref:
         lib.ref_pareto.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_double, C.c_int, C.c_int,
                                    C.c_int, C.c_char_p, C.c_int, C.c_void_p]
         lib.ref_max_assignment.argtypes = [C.c_int, C.c_void_p, C.c_void_p]
+        lib.ref_centralised_dims.argtypes = [C.c_void_p, C.c_long, C.c_void_p]
+        lib.ref_centralised_export.argtypes = [C.c_void_p, C.c_long] + [C.c_void_p] * 6
+        lib.ref_centralised_pareto.argtypes = [C.c_void_p, C.c_long, C.c_void_p, C.c_int, C.c_double, C.c_int,
+                                               C.c_char_p, C.c_int, C.c_void_p]
         self.lib = lib
 
     def _wrap(self, h):

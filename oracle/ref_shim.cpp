@@ -24,6 +24,7 @@
 #include <thread>
 
 #include "morap/assignment.hpp"
+#include "morap/centralised.hpp"
 #include "morap/engine.hpp"
 #include "morap/geometry.hpp"
 #include "morap/instance.hpp"
@@ -55,7 +56,14 @@ int guarded(F&& f) {
 
 struct Handle {
   MorapInstance inst;
+  std::unique_ptr<CentralisedMdp> cent;  // built on first use (ref_centralised_*)
 };
+
+const CentralisedMdp& centralised_of(void* p, long guard) {
+  Handle* h = static_cast<Handle*>(p);
+  if (!h->cent) h->cent = std::make_unique<CentralisedMdp>(buildCentralised(h->inst, guard));
+  return *h->cent;
+}
 
 // Scheduler fingerprint (test-only): FNV-style over 32-bit rows, same as capi.cpp rowsHash.
 uint64_t fnv_rows(const Scheduler& mu) {
@@ -79,6 +87,43 @@ Mdp csr_to_mdp(int S, int R, int nnz, int initial, const int* rowOffset, const i
   m.labels.assign(S, {});
   m.actionName.assign(R, "");
   return m;
+}
+
+// Report of one Pareto run: resultToJson plus converged, thresholds, lambdaStar, the
+// per-iteration tUp/tDown/scheduler hashes and the synthesis marginals.
+Json pareto_report(const ParetoResult& res) {
+  Json j;
+  std::unique_ptr<SynthesisResult> syn;
+  try {
+    if (res.converged) syn = std::make_unique<SynthesisResult>(synthesize(res));
+  } catch (const Error& e) {
+    j["synthesisError"] = static_cast<int>(e.code()) + 1;
+  }
+  j = resultToJson(res, syn.get());
+  j["converged"] = res.converged;
+  j["thresholds"] = res.thresholds;
+  j["lambdaStar"] = res.lambdaStar;
+  Json recs = Json::array();
+  for (const auto& rec : res.iterations) {
+    Json it;
+    it["tUp"] = rec.tUp;
+    it["tDown"] = rec.tDown;
+    Json hs = Json::array();
+    for (const auto& mu : rec.schedulers) hs.push_back(std::to_string(fnv_rows(mu)));
+    it["schedulerHash"] = hs;
+    recs.push_back(std::move(it));
+  }
+  j["records"] = recs;
+  if (syn) {
+    Json mg = Json::array();
+    for (int a = 0; a < syn->marginal.rows; ++a) {
+      Json row = Json::array();
+      for (int b = 0; b < syn->marginal.cols; ++b) row.push_back(syn->marginal(a, b));
+      mg.push_back(row);
+    }
+    j["marginal"] = mg;
+  }
+  return j;
 }
 
 }  // namespace
@@ -322,36 +367,7 @@ int ref_pareto(void* p, const double* thresholds, int nt, const double* norm, do
       ParetoResult res = paretoPoint(inst, t, M, eps, pool, iterCap);
       auto t1 = std::chrono::steady_clock::now();
       *seconds = std::chrono::duration<double>(t1 - t0).count();
-      std::unique_ptr<SynthesisResult> syn;
-      try {
-        if (res.converged) syn = std::make_unique<SynthesisResult>(synthesize(res));
-      } catch (const Error& e) {
-        j["synthesisError"] = static_cast<int>(e.code()) + 1;
-      }
-      j = resultToJson(res, syn.get());
-      j["converged"] = res.converged;
-      j["thresholds"] = res.thresholds;
-      j["lambdaStar"] = res.lambdaStar;
-      Json recs = Json::array();
-      for (const auto& rec : res.iterations) {
-        Json it;
-        it["tUp"] = rec.tUp;
-        it["tDown"] = rec.tDown;
-        Json hs = Json::array();
-        for (const auto& mu : rec.schedulers) hs.push_back(std::to_string(fnv_rows(mu)));
-        it["schedulerHash"] = hs;
-        recs.push_back(std::move(it));
-      }
-      j["records"] = recs;
-      if (syn) {
-        Json mg = Json::array();
-        for (int a = 0; a < syn->marginal.rows; ++a) {
-          Json row = Json::array();
-          for (int b = 0; b < syn->marginal.cols; ++b) row.push_back(syn->marginal(a, b));
-          mg.push_back(row);
-        }
-        j["marginal"] = mg;
-      }
+      j = pareto_report(res);
     }
     if (verify) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::string s = j.dump();
@@ -361,5 +377,46 @@ int ref_pareto(void* p, const double* thresholds, int nt, const double* norm, do
 }
 
 int ref_hardware_threads() { return static_cast<int>(std::thread::hardware_concurrency()); }
+
+// buildCentralised (centralised.hpp:54): dims[6] = {S, R, nnz, initial, rewardFinite, 2n}
+int ref_centralised_dims(void* p, long guard, int64_t* dims) {
+  return guarded([&] {
+    const CentralisedMdp& c = centralised_of(p, guard);
+    const int64_t v[6] = {c.mdp.numStates, c.mdp.numActions(), static_cast<int64_t>(c.mdp.succ.size()),
+                          c.mdp.initial, c.rewardFinite ? 1 : 0, static_cast<int64_t>(c.rewards.size())};
+    std::memcpy(dims, v, sizeof v);
+  });
+}
+
+int ref_centralised_export(void* p, long guard, int* rowOffset, int* trnOffset, int* succ, double* prob,
+                           unsigned char* done, double* rewards /* 2n x R, row-major */) {
+  return guarded([&] {
+    const CentralisedMdp& c = centralised_of(p, guard);
+    std::memcpy(rowOffset, c.mdp.rowOffset.data(), sizeof(int) * c.mdp.rowOffset.size());
+    std::memcpy(trnOffset, c.mdp.trnOffset.data(), sizeof(int) * c.mdp.trnOffset.size());
+    std::memcpy(succ, c.mdp.succ.data(), sizeof(int) * c.mdp.succ.size());
+    std::memcpy(prob, c.mdp.prob.data(), sizeof(double) * c.mdp.prob.size());
+    for (size_t s = 0; s < c.done.size(); ++s) done[s] = c.done[s] ? 1 : 0;
+    const size_t R = static_cast<size_t>(c.mdp.numActions());
+    for (size_t k = 0; k < c.rewards.size(); ++k) std::memcpy(rewards + k * R, c.rewards[k].data(), sizeof(double) * R);
+  });
+}
+
+// centralisedParetoPoint (centralised.hpp:216) with the identity norm; same JSON report as ref_pareto
+int ref_centralised_pareto(void* p, long guard, const double* thresholds, int nt, double eps, int iterCap, char* out,
+                           int outlen, double* seconds) {
+  return guarded([&] {
+    const CentralisedMdp& c = centralised_of(p, guard);
+    const int d = static_cast<int>(c.rewards.size());
+    Mat nm(d, d, 0.0);
+    for (int k = 0; k < d; ++k) nm(k, k) = 1.0;
+    auto t0 = std::chrono::steady_clock::now();
+    ParetoResult res = centralisedParetoPoint(c, Vec(thresholds, thresholds + nt), NormMatrix(nm), eps, iterCap);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::string s = pareto_report(res).dump();
+    if (static_cast<int>(s.size()) + 1 > outlen) fail(Errc::Io, "output buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+}
 
 }  // extern "C"

@@ -61,6 +61,11 @@ def load_host_library() -> C.CDLL:
         "morap_pareto": (i32, [p, p, p, i32, p, f64, i32, i32, C.c_char_p, i32, p]),
         "morap_pareto_core": (i32, [p, i32, i32, p, f64, i32, i32, QUERY_FN, p, C.c_char_p, i32]),
         "morap_max_assignment": (i32, [i32, p, p]),
+        "morap_centralised_build": (i32, [p, C.c_int64, C.POINTER(p)]),
+        "morap_centralised_free": (None, [p]),
+        "morap_centralised_info": (i32, [p, p]),
+        "morap_centralised_export": (i32, [p, p, p, p, p, p, p]),
+        "morap_centralised_pareto": (i32, [p, p, p, i32, p, f64, i32, C.c_char_p, i32, p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -182,6 +187,42 @@ class Instance:
         return p
 
 
+class Centralised:
+    """Centralised model of an instance (buildCentralised, centralised.hpp:54-179)."""
+
+    def __init__(self, inst: Instance, state_guard: int = 10000000):
+        self._lib = load_host_library()
+        h = C.c_void_p()
+        _check(self._lib.morap_centralised_build(inst.h, state_guard, C.byref(h)), "buildCentralised")
+        self.h = h
+        self.n = inst.n
+        info = np.zeros(6, np.int64)
+        _check(self._lib.morap_centralised_info(self.h, _ptr(info)), "centralised_info")
+        self.S, self.R, self.nnz, self.initial, fin, self.objectives = (int(x) for x in info)
+        self.reward_finite = bool(fin)
+
+    def arrays(self) -> dict:
+        out = {"rowOffset": np.zeros(self.S + 1, np.int32), "trnOffset": np.zeros(self.R + 1, np.int32),
+               "succ": np.zeros(self.nnz, np.int32), "prob": np.zeros(self.nnz), "done": np.zeros(self.S, np.uint8),
+               "rewards": np.zeros((self.objectives, self.R))}
+        rows = (C.c_void_p * max(1, self.objectives))(*[out["rewards"][k].ctypes.data for k in range(self.objectives)])
+        _check(self._lib.morap_centralised_export(self.h, _ptr(out["rowOffset"]), _ptr(out["trnOffset"]),
+                                                  _ptr(out["succ"]), _ptr(out["prob"]), _ptr(out["done"]),
+                                                  C.cast(rows, C.c_void_p)), "centralised_export")
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.morap_centralised_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Solver:
     """One CUDA context with the instance's products resident (GpuBackend)."""
 
@@ -255,6 +296,19 @@ class Solver:
         st = np.zeros(8)
         _check(self._lib.morap_pareto(self.h, inst.h, _ptr(t), t.shape[0], None if nm is None else _ptr(nm), eps,
                                       iteration_cap, int(verify), buf, len(buf), _ptr(st)), "paretoPoint")
+        out = json.loads(buf.value.decode())
+        out["stats"] = dict(zip(["optimize_jobs", "optimize_backups", "evaluate_jobs", "evaluate_state_backups",
+                                 "optimize_s", "evaluate_s", "host_s", "evaluate_batch_s"], st[:8].tolist()))
+        return out
+
+    def centralised_pareto(self, c: Centralised, thresholds, eps=0.01, norm=None, iteration_cap=500) -> dict:
+        """centralisedParetoPoint (centralised.hpp:216-222) on this solver's GPU."""
+        t = np.ascontiguousarray(thresholds, np.float64)
+        nm = None if norm is None else np.ascontiguousarray(norm, np.float64)
+        buf = self._json_buffer()
+        st = np.zeros(8)
+        _check(self._lib.morap_centralised_pareto(self.h, c.h, _ptr(t), t.shape[0], None if nm is None else _ptr(nm),
+                                                  eps, iteration_cap, buf, len(buf), _ptr(st)), "centralisedParetoPoint")
         out = json.loads(buf.value.decode())
         out["stats"] = dict(zip(["optimize_jobs", "optimize_backups", "evaluate_jobs", "evaluate_state_backups",
                                  "optimize_s", "evaluate_s", "host_s", "evaluate_batch_s"], st[:8].tolist()))

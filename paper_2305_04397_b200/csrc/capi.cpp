@@ -18,6 +18,10 @@ struct morap_solver {
   std::unique_ptr<morap::GpuBackend> gpu;
 };
 
+struct morap_centralised {
+  morap::CentralisedMdp c;
+};
+
 namespace {
 
 thread_local std::string g_error;
@@ -341,6 +345,56 @@ int morap_pareto_core(const double* thr, int d, int n, const double* norm, doubl
     morap::Json j = reportJson(res);
     if (verify) j["verdict"] = verdict;
     putJson(j, json_out, json_cap);
+  });
+}
+
+int morap_centralised_build(const morap_instance* inst, int64_t state_guard, morap_centralised** out) {
+  return guard([&] {
+    if (!inst || !out) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    *out = new morap_centralised{morap::buildCentralised(inst->inst, static_cast<long>(state_guard))};
+  });
+}
+
+void morap_centralised_free(morap_centralised* c) { delete c; }
+
+int morap_centralised_info(const morap_centralised* p, int64_t* out) {
+  return guard([&] {
+    const auto& c = p->c;
+    const int64_t v[6] = {c.mdp.numStates, c.mdp.numActions(), static_cast<int64_t>(c.mdp.succ.size()),
+                          c.mdp.initial, c.rewardFinite ? 1 : 0, static_cast<int64_t>(c.rewards.size())};
+    std::memcpy(out, v, sizeof v);
+  });
+}
+
+int morap_centralised_export(const morap_centralised* p, int32_t* ro, int32_t* to, int32_t* succ, double* prob,
+                             uint8_t* done, double* const* rewards) {
+  return guard([&] {
+    const auto& c = p->c;
+    auto cp = [](auto* dst, const auto& v) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(ro, c.mdp.rowOffset);
+    cp(to, c.mdp.trnOffset);
+    cp(succ, c.mdp.succ);
+    cp(prob, c.mdp.prob);
+    if (done)
+      for (size_t s = 0; s < c.done.size(); ++s) done[s] = c.done[s] ? 1 : 0;
+    if (rewards)
+      for (size_t k = 0; k < c.rewards.size(); ++k) cp(rewards[k], c.rewards[k]);
+  });
+}
+
+int morap_centralised_pareto(morap_solver* s, const morap_centralised* p, const double* thresholds, int nt,
+                             const double* norm, double eps, int iteration_cap, char* json_out, int json_cap,
+                             double* stats_out) {
+  return guard([&] {
+    const int d = static_cast<int>(p->c.rewards.size());
+    morap::NormMatrix M = normOf(norm, d);
+    morap::QueryStats st;
+    morap::ParetoResult res = morap::centralisedParetoPoint(p->c, morap::Vec(thresholds, thresholds + nt), M, eps,
+                                                            *s->gpu, iteration_cap, &st);
+    putJson(reportJson(res), json_out, json_cap);
+    putStats(st, stats_out);
   });
 }
 

@@ -100,6 +100,15 @@ int GpuBackend::modelId(const ProductMdp* p) {
   return id;
 }
 
+int GpuBackend::modelIdFor(uint64_t uid, const morap_csr_view& view) {
+  auto it = ids_.find(uid);
+  if (it != ids_.end()) return it->second;
+  int32_t id = -1;
+  check(ctx_, morap_cuda_upload(ctx_, 1, &view, &id), "upload model");
+  ids_.emplace(uid, id);
+  return id;
+}
+
 void GpuBackend::setLean(bool on) { check(ctx_, morap_cuda_set_lean(ctx_, on ? 1 : 0), "set lean"); }
 
 void GpuBackend::uploadInstance(const MorapInstance& inst) {

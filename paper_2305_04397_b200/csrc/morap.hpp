@@ -22,7 +22,7 @@
 
 #include "json.hpp"
 
-struct morap_ctx;
+#include "morap_cuda.h"  // morap_ctx, morap_csr_view
 
 namespace morap {
 
@@ -232,6 +232,7 @@ class GpuBackend {
   void uploadInstance(const MorapInstance& inst);  // all distinct products in one batch
   void uploadProducts(const std::vector<const ProductMdp*>& products);  // one batch, skips resident ones
   void setLean(bool on);  // morap_cuda_set_lean: compact-alphabet models without fp64 arrays
+  int modelIdFor(uint64_t uid, const morap_csr_view& view);  // any model keyed by a process-unique id
   morap_ctx* ctx() const { return ctx_; }
   int device() const { return device_; }
   void release();
@@ -353,5 +354,27 @@ Json resultToJson(const ParetoResult& result, const SynthesisResult* synthesis =
 
 // instance file (cli.hpp:84-117): agents inline or as paths, tasks as LTL strings / DFA JSON.
 MorapInstance instanceFromJson(const Json& j, const std::string& baseDir = ".");
+
+// ---- centralised model (centralised.hpp) -------------------------------------------------
+// One MDP over (agent block i, task j, product state, assigned-agent mask) with the control
+// rows b1 (assign the current task to agent i), b2 (pass it to the next free agent) and b3
+// (advance to the next task once the current one ended). Its Pareto query runs the same
+// device sweeps as the decentralised one, on a single large model.
+struct CentralisedMdp {
+  Mdp mdp;
+  int n = 0, realTasks = 0;
+  std::vector<char> taskEnded, done;
+  std::vector<RewardStructure> rewards;  // n agent costs, then n task successes
+  bool rewardFinite = false;
+  std::vector<int> agentIdx, taskIdx, productState;
+  std::vector<uint32_t> assigned;  // bitmask over agents
+  uint64_t uid = nextProductUid();
+};
+CentralisedMdp buildCentralised(const MorapInstance& inst, long stateGuard = 10000000);
+SupportingPoint centralisedSupportingPoint(const CentralisedMdp& c, const Vec& w, GpuBackend& gpu,
+                                           double valueEps = 1e-6, QueryStats* stats = nullptr);
+ParetoResult centralisedParetoPoint(const CentralisedMdp& c, const Vec& thresholds, const NormMatrix& norm,
+                                    double eps, GpuBackend& gpu, int iterationCap = 500,
+                                    QueryStats* stats = nullptr);
 
 }  // namespace morap
