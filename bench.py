@@ -47,7 +47,7 @@ UNIT = "nnz-backups/s"
 # Algorithm-1 iteration cap per workload: C3's 150-dimensional sandwich needs hundreds of
 # iterations to close an eps = 0.01 gap, so it is timed per iteration (the paper's own
 # metric) over the first 10 iterations.
-ITER_CAP = {"c3": 10, "c4": 3}
+ITER_CAP = {"c3": 10, "c4": 3, "cent": 5}
 # Instances whose host copy does not fit (C4: ~1e4 products, 4.6e9 nnz) are built streamed:
 # `chunk` products at a time, uploaded lean (compact alphabet only) and dropped on the host.
 STREAMED = {"c4": 256}
@@ -73,6 +73,11 @@ def workload(name: str, world: int = 1):
         cfg = {"W": W, "H": H, "n": n, "slip": 0.05,
                "racks": [[W - 1 - (k % W), H - 1 - (k // W)] for k in range(n)], "feed": [0, 0], "seed": 42}
         return cfg, [-20.0] * n + [0.99] * n, 0.01, 2
+    if name == "cent":  # centralised model: 6x6 grid, n = 4 agents x 4 tasks
+        n, W = 4, 6
+        cfg = {"W": W, "H": W, "n": n, "slip": 0.05,
+               "racks": [[W - 1 - (k % W), W - 1 - (k // W)] for k in range(n)], "feed": [0, 0], "seed": 42}
+        return cfg, [-30.0] * n + [0.9] * n, 0.01, 2
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -240,11 +245,60 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------------------
+def run_centralised(args):
+    """--workload cent: centralisedParetoPoint (centralised.hpp:216) on one large model, the
+    first ITER_CAP iterations, against the reference's own centralised solver on the host."""
+    import torch
+    import oracle
+    from paper_2305_04397_b200.api import Centralised, Instance, Solver
+    cfg, thr, eps, K = workload("cent", 1)
+    cap = ITER_CAP["cent"]
+    t0 = time.time()
+    inst = Instance.warehouse(cfg)
+    cm = Centralised(inst)
+    gen_s = time.time() - t0
+    solver = Solver(0)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    solver.set_stream(stream.cuda_stream)
+    for _ in range(max(args.warmup, 0)):
+        rep = solver.centralised_pareto(cm, thr, eps=eps, iteration_cap=cap)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    backups = 0.0
+    with ClockSampler(0) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rep = solver.centralised_pareto(cm, thr, eps=eps, iteration_cap=cap)
+            backups += rep["stats"]["optimize_backups"] + rep["stats"]["evaluate_state_backups"]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    iters = len(rep["iterations"])
+    cpu = None
+    if oracle.ref_available() and not args.no_cpu_baseline:
+        r = oracle.ref().warehouse(cfg).centralised_pareto(thr, eps=eps, iter_cap=cap)
+        cpu = {"value": r["seconds"] / len(r["iterations"]) * 1e3, "unit": "ms per iteration", "cores": 1,
+               "kind": "reference", "sample": f"oracle/_ref centralisedParetoPoint, same model, first {cap} iterations"}
+        assert r["tDown"] == rep["tDown"], "centralised query differs from the reference"
+    print(json.dumps({
+        "metric": METRIC, "value": backups / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded warehouse generator, warehouse.hpp:176)",
+        "config": {"workload": "cent", "grid": [cfg["W"], cfg["H"]], "agents": cfg["n"], "tasks": cfg["n"],
+                   "model": {"states": cm.S, "rows": cm.R, "nnz": cm.nnz, "objectives": cm.objectives},
+                   "pareto_iterations": iters, "ms_per_iteration": ms / args.steps / iters,
+                   "step": f"centralisedParetoPoint, first {cap} iterations", "generate_s": round(gen_s, 3)},
+        "cpu_baseline": cpu, "clocks": clk.summary()}))
+
+
 def run_ours(args):
     import torch
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload == "cent":
+        return run_centralised(args)
     if world > 1 or args.sharded:
         from paper_2305_04397_b200 import distributed
         return distributed.bench_main(args, rank, world, local)
