@@ -65,6 +65,15 @@ morap_ctx* morap_solver_cuda(morap_solver* s);
 int morap_solver_upload(morap_solver* s, const morap_instance* inst);
 /* Drop every resident product (device memory freed; next query re-uploads). */
 int morap_solver_release(morap_solver* s);
+/* Per-rank build for the multi-GPU query: every rank generates the instance streamed
+ * (`chunk` products at a time), assigns each distinct product to the least-loaded rank (by
+ * nnz, in first-occurrence order -- identical on every rank) and keeps host arrays only
+ * for its own products; morap_instance_product_owner reports the owner (-1 when the
+ * instance was not built sharded). */
+int morap_instance_warehouse_shard(const char* config_json, int threads, int rank, int world, int chunk,
+                                   morap_instance** out);
+int morap_instance_product_owner(const morap_instance* inst, int i, int j);
+
 /* morap_cuda_set_lean on the solver's context (applies to later uploads). */
 int morap_solver_set_lean(morap_solver* s, int on);
 

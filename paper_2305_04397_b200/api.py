@@ -56,6 +56,8 @@ def load_host_library() -> C.CDLL:
         "morap_solver_upload": (i32, [p, p]),
         "morap_solver_release": (i32, [p]),
         "morap_solver_set_lean": (i32, [p, i32]),
+        "morap_instance_warehouse_shard": (i32, [C.c_char_p, i32, i32, i32, i32, C.POINTER(p)]),
+        "morap_instance_product_owner": (i32, [p, i32, i32]),
         "morap_instance_warehouse_streamed": (i32, [C.c_char_p, i32, p, i32, C.POINTER(p)]),
         "morap_supporting_point": (i32, [p, p, p, i32, p, p, p]),
         "morap_pareto": (i32, [p, p, p, i32, p, f64, i32, i32, C.c_char_p, i32, p]),
@@ -134,6 +136,19 @@ class Instance:
         inst = cls(h)
         inst.streamed = True
         return inst
+
+    @classmethod
+    def warehouse_shard(cls, config: dict, rank: int, world: int, chunk: int = 256, threads: int = 0) -> "Instance":
+        """Per-rank build for the sharded query: host arrays only for this rank's products
+        (owners: least-loaded rank by nnz in first-occurrence order, see morap.h)."""
+        lib = load_host_library()
+        h = C.c_void_p()
+        _check(lib.morap_instance_warehouse_shard(json.dumps(config).encode(), threads, rank, world, chunk,
+                                                  C.byref(h)), "generateInstance (shard)")
+        return cls(h)
+
+    def product_owner(self, i, j) -> int:
+        return int(self._lib.morap_instance_product_owner(self.h, i, j))
 
     @classmethod
     def from_json(cls, text: str, base_dir: str = ".") -> "Instance":

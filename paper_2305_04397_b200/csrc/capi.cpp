@@ -12,6 +12,7 @@
 struct morap_instance {
   morap::MorapInstance inst;
   std::map<const morap::ProductMdp*, int64_t> firstSlot;  // lazily filled (product_dims)
+  std::map<uint64_t, int> owner;                           // sharded builds: product uid -> rank
 };
 
 struct morap_solver {
@@ -127,7 +128,7 @@ int morap_instance_warehouse(const char* config_json, int threads, morap_instanc
   return guard([&] {
     if (!out || !config_json) morap::fail(morap::Errc::InvalidConfig, "null argument");
     morap::WarehouseConfig cfg = morap::warehouseConfigFromJson(morap::Json::parse(config_json));
-    *out = new morap_instance{morap::generateInstance(cfg, threads), {}};
+    *out = new morap_instance{morap::generateInstance(cfg, threads), {}, {}};
   });
 }
 
@@ -142,7 +143,7 @@ int morap_instance_from_json(const char* text, const char* base_dir, morap_insta
       morap::fail(morap::Errc::Io, e.what());
     }
     const std::string base = base_dir ? base_dir : ".";
-    auto inst = std::make_unique<morap_instance>(morap_instance{morap::instanceFromJson(j, base), {}});
+    auto inst = std::make_unique<morap_instance>(morap_instance{morap::instanceFromJson(j, base), {}, {}});
     if (has_norm) *has_norm = 0;
     if (j.contains("norm") && norm_out) {
       morap::Json nj = j.at("norm");
@@ -266,6 +267,41 @@ int morap_solver_release(morap_solver* s) {
   return guard([&] { s->gpu->release(); });
 }
 
+int morap_instance_warehouse_shard(const char* config_json, int threads, int rank, int world, int chunk,
+                                   morap_instance** out) {
+  return guard([&] {
+    if (!out || !config_json) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    if (world < 1 || rank < 0 || rank >= world || chunk < 1) morap::fail(morap::Errc::InvalidConfig, "bad shard");
+    morap::WarehouseConfig cfg = morap::warehouseConfigFromJson(morap::Json::parse(config_json));
+    std::map<uint64_t, int> owner;
+    std::vector<double> load(static_cast<size_t>(world), 0.0);
+    // distinct products arrive in (i, j) order of first occurrence: each goes to the least
+    // loaded rank (by nnz, lowest rank on ties) -- the same decision on every rank
+    const morap::ProductSink sink = [&](const std::vector<morap::ProductMdp*>& fresh) {
+      std::vector<morap::ProductMdp*> drop;
+      for (morap::ProductMdp* p : fresh) {
+        const int r = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+        load[static_cast<size_t>(r)] += static_cast<double>(morap::productNnz(*p));
+        owner[p->uid] = r;
+        if (r != rank) drop.push_back(p);
+      }
+      for (morap::ProductMdp* p : drop) morap::slimProduct(*p);
+    };
+    const std::function<void()> retry = [&] {
+      owner.clear();
+      std::fill(load.begin(), load.end(), 0.0);
+    };
+    morap::MorapInstance inst = morap::generateInstance(cfg, threads, static_cast<size_t>(chunk), &sink, &retry);
+    *out = new morap_instance{std::move(inst), {}, std::move(owner)};
+  });
+}
+
+int morap_instance_product_owner(const morap_instance* p, int i, int j) {
+  if (!p || i < 0 || j < 0 || i >= p->inst.n || j >= p->inst.n) return -1;
+  auto it = p->owner.find(p->inst.products[i][j]->uid);
+  return it == p->owner.end() ? -1 : it->second;
+}
+
 int morap_solver_set_lean(morap_solver* s, int on) {
   return guard([&] { s->gpu->setLean(on != 0); });
 }
@@ -288,7 +324,7 @@ int morap_instance_warehouse_streamed(const char* config_json, int threads, mora
       for (auto& th : pool) th.join();
     };
     const std::function<void()> retry = [&] { gpu.release(); };
-    *out = new morap_instance{morap::generateInstance(cfg, threads, static_cast<size_t>(chunk), &sink, &retry), {}};
+    *out = new morap_instance{morap::generateInstance(cfg, threads, static_cast<size_t>(chunk), &sink, &retry), {}, {}};
   });
 }
 

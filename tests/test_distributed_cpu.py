@@ -57,7 +57,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, case, out_path):
+def _worker(rank, world, port, case, out_path, mode="full"):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -66,7 +66,10 @@ def _worker(rank, world, port, case, out_path):
         from paper_2305_04397_b200.api import Instance
         from paper_2305_04397_b200.distributed import ShardedQuery, _Exchange, pareto_sharded
 
-        inst = Instance.warehouse(case["config"])
+        if mode == "shard":  # every rank builds only its own products
+            inst = Instance.warehouse_shard(case["config"], rank, world, chunk=3)
+        else:
+            inst = Instance.warehouse(case["config"])
         res, q = pareto_sharded(inst, case["thresholds"], case["eps"], rank, world, backend=OracleBackend(),
                                 exchange=_Exchange(world, "cpu"))
         with open(f"{out_path}.{rank}", "w") as f:
@@ -75,12 +78,12 @@ def _worker(rank, world, port, case, out_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("which", [3, 6])
-def test_sharded_query_world2_matches_reference(which):
+@pytest.mark.parametrize("which,mode", [(3, "full"), (6, "full"), (6, "shard")])
+def test_sharded_query_world2_matches_reference(which, mode):
     case = load_golden("pareto.json")["suite"][which]  # n = 2 and n = 3 warehouse runs
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "res")
-        mp.spawn(_worker, args=(2, _free_port(), case, out), nprocs=2, join=True)
+        mp.spawn(_worker, args=(2, _free_port(), case, out, mode), nprocs=2, join=True)
         got = [json.load(open(f"{out}.{r}")) for r in range(2)]
     n = case["config"]["n"]
     assert got[0]["local"] + got[1]["local"] == n * n and min(g["local"] for g in got) > 0
