@@ -59,8 +59,15 @@ __device__ int g_dryRun = 0;
 struct TileDesc {
   int32_t s0, r0, k0, fits;
   int32_t wlo, wn;  // successor window: x[wlo, wlo + wn) is staged with the tile
-  int32_t allIn;  // compact: every successor of the tile lies inside the window
-  int32_t pad1;
+  int32_t allIn;    // compact: every successor of the tile lies inside the window
+  int32_t simple;   // compact: every row of the tile has at most two transitions
+};
+
+// Where a tile's slice starts in each compact sweep stream. Every slice starts on a 16-byte
+// boundary (the streams are padded per tile), so each lands at offset 0 of its stage region.
+struct TilePos {
+  int32_t row, trn, succ, idx;  // u16 row ends, u16 transition ends, u16 window offsets, u8 index
+  int32_t cls, done, pad0, pad1;  // u8 class, u8 done
 };
 
 struct DevModel {
@@ -79,9 +86,15 @@ struct DevModel {
   const double* probDict;     // <= 256 distinct probabilities
   const uint8_t* rclass;      // R
   const double* classTable;   // nclass x K objective tuples
-  const uint16_t* succW;      // compact: successor as offset into its tile's x window, 0xFFFF outside
-  const uint16_t* relRowEnd;  // compact: rowOffset[s + 1] - tile.r0 (u16, fitting tiles)
-  const uint16_t* relTrnEnd;  // compact: trnOffset[r + 1] - tile.k0 (u16, fitting tiles)
+  // compact sweep streams, tile-major and padded per tile (TilePos): rowOffset[s + 1] -
+  // tile.r0 and trnOffset[r + 1] - tile.k0 (u16), succW, and copies of probIdx / rclass / done
+  const uint16_t* relRowEnd;
+  const uint16_t* relTrnEnd;
+  const uint16_t* succWP;
+  const uint8_t* idxP;
+  const uint8_t* clsP;
+  const uint8_t* doneP;
+  const TilePos* tilePos;     // ntiles
   int32_t S, R, nnz, initial, ntiles, K, rewardFinite, compact;
   int32_t nclass, pad2;
   unsigned long long bytesPerSweep;  // algorithmic bytes of one greedy sweep
@@ -794,6 +807,9 @@ __global__ void __launch_bounds__(kTmaThreads, kStages >= 3 ? 2 : 3) k_greedy_sw
 #define MORAP_CMP_CTAS 4
 #endif
 constexpr int kCmpStages = MORAP_CMP_STAGES;
+#ifndef MORAP_CMP_LANES
+#define MORAP_CMP_LANES 1  // 4: four lanes per state on all-in-window tiles (A/B)
+#endif
 #ifndef MORAP_CMP_WAITER
 #define MORAP_CMP_WAITER 0  // A/B: one polling warp + named barrier was 7% slower (C2)
 #endif
@@ -819,7 +835,7 @@ constexpr int kCmpSmemBytes = kCmpStages * kCStageBytes;
 
 struct CmpInfo {
   const int32_t* succG;  // absolute successors (out-of-window transitions)
-  int t, job, fits, allIn;
+  int t, job, fits, allIn, simple;
   int s0, r0, k0, ns;
   int offRow, offTrn, offSucc, offIdx, offCls, offDone, offX, offXw;
   int wlo, wn;
@@ -844,6 +860,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
   __shared__ __align__(8) uint64_t full[kCmpStages], empty[kCmpStages];
   __shared__ CmpInfo info[kCmpStages];
   __shared__ double sRed[kConsumers / 32];
+  __shared__ int32_t sPos[32][8];  // producer: TilePos of the current batch of 32 tiles
 
   const int nact = ctl->nactive;
   const int total = ctl->totalTiles;
@@ -882,7 +899,9 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     for (int tb = t0; tb < t1; tb += 32) {
       // ---- resolve tiles tb .. tb+31, one per lane -----------------------------------
       const int tl = tb + lane;
-      int mJob = 0, mS0 = 0, mR0 = 0, mK0 = 0, mFits = 0, mWlo = 0, mWn = 0, mAll = 0, eS0 = 0, eR0 = 0, eK0 = 0;
+      int mJob = 0, mS0 = 0, mR0 = 0, mK0 = 0, mFits = 0, mWlo = 0, mWn = 0, mAll = 0, mSimple = 0, eS0 = 0,
+          eR0 = 0, eK0 = 0;
+      __syncwarp();  // the previous batch is done with sPos
       if (tl < t1) {
         int a = ai;
         while (tl >= prefix[a + 1]) ++a;
@@ -891,10 +910,15 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
         const DevModel* M = &models[jobs[mJob].model];
         const int4* tp = reinterpret_cast<const int4*>(M->tiles + lt);
         const int4 d0 = tp[0], d1 = tp[1], e0 = tp[2];
+        const int4* pp = reinterpret_cast<const int4*>(M->tilePos + lt);
+        const int4 p0 = pp[0], p1 = pp[1];
         mS0 = d0.x; mR0 = d0.y; mK0 = d0.z; mFits = d0.w;
-        mWlo = d1.x; mWn = d1.y; mAll = d1.z;
+        mWlo = d1.x; mWn = d1.y; mAll = d1.z; mSimple = d1.w;
         eS0 = e0.x; eR0 = e0.y; eK0 = e0.z;
+        sPos[lane][0] = p0.x; sPos[lane][1] = p0.y; sPos[lane][2] = p0.z; sPos[lane][3] = p0.w;
+        sPos[lane][4] = p1.x; sPos[lane][5] = p1.y;
       }
+      __syncwarp();
       {  // advance ai to the slot of the last tile of the batch
         const int last = min(t1, tb + 32) - 1;
         while (last >= prefix[ai + 1]) ++ai;
@@ -907,6 +931,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
         const int k0 = __shfl_sync(0xffffffffu, mK0, q), fits = __shfl_sync(0xffffffffu, mFits, q);
         const int wlo = __shfl_sync(0xffffffffu, mWlo, q), wn = __shfl_sync(0xffffffffu, mWn, q);
         const int allIn = __shfl_sync(0xffffffffu, mAll, q);
+        const int simple = __shfl_sync(0xffffffffu, mSimple, q);
         const int s1 = __shfl_sync(0xffffffffu, eS0, q), r1 = __shfl_sync(0xffffffffu, eR0, q);
         const int k1 = __shfl_sync(0xffffffffu, eK0, q);
         if (job != curJob) {  // uniform: reload this lane's stream base for the new job
@@ -918,10 +943,10 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           switch (lane) {
             case 0: bp = curM->relRowEnd; break;
             case 1: bp = curM->relTrnEnd; break;
-            case 2: bp = curM->succW; break;
-            case 3: bp = curM->probIdx; break;
-            case 4: bp = curM->rclass; break;
-            case 5: bp = curM->done; break;
+            case 2: bp = curM->succWP; break;
+            case 3: bp = curM->idxP; break;
+            case 4: bp = curM->clsP; break;
+            case 5: bp = curM->doneP; break;
             case 6: bp = POLICY ? nullptr : curJ->buf[parity]; break;
             case 7: bp = curJ->buf[parity]; break;
             default: break;
@@ -933,13 +958,15 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
         long long lo = 0, hi = 0;
         int sh = 0, dstOff = 0;
         uint64_t lp = pol;
+        // lanes 0-5: tile-major padded streams (slice start from TilePos, 16-byte aligned)
+        const int pos = lane < 6 ? sPos[q][lane] : 0;
         switch (lane) {
-          case 0: lo = s0; hi = s1; sh = 1; dstOff = kCOffRow; break;
-          case 1: lo = r0; hi = r1; sh = 1; dstOff = kCOffTrn; break;
-          case 2: lo = k0; hi = k1; sh = 1; dstOff = kCOffSucc; break;
-          case 3: lo = k0; hi = k1; sh = 0; dstOff = kCOffIdx; break;
-          case 4: lo = r0; hi = r1; sh = 0; dstOff = kCOffCls; break;
-          case 5: lo = s0; hi = s1; sh = 0; dstOff = kCOffDone; break;
+          case 0: lo = pos; hi = pos + (s1 - s0); sh = 1; dstOff = kCOffRow; break;
+          case 1: lo = pos; hi = pos + (r1 - r0); sh = 1; dstOff = kCOffTrn; break;
+          case 2: lo = pos; hi = pos + (k1 - k0); sh = 1; dstOff = kCOffSucc; break;
+          case 3: lo = pos; hi = pos + (k1 - k0); sh = 0; dstOff = kCOffIdx; break;
+          case 4: lo = pos; hi = pos + (r1 - r0); sh = 0; dstOff = kCOffCls; break;
+          case 5: lo = pos; hi = pos + (s1 - s0); sh = 0; dstOff = kCOffDone; break;
           case 6: lo = s0; hi = s1; sh = 3; dstOff = kCOffX; lp = polKeep; break;
           case 7: lo = wlo; hi = wlo + wn; sh = 3; dstOff = kCOffXw; lp = polKeep; break;
           default: break;
@@ -959,6 +986,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           v->job = job;
           v->fits = fits;
           v->allIn = allIn;
+          v->simple = simple;
           v->s0 = s0;
           v->r0 = r0;
           v->k0 = k0;
@@ -1029,14 +1057,72 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
       // Tile-relative u16 row / transition END offsets: state i owns rows
       // [relRowEnd[i-1], relRowEnd[i]) (0 for i = 0), row r owns transitions
       // [relTrnEnd[r-1], relTrnEnd[r]).
-      const uint16_t* rowE = reinterpret_cast<const uint16_t*>(st + kCOffRow) + v.offRow;
-      const uint16_t* trnE = reinterpret_cast<const uint16_t*>(st + kCOffTrn) + v.offTrn;
-      const uint16_t* succS = reinterpret_cast<const uint16_t*>(st + kCOffSucc) + v.offSucc;
-      const uint8_t* idxS = st + kCOffIdx + v.offIdx;
-      const uint8_t* clsS = st + kCOffCls + v.offCls;
-      const uint8_t* doneS = st + kCOffDone + v.offDone;
+      // padded per-tile streams: every slice starts at offset 0 of its region
+      const uint16_t* rowE = reinterpret_cast<const uint16_t*>(st + kCOffRow);
+      const uint16_t* trnE = reinterpret_cast<const uint16_t*>(st + kCOffTrn);
+      const uint16_t* succS = reinterpret_cast<const uint16_t*>(st + kCOffSucc);
+      const uint8_t* idxS = st + kCOffIdx;
+      const uint8_t* clsS = st + kCOffCls;
+      const uint8_t* doneS = st + kCOffDone;
       const double* xS = reinterpret_cast<const double*>(st + kCOffX) + v.offX;
       const double* xwS = reinterpret_cast<const double*>(st + kCOffXw);  // even wlo: no front offset
+#if MORAP_CMP_LANES == 4
+      if (v.allIn) {
+        // Four lanes per state, eight states per pass, four passes per warp: lane sub of a
+        // group owns rows rb + sub, rb + sub + 4, ... (in order), so the rows of a state are
+        // computed side by side instead of one after another; the group then combines its
+        // lanes' first strict maxima -- max value, lowest row on equal values, which is the
+        // row a left-to-right scan keeps (numerics.hpp:93-100).
+        const double* __restrict__ dict = v.dict;
+        const double* __restrict__ crho = v.classRho;
+        const int sub = lane & 3;
+#pragma unroll 1
+        for (int pass = 0; pass < 4; ++pass) {
+          const int li = (tid & ~31) + pass * 8 + (lane >> 2);
+          const bool valid = li < v.ns;
+          const int rb = valid ? (li ? rowE[li - 1] : 0) : 0, re = valid ? rowE[li] : 0;
+          const bool dn = valid && doneS[li];
+          double best = 0.0;
+          int bestRow = 0x7fffffff;
+          if (valid && !dn) {
+#pragma unroll 1
+            for (int r = rb + sub; r < re; r += 4) {
+              const int kb = r ? trnE[r - 1] : 0, ke = trnE[r];
+              double acc = __ldg(crho + clsS[r]);
+              if (kb < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[kb]), xwS[succS[kb]]));
+              if (kb + 1 < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[kb + 1]), xwS[succS[kb + 1]]));
+#pragma unroll 1
+              for (int q = kb + 2; q < ke; ++q)
+                acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[q]), xwS[succS[q]]));
+              if (bestRow == 0x7fffffff || acc > best) {
+                best = acc;
+                bestRow = r;
+              }
+            }
+          }
+#pragma unroll
+          for (int off = 1; off < 4; off <<= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const int orow = __shfl_xor_sync(0xffffffffu, bestRow, off);
+            if (orow != 0x7fffffff && (bestRow == 0x7fffffff || ob > best || (ob == best && orow < bestRow))) {
+              best = ob;
+              bestRow = orow;
+            }
+          }
+          if (valid && sub == 0) {
+            const int s = v.s0 + li;
+            if (dn) {
+              if (POLICY) v.policy[s] = v.r0 + rb;  // numerics.hpp:114-115
+            } else if (POLICY) {
+              v.policy[s] = v.r0 + bestRow;
+            } else {
+              v.y[s] = best;
+              dl = fmax(dl, fabs(__dsub_rn(best, xS[li])));
+            }
+          }
+        }
+      } else
+#endif
       if (tid < v.ns) {
         const int s = v.s0 + tid;
         const int rb = tid ? rowE[tid - 1] : 0, re = rowE[tid];
@@ -1046,7 +1132,30 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           double best = 0.0;
           int bestRow = -1;
           int kb = rb ? trnE[rb - 1] : 0;
-          if (v.allIn) {  // every successor inside the staged window: no out-of-window test
+          if (v.allIn && v.simple && re > rb) {
+            // every successor in the window, at most two transitions per row: straight-line
+            // rows, the first one peeled so the max needs no "no row yet" test
+            const double* __restrict__ dict = v.dict;
+            const double* __restrict__ crho = v.classRho;
+            auto row = [&](int r, int& k) {
+              const int ke = trnE[r];
+              double acc = __ldg(crho + clsS[r]);
+              if (k < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[k]), xwS[succS[k]]));
+              if (k + 1 < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[k + 1]), xwS[succS[k + 1]]));
+              k = ke;
+              return acc;
+            };
+            best = row(rb, kb);
+            bestRow = rb;
+#pragma unroll 1
+            for (int r = rb + 1; r < re; ++r) {
+              const double acc = row(r, kb);
+              if (acc > best) {
+                best = acc;
+                bestRow = r;
+              }
+            }
+          } else if (v.allIn) {  // every successor inside the staged window: no out-of-window test
             const double* __restrict__ dict = v.dict;
             const double* __restrict__ crho = v.classRho;
 #pragma unroll 1
@@ -2123,28 +2232,70 @@ struct CompactStream {
   bool ok = false;
   std::vector<uint8_t> idx, cls;
   std::vector<double> dict, table;
-  std::vector<uint16_t> succW;  // successor window offsets (needs the tile table)
-  std::vector<uint16_t> relRowEnd, relTrnEnd;  // tile-relative row / transition ends
+  std::vector<uint16_t> succW;  // successor window offsets (needs the tile table), padded per tile
+  std::vector<uint16_t> relRowEnd, relTrnEnd;  // tile-relative row / transition ends, padded per tile
+  std::vector<uint8_t> idxP, clsP, doneP;      // tile-major padded copies for the sweep
+  std::vector<TilePos> pos;
 };
 
-// succW[k] = succ[k] - wlo of k's tile when inside the tile's x window, else 0xFFFF
+// The sweep streams of a compact model, tile-major: each tile's slice of every stream
+// starts on a 16-byte boundary (padded), so one bulk copy per stream lands at offset 0 of
+// its stage region. u16 window offsets succW = succ - wlo inside the tile's x window
+// (0xFFFF outside), u16 ends relative to the tile, allIn / simple flags per tile.
 void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, CompactStream& c) {
-  c.succW.resize(static_cast<size_t>(v.nnz));
-  c.relRowEnd.resize(static_cast<size_t>(v.num_states));
-  c.relTrnEnd.resize(static_cast<size_t>(v.num_rows));
-  for (size_t t = 0; t + 1 < desc.size(); ++t) {
+  const size_t nt = desc.size() - 1;
+  c.pos.assign(nt, TilePos{});
+  auto up16 = [](size_t n, size_t es) { return (n * es + 15) / 16 * 16 / es; };  // elements, padded
+  size_t nRow = 0, nTrn = 0, nSucc = 0, nIdx = 0, nCls = 0, nDone = 0;
+  for (size_t t = 0; t < nt; ++t) {
+    const TileDesc &d = desc[t], &e = desc[t + 1];
+    const bool f = d.fits != 0;  // oversized tiles are swept from the global arrays
+    const size_t ns = f ? e.s0 - d.s0 : 0, nr = f ? e.r0 - d.r0 : 0, nz = f ? e.k0 - d.k0 : 0;
+    TilePos& p = c.pos[t];
+    p.row = static_cast<int32_t>(nRow);
+    p.trn = static_cast<int32_t>(nTrn);
+    p.succ = static_cast<int32_t>(nSucc);
+    p.idx = static_cast<int32_t>(nIdx);
+    p.cls = static_cast<int32_t>(nCls);
+    p.done = static_cast<int32_t>(nDone);
+    nRow += up16(ns, 2);
+    nTrn += up16(nr, 2);
+    nSucc += up16(nz, 2);
+    nIdx += up16(nz, 1);
+    nCls += up16(nr, 1);
+    nDone += up16(ns, 1);
+  }
+  c.relRowEnd.assign(nRow, 0);
+  c.relTrnEnd.assign(nTrn, 0);
+  c.succW.assign(nSucc, 0xFFFF);
+  c.idxP.assign(nIdx, 0);
+  c.clsP.assign(nCls, 0);
+  c.doneP.assign(nDone, 0);
+  for (size_t t = 0; t < nt; ++t) {
     TileDesc& d = desc[t];
     const TileDesc& e = desc[t + 1];
-    // u16 ends are only read for fitting tiles (<= kRowCap rows, <= kNnzCap transitions)
-    for (int q = d.s0; q < e.s0; ++q)
-      c.relRowEnd[q] = static_cast<uint16_t>(std::min(v.row_offset[q + 1] - d.r0, 0xFFFF));
-    for (int r = d.r0; r < e.r0; ++r)
-      c.relTrnEnd[r] = static_cast<uint16_t>(std::min(v.trn_offset[r + 1] - d.k0, 0xFFFF));
     d.allIn = 1;
-    for (int k = d.k0; k < desc[t + 1].k0; ++k) {
+    d.simple = 1;
+    for (int r = d.r0; r < e.r0; ++r)
+      if (v.trn_offset[r + 1] - v.trn_offset[r] > 2) d.simple = 0;
+    if (!d.fits) {
+      d.allIn = 0;
+      continue;
+    }
+    const TilePos& p = c.pos[t];
+    for (int q = d.s0; q < e.s0; ++q) {
+      c.relRowEnd[p.row + (q - d.s0)] = static_cast<uint16_t>(v.row_offset[q + 1] - d.r0);
+      c.doneP[p.done + (q - d.s0)] = v.done[q] ? 1 : 0;
+    }
+    for (int r = d.r0; r < e.r0; ++r) {
+      c.relTrnEnd[p.trn + (r - d.r0)] = static_cast<uint16_t>(v.trn_offset[r + 1] - d.k0);
+      c.clsP[p.cls + (r - d.r0)] = c.cls[r];
+    }
+    for (int k = d.k0; k < e.k0; ++k) {
       const unsigned o = static_cast<unsigned>(v.succ[k] - d.wlo);
       const bool in = o < static_cast<unsigned>(d.wn);
-      c.succW[k] = in ? static_cast<uint16_t>(o) : static_cast<uint16_t>(0xFFFF);
+      c.succW[p.succ + (k - d.k0)] = in ? static_cast<uint16_t>(o) : static_cast<uint16_t>(0xFFFF);
+      c.idxP[p.idx + (k - d.k0)] = c.idx[k];
       if (!in) d.allIn = 0;
     }
   }
@@ -2920,8 +3071,10 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
              align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
     if (compact[m].ok)
       bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(v.num_rows, 256) +
-               align_up(8ull * compact[m].table.size(), 256) + align_up(2ull * v.nnz, 256) +
-               align_up(2ull * v.num_states, 256) + align_up(2ull * v.num_rows, 256);
+               align_up(8ull * compact[m].table.size(), 256) + align_up(2ull * compact[m].succW.size(), 256) +
+               align_up(2ull * compact[m].relRowEnd.size(), 256) + align_up(2ull * compact[m].relTrnEnd.size(), 256) +
+               align_up(compact[m].idxP.size(), 256) + align_up(compact[m].clsP.size(), 256) +
+               align_up(compact[m].doneP.size(), 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256);
   }
   void* dev = nullptr;
   {
@@ -2999,9 +3152,13 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
       dmod.rclass = reinterpret_cast<const uint8_t*>(put(c.cls.data(), c.cls.size()));
       dmod.classTable = reinterpret_cast<const double*>(put(c.table.data(), 8ull * c.table.size()));
       dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
-      dmod.succW = reinterpret_cast<const uint16_t*>(put(c.succW.data(), 2ull * c.succW.size()));
+      dmod.succWP = reinterpret_cast<const uint16_t*>(put(c.succW.data(), 2ull * c.succW.size()));
       dmod.relRowEnd = reinterpret_cast<const uint16_t*>(put(c.relRowEnd.data(), 2ull * c.relRowEnd.size()));
       dmod.relTrnEnd = reinterpret_cast<const uint16_t*>(put(c.relTrnEnd.data(), 2ull * c.relTrnEnd.size()));
+      dmod.idxP = reinterpret_cast<const uint8_t*>(put(c.idxP.data(), c.idxP.size()));
+      dmod.clsP = reinterpret_cast<const uint8_t*>(put(c.clsP.data(), c.clsP.size()));
+      dmod.doneP = reinterpret_cast<const uint8_t*>(put(c.doneP.data(), c.doneP.size()));
+      dmod.tilePos = reinterpret_cast<const TilePos*>(put(c.pos.data(), sizeof(TilePos) * c.pos.size()));
       // compact stream: window offset 2 + prob index 1 per nnz; relative transition end 2 +
       // class 1 per row; relative row end 2 + done 1 + x 8 + y 8 per state
       dmod.bytesPerSweep = 3ull * v.nnz + 3ull * v.num_rows + 19ull * v.num_states;
