@@ -807,15 +807,6 @@ __global__ void __launch_bounds__(kTmaThreads, kStages >= 3 ? 2 : 3) k_greedy_sw
 #define MORAP_CMP_CTAS 4
 #endif
 constexpr int kCmpStages = MORAP_CMP_STAGES;
-#ifndef MORAP_CMP_LANES
-#define MORAP_CMP_LANES 1  // 4: four lanes per state on all-in-window tiles (A/B)
-#endif
-#ifndef MORAP_CMP_WAITER
-#define MORAP_CMP_WAITER 0  // A/B: one polling warp + named barrier was 7% slower (C2)
-#endif
-#ifndef MORAP_EXP
-#define MORAP_EXP 0  // timing experiments (scripts/probe_kernel.py); 0 in every shipped build
-#endif
 // stage: u16 tile-relative row ends per state and transition ends per row, u16 window
 // offsets, u8 probability index, u8 reward class, done, own x, successor window of x
 constexpr int kCOffRow = 0;
@@ -973,7 +964,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
         }
         const long long a0 = (lo << sh) & ~15ll, z0 = ((hi << sh) + 15) & ~15ll;
         const uint32_t bytes =
-            (myBase && fits && z0 > a0 && !(MORAP_EXP & 4)) ? static_cast<uint32_t>(z0 - a0) : 0u;
+            (myBase && fits && z0 > a0) ? static_cast<uint32_t>(z0 - a0) : 0u;
         const int off = static_cast<int>(((lo << sh) - a0) >> sh);
         const uint32_t txBytes = __reduce_add_sync(0xffffffffu, bytes);
         if (use >= kCmpStages) mbar_wait_sleep(&empty[b], ((use / kCmpStages) - 1) & 1);
@@ -1029,15 +1020,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
   const int lane = tid & 31;
   for (int use = 0;; ++use) {
     const int b = use % kCmpStages;
-#if MORAP_CMP_WAITER
-    // one consumer warp polls the stage barrier, the other seven park on a named barrier
-    // (no issue slots burnt spinning), then observe the completed phase themselves
-    if (tid < 32) mbar_wait(&full[b], (use / kCmpStages) & 1);
-    asm volatile("bar.sync 2, %0;" ::"n"(kConsumers) : "memory");
-    if (tid >= 32) mbar_wait(&full[b], (use / kCmpStages) & 1);
-#else
     mbar_wait_sleep(&full[b], (use / kCmpStages) & 1);
-#endif
     const CmpInfo v = info[b];
     if (v.t < 0) break;
     if (!POLICY && v.job != runJob) {  // uniform over the consumers
@@ -1066,63 +1049,6 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
       const uint8_t* doneS = st + kCOffDone;
       const double* xS = reinterpret_cast<const double*>(st + kCOffX) + v.offX;
       const double* xwS = reinterpret_cast<const double*>(st + kCOffXw);  // even wlo: no front offset
-#if MORAP_CMP_LANES == 4
-      if (v.allIn) {
-        // Four lanes per state, eight states per pass, four passes per warp: lane sub of a
-        // group owns rows rb + sub, rb + sub + 4, ... (in order), so the rows of a state are
-        // computed side by side instead of one after another; the group then combines its
-        // lanes' first strict maxima -- max value, lowest row on equal values, which is the
-        // row a left-to-right scan keeps (numerics.hpp:93-100).
-        const double* __restrict__ dict = v.dict;
-        const double* __restrict__ crho = v.classRho;
-        const int sub = lane & 3;
-#pragma unroll 1
-        for (int pass = 0; pass < 4; ++pass) {
-          const int li = (tid & ~31) + pass * 8 + (lane >> 2);
-          const bool valid = li < v.ns;
-          const int rb = valid ? (li ? rowE[li - 1] : 0) : 0, re = valid ? rowE[li] : 0;
-          const bool dn = valid && doneS[li];
-          double best = 0.0;
-          int bestRow = 0x7fffffff;
-          if (valid && !dn) {
-#pragma unroll 1
-            for (int r = rb + sub; r < re; r += 4) {
-              const int kb = r ? trnE[r - 1] : 0, ke = trnE[r];
-              double acc = __ldg(crho + clsS[r]);
-              if (kb < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[kb]), xwS[succS[kb]]));
-              if (kb + 1 < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[kb + 1]), xwS[succS[kb + 1]]));
-#pragma unroll 1
-              for (int q = kb + 2; q < ke; ++q)
-                acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[q]), xwS[succS[q]]));
-              if (bestRow == 0x7fffffff || acc > best) {
-                best = acc;
-                bestRow = r;
-              }
-            }
-          }
-#pragma unroll
-          for (int off = 1; off < 4; off <<= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-            const int orow = __shfl_xor_sync(0xffffffffu, bestRow, off);
-            if (orow != 0x7fffffff && (bestRow == 0x7fffffff || ob > best || (ob == best && orow < bestRow))) {
-              best = ob;
-              bestRow = orow;
-            }
-          }
-          if (valid && sub == 0) {
-            const int s = v.s0 + li;
-            if (dn) {
-              if (POLICY) v.policy[s] = v.r0 + rb;  // numerics.hpp:114-115
-            } else if (POLICY) {
-              v.policy[s] = v.r0 + bestRow;
-            } else {
-              v.y[s] = best;
-              dl = fmax(dl, fabs(__dsub_rn(best, xS[li])));
-            }
-          }
-        }
-      } else
-#endif
       if (tid < v.ns) {
         const int s = v.s0 + tid;
         const int rb = tid ? rowE[tid - 1] : 0, re = rowE[tid];
@@ -1141,7 +1067,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
               const int ke = trnE[r];
               double acc = __ldg(crho + clsS[r]);
               if (k < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[k]), xwS[succS[k]]));
-              if (k + 1 < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[k + 1]), xwS[succS[k + 1]]));
+                if (k + 1 < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[k + 1]), xwS[succS[k + 1]]));
               k = ke;
               return acc;
             };
