@@ -367,6 +367,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e_ms, e_backups = None, 0.0
     if not streamed:  # a streamed instance has no host copy to re-upload
+        up0 = solver.cuda_stats()["upload_bytes"]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e2e_steps):
@@ -377,6 +378,7 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1)
+        h2d = (solver.cuda_stats()["upload_bytes"] - up0) / e2e_steps  # bytes the uploads actually copied
 
     peak, peak_src = peak_hbm()
     achieved = cs["opt_bytes"] / (cs["opt_ms"] * 1e-3) / 1e9 if cs["opt_ms"] > 0 else None

@@ -100,9 +100,13 @@ int morap_cuda_release_models(morap_ctx* ctx);
  * compact alphabet (<= 256 distinct probabilities and objective tuples) is stored without
  * its fp64 prob / objective arrays -- the device reads the exact same values from the
  * model's dictionary and class table. Lean models take weighted optimize jobs and
- * policy-chain evaluations (<= 4 objectives), not explicit reward vectors. */
+ * policy-chain evaluations (<= 4 objectives), not explicit reward vectors. Applies to
+ * models uploaded after the call, and only where the compact sweep kernels run (with
+ * MORAP_COMPACT=0 or MORAP_SWEEP_KERNEL=global every model keeps its arrays). */
 int morap_cuda_set_lean(morap_ctx* ctx, int on);
 int morap_cuda_num_models(morap_ctx* ctx);
+/* out[6] = {S, R, nnz, number of objectives, compact (0/1), lean (0/1)} of a device model. */
+int morap_cuda_model_info(morap_ctx* ctx, int model_id, int32_t* out);
 
 /* JobKind::Optimize batch (engine.hpp:126-131 -> numerics.hpp:74). Job k runs on model
  * model_ids[k] with rho = weightedReward(objectives, weights[k*K .. k*K+K-1])
@@ -156,7 +160,8 @@ int morap_cuda_fetch_eval_values(morap_ctx* ctx, int job, int rhs, double* value
  *   profiling is on: CUDA events around each launch, no extra synchronisation), out[2] algorithmic bytes those
  *   launches moved (12*nnz + 12*R + 21*S per active job per sweep),
  *   out[3] nnz backups performed (sum over jobs of sweeps * nnz), out[4..7] the same four
- *   for evaluate sweeps, out[8] kernels launched in total. */
+ *   for evaluate sweeps, out[8] kernels launched in total, out[9] host-to-device bytes of model
+ *   uploads. */
 int morap_cuda_set_profiling(morap_ctx* ctx, int on);
 int morap_cuda_stats(morap_ctx* ctx, double* out, int nout);
 int morap_cuda_reset_stats(morap_ctx* ctx);

@@ -276,10 +276,10 @@ class Solver:
     def cuda_stats(self) -> dict:
         from .cuda import load_library
         lib = load_library()
-        out = np.zeros(9)
-        lib.morap_cuda_stats(self.cuda_ctx, _ptr(out), 9)
+        out = np.zeros(10)
+        lib.morap_cuda_stats(self.cuda_ctx, _ptr(out), 10)
         keys = ["opt_launches", "opt_ms", "opt_bytes", "opt_backups", "eval_launches", "eval_ms", "eval_bytes",
-                "eval_state_backups", "kernels"]
+                "eval_state_backups", "kernels", "upload_bytes"]
         return dict(zip(keys, out.tolist()))
 
     def reset_cuda_stats(self):

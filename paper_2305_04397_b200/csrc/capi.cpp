@@ -314,7 +314,7 @@ int morap_instance_warehouse_streamed(const char* config_json, int threads, mora
     morap::WarehouseConfig cfg = morap::warehouseConfigFromJson(morap::Json::parse(config_json));
     morap::GpuBackend& gpu = *s->gpu;
     const morap::ProductSink sink = [&](const std::vector<morap::ProductMdp*>& fresh) {
-      gpu.uploadProducts(std::vector<const morap::ProductMdp*>(fresh.begin(), fresh.end()));
+      gpu.uploadProducts(std::vector<const morap::ProductMdp*>(fresh.begin(), fresh.end()), gpu.lean());
       std::vector<std::thread> pool;
       const size_t T = std::max(1u, std::thread::hardware_concurrency());
       for (size_t t = 0; t < T; ++t)

@@ -86,30 +86,50 @@ GpuBackend::~GpuBackend() {
 void GpuBackend::release() {
   check(ctx_, morap_cuda_release_models(ctx_), "release models");
   ids_.clear();
+  fullIds_.clear();
 }
 
-int GpuBackend::modelId(const ProductMdp* p) {
+bool GpuBackend::isLean(int id) {
+  int32_t info[6];
+  check(ctx_, morap_cuda_model_info(ctx_, id, info), "model info");
+  return info[5] != 0;
+}
+
+// Pareto-query uploads are lean when the objectives fit the policy-chain evaluation
+// (K <= 4): compact products then travel without their fp64 arrays. Jobs with an explicit
+// reward vector (runBatch, optimalScheduler, evaluateScheduler) need those arrays and get a
+// full copy of such a product on first use.
+int GpuBackend::modelId(const ProductMdp* p, bool full) {
   auto it = ids_.find(p->uid);
-  if (it != ids_.end()) return it->second;
+  if (full) {
+    if (it != ids_.end() && !isLean(it->second)) return it->second;
+    auto f = fullIds_.find(p->uid);
+    if (f != fullIds_.end()) return f->second;
+  } else if (it != ids_.end()) {
+    return it->second;
+  }
   std::vector<const double*> objs = objectivesOf(*p);
   std::vector<uint8_t> done;
   morap_csr_view v = viewOf(*p, objs, done);
+  const bool lean = !full && leanDefault_ && objs.size() <= 4;
+  check(ctx_, morap_cuda_set_lean(ctx_, lean ? 1 : 0), "set lean");
   int32_t id = -1;
   check(ctx_, morap_cuda_upload(ctx_, 1, &v, &id), "upload model");
-  ids_.emplace(p->uid, id);
+  (full ? fullIds_ : ids_).emplace(p->uid, id);
   return id;
 }
 
 int GpuBackend::modelIdFor(uint64_t uid, const morap_csr_view& view) {
   auto it = ids_.find(uid);
   if (it != ids_.end()) return it->second;
+  check(ctx_, morap_cuda_set_lean(ctx_, 0), "set lean");
   int32_t id = -1;
   check(ctx_, morap_cuda_upload(ctx_, 1, &view, &id), "upload model");
   ids_.emplace(uid, id);
   return id;
 }
 
-void GpuBackend::setLean(bool on) { check(ctx_, morap_cuda_set_lean(ctx_, on ? 1 : 0), "set lean"); }
+void GpuBackend::setLean(bool on) { leanDefault_ = on; }
 
 void GpuBackend::uploadInstance(const MorapInstance& inst) {
   std::vector<const ProductMdp*> todo;
@@ -117,10 +137,10 @@ void GpuBackend::uploadInstance(const MorapInstance& inst) {
   for (const auto& row : inst.products)
     for (const auto& p : row)
       if (!ids_.count(p->uid) && queued.insert(p->uid).second) todo.push_back(p.get());
-  uploadProducts(todo);
+  uploadProducts(todo, leanDefault_ && inst.objectives <= 4);
 }
 
-void GpuBackend::uploadProducts(const std::vector<const ProductMdp*>& products) {
+void GpuBackend::uploadProducts(const std::vector<const ProductMdp*>& products, bool lean) {
   std::vector<const ProductMdp*> todo;
   std::set<uint64_t> queued;
   for (const ProductMdp* p : products)
@@ -133,6 +153,7 @@ void GpuBackend::uploadProducts(const std::vector<const ProductMdp*>& products) 
     objs[k] = objectivesOf(*todo[k]);
     views[k] = viewOf(*todo[k], objs[k], done[k]);
   }
+  check(ctx_, morap_cuda_set_lean(ctx_, lean ? 1 : 0), "set lean");
   std::vector<int32_t> ids(todo.size());
   check(ctx_, morap_cuda_upload(ctx_, static_cast<int>(todo.size()), views.data(), ids.data()), "upload instance");
   for (size_t k = 0; k < todo.size(); ++k) ids_.emplace(todo[k]->uid, ids[k]);
@@ -155,7 +176,7 @@ OptimizeResult optimalScheduler(GpuBackend& gpu, const ProductMdp& p, const Rewa
                                 int sweepCap) {
   if (static_cast<int>(rho.size()) != productRows(p))
     fail(Errc::DimensionMismatch, "reward structure does not match action rows");
-  const int32_t id = gpu.modelId(&p);
+  const int32_t id = gpu.modelId(&p, true);
   const double* r = rho.data();
   double value = 0, resid = 0;
   int32_t sweeps = 0, status = 0;
@@ -182,7 +203,7 @@ EvaluateResult evaluateScheduler(GpuBackend& gpu, const ProductMdp& p, const Sch
   if (static_cast<int>(rho.size()) != productRows(p))
     fail(Errc::DimensionMismatch, "reward structure does not match action rows");
   if (static_cast<int>(mu.rows.size()) != p.mdp.numStates) fail(Errc::InvalidModel, "scheduler does not cover every state");
-  const int32_t id = gpu.modelId(&p);
+  const int32_t id = gpu.modelId(&p, true);
   const int32_t* pol = mu.rows.data();
   const double* r = rho.data();
   double value = 0, resid = 0;
@@ -242,7 +263,7 @@ std::map<long, JobResult> runBatch(std::vector<Job> jobs, GpuBackend& gpu) {
       std::vector<const int32_t*> pol(n);
       std::vector<double> value(n), resid(n);
       for (size_t k = 0; k < n; ++k) {
-        ids[k] = gpu.modelId(grp[k]->model.get());
+        ids[k] = gpu.modelId(grp[k]->model.get(), true);
         rho[k] = grp[k]->reward.data();
         pol[k] = grp[k]->scheduler.rows.data();
       }

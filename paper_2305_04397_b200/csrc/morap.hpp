@@ -228,10 +228,12 @@ class GpuBackend {
   ~GpuBackend();
   GpuBackend(const GpuBackend&) = delete;
   GpuBackend& operator=(const GpuBackend&) = delete;
-  int modelId(const ProductMdp* p);           // uploads on first use
+  // device model of p, uploaded on first use; full = with its fp64 arrays (explicit-reward jobs)
+  int modelId(const ProductMdp* p, bool full = false);
   void uploadInstance(const MorapInstance& inst);  // all distinct products in one batch
-  void uploadProducts(const std::vector<const ProductMdp*>& products);  // one batch, skips resident ones
-  void setLean(bool on);  // morap_cuda_set_lean: compact-alphabet models without fp64 arrays
+  void uploadProducts(const std::vector<const ProductMdp*>& products, bool lean);  // skips resident ones
+  void setLean(bool on);  // default for query uploads (on): compact products without fp64 arrays
+  bool lean() const { return leanDefault_; }
   int modelIdFor(uint64_t uid, const morap_csr_view& view);  // any model keyed by a process-unique id
   morap_ctx* ctx() const { return ctx_; }
   int device() const { return device_; }
@@ -240,7 +242,10 @@ class GpuBackend {
  private:
   morap_ctx* ctx_ = nullptr;
   int device_ = 0;
-  std::map<uint64_t, int> ids_;  // ProductMdp::uid -> device model id
+  std::map<uint64_t, int> ids_;      // ProductMdp::uid -> device model id (query uploads)
+  std::map<uint64_t, int> fullIds_;  // full copies of lean products (explicit-reward jobs)
+  bool leanDefault_ = true;
+  bool isLean(int id);
 };
 
 OptimizeResult optimalScheduler(GpuBackend& gpu, const ProductMdp& p, const RewardStructure& rho, double eps = 1e-6,

@@ -1956,7 +1956,7 @@ struct morap_ctx {
   std::string err;
   bool profiling = false;
   bool trace = std::getenv("MORAP_TRACE") != nullptr;
-  double stats[9] = {0};
+  double stats[10] = {0};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   std::vector<HostModel> hm;
@@ -2256,15 +2256,31 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
   if (K < 1) return;
   c.idx.resize(static_cast<size_t>(v.nnz));
   SmallIds probs(1);
+  // the first few distinct values are matched by a linear scan (warehouse products have
+  // three probabilities), the rest through the hash table
+  constexpr int kScan = 8;
+  uint64_t seen[kScan];
+  int nseen = 0;
   uint64_t last = ~0ull;
   int lastId = -1;
   for (int k = 0; k < v.nnz; ++k) {
     uint64_t b;
     std::memcpy(&b, &v.prob[k], 8);
     if (b != last) {
-      lastId = probs.find(&b);
-      if (lastId < 0) return;
-      if (lastId == static_cast<int>(c.dict.size())) c.dict.push_back(v.prob[k]);
+      lastId = -1;
+      for (int q = 0; q < nseen; ++q)
+        if (seen[q] == b) {
+          lastId = q;
+          break;
+        }
+      if (lastId < 0) {
+        lastId = probs.find(&b);
+        if (lastId < 0) return;
+        if (lastId == static_cast<int>(c.dict.size())) {
+          c.dict.push_back(v.prob[k]);
+          if (nseen < kScan && lastId == nseen) seen[nseen++] = b;
+        }
+      }
       last = b;
     }
     c.idx[k] = static_cast<uint8_t>(lastId);
@@ -2280,7 +2296,14 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
       c.cls[r] = static_cast<uint8_t>(prevId);
       continue;
     }
-    const int id = classes.find(key);
+    int id = -1;
+    const int ncls = static_cast<int>(c.table.size()) / K;
+    for (int q = 0; q < ncls && q < kScan; ++q)  // small alphabets: linear scan of the table
+      if (std::memcmp(&c.table[static_cast<size_t>(q) * K], key, 8ull * K) == 0) {
+        id = q;
+        break;
+      }
+    if (id < 0) id = classes.find(key);
     if (id < 0) return;
     std::memcpy(prev, key, 8ull * K);
     prevId = id;
@@ -2968,19 +2991,34 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
       std::fprintf(stderr, "[morap] upload %d models: %s at %.3f ms\n", nmodels, what,
                    1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tu0).count());
   };
+  std::atomic<long long> phaseNs[4] = {0, 0, 0, 0};  // trace: validate, tiles, compact, streams
   parallel_for(nmodels, [&](int m) {
     morap_ctx scratch;  // per-model error text
+    auto tp = std::chrono::steady_clock::now();
+    auto lapP = [&](int k) {
+      if (!ctx->trace) return;
+      const auto now = std::chrono::steady_clock::now();
+      phaseNs[k] += std::chrono::duration_cast<std::chrono::nanoseconds>(now - tp).count();
+      tp = now;
+    };
     status[m] = validate_view(&scratch, models[m], m);
+    lapP(0);
     if (status[m]) {
       why[m] = scratch.err;
       return;
     }
     make_tiles(models[m], tiles[m], descs[m]);
+    lapP(1);
     if (ctx->useCompact) {
       build_compact(models[m], compact[m]);
+      lapP(2);
       if (compact[m].ok) build_window_offsets(models[m], descs[m], compact[m]);
+      lapP(3);
     }
   });
+  if (ctx->trace)
+    std::fprintf(stderr, "[morap] upload prep thread-ms: validate %.1f, tiles %.1f, compact %.1f, streams %.1f\n",
+                 phaseNs[0] * 1e-6, phaseNs[1] * 1e-6, phaseNs[2] * 1e-6, phaseNs[3] * 1e-6);
   for (int m = 0; m < nmodels; ++m)
     if (status[m]) return ctx->fail(status[m], why[m]);
   lapU("validated, tiled, compacted");
@@ -2990,7 +3028,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   for (int m = 0; m < nmodels; ++m) {
     const morap_csr_view& v = models[m];
     off[m] = bytes;
-    const bool lean = ctx->lean && compact[m].ok;
+    const bool lean = ctx->lean && compact[m].ok && ctx->useTma;
     bytes += align_up(4ull * (v.num_states + 1), 256) + align_up(4ull * (v.num_rows + 1), 256) +
              align_up(4ull * v.nnz, 256) + (lean ? 0 : align_up(8ull * v.nnz, 256)) + align_up(1ull * v.num_states, 256) +
              (lean ? 0 : static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256)) +
@@ -3036,6 +3074,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   const int first = static_cast<int>(ctx->hm.size());
   std::vector<DevModel> built(nmodels);
   std::atomic<bool> copyFailed{false};
+  std::atomic<long long> uploadBytes{0};
   parallel_for(nmodels, [&](int m) {
     const morap_csr_view& v = models[m];
     char* h = host + off[m];
@@ -3052,7 +3091,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     dmod.rowOffset = reinterpret_cast<const int32_t*>(put(v.row_offset, 4ull * (v.num_states + 1)));
     dmod.trnOffset = reinterpret_cast<const int32_t*>(put(v.trn_offset, 4ull * (v.num_rows + 1)));
     dmod.succ = reinterpret_cast<const int32_t*>(put(v.succ, 4ull * v.nnz));
-    const bool lean = ctx->lean && compact[m].ok;  // fp64 prob / objectives live in the tables
+    const bool lean = ctx->lean && compact[m].ok && ctx->useTma;  // fp64 prob / objectives live in the tables
     if (!lean) dmod.prob = reinterpret_cast<const double*>(put(v.prob, 8ull * v.nnz));
     dmod.done = reinterpret_cast<const uint8_t*>(put(v.done, v.num_states));
     if (!lean)
@@ -3096,6 +3135,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     built[m] = dmod;
     // this model's block goes out as soon as it is packed (copies overlap the packing)
     const size_t len = static_cast<size_t>(h - (host + off[m]));
+    uploadBytes += static_cast<long long>(len);
     cudaSetDevice(ctx->device);  // packing runs on pool threads
     if (cudaMemcpyAsync(static_cast<char*>(dev) + off[m], host + off[m], len, cudaMemcpyHostToDevice, ctx->stream) !=
         cudaSuccess)
@@ -3108,6 +3148,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     if (ids_out) ids_out[m] = first + m;
   }
   lapU("packed, copies queued");
+  ctx->stats[9] += static_cast<double>(uploadBytes.load());
   cudaError_t e = copyFailed ? cudaErrorUnknown : cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return ctx->cudaFail(e, "upload copy", __LINE__);
   lapU("copied");
@@ -3132,6 +3173,15 @@ int morap_cuda_release_models(morap_ctx* ctx) {
 }
 
 int morap_cuda_num_models(morap_ctx* ctx) { return ctx ? static_cast<int>(ctx->hm.size()) : -1; }
+
+int morap_cuda_model_info(morap_ctx* ctx, int id, int32_t* out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  if (id < 0 || id >= static_cast<int>(ctx->hm.size())) return ctx->fail(MORAP_INVALID_CONFIG, "unknown model id");
+  const DevModel& d = ctx->dm[static_cast<size_t>(id)];
+  const int32_t v[6] = {d.S, d.R, d.nnz, d.K, d.compact, d.prob ? 0 : 1};
+  std::memcpy(out, v, sizeof v);
+  return MORAP_OK;
+}
 
 int morap_cuda_optimize(morap_ctx* ctx, int njobs, const int32_t* model_ids, const double* weights, int K, double eps,
                         int sweep_cap, double* value_out, int32_t* sweeps_out, double* residual_out,
@@ -3351,7 +3401,7 @@ int morap_cuda_set_profiling(morap_ctx* ctx, int on) {
 
 int morap_cuda_stats(morap_ctx* ctx, double* out, int nout) {
   if (!ctx) return MORAP_INVALID_CONFIG;
-  for (int i = 0; i < nout && i < 9; ++i) out[i] = ctx->stats[i];
+  for (int i = 0; i < nout && i < 10; ++i) out[i] = ctx->stats[i];
   return MORAP_OK;
 }
 

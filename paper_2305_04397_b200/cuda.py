@@ -60,6 +60,7 @@ def load_library(path: str = CUDA_SO) -> C.CDLL:
         "morap_cuda_fetch_eval_values": (i32, [p, i32, i32, p]),
         "morap_cuda_set_profiling": (i32, [p, i32]),
         "morap_cuda_set_lean": (i32, [p, i32]),
+        "morap_cuda_model_info": (i32, [p, i32, p]),
         "morap_cuda_stats": (i32, [p, p, i32]),
         "morap_cuda_reset_stats": (i32, [p]),
         "morap_cuda_device_bytes": (i32, [p, p]),
@@ -229,10 +230,10 @@ class CudaBackend:
         self._check(self.lib.morap_cuda_set_profiling(self.h, int(on)), "set_profiling")
 
     def stats(self) -> dict:
-        out = np.zeros(9)
-        self._check(self.lib.morap_cuda_stats(self.h, _ptr(out), 9), "stats")
+        out = np.zeros(10)
+        self._check(self.lib.morap_cuda_stats(self.h, _ptr(out), 10), "stats")
         keys = ["opt_launches", "opt_ms", "opt_bytes", "opt_backups", "eval_launches", "eval_ms", "eval_bytes",
-                "eval_state_backups", "kernels"]
+                "eval_state_backups", "kernels", "upload_bytes"]
         return dict(zip(keys, out.tolist()))
 
     def reset_stats(self):
