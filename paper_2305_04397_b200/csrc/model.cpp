@@ -159,14 +159,26 @@ bool checkRewardFinite(const ProductMdp& p) { return checkRewardFinite(p.mdp, p.
 
 namespace {
 
+// Dedup key of a product (bucketing only -- equality is checked array by array): four
+// independent multiply-rotate lanes over 8-byte words, ~10x faster than a byte-wise FNV
+// on the ~10 MB of a C4 product.
 struct Fnv {
-  uint64_t h = 1469598103934665603ull;
+  uint64_t lane[4] = {0x9e3779b97f4a7c15ull, 0xc2b2ae3d27d4eb4full, 0x165667b19e3779f9ull, 0x27d4eb2f165667c5ull};
+  static uint64_t mix(uint64_t h, uint64_t w) {
+    h ^= w * 0x9fb21c651e98df25ull;
+    return ((h << 29) | (h >> 35)) * 0xff51afd7ed558ccdull;
+  }
   void bytes(const void* p, size_t n) {
     const unsigned char* c = static_cast<const unsigned char*>(p);
-    for (size_t i = 0; i < n; ++i) {
-      h ^= c[i];
-      h *= 1099511628211ull;
+    size_t i = 0;
+    for (; i + 32 <= n; i += 32) {
+      uint64_t w[4];
+      std::memcpy(w, c + i, 32);
+      for (int k = 0; k < 4; ++k) lane[k] = mix(lane[k], w[k]);
     }
+    uint64_t tail = n;
+    for (; i < n; ++i) tail = (tail << 8 | tail >> 56) ^ c[i];
+    lane[0] = mix(lane[0], tail);
   }
   template <class T>
   void vec(const std::vector<T>& v) {
@@ -174,6 +186,7 @@ struct Fnv {
     bytes(&n, sizeof n);
     if (!v.empty()) bytes(v.data(), v.size() * sizeof(T));
   }
+  uint64_t digest() const { return mix(mix(lane[0], lane[1]), mix(lane[2], lane[3])); }
 };
 
 }  // namespace
@@ -190,7 +203,7 @@ uint64_t productHash(const ProductMdp& p) {
   f.vec(p.success);
   f.vec(p.done);
   f.vec(p.accept);
-  return f.h;
+  return f.digest();
 }
 
 ProductMdp buildProduct(const Mdp& agent, const RewardStructure& agentCost, const Dfa& task, int agentId, int taskId) {
