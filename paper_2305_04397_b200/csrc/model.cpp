@@ -246,6 +246,16 @@ ProductMdp buildProduct(const Mdp& agent, const RewardStructure& agentCost, cons
   Mdp& M = p.mdp;
   M.initial = visit(agent.initial, q0);
   M.trnOffset.push_back(0);
+  std::vector<int> rowName;  // agent row of each product row (-1: internal), names filled at the end
+  {
+    const size_t guess = static_cast<size_t>(agent.numActions()) * static_cast<size_t>(Q) / 2;
+    rowName.reserve(guess);
+    M.trnOffset.reserve(guess + 1);
+    M.succ.reserve(guess + guess / 4);
+    M.prob.reserve(guess + guess / 4);
+    p.cost.reserve(guess);
+    p.success.reserve(guess);
+  }
   for (size_t x = 0; x < as.size(); ++x) {
     const int s = as[x], q = qs[x];
     M.rowOffset.push_back(M.numActions());
@@ -253,7 +263,7 @@ ProductMdp buildProduct(const Mdp& agent, const RewardStructure& agentCost, cons
       M.succ.push_back(visit(s, task.step(q, letter[s])));
       M.prob.push_back(1.0);
       M.trnOffset.push_back(static_cast<int>(M.succ.size()));
-      M.actionName.push_back(kInternalAction);
+      rowName.push_back(-1);
       p.cost.push_back(0.0);
       p.success.push_back(1.0);
       continue;
@@ -265,13 +275,16 @@ ProductMdp buildProduct(const Mdp& agent, const RewardStructure& agentCost, cons
         M.prob.push_back(agent.prob[k]);
       }
       M.trnOffset.push_back(static_cast<int>(M.succ.size()));
-      M.actionName.push_back(agent.actionName[r]);
+      rowName.push_back(r);
       p.cost.push_back(agentCost[r]);
       p.success.push_back(0.0);
     }
   }
   M.numStates = static_cast<int>(as.size());
   M.rowOffset.push_back(M.numActions());
+  M.actionName.resize(rowName.size());
+  for (size_t r = 0; r < rowName.size(); ++r)
+    M.actionName[r] = rowName[r] < 0 ? kInternalAction : agent.actionName[static_cast<size_t>(rowName[r])];
   M.labels.assign(static_cast<size_t>(M.numStates), {});
   p.agentState = as;
   p.dfaLocation = qs;
