@@ -62,7 +62,8 @@ def build_host(force: bool = False) -> str:
         return HOST_SO
     obj_dir = os.path.join(ROOT, "build", "host")
     os.makedirs(obj_dir, exist_ok=True)
-    flags = ["-std=c++20", "-O2", "-fPIC", "-pthread", "-ffp-contract=off", f"-I{os.path.join(ROOT, 'include')}",
+    # -O3 vectorises the elementwise loops (bit-identical: no FMA, reductions keep their order)
+    flags = ["-std=c++20", "-O3", "-mavx2", "-fPIC", "-pthread", "-ffp-contract=off", f"-I{os.path.join(ROOT, 'include')}",
              f"-I{CSRC}", f"-I{JSON_DIR}"]
     hdrs = [os.path.join(CSRC, n) for n in os.listdir(CSRC) if n.endswith(".hpp")] + \
         [os.path.join(ROOT, "include", n) for n in os.listdir(os.path.join(ROOT, "include"))]
