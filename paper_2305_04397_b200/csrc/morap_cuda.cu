@@ -228,6 +228,20 @@ __global__ void __launch_bounds__(kBlock) k_weighted_reward(const DevModel* __re
   }
 }
 
+// classRho of every active compact job (one CTA per job): the same rounded combination as
+// weightedReward for each reward class, rho_w[r] == classRho[rclass[r]].
+__global__ void __launch_bounds__(kBlock) k_class_rho(const DevModel* __restrict__ models,
+                                                      const OptJob* __restrict__ jobs,
+                                                      const int32_t* __restrict__ list) {
+  const OptJob& J = jobs[list[blockIdx.x]];
+  const DevModel& M = models[J.model];
+  for (int c = threadIdx.x; c < M.nclass; c += blockDim.x) {
+    double acc = 0.0;
+    for (int o = 0; o < M.K; ++o) acc = __dadd_rn(acc, __dmul_rn(J.w[o], M.classTable[c * M.K + o]));
+    J.classRho[c] = acc;
+  }
+}
+
 // --------------------------------------------------------------------------------------
 // K1: one greedy Jacobi sweep over the tiles of every active optimize job
 // (numerics.hpp:86-104). Phase 1: threads own action rows (coalesced trnOffset / rho /
@@ -2619,6 +2633,10 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
       const HostModel& m = ctx->hm[model_ids[j]];
       if (m.R) CK(cudaMemcpyAsync(ctx->hOptJobs[j].rho, rhoHost[j], sizeof(double) * m.R, cudaMemcpyHostToDevice, ctx->stream));
     }
+  } else if (!active.empty() && allCompact) {  // rho_w per reward class only: one CTA per job
+    k_class_rho<<<static_cast<int>(active.size()), kBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, ctx->dList);
+    CK(cudaGetLastError());
+    ctx->stats[8] += 1;
   } else if (!active.empty()) {
     k_weighted_reward<<<ctx->sweepBlocks, kBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, ctx->dList,
                                                                     ctx->dPrefix, ctx->hCtl->nactive,
