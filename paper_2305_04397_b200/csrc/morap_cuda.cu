@@ -838,6 +838,121 @@ static_assert(kCOffTrn % 16 == 0 && kCOffSucc % 16 == 0 && kCOffIdx % 16 == 0 &&
 constexpr int kCFbRows = kXWin + 2 < kRowCap ? kXWin + 2 : kRowCap;  // fallback row values in the window region
 constexpr int kCmpSmemBytes = kCmpStages * kCStageBytes;
 
+// Arguments of the finalize step fused into the compact sweep (count == nullptr: none).
+struct FinArgs {
+  unsigned* count;  // CTAs finished in this launch; reset by the last one
+  const int32_t* jobModel;
+  double eps;
+  int cap;
+  int32_t* sweeps;
+  double* residual;
+  int32_t* status;
+};
+
+// exclusive scan of (a, b) over the whole block (any multiple of 32 threads <= 1024)
+__device__ __forceinline__ void block_scan2n(int& a, int& b, int* sa, int* sb, int& totA, int& totB) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int xa = a, xb = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int ya = __shfl_up_sync(0xffffffffu, xa, o), yb = __shfl_up_sync(0xffffffffu, xb, o);
+    if (lane >= o) {
+      xa += ya;
+      xb += yb;
+    }
+  }
+  if (lane == 31) {
+    sa[wid] = xa;
+    sb[wid] = xb;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    int va = lane < nw ? sa[lane] : 0, vb = lane < nw ? sb[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ya = __shfl_up_sync(0xffffffffu, va, o), yb = __shfl_up_sync(0xffffffffu, vb, o);
+      if (lane >= o) {
+        va += ya;
+        vb += yb;
+      }
+    }
+    sa[lane] = va;
+    sb[lane] = vb;
+  }
+  __syncthreads();
+  const int offA = wid ? sa[wid - 1] : 0, offB = wid ? sb[wid - 1] : 0;
+  totA = sa[nw - 1];
+  totB = sb[nw - 1];
+  a = offA + xa - a;
+  b = offB + xb - b;
+  __syncthreads();
+}
+
+// Per-job stop test after an optimize sweep (numerics.hpp:105-112) and compaction of the
+// active list / tile prefix, by one block (k_finalize's body for the optimize kind).
+__device__ void finalize_opt(const DevModel* __restrict__ models, const int32_t* __restrict__ jobModel,
+                             int32_t* list, int32_t* prefix, Ctl* ctl, unsigned long long* deltaBits, double eps,
+                             int cap, int32_t* sweeps, double* residual, int32_t* status) {
+  __shared__ int sa[32], sb[32];
+  __shared__ unsigned long long sBytes[32], sBk[32];
+  const int nact = __ldcg(&ctl->nactive);
+  if (nact == 0) return;
+  const int k = __ldcg(&ctl->sweepsDone) + 1;  // sweeps completed including the one just run
+  int outBase = 0, tileBase = 0;
+  unsigned long long bytes = 0, backups = 0;
+  for (int base = 0; base < nact; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    int keep = 0, nt = 0, job = -1;
+    if (i < nact) {
+      job = __ldcg(list + i);
+      const DevModel& M = models[jobModel[job]];
+      const double d = __longlong_as_double(static_cast<long long>(__ldcg(deltaBits + job)));
+      deltaBits[job] = 0ull;
+      sweeps[job] = k;
+      residual[job] = d;
+      bytes += M.bytesPerSweep;
+      backups += static_cast<unsigned long long>(M.nnz);
+      if (d <= eps) status[job] = MORAP_OK;
+      else if (k >= cap) status[job] = MORAP_NON_CONVERGENCE;
+      else keep = 1;
+      if (keep) nt = M.ntiles;
+    }
+    int pa = keep, pb = nt, ta, tb;
+    block_scan2n(pa, pb, sa, sb, ta, tb);
+    if (keep) {
+      list[outBase + pa] = job;
+      prefix[outBase + pa] = tileBase + pb;
+    }
+    outBase += ta;
+    tileBase += tb;
+    __syncthreads();
+  }
+  unsigned long long vb = bytes, vk = backups;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    vb += __shfl_xor_sync(0xffffffffu, vb, o);
+    vk += __shfl_xor_sync(0xffffffffu, vk, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sBytes[threadIdx.x >> 5] = vb;
+    sBk[threadIdx.x >> 5] = vk;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tbytes = 0, tk = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      tbytes += sBytes[w];
+      tk += sBk[w];
+    }
+    prefix[outBase] = tileBase;
+    ctl->nactive = outBase;
+    ctl->totalTiles = tileBase;
+    ctl->sweepsDone = k;
+    ctl->bytes += tbytes;
+    ctl->backups += tk;
+  }
+}
+
 struct CmpInfo {
   const int32_t* succG;  // absolute successors (out-of-window transitions)
   int t, job, fits, allIn, simple;
@@ -860,7 +975,8 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
                                                                      const int32_t* __restrict__ prefix,
                                                                      const Ctl* __restrict__ ctl,
                                                                      const int32_t* __restrict__ jobSweeps,
-                                                                     unsigned long long* __restrict__ deltaBits) {
+                                                                     unsigned long long* __restrict__ deltaBits,
+                                                                     FinArgs fin) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[kCmpStages], empty[kCmpStages];
   __shared__ CmpInfo info[kCmpStages];
@@ -873,9 +989,9 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
   const int per = (total + gridDim.x - 1) / gridDim.x;
   const int t0 = blockIdx.x * per;
   const int t1 = min(total, t0 + per);
-  if (t0 >= t1) return;
   const int k = ctl->sweepsDone;
   const int tid = threadIdx.x;
+  if (t0 < t1) {  // this CTA has tiles (the fused finalize below runs in every CTA)
   if (tid == 0) {
     for (int q = 0; q < kCmpStages; ++q) {
       mbar_init(&full[q], 1);
@@ -1023,8 +1139,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
       info[b].t = -1;
       mbar_arrive(&full[b]);
     }
-    return;
-  }
+  } else {  // compute warps
 
   // The residual max is carried per thread across the consecutive tiles of one job and
   // reduced over the CTA only when the job changes (a CTA's tiles are contiguous in the
@@ -1181,6 +1296,25 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
   if (!POLICY && runJob >= 0) {  // residual of the last job of this CTA's range
     runMax = consumer_max(runMax, sRed);
     if (tid == 0 && runMax > 0.0) atomicMax(deltaBits + runJob, (unsigned long long)__double_as_longlong(runMax));
+  }
+  }  // compute warps
+  }  // CTA has tiles
+  if (!POLICY && fin.count) {
+    // fused k_finalize: the last CTA to finish runs the per-job stop test and rebuilds the
+    // active list / tile prefix (every other CTA has read them and published its residuals)
+    __shared__ int sLast;
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      sLast = atomicAdd(fin.count, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (sLast) {
+      __threadfence();
+      finalize_opt(models, fin.jobModel, const_cast<int32_t*>(list), const_cast<int32_t*>(prefix),
+                   const_cast<Ctl*>(ctl), deltaBits, fin.eps, fin.cap, fin.sweeps, fin.residual, fin.status);
+      if (tid == 0) *fin.count = 0u;
+    }
   }
 }
 
@@ -2045,6 +2179,7 @@ struct morap_ctx {
   bool usePersistent = true;  // evaluate batches as one cooperative launch
   int persistBlocks = 0;
   unsigned* dBar = nullptr;   // grid-barrier counter + generation
+  unsigned* dFinCount = nullptr;  // CTAs done in the current compact sweep (fused finalize)
   void* persistArena = nullptr;
   size_t persistArenaBytes = 0;
   void* polStage = nullptr;  // pinned staging for batched policy reads
@@ -2405,8 +2540,9 @@ int enqueue_sweeps(morap_ctx* ctx, int kind, double eps, int cap, int B, const c
   for (int i = 0; i < B; ++i) {
     if (ev) CK(cudaEventRecordWithFlags(ev[2 * i], ctx->stream, evFlags));
     if (kind == 0 && ctx->useTma && ctx->optCompact) {
+      const FinArgs fin{ctx->dFinCount, ctx->dJobModel, eps, cap, ctx->dSweeps, ctx->dResidual, ctx->dStatus};
       k_greedy_sweep_cmp<false><<<ctx->cmpBlocks, kTmaThreads, kCmpSmemBytes, ctx->stream>>>(
-          ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
+          ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta, fin);
     } else if (kind == 0 && ctx->useTma) {
       k_greedy_sweep_tma<false><<<ctx->tmaBlocks, kTmaThreads, kTmaSmemBytes, ctx->stream>>>(
           ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
@@ -2423,7 +2559,9 @@ int enqueue_sweeps(morap_ctx* ctx, int kind, double eps, int cap, int B, const c
     }
     CK(cudaGetLastError());
     if (ev) CK(cudaEventRecordWithFlags(ev[2 * i + 1], ctx->stream, evFlags));
-    if (kind == 0)
+    if (kind == 0 && ctx->useTma && ctx->optCompact)
+      ;  // finalize fused into the compact sweep's last CTA
+    else if (kind == 0)
       k_finalize<false><<<1, kFinBlock, 0, ctx->stream>>>(ctx->dModels, ctx->dJobModel, ctx->dList, ctx->dPrefix,
                                                          ctx->dCtl, ctx->dDelta, ctx->dMask, ctx->dNrhs, eps, cap,
                                                          ctx->dSweeps, ctx->dResidual, ctx->dStatus);
@@ -2512,7 +2650,7 @@ int run_loop(morap_ctx* ctx, int kind, double eps, int cap) {
       }
       if ((rc = enqueue_sweeps(ctx, kind, eps, cap, batch, timed ? ctx->evPool.data() : nullptr, false))) return rc;
     }
-    ctx->stats[8] += 2 * batch;
+    ctx->stats[8] += (kind == 0 && ctx->useTma && ctx->optCompact ? 1 : 2) * batch;
     CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (timed) {
@@ -2687,7 +2825,7 @@ int extract_policies(morap_ctx* ctx, const std::vector<int32_t>& jobsIn) {
   CK(cudaMemcpyAsync(ctx->dSweeps, ctx->optSweeps.data(), ctx->optSweeps.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->useTma && ctx->optCompact)
     k_greedy_sweep_cmp<true><<<ctx->cmpBlocks, kTmaThreads, kCmpSmemBytes, ctx->stream>>>(
-        ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr);
+        ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr, FinArgs{});
   else if (ctx->useTma)
     k_greedy_sweep_tma<true><<<ctx->tmaBlocks, kTmaThreads, kTmaSmemBytes, ctx->stream>>>(
         ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr);
@@ -2919,6 +3057,11 @@ int morap_cuda_create(int device, morap_ctx** out) {
   ctx->persistBlocks = ctx->numSMs * persistPerSm;
   const char* psel = std::getenv("MORAP_PERSISTENT");  // "0" keeps per-sweep launches (A/B)
   ctx->usePersistent = coop && occP > 0 && !(psel && std::string(psel) == "0");
+  if (cudaMalloc(&ctx->dFinCount, sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(ctx->dFinCount, 0, sizeof(unsigned)) != cudaSuccess) {
+    morap_cuda_destroy(ctx);
+    return MORAP_CUDA_ERROR;
+  }
   if (cudaMalloc(&ctx->dBar, 2 * sizeof(unsigned)) != cudaSuccess || cudaMemset(ctx->dBar, 0, 2 * sizeof(unsigned)) != cudaSuccess)
     ctx->usePersistent = false;
   cudaFuncSetAttribute(k_eval_sweep_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kEvSmemBytes);
@@ -2967,6 +3110,7 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   cudaFree(ctx->evalStage);
   cudaFreeHost(ctx->stage);
   cudaFree(ctx->dBar);
+  cudaFree(ctx->dFinCount);
   cudaFree(ctx->persistArena);
   cudaFreeHost(ctx->polStage);
   for (cudaEvent_t e : ctx->evPool) cudaEventDestroy(e);
