@@ -1,6 +1,9 @@
 """C5 scaling sweep (BASELINE.json configs[4]): single warehouse products from 3x3 to 32x32
 grids (1e3 .. 1e7 transitions), K = 2, 3, 5 objectives; optimize throughput on the GPU vs
 the reference engine on one host thread (the reference runs one job per worker thread).
+Two GPU numbers per size: one job alone (a small model cannot fill a B200: launch/latency
+bound) and a batch of jobs on the same model with different weights, enough to stream
+~3e7 transitions per sweep (how the Pareto query uses the GPU: n^2 jobs per batch).
 Writes one JSON line per (grid, K)."""
 import json
 import sys
@@ -40,6 +43,18 @@ for W in grids:
                 "gpu_backups_per_s_wall": float(sw[0]) * p.nnz / wall,
                 "gpu_kernel_backups_per_s": s["opt_backups"] / (s["opt_ms"] * 1e-3),
                 "gpu_kernel_GBps": s["opt_bytes"] / (s["opt_ms"] * 1e-3) / 1e9, "wall_ms": wall * 1e3}
+        # a batch of jobs on the same model, different weights, ~3e7 transitions per sweep
+        nb = int(min(4096, max(1, round(3e7 / p.nnz))))
+        wb = np.random.default_rng(K).dirichlet(np.ones(K), size=nb)
+        be.optimize(np.repeat(ids, nb), wb)
+        be.reset_stats()
+        t0 = time.perf_counter()
+        vb, swb, rb, stb = be.optimize(np.repeat(ids, nb), wb)
+        wallb = time.perf_counter() - t0
+        sb = be.stats()
+        line.update(batch_jobs=nb, batch_backups_per_s_wall=float(np.sum(swb)) * p.nnz / wallb,
+                    batch_kernel_backups_per_s=sb["opt_backups"] / (sb["opt_ms"] * 1e-3),
+                    batch_kernel_GBps=sb["opt_bytes"] / (sb["opt_ms"] * 1e-3) / 1e9, batch_wall_ms=wallb * 1e3)
         if K == 2 and oracle.ref_available():
             ri = oracle.ref().warehouse(cfg)
             sec, bk = ri.optimize_phase(np.array([0.5, 0.5]), 1)
