@@ -953,18 +953,18 @@ __device__ void finalize_opt(const DevModel* __restrict__ models, const int32_t*
   }
 }
 
-struct CmpInfo {
-  const int32_t* succG;  // absolute successors (out-of-window transitions)
-  int t, job, fits, allIn, simple;
-  int s0, r0, k0, ns;
-  int offRow, offTrn, offSucc, offIdx, offCls, offDone, offX, offXw;
-  int wlo, wn;
+// Stage record the producer publishes per tile (seven 16-byte words: one vector store each).
+struct alignas(16) CmpInfo {
+  int t, job, fits, allIn;
+  int simple, s0, r0, k0;
+  int ns, offX, pad0, pad1;
   const double* dict;
   const double* classRho;
   const double* x;
   double* y;
   int32_t* policy;
   const DevModel* model;
+  const int32_t* succG;  // absolute successors (out-of-window transitions)
   const double* rho;
 };
 
@@ -1014,6 +1014,10 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     int use = 0;
     int curJob = -1;
     const unsigned char* myBase = nullptr;  // stream base of this lane for curJob
+    // per-lane stream constants: element size (log2) and stage region
+    const int laneSh = lane == 6 || lane == 7 ? 3 : (lane <= 2 ? 1 : 0);
+    const int laneDst = lane == 0 ? kCOffRow : lane == 1 ? kCOffTrn : lane == 2 ? kCOffSucc : lane == 3 ? kCOffIdx
+                      : lane == 4 ? kCOffCls : lane == 5 ? kCOffDone : lane == 6 ? kCOffX : kCOffXw;
     const DevModel* curM = nullptr;
     const OptJob* curJ = nullptr;
     int parity = k & 1;
@@ -1075,23 +1079,15 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           myBase = static_cast<const unsigned char*>(bp);
         }
         const int b = use % kCmpStages;
-        // stream of this lane: [lo, hi) in elements of 1 << sh bytes
-        long long lo = 0, hi = 0;
-        int sh = 0, dstOff = 0;
-        uint64_t lp = pol;
-        // lanes 0-5: tile-major padded streams (slice start from TilePos, 16-byte aligned)
+        // stream of this lane: [lo, hi) in elements of 1 << sh bytes, selected without
+        // branching (lanes 0-5: tile-major padded streams, slice start from TilePos)
         const int pos = lane < 6 ? sPos[q][lane] : 0;
-        switch (lane) {
-          case 0: lo = pos; hi = pos + (s1 - s0); sh = 1; dstOff = kCOffRow; break;
-          case 1: lo = pos; hi = pos + (r1 - r0); sh = 1; dstOff = kCOffTrn; break;
-          case 2: lo = pos; hi = pos + (k1 - k0); sh = 1; dstOff = kCOffSucc; break;
-          case 3: lo = pos; hi = pos + (k1 - k0); sh = 0; dstOff = kCOffIdx; break;
-          case 4: lo = pos; hi = pos + (r1 - r0); sh = 0; dstOff = kCOffCls; break;
-          case 5: lo = pos; hi = pos + (s1 - s0); sh = 0; dstOff = kCOffDone; break;
-          case 6: lo = s0; hi = s1; sh = 3; dstOff = kCOffX; lp = polKeep; break;
-          case 7: lo = wlo; hi = wlo + wn; sh = 3; dstOff = kCOffXw; lp = polKeep; break;
-          default: break;
-        }
+        const int len = lane == 0 || lane == 5 ? s1 - s0 : (lane == 1 || lane == 4 ? r1 - r0 : k1 - k0);
+        long long lo = lane < 6 ? pos : (lane == 6 ? s0 : wlo);
+        long long hi = lane < 6 ? pos + len : (lane == 6 ? s1 : wlo + wn);
+        if (lane > 7) lo = hi = 0;
+        const int sh = laneSh, dstOff = laneDst;
+        const uint64_t lp = lane >= 6 ? polKeep : pol;
         const long long a0 = (lo << sh) & ~15ll, z0 = ((hi << sh) + 15) & ~15ll;
         const uint32_t bytes =
             (myBase && fits && z0 > a0) ? static_cast<uint32_t>(z0 - a0) : 0u;
@@ -1099,29 +1095,29 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
         const uint32_t txBytes = __reduce_add_sync(0xffffffffu, bytes);
         if (use >= kCmpStages) mbar_wait_sleep(&empty[b], ((use / kCmpStages) - 1) & 1);
         // bookkeeping for the consumers: lane i < 8 writes its stream offset, lane 0 the rest
-        CmpInfo* v = &info[b];
-        int* offSlot = &v->offRow;
-        if (lane < 8) offSlot[lane] = off;
+        const int offX = __shfl_sync(0xffffffffu, off, 6);  // own x: front offset of lane 6's copy
         if (lane == 0) {
-          v->t = ti;
-          v->job = job;
-          v->fits = fits;
-          v->allIn = allIn;
-          v->simple = simple;
-          v->s0 = s0;
-          v->r0 = r0;
-          v->k0 = k0;
-          v->ns = s1 - s0;
-          v->wlo = wlo;
-          v->wn = wn;
-          v->dict = curM->probDict;
-          v->classRho = curJ->classRho;
-          v->x = curJ->buf[parity];
-          v->y = curJ->buf[parity ^ 1];
-          v->policy = curJ->policy;
-          v->model = curM;
-          v->rho = curJ->rho;
-          v->succG = curM->succ;
+          CmpInfo rec;
+          rec.t = ti;
+          rec.job = job;
+          rec.fits = fits;
+          rec.allIn = allIn;
+          rec.simple = simple;
+          rec.s0 = s0;
+          rec.r0 = r0;
+          rec.k0 = k0;
+          rec.ns = s1 - s0;
+          rec.offX = offX;
+          rec.pad0 = rec.pad1 = 0;
+          rec.dict = curM->probDict;
+          rec.classRho = curJ->classRho;
+          rec.x = curJ->buf[parity];
+          rec.y = curJ->buf[parity ^ 1];
+          rec.policy = curJ->policy;
+          rec.model = curM;
+          rec.succG = curM->succ;
+          rec.rho = curJ->rho;
+          info[b] = rec;
         }
         __syncwarp();
         uint64_t* bar = &full[b];
