@@ -2413,11 +2413,7 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
     std::memcpy(&b, &v.prob[k], 8);
     if (b != last) {
       lastId = -1;
-      for (int q = 0; q < nseen; ++q)
-        if (seen[q] == b) {
-          lastId = q;
-          break;
-        }
+      for (int q = 0; q < nseen; ++q) lastId = seen[q] == b ? q : lastId;  // branch-free (selects)
       if (lastId < 0) {
         lastId = probs.find(&b);
         if (lastId < 0) return;
@@ -2436,21 +2432,29 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
   uint64_t prev[MORAP_MAX_OBJECTIVES];
   int prevId = -1;
   for (int r = 0; r < v.num_rows; ++r) {
-    for (int o = 0; o < K; ++o) std::memcpy(&key[o], &v.rewards[o][r], 8);
-    if (prevId >= 0 && std::memcmp(key, prev, 8ull * K) == 0) {  // runs of equal rows
+    bool same = prevId >= 0;
+    for (int o = 0; o < K; ++o) {
+      std::memcpy(&key[o], &v.rewards[o][r], 8);
+      same = same && key[o] == prev[o];
+    }
+    if (same) {  // runs of equal rows
       c.cls[r] = static_cast<uint8_t>(prevId);
       continue;
     }
     int id = -1;
     const int ncls = static_cast<int>(c.table.size()) / K;
-    for (int q = 0; q < ncls && q < kScan; ++q)  // small alphabets: linear scan of the table
-      if (std::memcmp(&c.table[static_cast<size_t>(q) * K], key, 8ull * K) == 0) {
-        id = q;
-        break;
+    for (int q = 0; q < ncls && q < kScan && id < 0; ++q) {  // small alphabets: linear scan of the table
+      bool eq = true;
+      for (int o = 0; o < K && eq; ++o) {
+        uint64_t tb;
+        std::memcpy(&tb, &c.table[static_cast<size_t>(q) * K + o], 8);
+        eq = tb == key[o];
       }
+      if (eq) id = q;
+    }
     if (id < 0) id = classes.find(key);
     if (id < 0) return;
-    std::memcpy(prev, key, 8ull * K);
+    for (int o = 0; o < K; ++o) prev[o] = key[o];
     prevId = id;
     if (id == static_cast<int>(c.table.size()) / K)
       for (int o = 0; o < K; ++o) c.table.push_back(v.rewards[o][r]);
