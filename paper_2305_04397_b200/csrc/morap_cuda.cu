@@ -1672,6 +1672,7 @@ struct PersistArgs {
   Ctl* ctl;
   unsigned* barCount;
   unsigned* barGen;
+  int cacheStates;  // > 0: every CTA keeps its states' chains (<= 2 transitions) in shared memory
 };
 
 #ifndef MORAP_PERSIST_THREADS
@@ -1681,6 +1682,7 @@ struct PersistArgs {
 #define MORAP_PERSIST_MINB (1024 / MORAP_PERSIST_THREADS)  // 64 registers: 1024 threads per SM
 #endif
 constexpr int kPersistThreads = MORAP_PERSIST_THREADS;
+constexpr int kPersistCacheBytes = 200 * 1024;  // shared-memory chain cache per CTA (at most)
 // Only reached with <= kEvRhs RHS per job (the policy-chain path), so the per-thread
 // residual accumulators are kEvRhs wide; done states carry an empty chain and rhoC = 0,
 // so they compute y = 0 + 1.0 * 0 = +0.0, the pinned value, without a branch.
@@ -1703,6 +1705,29 @@ __global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_pe
       if (A.statePrefix[mid] <= i0) lo = mid; else hi = mid - 1;
     }
     jBase = lo;
+  }
+  // The CTA owns the same states in every sweep: with cacheStates its chains (count,
+  // successors, probabilities) are read once into shared memory, so a sweep's dependent
+  // chain is one L2 gather of x instead of chainOff -> chainSucc -> x.
+  extern __shared__ __align__(16) unsigned char esm[];
+  const int C = A.cacheStates;
+  uint8_t* sN = esm;
+  int32_t* sSucc = reinterpret_cast<int32_t*>(esm + ((C + 15) & ~15));
+  double* sProb = reinterpret_cast<double*>(esm + ((C + 15) & ~15) + 8 * static_cast<size_t>(C));
+  if (C > 0) {
+    int jl = jBase;
+    for (long long i = i0 + tid; i < i1; i += blockDim.x) {
+      while (i >= A.statePrefix[jl + 1]) ++jl;
+      const EvalJob& J = A.jobs[jl];
+      const int sl = static_cast<int>(i - A.statePrefix[jl]);
+      const int li = static_cast<int>(i - i0);
+      const int cbl = __ldg(J.chainOff + sl), nl = __ldg(J.chainOff + sl + 1) - cbl;
+      sN[li] = static_cast<uint8_t>(nl);
+      sSucc[2 * li] = nl > 0 ? __ldg(J.chainSucc + cbl) : 0;
+      sSucc[2 * li + 1] = nl > 1 ? __ldg(J.chainSucc + cbl + 1) : 0;
+      sProb[2 * li] = nl > 0 ? __ldg(J.chainProb + cbl) : 0.0;
+      sProb[2 * li + 1] = nl > 1 ? __ldg(J.chainProb + cbl + 1) : 0.0;
+    }
   }
   __syncthreads();
   unsigned long long bytesAcc = 0, backupsAcc = 0;
@@ -1751,6 +1776,23 @@ __global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_pe
           sv[u] = static_cast<int>(i - A.statePrefix[j]);
         }
       }
+      if (C > 0) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          cb[u] = 0;
+          n[u] = 0;
+          sc0[u] = sc1[u] = 0;
+          p0[u] = p1[u] = 0.0;
+          if (mk[u]) {
+            const int li = static_cast<int>(ib + u * bd - i0);
+            n[u] = sN[li];
+            sc0[u] = sSucc[2 * li];
+            sc1[u] = sSucc[2 * li + 1];
+            p0[u] = sProb[2 * li];
+            p1[u] = sProb[2 * li + 1];
+          }
+        }
+      } else {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         cb[u] = 0;
@@ -1777,6 +1819,7 @@ __global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_pe
           }
         }
       }
+      }  // chains from global memory
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         if (!mk[u]) continue;
@@ -2076,6 +2119,7 @@ __global__ void k_gather_eval(const DevModel* __restrict__ models, const EvalJob
 
 struct HostModel {
   int32_t S, R, nnz, initial, ntiles, K, rewardFinite;
+  int32_t maxRowNnz;  // transitions of the widest row
 };
 
 template <class T>
@@ -2174,6 +2218,7 @@ struct morap_ctx {
   int cmpBlocks = 0;
   bool usePersistent = true;  // evaluate batches as one cooperative launch
   int persistBlocks = 0;
+  bool usePersistCache = false;
   unsigned* dBar = nullptr;   // grid-barrier counter + generation
   unsigned* dFinCount = nullptr;  // CTAs done in the current compact sweep (fused finalize)
   void* persistArena = nullptr;
@@ -2867,11 +2912,17 @@ int run_eval_persistent(morap_ctx* ctx, int njobs, double eps, int cap) {
   a.ctl = ctx->dCtl;
   a.barCount = ctx->dBar;
   a.barGen = ctx->dBar + 1;
+  // shared-memory chains when every job's rows have <= 2 transitions and a CTA's states fit
+  const long long per = (prefix[njobs] + ctx->persistBlocks - 1) / ctx->persistBlocks;
+  bool narrow = true;
+  for (int j = 0; j < njobs && narrow; ++j) narrow = ctx->hm[ctx->hEvalJobs[j].model].maxRowNnz <= 2;
+  const size_t cacheBytes = static_cast<size_t>((per + 15) & ~15ll) + 24ull * static_cast<size_t>(per);
+  a.cacheStates = (narrow && ctx->usePersistCache && cacheBytes <= kPersistCacheBytes) ? static_cast<int>(per) : 0;
   void* args[] = {&a};
   const bool timed = ctx->profiling;
   if (timed) CK(cudaEventRecord(ctx->ev0, ctx->stream));
   CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_eval_persistent), dim3(ctx->persistBlocks), dim3(kPersistThreads),
-                                 args, 0, ctx->stream));
+                                 args, a.cacheStates ? cacheBytes : 0, ctx->stream));
   if (timed) CK(cudaEventRecord(ctx->ev1, ctx->stream));
   ctx->stats[8] += 1;
   CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
@@ -3052,6 +3103,13 @@ int morap_cuda_create(int device, morap_ctx** out) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occP, k_eval_persistent, kPersistThreads, 0);
   int coop = 0;
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+  cudaFuncSetAttribute(k_eval_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, kPersistCacheBytes);
+  {
+    int occCache = 0;  // the chain cache must not cost the cooperative grid its residency
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occCache, k_eval_persistent, kPersistThreads, kPersistCacheBytes);
+    const char* pc = std::getenv("MORAP_PERSIST_CACHE");  // "0" disables the shared-memory chains (A/B)
+    ctx->usePersistCache = occCache >= occP && occP > 0 && !(pc && std::string(pc) == "0");
+  }
   int persistPerSm = std::max(1, occP);
   if (const char* pc = std::getenv("MORAP_PERSIST_CTAS")) persistPerSm = std::max(1, std::min(occP, std::atoi(pc)));
   ctx->persistBlocks = ctx->numSMs * persistPerSm;
@@ -3147,6 +3205,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   std::vector<int> status(nmodels, MORAP_OK);
   std::vector<std::string> why(nmodels);
   std::vector<CompactStream> compact(nmodels);
+  std::vector<int32_t> maxRowNnz(nmodels, 0);
   const auto tu0 = std::chrono::steady_clock::now();
   auto lapU = [&](const char* what) {
     if (ctx->trace)
@@ -3170,6 +3229,8 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
       return;
     }
     make_tiles(models[m], tiles[m], descs[m]);
+    for (int r = 0; r < models[m].num_rows; ++r)
+      maxRowNnz[m] = std::max(maxRowNnz[m], models[m].trn_offset[r + 1] - models[m].trn_offset[r]);
     lapP(1);
     if (ctx->useCompact) {
       build_compact(models[m], compact[m]);
@@ -3306,7 +3367,8 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   for (int m = 0; m < nmodels; ++m) {
     const DevModel& dmod = built[m];
     ctx->dm.push_back(dmod);
-    ctx->hm.push_back(HostModel{dmod.S, dmod.R, dmod.nnz, dmod.initial, dmod.ntiles, dmod.K, dmod.rewardFinite});
+    ctx->hm.push_back(HostModel{dmod.S, dmod.R, dmod.nnz, dmod.initial, dmod.ntiles, dmod.K, dmod.rewardFinite,
+                                maxRowNnz[m]});
     if (ids_out) ids_out[m] = first + m;
   }
   lapU("packed, copies queued");
