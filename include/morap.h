@@ -124,6 +124,35 @@ int morap_centralised_pareto(morap_solver* s, const morap_centralised* c, const 
                              const double* norm, double eps, int iteration_cap, char* json_out, int json_cap,
                              double* stats_out);
 
+/* runBatch (engine.hpp:370) -- the reference's job engine seam -- on the solver's GPU. Job k
+ * refers to product (agent, task) of `inst` (agent < 0: a job without a model) and carries
+ * its own reward vector (Job::reward, one entry per action row), the deterministic
+ * scheduler of an evaluate job (one row per state), eps and sweep cap (engine.hpp:40-54).
+ * Failures stay contained in their job (engine.hpp:140-150): result.status is 0 or
+ * 1 + Errc. values_out[k] / policy_out[k] (nullable) receive JobResult::values / policy
+ * (num_states entries) for successful jobs. Products uploaded lean for queries get a full
+ * device copy on their first explicit-reward job. */
+typedef struct {
+  int64_t id;
+  int32_t kind; /* 0 optimize, 1 evaluate */
+  int32_t agent, task;
+  const double* reward;
+  int32_t reward_len;
+  const int32_t* scheduler;
+  int32_t scheduler_len;
+  double eps;
+  int32_t sweep_cap;
+} morap_job;
+typedef struct {
+  int64_t id;
+  int32_t status;
+  int32_t sweeps;
+  double value;
+  double residual;
+} morap_job_result;
+int morap_run_batch(morap_solver* s, const morap_instance* inst, int njobs, const morap_job* jobs,
+                    morap_job_result* results, double* const* values_out, int32_t* const* policy_out);
+
 /* maxAssignment (assignment.hpp:54): agent_of[j] for the n x n row-major value matrix. */
 int morap_max_assignment(int n, const double* c, int32_t* agent_of);
 

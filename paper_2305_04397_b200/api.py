@@ -63,6 +63,7 @@ def load_host_library() -> C.CDLL:
         "morap_pareto": (i32, [p, p, p, i32, p, f64, i32, i32, C.c_char_p, i32, p]),
         "morap_pareto_core": (i32, [p, i32, i32, p, f64, i32, i32, QUERY_FN, p, C.c_char_p, i32]),
         "morap_max_assignment": (i32, [i32, p, p]),
+        "morap_run_batch": (i32, [p, p, i32, p, p, p, p]),
         "morap_centralised_build": (i32, [p, C.c_int64, C.POINTER(p)]),
         "morap_centralised_free": (None, [p]),
         "morap_centralised_info": (i32, [p, p]),
@@ -202,6 +203,18 @@ class Instance:
         return p
 
 
+class Job(C.Structure):
+    """morap_job (include/morap.h): one Job of the reference's engine (engine.hpp:40-54)."""
+    _fields_ = [("id", C.c_int64), ("kind", C.c_int32), ("agent", C.c_int32), ("task", C.c_int32),
+                ("reward", C.c_void_p), ("reward_len", C.c_int32), ("scheduler", C.c_void_p),
+                ("scheduler_len", C.c_int32), ("eps", C.c_double), ("sweep_cap", C.c_int32)]
+
+
+class JobResult(C.Structure):
+    _fields_ = [("id", C.c_int64), ("status", C.c_int32), ("sweeps", C.c_int32), ("value", C.c_double),
+                ("residual", C.c_double)]
+
+
 class Centralised:
     """Centralised model of an instance (buildCentralised, centralised.hpp:54-179)."""
 
@@ -314,6 +327,47 @@ class Solver:
         out = json.loads(buf.value.decode())
         out["stats"] = dict(zip(["optimize_jobs", "optimize_backups", "evaluate_jobs", "evaluate_state_backups",
                                  "optimize_s", "evaluate_s", "host_s", "evaluate_batch_s"], st[:8].tolist()))
+        return out
+
+    def run_batch(self, inst: Instance, jobs: list) -> list:
+        """runBatch (engine.hpp:370) on this GPU. jobs: dicts with id, kind ("optimize" |
+        "evaluate"), product (agent, task) or None, reward, scheduler (evaluate), eps,
+        sweep_cap. Returns dicts with id, ok, status, value, sweeps, residual, values
+        (and policy for optimize jobs) -- failures contained per job (engine.hpp:140-150)."""
+        n = len(jobs)
+        arr = (Job * max(1, n))()
+        keep, vals, pols = [], [], []
+        for k, j in enumerate(jobs):
+            a = arr[k]
+            a.id = int(j["id"])
+            a.kind = 1 if j.get("kind") == "evaluate" else 0
+            prod = j.get("product")
+            a.agent, a.task = (int(prod[0]), int(prod[1])) if prod is not None else (-1, -1)
+            rw = np.ascontiguousarray(j.get("reward", []), np.float64)
+            sc = np.ascontiguousarray(j.get("scheduler", []), np.int32)
+            keep += [rw, sc]
+            a.reward, a.reward_len = (rw.ctypes.data if rw.size else None), rw.size
+            a.scheduler, a.scheduler_len = (sc.ctypes.data if sc.size else None), sc.size
+            a.eps = float(j.get("eps", 1e-6))
+            a.sweep_cap = int(j.get("sweep_cap", 100000))
+            S = int(inst.product_dims(*prod)[0][0]) if prod is not None else 0
+            vals.append(np.zeros(max(S, 1)))
+            pols.append(np.zeros(max(S, 1), np.int32))
+        res = (JobResult * max(1, n))()
+        vp = (C.c_void_p * max(1, n))(*[v.ctypes.data for v in vals])
+        pp = (C.c_void_p * max(1, n))(*[q.ctypes.data for q in pols])
+        _check(self._lib.morap_run_batch(self.h, inst.h, n, arr, res, C.cast(vp, C.c_void_p), C.cast(pp, C.c_void_p)),
+               "runBatch")
+        out = []
+        for k, j in enumerate(jobs):
+            r = res[k]
+            d = {"id": int(r.id), "ok": r.status == 0, "status": int(r.status), "value": r.value, "sweeps": r.sweeps,
+                 "residual": r.residual}
+            if r.status == 0 and j.get("product") is not None:
+                d["values"] = vals[k]
+                if j.get("kind") != "evaluate":
+                    d["policy"] = pols[k]
+            out.append(d)
         return out
 
     def centralised_pareto(self, c: Centralised, thresholds, eps=0.01, norm=None, iteration_cap=500) -> dict:

@@ -434,6 +434,42 @@ int morap_centralised_pareto(morap_solver* s, const morap_centralised* p, const 
   });
 }
 
+int morap_run_batch(morap_solver* s, const morap_instance* p, int njobs, const morap_job* jobs,
+                    morap_job_result* results, double* const* values_out, int32_t* const* policy_out) {
+  return guard([&] {
+    if (!s || !p || njobs < 0 || (njobs > 0 && (!jobs || !results))) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    const auto& I = p->inst;
+    std::vector<morap::Job> batch(static_cast<size_t>(njobs));
+    for (int k = 0; k < njobs; ++k) {
+      const morap_job& j = jobs[k];
+      morap::Job& J = batch[static_cast<size_t>(k)];
+      J.id = static_cast<long>(j.id);
+      J.kind = j.kind == 1 ? morap::JobKind::Evaluate : morap::JobKind::Optimize;
+      if (j.agent >= 0) {
+        if (j.agent >= I.n || j.task < 0 || j.task >= I.n) morap::fail(morap::Errc::InvalidConfig, "product index out of range");
+        J.model = I.products[static_cast<size_t>(j.agent)][static_cast<size_t>(j.task)];
+      }
+      if (j.reward && j.reward_len > 0) J.reward.assign(j.reward, j.reward + j.reward_len);
+      if (j.scheduler && j.scheduler_len > 0) J.scheduler.rows.assign(j.scheduler, j.scheduler + j.scheduler_len);
+      J.eps = j.eps;
+      J.sweepCap = j.sweep_cap;
+    }
+    std::map<long, morap::JobResult> res = morap::runBatch(std::move(batch), *s->gpu);
+    for (int k = 0; k < njobs; ++k) {
+      const morap::JobResult& r = res.at(static_cast<long>(jobs[k].id));
+      morap_job_result& o = results[k];
+      o.id = jobs[k].id;
+      o.status = r.ok ? 0 : (r.errc ? morap::statusOf(*r.errc) : morap::statusOf(morap::Errc::SolverFailure));
+      o.sweeps = r.stats.sweeps;
+      o.value = r.value;
+      o.residual = r.stats.residual;
+      if (r.ok && values_out && values_out[k]) std::memcpy(values_out[k], r.values.data(), sizeof(double) * r.values.size());
+      if (r.ok && policy_out && policy_out[k])
+        for (size_t q = 0; q < r.policy.rows.size(); ++q) policy_out[k][q] = r.policy.rows[q];
+    }
+  });
+}
+
 int morap_max_assignment(int n, const double* c, int32_t* agent_of) {
   return guard([&] {
     morap::Mat m(n, n);
