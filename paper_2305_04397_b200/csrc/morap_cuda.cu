@@ -89,10 +89,8 @@ struct DevModel {
   // compact sweep streams, tile-major and padded per tile (TilePos): rowOffset[s + 1] -
   // tile.r0 and trnOffset[r + 1] - tile.k0 (u16), succW, and copies of probIdx / rclass / done
   const uint16_t* relRowEnd;
-  const uint16_t* relTrnEnd;
-  const uint16_t* succWP;
-  const uint8_t* idxP;
-  const uint8_t* clsP;
+  const uint32_t* rowW;  // per row: tile-relative transition end | reward class << 16
+  const uint32_t* trW;   // per transition: window offset (0xFFFF outside) | probability index << 16
   const uint8_t* doneP;
   const TilePos* tilePos;     // ntiles
   int32_t S, R, nnz, initial, ntiles, K, rewardFinite, compact;
@@ -823,17 +821,15 @@ __global__ void __launch_bounds__(kTmaThreads, kStages >= 3 ? 2 : 3) k_greedy_sw
 constexpr int kCmpStages = MORAP_CMP_STAGES;
 // stage: u16 tile-relative row ends per state and transition ends per row, u16 window
 // offsets, u8 probability index, u8 reward class, done, own x, successor window of x
-constexpr int kCOffRow = 0;
-constexpr int kCOffTrn = kCOffRow + 2 * (kBlock + 8);
-constexpr int kCOffSucc = kCOffTrn + 2 * (kRowCap + 8);
-constexpr int kCOffIdx = kCOffSucc + 2 * (kNnzCap + 8);  // u16 window offsets (+7 front misalignment)
-constexpr int kCOffCls = kCOffIdx + kNnzCap + 16;
-constexpr int kCOffDone = kCOffCls + kRowCap + 16;
+constexpr int kCOffRow = 0;                               // u16 row end per state
+constexpr int kCOffTrn = kCOffRow + 2 * (kBlock + 8);     // u32 row word: transition end | class << 16
+constexpr int kCOffSucc = kCOffTrn + 4 * (kRowCap + 4);   // u32 transition word: window offset | index << 16
+constexpr int kCOffDone = kCOffSucc + 4 * (kNnzCap + 4);
 constexpr int kCOffX = kCOffDone + kStDoneBytes;
 constexpr int kCOffXw = kCOffX + 8 * kStXDbls;
 constexpr int kCStageBytes = kCOffXw + 8 * (kXWin + 2);
-static_assert(kCOffTrn % 16 == 0 && kCOffSucc % 16 == 0 && kCOffIdx % 16 == 0 && kCOffCls % 16 == 0 &&
-                  kCOffDone % 16 == 0 && kCOffX % 16 == 0 && kCOffXw % 16 == 0 && kCStageBytes % 16 == 0,
+static_assert(kCOffTrn % 16 == 0 && kCOffSucc % 16 == 0 && kCOffDone % 16 == 0 && kCOffX % 16 == 0 &&
+                  kCOffXw % 16 == 0 && kCStageBytes % 16 == 0,
               "compact stage regions must be 16-byte aligned");
 constexpr int kCFbRows = kXWin + 2 < kRowCap ? kXWin + 2 : kRowCap;  // fallback row values in the window region
 constexpr int kCmpSmemBytes = kCmpStages * kCStageBytes;
@@ -1015,9 +1011,9 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     int curJob = -1;
     const unsigned char* myBase = nullptr;  // stream base of this lane for curJob
     // per-lane stream constants: element size (log2) and stage region
-    const int laneSh = lane == 6 || lane == 7 ? 3 : (lane <= 2 ? 1 : 0);
-    const int laneDst = lane == 0 ? kCOffRow : lane == 1 ? kCOffTrn : lane == 2 ? kCOffSucc : lane == 3 ? kCOffIdx
-                      : lane == 4 ? kCOffCls : lane == 5 ? kCOffDone : lane == 6 ? kCOffX : kCOffXw;
+    const int laneSh = lane == 6 || lane == 7 ? 3 : lane == 0 ? 1 : (lane == 1 || lane == 2) ? 2 : 0;
+    const int laneDst = lane == 0 ? kCOffRow : lane == 1 ? kCOffTrn : lane == 2 ? kCOffSucc : lane == 5 ? kCOffDone
+                      : lane == 6 ? kCOffX : kCOffXw;
     const DevModel* curM = nullptr;
     const OptJob* curJ = nullptr;
     int parity = k & 1;
@@ -1067,10 +1063,8 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           const void* bp = nullptr;
           switch (lane) {
             case 0: bp = curM->relRowEnd; break;
-            case 1: bp = curM->relTrnEnd; break;
-            case 2: bp = curM->succWP; break;
-            case 3: bp = curM->idxP; break;
-            case 4: bp = curM->clsP; break;
+            case 1: bp = curM->rowW; break;
+            case 2: bp = curM->trW; break;
             case 5: bp = curM->doneP; break;
             case 6: bp = POLICY ? nullptr : curJ->buf[parity]; break;
             case 7: bp = curJ->buf[parity]; break;
@@ -1082,10 +1076,10 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
         // stream of this lane: [lo, hi) in elements of 1 << sh bytes, selected without
         // branching (lanes 0-5: tile-major padded streams, slice start from TilePos)
         const int pos = lane < 6 ? sPos[q][lane] : 0;
-        const int len = lane == 0 || lane == 5 ? s1 - s0 : (lane == 1 || lane == 4 ? r1 - r0 : k1 - k0);
+        const int len = lane == 0 || lane == 5 ? s1 - s0 : (lane == 1 ? r1 - r0 : k1 - k0);
         long long lo = lane < 6 ? pos : (lane == 6 ? s0 : wlo);
         long long hi = lane < 6 ? pos + len : (lane == 6 ? s1 : wlo + wn);
-        if (lane > 7) lo = hi = 0;
+        if (lane > 7 || lane == 3 || lane == 4) lo = hi = 0;  // lanes 3, 4: no stream
         const int sh = laneSh, dstOff = laneDst;
         const uint64_t lp = lane >= 6 ? polKeep : pol;
         const long long a0 = (lo << sh) & ~15ll, z0 = ((hi << sh) + 15) & ~15ll;
@@ -1162,15 +1156,15 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     if (v.fits && g_dryRun) {
       // diagnostics: stream only
     } else if (v.fits) {
-      // Tile-relative u16 row / transition END offsets: state i owns rows
-      // [relRowEnd[i-1], relRowEnd[i]) (0 for i = 0), row r owns transitions
-      // [relTrnEnd[r-1], relTrnEnd[r]).
-      // padded per-tile streams: every slice starts at offset 0 of its region
+      // Tile-relative u16 row ends per state: state i owns rows [rowE[i-1], rowE[i]) (0 for
+      // i = 0). One u32 word per row: transition end (tile-relative, low 16 bits) and reward
+      // class (bits 16-23); one u32 word per transition: window offset (low 16 bits, 0xFFFF
+      // outside the window) and probability index (bits 16-23) -- one shared-memory load
+      // each instead of two (the compute warps are bound by shared-memory wavefronts).
+      // Padded per-tile streams: every slice starts at offset 0 of its region.
       const uint16_t* rowE = reinterpret_cast<const uint16_t*>(st + kCOffRow);
-      const uint16_t* trnE = reinterpret_cast<const uint16_t*>(st + kCOffTrn);
-      const uint16_t* succS = reinterpret_cast<const uint16_t*>(st + kCOffSucc);
-      const uint8_t* idxS = st + kCOffIdx;
-      const uint8_t* clsS = st + kCOffCls;
+      const uint32_t* rowW = reinterpret_cast<const uint32_t*>(st + kCOffTrn);
+      const uint32_t* trW = reinterpret_cast<const uint32_t*>(st + kCOffSucc);
       const uint8_t* doneS = st + kCOffDone;
       const double* xS = reinterpret_cast<const double*>(st + kCOffX) + v.offX;
       const double* xwS = reinterpret_cast<const double*>(st + kCOffXw);  // even wlo: no front offset
@@ -1182,17 +1176,19 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
         } else {
           double best = 0.0;
           int bestRow = -1;
-          int kb = rb ? trnE[rb - 1] : 0;
+          int kb = rb ? static_cast<int>(rowW[rb - 1] & 0xFFFFu) : 0;
+          const double* __restrict__ dict = v.dict;
+          const double* __restrict__ crho = v.classRho;
+          auto term = [&](uint32_t w) { return __dmul_rn(__ldg(dict + (w >> 16)), xwS[w & 0xFFFFu]); };
           if (v.allIn && v.simple && re > rb) {
             // every successor in the window, at most two transitions per row: straight-line
             // rows, the first one peeled so the max needs no "no row yet" test
-            const double* __restrict__ dict = v.dict;
-            const double* __restrict__ crho = v.classRho;
             auto row = [&](int r, int& k) {
-              const int ke = trnE[r];
-              double acc = __ldg(crho + clsS[r]);
-              if (k < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[k]), xwS[succS[k]]));
-                if (k + 1 < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[k + 1]), xwS[succS[k + 1]]));
+              const uint32_t rw = rowW[r];
+              const int ke = static_cast<int>(rw & 0xFFFFu);
+              double acc = __ldg(crho + (rw >> 16));
+              if (k < ke) acc = __dadd_rn(acc, term(trW[k]));
+              if (k + 1 < ke) acc = __dadd_rn(acc, term(trW[k + 1]));
               k = ke;
               return acc;
             };
@@ -1207,18 +1203,13 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
               }
             }
           } else if (v.allIn) {  // every successor inside the staged window: no out-of-window test
-            const double* __restrict__ dict = v.dict;
-            const double* __restrict__ crho = v.classRho;
 #pragma unroll 1
             for (int r = rb; r < re; ++r) {
-              const int ke = trnE[r];
-              double acc = __ldg(crho + clsS[r]);
-              // warehouse rows carry 1 or 2 transitions: straight-line for those, loop after
-              if (kb < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[kb]), xwS[succS[kb]]));
-              if (kb + 1 < ke) acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[kb + 1]), xwS[succS[kb + 1]]));
+              const uint32_t rw = rowW[r];
+              const int ke = static_cast<int>(rw & 0xFFFFu);
+              double acc = __ldg(crho + (rw >> 16));
 #pragma unroll 1
-              for (int q = kb + 2; q < ke; ++q)
-                acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + idxS[q]), xwS[succS[q]]));
+              for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, term(trW[q]));
               kb = ke;
               if (bestRow < 0 || acc > best) {
                 best = acc;
@@ -1226,14 +1217,18 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
               }
             }
           } else {
-            auto xAt = [&](int q) {  // window offset staged; absolute successor only outside it
-              const unsigned o = succS[q];
+            auto xAt = [&](int q, uint32_t w) {  // window offset staged; absolute successor only outside it
+              const unsigned o = w & 0xFFFFu;
               return o != 0xFFFFu ? xwS[o] : __ldg(x + __ldg(v.succG + v.k0 + q));
             };
             for (int r = rb; r < re; ++r) {
-              const int ke = trnE[r];
-              double acc = __ldg(v.classRho + clsS[r]);
-              for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(v.dict + idxS[q]), xAt(q)));
+              const uint32_t rw = rowW[r];
+              const int ke = static_cast<int>(rw & 0xFFFFu);
+              double acc = __ldg(crho + (rw >> 16));
+              for (int q = kb; q < ke; ++q) {
+                const uint32_t w = trW[q];
+                acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + (w >> 16)), xAt(q, w)));
+              }
               kb = ke;
               if (bestRow < 0 || acc > best) {
                 best = acc;
@@ -2348,9 +2343,9 @@ struct CompactStream {
   bool ok = false;
   std::vector<uint8_t> idx, cls;
   std::vector<double> dict, table;
-  std::vector<uint16_t> succW;  // successor window offsets (needs the tile table), padded per tile
-  std::vector<uint16_t> relRowEnd, relTrnEnd;  // tile-relative row / transition ends, padded per tile
-  std::vector<uint8_t> idxP, clsP, doneP;      // tile-major padded copies for the sweep
+  std::vector<uint16_t> relRowEnd;             // tile-relative row ends, padded per tile
+  std::vector<uint32_t> rowW, trW;             // packed row / transition words, padded per tile
+  std::vector<uint8_t> doneP;                  // tile-major padded copy for the sweep
   std::vector<TilePos> pos;
 };
 
@@ -2375,17 +2370,15 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
     p.cls = static_cast<int32_t>(nCls);
     p.done = static_cast<int32_t>(nDone);
     nRow += up16(ns, 2);
-    nTrn += up16(nr, 2);
-    nSucc += up16(nz, 2);
-    nIdx += up16(nz, 1);
-    nCls += up16(nr, 1);
+    nTrn += up16(nr, 4);
+    nSucc += up16(nz, 4);
     nDone += up16(ns, 1);
   }
+  (void)nIdx;
+  (void)nCls;
   c.relRowEnd.assign(nRow, 0);
-  c.relTrnEnd.assign(nTrn, 0);
-  c.succW.assign(nSucc, 0xFFFF);
-  c.idxP.assign(nIdx, 0);
-  c.clsP.assign(nCls, 0);
+  c.rowW.assign(nTrn, 0);
+  c.trW.assign(nSucc, 0xFFFFu);
   c.doneP.assign(nDone, 0);
   for (size_t t = 0; t < nt; ++t) {
     TileDesc& d = desc[t];
@@ -2403,15 +2396,13 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
       c.relRowEnd[p.row + (q - d.s0)] = static_cast<uint16_t>(v.row_offset[q + 1] - d.r0);
       c.doneP[p.done + (q - d.s0)] = v.done[q] ? 1 : 0;
     }
-    for (int r = d.r0; r < e.r0; ++r) {
-      c.relTrnEnd[p.trn + (r - d.r0)] = static_cast<uint16_t>(v.trn_offset[r + 1] - d.k0);
-      c.clsP[p.cls + (r - d.r0)] = c.cls[r];
-    }
+    for (int r = d.r0; r < e.r0; ++r)
+      c.rowW[p.trn + (r - d.r0)] =
+          static_cast<uint32_t>(v.trn_offset[r + 1] - d.k0) | (static_cast<uint32_t>(c.cls[r]) << 16);
     for (int k = d.k0; k < e.k0; ++k) {
       const unsigned o = static_cast<unsigned>(v.succ[k] - d.wlo);
       const bool in = o < static_cast<unsigned>(d.wn);
-      c.succW[p.succ + (k - d.k0)] = in ? static_cast<uint16_t>(o) : static_cast<uint16_t>(0xFFFF);
-      c.idxP[p.idx + (k - d.k0)] = c.idx[k];
+      c.trW[p.succ + (k - d.k0)] = (in ? o : 0xFFFFu) | (static_cast<uint32_t>(c.idx[k]) << 16);
       if (!in) d.allIn = 0;
     }
   }
@@ -3258,9 +3249,8 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
              align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
     if (compact[m].ok)
       bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(v.num_rows, 256) +
-               align_up(8ull * compact[m].table.size(), 256) + align_up(2ull * compact[m].succW.size(), 256) +
-               align_up(2ull * compact[m].relRowEnd.size(), 256) + align_up(2ull * compact[m].relTrnEnd.size(), 256) +
-               align_up(compact[m].idxP.size(), 256) + align_up(compact[m].clsP.size(), 256) +
+               align_up(8ull * compact[m].table.size(), 256) + align_up(4ull * compact[m].trW.size(), 256) +
+               align_up(2ull * compact[m].relRowEnd.size(), 256) + align_up(4ull * compact[m].rowW.size(), 256) +
                align_up(compact[m].doneP.size(), 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256);
   }
   void* dev = nullptr;
@@ -3340,16 +3330,14 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
       dmod.rclass = reinterpret_cast<const uint8_t*>(put(c.cls.data(), c.cls.size()));
       dmod.classTable = reinterpret_cast<const double*>(put(c.table.data(), 8ull * c.table.size()));
       dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
-      dmod.succWP = reinterpret_cast<const uint16_t*>(put(c.succW.data(), 2ull * c.succW.size()));
       dmod.relRowEnd = reinterpret_cast<const uint16_t*>(put(c.relRowEnd.data(), 2ull * c.relRowEnd.size()));
-      dmod.relTrnEnd = reinterpret_cast<const uint16_t*>(put(c.relTrnEnd.data(), 2ull * c.relTrnEnd.size()));
-      dmod.idxP = reinterpret_cast<const uint8_t*>(put(c.idxP.data(), c.idxP.size()));
-      dmod.clsP = reinterpret_cast<const uint8_t*>(put(c.clsP.data(), c.clsP.size()));
+      dmod.rowW = reinterpret_cast<const uint32_t*>(put(c.rowW.data(), 4ull * c.rowW.size()));
+      dmod.trW = reinterpret_cast<const uint32_t*>(put(c.trW.data(), 4ull * c.trW.size()));
       dmod.doneP = reinterpret_cast<const uint8_t*>(put(c.doneP.data(), c.doneP.size()));
       dmod.tilePos = reinterpret_cast<const TilePos*>(put(c.pos.data(), sizeof(TilePos) * c.pos.size()));
-      // compact stream: window offset 2 + prob index 1 per nnz; relative transition end 2 +
-      // class 1 per row; relative row end 2 + done 1 + x 8 + y 8 per state
-      dmod.bytesPerSweep = 3ull * v.nnz + 3ull * v.num_rows + 19ull * v.num_states;
+      // compact stream: one 4-byte word per transition (window offset | index) and per row
+      // (transition end | class); relative row end 2 + done 1 + x 8 + y 8 per state
+      dmod.bytesPerSweep = 4ull * v.nnz + 4ull * v.num_rows + 19ull * v.num_states;
     }
     // evaluate, one RHS over the policy chain: chainOff 4 + done 1 + rhoC 8 + x 8 + y 8 per
     // state + 12 per chosen transition (mean nnz per row)
