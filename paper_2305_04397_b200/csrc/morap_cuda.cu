@@ -88,10 +88,9 @@ struct DevModel {
   const double* classTable;   // nclass x K objective tuples
   // compact sweep streams, tile-major and padded per tile (TilePos): rowOffset[s + 1] -
   // tile.r0 and trnOffset[r + 1] - tile.k0 (u16), succW, and copies of probIdx / rclass / done
-  const uint16_t* relRowEnd;
+  const uint32_t* stW;   // per state: row end | transition end << 10 | done << 21 (tile-relative)
   const uint32_t* rowW;  // per row: tile-relative transition end | reward class << 16
   const uint32_t* trW;   // per transition: window offset (0xFFFF outside) | probability index << 16
-  const uint8_t* doneP;
   const TilePos* tilePos;     // ntiles
   int32_t S, R, nnz, initial, ntiles, K, rewardFinite, compact;
   int32_t nclass, pad2;
@@ -357,7 +356,7 @@ constexpr int kOffX = kOffDone + kStDoneBytes;
 constexpr int kOffIdx = kOffX + 8 * kStXDbls;  // compact models: u8 probability index per transition
 constexpr int kOffCls = kOffIdx + kNnzCap + 16;  // compact models: u8 reward class per row
 #ifndef MORAP_XWIN
-#define MORAP_XWIN 1024
+#define MORAP_XWIN 992
 #endif
 constexpr int kXWin = MORAP_XWIN;                        // successor window of x staged per tile
 constexpr int kOffXw = kOffCls + kRowCap + 16;
@@ -821,18 +820,20 @@ __global__ void __launch_bounds__(kTmaThreads, kStages >= 3 ? 2 : 3) k_greedy_sw
 constexpr int kCmpStages = MORAP_CMP_STAGES;
 // stage: u16 tile-relative row ends per state and transition ends per row, u16 window
 // offsets, u8 probability index, u8 reward class, done, own x, successor window of x
-constexpr int kCOffRow = 0;                               // u16 row end per state
-constexpr int kCOffTrn = kCOffRow + 2 * (kBlock + 8);     // u32 row word: transition end | class << 16
+constexpr int kCOffRow = 0;                               // u32 state word: row end | transition end << 10 | done << 21
+constexpr int kCOffTrn = kCOffRow + 4 * (kBlock + 4);     // u32 row word: transition end | class << 16
 constexpr int kCOffSucc = kCOffTrn + 4 * (kRowCap + 4);   // u32 transition word: window offset | index << 16
-constexpr int kCOffDone = kCOffSucc + 4 * (kNnzCap + 4);
-constexpr int kCOffX = kCOffDone + kStDoneBytes;
+constexpr int kCOffX = kCOffSucc + 4 * (kNnzCap + 4);
 constexpr int kCOffXw = kCOffX + 8 * kStXDbls;
 constexpr int kCStageBytes = kCOffXw + 8 * (kXWin + 2);
-static_assert(kCOffTrn % 16 == 0 && kCOffSucc % 16 == 0 && kCOffDone % 16 == 0 && kCOffX % 16 == 0 &&
+static_assert(kCOffTrn % 16 == 0 && kCOffSucc % 16 == 0 && kCOffX % 16 == 0 &&
                   kCOffXw % 16 == 0 && kCStageBytes % 16 == 0,
               "compact stage regions must be 16-byte aligned");
 constexpr int kCFbRows = kXWin + 2 < kRowCap ? kXWin + 2 : kRowCap;  // fallback row values in the window region
 constexpr int kCmpSmemBytes = kCmpStages * kCStageBytes;
+// MORAP_CMP_CTAS CTAs per SM must fit the 228 KB of shared memory (1 KB reserved per CTA,
+// ~2.5 KB of static shared memory): one CTA less costs ~5% (measured)
+static_assert(MORAP_CMP_CTAS * (kCmpSmemBytes + 2560 + 1024) <= 228 * 1024, "compact sweep stages too large");
 
 // Arguments of the finalize step fused into the compact sweep (count == nullptr: none).
 struct FinArgs {
@@ -1011,9 +1012,9 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     int curJob = -1;
     const unsigned char* myBase = nullptr;  // stream base of this lane for curJob
     // per-lane stream constants: element size (log2) and stage region
-    const int laneSh = lane == 6 || lane == 7 ? 3 : lane == 0 ? 1 : (lane == 1 || lane == 2) ? 2 : 0;
-    const int laneDst = lane == 0 ? kCOffRow : lane == 1 ? kCOffTrn : lane == 2 ? kCOffSucc : lane == 5 ? kCOffDone
-                      : lane == 6 ? kCOffX : kCOffXw;
+    const int laneSh = lane == 6 || lane == 7 ? 3 : 2;
+    const int laneDst = lane == 0 ? kCOffRow : lane == 1 ? kCOffTrn : lane == 2 ? kCOffSucc : lane == 6 ? kCOffX
+                      : kCOffXw;
     const DevModel* curM = nullptr;
     const OptJob* curJ = nullptr;
     int parity = k & 1;
@@ -1062,10 +1063,9 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           if (POLICY) parity = (jobSweeps[job] - 1) & 1;
           const void* bp = nullptr;
           switch (lane) {
-            case 0: bp = curM->relRowEnd; break;
+            case 0: bp = curM->stW; break;
             case 1: bp = curM->rowW; break;
             case 2: bp = curM->trW; break;
-            case 5: bp = curM->doneP; break;
             case 6: bp = POLICY ? nullptr : curJ->buf[parity]; break;
             case 7: bp = curJ->buf[parity]; break;
             default: break;
@@ -1079,7 +1079,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
         const int len = lane == 0 || lane == 5 ? s1 - s0 : (lane == 1 ? r1 - r0 : k1 - k0);
         long long lo = lane < 6 ? pos : (lane == 6 ? s0 : wlo);
         long long hi = lane < 6 ? pos + len : (lane == 6 ? s1 : wlo + wn);
-        if (lane > 7 || lane == 3 || lane == 4) lo = hi = 0;  // lanes 3, 4: no stream
+        if (lane > 7 || (lane >= 3 && lane <= 5)) lo = hi = 0;  // lanes 3-5: no stream
         const int sh = laneSh, dstOff = laneDst;
         const uint64_t lp = lane >= 6 ? polKeep : pol;
         const long long a0 = (lo << sh) & ~15ll, z0 = ((hi << sh) + 15) & ~15ll;
@@ -1162,21 +1162,22 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
       // outside the window) and probability index (bits 16-23) -- one shared-memory load
       // each instead of two (the compute warps are bound by shared-memory wavefronts).
       // Padded per-tile streams: every slice starts at offset 0 of its region.
-      const uint16_t* rowE = reinterpret_cast<const uint16_t*>(st + kCOffRow);
+      // one u32 word per state: row end (bits 0-9), transition end (bits 10-20), done (bit 21)
+      const uint32_t* stW = reinterpret_cast<const uint32_t*>(st + kCOffRow);
       const uint32_t* rowW = reinterpret_cast<const uint32_t*>(st + kCOffTrn);
       const uint32_t* trW = reinterpret_cast<const uint32_t*>(st + kCOffSucc);
-      const uint8_t* doneS = st + kCOffDone;
       const double* xS = reinterpret_cast<const double*>(st + kCOffX) + v.offX;
       const double* xwS = reinterpret_cast<const double*>(st + kCOffXw);  // even wlo: no front offset
       if (tid < v.ns) {
         const int s = v.s0 + tid;
-        const int rb = tid ? rowE[tid - 1] : 0, re = rowE[tid];
-        if (doneS[tid]) {
+        const uint32_t w0 = tid ? stW[tid - 1] : 0u, w1 = stW[tid];
+        const int rb = static_cast<int>(w0 & 0x3FFu), re = static_cast<int>(w1 & 0x3FFu);
+        if (w1 >> 21) {  // done state
           if (POLICY) v.policy[s] = v.r0 + rb;  // numerics.hpp:114-115
         } else {
           double best = 0.0;
           int bestRow = -1;
-          int kb = rb ? static_cast<int>(rowW[rb - 1] & 0xFFFFu) : 0;
+          int kb = static_cast<int>((w0 >> 10) & 0x7FFu);
           const double* __restrict__ dict = v.dict;
           const double* __restrict__ crho = v.classRho;
           auto term = [&](uint32_t w) { return __dmul_rn(__ldg(dict + (w >> 16)), xwS[w & 0xFFFFu]); };
@@ -2343,9 +2344,7 @@ struct CompactStream {
   bool ok = false;
   std::vector<uint8_t> idx, cls;
   std::vector<double> dict, table;
-  std::vector<uint16_t> relRowEnd;             // tile-relative row ends, padded per tile
-  std::vector<uint32_t> rowW, trW;             // packed row / transition words, padded per tile
-  std::vector<uint8_t> doneP;                  // tile-major padded copy for the sweep
+  std::vector<uint32_t> stW, rowW, trW;        // packed state / row / transition words, padded per tile
   std::vector<TilePos> pos;
 };
 
@@ -2369,17 +2368,17 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
     p.idx = static_cast<int32_t>(nIdx);
     p.cls = static_cast<int32_t>(nCls);
     p.done = static_cast<int32_t>(nDone);
-    nRow += up16(ns, 2);
+    nRow += up16(ns, 4);
     nTrn += up16(nr, 4);
     nSucc += up16(nz, 4);
     nDone += up16(ns, 1);
   }
   (void)nIdx;
   (void)nCls;
-  c.relRowEnd.assign(nRow, 0);
+  (void)nDone;
+  c.stW.assign(nRow, 0);
   c.rowW.assign(nTrn, 0);
   c.trW.assign(nSucc, 0xFFFFu);
-  c.doneP.assign(nDone, 0);
   for (size_t t = 0; t < nt; ++t) {
     TileDesc& d = desc[t];
     const TileDesc& e = desc[t + 1];
@@ -2392,10 +2391,10 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
       continue;
     }
     const TilePos& p = c.pos[t];
-    for (int q = d.s0; q < e.s0; ++q) {
-      c.relRowEnd[p.row + (q - d.s0)] = static_cast<uint16_t>(v.row_offset[q + 1] - d.r0);
-      c.doneP[p.done + (q - d.s0)] = v.done[q] ? 1 : 0;
-    }
+    for (int q = d.s0; q < e.s0; ++q)  // fitting tiles: row end <= 768 (10 bits), transition end <= 1024 (11)
+      c.stW[p.row + (q - d.s0)] = static_cast<uint32_t>(v.row_offset[q + 1] - d.r0) |
+                                  (static_cast<uint32_t>(v.trn_offset[v.row_offset[q + 1]] - d.k0) << 10) |
+                                  (v.done[q] ? 1u << 21 : 0u);
     for (int r = d.r0; r < e.r0; ++r)
       c.rowW[p.trn + (r - d.r0)] =
           static_cast<uint32_t>(v.trn_offset[r + 1] - d.k0) | (static_cast<uint32_t>(c.cls[r]) << 16);
@@ -3250,8 +3249,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     if (compact[m].ok)
       bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(v.num_rows, 256) +
                align_up(8ull * compact[m].table.size(), 256) + align_up(4ull * compact[m].trW.size(), 256) +
-               align_up(2ull * compact[m].relRowEnd.size(), 256) + align_up(4ull * compact[m].rowW.size(), 256) +
-               align_up(compact[m].doneP.size(), 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256);
+               align_up(4ull * compact[m].stW.size(), 256) + align_up(4ull * compact[m].rowW.size(), 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256);
   }
   void* dev = nullptr;
   {
@@ -3330,14 +3328,13 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
       dmod.rclass = reinterpret_cast<const uint8_t*>(put(c.cls.data(), c.cls.size()));
       dmod.classTable = reinterpret_cast<const double*>(put(c.table.data(), 8ull * c.table.size()));
       dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
-      dmod.relRowEnd = reinterpret_cast<const uint16_t*>(put(c.relRowEnd.data(), 2ull * c.relRowEnd.size()));
+      dmod.stW = reinterpret_cast<const uint32_t*>(put(c.stW.data(), 4ull * c.stW.size()));
       dmod.rowW = reinterpret_cast<const uint32_t*>(put(c.rowW.data(), 4ull * c.rowW.size()));
       dmod.trW = reinterpret_cast<const uint32_t*>(put(c.trW.data(), 4ull * c.trW.size()));
-      dmod.doneP = reinterpret_cast<const uint8_t*>(put(c.doneP.data(), c.doneP.size()));
       dmod.tilePos = reinterpret_cast<const TilePos*>(put(c.pos.data(), sizeof(TilePos) * c.pos.size()));
       // compact stream: one 4-byte word per transition (window offset | index) and per row
-      // (transition end | class); relative row end 2 + done 1 + x 8 + y 8 per state
-      dmod.bytesPerSweep = 4ull * v.nnz + 4ull * v.num_rows + 19ull * v.num_states;
+      // (transition end | class) and per state (row end | transition end | done) + x 8 + y 8
+      dmod.bytesPerSweep = 4ull * v.nnz + 4ull * v.num_rows + 20ull * v.num_states;
     }
     // evaluate, one RHS over the policy chain: chainOff 4 + done 1 + rhoC 8 + x 8 + y 8 per
     // state + 12 per chosen transition (mean nnz per row)
