@@ -14,7 +14,7 @@ generator (warehouse.hpp:176), built on the host before timing.
   e2e      the same metric through the host API with HOST buffers: every step uploads the
            instance's product CSR (H2D) and reads back values/policies (D2H)
   roofline dominant kernel k_greedy_sweep_cmp (compact streams): algorithmic bytes
-           (3 nnz + 3 R + 19 S per active job per sweep) / its CUDA-event time
+           (4 nnz + 4 R + 20 S per active job per sweep) / its CUDA-event time
            over a second pass of the timed steps; traffic from the committed ncu capture
   cpu_baseline  the reference's own engine (oracle/_ref, runBatch over all host threads)
            on one optimize phase of the same instance
@@ -383,10 +383,10 @@ def run_ours(args):
     peak, peak_src = peak_hbm()
     achieved = cs["opt_bytes"] / (cs["opt_ms"] * 1e-3) / 1e9 if cs["opt_ms"] > 0 else None
     # SURVEY.md §8(d) counts the reference layout: 12 nnz + 12 R + 21 S per job-sweep; the
-    # compact kernel moves 3 nnz + 3 R + 19 S. Same units, so the survey's
+    # compact kernel moves 4 nnz + 4 R + 20 S. Same units, so the survey's
     # figure is ours scaled by the ratio of the two over the instance.
     N, R, S = inst.total_nnz, inst.total_rows, inst.total_states
-    survey_ratio = (12 * N + 12 * R + 21 * S) / (3 * N + 3 * R + 19 * S)
+    survey_ratio = (12 * N + 12 * R + 21 * S) / (4 * N + 4 * R + 20 * S)
     ratio, traffic_src = ncu_traffic()
     alg_per_launch = cs["opt_bytes"] / max(cs["opt_launches"], 1)
     # ncu's dram bytes of the captured launch, scaled to this run's mean launch by the
