@@ -2466,7 +2466,36 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
   uint64_t key[MORAP_MAX_OBJECTIVES];
   uint64_t prev[MORAP_MAX_OBJECTIVES];
   int prevId = -1;
-  for (int r = 0; r < v.num_rows; ++r) {
+  int r0 = 0;
+  if (K == 2) {
+    // the common two-objective case: unrolled compare against up to kScan known tuples
+    // (sentinel-padded: ~0 is a NaN payload, never a reward's bits), no data-dependent branch
+    uint64_t ta[kScan], tb[kScan];
+    for (int q = 0; q < kScan; ++q) ta[q] = tb[q] = ~0ull;
+    int nt = 0;
+    for (; r0 < v.num_rows; ++r0) {
+      uint64_t a, b;
+      std::memcpy(&a, &v.rewards[0][r0], 8);
+      std::memcpy(&b, &v.rewards[1][r0], 8);
+      int id = -1;
+#pragma unroll
+      for (int q = 0; q < kScan; ++q) id = (ta[q] == a) & (tb[q] == b) ? q : id;
+      if (id < 0) {
+        if (nt == kScan) break;  // more tuples: finish in the general loop below
+        key[0] = a;
+        key[1] = b;
+        id = classes.find(key);
+        if (id < 0) return;
+        c.table.push_back(v.rewards[0][r0]);
+        c.table.push_back(v.rewards[1][r0]);
+        ta[nt] = a;
+        tb[nt] = b;
+        ++nt;
+      }
+      c.cls[r0] = static_cast<uint8_t>(id);
+    }
+  }
+  for (int r = r0; r < v.num_rows; ++r) {
     bool same = prevId >= 0;
     for (int o = 0; o < K; ++o) {
       std::memcpy(&key[o], &v.rewards[o][r], 8);
