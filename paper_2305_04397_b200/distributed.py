@@ -108,6 +108,7 @@ class ShardedQuery:
             from .cuda import CudaBackend
 
             backend = CudaBackend(device)
+            backend.set_lean(True)  # the query needs weighted optimize + chain evaluate only
         self.be = backend
         if self.K > 2:
             raise MorapError(18, "sharded query supports K = 2 objectives (cost, success)")
@@ -129,9 +130,13 @@ class ShardedQuery:
         if getattr(self, "_prods", None) is None:  # host buffers of this rank's products, kept
             self._prods = [self.inst.product(f // n, f % n) for f in self.local]
         prods = self._prods
+        measured = hasattr(self.be, "stats")
+        before = self.be.stats()["upload_bytes"] if measured else 0.0
         ids = self.be.upload(prods) if prods else []
         self.model_of = {f: int(m) for f, m in zip(self.local, ids)}
         self.slot_of_model = {m: f for f, m in self.model_of.items()}
+        if measured:  # the bytes the upload actually copied (lean compact layout)
+            return int(self.be.stats()["upload_bytes"] - before)
         return sum(4 * (p.S + 1) + 4 * (p.R + 1) + 12 * p.nnz + p.S + 16 * p.R for p in prods)
 
     def coord(self, k, i, j):
