@@ -2137,6 +2137,10 @@ struct morap_ctx {
   bool evalTma = false;  // current evaluate batch runs the pipelined chain kernel
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;           // policy prefetch copies (overlap the evaluate sweeps)
+  cudaEvent_t polReady = nullptr, polCopied = nullptr;
+  std::vector<int32_t> polPrefetched;    // jobs whose policies sit in polStage (in this order)
+  std::vector<size_t> polOff;
   std::string err;
   bool profiling = false;
   bool trace = std::getenv("MORAP_TRACE") != nullptr;
@@ -2758,6 +2762,8 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   if (!(eps >= 0.0)) return ctx->fail(MORAP_INVALID_CONFIG, "eps must be nonnegative");
   if (cap < 1) return ctx->fail(MORAP_INVALID_CONFIG, "sweep cap must be positive");
   if (!rhoHost && (K < 0 || K > MORAP_MAX_OBJECTIVES)) return ctx->fail(MORAP_DIMENSION_MISMATCH, "bad objective count");
+  CK(cudaEventSynchronize(ctx->polCopied));  // policy buffers are about to be rewritten
+  ctx->polPrefetched.clear();
   ctx->optJobs = 0;
   if (njobs == 0) return MORAP_OK;
   for (int j = 0; j < njobs; ++j) {
@@ -2899,6 +2905,35 @@ int extract_policies(morap_ctx* ctx, const std::vector<int32_t>& jobsIn) {
   CK(cudaGetLastError());
   ctx->stats[8] += 1;
   for (int j : jobs) ctx->optPolicyReady[j] = 1;
+  return MORAP_OK;
+}
+
+// Copy the final policies of `jobs` to the pinned staging area on the side stream (after
+// the policy kernel on the main stream); morap_cuda_fetch_policies then only waits for them.
+int prefetch_policies(morap_ctx* ctx, const std::vector<int32_t>& jobs) {
+  size_t bytes = 0;
+  for (int j : jobs) bytes += align_up(sizeof(int32_t) * ctx->hm[ctx->optModel[j]].S, 256);
+  if (bytes > ctx->polStageBytes) {
+    CK(cudaStreamSynchronize(ctx->side));
+    cudaFreeHost(ctx->polStage);
+    ctx->polStage = nullptr;
+    ctx->polStageBytes = 0;
+    CK(cudaMallocHost(&ctx->polStage, bytes));
+    ctx->polStageBytes = bytes;
+  }
+  CK(cudaEventRecord(ctx->polReady, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->side, ctx->polReady, 0));
+  ctx->polOff.assign(jobs.size(), 0);
+  size_t o = 0;
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    const size_t n = sizeof(int32_t) * ctx->hm[ctx->optModel[jobs[q]]].S;
+    ctx->polOff[q] = o;
+    CK(cudaMemcpyAsync(static_cast<char*>(ctx->polStage) + o, ctx->hOptJobs[jobs[q]].policy, n, cudaMemcpyDeviceToHost,
+                       ctx->side));
+    o += align_up(n, 256);
+  }
+  CK(cudaEventRecord(ctx->polCopied, ctx->side));
+  ctx->polPrefetched = jobs;
   return MORAP_OK;
 }
 
@@ -3156,6 +3191,12 @@ int morap_cuda_create(int device, morap_ctx** out) {
   const char* csel = std::getenv("MORAP_COMPACT");  // "0" keeps the plain fp64 streams (A/B)
   ctx->useCompact = !(csel && std::string(csel) == "0");
   if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return MORAP_CUDA_ERROR; }
+  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->polReady, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->polCopied, cudaEventDisableTiming) != cudaSuccess) {
+    delete ctx;
+    return MORAP_CUDA_ERROR;
+  }
   ctx->stream = ctx->own;
   cudaEventCreate(&ctx->ev0);
   cudaEventCreate(&ctx->ev1);
@@ -3186,6 +3227,12 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   cudaFree(ctx->dGather);
   cudaFree(ctx->evalStage);
   cudaFreeHost(ctx->stage);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+  }
+  if (ctx->polReady) cudaEventDestroy(ctx->polReady);
+  if (ctx->polCopied) cudaEventDestroy(ctx->polCopied);
   cudaFree(ctx->dBar);
   cudaFree(ctx->dFinCount);
   cudaFree(ctx->persistArena);
@@ -3479,6 +3526,15 @@ int morap_cuda_fetch_policies(morap_ctx* ctx, int njobs, const int32_t* jobs, in
     bytes += align_up(sizeof(int32_t) * ctx->hm[ctx->optModel[j]].S, 256);
   }
   cudaSetDevice(ctx->device);
+  if (list == ctx->polPrefetched) {  // staged by evaluate_optimized: wait for the side copies only
+    CK(cudaEventSynchronize(ctx->polCopied));
+    for (int q = 0; q < njobs; ++q)
+      std::memcpy(rows_out[q], static_cast<char*>(ctx->polStage) + ctx->polOff[q],
+                  sizeof(int32_t) * ctx->hm[ctx->optModel[list[q]]].S);
+    return MORAP_OK;
+  }
+  CK(cudaEventSynchronize(ctx->polCopied));  // a stale prefetch may still be copying into polStage
+  ctx->polPrefetched.clear();
   int rc = extract_policies(ctx, list);
   if (rc) return rc;
   // one pinned staging area, one synchronisation for the whole batch
@@ -3524,6 +3580,9 @@ int morap_cuda_evaluate_optimized(morap_ctx* ctx, int njobs, const int32_t* opt_
   const auto tp0 = std::chrono::steady_clock::now();
   int rc = extract_policies(ctx, jl);
   if (rc) return rc;
+  // the caller reads these policies next (supportingPoint's schedulers): copy them to the
+  // pinned staging area on a side stream while the evaluate sweeps run
+  if ((rc = prefetch_policies(ctx, jl))) return rc;
   if (trace) {
     cudaStreamSynchronize(ctx->stream);
     std::fprintf(stderr, "[morap] evaluate_optimized: policies %.3f ms\n",
