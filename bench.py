@@ -413,6 +413,9 @@ def run_ours(args):
                      "avg_launch_us": 1e3 * cs["opt_ms"] / max(cs["opt_launches"], 1),
                      "algorithmic_bytes_per_launch": alg_per_launch,
                      "kernel_backups_per_s": cs["opt_backups"] / (cs["opt_ms"] * 1e-3) if cs["opt_ms"] else None,
+                     "kernel_exec_backups_per_s": (cs["opt_exec_backups"] / (cs["opt_ms"] * 1e-3)
+                                                   if cs["opt_ms"] else None),
+                     "skipped_fraction": 1.0 - cs["opt_exec_backups"] / max(cs["opt_backups"], 1.0),
                      "peak_source": peak_src, "traffic_source": traffic_src and traffic_src.get("source"),
                      "timing": f"CUDA events around every sweep launch over a second pass of the "
                                f"{args.steps} timed steps ({prof_ms / args.steps:.1f} ms per query with the events)",

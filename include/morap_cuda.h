@@ -104,6 +104,16 @@ int morap_cuda_release_models(morap_ctx* ctx);
  * models uploaded after the call, and only where the compact sweep kernels run (with
  * MORAP_COMPACT=0 or MORAP_SWEEP_KERNEL=global every model keeps its arrays). */
 int morap_cuda_set_lean(morap_ctx* ctx, int on);
+/* Frozen-tile skipping in compact optimize sweeps (default on; MORAP_SKIP=0 at create turns
+ * it off): a tile whose successor window and own states did not change bitwise in the
+ * previous sweep is not swept again -- it would reproduce its values bit for bit. Values,
+ * policies, residuals and sweep counts are identical either way. */
+int morap_cuda_set_skip(morap_ctx* ctx, int on);
+/* Diagnostics: enable (1) / disable (0) / leave (-1) the per-CTA timeline of compact
+ * optimize sweeps, and copy up to n words of it to `out` (when non-null): 128 slots (sweep
+ * index mod 128) x sweep CTAs x 4 globaltimer ns {start, first stage consumed, all warps
+ * done, finalize done (last CTA only)}. */
+int morap_cuda_debug_cta_trace(morap_ctx* ctx, int enable, uint64_t* out, int64_t n);
 int morap_cuda_num_models(morap_ctx* ctx);
 /* out[6] = {S, R, nnz, number of objectives, compact (0/1), lean (0/1)} of a device model. */
 int morap_cuda_model_info(morap_ctx* ctx, int model_id, int32_t* out);
@@ -158,10 +168,11 @@ int morap_cuda_fetch_eval_values(morap_ctx* ctx, int job, int rhs, double* value
 /* Instrumentation (SweepStats/bench). Totals since the last reset:
  *   out[0] sweep-kernel launches (optimize), out[1] their summed device ms (only while
  *   profiling is on: CUDA events around each launch, no extra synchronisation), out[2] algorithmic bytes those
- *   launches moved (12*nnz + 12*R + 21*S per active job per sweep),
- *   out[3] nnz backups performed (sum over jobs of sweeps * nnz), out[4..7] the same four
- *   for evaluate sweeps, out[8] kernels launched in total, out[9] host-to-device bytes of model
- *   uploads. */
+ *   launches moved (per swept tile: 4*nnz + 4*R + 20*S for compact models, 12*nnz + 12*R +
+ *   21*S otherwise), out[3] nnz backups of the results (sum over jobs of
+ *   sweeps * nnz: the reference's work), out[4..7] the same four for evaluate sweeps,
+ *   out[8] kernels launched in total, out[9] host-to-device bytes of model uploads,
+ *   out[10] optimize backups actually executed (out[3] minus the frozen tiles skipped). */
 int morap_cuda_set_profiling(morap_ctx* ctx, int on);
 int morap_cuda_stats(morap_ctx* ctx, double* out, int nout);
 int morap_cuda_reset_stats(morap_ctx* ctx);

@@ -52,6 +52,15 @@ constexpr bool kFusedStates = true;  // TMA sweep: thread-per-state single pass 
 // Diagnostics only (MORAP_DEBUG_DRY=1): consumers skip the arithmetic, so the pipeline's
 // pure streaming rate can be measured. Never set in tests or the benchmark.
 __device__ int g_dryRun = 0;
+// diagnostics (morap_cuda_debug_cta_trace): per compact optimize sweep and CTA, globaltimer
+// stamps {start, first stage consumed, all warps done, finalize done (last CTA)}
+__device__ unsigned long long* g_ctaTrace = nullptr;
+constexpr int kTraceSlots = 128;
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Tile descriptor: first state / row / transition of the tile; `fits` = the tile's
 // streams fit one shared-memory stage of the TMA pipeline (every multi-state tile does;
@@ -66,8 +75,7 @@ struct TileDesc {
 // Where a tile's slice starts in each compact sweep stream. Every slice starts on a 16-byte
 // boundary (the streams are padded per tile), so each lands at offset 0 of its stage region.
 struct TilePos {
-  int32_t row, trn, succ, idx;  // u16 row ends, u16 transition ends, u16 window offsets, u8 index
-  int32_t cls, done, pad0, pad1;  // u8 class, u8 done
+  int32_t row, trn, succ, pad;  // u32 state words, u32 row words, u32 transition words
 };
 
 struct DevModel {
@@ -106,6 +114,7 @@ struct OptJob {
   double* classRho;  // compact models: rho_w of each reward class (<= 256)
   double* buf[2];
   int32_t* policy;
+  int32_t* stamp;  // frozen-tile skipping: last sweep in which a state of group g (32 states) changed
 };
 
 struct EvalJob {
@@ -127,9 +136,13 @@ struct Ctl {
   int32_t nactive;      // jobs in the active list
   int32_t totalTiles;   // tiles of active jobs (tilePrefix[nactive])
   int32_t sweepsDone;   // sweeps completed by every active job
+  int32_t nsel;         // tiles selected for the current sweep (k_select); reset by the finalize
+  int32_t claimed;      // dynamic tail of the selected tiles: claimed so far; reset by the finalize
   int32_t pad;
   unsigned long long bytes;    // algorithmic bytes of all sweeps so far
-  unsigned long long backups;  // nnz backups of all sweeps so far
+  unsigned long long backups;  // nnz backups of all sweeps so far (every tile of every active job)
+  unsigned long long execBytes;    // of the tiles actually swept (k_select mode)
+  unsigned long long execBackups;
 };
 
 // --------------------------------------------------------------------------------------
@@ -844,6 +857,7 @@ struct FinArgs {
   int32_t* sweeps;
   double* residual;
   int32_t* status;
+  int32_t* alive;  // per job: sweeps done while still active, -1 once it left the list (k_select)
 };
 
 // exclusive scan of (a, b) over the whole block (any multiple of 32 threads <= 1024)
@@ -889,7 +903,7 @@ __device__ __forceinline__ void block_scan2n(int& a, int& b, int* sa, int* sb, i
 // active list / tile prefix, by one block (k_finalize's body for the optimize kind).
 __device__ void finalize_opt(const DevModel* __restrict__ models, const int32_t* __restrict__ jobModel,
                              int32_t* list, int32_t* prefix, Ctl* ctl, unsigned long long* deltaBits, double eps,
-                             int cap, int32_t* sweeps, double* residual, int32_t* status) {
+                             int cap, int32_t* sweeps, double* residual, int32_t* status, int32_t* alive) {
   __shared__ int sa[32], sb[32];
   __shared__ unsigned long long sBytes[32], sBk[32];
   const int nact = __ldcg(&ctl->nactive);
@@ -913,6 +927,7 @@ __device__ void finalize_opt(const DevModel* __restrict__ models, const int32_t*
       else if (k >= cap) status[job] = MORAP_NON_CONVERGENCE;
       else keep = 1;
       if (keep) nt = M.ntiles;
+      if (alive) alive[job] = keep ? k : -1;
     }
     int pa = keep, pb = nt, ta, tb;
     block_scan2n(pa, pb, sa, sb, ta, tb);
@@ -945,8 +960,107 @@ __device__ void finalize_opt(const DevModel* __restrict__ models, const int32_t*
     ctl->nactive = outBase;
     ctl->totalTiles = tileBase;
     ctl->sweepsDone = k;
+    ctl->nsel = 0;
+    ctl->claimed = 0;
     ctl->bytes += tbytes;
     ctl->backups += tk;
+  }
+}
+
+// Frozen-tile selection (exact work skipping). A tile's new values are a function of x over
+// its successor window only (allIn tiles), so when no state of the window and none of the
+// tile's own states changed bitwise in the previous sweep, this sweep would reproduce the
+// previous values bit for bit -- and the y buffer (two sweeps old) already holds them; the
+// tile's residual contribution is exactly 0 and its policy is extracted after convergence
+// anyway. Such tiles are left out of the sweep. stamp[g] = the last sweep in which a state
+// of group g (32 states) of the job changed (written by the sweep's compute warps; 0 =
+// never). Values, residuals, sweep counts and policies are identical to sweeping every tile.
+//
+// The candidates of an optimize batch -- every tile of every initially active job, with
+// the stamp groups it depends on -- are listed once per batch (k_build_cand); per sweep,
+// k_select keeps the candidates whose job is still active (alive[job] == sweeps done: the
+// finalize stamps every job it keeps, -1 the ones it drops) and whose groups changed in the
+// previous sweep, and
+// compacts them into `sel` (in order within each block, one atomic per block).
+constexpr int kSelThreads = 256;
+#ifndef MORAP_TAIL_PCT
+#define MORAP_TAIL_PCT 25
+#endif
+#ifndef MORAP_CLAIM
+#define MORAP_CLAIM 2
+#endif
+constexpr int kTailPct = MORAP_TAIL_PCT;  // share of the selected tiles handed out dynamically
+constexpr int kClaim = MORAP_CLAIM;       // tiles per claim
+
+// cand[prefix[slot] + lt] = {job, lt, first stamp group (16-byte aligned; -1: never
+// skipped -- oversized or out-of-window tiles), last stamp group}; grid (tile blocks, slots)
+__global__ void __launch_bounds__(kSelThreads) k_build_cand(const DevModel* __restrict__ models,
+                                                            const OptJob* __restrict__ jobs,
+                                                            const int32_t* __restrict__ list,
+                                                            const int32_t* __restrict__ prefix,
+                                                            int4* __restrict__ cand, int slotBase) {
+  const int slot = slotBase + blockIdx.y;
+  const int job = list[slot];
+  const int base = prefix[slot], nt = prefix[slot + 1] - base;
+  const int lt = blockIdx.x * kSelThreads + threadIdx.x;
+  if (lt >= nt) return;
+  const DevModel& M = models[jobs[job].model];
+  const int4* tp = reinterpret_cast<const int4*>(M.tiles + lt);
+  const int4 d0 = tp[0], d1 = tp[1], e0 = tp[2];  // (s0 r0 k0 fits) (wlo wn allIn simple) (next s0 ...)
+  int g0 = -1, g1 = -1;
+  if (d0.w && d1.z) {
+    const int lo = min(d1.x, d0.x), hi = max(d1.x + d1.y, e0.x);
+    g0 = (lo >> 5) & ~3;
+    g1 = (hi - 1) >> 5;
+  }
+  cand[base + lt] = make_int4(job, lt, g0, g1);
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_select(const OptJob* __restrict__ jobs,
+                                                        const int32_t* __restrict__ alive,
+                                                        const int4* __restrict__ cand, int ncand, Ctl* ctl,
+                                                        int2* __restrict__ sel) {
+  __shared__ int sCnt[kSelThreads / 32];
+  __shared__ int sBase;
+  const int k = ctl->sweepsDone;
+  if (ctl->nactive == 0) return;
+  const int per = ((ncand + gridDim.x - 1) / gridDim.x + kSelThreads - 1) / kSelThreads * kSelThreads;
+  const int t0 = blockIdx.x * per, t1 = min(ncand, t0 + per);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = t0; base < t1; base += kSelThreads) {
+    const int t = base + threadIdx.x;
+    int keep = 0;
+    int4 c = make_int4(0, 0, 0, 0);
+    if (t < t1) {
+      c = __ldg(cand + t);
+      if (__ldcg(alive + c.x) == k) {  // job still active
+        keep = 1;
+        if (k > 0 && c.z >= 0) {
+          const int32_t* stamp = jobs[c.x].stamp;
+          int m = 0;
+          for (int g = c.z; g <= c.w; g += 4) {  // 16-byte aligned groups of 4 stamps
+            const int4 q = __ldcg(reinterpret_cast<const int4*>(stamp + g));
+            m = max(m, max(max(q.x, q.y), max(q.z, q.w)));
+          }
+          keep = m >= k;  // something it depends on changed in the previous sweep
+        }
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) sCnt[wid] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run = 0;
+      for (int w = 0; w < kSelThreads / 32; ++w) {
+        const int n = sCnt[w];
+        sCnt[w] = run;
+        run += n;
+      }
+      sBase = run ? atomicAdd(&ctl->nsel, run) : 0;
+    }
+    __syncthreads();
+    if (keep) sel[sBase + sCnt[wid] + __popc(bal & ((1u << lane) - 1u))] = make_int2(c.x, c.y);
+    __syncthreads();
   }
 }
 
@@ -954,7 +1068,8 @@ __device__ void finalize_opt(const DevModel* __restrict__ models, const int32_t*
 struct alignas(16) CmpInfo {
   int t, job, fits, allIn;
   int simple, s0, r0, k0;
-  int ns, offX, pad0, pad1;
+  int ns, offX;
+  int32_t* stamp;  // frozen-tile stamps of the job (nullptr: no skipping)
   const double* dict;
   const double* classRho;
   const double* x;
@@ -973,22 +1088,30 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
                                                                      const Ctl* __restrict__ ctl,
                                                                      const int32_t* __restrict__ jobSweeps,
                                                                      unsigned long long* __restrict__ deltaBits,
-                                                                     FinArgs fin) {
+                                                                     const int2* __restrict__ sel, FinArgs fin) {
+  // sel != nullptr: sweep only the (job, tile) pairs k_select kept (frozen-tile skipping);
+  // otherwise every tile of every active job (prefix / list)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[kCmpStages], empty[kCmpStages];
   __shared__ CmpInfo info[kCmpStages];
   __shared__ double sRed[kConsumers / 32];
-  __shared__ int32_t sPos[32][8];  // producer: TilePos of the current batch of 32 tiles
+  __shared__ int32_t sPos[32][4];  // producer: TilePos of the current batch of 32 tiles
 
   const int nact = ctl->nactive;
-  const int total = ctl->totalTiles;
-  if (total <= 0) return;
-  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int total = sel ? ctl->nsel : ctl->totalTiles;
+  // sel mode: the first (100 - kTailPct)% of the tiles are split evenly over the CTAs, the
+  // rest is claimed kClaim tiles at a time by whichever CTAs finish first (tiles differ in
+  // work, and a static split alone leaves a ~25% tail)
+  const int staticN = sel ? total - static_cast<int>(static_cast<long long>(total) * kTailPct / 100) : total;
+  const int per = (staticN + gridDim.x - 1) / gridDim.x;
   const int t0 = blockIdx.x * per;
-  const int t1 = min(total, t0 + per);
+  const int t1 = min(staticN, t0 + per);
   const int k = ctl->sweepsDone;
   const int tid = threadIdx.x;
-  if (t0 < t1) {  // this CTA has tiles (the fused finalize below runs in every CTA)
+  unsigned long long* trace =
+      !POLICY && g_ctaTrace ? g_ctaTrace + (static_cast<size_t>(k % kTraceSlots) * gridDim.x + blockIdx.x) * 4 : nullptr;
+  if (trace && tid == 0) trace[0] = global_ns();
+  if (t0 < t1 || staticN < total) {  // this CTA has tiles (the fused finalize below runs in every CTA)
   if (tid == 0) {
     for (int q = 0; q < kCmpStages; ++q) {
       mbar_init(&full[q], 1);
@@ -1007,7 +1130,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     // bulk copy of stream i.
     const int lane = tid & 31;
     const uint64_t pol = evict_first_policy(), polKeep = evict_last_policy();
-    int ai = find_slot(prefix, nact + 1, t0);
+    int ai = sel ? 0 : find_slot(prefix, nact + 1, t0);
     int use = 0;
     int curJob = -1;
     const unsigned char* myBase = nullptr;  // stream base of this lane for curJob
@@ -1018,34 +1141,48 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     const DevModel* curM = nullptr;
     const OptJob* curJ = nullptr;
     int parity = k & 1;
-    for (int tb = t0; tb < t1; tb += 32) {
-      // ---- resolve tiles tb .. tb+31, one per lane -----------------------------------
+    uint32_t exBytes = 0, exNnz = 0;  // sel mode: what this CTA swept (DESIGN.md §4 bytes)
+    for (int tb = t0, tEnd = t1;;) {
+      if (tb >= tEnd) {  // static range done: claim from the dynamic tail
+        if (staticN >= total) break;
+        int c = 0;
+        if (lane == 0) c = atomicAdd(&const_cast<Ctl*>(ctl)->claimed, kClaim);
+        tb = staticN + __shfl_sync(0xffffffffu, c, 0);
+        if (tb >= total) break;
+        tEnd = min(total, tb + kClaim);
+      }
+      const int nb = min(32, tEnd - tb);
+      // ---- resolve tiles tb .. tb+nb-1, one per lane ---------------------------------
       const int tl = tb + lane;
       int mJob = 0, mS0 = 0, mR0 = 0, mK0 = 0, mFits = 0, mWlo = 0, mWn = 0, mAll = 0, mSimple = 0, eS0 = 0,
           eR0 = 0, eK0 = 0;
       __syncwarp();  // the previous batch is done with sPos
-      if (tl < t1) {
-        int a = ai;
-        while (tl >= prefix[a + 1]) ++a;
-        mJob = list[a];
-        const int lt = tl - prefix[a];
+      if (lane < nb) {
+        int lt;
+        if (sel) {
+          const int2 e = sel[tl];
+          mJob = e.x;
+          lt = e.y;
+        } else {
+          int a = ai;
+          while (tl >= prefix[a + 1]) ++a;
+          mJob = list[a];
+          lt = tl - prefix[a];
+        }
         const DevModel* M = &models[jobs[mJob].model];
         const int4* tp = reinterpret_cast<const int4*>(M->tiles + lt);
         const int4 d0 = tp[0], d1 = tp[1], e0 = tp[2];
-        const int4* pp = reinterpret_cast<const int4*>(M->tilePos + lt);
-        const int4 p0 = pp[0], p1 = pp[1];
+        const int4 p0 = *reinterpret_cast<const int4*>(M->tilePos + lt);
         mS0 = d0.x; mR0 = d0.y; mK0 = d0.z; mFits = d0.w;
         mWlo = d1.x; mWn = d1.y; mAll = d1.z; mSimple = d1.w;
         eS0 = e0.x; eR0 = e0.y; eK0 = e0.z;
-        sPos[lane][0] = p0.x; sPos[lane][1] = p0.y; sPos[lane][2] = p0.z; sPos[lane][3] = p0.w;
-        sPos[lane][4] = p1.x; sPos[lane][5] = p1.y;
+        sPos[lane][0] = p0.x; sPos[lane][1] = p0.y; sPos[lane][2] = p0.z;
       }
       __syncwarp();
-      {  // advance ai to the slot of the last tile of the batch
-        const int last = min(t1, tb + 32) - 1;
+      if (!sel) {  // advance ai to the slot of the last tile of the batch
+        const int last = tb + nb - 1;
         while (last >= prefix[ai + 1]) ++ai;
       }
-      const int nb = min(32, t1 - tb);
       for (int q = 0; q < nb; ++q, ++use) {
         const int ti = tb + q;
         const int job = __shfl_sync(0xffffffffu, mJob, q);
@@ -1056,6 +1193,10 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
         const int simple = __shfl_sync(0xffffffffu, mSimple, q);
         const int s1 = __shfl_sync(0xffffffffu, eS0, q), r1 = __shfl_sync(0xffffffffu, eR0, q);
         const int k1 = __shfl_sync(0xffffffffu, eK0, q);
+        if (sel) {
+          exBytes += 4u * (k1 - k0) + 4u * (r1 - r0) + 20u * (s1 - s0);
+          exNnz += static_cast<uint32_t>(k1 - k0);
+        }
         if (job != curJob) {  // uniform: reload this lane's stream base for the new job
           curJob = job;
           curJ = &jobs[job];
@@ -1074,9 +1215,10 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
         }
         const int b = use % kCmpStages;
         // stream of this lane: [lo, hi) in elements of 1 << sh bytes, selected without
-        // branching (lanes 0-5: tile-major padded streams, slice start from TilePos)
-        const int pos = lane < 6 ? sPos[q][lane] : 0;
-        const int len = lane == 0 || lane == 5 ? s1 - s0 : (lane == 1 ? r1 - r0 : k1 - k0);
+        // branching (lanes 0-2: tile-major padded streams, slice start from TilePos;
+        // lane 6: own x; lane 7: the successor window)
+        const int pos = lane < 3 ? sPos[q][lane] : 0;
+        const int len = lane == 0 ? s1 - s0 : (lane == 1 ? r1 - r0 : k1 - k0);
         long long lo = lane < 6 ? pos : (lane == 6 ? s0 : wlo);
         long long hi = lane < 6 ? pos + len : (lane == 6 ? s1 : wlo + wn);
         if (lane > 7 || (lane >= 3 && lane <= 5)) lo = hi = 0;  // lanes 3-5: no stream
@@ -1102,7 +1244,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           rec.k0 = k0;
           rec.ns = s1 - s0;
           rec.offX = offX;
-          rec.pad0 = rec.pad1 = 0;
+          rec.stamp = POLICY ? nullptr : curJ->stamp;
           rec.dict = curM->probDict;
           rec.classRho = curJ->classRho;
           rec.x = curJ->buf[parity];
@@ -1122,6 +1264,11 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
         __syncwarp();
         if (bytes) bulk_g2s(smem + b * kCStageBytes + dstOff, myBase + a0, bytes, bar, lp);
       }
+      tb += nb;
+    }
+    if (sel && lane == 0 && exNnz) {
+      atomicAdd(&const_cast<Ctl*>(ctl)->execBytes, static_cast<unsigned long long>(exBytes));
+      atomicAdd(&const_cast<Ctl*>(ctl)->execBackups, static_cast<unsigned long long>(exNnz));
     }
     if (lane == 0) {
       const int b = use % kCmpStages;
@@ -1141,6 +1288,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     const int b = use % kCmpStages;
     mbar_wait_sleep(&full[b], (use / kCmpStages) & 1);
     const CmpInfo v = info[b];
+    if (trace && use == 0 && tid == 0) trace[1] = global_ns();
     if (v.t < 0) break;
     if (!POLICY && v.job != runJob) {  // uniform over the consumers
       if (runJob >= 0) {
@@ -1240,8 +1388,11 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           if (POLICY) {
             v.policy[s] = v.r0 + bestRow;
           } else {
+            const double xo = xS[tid];
             v.y[s] = best;
-            dl = fabs(__dsub_rn(best, xS[tid]));
+            dl = fabs(__dsub_rn(best, xo));
+            // bitwise change (not |y - x| > 0: -0.0 and +0.0 differ for the skip invariant)
+            if (v.stamp && __double_as_longlong(best) != __double_as_longlong(xo)) v.stamp[s >> 5] = k + 1;
           }
         }
       }
@@ -1275,8 +1426,10 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           if (POLICY) {
             v.policy[s] = r0 + bestRow;
           } else {
+            const double xo = x[s];
             v.y[s] = best;
-            dl = fabs(__dsub_rn(best, x[s]));
+            dl = fabs(__dsub_rn(best, xo));
+            if (v.stamp && __double_as_longlong(best) != __double_as_longlong(xo)) v.stamp[s >> 5] = k + 1;
           }
         }
       }
@@ -1297,6 +1450,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     __shared__ int sLast;
     __syncthreads();
     if (tid == 0) {
+      if (trace) trace[2] = global_ns();
       __threadfence();
       sLast = atomicAdd(fin.count, 1u) == gridDim.x - 1;
     }
@@ -1304,8 +1458,12 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     if (sLast) {
       __threadfence();
       finalize_opt(models, fin.jobModel, const_cast<int32_t*>(list), const_cast<int32_t*>(prefix),
-                   const_cast<Ctl*>(ctl), deltaBits, fin.eps, fin.cap, fin.sweeps, fin.residual, fin.status);
-      if (tid == 0) *fin.count = 0u;
+                   const_cast<Ctl*>(ctl), deltaBits, fin.eps, fin.cap, fin.sweeps, fin.residual, fin.status,
+                   fin.alive);
+      if (tid == 0) {
+        *fin.count = 0u;
+        if (trace) trace[3] = global_ns();
+      }
     }
   }
 }
@@ -2144,7 +2302,7 @@ struct morap_ctx {
   std::string err;
   bool profiling = false;
   bool trace = std::getenv("MORAP_TRACE") != nullptr;
-  double stats[10] = {0};
+  double stats[11] = {0};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   std::vector<HostModel> hm;
@@ -2186,19 +2344,21 @@ struct morap_ctx {
   double* dResidual = nullptr;
   double* dGather = nullptr;
   int32_t* dStatus = nullptr;
+  int32_t* dAlive = nullptr;
   void* evalStage = nullptr;
   size_t evalStageBytes = 0;
   void* stage = nullptr;  // pinned host staging for uploads
   size_t stageBytes = 0;
   std::vector<cudaEvent_t> evPool;  // per-sweep start/stop events (profiling, no graphs)
-  static constexpr int kKeyPtrs = 14;
+  static constexpr int kKeyPtrs = 16;
   struct GraphKey {
-    int kind, B, cap, variant;
+    int kind, B, cap, variant, ncand;
     double eps;
     bool timed;
     const void* ptrs[kKeyPtrs];
     bool operator==(const GraphKey& o) const {
-      if (kind != o.kind || B != o.B || cap != o.cap || variant != o.variant || eps != o.eps || timed != o.timed)
+      if (kind != o.kind || B != o.B || cap != o.cap || variant != o.variant || ncand != o.ncand || eps != o.eps ||
+          timed != o.timed)
         return false;
       for (int i = 0; i < kKeyPtrs; ++i)
         if (ptrs[i] != o.ptrs[i]) return false;
@@ -2216,6 +2376,15 @@ struct morap_ctx {
   bool lean = false;       // compact models uploaded without their fp64 prob / objective arrays
   bool optCompact = false; // current optimize batch runs the deep compact pipeline
   int cmpBlocks = 0;
+  bool skip = true;        // frozen-tile skipping in compact optimize sweeps (k_select)
+  bool timeSweepOnly = std::getenv("MORAP_TIME_SWEEP_ONLY") != nullptr;  // profiling: k_select outside the events
+  bool optSkip = false;    // current optimize batch uses it
+  int selBlocks = 0;
+  int2* dSel = nullptr;    // (job, tile) pairs of the current sweep
+  int4* dCand = nullptr;   // candidates of the current optimize batch (k_build_cand)
+  int nCand = 0;
+  void* dTrace = nullptr;  // diagnostics: per-CTA sweep timeline (morap_cuda_debug_cta_trace)
+  size_t selCap = 0;
   bool usePersistent = true;  // evaluate batches as one cooperative launch
   int persistBlocks = 0;
   bool usePersistCache = false;
@@ -2257,7 +2426,9 @@ int ensure_ctl(morap_ctx* ctx, size_t njobs) {
   cudaFree(ctx->dResidual);
   cudaFree(ctx->dStatus);
   cudaFree(ctx->dGather);
+  cudaFree(ctx->dAlive);
   CK(cudaMalloc(&ctx->dGather, cap * MORAP_MAX_RHS * sizeof(double)));
+  CK(cudaMalloc(&ctx->dAlive, cap * sizeof(int32_t)));
   CK(cudaMalloc(&ctx->dList, cap * sizeof(int32_t)));
   CK(cudaMalloc(&ctx->dPrefix, (cap + 1) * sizeof(int32_t)));
   CK(cudaMalloc(&ctx->dJobModel, cap * sizeof(int32_t)));
@@ -2360,7 +2531,7 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
   const size_t nt = desc.size() - 1;
   c.pos.assign(nt, TilePos{});
   auto up16 = [](size_t n, size_t es) { return (n * es + 15) / 16 * 16 / es; };  // elements, padded
-  size_t nRow = 0, nTrn = 0, nSucc = 0, nIdx = 0, nCls = 0, nDone = 0;
+  size_t nRow = 0, nTrn = 0, nSucc = 0;
   for (size_t t = 0; t < nt; ++t) {
     const TileDesc &d = desc[t], &e = desc[t + 1];
     const bool f = d.fits != 0;  // oversized tiles are swept from the global arrays
@@ -2369,27 +2540,19 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
     p.row = static_cast<int32_t>(nRow);
     p.trn = static_cast<int32_t>(nTrn);
     p.succ = static_cast<int32_t>(nSucc);
-    p.idx = static_cast<int32_t>(nIdx);
-    p.cls = static_cast<int32_t>(nCls);
-    p.done = static_cast<int32_t>(nDone);
     nRow += up16(ns, 4);
     nTrn += up16(nr, 4);
     nSucc += up16(nz, 4);
-    nDone += up16(ns, 1);
   }
-  (void)nIdx;
-  (void)nCls;
-  (void)nDone;
   c.stW.assign(nRow, 0);
   c.rowW.assign(nTrn, 0);
   c.trW.assign(nSucc, 0xFFFFu);
   for (size_t t = 0; t < nt; ++t) {
     TileDesc& d = desc[t];
     const TileDesc& e = desc[t + 1];
-    d.allIn = 1;
-    d.simple = 1;
-    for (int r = d.r0; r < e.r0; ++r)
-      if (v.trn_offset[r + 1] - v.trn_offset[r] > 2) d.simple = 0;
+    int simple = 1;
+    for (int r = d.r0; r < e.r0; ++r) simple &= v.trn_offset[r + 1] - v.trn_offset[r] <= 2 ? 1 : 0;
+    d.simple = simple;
     if (!d.fits) {
       d.allIn = 0;
       continue;
@@ -2402,12 +2565,14 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
     for (int r = d.r0; r < e.r0; ++r)
       c.rowW[p.trn + (r - d.r0)] =
           static_cast<uint32_t>(v.trn_offset[r + 1] - d.k0) | (static_cast<uint32_t>(c.cls[r]) << 16);
+    int allIn = 1;
     for (int k = d.k0; k < e.k0; ++k) {
       const unsigned o = static_cast<unsigned>(v.succ[k] - d.wlo);
       const bool in = o < static_cast<unsigned>(d.wn);
       c.trW[p.succ + (k - d.k0)] = (in ? o : 0xFFFFu) | (static_cast<uint32_t>(c.idx[k]) << 16);
-      if (!in) d.allIn = 0;
+      allIn &= in ? 1 : 0;
     }
+    d.allIn = allIn;
   }
 }
 
@@ -2440,30 +2605,29 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
   if (K < 1) return;
   c.idx.resize(static_cast<size_t>(v.nnz));
   SmallIds probs(1);
-  // the first few distinct values are matched by a linear scan (warehouse products have
-  // three probabilities), the rest through the hash table
+  // the first few distinct values are matched by an unrolled compare against a sentinel-padded
+  // list (warehouse products have three probabilities; ~0 is a NaN payload, never a valid
+  // probability's bits), so the common case has no data-dependent branch; the rest go
+  // through the hash table
   constexpr int kScan = 8;
   uint64_t seen[kScan];
+  for (int q = 0; q < kScan; ++q) seen[q] = ~0ull;
   int nseen = 0;
-  uint64_t last = ~0ull;
-  int lastId = -1;
   for (int k = 0; k < v.nnz; ++k) {
     uint64_t b;
     std::memcpy(&b, &v.prob[k], 8);
-    if (b != last) {
-      lastId = -1;
-      for (int q = 0; q < nseen; ++q) lastId = seen[q] == b ? q : lastId;  // branch-free (selects)
-      if (lastId < 0) {
-        lastId = probs.find(&b);
-        if (lastId < 0) return;
-        if (lastId == static_cast<int>(c.dict.size())) {
-          c.dict.push_back(v.prob[k]);
-          if (nseen < kScan && lastId == nseen) seen[nseen++] = b;
-        }
+    int id = -1;
+#pragma unroll
+    for (int q = 0; q < kScan; ++q) id = seen[q] == b ? q : id;
+    if (id < 0) {
+      id = probs.find(&b);
+      if (id < 0) return;
+      if (id == static_cast<int>(c.dict.size())) {
+        c.dict.push_back(v.prob[k]);
+        if (nseen < kScan && id == nseen) seen[nseen++] = b;
       }
-      last = b;
     }
-    c.idx[k] = static_cast<uint8_t>(lastId);
+    c.idx[k] = static_cast<uint8_t>(id);
   }
   c.cls.resize(static_cast<size_t>(v.num_rows));
   SmallIds classes(K);
@@ -2559,13 +2723,16 @@ int validate_view(morap_ctx* ctx, const morap_csr_view& v, int idx) {
   if (v.num_objectives < 0 || v.num_objectives > MORAP_MAX_OBJECTIVES) return bad("too many objectives");
   if (!v.row_offset || !v.trn_offset || !v.done || (v.nnz && (!v.succ || !v.prob))) return bad("null array");
   if (v.row_offset[0] != 0 || v.row_offset[v.num_states] != v.num_rows) return bad("rowOffset does not span the rows");
-  for (int s = 0; s < v.num_states; ++s)
-    if (v.row_offset[s + 1] < v.row_offset[s]) return bad("rowOffset not monotone");
+  // branch-free reductions (vectorised), the message picked afterwards
+  int ok = 1;
+  for (int s = 0; s < v.num_states; ++s) ok &= v.row_offset[s + 1] >= v.row_offset[s] ? 1 : 0;
+  if (!ok) return bad("rowOffset not monotone");
   if (v.trn_offset[0] != 0 || v.trn_offset[v.num_rows] != v.nnz) return bad("trnOffset does not span nnz");
-  for (int r = 0; r < v.num_rows; ++r)
-    if (v.trn_offset[r + 1] < v.trn_offset[r]) return bad("trnOffset not monotone");
-  for (int k = 0; k < v.nnz; ++k)
-    if (v.succ[k] < 0 || v.succ[k] >= v.num_states) return bad("successor out of range");
+  for (int r = 0; r < v.num_rows; ++r) ok &= v.trn_offset[r + 1] >= v.trn_offset[r] ? 1 : 0;
+  if (!ok) return bad("trnOffset not monotone");
+  const unsigned S = static_cast<unsigned>(v.num_states);
+  for (int k = 0; k < v.nnz; ++k) ok &= static_cast<unsigned>(v.succ[k]) < S ? 1 : 0;
+  if (!ok) return bad("successor out of range");
   for (int o = 0; o < v.num_objectives; ++o)
     if (!v.rewards || !v.rewards[o]) return bad("null reward vector");
   return MORAP_OK;
@@ -2606,11 +2773,20 @@ int ensure_arena(morap_ctx* ctx, void** arena, size_t* have, size_t need) {
 int enqueue_sweeps(morap_ctx* ctx, int kind, double eps, int cap, int B, const cudaEvent_t* ev, bool capturing) {
   const unsigned evFlags = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
   for (int i = 0; i < B; ++i) {
-    if (ev) CK(cudaEventRecordWithFlags(ev[2 * i], ctx->stream, evFlags));
+    const bool selTimed = !(kind == 0 && ctx->useTma && ctx->optCompact && ctx->optSkip && ctx->timeSweepOnly);
+    if (ev && selTimed) CK(cudaEventRecordWithFlags(ev[2 * i], ctx->stream, evFlags));
     if (kind == 0 && ctx->useTma && ctx->optCompact) {
-      const FinArgs fin{ctx->dFinCount, ctx->dJobModel, eps, cap, ctx->dSweeps, ctx->dResidual, ctx->dStatus};
+      const FinArgs fin{ctx->dFinCount, ctx->dJobModel, eps, cap, ctx->dSweeps, ctx->dResidual, ctx->dStatus,
+                        ctx->optSkip ? ctx->dAlive : nullptr};
+      if (ctx->optSkip) {
+        k_select<<<ctx->selBlocks, kSelThreads, 0, ctx->stream>>>(ctx->dOptJobs, ctx->dAlive, ctx->dCand,
+                                                                  ctx->nCand, ctx->dCtl, ctx->dSel);
+        CK(cudaGetLastError());
+      }
+      if (ev && !selTimed) CK(cudaEventRecordWithFlags(ev[2 * i], ctx->stream, evFlags));
       k_greedy_sweep_cmp<false><<<ctx->cmpBlocks, kTmaThreads, kCmpSmemBytes, ctx->stream>>>(
-          ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta, fin);
+          ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta,
+          ctx->optSkip ? ctx->dSel : nullptr, fin);
     } else if (kind == 0 && ctx->useTma) {
       k_greedy_sweep_tma<false><<<ctx->tmaBlocks, kTmaThreads, kTmaSmemBytes, ctx->stream>>>(
           ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, nullptr, ctx->dDelta);
@@ -2652,10 +2828,11 @@ int batch_graph(morap_ctx* ctx, int kind, double eps, int cap, int B, bool timed
   key.eps = eps;
   key.cap = cap;
   key.timed = timed;
-  key.variant = (ctx->useTma ? 1 : 0) | (ctx->evalTma ? 2 : 0) | (ctx->optCompact ? 4 : 0);
+  key.variant = (ctx->useTma ? 1 : 0) | (ctx->evalTma ? 2 : 0) | (ctx->optCompact ? 4 : 0) | (ctx->optSkip ? 8 : 0);
+  key.ncand = kind == 0 && ctx->optSkip ? ctx->nCand : 0;
   const void* ptrs[] = {ctx->dModels, ctx->dOptJobs, ctx->dList,  ctx->dPrefix,    ctx->dCtl,      ctx->dDelta,
                         ctx->dMask,   ctx->dNrhs,    ctx->dSweeps, ctx->dResidual, ctx->dStatus,   ctx->dJobModel,
-                        ctx->dEvalJobsRaw, ctx->stream};
+                        ctx->dEvalJobsRaw, ctx->stream, ctx->dSel, ctx->dCand};
   static_assert(sizeof(ptrs) / sizeof(ptrs[0]) == morap_ctx::kKeyPtrs, "graph key size");
   for (int i = 0; i < morap_ctx::kKeyPtrs; ++i) key.ptrs[i] = ptrs[i];
   for (auto& g : ctx->graphs)
@@ -2718,7 +2895,7 @@ int run_loop(morap_ctx* ctx, int kind, double eps, int cap) {
       }
       if ((rc = enqueue_sweeps(ctx, kind, eps, cap, batch, timed ? ctx->evPool.data() : nullptr, false))) return rc;
     }
-    ctx->stats[8] += (kind == 0 && ctx->useTma && ctx->optCompact ? 1 : 2) * batch;
+    ctx->stats[8] += (kind == 0 && ctx->useTma && ctx->optCompact ? (ctx->optSkip ? 2 : 1) : 2) * batch;
     CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (timed) {
@@ -2778,6 +2955,7 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   // x region is zeroed with one memset (x = y = 0 at the start, numerics.hpp:81)
   size_t rhoBytes = 0, xBytes = 0, polBytes = 0;
   std::vector<size_t> offRho(njobs), offX(njobs), offPol(njobs);
+  auto stampBytes = [](int S) { return align_up(sizeof(int32_t) * (((S + 31) / 32 + 7) & ~3), 256); };
   // compact sweeps read rho_w per reward class only: no per-row rho vector then
   bool allCompact = ctx->useCompact && ctx->useTma && !rhoHost;
   for (int j = 0; j < njobs && allCompact; ++j)
@@ -2788,7 +2966,7 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     const bool lean = !ctx->dm[model_ids[j]].prob;  // lean compact model: class table only
     if (!lean && !allCompact) rhoBytes += align_up(sizeof(double) * m.R, 256);
     offX[j] = xBytes;
-    xBytes += 2 * align_up(sizeof(double) * m.S, 256);
+    xBytes += 2 * align_up(sizeof(double) * m.S, 256) + stampBytes(m.S);  // x0 | x1 | stamps
     offPol[j] = polBytes;
     polBytes += align_up(sizeof(int32_t) * m.S, 256);
   }
@@ -2814,6 +2992,7 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     J.buf[0] = reinterpret_cast<double*>(base + rhoBytes + offX[j]);
     J.buf[1] = reinterpret_cast<double*>(base + rhoBytes + offX[j] + align_up(sizeof(double) * m.S, 256));
     J.policy = reinterpret_cast<int32_t*>(base + rhoBytes + xBytes + offPol[j]);
+    J.stamp = reinterpret_cast<int32_t*>(base + rhoBytes + offX[j] + 2 * align_up(sizeof(double) * m.S, 256));
     J.classRho = (!rhoHost && ctx->dm[model_ids[j]].compact)
                      ? reinterpret_cast<double*>(base + rhoBytes + xBytes + polBytes + 256ull * sizeof(double) * j)
                      : nullptr;
@@ -2824,6 +3003,24 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   }
   CK(cudaMemsetAsync(base + rhoBytes, 0, xBytes, ctx->stream));
   ctx->optCompact = allCompact;
+  ctx->optSkip = allCompact && ctx->skip;
+  if (ctx->optSkip) {
+    size_t tiles = 0;
+    for (int j : active) tiles += static_cast<size_t>(ctx->hm[model_ids[j]].ntiles);
+    if (tiles > ctx->selCap) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      cudaFree(ctx->dSel);
+      cudaFree(ctx->dCand);
+      ctx->dSel = nullptr;
+      ctx->dCand = nullptr;
+      ctx->selCap = std::max(tiles, ctx->selCap + ctx->selCap / 2);
+      CK(cudaMalloc(&ctx->dSel, ctx->selCap * sizeof(int2)));
+      CK(cudaMalloc(&ctx->dCand, ctx->selCap * sizeof(int4)));
+    }
+    ctx->nCand = static_cast<int>(tiles);
+  }
+  if (!ctx->optSkip)
+    for (int j = 0; j < njobs; ++j) ctx->hOptJobs[j].stamp = nullptr;
   if (!ctx->optCompact)
     for (int j = 0; j < njobs; ++j)
       if (!ctx->dm[model_ids[j]].prob)
@@ -2834,6 +3031,21 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   CK(cudaMemsetAsync(ctx->dDelta, 0, njobs * sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->dResidual, 0, njobs * sizeof(double), ctx->stream));
   if ((rc = init_ctl(ctx, active, ctx->optModel))) return rc;
+  if (ctx->optSkip && !active.empty()) {
+    std::vector<int32_t> alive(njobs, -1);
+    for (int j : active) alive[j] = 0;
+    CK(cudaMemcpyAsync(ctx->dAlive, alive.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));  // `alive` is a local
+    int maxTiles = 0;
+    for (int j : active) maxTiles = std::max(maxTiles, ctx->hm[model_ids[j]].ntiles);
+    for (size_t s0 = 0; s0 < active.size(); s0 += 65535) {  // gridDim.y limit
+      const dim3 grid((maxTiles + kSelThreads - 1) / kSelThreads, static_cast<unsigned>(std::min<size_t>(65535, active.size() - s0)));
+      k_build_cand<<<grid, kSelThreads, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix,
+                                                          ctx->dCand, static_cast<int>(s0));
+      CK(cudaGetLastError());
+      ctx->stats[8] += 1;
+    }
+  }
 
   // rho: device-side weighted reward, or host-provided vectors
   if (rhoHost) {
@@ -2877,8 +3089,11 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     backups += static_cast<double>(ctx->optSweeps[j]) * ctx->hm[model_ids[j]].nnz;
   }
   ctx->stats[0] += ctx->hCtl->sweepsDone;
-  ctx->stats[2] += static_cast<double>(ctx->hCtl->bytes);
+  // bytes: what the sweeps actually streamed; backups: sweeps x nnz of every job (the
+  // reference's work for the same results); [10]: backups actually executed
+  ctx->stats[2] += static_cast<double>(ctx->optSkip ? ctx->hCtl->execBytes : ctx->hCtl->bytes);
   ctx->stats[3] += backups;
+  ctx->stats[10] += ctx->optSkip ? static_cast<double>(ctx->hCtl->execBackups) : backups;
   ctx->optPolicyReady.assign(njobs, 0);
   ctx->optJobs = njobs;
   return MORAP_OK;
@@ -2895,7 +3110,7 @@ int extract_policies(morap_ctx* ctx, const std::vector<int32_t>& jobsIn) {
   CK(cudaMemcpyAsync(ctx->dSweeps, ctx->optSweeps.data(), ctx->optSweeps.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->useTma && ctx->optCompact)
     k_greedy_sweep_cmp<true><<<ctx->cmpBlocks, kTmaThreads, kCmpSmemBytes, ctx->stream>>>(
-        ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr, FinArgs{});
+        ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr, nullptr, FinArgs{});
   else if (ctx->useTma)
     k_greedy_sweep_tma<true><<<ctx->tmaBlocks, kTmaThreads, kTmaSmemBytes, ctx->stream>>>(
         ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr);
@@ -3190,6 +3405,9 @@ int morap_cuda_create(int device, morap_ctx** out) {
   }
   const char* csel = std::getenv("MORAP_COMPACT");  // "0" keeps the plain fp64 streams (A/B)
   ctx->useCompact = !(csel && std::string(csel) == "0");
+  const char* ksel = std::getenv("MORAP_SKIP");  // "0" sweeps every tile every sweep (A/B)
+  ctx->skip = !(ksel && std::string(ksel) == "0");
+  ctx->selBlocks = ctx->numSMs * 4;
   if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return MORAP_CUDA_ERROR; }
   if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->polReady, cudaEventDisableTiming) != cudaSuccess ||
@@ -3242,6 +3460,9 @@ int morap_cuda_destroy(morap_ctx* ctx) {
     cudaGraphExecDestroy(g.exec);
     for (cudaEvent_t e : g.ev) cudaEventDestroy(e);
   }
+  cudaFree(ctx->dSel);
+  cudaFree(ctx->dCand);
+  cudaFree(ctx->dTrace);
   cudaFree(ctx->dCtl);
   cudaFreeHost(ctx->hCtl);
   cudaEventDestroy(ctx->ev0);
@@ -3690,6 +3911,32 @@ int morap_cuda_set_lean(morap_ctx* ctx, int on) {
   return MORAP_OK;
 }
 
+int morap_cuda_debug_cta_trace(morap_ctx* ctx, int enable, uint64_t* out, int64_t n) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  cudaSetDevice(ctx->device);
+  const size_t words = static_cast<size_t>(kTraceSlots) * ctx->cmpBlocks * 4;
+  if (enable > 0) {
+    if (!ctx->dTrace) CK(cudaMalloc(&ctx->dTrace, words * 8));
+    CK(cudaMemset(ctx->dTrace, 0, words * 8));
+    unsigned long long* p = static_cast<unsigned long long*>(ctx->dTrace);
+    CK(cudaMemcpyToSymbol(g_ctaTrace, &p, sizeof(p)));
+  } else if (enable == 0) {
+    unsigned long long* p = nullptr;
+    CK(cudaMemcpyToSymbol(g_ctaTrace, &p, sizeof(p)));
+  }
+  if (out && ctx->dTrace) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(out, ctx->dTrace, std::min<size_t>(words, static_cast<size_t>(n)) * 8, cudaMemcpyDeviceToHost));
+  }
+  return MORAP_OK;
+}
+
+int morap_cuda_set_skip(morap_ctx* ctx, int on) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  ctx->skip = on != 0;
+  return MORAP_OK;
+}
+
 int morap_cuda_set_profiling(morap_ctx* ctx, int on) {
   if (!ctx) return MORAP_INVALID_CONFIG;
   ctx->profiling = on != 0;
@@ -3698,7 +3945,7 @@ int morap_cuda_set_profiling(morap_ctx* ctx, int on) {
 
 int morap_cuda_stats(morap_ctx* ctx, double* out, int nout) {
   if (!ctx) return MORAP_INVALID_CONFIG;
-  for (int i = 0; i < nout && i < 10; ++i) out[i] = ctx->stats[i];
+  for (int i = 0; i < nout && i < 11; ++i) out[i] = ctx->stats[i];
   return MORAP_OK;
 }
 

@@ -60,6 +60,8 @@ def load_library(path: str = CUDA_SO) -> C.CDLL:
         "morap_cuda_fetch_eval_values": (i32, [p, i32, i32, p]),
         "morap_cuda_set_profiling": (i32, [p, i32]),
         "morap_cuda_set_lean": (i32, [p, i32]),
+        "morap_cuda_set_skip": (i32, [p, i32]),
+        "morap_cuda_debug_cta_trace": (i32, [p, i32, p, C.c_int64]),
         "morap_cuda_model_info": (i32, [p, i32, p]),
         "morap_cuda_stats": (i32, [p, p, i32]),
         "morap_cuda_reset_stats": (i32, [p]),
@@ -149,6 +151,10 @@ class CudaBackend:
         """Store compact-alphabet models without their fp64 prob/objective arrays (morap_cuda.h)."""
         self._check(self.lib.morap_cuda_set_lean(self.h, int(on)), "set_lean")
 
+    def set_skip(self, on: bool):
+        """Frozen-tile skipping in compact optimize sweeps (bitwise-neutral, morap_cuda.h)."""
+        self._check(self.lib.morap_cuda_set_skip(self.h, int(on)), "set_skip")
+
     def release_models(self):
         self._check(self.lib.morap_cuda_release_models(self.h), "release")
         self._models = []
@@ -230,10 +236,10 @@ class CudaBackend:
         self._check(self.lib.morap_cuda_set_profiling(self.h, int(on)), "set_profiling")
 
     def stats(self) -> dict:
-        out = np.zeros(10)
-        self._check(self.lib.morap_cuda_stats(self.h, _ptr(out), 10), "stats")
+        out = np.zeros(11)
+        self._check(self.lib.morap_cuda_stats(self.h, _ptr(out), 11), "stats")
         keys = ["opt_launches", "opt_ms", "opt_bytes", "opt_backups", "eval_launches", "eval_ms", "eval_bytes",
-                "eval_state_backups", "kernels", "upload_bytes"]
+                "eval_state_backups", "kernels", "upload_bytes", "opt_exec_backups"]
         return dict(zip(keys, out.tolist()))
 
     def reset_stats(self):

@@ -1,0 +1,53 @@
+"""Dev probe: per-CTA timeline of the compact optimize sweeps (morap_cuda_debug_cta_trace)
+for one C2 optimize batch (100 jobs, w = (0.5, 0.5)): per sweep, the span from the first
+CTA start to the finalize end, when the CTAs start / get their first stage / finish, and
+the finalize time. Args: mode (skip|full), sweep CTAs (148 x 4)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2305_04397_b200.api import Instance
+from paper_2305_04397_b200.cuda import CudaBackend
+
+import bench
+
+mode = sys.argv[1] if len(sys.argv) > 1 else "skip"
+inst = Instance.warehouse(bench.workload("c2")[0])
+prods = [inst.product(i, j) for i in range(10) for j in range(10)]
+be = CudaBackend(0)
+be.set_lean(True)
+ids = be.upload(prods)
+Wm = np.tile([0.5, 0.5], (len(ids), 1))
+be.set_skip(mode == "skip")
+be.optimize(ids, Wm)
+lib = be.lib
+assert lib.morap_cuda_debug_cta_trace(be.h, 1, None, 0) == 0
+val, sw, res, st = be.optimize(ids, Wm)
+n = 128 * 148 * 8 * 4
+buf = np.zeros(n, np.uint64)
+assert lib.morap_cuda_debug_cta_trace(be.h, 0, buf.ctypes.data_as(C.c_void_p), n) == 0
+blocks = int(sys.argv[2]) if len(sys.argv) > 2 else 148 * 4  # the compact sweep's grid
+T = buf[: 128 * blocks * 4].reshape(128, blocks, 4).astype(np.int64)
+rows = []
+for k in range(int(sw.max())):
+    t = T[k]
+    live = t[:, 0] > 0
+    if not live.any():
+        continue
+    t = t[live]
+    t0 = t[:, 0].min()
+    fin = t[:, 3].max() - t0
+    has = t[:, 1] > 0
+    first = (t[has, 1] - t[has, 0]) / 1e3 if has.any() else np.zeros(1)
+    end = (t[:, 2] - t0) / 1e3
+    rows.append((k + 1, fin / 1e3, (t[:, 0] - t0).max() / 1e3, np.median(first), np.median(end), end.max(),
+                 fin / 1e3 - end.max()))
+print(f"{mode}: CTAs {T.shape[1]}")
+print("sweep  span_us  start_spread  first_stage_med  work_end_med  work_end_max  finalize_us")
+for r in rows[:: max(1, len(rows) // 12)]:
+    print("%5d  %7.1f  %12.1f  %15.1f  %12.1f  %12.1f  %11.1f" % r)
+a = np.array(rows)[:, 1:]
+print("mean   %7.1f  %12.1f  %15.1f  %12.1f  %12.1f  %11.1f" % tuple(a.mean(0)))

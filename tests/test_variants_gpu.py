@@ -5,6 +5,7 @@ CUDA context is created (environment), so each variant runs in its own process:
   MORAP_COMPACT=0    fp64 streams, 2-stage TMA pipeline (k_greedy_sweep_tma)
   MORAP_SWEEP_KERNEL=global   plain global-memory sweep (k_greedy_sweep)
   MORAP_GRAPHS=0     sweeps launched one by one instead of CUDA-graph batches
+  MORAP_SKIP=0       every tile swept every sweep (no frozen-tile skipping)
 
 Each process runs optimize + fused evaluate on 6x6 warehouse products and random models
 and prints fingerprints; all variants must agree with each other and with the oracle."""
@@ -59,6 +60,7 @@ VARIANTS = {
     "global": {"MORAP_SWEEP_KERNEL": "global", "MORAP_COMPACT": "0"},
     "no_graphs": {"MORAP_GRAPHS": "0"},
     "no_persistent_eval": {"MORAP_PERSISTENT": "0"},
+    "no_skip": {"MORAP_SKIP": "0"},
 }
 
 
