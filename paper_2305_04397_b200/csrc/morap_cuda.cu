@@ -992,8 +992,12 @@ constexpr int kSelThreads = 256;
 constexpr int kTailPct = MORAP_TAIL_PCT;  // share of the selected tiles handed out dynamically
 constexpr int kClaim = MORAP_CLAIM;       // tiles per claim
 
-// cand[prefix[slot] + lt] = {job, lt, first stamp group (16-byte aligned; -1: never
-// skipped -- oversized or out-of-window tiles), last stamp group}; grid (tile blocks, slots)
+// cand[prefix[slot] + lt] = {job, lt | (n window loads << 20) | (n own loads << 25), first
+// stamp group of the successor window, first stamp group of the tile's own states}. Groups
+// are rounded down to multiples of 4 (16-byte loads of 4 stamps); the two ranges are kept
+// apart because a window can lie far from the tile's own states (centralised models).
+// Oversized and out-of-window tiles are never skipped: window group -1.
+constexpr int kCandLtBits = 20;  // tiles per model < 2^20 (skipping is off for larger models)
 __global__ void __launch_bounds__(kSelThreads) k_build_cand(const DevModel* __restrict__ models,
                                                             const OptJob* __restrict__ jobs,
                                                             const int32_t* __restrict__ list,
@@ -1007,13 +1011,15 @@ __global__ void __launch_bounds__(kSelThreads) k_build_cand(const DevModel* __re
   const DevModel& M = models[jobs[job].model];
   const int4* tp = reinterpret_cast<const int4*>(M.tiles + lt);
   const int4 d0 = tp[0], d1 = tp[1], e0 = tp[2];  // (s0 r0 k0 fits) (wlo wn allIn simple) (next s0 ...)
-  int g0 = -1, g1 = -1;
-  if (d0.w && d1.z) {
-    const int lo = min(d1.x, d0.x), hi = max(d1.x + d1.y, e0.x);
-    g0 = (lo >> 5) & ~3;
-    g1 = (hi - 1) >> 5;
+  int gw = -1, go = 0, packed = lt;
+  if (d0.w && d1.z && d1.y > 0) {
+    gw = (d1.x >> 5) & ~3;
+    const int nw = (((d1.x + d1.y - 1) >> 5) - gw) / 4 + 1;  // <= 9 for a 992-state window
+    go = (d0.x >> 5) & ~3;
+    const int no = (((e0.x - 1) >> 5) - go) / 4 + 1;         // <= 3 for 256 states
+    packed = lt | (nw << kCandLtBits) | (no << (kCandLtBits + 5));
   }
-  cand[base + lt] = make_int4(job, lt, g0, g1);
+  cand[base + lt] = make_int4(job, packed, gw, go);
 }
 
 __global__ void __launch_bounds__(kSelThreads) k_select(const OptJob* __restrict__ jobs,
@@ -1036,15 +1042,21 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const OptJob* __restrict
       if (__ldcg(alive + c.x) == k) {  // job still active
         keep = 1;
         if (k > 0 && c.z >= 0) {
-          const int32_t* stamp = jobs[c.x].stamp;
+          const int4* stamp = reinterpret_cast<const int4*>(jobs[c.x].stamp);
+          const int nw = (c.y >> kCandLtBits) & 31, no = (c.y >> (kCandLtBits + 5)) & 31;
           int m = 0;
-          for (int g = c.z; g <= c.w; g += 4) {  // 16-byte aligned groups of 4 stamps
-            const int4 q = __ldcg(reinterpret_cast<const int4*>(stamp + g));
-            m = max(m, max(max(q.x, q.y), max(q.z, q.w)));
+          for (int q = 0; q < nw; ++q) {  // successor window
+            const int4 v = __ldcg(stamp + (c.z >> 2) + q);
+            m = max(m, max(max(v.x, v.y), max(v.z, v.w)));
+          }
+          for (int q = 0; q < no; ++q) {  // own states
+            const int4 v = __ldcg(stamp + (c.w >> 2) + q);
+            m = max(m, max(max(v.x, v.y), max(v.z, v.w)));
           }
           keep = m >= k;  // something it depends on changed in the previous sweep
         }
       }
+      c.y &= (1 << kCandLtBits) - 1;
     }
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) sCnt[wid] = __popc(bal);
@@ -3004,6 +3016,8 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   CK(cudaMemsetAsync(base + rhoBytes, 0, xBytes, ctx->stream));
   ctx->optCompact = allCompact;
   ctx->optSkip = allCompact && ctx->skip;
+  for (int j = 0; j < njobs && ctx->optSkip; ++j)
+    if (ctx->hm[model_ids[j]].ntiles >= (1 << kCandLtBits)) ctx->optSkip = false;  // k_build_cand packing
   if (ctx->optSkip) {
     size_t tiles = 0;
     for (int j : active) tiles += static_cast<size_t>(ctx->hm[model_ids[j]].ntiles);

@@ -1,7 +1,7 @@
 """Dev probe: per-CTA timeline of the compact optimize sweeps (morap_cuda_debug_cta_trace)
 for one C2 optimize batch (100 jobs, w = (0.5, 0.5)): per sweep, the span from the first
 CTA start to the finalize end, when the CTAs start / get their first stage / finish, and
-the finalize time. Args: mode (skip|full), sweep CTAs (148 x 4)."""
+the finalize time. Args: mode (skip|full), sweep CTAs (148 x 4), workload (c2|cent)."""
 import ctypes as C
 import os
 import sys
@@ -15,12 +15,24 @@ from paper_2305_04397_b200.cuda import CudaBackend
 import bench
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "skip"
-inst = Instance.warehouse(bench.workload("c2")[0])
-prods = [inst.product(i, j) for i in range(10) for j in range(10)]
+work = sys.argv[3] if len(sys.argv) > 3 else "c2"
 be = CudaBackend(0)
 be.set_lean(True)
+if work == "cent":  # the centralised model of bench's `cent` workload, one job
+    from types import SimpleNamespace
+    from paper_2305_04397_b200.api import Centralised
+    cm = Centralised(Instance.warehouse(bench.workload("cent")[0]))
+    a = cm.arrays()
+    prods = [SimpleNamespace(rowOffset=a["rowOffset"], trnOffset=a["trnOffset"], succ=a["succ"], prob=a["prob"],
+                             done=a["done"], initial=cm.initial, rewardFinite=cm.reward_finite,
+                             objectives=list(a["rewards"]))]
+    K = cm.objectives
+else:
+    inst = Instance.warehouse(bench.workload("c2")[0])
+    prods = [inst.product(i, j) for i in range(10) for j in range(10)]
+    K = 2
 ids = be.upload(prods)
-Wm = np.tile([0.5, 0.5], (len(ids), 1))
+Wm = np.tile(np.full(K, 1.0 / K), (len(ids), 1))
 be.set_skip(mode == "skip")
 be.optimize(ids, Wm)
 lib = be.lib
@@ -32,8 +44,9 @@ assert lib.morap_cuda_debug_cta_trace(be.h, 0, buf.ctypes.data_as(C.c_void_p), n
 blocks = int(sys.argv[2]) if len(sys.argv) > 2 else 148 * 4  # the compact sweep's grid
 T = buf[: 128 * blocks * 4].reshape(128, blocks, 4).astype(np.int64)
 rows = []
-for k in range(int(sw.max())):
-    t = T[k]
+nsw = int(sw.max())
+for k in range(max(0, nsw - 128), nsw):  # the slots keep the last 128 sweeps
+    t = T[k % 128]
     live = t[:, 0] > 0
     if not live.any():
         continue
