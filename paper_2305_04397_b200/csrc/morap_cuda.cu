@@ -100,6 +100,10 @@ struct DevModel {
   const uint32_t* rowW;  // per row: tile-relative transition end | reward class << 16
   const uint32_t* trW;   // per transition: window offset (0xFFFF outside) | probability index << 16
   const TilePos* tilePos;     // ntiles
+  // frozen-tile skipping: stamp groups (32 states) of the successors outside each tile's
+  // window, outGrp[outIdx[t] .. outIdx[t + 1]) (sorted, distinct; a single -1: too many)
+  const int32_t* outIdx;      // ntiles + 1
+  const int32_t* outGrp;
   int32_t S, R, nnz, initial, ntiles, K, rewardFinite, compact;
   int32_t nclass, pad2;
   unsigned long long bytesPerSweep;  // algorithmic bytes of one greedy sweep
@@ -115,6 +119,7 @@ struct OptJob {
   double* buf[2];
   int32_t* policy;
   int32_t* stamp;  // frozen-tile skipping: last sweep in which a state of group g (32 states) changed
+  const int32_t* outGrp;  // the model's out-of-window stamp groups (DevModel::outGrp)
 };
 
 struct EvalJob {
@@ -992,17 +997,21 @@ constexpr int kSelThreads = 256;
 constexpr int kTailPct = MORAP_TAIL_PCT;  // share of the selected tiles handed out dynamically
 constexpr int kClaim = MORAP_CLAIM;       // tiles per claim
 
-// cand[prefix[slot] + lt] = {job, lt | (n window loads << 20) | (n own loads << 25), first
-// stamp group of the successor window, first stamp group of the tile's own states}. Groups
-// are rounded down to multiples of 4 (16-byte loads of 4 stamps); the two ranges are kept
-// apart because a window can lie far from the tile's own states (centralised models).
-// Oversized and out-of-window tiles are never skipped: window group -1.
+// cand[prefix[slot] + lt] = {job, lt | (n window loads << 20) | (n own loads << 24) | (n out
+// groups << 27), first stamp group of the successor window, first stamp group of the tile's
+// own states}; candOut[...] = offset of its out-of-window groups in the model's outGrp.
+// Window / own groups are rounded down to multiples of 4 (16-byte loads of 4 stamps); the
+// two ranges are kept apart because a window can lie far from the tile's own states
+// (centralised models). Oversized tiles and tiles with more than kMaxOutGroups
+// out-of-window groups are never skipped: window group -1.
 constexpr int kCandLtBits = 20;  // tiles per model < 2^20 (skipping is off for larger models)
+constexpr int kMaxOutGroups = 16;  // out-of-window stamp groups a skippable tile may depend on
 __global__ void __launch_bounds__(kSelThreads) k_build_cand(const DevModel* __restrict__ models,
                                                             const OptJob* __restrict__ jobs,
                                                             const int32_t* __restrict__ list,
                                                             const int32_t* __restrict__ prefix,
-                                                            int4* __restrict__ cand, int slotBase) {
+                                                            int4* __restrict__ cand, int32_t* __restrict__ candOut,
+                                                            int slotBase) {
   const int slot = slotBase + blockIdx.y;
   const int job = list[slot];
   const int base = prefix[slot], nt = prefix[slot + 1] - base;
@@ -1011,20 +1020,27 @@ __global__ void __launch_bounds__(kSelThreads) k_build_cand(const DevModel* __re
   const DevModel& M = models[jobs[job].model];
   const int4* tp = reinterpret_cast<const int4*>(M.tiles + lt);
   const int4 d0 = tp[0], d1 = tp[1], e0 = tp[2];  // (s0 r0 k0 fits) (wlo wn allIn simple) (next s0 ...)
-  int gw = -1, go = 0, packed = lt;
-  if (d0.w && d1.z && d1.y > 0) {
-    gw = (d1.x >> 5) & ~3;
-    const int nw = (((d1.x + d1.y - 1) >> 5) - gw) / 4 + 1;  // <= 9 for a 992-state window
+  int gw = -1, go = 0, oOff = 0;
+  unsigned packed = static_cast<unsigned>(lt);
+  const int ob = M.outIdx[lt], on = M.outIdx[lt + 1] - ob;
+  const bool outOk = on <= kMaxOutGroups && (on == 0 || M.outGrp[ob] >= 0);
+  if (d0.w && outOk) {
+    gw = d1.y > 0 ? (d1.x >> 5) & ~3 : 0;  // no successors at all: own states only
+    const int nw = d1.y > 0 ? (((d1.x + d1.y - 1) >> 5) - gw) / 4 + 1 : 0;  // <= 9 for a 992-state window
     go = (d0.x >> 5) & ~3;
     const int no = (((e0.x - 1) >> 5) - go) / 4 + 1;         // <= 3 for 256 states
-    packed = lt | (nw << kCandLtBits) | (no << (kCandLtBits + 5));
+    packed |= (static_cast<unsigned>(nw) << kCandLtBits) | (static_cast<unsigned>(no) << (kCandLtBits + 4)) |
+              (static_cast<unsigned>(on) << (kCandLtBits + 7));
+    oOff = ob;
   }
-  cand[base + lt] = make_int4(job, packed, gw, go);
+  cand[base + lt] = make_int4(job, static_cast<int>(packed), gw, go);
+  candOut[base + lt] = oOff;
 }
 
 __global__ void __launch_bounds__(kSelThreads) k_select(const OptJob* __restrict__ jobs,
                                                         const int32_t* __restrict__ alive,
-                                                        const int4* __restrict__ cand, int ncand, Ctl* ctl,
+                                                        const int4* __restrict__ cand,
+                                                        const int32_t* __restrict__ candOut, int ncand, Ctl* ctl,
                                                         int2* __restrict__ sel) {
   __shared__ int sCnt[kSelThreads / 32];
   __shared__ int sBase;
@@ -1042,9 +1058,15 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const OptJob* __restrict
       if (__ldcg(alive + c.x) == k) {  // job still active
         keep = 1;
         if (k > 0 && c.z >= 0) {
-          const int4* stamp = reinterpret_cast<const int4*>(jobs[c.x].stamp);
-          const int nw = (c.y >> kCandLtBits) & 31, no = (c.y >> (kCandLtBits + 5)) & 31;
+          const OptJob& J = jobs[c.x];
+          const int4* stamp = reinterpret_cast<const int4*>(J.stamp);
+          const unsigned u = static_cast<unsigned>(c.y);
+          const int nw = (u >> kCandLtBits) & 15, no = (u >> (kCandLtBits + 4)) & 7, nout = u >> (kCandLtBits + 7);
           int m = 0;
+          if (nout) {  // successors outside the window: their groups one by one
+            const int32_t* og = J.outGrp + __ldg(candOut + t);
+            for (int q = 0; q < nout; ++q) m = max(m, __ldcg(J.stamp + __ldg(og + q)));
+          }
           for (int q = 0; q < nw; ++q) {  // successor window
             const int4 v = __ldcg(stamp + (c.z >> 2) + q);
             m = max(m, max(max(v.x, v.y), max(v.z, v.w)));
@@ -2362,7 +2384,7 @@ struct morap_ctx {
   void* stage = nullptr;  // pinned host staging for uploads
   size_t stageBytes = 0;
   std::vector<cudaEvent_t> evPool;  // per-sweep start/stop events (profiling, no graphs)
-  static constexpr int kKeyPtrs = 16;
+  static constexpr int kKeyPtrs = 17;
   struct GraphKey {
     int kind, B, cap, variant, ncand;
     double eps;
@@ -2394,6 +2416,7 @@ struct morap_ctx {
   int selBlocks = 0;
   int2* dSel = nullptr;    // (job, tile) pairs of the current sweep
   int4* dCand = nullptr;   // candidates of the current optimize batch (k_build_cand)
+  int32_t* dCandOut = nullptr;
   int nCand = 0;
   void* dTrace = nullptr;  // diagnostics: per-CTA sweep timeline (morap_cuda_debug_cta_trace)
   size_t selCap = 0;
@@ -2533,6 +2556,7 @@ struct CompactStream {
   std::vector<double> dict, table;
   std::vector<uint32_t> stW, rowW, trW;        // packed state / row / transition words, padded per tile
   std::vector<TilePos> pos;
+  std::vector<int32_t> outIdx, outGrp;        // out-of-window stamp groups per tile (DevModel)
 };
 
 // The sweep streams of a compact model, tile-major: each tile's slice of every stream
@@ -2559,6 +2583,8 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
   c.stW.assign(nRow, 0);
   c.rowW.assign(nTrn, 0);
   c.trW.assign(nSucc, 0xFFFFu);
+  c.outIdx.assign(nt + 1, 0);
+  c.outGrp.clear();
   for (size_t t = 0; t < nt; ++t) {
     TileDesc& d = desc[t];
     const TileDesc& e = desc[t + 1];
@@ -2567,6 +2593,8 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
     d.simple = simple;
     if (!d.fits) {
       d.allIn = 0;
+      c.outGrp.push_back(-1);  // swept from the global arrays: never skipped
+      c.outIdx[t + 1] = static_cast<int32_t>(c.outGrp.size());
       continue;
     }
     const TilePos& p = c.pos[t];
@@ -2585,6 +2613,18 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
       allIn &= in ? 1 : 0;
     }
     d.allIn = allIn;
+    if (!allIn) {  // stamp groups of the out-of-window successors (sorted, distinct, <= kMaxOutGroups)
+      const size_t at = c.outGrp.size();
+      for (int k = d.k0; k < e.k0; ++k)
+        if (static_cast<unsigned>(v.succ[k] - d.wlo) >= static_cast<unsigned>(d.wn)) c.outGrp.push_back(v.succ[k] >> 5);
+      std::sort(c.outGrp.begin() + at, c.outGrp.end());
+      c.outGrp.erase(std::unique(c.outGrp.begin() + at, c.outGrp.end()), c.outGrp.end());
+      if (c.outGrp.size() - at > static_cast<size_t>(kMaxOutGroups)) {
+        c.outGrp.resize(at);
+        c.outGrp.push_back(-1);
+      }
+    }
+    c.outIdx[t + 1] = static_cast<int32_t>(c.outGrp.size());
   }
 }
 
@@ -2792,7 +2832,7 @@ int enqueue_sweeps(morap_ctx* ctx, int kind, double eps, int cap, int B, const c
                         ctx->optSkip ? ctx->dAlive : nullptr};
       if (ctx->optSkip) {
         k_select<<<ctx->selBlocks, kSelThreads, 0, ctx->stream>>>(ctx->dOptJobs, ctx->dAlive, ctx->dCand,
-                                                                  ctx->nCand, ctx->dCtl, ctx->dSel);
+                                                                  ctx->dCandOut, ctx->nCand, ctx->dCtl, ctx->dSel);
         CK(cudaGetLastError());
       }
       if (ev && !selTimed) CK(cudaEventRecordWithFlags(ev[2 * i], ctx->stream, evFlags));
@@ -2844,7 +2884,7 @@ int batch_graph(morap_ctx* ctx, int kind, double eps, int cap, int B, bool timed
   key.ncand = kind == 0 && ctx->optSkip ? ctx->nCand : 0;
   const void* ptrs[] = {ctx->dModels, ctx->dOptJobs, ctx->dList,  ctx->dPrefix,    ctx->dCtl,      ctx->dDelta,
                         ctx->dMask,   ctx->dNrhs,    ctx->dSweeps, ctx->dResidual, ctx->dStatus,   ctx->dJobModel,
-                        ctx->dEvalJobsRaw, ctx->stream, ctx->dSel, ctx->dCand};
+                        ctx->dEvalJobsRaw, ctx->stream, ctx->dSel, ctx->dCand, ctx->dCandOut};
   static_assert(sizeof(ptrs) / sizeof(ptrs[0]) == morap_ctx::kKeyPtrs, "graph key size");
   for (int i = 0; i < morap_ctx::kKeyPtrs; ++i) key.ptrs[i] = ptrs[i];
   for (auto& g : ctx->graphs)
@@ -3005,6 +3045,7 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     J.buf[1] = reinterpret_cast<double*>(base + rhoBytes + offX[j] + align_up(sizeof(double) * m.S, 256));
     J.policy = reinterpret_cast<int32_t*>(base + rhoBytes + xBytes + offPol[j]);
     J.stamp = reinterpret_cast<int32_t*>(base + rhoBytes + offX[j] + 2 * align_up(sizeof(double) * m.S, 256));
+    J.outGrp = ctx->dm[model_ids[j]].outGrp;
     J.classRho = (!rhoHost && ctx->dm[model_ids[j]].compact)
                      ? reinterpret_cast<double*>(base + rhoBytes + xBytes + polBytes + 256ull * sizeof(double) * j)
                      : nullptr;
@@ -3025,11 +3066,14 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
       CK(cudaStreamSynchronize(ctx->stream));
       cudaFree(ctx->dSel);
       cudaFree(ctx->dCand);
+      cudaFree(ctx->dCandOut);
       ctx->dSel = nullptr;
       ctx->dCand = nullptr;
+      ctx->dCandOut = nullptr;
       ctx->selCap = std::max(tiles, ctx->selCap + ctx->selCap / 2);
       CK(cudaMalloc(&ctx->dSel, ctx->selCap * sizeof(int2)));
       CK(cudaMalloc(&ctx->dCand, ctx->selCap * sizeof(int4)));
+      CK(cudaMalloc(&ctx->dCandOut, ctx->selCap * sizeof(int32_t)));
     }
     ctx->nCand = static_cast<int>(tiles);
   }
@@ -3055,7 +3099,7 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     for (size_t s0 = 0; s0 < active.size(); s0 += 65535) {  // gridDim.y limit
       const dim3 grid((maxTiles + kSelThreads - 1) / kSelThreads, static_cast<unsigned>(std::min<size_t>(65535, active.size() - s0)));
       k_build_cand<<<grid, kSelThreads, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix,
-                                                          ctx->dCand, static_cast<int>(s0));
+                                                          ctx->dCand, ctx->dCandOut, static_cast<int>(s0));
       CK(cudaGetLastError());
       ctx->stats[8] += 1;
     }
@@ -3476,6 +3520,7 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   }
   cudaFree(ctx->dSel);
   cudaFree(ctx->dCand);
+  cudaFree(ctx->dCandOut);
   cudaFree(ctx->dTrace);
   cudaFree(ctx->dCtl);
   cudaFreeHost(ctx->hCtl);
@@ -3560,7 +3605,8 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     if (compact[m].ok)
       bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(v.num_rows, 256) +
                align_up(8ull * compact[m].table.size(), 256) + align_up(4ull * compact[m].trW.size(), 256) +
-               align_up(4ull * compact[m].stW.size(), 256) + align_up(4ull * compact[m].rowW.size(), 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256);
+               align_up(4ull * compact[m].stW.size(), 256) + align_up(4ull * compact[m].rowW.size(), 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256) +
+               align_up(4ull * compact[m].outIdx.size(), 256) + align_up(4ull * compact[m].outGrp.size(), 256);
   }
   void* dev = nullptr;
   {
@@ -3643,6 +3689,8 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
       dmod.rowW = reinterpret_cast<const uint32_t*>(put(c.rowW.data(), 4ull * c.rowW.size()));
       dmod.trW = reinterpret_cast<const uint32_t*>(put(c.trW.data(), 4ull * c.trW.size()));
       dmod.tilePos = reinterpret_cast<const TilePos*>(put(c.pos.data(), sizeof(TilePos) * c.pos.size()));
+      dmod.outIdx = reinterpret_cast<const int32_t*>(put(c.outIdx.data(), 4ull * c.outIdx.size()));
+      dmod.outGrp = reinterpret_cast<const int32_t*>(put(c.outGrp.data(), 4ull * c.outGrp.size()));
       // compact stream: one 4-byte word per transition (window offset | index) and per row
       // (transition end | class) and per state (row end | transition end | done) + x 8 + y 8
       dmod.bytesPerSweep = 4ull * v.nnz + 4ull * v.num_rows + 20ull * v.num_states;
