@@ -112,7 +112,7 @@ struct DevModel {
 
 struct OptJob {
   int32_t model;
-  int32_t pad;
+  int32_t stampOff;  // first stamp of this job in the batch's stamp array (multiple of 4)
   double w[MORAP_MAX_OBJECTIVES];
   double* rho;
   double* classRho;  // compact models: rho_w of each reward class (<= 256)
@@ -120,6 +120,9 @@ struct OptJob {
   int32_t* policy;
   int32_t* stamp;  // frozen-tile skipping: last sweep in which a state of group g (32 states) changed
   const int32_t* outGrp;  // the model's out-of-window stamp groups (DevModel::outGrp)
+  unsigned long long bytesPerSweep;  // the model's (stats)
+  int32_t nnz;
+  int32_t outBase;  // this job's slice of the batch's absolute out-group list (k_build_cand)
 };
 
 struct EvalJob {
@@ -143,7 +146,7 @@ struct Ctl {
   int32_t sweepsDone;   // sweeps completed by every active job
   int32_t nsel;         // tiles selected for the current sweep (k_select); reset by the finalize
   int32_t claimed;      // dynamic tail of the selected tiles: claimed so far; reset by the finalize
-  int32_t pad;
+  int32_t nactNext;     // k_select mode: jobs k_select let into the coming sweep
   unsigned long long bytes;    // algorithmic bytes of all sweeps so far
   unsigned long long backups;  // nnz backups of all sweeps so far (every tile of every active job)
   unsigned long long execBytes;    // of the tiles actually swept (k_select mode)
@@ -862,7 +865,6 @@ struct FinArgs {
   int32_t* sweeps;
   double* residual;
   int32_t* status;
-  int32_t* alive;  // per job: sweeps done while still active, -1 once it left the list (k_select)
 };
 
 // exclusive scan of (a, b) over the whole block (any multiple of 32 threads <= 1024)
@@ -908,7 +910,7 @@ __device__ __forceinline__ void block_scan2n(int& a, int& b, int* sa, int* sb, i
 // active list / tile prefix, by one block (k_finalize's body for the optimize kind).
 __device__ void finalize_opt(const DevModel* __restrict__ models, const int32_t* __restrict__ jobModel,
                              int32_t* list, int32_t* prefix, Ctl* ctl, unsigned long long* deltaBits, double eps,
-                             int cap, int32_t* sweeps, double* residual, int32_t* status, int32_t* alive) {
+                             int cap, int32_t* sweeps, double* residual, int32_t* status) {
   __shared__ int sa[32], sb[32];
   __shared__ unsigned long long sBytes[32], sBk[32];
   const int nact = __ldcg(&ctl->nactive);
@@ -932,7 +934,6 @@ __device__ void finalize_opt(const DevModel* __restrict__ models, const int32_t*
       else if (k >= cap) status[job] = MORAP_NON_CONVERGENCE;
       else keep = 1;
       if (keep) nt = M.ntiles;
-      if (alive) alive[job] = keep ? k : -1;
     }
     int pa = keep, pb = nt, ta, tb;
     block_scan2n(pa, pb, sa, sb, ta, tb);
@@ -998,8 +999,9 @@ constexpr int kTailPct = MORAP_TAIL_PCT;  // share of the selected tiles handed 
 constexpr int kClaim = MORAP_CLAIM;       // tiles per claim
 
 // cand[prefix[slot] + lt] = {job, lt | (n window loads << 20) | (n own loads << 24) | (n out
-// groups << 27), first stamp group of the successor window, first stamp group of the tile's
-// own states}; candOut[...] = offset of its out-of-window groups in the model's outGrp.
+// groups << 27), first stamp of the successor window, first stamp of the tile's own states}
+// as absolute indices into the batch's stamp array; candOut[...] = offset of the tile's
+// out-of-window stamps (absolute) in candOutG.
 // Window / own groups are rounded down to multiples of 4 (16-byte loads of 4 stamps); the
 // two ranges are kept apart because a window can lie far from the tile's own states
 // (centralised models). Oversized tiles and tiles with more than kMaxOutGroups
@@ -1011,13 +1013,14 @@ __global__ void __launch_bounds__(kSelThreads) k_build_cand(const DevModel* __re
                                                             const int32_t* __restrict__ list,
                                                             const int32_t* __restrict__ prefix,
                                                             int4* __restrict__ cand, int32_t* __restrict__ candOut,
-                                                            int slotBase) {
+                                                            int32_t* __restrict__ candOutG, int slotBase) {
   const int slot = slotBase + blockIdx.y;
   const int job = list[slot];
   const int base = prefix[slot], nt = prefix[slot + 1] - base;
   const int lt = blockIdx.x * kSelThreads + threadIdx.x;
   if (lt >= nt) return;
-  const DevModel& M = models[jobs[job].model];
+  const OptJob& J = jobs[job];
+  const DevModel& M = models[J.model];
   const int4* tp = reinterpret_cast<const int4*>(M.tiles + lt);
   const int4 d0 = tp[0], d1 = tp[1], e0 = tp[2];  // (s0 r0 k0 fits) (wlo wn allIn simple) (next s0 ...)
   int gw = -1, go = 0, oOff = 0;
@@ -1031,42 +1034,78 @@ __global__ void __launch_bounds__(kSelThreads) k_build_cand(const DevModel* __re
     const int no = (((e0.x - 1) >> 5) - go) / 4 + 1;         // <= 3 for 256 states
     packed |= (static_cast<unsigned>(nw) << kCandLtBits) | (static_cast<unsigned>(no) << (kCandLtBits + 4)) |
               (static_cast<unsigned>(on) << (kCandLtBits + 7));
-    oOff = ob;
+    gw += J.stampOff;  // absolute stamp indices (multiples of 4)
+    go += J.stampOff;
+    oOff = J.outBase + ob;
+    for (int q = 0; q < on; ++q) candOutG[oOff + q] = J.stampOff + M.outGrp[ob + q];
   }
   cand[base + lt] = make_int4(job, static_cast<int>(packed), gw, go);
   candOut[base + lt] = oOff;
 }
 
-__global__ void __launch_bounds__(kSelThreads) k_select(const OptJob* __restrict__ jobs,
-                                                        const int32_t* __restrict__ alive,
+// k_select also carries the stop test of the sweep just completed (numerics.hpp:105-112),
+// distributed: every candidate thread decides for its own job from that job's residual
+// (the same inputs give the same decision in every thread), and the thread of the job's
+// first tile records it (sweeps, residual, status, act = 0 once stopped), clears the
+// job's residual slot for the coming sweep and counts the job in. Residual slots alternate
+// by sweep parity: deltaBits[2 * job + (sweep & 1)]. The sweep kernel then only bumps the
+// sweep count (last-CTA ticket) -- no serial finalize between sweeps.
+__global__ void __launch_bounds__(kSelThreads) k_select(const DevModel* __restrict__ models,
+                                                        const OptJob* __restrict__ jobs, int32_t* act,
                                                         const int4* __restrict__ cand,
-                                                        const int32_t* __restrict__ candOut, int ncand, Ctl* ctl,
-                                                        int2* __restrict__ sel) {
+                                                        const int32_t* __restrict__ candOut,
+                                                        const int32_t* __restrict__ candOutG,
+                                                        const int32_t* __restrict__ stampAll, int ncand, Ctl* ctl,
+                                                        int2* __restrict__ sel, unsigned long long* deltaBits,
+                                                        double eps, int cap, int32_t* sweeps, double* residual,
+                                                        int32_t* status) {
   __shared__ int sCnt[kSelThreads / 32];
   __shared__ int sBase;
+  __shared__ unsigned long long sB[kSelThreads / 32], sK[kSelThreads / 32];
   const int k = ctl->sweepsDone;
   if (ctl->nactive == 0) return;
   const int per = ((ncand + gridDim.x - 1) / gridDim.x + kSelThreads - 1) / kSelThreads * kSelThreads;
   const int t0 = blockIdx.x * per, t1 = min(ncand, t0 + per);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long ranBytes = 0, ranNnz = 0;  // jobs that ran sweep k (reference-layout stats)
   for (int base = t0; base < t1; base += kSelThreads) {
     const int t = base + threadIdx.x;
     int keep = 0;
     int4 c = make_int4(0, 0, 0, 0);
     if (t < t1) {
       c = __ldg(cand + t);
-      if (__ldcg(alive + c.x) == k) {  // job still active
+      const int oo = __ldg(candOut + t);
+      const int job = c.x;
+      const bool first = (c.y & ((1 << kCandLtBits) - 1)) == 0;
+      bool run = __ldcg(act + job) != 0;
+      if (run && k > 0) {  // stop test of sweep k
+        const double d = __longlong_as_double(static_cast<long long>(__ldcg(deltaBits + 2 * job + (k & 1))));
+        const bool stop = d <= eps || k >= cap;
+        if (first) {
+          sweeps[job] = k;
+          residual[job] = d;
+          if (stop) {
+            status[job] = d <= eps ? MORAP_OK : MORAP_NON_CONVERGENCE;
+            act[job] = 0;
+          }
+          ranBytes += jobs[job].bytesPerSweep;
+          ranNnz += static_cast<unsigned long long>(jobs[job].nnz);
+        }
+        run = !stop;
+      }
+      if (run && first) {
+        deltaBits[2 * job + ((k + 1) & 1)] = 0ull;
+        atomicAdd(&ctl->nactNext, 1);
+      }
+      if (run) {
         keep = 1;
         if (k > 0 && c.z >= 0) {
-          const OptJob& J = jobs[c.x];
-          const int4* stamp = reinterpret_cast<const int4*>(J.stamp);
+          const int4* stamp = reinterpret_cast<const int4*>(stampAll);
           const unsigned u = static_cast<unsigned>(c.y);
           const int nw = (u >> kCandLtBits) & 15, no = (u >> (kCandLtBits + 4)) & 7, nout = u >> (kCandLtBits + 7);
           int m = 0;
-          if (nout) {  // successors outside the window: their groups one by one
-            const int32_t* og = J.outGrp + __ldg(candOut + t);
-            for (int q = 0; q < nout; ++q) m = max(m, __ldcg(J.stamp + __ldg(og + q)));
-          }
+          for (int q = 0; q < nout; ++q)  // successors outside the window: their groups one by one
+            m = max(m, __ldcg(stampAll + __ldg(candOutG + oo + q)));
           for (int q = 0; q < nw; ++q) {  // successor window
             const int4 v = __ldcg(stamp + (c.z >> 2) + q);
             m = max(m, max(max(v.x, v.y), max(v.z, v.w)));
@@ -1095,6 +1134,25 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const OptJob* __restrict
     __syncthreads();
     if (keep) sel[sBase + sCnt[wid] + __popc(bal & ((1u << lane) - 1u))] = make_int2(c.x, c.y);
     __syncthreads();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ranBytes += __shfl_xor_sync(0xffffffffu, ranBytes, o);
+    ranNnz += __shfl_xor_sync(0xffffffffu, ranNnz, o);
+  }
+  if (lane == 0) {
+    sB[wid] = ranBytes;
+    sK[wid] = ranNnz;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tb = 0, tk = 0;
+    for (int w = 0; w < kSelThreads / 32; ++w) {
+      tb += sB[w];
+      tk += sK[w];
+    }
+    if (tb) atomicAdd(&ctl->bytes, tb);
+    if (tk) atomicAdd(&ctl->backups, tk);
   }
 }
 
@@ -1327,7 +1385,9 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     if (!POLICY && v.job != runJob) {  // uniform over the consumers
       if (runJob >= 0) {
         runMax = consumer_max(runMax, sRed);
-        if (tid == 0 && runMax > 0.0) atomicMax(deltaBits + runJob, (unsigned long long)__double_as_longlong(runMax));
+        if (tid == 0 && runMax > 0.0)
+          atomicMax(deltaBits + (sel ? 2 * runJob + ((k + 1) & 1) : runJob),
+                    (unsigned long long)__double_as_longlong(runMax));
       }
       runMax = 0.0;
       runJob = v.job;
@@ -1474,7 +1534,9 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
   }
   if (!POLICY && runJob >= 0) {  // residual of the last job of this CTA's range
     runMax = consumer_max(runMax, sRed);
-    if (tid == 0 && runMax > 0.0) atomicMax(deltaBits + runJob, (unsigned long long)__double_as_longlong(runMax));
+    if (tid == 0 && runMax > 0.0)
+      atomicMax(deltaBits + (sel ? 2 * runJob + ((k + 1) & 1) : runJob),
+                (unsigned long long)__double_as_longlong(runMax));
   }
   }  // compute warps
   }  // CTA has tiles
@@ -1491,9 +1553,20 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     __syncthreads();
     if (sLast) {
       __threadfence();
-      finalize_opt(models, fin.jobModel, const_cast<int32_t*>(list), const_cast<int32_t*>(prefix),
-                   const_cast<Ctl*>(ctl), deltaBits, fin.eps, fin.cap, fin.sweeps, fin.residual, fin.status,
-                   fin.alive);
+      if (sel) {  // k_select mode: the stop test runs in the next k_select; count the sweep
+        if (tid == 0) {
+          Ctl* c = const_cast<Ctl*>(ctl);
+          const int ran = c->nactNext;
+          if (ran > 0) c->sweepsDone = k + 1;
+          c->nactive = ran;
+          c->nactNext = 0;
+          c->nsel = 0;
+          c->claimed = 0;
+        }
+      } else {
+        finalize_opt(models, fin.jobModel, const_cast<int32_t*>(list), const_cast<int32_t*>(prefix),
+                     const_cast<Ctl*>(ctl), deltaBits, fin.eps, fin.cap, fin.sweeps, fin.residual, fin.status);
+      }
       if (tid == 0) {
         *fin.count = 0u;
         if (trace) trace[3] = global_ns();
@@ -2308,6 +2381,7 @@ __global__ void k_gather_eval(const DevModel* __restrict__ models, const EvalJob
 struct HostModel {
   int32_t S, R, nnz, initial, ntiles, K, rewardFinite;
   int32_t maxRowNnz;  // transitions of the widest row
+  int32_t nOutGrp;    // entries of the model's out-of-window group lists (frozen-tile skipping)
 };
 
 template <class T>
@@ -2384,7 +2458,7 @@ struct morap_ctx {
   void* stage = nullptr;  // pinned host staging for uploads
   size_t stageBytes = 0;
   std::vector<cudaEvent_t> evPool;  // per-sweep start/stop events (profiling, no graphs)
-  static constexpr int kKeyPtrs = 17;
+  static constexpr int kKeyPtrs = 19;
   struct GraphKey {
     int kind, B, cap, variant, ncand;
     double eps;
@@ -2416,7 +2490,10 @@ struct morap_ctx {
   int selBlocks = 0;
   int2* dSel = nullptr;    // (job, tile) pairs of the current sweep
   int4* dCand = nullptr;   // candidates of the current optimize batch (k_build_cand)
-  int32_t* dCandOut = nullptr;
+  int32_t* dCandOut = nullptr;  // per candidate: offset of its absolute out-group stamps in dCandOutG
+  int32_t* dCandOutG = nullptr;
+  size_t candOutGCap = 0;
+  int32_t* dStampAll = nullptr;  // stamps of the current optimize batch (inside optArena)
   int nCand = 0;
   void* dTrace = nullptr;  // diagnostics: per-CTA sweep timeline (morap_cuda_debug_cta_trace)
   size_t selCap = 0;
@@ -2828,11 +2905,11 @@ int enqueue_sweeps(morap_ctx* ctx, int kind, double eps, int cap, int B, const c
     const bool selTimed = !(kind == 0 && ctx->useTma && ctx->optCompact && ctx->optSkip && ctx->timeSweepOnly);
     if (ev && selTimed) CK(cudaEventRecordWithFlags(ev[2 * i], ctx->stream, evFlags));
     if (kind == 0 && ctx->useTma && ctx->optCompact) {
-      const FinArgs fin{ctx->dFinCount, ctx->dJobModel, eps, cap, ctx->dSweeps, ctx->dResidual, ctx->dStatus,
-                        ctx->optSkip ? ctx->dAlive : nullptr};
+      const FinArgs fin{ctx->dFinCount, ctx->dJobModel, eps, cap, ctx->dSweeps, ctx->dResidual, ctx->dStatus};
       if (ctx->optSkip) {
-        k_select<<<ctx->selBlocks, kSelThreads, 0, ctx->stream>>>(ctx->dOptJobs, ctx->dAlive, ctx->dCand,
-                                                                  ctx->dCandOut, ctx->nCand, ctx->dCtl, ctx->dSel);
+        k_select<<<ctx->selBlocks, kSelThreads, 0, ctx->stream>>>(
+            ctx->dModels, ctx->dOptJobs, ctx->dAlive, ctx->dCand, ctx->dCandOut, ctx->dCandOutG, ctx->dStampAll,
+            ctx->nCand, ctx->dCtl, ctx->dSel, ctx->dDelta, eps, cap, ctx->dSweeps, ctx->dResidual, ctx->dStatus);
         CK(cudaGetLastError());
       }
       if (ev && !selTimed) CK(cudaEventRecordWithFlags(ev[2 * i], ctx->stream, evFlags));
@@ -2884,7 +2961,8 @@ int batch_graph(morap_ctx* ctx, int kind, double eps, int cap, int B, bool timed
   key.ncand = kind == 0 && ctx->optSkip ? ctx->nCand : 0;
   const void* ptrs[] = {ctx->dModels, ctx->dOptJobs, ctx->dList,  ctx->dPrefix,    ctx->dCtl,      ctx->dDelta,
                         ctx->dMask,   ctx->dNrhs,    ctx->dSweeps, ctx->dResidual, ctx->dStatus,   ctx->dJobModel,
-                        ctx->dEvalJobsRaw, ctx->stream, ctx->dSel, ctx->dCand, ctx->dCandOut};
+                        ctx->dEvalJobsRaw, ctx->stream, ctx->dSel, ctx->dCand, ctx->dCandOut, ctx->dCandOutG,
+                        ctx->dStampAll};
   static_assert(sizeof(ptrs) / sizeof(ptrs[0]) == morap_ctx::kKeyPtrs, "graph key size");
   for (int i = 0; i < morap_ctx::kKeyPtrs; ++i) key.ptrs[i] = ptrs[i];
   for (auto& g : ctx->graphs)
@@ -3007,7 +3085,8 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   // x region is zeroed with one memset (x = y = 0 at the start, numerics.hpp:81)
   size_t rhoBytes = 0, xBytes = 0, polBytes = 0;
   std::vector<size_t> offRho(njobs), offX(njobs), offPol(njobs);
-  auto stampBytes = [](int S) { return align_up(sizeof(int32_t) * (((S + 31) / 32 + 7) & ~3), 256); };
+  std::vector<int32_t> stampOff(njobs);
+  size_t stampInts = 0;  // stamps of every job, contiguous (k_select indexes them absolutely)
   // compact sweeps read rho_w per reward class only: no per-row rho vector then
   bool allCompact = ctx->useCompact && ctx->useTma && !rhoHost;
   for (int j = 0; j < njobs && allCompact; ++j)
@@ -3018,10 +3097,15 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     const bool lean = !ctx->dm[model_ids[j]].prob;  // lean compact model: class table only
     if (!lean && !allCompact) rhoBytes += align_up(sizeof(double) * m.R, 256);
     offX[j] = xBytes;
-    xBytes += 2 * align_up(sizeof(double) * m.S, 256) + stampBytes(m.S);  // x0 | x1 | stamps
+    xBytes += 2 * align_up(sizeof(double) * m.S, 256);  // x0 | x1
+    stampOff[j] = static_cast<int32_t>(stampInts);
+    stampInts += static_cast<size_t>(((m.S + 31) / 32 + 7) & ~3);
     offPol[j] = polBytes;
     polBytes += align_up(sizeof(int32_t) * m.S, 256);
   }
+  if (stampInts >= (1u << 31)) return ctx->fail(MORAP_SIZE_GUARD, "stamp array exceeds 2^31 entries");
+  const size_t xJobBytes = xBytes;
+  xBytes += align_up(sizeof(int32_t) * stampInts, 256);  // zeroed with x
   const size_t classBytes = static_cast<size_t>(njobs) * 256 * sizeof(double);  // rho_w per reward class
   const size_t need = rhoBytes + xBytes + polBytes + classBytes;
   int rc;
@@ -3044,8 +3128,11 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     J.buf[0] = reinterpret_cast<double*>(base + rhoBytes + offX[j]);
     J.buf[1] = reinterpret_cast<double*>(base + rhoBytes + offX[j] + align_up(sizeof(double) * m.S, 256));
     J.policy = reinterpret_cast<int32_t*>(base + rhoBytes + xBytes + offPol[j]);
-    J.stamp = reinterpret_cast<int32_t*>(base + rhoBytes + offX[j] + 2 * align_up(sizeof(double) * m.S, 256));
+    J.stampOff = stampOff[j];
+    J.stamp = reinterpret_cast<int32_t*>(base + rhoBytes + xJobBytes) + stampOff[j];
     J.outGrp = ctx->dm[model_ids[j]].outGrp;
+    J.bytesPerSweep = ctx->dm[model_ids[j]].bytesPerSweep;
+    J.nnz = m.nnz;
     J.classRho = (!rhoHost && ctx->dm[model_ids[j]].compact)
                      ? reinterpret_cast<double*>(base + rhoBytes + xBytes + polBytes + 256ull * sizeof(double) * j)
                      : nullptr;
@@ -3059,9 +3146,22 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   ctx->optSkip = allCompact && ctx->skip;
   for (int j = 0; j < njobs && ctx->optSkip; ++j)
     if (ctx->hm[model_ids[j]].ntiles >= (1 << kCandLtBits)) ctx->optSkip = false;  // k_build_cand packing
+  ctx->dStampAll = reinterpret_cast<int32_t*>(base + rhoBytes + xJobBytes);
   if (ctx->optSkip) {
-    size_t tiles = 0;
-    for (int j : active) tiles += static_cast<size_t>(ctx->hm[model_ids[j]].ntiles);
+    size_t tiles = 0, outs = 0;
+    for (int j : active) {
+      tiles += static_cast<size_t>(ctx->hm[model_ids[j]].ntiles);
+      ctx->hOptJobs[j].outBase = static_cast<int32_t>(outs);
+      outs += static_cast<size_t>(ctx->hm[model_ids[j]].nOutGrp);
+    }
+    if (outs >= (1u << 31)) ctx->optSkip = false;
+    if (outs > ctx->candOutGCap) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      cudaFree(ctx->dCandOutG);
+      ctx->dCandOutG = nullptr;
+      ctx->candOutGCap = std::max(outs, ctx->candOutGCap + ctx->candOutGCap / 2);
+      CK(cudaMalloc(&ctx->dCandOutG, ctx->candOutGCap * sizeof(int32_t)));
+    }
     if (tiles > ctx->selCap) {
       CK(cudaStreamSynchronize(ctx->stream));
       cudaFree(ctx->dSel);
@@ -3086,12 +3186,12 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   CK(cudaMemcpyAsync(ctx->dOptJobs, ctx->hOptJobs.data(), njobs * sizeof(OptJob), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->dStatus, statusInit.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->dSweeps, zeroI.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemsetAsync(ctx->dDelta, 0, njobs * sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->dDelta, 0, 2 * njobs * sizeof(unsigned long long), ctx->stream));  // two parities
   CK(cudaMemsetAsync(ctx->dResidual, 0, njobs * sizeof(double), ctx->stream));
   if ((rc = init_ctl(ctx, active, ctx->optModel))) return rc;
   if (ctx->optSkip && !active.empty()) {
-    std::vector<int32_t> alive(njobs, -1);
-    for (int j : active) alive[j] = 0;
+    std::vector<int32_t> alive(njobs, 0);  // act: 1 while the job iterates
+    for (int j : active) alive[j] = 1;
     CK(cudaMemcpyAsync(ctx->dAlive, alive.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));  // `alive` is a local
     int maxTiles = 0;
@@ -3099,7 +3199,8 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     for (size_t s0 = 0; s0 < active.size(); s0 += 65535) {  // gridDim.y limit
       const dim3 grid((maxTiles + kSelThreads - 1) / kSelThreads, static_cast<unsigned>(std::min<size_t>(65535, active.size() - s0)));
       k_build_cand<<<grid, kSelThreads, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix,
-                                                          ctx->dCand, ctx->dCandOut, static_cast<int>(s0));
+                                                          ctx->dCand, ctx->dCandOut, ctx->dCandOutG,
+                                                          static_cast<int>(s0));
       CK(cudaGetLastError());
       ctx->stats[8] += 1;
     }
@@ -3521,6 +3622,7 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   cudaFree(ctx->dSel);
   cudaFree(ctx->dCand);
   cudaFree(ctx->dCandOut);
+  cudaFree(ctx->dCandOutG);
   cudaFree(ctx->dTrace);
   cudaFree(ctx->dCtl);
   cudaFreeHost(ctx->hCtl);
@@ -3712,7 +3814,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     const DevModel& dmod = built[m];
     ctx->dm.push_back(dmod);
     ctx->hm.push_back(HostModel{dmod.S, dmod.R, dmod.nnz, dmod.initial, dmod.ntiles, dmod.K, dmod.rewardFinite,
-                                maxRowNnz[m]});
+                                maxRowNnz[m], static_cast<int32_t>(compact[m].outGrp.size())});
     if (ids_out) ids_out[m] = first + m;
   }
   lapU("packed, copies queued");
