@@ -2631,7 +2631,8 @@ struct CompactStream {
   bool ok = false;
   std::vector<uint8_t> idx, cls;
   std::vector<double> dict, table;
-  std::vector<uint32_t> stW, rowW, trW;        // packed state / row / transition words, padded per tile
+  size_t nStW = 0, nRowW = 0, nTrW = 0;        // packed state / row / transition words, padded per tile
+                                               // (written straight into the upload staging: fill_streams)
   std::vector<TilePos> pos;
   std::vector<int32_t> outIdx, outGrp;        // out-of-window stamp groups per tile (DevModel)
 };
@@ -2640,7 +2641,9 @@ struct CompactStream {
 // starts on a 16-byte boundary (padded), so one bulk copy per stream lands at offset 0 of
 // its stage region. u16 window offsets succW = succ - wlo inside the tile's x window
 // (0xFFFF outside), u16 ends relative to the tile, allIn / simple flags per tile.
-void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, CompactStream& c) {
+// layout_streams: slice positions, stream sizes, the per-tile flags and out-of-window
+// stamp groups; fill_streams (at packing time) writes the words into the staging buffer.
+void layout_streams(const morap_csr_view& v, std::vector<TileDesc>& desc, CompactStream& c) {
   const size_t nt = desc.size() - 1;
   c.pos.assign(nt, TilePos{});
   auto up16 = [](size_t n, size_t es) { return (n * es + 15) / 16 * 16 / es; };  // elements, padded
@@ -2657,9 +2660,9 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
     nTrn += up16(nr, 4);
     nSucc += up16(nz, 4);
   }
-  c.stW.assign(nRow, 0);
-  c.rowW.assign(nTrn, 0);
-  c.trW.assign(nSucc, 0xFFFFu);
+  c.nStW = nRow;
+  c.nRowW = nTrn;
+  c.nTrW = nSucc;
   c.outIdx.assign(nt + 1, 0);
   c.outGrp.clear();
   for (size_t t = 0; t < nt; ++t) {
@@ -2674,21 +2677,8 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
       c.outIdx[t + 1] = static_cast<int32_t>(c.outGrp.size());
       continue;
     }
-    const TilePos& p = c.pos[t];
-    for (int q = d.s0; q < e.s0; ++q)  // fitting tiles: row end <= 768 (10 bits), transition end <= 1024 (11)
-      c.stW[p.row + (q - d.s0)] = static_cast<uint32_t>(v.row_offset[q + 1] - d.r0) |
-                                  (static_cast<uint32_t>(v.trn_offset[v.row_offset[q + 1]] - d.k0) << 10) |
-                                  (v.done[q] ? 1u << 21 : 0u);
-    for (int r = d.r0; r < e.r0; ++r)
-      c.rowW[p.trn + (r - d.r0)] =
-          static_cast<uint32_t>(v.trn_offset[r + 1] - d.k0) | (static_cast<uint32_t>(c.cls[r]) << 16);
     int allIn = 1;
-    for (int k = d.k0; k < e.k0; ++k) {
-      const unsigned o = static_cast<unsigned>(v.succ[k] - d.wlo);
-      const bool in = o < static_cast<unsigned>(d.wn);
-      c.trW[p.succ + (k - d.k0)] = (in ? o : 0xFFFFu) | (static_cast<uint32_t>(c.idx[k]) << 16);
-      allIn &= in ? 1 : 0;
-    }
+    for (int k = d.k0; k < e.k0; ++k) allIn &= static_cast<unsigned>(v.succ[k] - d.wlo) < static_cast<unsigned>(d.wn);
     d.allIn = allIn;
     if (!allIn) {  // stamp groups of the out-of-window successors (sorted, distinct, <= kMaxOutGroups)
       const size_t at = c.outGrp.size();
@@ -2702,6 +2692,33 @@ void build_window_offsets(const morap_csr_view& v, std::vector<TileDesc>& desc, 
       }
     }
     c.outIdx[t + 1] = static_cast<int32_t>(c.outGrp.size());
+  }
+}
+
+void fill_streams(const morap_csr_view& v, const std::vector<TileDesc>& desc, const CompactStream& c, uint32_t* stW,
+                  uint32_t* rowW, uint32_t* trW) {
+  const size_t nt = desc.size() - 1;
+  for (size_t t = 0; t < nt; ++t) {
+    const TileDesc &d = desc[t], &e = desc[t + 1];
+    const TilePos& p = c.pos[t];
+    const size_t endRow = t + 1 < nt ? static_cast<size_t>(c.pos[t + 1].row) : c.nStW;
+    const size_t endTrn = t + 1 < nt ? static_cast<size_t>(c.pos[t + 1].trn) : c.nRowW;
+    const size_t endSucc = t + 1 < nt ? static_cast<size_t>(c.pos[t + 1].succ) : c.nTrW;
+    size_t a = p.row, b = p.trn, z = p.succ;
+    if (d.fits) {
+      for (int q = d.s0; q < e.s0; ++q)  // fitting tiles: row end <= 768 (10 bits), transition end <= 1024 (11)
+        stW[a++] = static_cast<uint32_t>(v.row_offset[q + 1] - d.r0) |
+                   (static_cast<uint32_t>(v.trn_offset[v.row_offset[q + 1]] - d.k0) << 10) | (v.done[q] ? 1u << 21 : 0u);
+      for (int r = d.r0; r < e.r0; ++r)
+        rowW[b++] = static_cast<uint32_t>(v.trn_offset[r + 1] - d.k0) | (static_cast<uint32_t>(c.cls[r]) << 16);
+      for (int k = d.k0; k < e.k0; ++k) {
+        const unsigned o = static_cast<unsigned>(v.succ[k] - d.wlo);
+        trW[z++] = (o < static_cast<unsigned>(d.wn) ? o : 0xFFFFu) | (static_cast<uint32_t>(c.idx[k]) << 16);
+      }
+    }
+    for (; a < endRow; ++a) stW[a] = 0u;  // padding (never read)
+    for (; b < endTrn; ++b) rowW[b] = 0u;
+    for (; z < endSucc; ++z) trW[z] = 0xFFFFu;
   }
 }
 
@@ -3683,7 +3700,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     if (ctx->useCompact) {
       build_compact(models[m], compact[m]);
       lapP(2);
-      if (compact[m].ok) build_window_offsets(models[m], descs[m], compact[m]);
+      if (compact[m].ok) layout_streams(models[m], descs[m], compact[m]);
       lapP(3);
     }
   });
@@ -3706,8 +3723,8 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
              align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
     if (compact[m].ok)
       bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(v.num_rows, 256) +
-               align_up(8ull * compact[m].table.size(), 256) + align_up(4ull * compact[m].trW.size(), 256) +
-               align_up(4ull * compact[m].stW.size(), 256) + align_up(4ull * compact[m].rowW.size(), 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256) +
+               align_up(8ull * compact[m].table.size(), 256) + align_up(4ull * compact[m].nTrW, 256) +
+               align_up(4ull * compact[m].nStW, 256) + align_up(4ull * compact[m].nRowW, 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256) +
                align_up(4ull * compact[m].outIdx.size(), 256) + align_up(4ull * compact[m].outGrp.size(), 256);
   }
   void* dev = nullptr;
@@ -3750,8 +3767,8 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
     char* h = host + off[m];
     char* d = static_cast<char*>(dev) + off[m];
     DevModel dmod{};
-    auto put = [&](const void* src, size_t n) {
-      if (n) std::memcpy(h, src, n);
+    auto put = [&](const void* src, size_t n) {  // src == nullptr: reserve (filled by the caller)
+      if (n && src) std::memcpy(h, src, n);
       char* at = d;
       const size_t a = align_up(n, 256);
       h += a;
@@ -3787,9 +3804,13 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
       dmod.rclass = reinterpret_cast<const uint8_t*>(put(c.cls.data(), c.cls.size()));
       dmod.classTable = reinterpret_cast<const double*>(put(c.table.data(), 8ull * c.table.size()));
       dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
-      dmod.stW = reinterpret_cast<const uint32_t*>(put(c.stW.data(), 4ull * c.stW.size()));
-      dmod.rowW = reinterpret_cast<const uint32_t*>(put(c.rowW.data(), 4ull * c.rowW.size()));
-      dmod.trW = reinterpret_cast<const uint32_t*>(put(c.trW.data(), 4ull * c.trW.size()));
+      uint32_t* hs = reinterpret_cast<uint32_t*>(h);
+      dmod.stW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nStW));
+      uint32_t* hr = reinterpret_cast<uint32_t*>(h);
+      dmod.rowW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nRowW));
+      uint32_t* ht = reinterpret_cast<uint32_t*>(h);
+      dmod.trW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nTrW));
+      fill_streams(v, descs[m], c, hs, hr, ht);  // straight into the staging buffer
       dmod.tilePos = reinterpret_cast<const TilePos*>(put(c.pos.data(), sizeof(TilePos) * c.pos.size()));
       dmod.outIdx = reinterpret_cast<const int32_t*>(put(c.outIdx.data(), 4ull * c.outIdx.size()));
       dmod.outGrp = reinterpret_cast<const int32_t*>(put(c.outGrp.data(), 4ull * c.outGrp.size()));
