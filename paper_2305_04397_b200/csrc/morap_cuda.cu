@@ -2485,7 +2485,9 @@ struct morap_ctx {
   bool optCompact = false; // current optimize batch runs the deep compact pipeline
   int cmpBlocks = 0;
   bool skip = true;        // frozen-tile skipping in compact optimize sweeps (k_select)
-  bool timeSweepOnly = std::getenv("MORAP_TIME_SWEEP_ONLY") != nullptr;  // profiling: k_select outside the events
+  // profiling: the events bracket the sweep kernel alone (k_select outside); MORAP_TIME_SELECT=1
+  // brackets k_select + sweep
+  bool timeSweepOnly = std::getenv("MORAP_TIME_SELECT") == nullptr;
   bool optSkip = false;    // current optimize batch uses it
   int selBlocks = 0;
   int2* dSel = nullptr;    // (job, tile) pairs of the current sweep
