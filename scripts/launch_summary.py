@@ -16,7 +16,7 @@ for r in rows[hdr + 1:]:
         continue
     name = re.sub(r"^(void )?<unnamed>::", "", r[ki]).split("(")[0]
     name = name.replace("<(bool)0>", "<0>").replace("<(bool)1>", "<1>").replace("<false>", "<0>").replace("<true>", "<1>")
-    us = float(r[vi].replace(",", "")) * (1e-3 if r[ui] == "nsecond" else (1e3 if r[ui] == "msecond" else 1.0))
+    us = float(r[vi].replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
     n, t = agg.get(name, (0, 0.0))
     agg[name] = (n + 1, t + us)
 total = sum(t for _, t in agg.values())
