@@ -1911,7 +1911,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, uns
       __threadfence();
       atomicAdd(gen, 1u);
     } else {
-      while (*vg == g) __nanosleep(20);
+      while (*vg == g) {
+      }
     }
     __threadfence();
   }
