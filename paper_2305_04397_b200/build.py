@@ -23,6 +23,9 @@ CUDA_FLAGS = [
     "-lineinfo", "-O3", "-std=c++17",
     "-fmad=false",  # bitwise parity with the reference's no-FMA CPU arithmetic
     "-Xcompiler", "-fPIC", "-shared",
+    # host side of the .cu (upload preparation: validation, tiling, compact streams -- integer
+    # and bit-pattern work only): vectorised like the host library, no FP contraction
+    "-Xcompiler", "-O3,-mavx2,-ffp-contract=off",
 ]
 
 HOST_SOURCES = ["linalg.cpp", "logic.cpp", "model.cpp", "warehouse.cpp", "assignment.cpp", "geometry.cpp",

@@ -26,6 +26,8 @@
 // equal the reference CPU solver bit for bit.
 #include <cuda_runtime.h>
 
+#include <immintrin.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -2762,7 +2764,7 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
   uint64_t seen[kScan];
   for (int q = 0; q < kScan; ++q) seen[q] = ~0ull;
   int nseen = 0;
-  for (int k = 0; k < v.nnz; ++k) {
+  auto scalarProb = [&](int k) {  // false: more than 256 distinct probabilities
     uint64_t b;
     std::memcpy(&b, &v.prob[k], 8);
     int id = -1;
@@ -2770,14 +2772,44 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
     for (int q = 0; q < kScan; ++q) id = seen[q] == b ? q : id;
     if (id < 0) {
       id = probs.find(&b);
-      if (id < 0) return;
+      if (id < 0) return false;
       if (id == static_cast<int>(c.dict.size())) {
         c.dict.push_back(v.prob[k]);
         if (nseen < kScan && id == nseen) seen[nseen++] = b;
       }
     }
     c.idx[k] = static_cast<uint8_t>(id);
+    return true;
+  };
+  // AVX2: four probabilities per step against the known values (lane id = position + 1, 0 =
+  // unknown); a step with an unknown value goes through the scalar path, which learns it
+  int k = 0;
+  while (k < v.nnz && nseen == 0)
+    if (!scalarProb(k++)) return;
+  for (int known = 0; k + 4 <= v.nnz;) {
+    __m256i sv[kScan], iv[kScan];
+    known = nseen;
+    for (int q = 0; q < known; ++q) {
+      sv[q] = _mm256_set1_epi64x(static_cast<long long>(seen[q]));
+      iv[q] = _mm256_set1_epi64x(q + 1);
+    }
+    for (; k + 4 <= v.nnz; k += 4) {
+      const __m256i x = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(v.prob + k));
+      __m256i id = _mm256_setzero_si256();
+      for (int q = 0; q < known; ++q) id = _mm256_or_si256(id, _mm256_and_si256(_mm256_cmpeq_epi64(x, sv[q]), iv[q]));
+      if (_mm256_movemask_pd(_mm256_castsi256_pd(_mm256_cmpeq_epi64(id, _mm256_setzero_si256())))) break;
+      alignas(32) uint64_t t[4];
+      _mm256_store_si256(reinterpret_cast<__m256i*>(t), id);
+      const uint32_t w = static_cast<uint32_t>(t[0] - 1) | static_cast<uint32_t>(t[1] - 1) << 8 |
+                         static_cast<uint32_t>(t[2] - 1) << 16 | static_cast<uint32_t>(t[3] - 1) << 24;
+      std::memcpy(&c.idx[k], &w, 4);
+    }
+    if (k + 4 > v.nnz) break;
+    for (int e = k + 4; k < e; ++k)  // a step with an unknown value: scalar (learns it)
+      if (!scalarProb(k)) return;
   }
+  for (; k < v.nnz; ++k)
+    if (!scalarProb(k)) return;
   c.cls.resize(static_cast<size_t>(v.num_rows));
   SmallIds classes(K);
   uint64_t key[MORAP_MAX_OBJECTIVES];
@@ -2790,26 +2822,59 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
     uint64_t ta[kScan], tb[kScan];
     for (int q = 0; q < kScan; ++q) ta[q] = tb[q] = ~0ull;
     int nt = 0;
-    for (; r0 < v.num_rows; ++r0) {
-      uint64_t a, b;
-      std::memcpy(&a, &v.rewards[0][r0], 8);
-      std::memcpy(&b, &v.rewards[1][r0], 8);
-      int id = -1;
-#pragma unroll
-      for (int q = 0; q < kScan; ++q) id = (ta[q] == a) & (tb[q] == b) ? q : id;
-      if (id < 0) {
-        if (nt == kScan) break;  // more tuples: finish in the general loop below
-        key[0] = a;
-        key[1] = b;
-        id = classes.find(key);
-        if (id < 0) return;
-        c.table.push_back(v.rewards[0][r0]);
-        c.table.push_back(v.rewards[1][r0]);
-        ta[nt] = a;
-        tb[nt] = b;
-        ++nt;
+    // AVX2 steps of four rows once a tuple is known (a step with an unknown tuple drops to
+    // the scalar loop below for one step, which learns it)
+    for (;;) {
+      if (nt > 0) {
+        __m256i va[kScan], vb[kScan], iv[kScan];
+        for (int q = 0; q < nt; ++q) {
+          va[q] = _mm256_set1_epi64x(static_cast<long long>(ta[q]));
+          vb[q] = _mm256_set1_epi64x(static_cast<long long>(tb[q]));
+          iv[q] = _mm256_set1_epi64x(q + 1);
+        }
+        for (; r0 + 4 <= v.num_rows; r0 += 4) {
+          const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(v.rewards[0] + r0));
+          const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(v.rewards[1] + r0));
+          __m256i id = _mm256_setzero_si256();
+          for (int q = 0; q < nt; ++q)
+            id = _mm256_or_si256(id, _mm256_and_si256(_mm256_and_si256(_mm256_cmpeq_epi64(a, va[q]),
+                                                                        _mm256_cmpeq_epi64(b, vb[q])), iv[q]));
+          if (_mm256_movemask_pd(_mm256_castsi256_pd(_mm256_cmpeq_epi64(id, _mm256_setzero_si256())))) break;
+          alignas(32) uint64_t t[4];
+          _mm256_store_si256(reinterpret_cast<__m256i*>(t), id);
+          const uint32_t w = static_cast<uint32_t>(t[0] - 1) | static_cast<uint32_t>(t[1] - 1) << 8 |
+                             static_cast<uint32_t>(t[2] - 1) << 16 | static_cast<uint32_t>(t[3] - 1) << 24;
+          std::memcpy(&c.cls[r0], &w, 4);
+        }
       }
-      c.cls[r0] = static_cast<uint8_t>(id);
+      if (r0 >= v.num_rows) break;
+      const int stepEnd = std::min(v.num_rows, r0 + 4);  // scalar: this step (or the tail)
+      bool more = false;
+      for (; r0 < stepEnd; ++r0) {
+        uint64_t a, b;
+        std::memcpy(&a, &v.rewards[0][r0], 8);
+        std::memcpy(&b, &v.rewards[1][r0], 8);
+        int id = -1;
+#pragma unroll
+        for (int q = 0; q < kScan; ++q) id = (ta[q] == a) & (tb[q] == b) ? q : id;
+        if (id < 0) {
+          if (nt == kScan) {
+            more = true;  // more tuples: finish in the general loop below
+            break;
+          }
+          key[0] = a;
+          key[1] = b;
+          id = classes.find(key);
+          if (id < 0) return;
+          c.table.push_back(v.rewards[0][r0]);
+          c.table.push_back(v.rewards[1][r0]);
+          ta[nt] = a;
+          tb[nt] = b;
+          ++nt;
+        }
+        c.cls[r0] = static_cast<uint8_t>(id);
+      }
+      if (more || r0 >= v.num_rows) break;
     }
   }
   for (int r = r0; r < v.num_rows; ++r) {
