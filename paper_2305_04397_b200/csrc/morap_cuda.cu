@@ -2438,6 +2438,7 @@ struct morap_ctx {
 
   // evaluate batch state
   int evalJobs = 0;
+  int evalSplitG = 1, evalSplitChunk = 0;  // evaluate_optimized split each job's RHS into G sub-jobs
   std::vector<EvalJob> hEvalJobs;
   std::vector<int32_t> evalSweeps;  // njobs * MAX_RHS
   void* evalArena = nullptr;
@@ -3554,10 +3555,11 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
   CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   double backups = 0;
+  size_t q = 0;  // outputs: every job's RHS in order (j * nrhs + o for a uniform batch)
   for (int j = 0; j < njobs; ++j) {
     const EvalJob& J = ctx->hEvalJobs[j];
-    for (int o = 0; o < J.nrhs; ++o) {
-      const size_t q = static_cast<size_t>(j) * J.nrhs + o, s = static_cast<size_t>(j) * MORAP_MAX_RHS + o;
+    for (int o = 0; o < J.nrhs; ++o, ++q) {
+      const size_t s = static_cast<size_t>(j) * MORAP_MAX_RHS + o;
       value_out[q] = vals[s];
       if (sweeps_out) sweeps_out[q] = ctx->evalSweeps[s];
       if (residual_out) residual_out[q] = res[s];
@@ -3928,6 +3930,8 @@ int morap_cuda_release_models(morap_ctx* ctx) {
   ctx->hm.clear();
   ctx->optJobs = 0;
   ctx->evalJobs = 0;
+  ctx->evalSplitG = 1;
+  ctx->evalSplitChunk = 0;
   return MORAP_OK;
 }
 
@@ -4043,6 +4047,8 @@ int morap_cuda_evaluate_optimized(morap_ctx* ctx, int njobs, const int32_t* opt_
   if (njobs < 0 || nrhs < 1 || nrhs > MORAP_MAX_RHS) return ctx->fail(MORAP_INVALID_CONFIG, "bad evaluate batch");
   if (!(eps >= 0.0) || sweep_cap < 1) return ctx->fail(MORAP_INVALID_CONFIG, "bad eps / sweep cap");
   ctx->evalJobs = 0;
+  ctx->evalSplitG = 1;
+  ctx->evalSplitChunk = 0;
   if (njobs == 0) return MORAP_OK;
   std::vector<int32_t> jl(opt_jobs, opt_jobs + njobs);
   for (int j : jl)
@@ -4062,27 +4068,40 @@ int morap_cuda_evaluate_optimized(morap_ctx* ctx, int njobs, const int32_t* opt_
     std::fprintf(stderr, "[morap] evaluate_optimized: policies %.3f ms\n",
                  1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count());
   }
-  std::vector<EvalJob> proto(njobs);
-  std::vector<uint32_t> mask(njobs, (1u << nrhs) - 1u);
-  std::vector<int32_t> st(static_cast<size_t>(njobs) * MORAP_MAX_RHS, MORAP_OK);
+  // more RHS than the chain kernels take (e.g. the 2n objectives of a centralised model):
+  // G sub-jobs of <= kEvRhs RHS each on the same policy chain, consecutive, so the outputs
+  // keep the caller's layout (every RHS is its own stop test: splitting changes nothing)
+  const int G = nrhs > kEvRhs && ctx->useTma ? (nrhs + kEvRhs - 1) / kEvRhs : 1;
+  const int chunk = (nrhs + G - 1) / G;
+  std::vector<EvalJob> proto(static_cast<size_t>(njobs) * G);
+  std::vector<uint32_t> mask(proto.size());
+  std::vector<int32_t> st(proto.size() * MORAP_MAX_RHS, MORAP_OK);
   for (int q = 0; q < njobs; ++q) {
     const int j = jl[q];
     const int model = ctx->optModel[j];
-    EvalJob& E = proto[q];
-    E = EvalJob{};
-    E.model = model;
-    E.nrhs = nrhs;
-    E.policy = ctx->hOptJobs[j].policy;
-    for (int o = 0; o < nrhs; ++o) {
+    for (int o = 0; o < nrhs; ++o)
       if (objective[o] < 0 || objective[o] >= ctx->hm[model].K)
         return ctx->fail(MORAP_DIMENSION_MISMATCH, "objective index out of range");
-      E.rho[o] = ctx->dm[model].obj[objective[o]];  // null for lean models (class table used)
-      E.objIdx[o] = objective[o];
+    for (int g = 0; g < G; ++g) {
+      EvalJob& E = proto[static_cast<size_t>(q) * G + g];
+      E = EvalJob{};
+      E.model = model;
+      E.nrhs = std::min(chunk, nrhs - g * chunk);
+      E.policy = ctx->hOptJobs[j].policy;
+      for (int o = 0; o < E.nrhs; ++o) {
+        E.rho[o] = ctx->dm[model].obj[objective[g * chunk + o]];  // null for lean models (class table used)
+        E.objIdx[o] = objective[g * chunk + o];
+      }
+      mask[static_cast<size_t>(q) * G + g] = (1u << E.nrhs) - 1u;
     }
-    if (!ctx->dm[model].obj[0] && (nrhs > kEvRhs || !ctx->useTma))
-      return ctx->fail(MORAP_INVALID_CONFIG, "lean models are evaluated through policy chains (<= 4 objectives)");
+    if (!ctx->dm[model].obj[0] && !ctx->useTma)
+      return ctx->fail(MORAP_INVALID_CONFIG, "lean models are evaluated through policy chains");
   }
-  return evaluate_impl(ctx, njobs, proto, eps, sweep_cap, value_out, sweeps_out, residual_out, status_out, mask, st);
+  const int rc2 = evaluate_impl(ctx, static_cast<int>(proto.size()), proto, eps, sweep_cap, value_out, sweeps_out,
+                                residual_out, status_out, mask, st);
+  ctx->evalSplitG = G;
+  ctx->evalSplitChunk = G > 1 ? chunk : 0;
+  return rc2;
 }
 
 int morap_cuda_evaluate(morap_ctx* ctx, int njobs, const int32_t* model_ids, const int32_t* const* policies,
@@ -4094,6 +4113,8 @@ int morap_cuda_evaluate(morap_ctx* ctx, int njobs, const int32_t* model_ids, con
     return ctx->fail(MORAP_INVALID_CONFIG, "bad evaluate batch");
   if (!(eps >= 0.0) || sweep_cap < 1) return ctx->fail(MORAP_INVALID_CONFIG, "bad eps / sweep cap");
   ctx->evalJobs = 0;
+  ctx->evalSplitG = 1;
+  ctx->evalSplitChunk = 0;
   if (njobs == 0) return MORAP_OK;
   // stage policies + rewards in one device block
   size_t bytes = 0;
@@ -4142,6 +4163,12 @@ int morap_cuda_evaluate(morap_ctx* ctx, int njobs, const int32_t* model_ids, con
 
 int morap_cuda_fetch_eval_values(morap_ctx* ctx, int job, int rhs, double* out) {
   if (!ctx) return MORAP_INVALID_CONFIG;
+  if (ctx->evalSplitChunk > 0) {  // the caller's (job, rhs) in the split batch
+    if (job < 0 || job >= ctx->evalJobs / ctx->evalSplitG || rhs < 0)
+      return ctx->fail(MORAP_INVALID_CONFIG, "job out of range");
+    job = job * ctx->evalSplitG + rhs / ctx->evalSplitChunk;
+    rhs %= ctx->evalSplitChunk;
+  }
   if (job < 0 || job >= ctx->evalJobs) return ctx->fail(MORAP_INVALID_CONFIG, "job out of range");
   const EvalJob& J = ctx->hEvalJobs[job];
   if (rhs < 0 || rhs >= J.nrhs) return ctx->fail(MORAP_INVALID_CONFIG, "rhs out of range");
