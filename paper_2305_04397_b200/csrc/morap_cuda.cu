@@ -1061,8 +1061,6 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const DevModel* __restri
                                                         int2* __restrict__ sel, unsigned long long* deltaBits,
                                                         double eps, int cap, int32_t* sweeps, double* residual,
                                                         int32_t* status) {
-  __shared__ int sCnt[kSelThreads / 32];
-  __shared__ int sBase;
   __shared__ unsigned long long sB[kSelThreads / 32], sK[kSelThreads / 32];
   const int k = ctl->sweepsDone;
   if (ctl->nactive == 0) return;
@@ -1121,21 +1119,12 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const DevModel* __restri
       }
       c.y &= (1 << kCandLtBits) - 1;
     }
+    // compaction per warp: one atomic per warp with a kept tile, order kept within the warp
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) sCnt[wid] = __popc(bal);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int run = 0;
-      for (int w = 0; w < kSelThreads / 32; ++w) {
-        const int n = sCnt[w];
-        sCnt[w] = run;
-        run += n;
-      }
-      sBase = run ? atomicAdd(&ctl->nsel, run) : 0;
-    }
-    __syncthreads();
-    if (keep) sel[sBase + sCnt[wid] + __popc(bal & ((1u << lane) - 1u))] = make_int2(c.x, c.y);
-    __syncthreads();
+    int at = 0;
+    if (lane == 0 && bal) at = atomicAdd(&ctl->nsel, __popc(bal));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (keep) sel[at + __popc(bal & ((1u << lane) - 1u))] = make_int2(c.x, c.y);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
