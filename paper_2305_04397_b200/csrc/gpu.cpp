@@ -159,7 +159,7 @@ void GpuBackend::uploadProducts(const std::vector<const ProductMdp*>& products, 
   for (size_t k = 0; k < todo.size(); ++k) ids_.emplace(todo[k]->uid, ids[k]);
 }
 
-Scheduler makeDeterministic(std::vector<int> rows) { return Scheduler{std::move(rows)}; }
+Scheduler makeDeterministic(std::vector<int> rows) { return Scheduler{SchedulerRows(rows.begin(), rows.end())}; }
 
 RewardStructure weightedReward(const std::vector<const RewardStructure*>& parts, const Vec& w) {
   if (parts.size() != w.size()) fail(Errc::DimensionMismatch, "one weight per reward structure");

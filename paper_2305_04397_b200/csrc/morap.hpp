@@ -15,6 +15,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <type_traits>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -200,8 +201,30 @@ MorapInstance generateInstance(const WarehouseConfig& cfg, int threads = 0, size
 WarehouseConfig warehouseConfigFromJson(const Json& j);
 
 // ---- per-model solve on the GPU (numerics.hpp, engine.hpp) --------------------------------
+// Allocator that default-initialises (no zero fill): scheduler rows are always written in
+// full right after they are sized (a C2 query sizes 10 x ~0.3 MB of them per iteration).
+template <class T>
+struct DefaultInitAllocator : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = DefaultInitAllocator<U>;
+  };
+  DefaultInitAllocator() = default;
+  template <class U>
+  DefaultInitAllocator(const DefaultInitAllocator<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept(std::is_nothrow_default_constructible<U>::value) {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+using SchedulerRows = std::vector<int, DefaultInitAllocator<int>>;
+
 struct Scheduler {  // deterministic: one action row per state (the solver only produces these)
-  std::vector<int> rows;
+  SchedulerRows rows;
 };
 Scheduler makeDeterministic(std::vector<int> rows);
 struct SweepStats {
