@@ -12,7 +12,7 @@ import os
 
 import numpy as np
 
-from .errors import MorapError, check_status
+from .errors import MorapError
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CUDA_SO = os.path.join(PKG, "libmorap_cuda.so")

@@ -1,5 +1,5 @@
 """Dev probe: persistent evaluate kernel time per sweep against the batch size (1-20 C2 jobs)."""
-import sys, json, numpy as np
+import sys, numpy as np
 sys.path.insert(0, '.')
 from paper_2305_04397_b200.api import Instance
 from paper_2305_04397_b200.cuda import CudaBackend

@@ -1,4 +1,4 @@
-import sys, os
+import sys
 sys.path.insert(0, '.')
 from paper_2305_04397_b200.api import Instance, Solver
 from tests.helpers import warehouse_config

@@ -64,7 +64,7 @@ def _worker(rank, world, port, case, out_path, mode="full"):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2305_04397_b200.api import Instance
-        from paper_2305_04397_b200.distributed import ShardedQuery, _Exchange, pareto_sharded
+        from paper_2305_04397_b200.distributed import _Exchange, pareto_sharded
 
         if mode == "shard":  # every rank builds only its own products
             inst = Instance.warehouse_shard(case["config"], rank, world, chunk=3)
