@@ -94,12 +94,12 @@ struct DevModel {
   // per transition and a u8 reward class per row instead of fp64 prob and rho_w.
   const uint8_t* probIdx;     // nnz
   const double* probDict;     // <= 256 distinct probabilities
-  const uint8_t* rclass;      // R
+  const uint16_t* rclass;     // R (u16: up to kMaxClasses reward tuples)
   const double* classTable;   // nclass x K objective tuples
   // compact sweep streams, tile-major and padded per tile (TilePos): rowOffset[s + 1] -
   // tile.r0 and trnOffset[r + 1] - tile.k0 (u16), succW, and copies of probIdx / rclass / done
   const uint32_t* stW;   // per state: row end | transition end << 10 | done << 21 (tile-relative)
-  const uint32_t* rowW;  // per row: tile-relative transition end | reward class << 16
+  const uint32_t* rowW;  // per row: tile-relative transition end (11 bits) | reward class << 11
   const uint32_t* trW;   // per transition: window offset (0xFFFF outside) | probability index << 16
   const TilePos* tilePos;     // ntiles
   // frozen-tile skipping: stamp groups (32 states) of the successors outside each tile's
@@ -117,7 +117,7 @@ struct OptJob {
   int32_t stampOff;  // first stamp of this job in the batch's stamp array (multiple of 4)
   double w[MORAP_MAX_OBJECTIVES];
   double* rho;
-  double* classRho;  // compact models: rho_w of each reward class (<= 256)
+  double* classRho;  // compact models: rho_w of each reward class (nclass <= kMaxClasses)
   double* buf[2];
   int32_t* policy;
   int32_t* stamp;  // frozen-tile skipping: last sweep in which a state of group g (32 states) changed
@@ -377,12 +377,12 @@ constexpr int kOffProb = kOffSucc + 4 * kStSuccInts;
 constexpr int kOffDone = kOffProb + 8 * kStProbDbls;
 constexpr int kOffX = kOffDone + kStDoneBytes;
 constexpr int kOffIdx = kOffX + 8 * kStXDbls;  // compact models: u8 probability index per transition
-constexpr int kOffCls = kOffIdx + kNnzCap + 16;  // compact models: u8 reward class per row
+constexpr int kOffCls = kOffIdx + kNnzCap + 16;  // compact models: u16 reward class per row
 #ifndef MORAP_XWIN
 #define MORAP_XWIN 992
 #endif
 constexpr int kXWin = MORAP_XWIN;                        // successor window of x staged per tile
-constexpr int kOffXw = kOffCls + kRowCap + 16;
+constexpr int kOffXw = kOffCls + 2 * kRowCap + 16;
 constexpr int kStageBytes = kOffXw + 8 * (kXWin + 2);
 static_assert(kStageBytes % 16 == 0 && kOffTrn % 16 == 0 && kOffRho % 16 == 0 && kOffSucc % 16 == 0 &&
                   kOffProb % 16 == 0 && kOffDone % 16 == 0 && kOffX % 16 == 0 && kOffIdx % 16 == 0 &&
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(kTmaThreads, kStages >= 3 ? 2 : 3) k_greedy_sw
         case 1: src = M->trnOffset; lo = d.r0; hi = e.r0 + 1; es = 4; dstOff = kOffTrn; break;
         case 2: src = M->succ; lo = d.k0; hi = e.k0; es = 4; dstOff = kOffSucc; break;
         case 3:
-          if (cp) { src = M->rclass; es = 1; dstOff = kOffCls; }
+          if (cp) { src = M->rclass; es = 2; dstOff = kOffCls; }
           else { src = J.rho; es = 8; dstOff = kOffRho; }
           lo = d.r0; hi = e.r0;
           break;
@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(kTmaThreads, kStages >= 3 ? 2 : 3) k_greedy_sw
 #pragma unroll 4
               for (int q = qb; q < qe; ++q) prodS[q] = __dmul_rn(prodS[q], xAt(succS[q]));
             }
-            const uint8_t* clsS = st + kOffCls + v.offCls;
+            const uint16_t* clsS = reinterpret_cast<const uint16_t*>(st + kOffCls) + v.offCls;
             double best = 0.0;
             int bestRow = -1;
             int kb = qb;
@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(kTmaThreads, kStages >= 3 ? 2 : 3) k_greedy_sw
         // compact stream: prob from the model's dictionary, rho_w from the job's class table
         // (the same fp64 values, so the same rounded products and sums)
         const uint8_t* idxS = st + kOffIdx + v.offIdx;
-        const uint8_t* clsS = st + kOffCls + v.offCls;
+        const uint16_t* clsS = reinterpret_cast<const uint16_t*>(st + kOffCls) + v.offCls;
 #pragma unroll 4
         for (int i = tid; i < v.nz; i += kConsumers)
           prodS[i] = __dmul_rn(__ldg(v.dict + idxS[i]), __ldg(x + succS[i]));
@@ -844,7 +844,7 @@ constexpr int kCmpStages = MORAP_CMP_STAGES;
 // stage: u16 tile-relative row ends per state and transition ends per row, u16 window
 // offsets, u8 probability index, u8 reward class, done, own x, successor window of x
 constexpr int kCOffRow = 0;                               // u32 state word: row end | transition end << 10 | done << 21
-constexpr int kCOffTrn = kCOffRow + 4 * (kBlock + 4);     // u32 row word: transition end | class << 16
+constexpr int kCOffTrn = kCOffRow + 4 * (kBlock + 4);     // u32 row word: transition end | class << 11
 constexpr int kCOffSucc = kCOffTrn + 4 * (kRowCap + 4);   // u32 transition word: window offset | index << 16
 constexpr int kCOffX = kCOffSucc + 4 * (kNnzCap + 4);
 constexpr int kCOffXw = kCOffX + 8 * kStXDbls;
@@ -1390,8 +1390,8 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
       // diagnostics: stream only
     } else if (v.fits) {
       // Tile-relative u16 row ends per state: state i owns rows [rowE[i-1], rowE[i]) (0 for
-      // i = 0). One u32 word per row: transition end (tile-relative, low 16 bits) and reward
-      // class (bits 16-23); one u32 word per transition: window offset (low 16 bits, 0xFFFF
+      // i = 0). One u32 word per row: transition end (tile-relative, bits 0-10) and reward
+      // class (bits 11-31); one u32 word per transition: window offset (low 16 bits, 0xFFFF
       // outside the window) and probability index (bits 16-23) -- one shared-memory load
       // each instead of two (the compute warps are bound by shared-memory wavefronts).
       // Padded per-tile streams: every slice starts at offset 0 of its region.
@@ -1419,8 +1419,8 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
             // rows, the first one peeled so the max needs no "no row yet" test
             auto row = [&](int r, int& k) {
               const uint32_t rw = rowW[r];
-              const int ke = static_cast<int>(rw & 0xFFFFu);
-              double acc = __ldg(crho + (rw >> 16));
+              const int ke = static_cast<int>(rw & 0x7FFu);
+              double acc = __ldg(crho + (rw >> 11));
               if (k < ke) acc = __dadd_rn(acc, term(trW[k]));
               if (k + 1 < ke) acc = __dadd_rn(acc, term(trW[k + 1]));
               k = ke;
@@ -1440,8 +1440,8 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
 #pragma unroll 1
             for (int r = rb; r < re; ++r) {
               const uint32_t rw = rowW[r];
-              const int ke = static_cast<int>(rw & 0xFFFFu);
-              double acc = __ldg(crho + (rw >> 16));
+              const int ke = static_cast<int>(rw & 0x7FFu);
+              double acc = __ldg(crho + (rw >> 11));
 #pragma unroll 1
               for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, term(trW[q]));
               kb = ke;
@@ -1457,8 +1457,8 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
             };
             for (int r = rb; r < re; ++r) {
               const uint32_t rw = rowW[r];
-              const int ke = static_cast<int>(rw & 0xFFFFu);
-              double acc = __ldg(crho + (rw >> 16));
+              const int ke = static_cast<int>(rw & 0x7FFu);
+              double acc = __ldg(crho + (rw >> 11));
               for (int q = kb; q < ke; ++q) {
                 const uint32_t w = trW[q];
                 acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + (w >> 16)), xAt(q, w)));
@@ -2624,7 +2624,8 @@ void make_tiles(const morap_csr_view& v, std::vector<int32_t>& out, std::vector<
 // alphabet exceeds 256 entries (the model then streams the plain fp64 arrays).
 struct CompactStream {
   bool ok = false;
-  std::vector<uint8_t> idx, cls;
+  std::vector<uint8_t> idx;    // per transition: probability index (<= 256 distinct)
+  std::vector<uint16_t> cls;   // per row: reward class (<= kMaxClasses distinct tuples)
   std::vector<double> dict, table;
   size_t nStW = 0, nRowW = 0, nTrW = 0;        // packed state / row / transition words, padded per tile
                                                // (written straight into the upload staging: fill_streams)
@@ -2705,7 +2706,7 @@ void fill_streams(const morap_csr_view& v, const std::vector<TileDesc>& desc, co
         stW[a++] = static_cast<uint32_t>(v.row_offset[q + 1] - d.r0) |
                    (static_cast<uint32_t>(v.trn_offset[v.row_offset[q + 1]] - d.k0) << 10) | (v.done[q] ? 1u << 21 : 0u);
       for (int r = d.r0; r < e.r0; ++r)
-        rowW[b++] = static_cast<uint32_t>(v.trn_offset[r + 1] - d.k0) | (static_cast<uint32_t>(c.cls[r]) << 16);
+        rowW[b++] = static_cast<uint32_t>(v.trn_offset[r + 1] - d.k0) | (static_cast<uint32_t>(c.cls[r]) << 11);
       for (int k = d.k0; k < e.k0; ++k) {
         const unsigned o = static_cast<unsigned>(v.succ[k] - d.wlo);
         trW[z++] = (o < static_cast<unsigned>(d.wn) ? o : 0xFFFFu) | (static_cast<uint32_t>(c.idx[k]) << 16);
@@ -2717,22 +2718,45 @@ void fill_streams(const morap_csr_view& v, const std::vector<TileDesc>& desc, co
   }
 }
 
-// Tiny open-addressing table (<= 256 keys of up to 8 words) for build_compact.
+// Open-addressing table of up to `cap` keys of up to 8 words for build_compact (grows by
+// doubling; ids in insertion order).
+constexpr int kMaxClasses = 65535;  // reward tuples of a compact model (u16 class index)
 struct SmallIds {
-  static constexpr int kSlots = 1024;
-  int words = 1, count = 0;
+  int words = 1, count = 0, cap = 256, slots = 1024;
   std::vector<uint64_t> keys;
-  std::vector<int16_t> ids;
-  explicit SmallIds(int w) : words(w), keys(static_cast<size_t>(kSlots) * w), ids(kSlots, -1) {}
-  // id of `k` (inserted if new); -1 when a 257th key would be needed
-  int find(const uint64_t* k) {
+  std::vector<int32_t> ids;
+  SmallIds(int w, int maxKeys) : words(w), cap(maxKeys), keys(static_cast<size_t>(slots) * w), ids(slots, -1) {}
+  int slotOf(const uint64_t* k) const {
     uint64_t h = 1469598103934665603ull;
     for (int i = 0; i < words; ++i) h = (h ^ k[i]) * 1099511628211ull;
-    for (int slot = static_cast<int>(h >> 54) & (kSlots - 1);; slot = (slot + 1) & (kSlots - 1)) {
+    return static_cast<int>((h >> 32) & static_cast<uint64_t>(slots - 1));
+  }
+  void grow() {
+    std::vector<uint64_t> ok = std::move(keys);
+    std::vector<int32_t> oi = std::move(ids);
+    const int old = slots;
+    slots *= 2;
+    keys.assign(static_cast<size_t>(slots) * words, 0);
+    ids.assign(slots, -1);
+    for (int q = 0; q < old; ++q) {
+      if (oi[q] < 0) continue;
+      int at = slotOf(&ok[static_cast<size_t>(q) * words]);
+      while (ids[at] >= 0) at = (at + 1) & (slots - 1);
+      std::memcpy(&keys[static_cast<size_t>(at) * words], &ok[static_cast<size_t>(q) * words], 8ull * words);
+      ids[at] = oi[q];
+    }
+  }
+  // id of `k` (inserted if new); -1 when more than `cap` keys would be needed
+  int find(const uint64_t* k) {
+    for (int slot = slotOf(k);; slot = (slot + 1) & (slots - 1)) {
       if (ids[slot] < 0) {
-        if (count == 256) return -1;
+        if (count == cap) return -1;
+        if (2 * (count + 1) > slots) {  // keep the load factor <= 1/2
+          grow();
+          return find(k);
+        }
         std::memcpy(&keys[static_cast<size_t>(slot) * words], k, 8ull * words);
-        ids[slot] = static_cast<int16_t>(count);
+        ids[slot] = count;
         return count++;
       }
       if (std::memcmp(&keys[static_cast<size_t>(slot) * words], k, 8ull * words) == 0) return ids[slot];
@@ -2745,7 +2769,7 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
   const int K = v.num_objectives;
   if (K < 1) return;
   c.idx.resize(static_cast<size_t>(v.nnz));
-  SmallIds probs(1);
+  SmallIds probs(1, 256);
   // the first few distinct values are matched by an unrolled compare against a sentinel-padded
   // list (warehouse products have three probabilities; ~0 is a NaN payload, never a valid
   // probability's bits), so the common case has no data-dependent branch; the rest go
@@ -2801,7 +2825,7 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
   for (; k < v.nnz; ++k)
     if (!scalarProb(k)) return;
   c.cls.resize(static_cast<size_t>(v.num_rows));
-  SmallIds classes(K);
+  SmallIds classes(K, kMaxClasses);
   uint64_t key[MORAP_MAX_OBJECTIVES];
   uint64_t prev[MORAP_MAX_OBJECTIVES];
   int prevId = -1;
@@ -2832,9 +2856,8 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
           if (_mm256_movemask_pd(_mm256_castsi256_pd(_mm256_cmpeq_epi64(id, _mm256_setzero_si256())))) break;
           alignas(32) uint64_t t[4];
           _mm256_store_si256(reinterpret_cast<__m256i*>(t), id);
-          const uint32_t w = static_cast<uint32_t>(t[0] - 1) | static_cast<uint32_t>(t[1] - 1) << 8 |
-                             static_cast<uint32_t>(t[2] - 1) << 16 | static_cast<uint32_t>(t[3] - 1) << 24;
-          std::memcpy(&c.cls[r0], &w, 4);
+          const uint64_t w = (t[0] - 1) | (t[1] - 1) << 16 | (t[2] - 1) << 32 | (t[3] - 1) << 48;
+          std::memcpy(&c.cls[r0], &w, 8);
         }
       }
       if (r0 >= v.num_rows) break;
@@ -2862,7 +2885,7 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
           tb[nt] = b;
           ++nt;
         }
-        c.cls[r0] = static_cast<uint8_t>(id);
+        c.cls[r0] = static_cast<uint16_t>(id);
       }
       if (more || r0 >= v.num_rows) break;
     }
@@ -2874,7 +2897,7 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
       same = same && key[o] == prev[o];
     }
     if (same) {  // runs of equal rows
-      c.cls[r] = static_cast<uint8_t>(prevId);
+      c.cls[r] = static_cast<uint16_t>(prevId);
       continue;
     }
     int id = -1;
@@ -2894,7 +2917,7 @@ void build_compact(const morap_csr_view& v, CompactStream& c) {
     prevId = id;
     if (id == static_cast<int>(c.table.size()) / K)
       for (int o = 0; o < K; ++o) c.table.push_back(v.rewards[o][r]);
-    c.cls[r] = static_cast<uint8_t>(id);
+    c.cls[r] = static_cast<uint16_t>(id);
   }
   if (c.table.empty()) c.table.assign(static_cast<size_t>(K), 0.0);
   c.ok = true;
@@ -3181,7 +3204,12 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   if (stampInts >= (1u << 31)) return ctx->fail(MORAP_SIZE_GUARD, "stamp array exceeds 2^31 entries");
   const size_t xJobBytes = xBytes;
   xBytes += align_up(sizeof(int32_t) * stampInts, 256);  // zeroed with x
-  const size_t classBytes = static_cast<size_t>(njobs) * 256 * sizeof(double);  // rho_w per reward class
+  std::vector<size_t> offClass(njobs);  // rho_w per reward class, per job
+  size_t classBytes = 0;
+  for (int j = 0; j < njobs; ++j) {
+    offClass[j] = classBytes;
+    classBytes += align_up(sizeof(double) * std::max(1, ctx->dm[model_ids[j]].nclass), 256);
+  }
   const size_t need = rhoBytes + xBytes + polBytes + classBytes;
   int rc;
   if ((rc = ensure_arena(ctx, &ctx->optArena, &ctx->optArenaBytes, need))) return rc;
@@ -3209,7 +3237,7 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     J.bytesPerSweep = ctx->dm[model_ids[j]].bytesPerSweep;
     J.nnz = m.nnz;
     J.classRho = (!rhoHost && ctx->dm[model_ids[j]].compact)
-                     ? reinterpret_cast<double*>(base + rhoBytes + xBytes + polBytes + 256ull * sizeof(double) * j)
+                     ? reinterpret_cast<double*>(base + rhoBytes + xBytes + polBytes + offClass[j])
                      : nullptr;
     if (!rhoHost)
       for (int o = 0; o < K; ++o) J.w[o] = weights[static_cast<size_t>(j) * K + o];
@@ -3781,7 +3809,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
              (lean ? 0 : static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256)) +
              align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
     if (compact[m].ok)
-      bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(v.num_rows, 256) +
+      bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(2ull * v.num_rows, 256) +
                align_up(8ull * compact[m].table.size(), 256) + align_up(4ull * compact[m].nTrW, 256) +
                align_up(4ull * compact[m].nStW, 256) + align_up(4ull * compact[m].nRowW, 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256) +
                align_up(4ull * compact[m].outIdx.size(), 256) + align_up(4ull * compact[m].outGrp.size(), 256);
@@ -3860,7 +3888,7 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
       dmod.compact = 1;
       dmod.probIdx = reinterpret_cast<const uint8_t*>(put(c.idx.data(), c.idx.size()));
       dmod.probDict = reinterpret_cast<const double*>(put(c.dict.data(), 8ull * c.dict.size()));
-      dmod.rclass = reinterpret_cast<const uint8_t*>(put(c.cls.data(), c.cls.size()));
+      dmod.rclass = reinterpret_cast<const uint16_t*>(put(c.cls.data(), 2ull * c.cls.size()));
       dmod.classTable = reinterpret_cast<const double*>(put(c.table.data(), 8ull * c.table.size()));
       dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
       uint32_t* hs = reinterpret_cast<uint32_t*>(h);
