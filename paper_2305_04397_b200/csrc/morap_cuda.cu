@@ -2727,9 +2727,14 @@ struct SmallIds {
   std::vector<int32_t> ids;
   SmallIds(int w, int maxKeys) : words(w), cap(maxKeys), keys(static_cast<size_t>(slots) * w), ids(slots, -1) {}
   int slotOf(const uint64_t* k) const {
+    // FNV over whole words, then the TOP bits: the low product bits only see the low key
+    // bits, which are all zero for short-mantissa doubles (-1, 0.125, ...)
     uint64_t h = 1469598103934665603ull;
     for (int i = 0; i < words; ++i) h = (h ^ k[i]) * 1099511628211ull;
-    return static_cast<int>((h >> 32) & static_cast<uint64_t>(slots - 1));
+    h ^= h >> 29;
+    h *= 0xbf58476d1ce4e5b9ull;
+    h ^= h >> 32;
+    return static_cast<int>(h & static_cast<uint64_t>(slots - 1));
   }
   void grow() {
     std::vector<uint64_t> ok = std::move(keys);
