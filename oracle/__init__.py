@@ -323,6 +323,35 @@ class _Ref:
     def hardware_threads(self) -> int:
         return int(self.lib.ref_hardware_threads())
 
+    def pareto_core(self, thresholds, n, query, eps=0.01, norm=None, iter_cap=500, verify=False) -> dict:
+        """runParetoCore (solver.hpp:192) over a Python supporting-point source
+        query(w) -> (r, agent_of), same callback contract as the product's morap_pareto_core."""
+        t = np.ascontiguousarray(thresholds, np.float64)
+        d = t.shape[0]
+        nm = None if norm is None else np.ascontiguousarray(norm, np.float64)
+        proto = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double),
+                            C.POINTER(C.c_int32), C.c_int)
+
+        def cb(user, wp, dd, rp, ap, nn):
+            try:
+                r, a = query(np.ctypeslib.as_array(wp, shape=(dd,)).copy())
+                np.ctypeslib.as_array(rp, shape=(dd,))[:] = r
+                np.ctypeslib.as_array(ap, shape=(nn,))[:] = a
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        fn = proto(cb)
+        self.lib.ref_pareto_core.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_double, C.c_int, C.c_int,
+                                             proto, C.c_void_p, C.c_char_p, C.c_int]
+        buf = C.create_string_buffer(1 << 24)
+        rc = self.lib.ref_pareto_core(t.ctypes.data_as(C.c_void_p), d, n,
+                                      None if nm is None else nm.ctypes.data_as(C.c_void_p), eps, iter_cap,
+                                      int(verify), fn, None, buf, len(buf))
+        if rc:
+            raise RefError(rc, self.lib.ref_last_error().decode())
+        return json.loads(buf.value.decode())
+
 
 _vi = None
 _ref = None

@@ -376,6 +376,40 @@ int ref_pareto(void* p, const double* thresholds, int nt, const double* norm, do
   });
 }
 
+// runParetoCore (solver.hpp:192-266) over an external supporting-point source: the same
+// callback signature as morap_pareto_core (include/morap.h), so the restated sandwich loop
+// and geometry QPs can be compared with the reference's at any dimension (identity norm
+// when `norm` is null).
+typedef int (*ref_query_fn)(void* user, const double* w, int d, double* r_out, int32_t* agent_of_out, int n);
+int ref_pareto_core(const double* thresholds, int d, int n, const double* norm, double eps, int iterCap, int verify,
+                    ref_query_fn query, void* user, char* out, int outlen) {
+  return guarded([&] {
+    Mat nm(d, d, 0.0);
+    if (norm)
+      for (int k = 0; k < d * d; ++k) nm.a[k] = norm[k];
+    else
+      for (int k = 0; k < d; ++k) nm(k, k) = 1.0;
+    bool verdict = false;
+    auto q = [&](const Vec& w) {
+      SupportingPoint sp;
+      sp.r.assign(d, 0.0);
+      sp.assignment.agentOf.assign(n, 0);
+      std::vector<int32_t> a(n, 0);
+      if (query(user, w.data(), d, sp.r.data(), a.data(), n) != 0) fail(Errc::SolverFailure, "query callback failed");
+      for (int j = 0; j < n; ++j) sp.assignment.agentOf[j] = a[j];
+      sp.schedulers.resize(n);
+      return sp;
+    };
+    ParetoResult res = solverdetail::runParetoCore(Vec(thresholds, thresholds + d), NormMatrix(nm), eps, iterCap,
+                                                   verify != 0, verify ? &verdict : nullptr, q);
+    Json j = pareto_report(res);
+    if (verify) j["verdict"] = verdict;
+    std::string s = j.dump();
+    if (static_cast<int>(s.size()) + 1 > outlen) fail(Errc::Io, "output buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+}
+
 int ref_hardware_threads() { return static_cast<int>(std::thread::hardware_concurrency()); }
 
 // buildCentralised (centralised.hpp:54): dims[6] = {S, R, nnz, initial, rewardFinite, 2n}

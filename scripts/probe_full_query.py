@@ -1,0 +1,42 @@
+"""Dev probe: one full point-oriented query (to convergence or a cap) on a large workload,
+printing per-iteration progress, the verdict and the phase split.
+
+    python scripts/probe_full_query.py c4 [cap]
+"""
+import json
+import sys
+import time
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+from paper_2305_04397_b200.api import Instance, Solver  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c4"
+cap = int(sys.argv[2]) if len(sys.argv) > 2 else 500
+cfg, thr, eps, K = bench.workload(name)
+s = Solver(0)
+t = time.time()
+if name in bench.STREAMED:
+    s.set_lean(True)
+    inst = Instance.warehouse_streamed(cfg, s, chunk=bench.STREAMED[name])
+else:
+    inst = Instance.warehouse(cfg)
+    if K > 2:
+        inst.add_objectives(K, seed=7)
+    s.upload(inst)
+print("build+upload", round(time.time() - t, 2), "s", inst.distinct, "products", inst.total_nnz, "nnz", flush=True)
+t = time.time()
+r = s.pareto(inst, thr, eps=eps, iteration_cap=cap)
+q = time.time() - t
+it = r["iterations"]
+print(json.dumps({"workload": name, "query_s": q, "iterations": len(it), "converged": r["converged"],
+                  "feasible": r["feasible"], "s_per_iteration": q / max(len(it), 1), "stats": r["stats"],
+                  }), flush=True)
+# the supporting points of every iteration, for an offline replay of the sandwich loop
+# (scripts/replay_sandwich.py: same weight sequence from the reference's geometry)
+import numpy as np  # noqa: E402
+np.savez_compressed(f"gpurun_out/report_{name}.npz", thresholds=np.array(r["thresholds"]),
+                    w=np.array([x["w"] for x in it]), r=np.array([x["r"] for x in it]),
+                    assignment=np.array([x["assignment"] for x in it], dtype=np.int32),
+                    tUp=np.array(r["tUp"]), tDown=np.array(r["tDown"]), lambdaStar=np.array(r["lambdaStar"]),
+                    eps=eps, n=cfg["n"], converged=r["converged"], feasible=r["feasible"])
