@@ -204,43 +204,66 @@ def cpu_baseline(cfg, n):
                       f"{backups:.3e} backups"}
 
 
+REF_BUDGET_S = float(os.environ.get("MORAP_REF_BUDGET_S", "150"))  # timed reference queries per run
+
+
 def run_reference(args):
+    """--impl reference: the reference's own paretoPoint (solver.hpp:281, oracle/_ref built
+    from /root/reference) on the same instance and query as our arm, on all host threads.
+    A step is one whole query (the reference bench verb's solveSeconds, cli.hpp:304-315:
+    instance build excluded). value = the query's nnz backups (optimize sweeps x nnz +
+    evaluate sweeps x states, counted once on the reference engine, untimed) / query
+    seconds -- the same units as our arm. The run is bounded: one warm-up query, then as
+    many of the --steps queries as fit in REF_BUDGET_S seconds (at least one)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
     world = int(os.environ.get("WORLD_SIZE", "1"))
     cfg, thr, eps, K = workload(args.workload, world)
-    cfg, what = cpu_sample(cfg)
-    n = cfg["n"]
-    line = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True}
+    line = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "warmup": args.warmup,
+            "higher_is_better": True}
     if not oracle.ref_available():
         line["unavailable"] = "oracle/_ref/libmorap_ref.so was not built (needs /root/reference at build time)"
         print(json.dumps(line))
         return
+    if K != 2 or cfg["n"] > 50:
+        line["unavailable"] = (f"the reference has no K={K} objectives" if K != 2 else
+                               f"the reference cannot hold the {cfg['n']}x{cfg['n']} instance in host memory")
+        print(json.dumps(line))
+        return
     ref = oracle.ref()
+    n = cfg["n"]
     t0 = time.time()
     inst = ref.warehouse(cfg)
     gen = time.time() - t0
-    w = np.full(2 * n, 1.0 / (2 * n))
-    for _ in range(args.warmup):
-        inst.optimize_phase(w, 0)
-    secs, bks = [], []
-    for _ in range(args.steps):
-        s, b = inst.optimize_phase(w, 0)
-        secs.append(s)
-        bks.append(b)
-    value = sum(bks) / sum(secs)
     threads = ref.hardware_threads()
+    rep = inst.pareto(thr, eps=eps, workers=0)  # warm-up query (its report gives the work count)
+    first_s = rep["seconds"]
+    ob, eb = inst.query_backups(rep, workers=0)
+    backups = ob + eb
+    steps = max(1, min(args.steps, int(REF_BUDGET_S // max(first_s, 1e-3))))
+    secs = []
+    for _ in range(steps):
+        r = inst.pareto(thr, eps=eps, workers=0)
+        assert r["tDown"] == rep["tDown"] and len(r["iterations"]) == len(rep["iterations"])
+        secs.append(r["seconds"])
+    q = sum(secs) / len(secs)
+    value = backups / q
     line.update({
-        "value": value, "ms_per_step": 1e3 * sum(secs) / len(secs), "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded warehouse generator, warehouse.hpp:176)",
-        "config": {"workload": args.workload, "grid": [cfg["W"], cfg["H"]], "agents": n, "tasks": n, "objectives": 2,
-                   "step": f"one optimize phase of supportingPoint (n^2 jobs, runBatch) at uniform w on {what}",
-                   "generate_s": gen},
+        "value": value, "steps": steps, "ms_per_step": 1e3 * q, "pareto_query_ms": 1e3 * q, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded warehouse generator, warehouse.hpp:176)",
+        "config": {"workload": args.workload, "grid": [cfg["W"], cfg["H"]], "agents": n, "tasks": n, "objectives": K,
+                   "eps": eps, "thresholds": f"costs {thr[0]} x{n}, probs {thr[-1]}",
+                   "feasible": rep["feasible"], "pareto_iterations": len(rep["iterations"]),
+                   "step": "one paretoPoint query (solver.hpp:281) on the reference's CPU engine, instance build "
+                           "excluded (cli.hpp:304-315 solveSeconds)",
+                   "steps_requested": args.steps, "bounded": f"{steps} timed queries within {REF_BUDGET_S:.0f} s",
+                   "generate_s": round(gen, 3)},
+        "backups_per_query": {"optimize": ob, "evaluate_states": eb},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{args.steps} optimize phases of {n * n} jobs on {threads} host threads"},
+                         "sample": f"{steps} whole paretoPoint queries ({len(rep['iterations'])} iterations of "
+                                   f"{n * n} optimize + {2 * n} evaluate jobs) on {threads} host threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     })
     print(json.dumps(line))

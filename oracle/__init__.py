@@ -216,6 +216,20 @@ class RefInstance:
                                                    a.ctypes.data_as(v), C.byref(sec)))
         return r, a, sec.value
 
+    def query_backups(self, report, workers=0):
+        """Backups of a recorded query on the reference engine (ref_query_backups):
+        (optimize sweeps x nnz, evaluate sweeps x states), summed over its iterations."""
+        its = report["iterations"]
+        w = np.ascontiguousarray([it["w"] for it in its], np.float64)
+        a = np.ascontiguousarray([it["assignment"] for it in its], np.int32)
+        ob, eb = C.c_double(), C.c_double()
+        self._lib.ref_query_backups.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                                C.c_void_p]
+        rc = self._lib.ref_query_backups(self._h, w.ctypes.data_as(C.c_void_p), a.ctypes.data_as(C.c_void_p),
+                                         len(its), workers, C.byref(ob), C.byref(eb))
+        self._check(rc)
+        return ob.value, eb.value
+
     def pareto(self, thresholds, eps=0.01, norm=None, workers=0, iter_cap=500, verify=False):
         t = np.ascontiguousarray(thresholds, dtype=np.float64)
         nm = None if norm is None else np.ascontiguousarray(norm, dtype=np.float64)

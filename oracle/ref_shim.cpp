@@ -327,6 +327,71 @@ int ref_optimize_phase(void* p, const double* w, int workers, double* seconds, d
   });
 }
 
+// Work of a recorded Pareto query, counted on the reference engine (untimed): for every
+// iteration, the supportingPoint jobs (solver.hpp:110-171) at that iteration's w and
+// assignment through runBatch; optimize backups = sweeps x nnz, evaluate state backups =
+// sweeps x states (the units bench.py's `value` counts). w: iters x 2n, agentOf: iters x n.
+int ref_query_backups(void* p, const double* wAll, const int* agentOfAll, int iters, int workers, double* optBackups,
+                      double* evalBackups) {
+  return guarded([&] {
+    const MorapInstance& inst = static_cast<Handle*>(p)->inst;
+    const int n = inst.n;
+    PoolConfig pool = configurePool(workers > 0 ? workers : defaultWorkerCount());
+    double ob = 0.0, eb = 0.0;
+    for (int it = 0; it < iters; ++it) {
+      const double* w = wAll + static_cast<size_t>(it) * 2 * n;
+      using Key = std::tuple<uintptr_t, uint64_t, uint64_t>;
+      std::map<Key, long> jobOf;
+      std::vector<Job> jobs;
+      std::vector<double> nnzOf;
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+          const auto& m = inst.products[i][j];
+          Key k{reinterpret_cast<uintptr_t>(m.get()), solverdetail::doubleBits(w[i]),
+                solverdetail::doubleBits(w[n + j])};
+          if (jobOf.count(k)) continue;
+          Job job;
+          job.id = static_cast<long>(jobs.size());
+          job.kind = JobKind::Optimize;
+          job.model = m;
+          job.reward = weightedReward({&m->cost, &m->success}, {w[i], w[n + j]});
+          jobOf.emplace(k, job.id);
+          nnzOf.push_back(static_cast<double>(m->mdp.succ.size()));
+          jobs.push_back(std::move(job));
+        }
+      auto opt = runBatch(std::move(jobs), pool);
+      for (auto& [id, r] : opt) {
+        if (!r.ok) solverdetail::rethrowJobFailure(r, "optimize");
+        ob += static_cast<double>(r.stats.sweeps) * nnzOf[id];
+      }
+      std::vector<Job> ev;
+      std::vector<double> statesOf;
+      for (int j = 0; j < n; ++j) {
+        const int i = agentOfAll[static_cast<size_t>(it) * n + j];
+        const auto& m = inst.products[i][j];
+        Key k{reinterpret_cast<uintptr_t>(m.get()), solverdetail::doubleBits(w[i]), solverdetail::doubleBits(w[n + j])};
+        for (int which = 0; which < 2; ++which) {
+          Job job;
+          job.id = 2 * j + which;
+          job.kind = JobKind::Evaluate;
+          job.model = m;
+          job.scheduler = opt.at(jobOf.at(k)).policy;
+          job.reward = which ? m->success : m->cost;
+          ev.push_back(std::move(job));
+        }
+        statesOf.push_back(static_cast<double>(m->mdp.numStates));
+      }
+      auto er = runBatch(std::move(ev), pool);
+      for (auto& [id, r] : er) {
+        if (!r.ok) solverdetail::rethrowJobFailure(r, "evaluate");
+        eb += static_cast<double>(r.stats.sweeps) * statesOf[id / 2];
+      }
+    }
+    *optBackups = ob;
+    *evalBackups = eb;
+  });
+}
+
 // Full supportingPoint (solver.hpp:103) on the reference engine.
 int ref_supporting_point(void* p, const double* w, int workers, double* r_out, int* agentOf, double* seconds) {
   return guarded([&] {

@@ -289,10 +289,10 @@ class Solver:
     def cuda_stats(self) -> dict:
         from .cuda import load_library
         lib = load_library()
-        out = np.zeros(11)
-        lib.morap_cuda_stats(self.cuda_ctx, _ptr(out), 11)
+        out = np.zeros(12)
+        lib.morap_cuda_stats(self.cuda_ctx, _ptr(out), 12)
         keys = ["opt_launches", "opt_ms", "opt_bytes", "opt_backups", "eval_launches", "eval_ms", "eval_bytes",
-                "eval_state_backups", "kernels", "upload_bytes", "opt_exec_backups"]
+                "eval_state_backups", "kernels", "upload_bytes", "opt_exec_backups", "d2h_bytes"]
         return dict(zip(keys, out.tolist()))
 
     def reset_cuda_stats(self):

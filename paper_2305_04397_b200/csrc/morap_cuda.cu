@@ -125,6 +125,8 @@ struct OptJob {
   unsigned long long bytesPerSweep;  // the model's (stats)
   int32_t nnz;
   int32_t outBase;  // this job's slice of the batch's absolute out-group list (k_build_cand)
+  int32_t candBase;  // this job's first candidate record (k_build_cand order), dataflow batches
+  int32_t pad;
 };
 
 struct EvalJob {
@@ -1163,6 +1165,150 @@ struct alignas(16) CmpInfo {
   const double* rho;
 };
 
+// One tile of a compact optimize sweep (numerics.hpp:84-113), thread per state: the tile's
+// streams are staged at `st`; returns |y - x| of this thread's state (0 for done states and
+// idle threads). POLICY: record the argmax row instead of writing y. `k` is the sweep being
+// run (stamps of changed states become k + 1, frozen-tile skipping).
+template <bool POLICY>
+__device__ __forceinline__ double cmp_tile(const CmpInfo& v, unsigned char* st, int tid, int k) {
+  double dl = 0.0;
+  const double* __restrict__ x = v.x;
+  if (v.fits && g_dryRun) {
+    // diagnostics: stream only
+  } else if (v.fits) {
+    // Tile-relative u16 row ends per state: state i owns rows [rowE[i-1], rowE[i]) (0 for
+    // i = 0). One u32 word per row: transition end (tile-relative, bits 0-10) and reward
+    // class (bits 11-31); one u32 word per transition: window offset (low 16 bits, 0xFFFF
+    // outside the window) and probability index (bits 16-23) -- one shared-memory load
+    // each instead of two (the compute warps are bound by shared-memory wavefronts).
+    // Padded per-tile streams: every slice starts at offset 0 of its region.
+    // one u32 word per state: row end (bits 0-9), transition end (bits 10-20), done (bit 21)
+    const uint32_t* stW = reinterpret_cast<const uint32_t*>(st + kCOffRow);
+    const uint32_t* rowW = reinterpret_cast<const uint32_t*>(st + kCOffTrn);
+    const uint32_t* trW = reinterpret_cast<const uint32_t*>(st + kCOffSucc);
+    const double* xS = reinterpret_cast<const double*>(st + kCOffX) + v.offX;
+    const double* xwS = reinterpret_cast<const double*>(st + kCOffXw);  // even wlo: no front offset
+    if (tid < v.ns) {
+      const int s = v.s0 + tid;
+      const uint32_t w0 = tid ? stW[tid - 1] : 0u, w1 = stW[tid];
+      const int rb = static_cast<int>(w0 & 0x3FFu), re = static_cast<int>(w1 & 0x3FFu);
+      if (w1 >> 21) {  // done state
+        if (POLICY) v.policy[s] = v.r0 + rb;  // numerics.hpp:114-115
+      } else {
+        double best = 0.0;
+        int bestRow = -1;
+        int kb = static_cast<int>((w0 >> 10) & 0x7FFu);
+        const double* __restrict__ dict = v.dict;
+        const double* __restrict__ crho = v.classRho;
+        auto term = [&](uint32_t w) { return __dmul_rn(__ldg(dict + (w >> 16)), xwS[w & 0xFFFFu]); };
+        if (v.allIn && v.simple && re > rb) {
+          // every successor in the window, at most two transitions per row: straight-line
+          // rows, the first one peeled so the max needs no "no row yet" test
+          auto row = [&](int r, int& k) {
+            const uint32_t rw = rowW[r];
+            const int ke = static_cast<int>(rw & 0x7FFu);
+            double acc = __ldg(crho + (rw >> 11));
+            if (k < ke) acc = __dadd_rn(acc, term(trW[k]));
+            if (k + 1 < ke) acc = __dadd_rn(acc, term(trW[k + 1]));
+            k = ke;
+            return acc;
+          };
+          best = row(rb, kb);
+          bestRow = rb;
+#pragma unroll 1
+          for (int r = rb + 1; r < re; ++r) {
+            const double acc = row(r, kb);
+            if (acc > best) {
+              best = acc;
+              bestRow = r;
+            }
+          }
+        } else if (v.allIn) {  // every successor inside the staged window: no out-of-window test
+#pragma unroll 1
+          for (int r = rb; r < re; ++r) {
+            const uint32_t rw = rowW[r];
+            const int ke = static_cast<int>(rw & 0x7FFu);
+            double acc = __ldg(crho + (rw >> 11));
+#pragma unroll 1
+            for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, term(trW[q]));
+            kb = ke;
+            if (bestRow < 0 || acc > best) {
+              best = acc;
+              bestRow = r;
+            }
+          }
+        } else {
+          auto xAt = [&](int q, uint32_t w) {  // window offset staged; absolute successor only outside it
+            const unsigned o = w & 0xFFFFu;
+            return o != 0xFFFFu ? xwS[o] : __ldg(x + __ldg(v.succG + v.k0 + q));
+          };
+          for (int r = rb; r < re; ++r) {
+            const uint32_t rw = rowW[r];
+            const int ke = static_cast<int>(rw & 0x7FFu);
+            double acc = __ldg(crho + (rw >> 11));
+            for (int q = kb; q < ke; ++q) {
+              const uint32_t w = trW[q];
+              acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + (w >> 16)), xAt(q, w)));
+            }
+            kb = ke;
+            if (bestRow < 0 || acc > best) {
+              best = acc;
+              bestRow = r;
+            }
+          }
+        }
+        if (POLICY) {
+          v.policy[s] = v.r0 + bestRow;
+        } else {
+          const double xo = xS[tid];
+          v.y[s] = best;
+          dl = fabs(__dsub_rn(best, xo));
+          // bitwise change (not |y - x| > 0: -0.0 and +0.0 differ for the skip invariant)
+          if (v.stamp && __double_as_longlong(best) != __double_as_longlong(xo)) v.stamp[s >> 5] = k + 1;
+        }
+      }
+    }
+  } else {
+    // oversized single-state tile from global memory (stage slot reused as scratch)
+    const DevModel& M = *v.model;
+    int32_t* sRow = reinterpret_cast<int32_t*>(st + kCOffRow);
+    double* sVal = reinterpret_cast<double*>(st + kCOffXw);
+    for (int i = tid; i <= v.ns; i += kConsumers) sRow[i] = M.rowOffset[v.s0 + i];
+    consumer_sync();
+    const int r0 = sRow[0];
+    const int nr = sRow[v.ns] - r0;
+    const int nstage = min(nr, kCFbRows);
+    for (int i = tid; i < nstage; i += kConsumers) sVal[i] = row_value_cmp(M, v.classRho, x, r0 + i);
+    consumer_sync();
+    if (tid < v.ns) {
+      const int s = v.s0 + tid;
+      const int rb = sRow[tid] - r0, re = sRow[tid + 1] - r0;
+      if (M.done[s]) {
+        if (POLICY) v.policy[s] = r0 + rb;
+      } else {
+        double best = 0.0;
+        int bestRow = -1;
+        for (int q = rb; q < re; ++q) {
+          const double val = q < kCFbRows ? sVal[q] : row_value_cmp(M, v.classRho, x, r0 + q);
+          if (bestRow < 0 || val > best) {
+            best = val;
+            bestRow = q;
+          }
+        }
+        if (POLICY) {
+          v.policy[s] = r0 + bestRow;
+        } else {
+          const double xo = x[s];
+          v.y[s] = best;
+          dl = fabs(__dsub_rn(best, xo));
+          if (v.stamp && __double_as_longlong(best) != __double_as_longlong(xo)) v.stamp[s >> 5] = k + 1;
+        }
+      }
+    }
+  }
+  return dl;
+}
+
 template <bool POLICY>
 __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cmp(const DevModel* __restrict__ models,
                                                                      const OptJob* __restrict__ jobs,
@@ -1383,142 +1529,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
       runMax = 0.0;
       runJob = v.job;
     }
-    double dl = 0.0;
-    unsigned char* st = smem + b * kCStageBytes;
-    const double* __restrict__ x = v.x;
-    if (v.fits && g_dryRun) {
-      // diagnostics: stream only
-    } else if (v.fits) {
-      // Tile-relative u16 row ends per state: state i owns rows [rowE[i-1], rowE[i]) (0 for
-      // i = 0). One u32 word per row: transition end (tile-relative, bits 0-10) and reward
-      // class (bits 11-31); one u32 word per transition: window offset (low 16 bits, 0xFFFF
-      // outside the window) and probability index (bits 16-23) -- one shared-memory load
-      // each instead of two (the compute warps are bound by shared-memory wavefronts).
-      // Padded per-tile streams: every slice starts at offset 0 of its region.
-      // one u32 word per state: row end (bits 0-9), transition end (bits 10-20), done (bit 21)
-      const uint32_t* stW = reinterpret_cast<const uint32_t*>(st + kCOffRow);
-      const uint32_t* rowW = reinterpret_cast<const uint32_t*>(st + kCOffTrn);
-      const uint32_t* trW = reinterpret_cast<const uint32_t*>(st + kCOffSucc);
-      const double* xS = reinterpret_cast<const double*>(st + kCOffX) + v.offX;
-      const double* xwS = reinterpret_cast<const double*>(st + kCOffXw);  // even wlo: no front offset
-      if (tid < v.ns) {
-        const int s = v.s0 + tid;
-        const uint32_t w0 = tid ? stW[tid - 1] : 0u, w1 = stW[tid];
-        const int rb = static_cast<int>(w0 & 0x3FFu), re = static_cast<int>(w1 & 0x3FFu);
-        if (w1 >> 21) {  // done state
-          if (POLICY) v.policy[s] = v.r0 + rb;  // numerics.hpp:114-115
-        } else {
-          double best = 0.0;
-          int bestRow = -1;
-          int kb = static_cast<int>((w0 >> 10) & 0x7FFu);
-          const double* __restrict__ dict = v.dict;
-          const double* __restrict__ crho = v.classRho;
-          auto term = [&](uint32_t w) { return __dmul_rn(__ldg(dict + (w >> 16)), xwS[w & 0xFFFFu]); };
-          if (v.allIn && v.simple && re > rb) {
-            // every successor in the window, at most two transitions per row: straight-line
-            // rows, the first one peeled so the max needs no "no row yet" test
-            auto row = [&](int r, int& k) {
-              const uint32_t rw = rowW[r];
-              const int ke = static_cast<int>(rw & 0x7FFu);
-              double acc = __ldg(crho + (rw >> 11));
-              if (k < ke) acc = __dadd_rn(acc, term(trW[k]));
-              if (k + 1 < ke) acc = __dadd_rn(acc, term(trW[k + 1]));
-              k = ke;
-              return acc;
-            };
-            best = row(rb, kb);
-            bestRow = rb;
-#pragma unroll 1
-            for (int r = rb + 1; r < re; ++r) {
-              const double acc = row(r, kb);
-              if (acc > best) {
-                best = acc;
-                bestRow = r;
-              }
-            }
-          } else if (v.allIn) {  // every successor inside the staged window: no out-of-window test
-#pragma unroll 1
-            for (int r = rb; r < re; ++r) {
-              const uint32_t rw = rowW[r];
-              const int ke = static_cast<int>(rw & 0x7FFu);
-              double acc = __ldg(crho + (rw >> 11));
-#pragma unroll 1
-              for (int q = kb; q < ke; ++q) acc = __dadd_rn(acc, term(trW[q]));
-              kb = ke;
-              if (bestRow < 0 || acc > best) {
-                best = acc;
-                bestRow = r;
-              }
-            }
-          } else {
-            auto xAt = [&](int q, uint32_t w) {  // window offset staged; absolute successor only outside it
-              const unsigned o = w & 0xFFFFu;
-              return o != 0xFFFFu ? xwS[o] : __ldg(x + __ldg(v.succG + v.k0 + q));
-            };
-            for (int r = rb; r < re; ++r) {
-              const uint32_t rw = rowW[r];
-              const int ke = static_cast<int>(rw & 0x7FFu);
-              double acc = __ldg(crho + (rw >> 11));
-              for (int q = kb; q < ke; ++q) {
-                const uint32_t w = trW[q];
-                acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + (w >> 16)), xAt(q, w)));
-              }
-              kb = ke;
-              if (bestRow < 0 || acc > best) {
-                best = acc;
-                bestRow = r;
-              }
-            }
-          }
-          if (POLICY) {
-            v.policy[s] = v.r0 + bestRow;
-          } else {
-            const double xo = xS[tid];
-            v.y[s] = best;
-            dl = fabs(__dsub_rn(best, xo));
-            // bitwise change (not |y - x| > 0: -0.0 and +0.0 differ for the skip invariant)
-            if (v.stamp && __double_as_longlong(best) != __double_as_longlong(xo)) v.stamp[s >> 5] = k + 1;
-          }
-        }
-      }
-    } else {
-      // oversized single-state tile from global memory (stage slot reused as scratch)
-      const DevModel& M = *v.model;
-      int32_t* sRow = reinterpret_cast<int32_t*>(st + kCOffRow);
-      double* sVal = reinterpret_cast<double*>(st + kCOffXw);
-      for (int i = tid; i <= v.ns; i += kConsumers) sRow[i] = M.rowOffset[v.s0 + i];
-      consumer_sync();
-      const int r0 = sRow[0];
-      const int nr = sRow[v.ns] - r0;
-      const int nstage = min(nr, kCFbRows);
-      for (int i = tid; i < nstage; i += kConsumers) sVal[i] = row_value_cmp(M, v.classRho, x, r0 + i);
-      consumer_sync();
-      if (tid < v.ns) {
-        const int s = v.s0 + tid;
-        const int rb = sRow[tid] - r0, re = sRow[tid + 1] - r0;
-        if (M.done[s]) {
-          if (POLICY) v.policy[s] = r0 + rb;
-        } else {
-          double best = 0.0;
-          int bestRow = -1;
-          for (int q = rb; q < re; ++q) {
-            const double val = q < kCFbRows ? sVal[q] : row_value_cmp(M, v.classRho, x, r0 + q);
-            if (bestRow < 0 || val > best) {
-              best = val;
-              bestRow = q;
-            }
-          }
-          if (POLICY) {
-            v.policy[s] = r0 + bestRow;
-          } else {
-            const double xo = x[s];
-            v.y[s] = best;
-            dl = fabs(__dsub_rn(best, xo));
-            if (v.stamp && __double_as_longlong(best) != __double_as_longlong(xo)) v.stamp[s >> 5] = k + 1;
-          }
-        }
-      }
-    }
+    const double dl = cmp_tile<POLICY>(v, smem + b * kCStageBytes, tid, k);
     runMax = fmax(runMax, dl);
     __syncwarp();  // this warp is done with stage b (warps drift apart up to the pipeline depth)
     if (lane == 0) mbar_arrive(&empty[b]);
@@ -1565,6 +1576,8 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     }
   }
 }
+
+#include "opt_flow.cuh"
 
 // --------------------------------------------------------------------------------------
 // Policy chain: a fixed deterministic scheduler turns the product into a Markov chain
@@ -2402,7 +2415,7 @@ struct morap_ctx {
   std::string err;
   bool profiling = false;
   bool trace = std::getenv("MORAP_TRACE") != nullptr;
-  double stats[11] = {0};
+  double stats[12] = {0};  // [11]: device-to-host bytes copied
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   std::vector<HostModel> hm;
@@ -2477,6 +2490,7 @@ struct morap_ctx {
   bool lean = false;       // compact models uploaded without their fp64 prob / objective arrays
   bool optCompact = false; // current optimize batch runs the deep compact pipeline
   int cmpBlocks = 0;
+  int flowBlocks = 0;
   bool skip = true;        // frozen-tile skipping in compact optimize sweeps (k_select)
   // profiling: the events bracket the sweep kernel alone (k_select outside); MORAP_TIME_SELECT=1
   // brackets k_select + sweep
@@ -2503,6 +2517,16 @@ struct morap_ctx {
   size_t polStageBytes = 0;
   Ctl* dCtl = nullptr;
   Ctl* hCtl = nullptr;  // pinned mirror
+  // dataflow optimize batches (k_opt_flow, opt_flow.cuh); MORAP_FLOW=0: lock-step sweeps
+  bool useFlow = std::getenv("MORAP_FLOW") == nullptr || std::getenv("MORAP_FLOW")[0] != '0';
+  bool optFlow = false;  // current optimize batch ran as one dataflow launch
+  unsigned long long* dRing = nullptr;
+  size_t ringCap = 0;
+  int32_t* dJobSweep = nullptr;
+  int32_t* dPending = nullptr;
+  size_t flowJobsCap = 0;
+  FlowCtl* dFlow = nullptr;
+  FlowCtl* hFlow = nullptr;  // pinned mirror
   void* dEvalJobsRaw = nullptr;
   size_t dEvalJobsCap = 0;
   size_t dOptJobsCap = 0;
@@ -2519,6 +2543,14 @@ struct morap_ctx {
 };
 
 namespace {
+
+// Every device-to-host copy of the library goes through here and is counted (stats[11]),
+// so the end-to-end bench reports the D2H bytes it actually moved.
+cudaError_t d2h(morap_ctx* ctx, void* dst, const void* src, size_t bytes, bool sync = false) {
+  ctx->stats[11] += static_cast<double>(bytes);
+  return sync ? cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)
+              : cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+}
 
 int ensure_ctl(morap_ctx* ctx, size_t njobs) {
   if (njobs <= ctx->ctlCap && ctx->dCtl) return MORAP_OK;
@@ -3129,7 +3161,7 @@ int run_loop(morap_ctx* ctx, int kind, double eps, int cap) {
       if ((rc = enqueue_sweeps(ctx, kind, eps, cap, batch, timed ? ctx->evPool.data() : nullptr, false))) return rc;
     }
     ctx->stats[8] += (kind == 0 && ctx->useTma && ctx->optCompact ? (ctx->optSkip ? 2 : 1) : 2) * batch;
-    CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(d2h(ctx, ctx->hCtl, ctx->dCtl, sizeof(Ctl)));
     CK(cudaStreamSynchronize(ctx->stream));
     if (timed) {
       const int worked = ctx->hCtl->sweepsDone - before;
@@ -3161,6 +3193,104 @@ int init_ctl(morap_ctx* ctx, const std::vector<int32_t>& active, const std::vect
   c.sweepsDone = 0;
   *ctx->hCtl = c;
   CK(cudaMemcpyAsync(ctx->dCtl, ctx->hCtl, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+  return MORAP_OK;
+}
+
+// One dataflow launch for the whole optimize batch (k_opt_flow): seeds the ring with every
+// active job's sweep-0 items, launches, waits once. Values, policies, sweeps and residuals
+// are those of the lock-step loop (same tiles, same arithmetic, same stop tests).
+int run_flow(morap_ctx* ctx, const std::vector<int32_t>& active, const std::vector<int32_t>& jobModel, double eps,
+             int cap) {
+  const int njobs = static_cast<int>(jobModel.size());
+  const int seg = flow_seg(static_cast<int>(active.size()));
+  std::vector<unsigned long long> items;
+  std::vector<int32_t> pend(njobs, 0);
+  size_t worst = 0;  // items one sweep of every job can need (smallest segments)
+  for (int j : active) {
+    const int nt = ctx->hm[jobModel[j]].ntiles;
+    const int nseg = (nt + seg - 1) / seg;
+    pend[j] = nseg;
+    for (int q = 0; q < nseg; ++q) {
+      const int lt0 = q * seg, cnt = std::min(seg, nt - lt0);
+      items.push_back((1ull << 48) | (static_cast<unsigned long long>(j) << 25) |
+                      (static_cast<unsigned long long>(lt0) << 5) | static_cast<unsigned long long>(cnt - 1));
+    }
+    worst += static_cast<size_t>((nt + 1) / 2);  // flow_seg's smallest items
+  }
+  // capacity: a power of two >= 4x what one sweep of every job can queue (a reader never lags
+  // a whole lap; an overrun is detected and reported, never silently wrong)
+  size_t capNeed = 1024;  // + the positions CTAs claim ahead (two each)
+  while (capNeed < 4 * (std::max(worst, items.size()) + 2 * static_cast<size_t>(ctx->flowBlocks))) capNeed <<= 1;
+  int logCap = 0;
+  while ((1ull << logCap) < capNeed) ++logCap;
+  if (capNeed > ctx->ringCap) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(ctx->dRing);
+    ctx->dRing = nullptr;
+    ctx->ringCap = 0;
+    CK(cudaMalloc(&ctx->dRing, capNeed * sizeof(unsigned long long)));
+    ctx->ringCap = capNeed;
+  }
+  if (static_cast<size_t>(njobs) > ctx->flowJobsCap) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(ctx->dJobSweep);
+    cudaFree(ctx->dPending);
+    ctx->dJobSweep = ctx->dPending = nullptr;
+    ctx->flowJobsCap = std::max<size_t>(njobs, 256);
+    CK(cudaMalloc(&ctx->dJobSweep, ctx->flowJobsCap * sizeof(int32_t)));
+    CK(cudaMalloc(&ctx->dPending, ctx->flowJobsCap * sizeof(int32_t)));
+  }
+  if (!ctx->dFlow) {
+    CK(cudaMalloc(&ctx->dFlow, sizeof(FlowCtl)));
+    CK(cudaMallocHost(&ctx->hFlow, sizeof(FlowCtl)));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));  // the pinned mirror and `items` are reused below
+  CK(cudaMemsetAsync(ctx->dRing, 0, capNeed * sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dRing, items.data(), items.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemsetAsync(ctx->dJobSweep, 0, njobs * sizeof(int32_t), ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dPending, pend.data(), njobs * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+  FlowCtl f{};
+  f.tail = items.size();
+  f.remaining = static_cast<int32_t>(active.size());
+  *ctx->hFlow = f;
+  CK(cudaMemcpyAsync(ctx->dFlow, ctx->hFlow, sizeof(FlowCtl), cudaMemcpyHostToDevice, ctx->stream));
+  FlowArgs A{};
+  A.models = ctx->dModels;
+  A.jobs = ctx->dOptJobs;
+  A.cand = ctx->dCand;
+  A.candOut = ctx->dCandOut;
+  A.candOutG = ctx->dCandOutG;
+  A.stampAll = ctx->dStampAll;
+  A.ring = ctx->dRing;
+  A.mask = capNeed - 1;
+  A.logCap = logCap;
+  A.skip = ctx->optSkip ? 1 : 0;
+  A.fc = ctx->dFlow;
+  A.jobSweep = ctx->dJobSweep;
+  A.pending = ctx->dPending;
+  A.delta = ctx->dDelta;
+  A.eps = eps;
+  A.cap = cap;
+  A.sweeps = ctx->dSweeps;
+  A.residual = ctx->dResidual;
+  A.status = ctx->dStatus;
+  if (ctx->profiling) CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  k_opt_flow<<<ctx->flowBlocks, kTmaThreads, kCmpSmemBytes, ctx->stream>>>(A);
+  CK(cudaGetLastError());
+  if (ctx->profiling) CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->stats[8] += 1;
+  CK(d2h(ctx, ctx->hFlow, ctx->dFlow, sizeof(FlowCtl)));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->hFlow->err)
+    return ctx->fail(MORAP_CUDA_ERROR, ctx->hFlow->err == 1 ? "dataflow optimize: work queue stalled (watchdog)"
+                                                            : "dataflow optimize: work ring overrun");
+  if (ctx->profiling) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    ctx->stats[1] += ms;
+  }
+  ctx->stats[0] += 1;  // launches of the dominant kernel
   return MORAP_OK;
 }
 
@@ -3258,6 +3388,7 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   if (ctx->optSkip) {
     size_t tiles = 0, outs = 0;
     for (int j : active) {
+      ctx->hOptJobs[j].candBase = static_cast<int32_t>(tiles);  // k_build_cand's prefix (init_ctl order)
       tiles += static_cast<size_t>(ctx->hm[model_ids[j]].ntiles);
       ctx->hOptJobs[j].outBase = static_cast<int32_t>(outs);
       outs += static_cast<size_t>(ctx->hm[model_ids[j]].nOutGrp);
@@ -3331,8 +3462,18 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     CK(cudaGetLastError());
     ctx->stats[8] += 1;
   }
-  if (!active.empty())
-    if ((rc = run_loop(ctx, 0, eps, cap))) return rc;
+  // dataflow batch (one launch, jobs advance independently) when every job runs the compact
+  // kernel and the work-item encoding fits (jobs < 2^22, tiles per model < 2^20)
+  ctx->optFlow = ctx->useFlow && allCompact && njobs < (1 << 22);
+  for (int j = 0; j < njobs && ctx->optFlow; ++j)
+    if (ctx->hm[model_ids[j]].ntiles >= (1 << 20)) ctx->optFlow = false;
+  if (!active.empty()) {
+    if (ctx->optFlow) {
+      if ((rc = run_flow(ctx, active, ctx->optModel, eps, cap))) return rc;
+    } else if ((rc = run_loop(ctx, 0, eps, cap))) {
+      return rc;
+    }
+  }
 
   // results: one gather kernel + one copy per array, one synchronisation
   ctx->optSweeps.assign(njobs, 0);
@@ -3341,11 +3482,11 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   k_gather_opt<<<(njobs + 255) / 256, 256, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, njobs, ctx->dSweeps,
                                                              ctx->dGather);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(ctx->optSweeps.data(), ctx->dSweeps, njobs * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->optStatus.data(), ctx->dStatus, njobs * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(resid.data(), ctx->dResidual, njobs * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(vals.data(), ctx->dGather, njobs * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(d2h(ctx, ctx->optSweeps.data(), ctx->dSweeps, njobs * 4));
+  CK(d2h(ctx, ctx->optStatus.data(), ctx->dStatus, njobs * 4));
+  CK(d2h(ctx, resid.data(), ctx->dResidual, njobs * 8));
+  CK(d2h(ctx, vals.data(), ctx->dGather, njobs * 8));
+  CK(d2h(ctx, ctx->hCtl, ctx->dCtl, sizeof(Ctl)));
   CK(cudaStreamSynchronize(ctx->stream));
   double backups = 0;
   for (int j = 0; j < njobs; ++j) {
@@ -3355,12 +3496,17 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     if (status_out) status_out[j] = ctx->optStatus[j];
     backups += static_cast<double>(ctx->optSweeps[j]) * ctx->hm[model_ids[j]].nnz;
   }
-  ctx->stats[0] += ctx->hCtl->sweepsDone;
   // bytes: what the sweeps actually streamed; backups: sweeps x nnz of every job (the
   // reference's work for the same results); [10]: backups actually executed
-  ctx->stats[2] += static_cast<double>(ctx->optSkip ? ctx->hCtl->execBytes : ctx->hCtl->bytes);
+  if (ctx->optFlow && !active.empty()) {  // [0] counted by run_flow (one launch)
+    ctx->stats[2] += static_cast<double>(ctx->hFlow->execBytes);
+    ctx->stats[10] += static_cast<double>(ctx->hFlow->execBackups);
+  } else if (!ctx->optFlow) {
+    ctx->stats[0] += ctx->hCtl->sweepsDone;
+    ctx->stats[2] += static_cast<double>(ctx->optSkip ? ctx->hCtl->execBytes : ctx->hCtl->bytes);
+    ctx->stats[10] += ctx->optSkip ? static_cast<double>(ctx->hCtl->execBackups) : backups;
+  }
   ctx->stats[3] += backups;
-  ctx->stats[10] += ctx->optSkip ? static_cast<double>(ctx->hCtl->execBackups) : backups;
   ctx->optPolicyReady.assign(njobs, 0);
   ctx->optJobs = njobs;
   return MORAP_OK;
@@ -3410,6 +3556,7 @@ int prefetch_policies(morap_ctx* ctx, const std::vector<int32_t>& jobs) {
   for (size_t q = 0; q < jobs.size(); ++q) {
     const size_t n = sizeof(int32_t) * ctx->hm[ctx->optModel[jobs[q]]].S;
     ctx->polOff[q] = o;
+    ctx->stats[11] += static_cast<double>(n);  // counted like d2h()
     CK(cudaMemcpyAsync(static_cast<char*>(ctx->polStage) + o, ctx->hOptJobs[jobs[q]].policy, n, cudaMemcpyDeviceToHost,
                        ctx->side));
     o += align_up(n, 256);
@@ -3461,7 +3608,7 @@ int run_eval_persistent(morap_ctx* ctx, int njobs, double eps, int cap) {
                                  args, a.cacheStates ? cacheBytes : 0, ctx->stream));
   if (timed) CK(cudaEventRecord(ctx->ev1, ctx->stream));
   ctx->stats[8] += 1;
-  CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(d2h(ctx, ctx->hCtl, ctx->dCtl, sizeof(Ctl)));
   CK(cudaStreamSynchronize(ctx->stream));
   if (timed) {
     float ms = 0.f;
@@ -3566,15 +3713,15 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
   ctx->evalSweeps.assign(static_cast<size_t>(njobs) * MORAP_MAX_RHS, 0);
   std::vector<int32_t> st(static_cast<size_t>(njobs) * MORAP_MAX_RHS);
   std::vector<double> res(static_cast<size_t>(njobs) * MORAP_MAX_RHS);
-  CK(cudaMemcpyAsync(ctx->evalSweeps.data(), ctx->dSweeps, njobs * MORAP_MAX_RHS * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(st.data(), ctx->dStatus, njobs * MORAP_MAX_RHS * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(res.data(), ctx->dResidual, njobs * MORAP_MAX_RHS * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(d2h(ctx, ctx->evalSweeps.data(), ctx->dSweeps, njobs * MORAP_MAX_RHS * 4));
+  CK(d2h(ctx, st.data(), ctx->dStatus, njobs * MORAP_MAX_RHS * 4));
+  CK(d2h(ctx, res.data(), ctx->dResidual, njobs * MORAP_MAX_RHS * 8));
   std::vector<double> vals(static_cast<size_t>(njobs) * MORAP_MAX_RHS, 0.0);
   k_gather_eval<<<(njobs * MORAP_MAX_RHS + 255) / 256, 256, 0, ctx->stream>>>(
       ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw, njobs, ctx->dSweeps, ctx->dGather);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(vals.data(), ctx->dGather, njobs * MORAP_MAX_RHS * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->hCtl, ctx->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(d2h(ctx, vals.data(), ctx->dGather, njobs * MORAP_MAX_RHS * 8));
+  CK(d2h(ctx, ctx->hCtl, ctx->dCtl, sizeof(Ctl)));
   CK(cudaStreamSynchronize(ctx->stream));
   double backups = 0;
   size_t q = 0;  // outputs: every job's RHS in order (j * nrhs + o for a uniform batch)
@@ -3636,6 +3783,10 @@ int morap_cuda_create(int device, morap_ctx** out) {
   int occC = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occC, k_greedy_sweep_cmp<false>, kTmaThreads, kCmpSmemBytes);
   ctx->cmpBlocks = ctx->numSMs * std::max(1, occC);
+  cudaFuncSetAttribute(k_opt_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, kCmpSmemBytes);
+  int occF = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occF, k_opt_flow, kTmaThreads, kCmpSmemBytes);
+  ctx->flowBlocks = ctx->numSMs * std::max(1, occF);  // every CTA resident (persistent)
   int occP = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occP, k_eval_persistent, kPersistThreads, 0);
   int coop = 0;
@@ -3735,6 +3886,11 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   cudaFree(ctx->dTrace);
   cudaFree(ctx->dCtl);
   cudaFreeHost(ctx->hCtl);
+  cudaFree(ctx->dRing);
+  cudaFree(ctx->dJobSweep);
+  cudaFree(ctx->dPending);
+  cudaFree(ctx->dFlow);
+  cudaFreeHost(ctx->hFlow);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
   cudaStreamDestroy(ctx->own);
@@ -3996,8 +4152,7 @@ int morap_cuda_fetch_values(morap_ctx* ctx, int job, double* out) {
     std::fill(out, out + m.S, 0.0);
     return MORAP_OK;
   }
-  CK(cudaMemcpyAsync(out, ctx->hOptJobs[job].buf[ctx->optSweeps[job] & 1], sizeof(double) * m.S,
-                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(d2h(ctx, out, ctx->hOptJobs[job].buf[ctx->optSweeps[job] & 1], sizeof(double) * m.S));
   CK(cudaStreamSynchronize(ctx->stream));
   return MORAP_OK;
 }
@@ -4010,7 +4165,7 @@ int morap_cuda_fetch_policy(morap_ctx* ctx, int job, int32_t* out) {
   int rc = extract_policies(ctx, {job});
   if (rc) return rc;
   const HostModel& m = ctx->hm[ctx->optModel[job]];
-  CK(cudaMemcpyAsync(out, ctx->hOptJobs[job].policy, sizeof(int32_t) * m.S, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(d2h(ctx, out, ctx->hOptJobs[job].policy, sizeof(int32_t) * m.S));
   CK(cudaStreamSynchronize(ctx->stream));
   return MORAP_OK;
 }
@@ -4050,8 +4205,7 @@ int morap_cuda_fetch_policies(morap_ctx* ctx, int njobs, const int32_t* jobs, in
   for (int q = 0; q < njobs; ++q) {
     const size_t n = sizeof(int32_t) * ctx->hm[ctx->optModel[list[q]]].S;
     off[q] = o;
-    CK(cudaMemcpyAsync(static_cast<char*>(ctx->polStage) + o, ctx->hOptJobs[list[q]].policy, n, cudaMemcpyDeviceToHost,
-                       ctx->stream));
+    CK(d2h(ctx, static_cast<char*>(ctx->polStage) + o, ctx->hOptJobs[list[q]].policy, n));
     o += align_up(n, 256);
   }
   CK(cudaStreamSynchronize(ctx->stream));
@@ -4159,9 +4313,9 @@ int morap_cuda_evaluate(morap_ctx* ctx, int njobs, const int32_t* model_ids, con
     const HostModel& m = ctx->hm[model];
     // checkScheduler (numerics.hpp:51-66) needs rowOffset; validate against host copy
     std::vector<int32_t> ro(m.S + 1);
-    CK(cudaMemcpy(ro.data(), ctx->dm[model].rowOffset, 4ull * (m.S + 1), cudaMemcpyDeviceToHost));
+    CK(d2h(ctx, ro.data(), ctx->dm[model].rowOffset, 4ull * (m.S + 1), true));
     std::vector<uint8_t> dn(m.S);
-    CK(cudaMemcpy(dn.data(), ctx->dm[model].done, m.S, cudaMemcpyDeviceToHost));
+    CK(d2h(ctx, dn.data(), ctx->dm[model].done, m.S, true));
     bool ok = true;
     for (int s = 0; s < m.S && ok; ++s)
       if (!dn[s] && (policies[j][s] < ro[s] || policies[j][s] >= ro[s + 1])) ok = false;
@@ -4201,7 +4355,7 @@ int morap_cuda_fetch_eval_values(morap_ctx* ctx, int job, int rhs, double* out) 
     std::fill(out, out + m.S, 0.0);
     return MORAP_OK;
   }
-  CK(cudaMemcpyAsync(out, J.buf[rhs][sw & 1], 8ull * m.S, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(d2h(ctx, out, J.buf[rhs][sw & 1], 8ull * m.S));
   CK(cudaStreamSynchronize(ctx->stream));
   return MORAP_OK;
 }
@@ -4228,10 +4382,23 @@ int morap_cuda_debug_cta_trace(morap_ctx* ctx, int enable, uint64_t* out, int64_
   }
   if (out && ctx->dTrace) {
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(out, ctx->dTrace, std::min<size_t>(words, static_cast<size_t>(n)) * 8, cudaMemcpyDeviceToHost));
+    CK(d2h(ctx, out, ctx->dTrace, std::min<size_t>(words, static_cast<size_t>(n)) * 8, true));
   }
   return MORAP_OK;
 }
+
+#ifdef MORAP_FLOW_PROF
+// diagnostics build only: the dataflow kernel's per-CTA wait counters (opt_flow.cuh)
+int morap_cuda_debug_flow_prof(morap_ctx* ctx, unsigned long long* out, int n, int reset) {
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyFromSymbol(out, g_flowProf, sizeof(unsigned long long) * std::min(n, 4096 * 8)));
+  if (reset) {
+    std::vector<unsigned long long> z(4096 * 8, 0);
+    CK(cudaMemcpyToSymbol(g_flowProf, z.data(), z.size() * 8));
+  }
+  return ctx->flowBlocks;
+}
+#endif
 
 int morap_cuda_set_skip(morap_ctx* ctx, int on) {
   if (!ctx) return MORAP_INVALID_CONFIG;
@@ -4247,7 +4414,7 @@ int morap_cuda_set_profiling(morap_ctx* ctx, int on) {
 
 int morap_cuda_stats(morap_ctx* ctx, double* out, int nout) {
   if (!ctx) return MORAP_INVALID_CONFIG;
-  for (int i = 0; i < nout && i < 11; ++i) out[i] = ctx->stats[i];
+  for (int i = 0; i < nout && i < 12; ++i) out[i] = ctx->stats[i];
   return MORAP_OK;
 }
 

@@ -236,10 +236,10 @@ class CudaBackend:
         self._check(self.lib.morap_cuda_set_profiling(self.h, int(on)), "set_profiling")
 
     def stats(self) -> dict:
-        out = np.zeros(11)
-        self._check(self.lib.morap_cuda_stats(self.h, _ptr(out), 11), "stats")
+        out = np.zeros(12)
+        self._check(self.lib.morap_cuda_stats(self.h, _ptr(out), 12), "stats")
         keys = ["opt_launches", "opt_ms", "opt_bytes", "opt_backups", "eval_launches", "eval_ms", "eval_bytes",
-                "eval_state_backups", "kernels", "upload_bytes", "opt_exec_backups"]
+                "eval_state_backups", "kernels", "upload_bytes", "opt_exec_backups", "d2h_bytes"]
         return dict(zip(keys, out.tolist()))
 
     def reset_stats(self):
