@@ -143,65 +143,48 @@ def peak_hbm():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """DRAM bytes / algorithmic bytes of one sweep launch from the committed ncu capture."""
+def ncu_traffic(workload: str):
+    """DRAM bytes / algorithmic bytes of one sweep launch of this workload, from the committed
+    ncu --set full capture (profiles/ncu_traffic.json, one entry per workload)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
-        d = json.load(open(p))
-        return d.get("traffic_over_algorithmic"), d
+        d = json.load(open(p)).get(workload)
+        if d:
+            return d.get("traffic_over_algorithmic"), d
     return None, None
-
-
-def csr_bytes(inst) -> int:
-    """Host->device bytes of one instance upload (distinct products, morap_cuda_upload)."""
-    seen, total = set(), 0
-    for i in range(inst.n):
-        for j in range(inst.n):
-            dims, _ = inst.product_dims(i, j)
-            S, R, nnz, first = int(dims[0]), int(dims[1]), int(dims[2]), int(dims[5])
-            if first in seen:
-                continue
-            seen.add(first)
-            total += 4 * (S + 1) + 4 * (R + 1) + 12 * nnz + S + 8 * R * inst.objectives
-    return total
-
-
-def d2h_bytes(inst, report) -> int:
-    n, K = inst.n, inst.objectives
-    per_iter = 8 * n * n + 8 * K * n + 4 * n
-    pol = 0
-    for it in report["iterations"]:
-        for j, i in enumerate(it["assignment"]):
-            pol += 4 * int(inst.product_dims(i, j)[0][0])
-    return per_iter * len(report["iterations"]) + pol
 
 
 # ------------------------------------------------------------------------------------------
 def cpu_sample(cfg):
     """Bounded CPU sample of a workload: the whole instance when the reference can hold it,
-    else the first 4 agents x 4 tasks of the same grid / racks (same per-product size)."""
+    else the first 4 agents x 4 tasks of the same grid / racks (the same (i, j < 4) products:
+    start poses and tasks do not depend on n, warehouse.hpp:69-84,157-174)."""
     if cfg["n"] <= 50:
         return cfg, "the same instance"
     sub = dict(cfg, n=4)
-    return sub, f"a 4 x 4 sub-instance (agents 0-3, tasks 0-3) of the same {cfg['W']}x{cfg['H']} grid and racks"
+    return sub, f"its 4 x 4 sub-instance (agents 0-3, tasks 0-3: the same products) of the {cfg['W']}x{cfg['H']} grid"
 
 
-def cpu_baseline(cfg, n):
-    """The reference engine (oracle/_ref) on this host, one optimize phase at uniform w."""
+def cpu_baseline(cfg, thr, eps):
+    """The reference's own paretoPoint (oracle/_ref, all host threads) on the same query: one
+    whole query timed (solveSeconds), its backups counted on the reference engine."""
     import oracle
     if not oracle.ref_available():
         return None
     ref = oracle.ref()
-    cfg, what = cpu_sample(cfg)
-    n = cfg["n"]
-    inst = ref.warehouse(cfg)
-    w = np.full(2 * n, 1.0 / (2 * n))
-    sec, backups = inst.optimize_phase(w, 0)
+    sub, what = cpu_sample(cfg)
+    n = sub["n"]
+    if n != cfg["n"]:
+        thr = [thr[0]] * n + [thr[-1]] * n
+    inst = ref.warehouse(sub)
+    rep = inst.pareto(thr, eps=eps, workers=0)
+    ob, eb = inst.query_backups(rep, workers=0)
     threads = ref.hardware_threads()
-    return {"value": backups / sec, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"oracle/_ref runBatch (engine.hpp:370) of the {n * n} optimize jobs of one supportingPoint at "
-                      f"uniform w on {what}, {threads} worker threads, {sec:.2f} s wall, "
-                      f"{backups:.3e} backups"}
+    return {"value": (ob + eb) / rep["seconds"], "unit": UNIT, "cores": threads, "kind": "reference",
+            "pareto_query_ms": 1e3 * rep["seconds"], "pareto_iterations": len(rep["iterations"]),
+            "sample": f"oracle/_ref paretoPoint (solver.hpp:281) on {what}, one whole query "
+                      f"({len(rep['iterations'])} iterations, {rep['seconds']:.2f} s) on {threads} host threads; "
+                      f"backups {ob + eb:.3e} counted on the reference engine"}
 
 
 REF_BUDGET_S = float(os.environ.get("MORAP_REF_BUDGET_S", "150"))  # timed reference queries per run
@@ -317,6 +300,98 @@ def run_centralised(args):
         "cpu_baseline": cpu, "clocks": clk.summary()}))
 
 
+def query_pass(solver, inst, thr, eps, cap, steps, stream, profiling=False):
+    """`steps` paretoPoint queries with the products resident, device-timed on `stream`."""
+    import torch
+    solver.set_profiling(profiling)
+    solver.reset_cuda_stats()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    backups, reps = 0.0, []
+    phase = {"optimize_s": 0.0, "evaluate_s": 0.0, "host_s": 0.0}
+    e0.record(stream)
+    for _ in range(steps):
+        rep = solver.pareto(inst, thr, eps=eps, iteration_cap=cap)
+        st = rep["stats"]
+        backups += st["optimize_backups"] + st["evaluate_state_backups"]
+        for k in phase:
+            phase[k] += st[k] / steps
+        reps.append(rep)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    cs = solver.cuda_stats()
+    solver.set_profiling(False)
+    return {"ms": e0.elapsed_time(e1), "backups": backups, "reports": reps, "phase": phase, "cuda": cs}
+
+
+def roofline(cs, prof_ms, workload_name, inst):
+    """Roofline of the dominant kernel (k_greedy_sweep_cmp) from a profiling pass: algorithmic
+    bytes of the swept tiles / the CUDA-event time of its launches."""
+    peak, peak_src = peak_hbm()
+    achieved = cs["opt_bytes"] / (cs["opt_ms"] * 1e-3) / 1e9 if cs["opt_ms"] > 0 else None
+    N, R, S = inst.total_nnz, inst.total_rows, inst.total_states
+    survey_ratio = (12 * N + 12 * R + 21 * S) / (4 * N + 4 * R + 20 * S)
+    ratio, tsrc = ncu_traffic(workload_name)
+    alg_per_launch = cs["opt_bytes"] / max(cs["opt_launches"], 1)
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None,
+            "traffic": ratio * alg_per_launch if ratio else None,
+            "kernel": "k_greedy_sweep_cmp", "workload": workload_name, "launches": cs["opt_launches"],
+            "traffic_over_algorithmic": ratio, "traffic_source": tsrc and tsrc.get("source"),
+            "avg_launch_us": 1e3 * cs["opt_ms"] / max(cs["opt_launches"], 1),
+            "algorithmic_bytes_per_launch": alg_per_launch,
+            "kernel_exec_backups_per_s": cs["opt_exec_backups"] / (cs["opt_ms"] * 1e-3) if cs["opt_ms"] else None,
+            "skipped_fraction": 1.0 - cs["opt_exec_backups"] / max(cs["opt_backups"], 1.0),
+            "peak_source": peak_src,
+            "timing": "CUDA events around every sweep-kernel launch (k_select outside them), in a separate "
+                      f"profiling pass ({prof_ms:.1f} ms per query with the events)",
+            "share_of_step": cs["opt_ms"] / prof_ms if prof_ms else None,
+            "survey_8d": {"bytes_per_backup": (12 * N + 12 * R + 21 * S) / N,
+                          "frac": achieved * survey_ratio / peak if achieved else None,
+                          "note": "the same launches counted with SURVEY.md §8(d)'s reference-layout bytes "
+                                  "(12 nnz + 12 R + 21 S); > 1 means the compact layout moves fewer bytes than "
+                                  "the reference layout would at this rate"}}
+
+
+NS_ITERS = 8  # Algorithm-1 iterations of the C4 north-star leg timed inside the default run
+
+
+def north_star(args, local):
+    """BASELINE north_star: the point-oriented query on 100 agents x 100 tasks on one B200.
+    Builds C4 streamed (lean uploads), times its first NS_ITERS Algorithm-1 iterations with
+    the products resident, and reports s/iteration, nnz-backups/s and the sweep kernel's
+    roofline at C4; the full query to convergence is a committed run (profiles/)."""
+    import torch
+    from paper_2305_04397_b200.api import Instance, Solver
+    cfg, thr, eps, K = workload("c4", 1)
+    solver = Solver(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    solver.set_stream(stream.cuda_stream)
+    solver.set_lean(True)
+    t0 = time.time()
+    inst = Instance.warehouse_streamed(cfg, solver, chunk=STREAMED["c4"])
+    build_s = time.time() - t0
+    solver.pareto(inst, thr, eps=eps, iteration_cap=1)  # warm-up
+    run = query_pass(solver, inst, thr, eps, NS_ITERS, 1, stream)
+    prof = query_pass(solver, inst, thr, eps, NS_ITERS, 1, stream, profiling=True)
+    rep = run["reports"][0]
+    it = len(rep["iterations"])
+    out = {"workload": "c4", "grid": [cfg["W"], cfg["H"]], "agents": cfg["n"], "tasks": cfg["n"],
+           "products": inst.distinct, "states": inst.total_states, "nnz": inst.total_nnz,
+           "build_upload_s": round(build_s, 2),
+           "step": f"the first {it} Algorithm-1 iterations of paretoPoint (thresholds -20 x100, 0.99 x100, eps 0.01), "
+                   "products resident (lean compact uploads)",
+           "s_per_iteration": run["ms"] * 1e-3 / it, "value": run["backups"] / (run["ms"] * 1e-3), "unit": UNIT,
+           "phase_s_per_iteration": {k: v / it for k, v in run["phase"].items()},
+           "roofline": roofline(prof["cuda"], prof["ms"], "c4", inst)}
+    full = os.path.join(ROOT, "profiles", "r02_c4_full_query.json")
+    if os.path.exists(full):
+        out["full_query"] = json.load(open(full))
+    solver.close()
+    return out
+
+
 def run_ours(args):
     import torch
     rank = int(os.environ.get("RANK", "0"))
@@ -331,6 +406,7 @@ def run_ours(args):
 
     torch.cuda.set_device(local)
     cfg, thr, eps, K = workload(args.workload, 1)
+    cap = ITER_CAP.get(args.workload, 500)
     streamed = STREAMED.get(args.workload)
     solver = Solver(local)
     stream = torch.cuda.Stream()  # the library launches on this stream; the CUDA events below are recorded on it
@@ -344,131 +420,82 @@ def run_ours(args):
         inst = Instance.warehouse(cfg)
         if K > 2:
             inst.add_objectives(K, seed=7)
+        solver.upload(inst)
     gen_s = time.time() - t0
-    solver.upload(inst)
-    # ---- device-resident timed region --------------------------------------------------
     for _ in range(max(args.warmup, 0)):
-        report = solver.pareto(inst, thr, eps=eps, iteration_cap=ITER_CAP.get(args.workload, 500))
-    solver.set_profiling(False)
-    solver.reset_cuda_stats()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    backups, reports = 0.0, []
-    phase = {"optimize_s": 0.0, "evaluate_s": 0.0, "host_s": 0.0}
+        solver.pareto(inst, thr, eps=eps, iteration_cap=cap)
+
+    # ---- device-resident timed region (clocks sampled during it) -------------------------
     with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            report = solver.pareto(inst, thr, eps=eps, iteration_cap=ITER_CAP.get(args.workload, 500))
-            st = report["stats"]
-            backups += st["optimize_backups"] + st["evaluate_state_backups"]
-            for k in phase:
-                phase[k] += st[k] / args.steps
-            reports.append(report)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    kernels_timed = int(solver.cuda_stats()["kernels"])
-    value = backups / (ms * 1e-3)
+        run = query_pass(solver, inst, thr, eps, cap, args.steps, stream)
+    ms, cs = run["ms"], run["cuda"]
+    kernels_timed = int(cs["kernels"])
+    value = run["backups"] / (ms * 1e-3)
+    first = run["reports"][0]
+    assert all(r["tDown"] == first["tDown"] and r["records"] == first["records"] for r in run["reports"]), \
+        "queries of the timed region differ"
 
     # ---- the same steps again with CUDA events around every sweep launch (roofline) -----
-    # (kept out of the first region: the per-launch event records cost ~1 ms per query)
-    solver.set_profiling(True)
-    solver.reset_cuda_stats()
-    torch.cuda.synchronize()
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    for _ in range(args.steps):
-        solver.pareto(inst, thr, eps=eps, iteration_cap=ITER_CAP.get(args.workload, 500))
-    p1.record(stream)
-    torch.cuda.synchronize()
-    prof_ms = p0.elapsed_time(p1)
-    cs = solver.cuda_stats()
-    solver.set_profiling(False)
+    prof = query_pass(solver, inst, thr, eps, cap, args.steps, stream, profiling=True)
 
-    # ---- end to end through the host API with host buffers ------------------------------
-    e2e_steps = max(1, min(args.steps, 3))
-    h2d = csr_bytes(inst)
-    solver.set_profiling(False)
-    torch.cuda.synchronize()
-    e_ms, e_backups = None, 0.0
+    # ---- end to end through the host API with host buffers (every step) ------------------
+    e2e = None
     if not streamed:  # a streamed instance has no host copy to re-upload
-        up0 = solver.cuda_stats()["upload_bytes"]
+        solver.reset_cuda_stats()
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_backups = 0.0
         e0.record(stream)
-        for _ in range(e2e_steps):
+        for _ in range(args.steps):
             solver.release()
             solver.upload(inst)
-            rep = solver.pareto(inst, thr, eps=eps, iteration_cap=ITER_CAP.get(args.workload, 500))
+            rep = solver.pareto(inst, thr, eps=eps, iteration_cap=cap)
             e_backups += rep["stats"]["optimize_backups"] + rep["stats"]["evaluate_state_backups"]
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1)
-        h2d = (solver.cuda_stats()["upload_bytes"] - up0) / e2e_steps  # bytes the uploads actually copied
+        ecs = solver.cuda_stats()
+        e2e = {"value": e_backups / (e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": ecs["upload_bytes"] / args.steps,
+               "d2h_bytes_per_step": ecs["d2h_bytes"] / args.steps, "steps": args.steps,
+               "ms_per_step": e_ms / args.steps, "pareto_query_ms": e_ms / args.steps,
+               "what": "release + re-upload of the instance's products from host memory (tiling and compact "
+                       "streams built on the host, H2D), the query, and every result read (D2H), per step; "
+                       "bytes counted by the library's copy calls"}
+    else:
+        e2e = {"value": None, "unit": UNIT, "note": f"streamed instance: products are built, uploaded lean and "
+                                                   f"dropped on the host in chunks of {streamed} "
+                                                   f"({gen_s:.1f} s build+upload); no host copy to re-upload"}
 
-    peak, peak_src = peak_hbm()
-    achieved = cs["opt_bytes"] / (cs["opt_ms"] * 1e-3) / 1e9 if cs["opt_ms"] > 0 else None
-    # SURVEY.md §8(d) counts the reference layout: 12 nnz + 12 R + 21 S per job-sweep; the
-    # compact kernel moves 4 nnz + 4 R + 20 S. Same units, so the survey's
-    # figure is ours scaled by the ratio of the two over the instance.
-    N, R, S = inst.total_nnz, inst.total_rows, inst.total_states
-    survey_ratio = (12 * N + 12 * R + 21 * S) / (4 * N + 4 * R + 20 * S)
-    ratio, traffic_src = ncu_traffic()
-    alg_per_launch = cs["opt_bytes"] / max(cs["opt_launches"], 1)
-    # ncu's dram bytes of the captured launch, scaled to this run's mean launch by the
-    # captured launch's traffic / algorithmic ratio (the kernel and layout are the same)
-    traffic = ratio * alg_per_launch if ratio else None
-    first = reports[0]
     iters = len(first["iterations"])
-    cpu = None if args.no_cpu_baseline else cpu_baseline(cfg, cfg["n"]) if K == 2 else None
+    rl = roofline(prof["cuda"], prof["ms"], args.workload, inst)
+    cpu = None if args.no_cpu_baseline or K != 2 else cpu_baseline(cfg, thr, eps)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded warehouse generator, warehouse.hpp:176; built before timing)",
         "config": {"workload": args.workload, "grid": [cfg["W"], cfg["H"]], "agents": cfg["n"], "tasks": cfg["n"],
                    "objectives": K, "eps": eps, "thresholds": f"costs {thr[0]} x{(K - 1) * cfg['n']}, probs {thr[-1]}",
-                   "feasible": first["feasible"], "pareto_iterations": iters,
+                   "feasible": first["feasible"], "converged": first["converged"], "pareto_iterations": iters,
                    "products": inst.distinct, "states": inst.total_states, "nnz": inst.total_nnz,
-                   "step": "one paretoPoint query (Alg. 1) with products resident in HBM",
-                   "l2": f"inputs larger than L2 (product CSR {h2d / 1e6:.0f} MB > 126 MB)",
+                   "step": "one paretoPoint query (Alg. 1, solver.hpp:281) with products resident in HBM",
+                   "l2": "inputs larger than L2 (product streams > 126 MB)",
                    "generate_s": round(gen_s, 3), "parallelism": "single GPU"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": ("k_greedy_sweep_tma" if os.environ.get("MORAP_COMPACT") == "0" else "k_greedy_sweep_cmp"), "launches": cs["opt_launches"],
-                     "traffic_over_algorithmic": ratio,
-                     "avg_launch_us": 1e3 * cs["opt_ms"] / max(cs["opt_launches"], 1),
-                     "algorithmic_bytes_per_launch": alg_per_launch,
-                     "kernel_backups_per_s": cs["opt_backups"] / (cs["opt_ms"] * 1e-3) if cs["opt_ms"] else None,
-                     "kernel_exec_backups_per_s": (cs["opt_exec_backups"] / (cs["opt_ms"] * 1e-3)
-                                                   if cs["opt_ms"] else None),
-                     "skipped_fraction": 1.0 - cs["opt_exec_backups"] / max(cs["opt_backups"], 1.0),
-                     "peak_source": peak_src, "traffic_source": traffic_src and traffic_src.get("source"),
-                     "timing": f"CUDA events around every sweep-kernel launch (the per-sweep frozen-tile "
-                               f"selection k_select outside them) over a second pass of the {args.steps} timed "
-                               f"steps ({prof_ms / args.steps:.1f} ms per query with the events)",
-                     "backups_note": "kernel_backups_per_s counts sweeps x nnz of every job (the reference's "
-                                     "work for the same results); kernel_exec_backups_per_s only the tiles "
-                                     "actually swept (frozen tiles are skipped, bit-identical results); "
-                                     "achieved / traffic are the bytes actually streamed",
-                     "share_of_step": cs["opt_ms"] / prof_ms if prof_ms else None,
-                     "survey_8d": {"bytes_per_backup": (12 * N + 12 * R + 21 * S) / N,
-                                   "achieved": achieved * survey_ratio if achieved else None,
-                                   "frac": achieved * survey_ratio / peak if achieved else None,
-                                   "note": "the same launches counted with SURVEY.md §8(d)'s reference-layout "
-                                           "bytes (12 nnz + 12 R + 21 S); > 1 means the compact layout moves "
-                                           "fewer bytes than the reference layout would at this rate"}},
+        "value_executed": cs["opt_exec_backups"] / (ms * 1e-3) + 0.0,
+        "value_note": "value counts sweeps x nnz of every optimize job plus evaluate sweeps x states (the "
+                      "reference's work for the same, bitwise-identical results); value_executed counts only "
+                      "the optimize backups the device executed (frozen tiles are skipped) per second of query",
+        "pareto_query_ms": ms / args.steps,
+        "roofline": rl,
         "cpu_baseline": cpu,
-        "e2e": ({"value": e_backups / (e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                 "d2h_bytes_per_step": d2h_bytes(inst, first), "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps}
-                if e_ms else
-                {"value": None, "unit": UNIT, "note": f"streamed instance: products are built, uploaded lean and "
-                                                      f"dropped on the host in chunks of {streamed} "
-                                                      f"({gen_s:.1f} s build+upload); no host copy to re-upload"}),
+        "e2e": e2e,
         "clocks": clk.summary(),
         "gpu_launches": kernels_timed,
-        "pareto_query_ms": ms / args.steps,
-        "phase_s_per_query": phase,
+        "phase_s_per_query": run["phase"],
         "kernel_stats": cs,
     }
+    if not args.no_north_star and args.workload == "c2":
+        line["north_star"] = north_star(args, local)
     if rank == 0:
         print(json.dumps(line))
 
@@ -481,6 +508,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-north-star", action="store_true", help="skip the C4 north-star leg of the default run")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU (sharded, NCCL) path even on one rank (testing)")
     args = ap.parse_args()

@@ -125,8 +125,6 @@ struct OptJob {
   unsigned long long bytesPerSweep;  // the model's (stats)
   int32_t nnz;
   int32_t outBase;  // this job's slice of the batch's absolute out-group list (k_build_cand)
-  int32_t candBase;  // this job's first candidate record (k_build_cand order), dataflow batches
-  int32_t pad;
 };
 
 struct EvalJob {
@@ -1012,6 +1010,11 @@ constexpr int kClaim = MORAP_CLAIM;       // tiles per claim
 // out-of-window groups are never skipped: window group -1.
 constexpr int kCandLtBits = 20;  // tiles per model < 2^20 (skipping is off for larger models)
 constexpr int kMaxOutGroups = 16;  // out-of-window stamp groups a skippable tile may depend on
+// the packed candidate word holds the window's 16-byte stamp loads in 4 bits, the tile's own
+// in 3 and the out-of-window group count in 5: the -D knobs must keep them in range
+static_assert((kXWin + 31) / 32 / 4 + 2 <= 15, "successor-window stamp loads overflow 4 bits");
+static_assert((kBlock / 32) / 4 + 2 <= 7, "own-state stamp loads overflow 3 bits");
+static_assert(kMaxOutGroups < 32 && kCandLtBits + 7 + 5 <= 32, "candidate word layout");
 __global__ void __launch_bounds__(kSelThreads) k_build_cand(const DevModel* __restrict__ models,
                                                             const OptJob* __restrict__ jobs,
                                                             const int32_t* __restrict__ list,
@@ -1576,8 +1579,6 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     }
   }
 }
-
-#include "opt_flow.cuh"
 
 // --------------------------------------------------------------------------------------
 // Policy chain: a fixed deterministic scheduler turns the product into a Markov chain
@@ -2490,7 +2491,6 @@ struct morap_ctx {
   bool lean = false;       // compact models uploaded without their fp64 prob / objective arrays
   bool optCompact = false; // current optimize batch runs the deep compact pipeline
   int cmpBlocks = 0;
-  int flowBlocks = 0;
   bool skip = true;        // frozen-tile skipping in compact optimize sweeps (k_select)
   // profiling: the events bracket the sweep kernel alone (k_select outside); MORAP_TIME_SELECT=1
   // brackets k_select + sweep
@@ -2517,16 +2517,6 @@ struct morap_ctx {
   size_t polStageBytes = 0;
   Ctl* dCtl = nullptr;
   Ctl* hCtl = nullptr;  // pinned mirror
-  // dataflow optimize batches (k_opt_flow, opt_flow.cuh); MORAP_FLOW=0: lock-step sweeps
-  bool useFlow = std::getenv("MORAP_FLOW") == nullptr || std::getenv("MORAP_FLOW")[0] != '0';
-  bool optFlow = false;  // current optimize batch ran as one dataflow launch
-  unsigned long long* dRing = nullptr;
-  size_t ringCap = 0;
-  int32_t* dJobSweep = nullptr;
-  int32_t* dPending = nullptr;
-  size_t flowJobsCap = 0;
-  FlowCtl* dFlow = nullptr;
-  FlowCtl* hFlow = nullptr;  // pinned mirror
   void* dEvalJobsRaw = nullptr;
   size_t dEvalJobsCap = 0;
   size_t dOptJobsCap = 0;
@@ -3196,104 +3186,6 @@ int init_ctl(morap_ctx* ctx, const std::vector<int32_t>& active, const std::vect
   return MORAP_OK;
 }
 
-// One dataflow launch for the whole optimize batch (k_opt_flow): seeds the ring with every
-// active job's sweep-0 items, launches, waits once. Values, policies, sweeps and residuals
-// are those of the lock-step loop (same tiles, same arithmetic, same stop tests).
-int run_flow(morap_ctx* ctx, const std::vector<int32_t>& active, const std::vector<int32_t>& jobModel, double eps,
-             int cap) {
-  const int njobs = static_cast<int>(jobModel.size());
-  const int seg = flow_seg(static_cast<int>(active.size()));
-  std::vector<unsigned long long> items;
-  std::vector<int32_t> pend(njobs, 0);
-  size_t worst = 0;  // items one sweep of every job can need (smallest segments)
-  for (int j : active) {
-    const int nt = ctx->hm[jobModel[j]].ntiles;
-    const int nseg = (nt + seg - 1) / seg;
-    pend[j] = nseg;
-    for (int q = 0; q < nseg; ++q) {
-      const int lt0 = q * seg, cnt = std::min(seg, nt - lt0);
-      items.push_back((1ull << 48) | (static_cast<unsigned long long>(j) << 25) |
-                      (static_cast<unsigned long long>(lt0) << 5) | static_cast<unsigned long long>(cnt - 1));
-    }
-    worst += static_cast<size_t>((nt + 1) / 2);  // flow_seg's smallest items
-  }
-  // capacity: a power of two >= 4x what one sweep of every job can queue (a reader never lags
-  // a whole lap; an overrun is detected and reported, never silently wrong)
-  size_t capNeed = 1024;  // + the positions CTAs claim ahead (two each)
-  while (capNeed < 4 * (std::max(worst, items.size()) + 2 * static_cast<size_t>(ctx->flowBlocks))) capNeed <<= 1;
-  int logCap = 0;
-  while ((1ull << logCap) < capNeed) ++logCap;
-  if (capNeed > ctx->ringCap) {
-    CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(ctx->dRing);
-    ctx->dRing = nullptr;
-    ctx->ringCap = 0;
-    CK(cudaMalloc(&ctx->dRing, capNeed * sizeof(unsigned long long)));
-    ctx->ringCap = capNeed;
-  }
-  if (static_cast<size_t>(njobs) > ctx->flowJobsCap) {
-    CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(ctx->dJobSweep);
-    cudaFree(ctx->dPending);
-    ctx->dJobSweep = ctx->dPending = nullptr;
-    ctx->flowJobsCap = std::max<size_t>(njobs, 256);
-    CK(cudaMalloc(&ctx->dJobSweep, ctx->flowJobsCap * sizeof(int32_t)));
-    CK(cudaMalloc(&ctx->dPending, ctx->flowJobsCap * sizeof(int32_t)));
-  }
-  if (!ctx->dFlow) {
-    CK(cudaMalloc(&ctx->dFlow, sizeof(FlowCtl)));
-    CK(cudaMallocHost(&ctx->hFlow, sizeof(FlowCtl)));
-  }
-  CK(cudaStreamSynchronize(ctx->stream));  // the pinned mirror and `items` are reused below
-  CK(cudaMemsetAsync(ctx->dRing, 0, capNeed * sizeof(unsigned long long), ctx->stream));
-  CK(cudaMemcpyAsync(ctx->dRing, items.data(), items.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice,
-                     ctx->stream));
-  CK(cudaMemsetAsync(ctx->dJobSweep, 0, njobs * sizeof(int32_t), ctx->stream));
-  CK(cudaMemcpyAsync(ctx->dPending, pend.data(), njobs * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
-  FlowCtl f{};
-  f.tail = items.size();
-  f.remaining = static_cast<int32_t>(active.size());
-  *ctx->hFlow = f;
-  CK(cudaMemcpyAsync(ctx->dFlow, ctx->hFlow, sizeof(FlowCtl), cudaMemcpyHostToDevice, ctx->stream));
-  FlowArgs A{};
-  A.models = ctx->dModels;
-  A.jobs = ctx->dOptJobs;
-  A.cand = ctx->dCand;
-  A.candOut = ctx->dCandOut;
-  A.candOutG = ctx->dCandOutG;
-  A.stampAll = ctx->dStampAll;
-  A.ring = ctx->dRing;
-  A.mask = capNeed - 1;
-  A.logCap = logCap;
-  A.skip = ctx->optSkip ? 1 : 0;
-  A.fc = ctx->dFlow;
-  A.jobSweep = ctx->dJobSweep;
-  A.pending = ctx->dPending;
-  A.delta = ctx->dDelta;
-  A.eps = eps;
-  A.cap = cap;
-  A.sweeps = ctx->dSweeps;
-  A.residual = ctx->dResidual;
-  A.status = ctx->dStatus;
-  if (ctx->profiling) CK(cudaEventRecord(ctx->ev0, ctx->stream));
-  k_opt_flow<<<ctx->flowBlocks, kTmaThreads, kCmpSmemBytes, ctx->stream>>>(A);
-  CK(cudaGetLastError());
-  if (ctx->profiling) CK(cudaEventRecord(ctx->ev1, ctx->stream));
-  ctx->stats[8] += 1;
-  CK(d2h(ctx, ctx->hFlow, ctx->dFlow, sizeof(FlowCtl)));
-  CK(cudaStreamSynchronize(ctx->stream));
-  if (ctx->hFlow->err)
-    return ctx->fail(MORAP_CUDA_ERROR, ctx->hFlow->err == 1 ? "dataflow optimize: work queue stalled (watchdog)"
-                                                            : "dataflow optimize: work ring overrun");
-  if (ctx->profiling) {
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-    ctx->stats[1] += ms;
-  }
-  ctx->stats[0] += 1;  // launches of the dominant kernel
-  return MORAP_OK;
-}
-
 // Shared body of the two optimize entry points. rhoHost == nullptr -> weights mode.
 int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const double* weights, int K,
                   const double* const* rhoHost, double eps, int cap, double* value_out, int32_t* sweeps_out,
@@ -3388,7 +3280,6 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   if (ctx->optSkip) {
     size_t tiles = 0, outs = 0;
     for (int j : active) {
-      ctx->hOptJobs[j].candBase = static_cast<int32_t>(tiles);  // k_build_cand's prefix (init_ctl order)
       tiles += static_cast<size_t>(ctx->hm[model_ids[j]].ntiles);
       ctx->hOptJobs[j].outBase = static_cast<int32_t>(outs);
       outs += static_cast<size_t>(ctx->hm[model_ids[j]].nOutGrp);
@@ -3462,18 +3353,8 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     CK(cudaGetLastError());
     ctx->stats[8] += 1;
   }
-  // dataflow batch (one launch, jobs advance independently) when every job runs the compact
-  // kernel and the work-item encoding fits (jobs < 2^22, tiles per model < 2^20)
-  ctx->optFlow = ctx->useFlow && allCompact && njobs < (1 << 22);
-  for (int j = 0; j < njobs && ctx->optFlow; ++j)
-    if (ctx->hm[model_ids[j]].ntiles >= (1 << 20)) ctx->optFlow = false;
-  if (!active.empty()) {
-    if (ctx->optFlow) {
-      if ((rc = run_flow(ctx, active, ctx->optModel, eps, cap))) return rc;
-    } else if ((rc = run_loop(ctx, 0, eps, cap))) {
-      return rc;
-    }
-  }
+  if (!active.empty())
+    if ((rc = run_loop(ctx, 0, eps, cap))) return rc;
 
   // results: one gather kernel + one copy per array, one synchronisation
   ctx->optSweeps.assign(njobs, 0);
@@ -3498,15 +3379,10 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   }
   // bytes: what the sweeps actually streamed; backups: sweeps x nnz of every job (the
   // reference's work for the same results); [10]: backups actually executed
-  if (ctx->optFlow && !active.empty()) {  // [0] counted by run_flow (one launch)
-    ctx->stats[2] += static_cast<double>(ctx->hFlow->execBytes);
-    ctx->stats[10] += static_cast<double>(ctx->hFlow->execBackups);
-  } else if (!ctx->optFlow) {
-    ctx->stats[0] += ctx->hCtl->sweepsDone;
-    ctx->stats[2] += static_cast<double>(ctx->optSkip ? ctx->hCtl->execBytes : ctx->hCtl->bytes);
-    ctx->stats[10] += ctx->optSkip ? static_cast<double>(ctx->hCtl->execBackups) : backups;
-  }
+  ctx->stats[0] += ctx->hCtl->sweepsDone;
+  ctx->stats[2] += static_cast<double>(ctx->optSkip ? ctx->hCtl->execBytes : ctx->hCtl->bytes);
   ctx->stats[3] += backups;
+  ctx->stats[10] += ctx->optSkip ? static_cast<double>(ctx->hCtl->execBackups) : backups;
   ctx->optPolicyReady.assign(njobs, 0);
   ctx->optJobs = njobs;
   return MORAP_OK;
@@ -3783,10 +3659,6 @@ int morap_cuda_create(int device, morap_ctx** out) {
   int occC = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occC, k_greedy_sweep_cmp<false>, kTmaThreads, kCmpSmemBytes);
   ctx->cmpBlocks = ctx->numSMs * std::max(1, occC);
-  cudaFuncSetAttribute(k_opt_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, kCmpSmemBytes);
-  int occF = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occF, k_opt_flow, kTmaThreads, kCmpSmemBytes);
-  ctx->flowBlocks = ctx->numSMs * std::max(1, occF);  // every CTA resident (persistent)
   int occP = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occP, k_eval_persistent, kPersistThreads, 0);
   int coop = 0;
@@ -3886,11 +3758,6 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   cudaFree(ctx->dTrace);
   cudaFree(ctx->dCtl);
   cudaFreeHost(ctx->hCtl);
-  cudaFree(ctx->dRing);
-  cudaFree(ctx->dJobSweep);
-  cudaFree(ctx->dPending);
-  cudaFree(ctx->dFlow);
-  cudaFreeHost(ctx->hFlow);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
   cudaStreamDestroy(ctx->own);
@@ -4386,19 +4253,6 @@ int morap_cuda_debug_cta_trace(morap_ctx* ctx, int enable, uint64_t* out, int64_
   }
   return MORAP_OK;
 }
-
-#ifdef MORAP_FLOW_PROF
-// diagnostics build only: the dataflow kernel's per-CTA wait counters (opt_flow.cuh)
-int morap_cuda_debug_flow_prof(morap_ctx* ctx, unsigned long long* out, int n, int reset) {
-  CK(cudaDeviceSynchronize());
-  CK(cudaMemcpyFromSymbol(out, g_flowProf, sizeof(unsigned long long) * std::min(n, 4096 * 8)));
-  if (reset) {
-    std::vector<unsigned long long> z(4096 * 8, 0);
-    CK(cudaMemcpyToSymbol(g_flowProf, z.data(), z.size() * 8));
-  }
-  return ctx->flowBlocks;
-}
-#endif
 
 int morap_cuda_set_skip(morap_ctx* ctx, int on) {
   if (!ctx) return MORAP_INVALID_CONFIG;

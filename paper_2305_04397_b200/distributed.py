@@ -19,7 +19,6 @@ all ranks see the same w sequence. There is no per-sweep communication.
 from __future__ import annotations
 
 import os
-import struct
 
 import numpy as np
 
@@ -40,7 +39,8 @@ def lpt_partition(weights, world: int):
 
 
 class _Exchange:
-    """all_gather of float64 arrays that preserves bits, over the default process group."""
+    """all_gather of float64 arrays that preserves bits, over the default process group: one
+    collective and one device-to-host copy per exchange."""
 
     def __init__(self, world: int, device):
         import torch
@@ -54,29 +54,20 @@ class _Exchange:
         torch = self.torch
         import torch.distributed as dist
 
-        packed = np.concatenate([values.astype(np.float64), mask.astype(np.float64)])
-        t = torch.from_numpy(packed).to(self.device)
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(out, t)
-        res = np.zeros_like(values, dtype=np.float64)
-        hit = np.zeros(values.shape[0], dtype=bool)
         m = values.shape[0]
-        for o in out:
-            a = o.cpu().numpy()
-            sel = a[m:] > 0.5
-            res[sel] = a[:m][sel]
-            hit |= sel
-        if not hit.all():
-            raise MorapError(14, "sharded exchange: some entries have no owner")
-        return res
-
-
-def _bits(x: float) -> bytes:
-    return struct.pack("<d", x)
+        t = torch.from_numpy(np.concatenate([values.astype(np.float64), mask.astype(np.float64)])).to(self.device)
+        out = torch.empty(self.world * 2 * m, dtype=torch.float64, device=self.device)
+        dist.all_gather_into_tensor(out, t)
+        a = out.cpu().numpy().reshape(self.world, 2 * m)
+        sel = a[:, m:] > 0.5
+        if not np.all(sel.sum(axis=0) == 1):
+            raise MorapError(14, "sharded exchange: every entry needs exactly one owner")
+        return np.take_along_axis(a[:, :m], np.argmax(sel, axis=0)[None, :], axis=0)[0]  # owner's exact bits
 
 
 class ShardedQuery:
-    """Supporting-point source (w -> (r, agent_of)) over products sharded across ranks."""
+    """Supporting-point source (w -> (r, agent_of)) over products sharded across ranks.
+    Per-iteration work on the host is vectorised (numpy) over the n^2 pairs."""
 
     def __init__(self, inst: Instance, rank: int, world: int, device: int = 0, backend=None, exchange=None,
                  eps: float = 1e-6, sweep_cap: int = 100000):
@@ -85,42 +76,47 @@ class ShardedQuery:
         self.eps, self.cap = eps, sweep_cap
         n = self.n
         # distinct products (slot of first occurrence) and their owners
-        self.slot_of = {}
+        slot = np.zeros((n, n), np.int64)
         firsts, sizes, states = [], [], []
         for i in range(n):
             for j in range(n):
                 dims, _ = inst.product_dims(i, j)
                 first = int(dims[5])
-                self.slot_of[(i, j)] = first
+                slot[i, j] = first
                 if first == i * n + j:
                     firsts.append(first)
                     sizes.append(float(dims[2]))
                     states.append(int(dims[0]))
         if inst.product_owner(0, 0) >= 0:  # built per rank (Instance.warehouse_shard): its owners
-            self.owner = {f: inst.product_owner(f // n, f % n) for f in firsts}
-            if any(o < 0 or o >= world for o in self.owner.values()):
+            owner = {f: inst.product_owner(f // n, f % n) for f in firsts}
+            if any(o < 0 or o >= world for o in owner.values()):
                 raise MorapError(18, "instance was sharded for a different world size")
         else:
-            owner = lpt_partition(sizes, world)
-            self.owner = {f: o for f, o in zip(firsts, owner)}
-        self.local = [f for f in firsts if self.owner[f] == rank]
+            owner = dict(zip(firsts, lpt_partition(sizes, world)))
+        self.slot = slot
+        self.local = [f for f in firsts if owner[f] == rank]
+        self.owner_of_slot = owner
+        self.nnz_of_slot = dict(zip(firsts, sizes))
+        self.states_of_slot = dict(zip(firsts, states))
         if backend is None:
             from .cuda import CudaBackend
 
             backend = CudaBackend(device)
             backend.set_lean(True)  # the query needs weighted optimize + chain evaluate only
         self.be = backend
-        if self.K > 2:
-            raise MorapError(18, "sharded query supports K = 2 objectives (cost, success)")
         self.upload()
+        # per pair: owned here?, device model id
+        own = np.vectorize(lambda f: owner[f] == rank)(slot) if n else np.zeros((0, 0), bool)
+        self.mine = own.astype(bool)
         if exchange is None:
             import torch
 
             exchange = _Exchange(world, torch.device("cuda", device) if torch.cuda.is_available() else "cpu")
         self.ex = exchange
         self.stats = {"optimize_backups": 0.0, "evaluate_state_backups": 0.0, "local_products": len(self.local)}
-        self.nnz = {f: s for f, s in zip(firsts, sizes)}
-        self.states = {f: s for f, s in zip(firsts, states)}
+        # objective coordinates g_k(i, j) (SURVEY.md §8a K-objective extension; K = 2: solver.hpp:118-119)
+        ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+        self.coords = np.stack([k * n + ii if k < self.K - 1 else (self.K - 1) * n + jj for k in range(self.K)], -1)
 
     def upload(self) -> int:
         """(Re-)upload this rank's products from their host arrays; returns the CSR bytes."""
@@ -134,13 +130,12 @@ class ShardedQuery:
         before = self.be.stats()["upload_bytes"] if measured else 0.0
         ids = self.be.upload(prods) if prods else []
         self.model_of = {f: int(m) for f, m in zip(self.local, ids)}
-        self.slot_of_model = {m: f for f, m in self.model_of.items()}
+        self.model_nnz = np.array([self.nnz_of_slot[f] for f in self.local], np.float64)
+        self.model_states = np.array([self.states_of_slot[f] for f in self.local], np.float64)
+        self.model_index = {f: q for q, f in enumerate(self.local)}
         if measured:  # the bytes the upload actually copied (lean compact layout)
             return int(self.be.stats()["upload_bytes"] - before)
         return sum(4 * (p.S + 1) + 4 * (p.R + 1) + 12 * p.nnz + p.S + 16 * p.R for p in prods)
-
-    def coord(self, k, i, j):
-        return k * self.n + i if k < self.K - 1 else (self.K - 1) * self.n + j
 
     def __call__(self, w):
         n, K = self.n, self.K
@@ -150,47 +145,44 @@ class ShardedQuery:
         if not np.all(np.isfinite(w)) or abs(np.abs(w).sum() - 1.0) > 1e-6:
             raise MorapError(18, "weight vector must be finite with unit 1-norm")
         # 1. local optimize jobs, deduplicated on (product, weight bits) as solver.hpp:110-131
-        job_of, models, weights, pair_job = {}, [], [], {}
-        for i in range(n):
-            for j in range(n):
-                f = self.slot_of[(i, j)]
-                if self.owner[f] != self.rank:
-                    continue
-                wk = tuple(w[self.coord(k, i, j)] for k in range(K))
-                key = (f,) + tuple(_bits(x) for x in wk)
-                if key not in job_of:
-                    job_of[key] = len(models)
-                    models.append(self.model_of[f])
-                    weights.append(wk)
-                pair_job[(i, j)] = job_of[key]
+        pi, pj = np.nonzero(self.mine)
+        wk = w[self.coords[pi, pj]]  # (pairs, K)
         vals = np.zeros(n * n)
         mask = np.zeros(n * n)
-        if models:
-            v, sw, res, st = self.be.optimize(np.array(models, np.int32), np.array(weights), self.eps, self.cap)
-            for (i, j), q in pair_job.items():
-                if st[q] != 0:
-                    raise MorapError(int(st[q]), "weighted optimization failed")
-                vals[i * n + j] = v[q]
-                mask[i * n + j] = 1.0
-            self.stats["optimize_backups"] += float(np.sum(sw.astype(np.float64) *
-                                                           np.array([self.nnz[self.slot_of_model[m]] for m in models])))
+        job = np.zeros(pi.shape[0], np.int64)
+        models = np.zeros(0, np.int32)
+        if pi.size:
+            key = np.concatenate([self.slot[pi, pj][:, None].astype(np.uint64), wk.view(np.uint64)], axis=1)
+            uniq, first, job = np.unique(key, axis=0, return_index=True, return_inverse=True)
+            job = job.reshape(-1)
+            slots = self.slot[pi, pj][first]
+            midx = np.array([self.model_index[int(f)] for f in slots], np.int64)
+            models = np.array([self.model_of[int(f)] for f in slots], np.int32)
+            v, sw, res, st = self.be.optimize(models, wk[first], self.eps, self.cap)
+            if np.any(st != 0):
+                raise MorapError(int(st[st != 0][0]), "weighted optimization failed")
+            vals[pi * n + pj] = v[job]
+            mask[pi * n + pj] = 1.0
+            self.stats["optimize_backups"] += float(np.dot(sw.astype(np.float64), self.model_nnz[midx]))
         # 2. exchange the n^2 values, 3. identical Hungarian everywhere
         c = self.ex.gather(vals, mask).reshape(n, n)
         agent_of = max_assignment(c)
-        # 4. owners evaluate their assigned pairs under all K objectives
-        mine = [(j, int(agent_of[j])) for j in range(n) if (int(agent_of[j]), j) in pair_job]
+        # 4. owners evaluate their assigned pairs under all K objectives (fused multi-RHS)
         r = np.zeros(K * n)
         rmask = np.zeros(K * n)
+        jobs_of_pair = {(int(a), int(b)): int(q) for a, b, q in zip(pi, pj, job)}
+        mine = [(j, int(agent_of[j])) for j in range(n) if (int(agent_of[j]), j) in jobs_of_pair]
         if mine:
-            ev, esw, eres, est = self.be.evaluate_optimized([pair_job[(i, j)] for j, i in mine], tuple(range(K)),
-                                                            self.eps, self.cap)
+            qs = [jobs_of_pair[(i, j)] for j, i in mine]
+            ev, esw, eres, est = self.be.evaluate_optimized(qs, tuple(range(K)), self.eps, self.cap)
+            if np.any(est != 0):
+                raise MorapError(int(est[est != 0][0]), "evaluation failed")
             for q, (j, i) in enumerate(mine):
-                self.stats["evaluate_state_backups"] += float(np.sum(esw[q])) * self.states[self.slot_of[(i, j)]]
-                for k in range(K):
-                    if est[q, k] != 0:
-                        raise MorapError(int(est[q, k]), "evaluation failed")
-                    r[self.coord(k, i, j)] = ev[q, k]
-                    rmask[self.coord(k, i, j)] = 1.0
+                self.stats["evaluate_state_backups"] += float(np.sum(esw[q])) * \
+                    self.states_of_slot[int(self.slot[i, j])]
+                cc = self.coords[i, j]
+                r[cc] = ev[q, :K]
+                rmask[cc] = 1.0
         r = self.ex.gather(r, rmask)
         return r, agent_of
 
@@ -200,8 +192,8 @@ def pareto_sharded(inst: Instance, thresholds, eps: float, rank: int, world: int
     """paretoPoint (solver.hpp:281) over products sharded across ranks."""
     q = ShardedQuery(inst, rank, world, device, backend, exchange)
     t = np.asarray(thresholds, np.float64)
-    if inst.real_tasks != inst.n or t.shape[0] != 2 * inst.n:
-        raise MorapError(9, "sharded query expects n real tasks and 2n thresholds (expandThresholds identity)")
+    if inst.real_tasks != inst.n or t.shape[0] != inst.objectives * inst.n:
+        raise MorapError(9, "sharded query expects n real tasks and K*n thresholds (expandThresholds identity)")
     return pareto_core(t, inst.n, q, eps=eps, iteration_cap=iteration_cap, verify=verify), q
 
 

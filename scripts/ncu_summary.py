@@ -27,10 +27,11 @@ for k in keys:
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 rd = float(get("dram__bytes_read.sum")) * scale[units[h.index("dram__bytes_read.sum")]]
 wr = float(get("dram__bytes_write.sum")) * scale[units[h.index("dram__bytes_write.sum")]]
-us = float(get("gpu__time_duration.sum")) * (1e-3 if units[h.index("gpu__time_duration.sum")] == "nsecond" else 1)
+us = float(get("gpu__time_duration.sum")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}[units[h.index("gpu__time_duration.sum")]]
 print(f"dram traffic per launch: {(rd + wr) / 1e6:.1f} MB; algorithmic bytes per launch: {alg / 1e6:.1f} MB; "
       f"traffic/algorithmic = {(rd + wr) / alg:.3f}")
-print(f"dram GB/s under ncu (cold L2, serialised): {(rd + wr) / (us * 1e-6) / 1e9:.0f}")
+print(f"dram GB/s under ncu (cold L2, serialised): {(rd + wr) / (us * 1e-6) / 1e9:.0f}; "
+      f"algorithmic GB/s: {alg / (us * 1e-6) / 1e9:.0f}")
 print("stall reasons (warps per issue):")
 st = [(float(v[i]), n) for i, n in enumerate(h)
       if n.startswith("smsp__average_warps_issue_stalled_") and n.endswith("_per_issue_active.ratio")]
