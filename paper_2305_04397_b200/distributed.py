@@ -125,6 +125,9 @@ class ShardedQuery:
             self.be.release_models()
         if getattr(self, "_prods", None) is None:  # host buffers of this rank's products, kept
             self._prods = [self.inst.product(f // n, f % n) for f in self.local]
+            if self.K > 2:  # device objective order: cost, extras, success (weights w[g_k(i, j)])
+                for f, p in zip(self.local, self._prods):
+                    p.objectives = [self.inst.objective(f // n, f % n, k) for k in range(self.K)]
         prods = self._prods
         measured = hasattr(self.be, "stats")
         before = self.be.stats()["upload_bytes"] if measured else 0.0
