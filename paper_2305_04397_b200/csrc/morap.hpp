@@ -65,6 +65,10 @@ double dot(const Vec& x, const Vec& y);
 Vec matVec(const Mat& m, const Vec& x);
 double maxAbs(const Vec& v);
 Vec solveDense(Mat A, Vec b, double pivotTol = 1e-12);
+Vec solveDenseInPlace(Mat& A, Vec& b, double pivotTol = 1e-12);  // A and b are destroyed
+// 0: blocked + host threads for n >= 128 (bitwise the unblocked elimination), 1: unblocked
+// only (A/B and tests; env MORAP_DENSE=unblocked)
+int& denseSolveMode();
 bool choleskyLower(const Mat& m, Mat& lower);
 
 // ---- task logic (logic.hpp) --------------------------------------------------------------
