@@ -365,6 +365,7 @@ def north_star(args, local):
     from paper_2305_04397_b200.api import Instance, Solver
     cfg, thr, eps, K = workload("c4", 1)
     solver = Solver(local)
+    solver.set_fingerprints(False)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     solver.set_stream(stream.cuda_stream)
@@ -409,6 +410,7 @@ def run_ours(args):
     cap = ITER_CAP.get(args.workload, 500)
     streamed = STREAMED.get(args.workload)
     solver = Solver(local)
+    solver.set_fingerprints(False)  # scheduler hashes are test evidence, not part of paretoPoint
     stream = torch.cuda.Stream()  # the library launches on this stream; the CUDA events below are recorded on it
     torch.cuda.set_stream(stream)
     solver.set_stream(stream.cuda_stream)

@@ -76,6 +76,9 @@ int morap_instance_product_owner(const morap_instance* inst, int i, int j);
 
 /* morap_cuda_set_lean on the solver's context (applies to later uploads). */
 int morap_solver_set_lean(morap_solver* s, int on);
+/* Per-iteration scheduler fingerprints ("schedulerHash") in morap_pareto's report: on by
+ * default (the parity tests compare them); off leaves the records' tUp / tDown only. */
+int morap_solver_set_fingerprints(morap_solver* s, int on);
 
 /* Streamed generateInstance for instances whose host copy would not fit (C4: 100 x 100,
  * ~1e4 products of ~1e5 states): products are built `chunk` at a time on `threads` host

@@ -144,6 +144,10 @@ int morap_cuda_fetch_policy(morap_ctx* ctx, int job, int32_t* rows_out);
 /* Policies of several optimize jobs in one batch (one synchronisation): rows_out[q]
  * receives the num_states rows of job jobs[q]. */
 int morap_cuda_fetch_policies(morap_ctx* ctx, int njobs, const int32_t* jobs, int32_t* const* rows_out);
+/* Zero-copy variant: rows_out[q] points at job jobs[q]'s rows in the library's pinned
+ * staging area (morap_cuda_evaluate_optimized stages the evaluated jobs' policies there
+ * while its sweeps run), valid until the next optimize batch or policy fetch. */
+int morap_cuda_policy_views(morap_ctx* ctx, int njobs, const int32_t* jobs, const int32_t** rows_out);
 
 /* Fused JobKind::Evaluate of optimize jobs' own schedulers (supportingPoint's cost and
  * success jobs, solver.hpp:148-172): for each listed optimize job, evaluate its final

@@ -56,6 +56,7 @@ def load_host_library() -> C.CDLL:
         "morap_solver_upload": (i32, [p, p]),
         "morap_solver_release": (i32, [p]),
         "morap_solver_set_lean": (i32, [p, i32]),
+        "morap_solver_set_fingerprints": (i32, [p, i32]),
         "morap_instance_warehouse_shard": (i32, [C.c_char_p, i32, i32, i32, i32, C.POINTER(p)]),
         "morap_instance_product_owner": (i32, [p, i32, i32]),
         "morap_instance_warehouse_streamed": (i32, [C.c_char_p, i32, p, i32, C.POINTER(p)]),
@@ -281,6 +282,11 @@ class Solver:
 
     def release(self):
         _check(self._lib.morap_solver_release(self.h), "release")
+
+    def set_fingerprints(self, on: bool):
+        """Scheduler fingerprints in pareto()'s records (on by default; the benchmark turns
+        them off: hashing the schedulers is test evidence, not part of paretoPoint)."""
+        _check(self._lib.morap_solver_set_fingerprints(self.h, int(on)), "set_fingerprints")
 
     def set_lean(self, on: bool):
         """Store compact-alphabet products without fp64 prob/objective arrays (morap_cuda_set_lean)."""

@@ -17,6 +17,7 @@ struct morap_instance {
 
 struct morap_solver {
   std::unique_ptr<morap::GpuBackend> gpu;
+  bool fingerprints = true;  // per-iteration scheduler hashes in the pareto report
 };
 
 struct morap_centralised {
@@ -53,7 +54,7 @@ void putJson(const morap::Json& j, char* out, int cap) {
   std::memcpy(out, s.c_str(), s.size() + 1);
 }
 
-morap::Json reportJson(const morap::ParetoResult& res) {
+morap::Json reportJson(const morap::ParetoResult& res, bool fingerprints = true) {
   std::unique_ptr<morap::SynthesisResult> syn;
   int synErr = 0;
   if (res.converged) {
@@ -67,22 +68,28 @@ morap::Json reportJson(const morap::ParetoResult& res) {
   j["converged"] = res.converged;
   j["thresholds"] = res.thresholds;
   j["lambdaStar"] = res.lambdaStar;
-  // scheduler fingerprints, one thread per iteration record
+  // scheduler fingerprints (test evidence, not part of paretoPoint): every (record,
+  // scheduler) pair on the host worker pool
   std::vector<std::vector<uint64_t>> hashes(res.iterations.size());
-  {
-    std::vector<std::thread> pool;
-    for (size_t k = 0; k < res.iterations.size(); ++k)
-      pool.emplace_back([&, k] {
-        for (const auto& mu : res.iterations[k].schedulers) hashes[k].push_back(rowsHash(mu));
-      });
-    for (auto& t : pool) t.join();
+  if (fingerprints) {
+    std::vector<std::pair<int, int>> items;
+    for (size_t k = 0; k < res.iterations.size(); ++k) {
+      hashes[k].resize(res.iterations[k].schedulers.size());
+      for (size_t q = 0; q < res.iterations[k].schedulers.size(); ++q)
+        items.push_back({static_cast<int>(k), static_cast<int>(q)});
+    }
+    morap::parallelFor(static_cast<int>(items.size()), [&](int i) {
+      const auto [k, q] = items[i];
+      hashes[k][q] = rowsHash(res.iterations[k].schedulers[q]);
+    });
   }
   morap::Json recs = morap::Json::array();
   for (size_t k = 0; k < res.iterations.size(); ++k) {
     const auto& rec = res.iterations[k];
     morap::Json hs = morap::Json::array();
     for (uint64_t h : hashes[k]) hs.push_back(std::to_string(h));
-    recs.push_back({{"tUp", rec.tUp}, {"tDown", rec.tDown}, {"schedulerHash", hs}});
+    if (fingerprints) recs.push_back({{"tUp", rec.tUp}, {"tDown", rec.tDown}, {"schedulerHash", hs}});
+    else recs.push_back({{"tUp", rec.tUp}, {"tDown", rec.tDown}});
   }
   j["records"] = recs;
   if (syn) {
@@ -306,6 +313,13 @@ int morap_solver_set_lean(morap_solver* s, int on) {
   return guard([&] { s->gpu->setLean(on != 0); });
 }
 
+int morap_solver_set_fingerprints(morap_solver* s, int on) {
+  return guard([&] {
+    if (!s) morap::fail(morap::Errc::InvalidConfig, "null solver");
+    s->fingerprints = on != 0;
+  });
+}
+
 int morap_instance_warehouse_streamed(const char* config_json, int threads, morap_solver* s, int chunk,
                                       morap_instance** out) {
   return guard([&] {
@@ -351,7 +365,7 @@ int morap_pareto(morap_solver* s, const morap_instance* p, const double* thresho
       putJson(morap::Json{{"verdict", v}}, json_out, json_cap);
     } else {
       morap::ParetoResult res = morap::paretoPoint(p->inst, t, M, eps, *s->gpu, iteration_cap, &st);
-      putJson(reportJson(res), json_out, json_cap);
+      putJson(reportJson(res, s->fingerprints), json_out, json_cap);
     }
     putStats(st, stats_out);
   });

@@ -69,6 +69,8 @@ Vec solveDenseInPlace(Mat& A, Vec& b, double pivotTol = 1e-12);  // A and b are 
 // 0: blocked + host threads for n >= 128 (bitwise the unblocked elimination), 1: unblocked
 // only (A/B and tests; env MORAP_DENSE=unblocked)
 int& denseSolveMode();
+// fn(0 .. n-1) on the host worker pool (the dense solve's threads); returns when all are done
+void parallelFor(int n, const std::function<void(int)>& fn);
 bool choleskyLower(const Mat& m, Mat& lower);
 
 // ---- task logic (logic.hpp) --------------------------------------------------------------

@@ -2487,6 +2487,8 @@ struct morap_ctx {
   };
   std::vector<Graph> graphs;  // cached sweep batches
   bool useGraphs = true;
+  int lastOptSweeps = 0;      // sweeps the previous optimize batch needed (run_loop's first round)
+  int launchedOptSweeps = 0;  // sweep launches of the previous optimize batch (>= its sweeps)
   bool useCompact = true;  // compact u8 probability / reward-class streams where possible
   bool lean = false;       // compact models uploaded without their fp64 prob / objective arrays
   bool optCompact = false; // current optimize batch runs the deep compact pipeline
@@ -3123,48 +3125,70 @@ int batch_graph(morap_ctx* ctx, int kind, double eps, int cap, int B, bool timed
 }
 
 // Runs sweeps (+finalize) until no job is active. kind 0 optimize, 1 evaluate.
-// Batches of 4, 8, 16, 32 sweep/finalize pairs go out as one graph launch each and the
-// 4-byte active count is polled once per batch (converged jobs are already frozen on the
-// device, so overshooting a batch only costs empty launches). With profiling on, every
-// sweep launch inside the graphs is bracketed by CUDA events; only launches that still
-// had active jobs are counted.
+// Sweep/finalize pairs go out as CUDA graphs of 4, 8, 16 or 32 pairs and the 4-byte active
+// count is polled between rounds of graphs (converged jobs are already frozen on the device,
+// so overshooting only costs empty launches). The optimize batches of one Pareto query need
+// similar sweep counts from call to call, so the first round launches (previous call's count
+// - 2) pairs at once and later rounds 4, 8, 16, 32; without a history, 4, 8, 16, 32. With
+// profiling on, every sweep launch inside the graphs is bracketed by CUDA events; only
+// launches that still had active jobs are counted.
 int run_loop(morap_ctx* ctx, int kind, double eps, int cap) {
   const bool timed = ctx->profiling;
-  int batch = 4;
-  int before = ctx->hCtl->sweepsDone;
+  const int start = ctx->hCtl->sweepsDone;
+  int before = start;
   double ms = 0.0;
+  int launched = 0;
+  int ahead = kind == 0 && ctx->lastOptSweeps > 6 ? ((ctx->lastOptSweeps - 2 + 3) & ~3) : 4;
+  int next = 4;
   for (;;) {
-    morap_ctx::Graph* g = nullptr;
-    int rc = ctx->useGraphs ? batch_graph(ctx, kind, eps, cap, batch, timed, &g) : MORAP_OK;
-    if (rc) return rc;
-    std::vector<cudaEvent_t> direct;
-    if (g) {
-      CK(cudaGraphLaunch(g->exec, ctx->stream));
-    } else {
-      if (timed) {
-        while (ctx->evPool.size() < 2u * batch) {
-          cudaEvent_t e;
-          CK(cudaEventCreate(&e));
-          ctx->evPool.push_back(e);
-        }
-      }
-      if ((rc = enqueue_sweeps(ctx, kind, eps, cap, batch, timed ? ctx->evPool.data() : nullptr, false))) return rc;
+    // this round: `ahead` pairs as graphs of 32 / 16 / 8 / 4
+    std::vector<int> pieces;
+    for (int left = ahead; left > 0;) {
+      const int b = left >= 32 ? 32 : left >= 16 ? 16 : left >= 8 ? 8 : 4;
+      pieces.push_back(b);
+      left -= b;
     }
-    ctx->stats[8] += (kind == 0 && ctx->useTma && ctx->optCompact ? (ctx->optSkip ? 2 : 1) : 2) * batch;
+    std::vector<const cudaEvent_t*> evs;
+    if (timed && !ctx->useGraphs)  // pointers into the pool stay valid for the whole round
+      while (ctx->evPool.size() < 2u * 32u * pieces.size()) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        ctx->evPool.push_back(e);
+      }
+    for (int b : pieces) {
+      morap_ctx::Graph* g = nullptr;
+      int rc = ctx->useGraphs ? batch_graph(ctx, kind, eps, cap, b, timed, &g) : MORAP_OK;
+      if (rc) return rc;
+      if (g) {
+        CK(cudaGraphLaunch(g->exec, ctx->stream));
+        evs.push_back(g->ev.data());
+      } else {
+        const cudaEvent_t* ev = timed ? ctx->evPool.data() + 2 * evs.size() * 32 : nullptr;
+        if ((rc = enqueue_sweeps(ctx, kind, eps, cap, b, ev, false))) return rc;
+        evs.push_back(ev);
+      }
+      launched += b;
+      ctx->stats[8] += (kind == 0 && ctx->useTma && ctx->optCompact ? (ctx->optSkip ? 2 : 1) : 2) * b;
+    }
     CK(d2h(ctx, ctx->hCtl, ctx->dCtl, sizeof(Ctl)));
     CK(cudaStreamSynchronize(ctx->stream));
     if (timed) {
-      const int worked = ctx->hCtl->sweepsDone - before;
-      const cudaEvent_t* ev = g ? g->ev.data() : ctx->evPool.data();
-      for (int i = 0; i < worked && i < batch; ++i) {
-        float t = 0.f;
-        CK(cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]));
-        ms += t;
-      }
+      int worked = ctx->hCtl->sweepsDone - before;
+      for (size_t q = 0; q < pieces.size() && worked > 0; ++q)
+        for (int i = 0; i < pieces[q] && worked > 0; ++i, --worked) {
+          float t = 0.f;
+          CK(cudaEventElapsedTime(&t, evs[q][2 * i], evs[q][2 * i + 1]));
+          ms += t;
+        }
     }
     before = ctx->hCtl->sweepsDone;
     if (ctx->hCtl->nactive == 0) break;
-    batch = std::min(batch * 2, 32);
+    ahead = next;
+    next = std::min(next * 2, 32);
+  }
+  if (kind == 0) {
+    ctx->lastOptSweeps = ctx->hCtl->sweepsDone - start;
+    ctx->launchedOptSweeps = launched;
   }
   if (timed) ctx->stats[kind == 0 ? 1 : 5] += ms;
   return MORAP_OK;
@@ -3353,8 +3377,12 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     CK(cudaGetLastError());
     ctx->stats[8] += 1;
   }
-  if (!active.empty())
+  if (!active.empty()) {
     if ((rc = run_loop(ctx, 0, eps, cap))) return rc;
+    if (ctx->trace)
+      std::fprintf(stderr, "[morap] optimize batch: %d jobs, %d sweeps, %d sweep launches\n", njobs,
+                   ctx->lastOptSweeps, ctx->launchedOptSweeps);
+  }
 
   // results: one gather kernel + one copy per array, one synchronisation
   ctx->optSweeps.assign(njobs, 0);
@@ -4037,7 +4065,7 @@ int morap_cuda_fetch_policy(morap_ctx* ctx, int job, int32_t* out) {
   return MORAP_OK;
 }
 
-int morap_cuda_fetch_policies(morap_ctx* ctx, int njobs, const int32_t* jobs, int32_t* const* rows_out) {
+int morap_cuda_policy_views(morap_ctx* ctx, int njobs, const int32_t* jobs, const int32_t** rows_out) {
   if (!ctx) return MORAP_INVALID_CONFIG;
   if (njobs <= 0) return MORAP_OK;
   std::vector<int32_t> list(jobs, jobs + njobs);
@@ -4048,37 +4076,43 @@ int morap_cuda_fetch_policies(morap_ctx* ctx, int njobs, const int32_t* jobs, in
     bytes += align_up(sizeof(int32_t) * ctx->hm[ctx->optModel[j]].S, 256);
   }
   cudaSetDevice(ctx->device);
-  if (list == ctx->polPrefetched) {  // staged by evaluate_optimized: wait for the side copies only
-    CK(cudaEventSynchronize(ctx->polCopied));
-    for (int q = 0; q < njobs; ++q)
-      std::memcpy(rows_out[q], static_cast<char*>(ctx->polStage) + ctx->polOff[q],
-                  sizeof(int32_t) * ctx->hm[ctx->optModel[list[q]]].S);
-    return MORAP_OK;
+  CK(cudaEventSynchronize(ctx->polCopied));  // staged by evaluate_optimized (or a stale prefetch still copying)
+  if (list != ctx->polPrefetched) {
+    ctx->polPrefetched.clear();
+    int rc = extract_policies(ctx, list);
+    if (rc) return rc;
+    // one pinned staging area, one synchronisation for the whole batch
+    if (bytes > ctx->polStageBytes) {
+      cudaFreeHost(ctx->polStage);
+      ctx->polStage = nullptr;
+      ctx->polStageBytes = 0;
+      CK(cudaMallocHost(&ctx->polStage, bytes));
+      ctx->polStageBytes = bytes;
+    }
+    ctx->polOff.assign(static_cast<size_t>(njobs), 0);
+    size_t o = 0;
+    for (int q = 0; q < njobs; ++q) {
+      const size_t n = sizeof(int32_t) * ctx->hm[ctx->optModel[list[q]]].S;
+      ctx->polOff[q] = o;
+      CK(d2h(ctx, static_cast<char*>(ctx->polStage) + o, ctx->hOptJobs[list[q]].policy, n));
+      o += align_up(n, 256);
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->polPrefetched = list;
   }
-  CK(cudaEventSynchronize(ctx->polCopied));  // a stale prefetch may still be copying into polStage
-  ctx->polPrefetched.clear();
-  int rc = extract_policies(ctx, list);
-  if (rc) return rc;
-  // one pinned staging area, one synchronisation for the whole batch
-  if (bytes > ctx->polStageBytes) {
-    cudaFreeHost(ctx->polStage);
-    ctx->polStage = nullptr;
-    ctx->polStageBytes = 0;
-    CK(cudaMallocHost(&ctx->polStage, bytes));
-    ctx->polStageBytes = bytes;
-  }
-  std::vector<size_t> off(static_cast<size_t>(njobs));
-  size_t o = 0;
-  for (int q = 0; q < njobs; ++q) {
-    const size_t n = sizeof(int32_t) * ctx->hm[ctx->optModel[list[q]]].S;
-    off[q] = o;
-    CK(d2h(ctx, static_cast<char*>(ctx->polStage) + o, ctx->hOptJobs[list[q]].policy, n));
-    o += align_up(n, 256);
-  }
-  CK(cudaStreamSynchronize(ctx->stream));
   for (int q = 0; q < njobs; ++q)
-    std::memcpy(rows_out[q], static_cast<char*>(ctx->polStage) + off[q],
-                sizeof(int32_t) * ctx->hm[ctx->optModel[list[q]]].S);
+    rows_out[q] = reinterpret_cast<const int32_t*>(static_cast<char*>(ctx->polStage) + ctx->polOff[q]);
+  return MORAP_OK;
+}
+
+int morap_cuda_fetch_policies(morap_ctx* ctx, int njobs, const int32_t* jobs, int32_t* const* rows_out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  if (njobs <= 0) return MORAP_OK;
+  std::vector<const int32_t*> views(static_cast<size_t>(njobs));
+  const int rc = morap_cuda_policy_views(ctx, njobs, jobs, views.data());
+  if (rc) return rc;
+  for (int q = 0; q < njobs; ++q)
+    std::memcpy(rows_out[q], views[q], sizeof(int32_t) * ctx->hm[ctx->optModel[jobs[q]]].S);
   return MORAP_OK;
 }
 

@@ -120,7 +120,6 @@ SupportingPoint supportingPoint(const MorapInstance& inst, const Vec& w, GpuBack
   if (stats) stats->evaluateSweepSeconds += seconds(t2);
   out.r.assign(static_cast<size_t>(K) * n, 0.0);
   out.schedulers.resize(static_cast<size_t>(n));
-  std::vector<int32_t*> rowsOut(static_cast<size_t>(n));
   for (int j = 0; j < n; ++j) {
     const int i = out.assignment.agentOf[j];
     for (int k = 0; k < K; ++k) {
@@ -128,20 +127,26 @@ SupportingPoint supportingPoint(const MorapInstance& inst, const Vec& w, GpuBack
       if (st != MORAP_OK) jobFailed(st, k == K - 1 ? "success evaluation failed" : "cost evaluation failed");
     }
     for (int k = 0; k < K; ++k) out.r[coord(k, i, j)] = ev[static_cast<size_t>(j) * K + k];
-    const ProductMdp& p = *inst.products[i][j];
-    out.schedulers[j].rows.resize(static_cast<size_t>(p.mdp.numStates));
-    rowsOut[j] = out.schedulers[j].rows.data();
   }
-  // the n schedulers of the assigned pairs (IterationRecord::schedulers, solver.hpp:38-45)
+  // the n schedulers of the assigned pairs (IterationRecord::schedulers, solver.hpp:38-45),
+  // copied out of the pinned staging area on the host threads (page faults of the fresh
+  // vectors included)
   const auto t3 = std::chrono::steady_clock::now();
-  ck(ctx, morap_cuda_fetch_policies(ctx, n, evalJobs.data(), rowsOut.data()), "fetch policies");
+  std::vector<const int32_t*> rowsIn(static_cast<size_t>(n));
+  ck(ctx, morap_cuda_policy_views(ctx, n, evalJobs.data(), rowsIn.data()), "fetch policies");
+  const auto t3b = std::chrono::steady_clock::now();
+  parallelFor(n, [&](int j) {
+    const ProductMdp& p = *inst.products[out.assignment.agentOf[j]][j];
+    out.schedulers[j].rows.assign(rowsIn[j], rowsIn[j] + p.mdp.numStates);
+  });
   if (std::getenv("MORAP_TRACE"))
     std::fprintf(stderr, "[morap] supportingPoint: optimize %.3f ms (%d jobs), assign %.3f ms, evaluate %.3f ms "
-                         "(device batch %.3f ms), policies %.3f ms\n",
+                         "(device batch %.3f ms), policies %.3f ms (wait %.3f ms)\n",
                  1e3 * std::chrono::duration<double>(t1 - t0).count(), nj,
                  1e3 * std::chrono::duration<double>(t2 - t1).count(),
                  1e3 * std::chrono::duration<double>(t3 - t2).count(),
-                 1e3 * std::chrono::duration<double>(t2b - t2).count(), 1e3 * seconds(t3));
+                 1e3 * std::chrono::duration<double>(t2b - t2).count(), 1e3 * seconds(t3),
+                 1e3 * std::chrono::duration<double>(t3b - t3).count());
   if (stats) {
     stats->evaluateJobs += static_cast<long>(n) * K;
     for (int j = 0; j < n; ++j)
