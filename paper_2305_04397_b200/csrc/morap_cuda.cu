@@ -2000,6 +2000,10 @@ __global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_pe
   unsigned long long bytesAcc = 0, backupsAcc = 0;
   for (int k = 0;; ++k) {
     const int parity = k & 1;
+    // diagnostics (morap_cuda_debug_cta_trace): {start, states done, barrier passed, decided}
+    unsigned long long* trace = g_ctaTrace ? g_ctaTrace + (static_cast<size_t>(k % kTraceSlots) * gridDim.x + blockIdx.x) * 4
+                                           : nullptr;
+    if (trace && tid == 0) trace[0] = global_ns();
     unsigned long long* slot = A.slots + static_cast<size_t>(k % 3) * A.njobs * MORAP_MAX_RHS;
     for (int q = tid; q < kPersistJobs * MORAP_MAX_RHS; q += blockDim.x) sDelta[q] = 0ull;
     __syncthreads();
@@ -2116,11 +2120,13 @@ __global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_pe
     }
     flush();
     __syncthreads();
+    if (trace && tid == 0) trace[1] = global_ns();
     for (int q = tid; q < kPersistJobs * MORAP_MAX_RHS; q += blockDim.x) {
       const int jj = jBase + q / MORAP_MAX_RHS;
       if (sDelta[q] && jj < A.njobs) atomicMax(&slot[jj * MORAP_MAX_RHS + (q % MORAP_MAX_RHS)], sDelta[q]);
     }
     grid_barrier(A.barCount, A.barGen, gridDim.x);
+    if (trace && tid == 0) trace[2] = global_ns();
     // every CTA takes the same decisions (numerics.hpp:105-112)
     if (tid == 0) sActive = 0;
     __syncthreads();
@@ -2150,6 +2156,7 @@ __global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_pe
         for (int o = 0; o < MORAP_MAX_RHS; ++o) nextClear[jj * MORAP_MAX_RHS + o] = 0ull;
     }
     __syncthreads();
+    if (trace && tid == 0) trace[3] = global_ns();
     if (!sActive) {
       if (blockIdx.x == 0) {
         if (tid == 0) A.ctl->sweepsDone = k + 1;
@@ -2163,6 +2170,8 @@ __global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_pe
     // above and is next written two barriers from now
   }
 }
+
+#include "eval_interleaved.cuh"
 
 // --------------------------------------------------------------------------------------
 // K2: fused multi-RHS fixed-scheduler sweep (numerics.hpp:140-153 with a deterministic
@@ -2511,6 +2520,7 @@ struct morap_ctx {
   bool usePersistent = true;  // evaluate batches as one cooperative launch
   int persistBlocks = 0;
   bool usePersistCache = false;
+  bool useInterleaved = false;  // k_eval_interleaved for cached-chain evaluate batches
   unsigned* dBar = nullptr;   // grid-barrier counter + generation
   unsigned* dFinCount = nullptr;  // CTAs done in the current compact sweep (fused finalize)
   void* persistArena = nullptr;
@@ -3476,7 +3486,11 @@ int run_eval_persistent(morap_ctx* ctx, int njobs, double eps, int cap) {
   std::vector<long long> prefix(static_cast<size_t>(njobs) + 1, 0);
   for (int j = 0; j < njobs; ++j) prefix[j + 1] = prefix[j] + ctx->hm[ctx->hEvalJobs[j].model].S;
   const size_t slotBytes = 3ull * njobs * MORAP_MAX_RHS * sizeof(unsigned long long);
-  const size_t need = align_up(slotBytes, 256) + align_up(8ull * (njobs + 1), 256);
+  int maxRhs = 1;
+  for (int j = 0; j < njobs; ++j) maxRhs = std::max(maxRhs, ctx->hEvalJobs[j].nrhs);
+  const int R = maxRhs <= 2 ? 2 : 4;
+  const size_t interBytes = 3ull * prefix[njobs] * R * sizeof(double);  // xi (2 parities) + rhoI
+  const size_t need = align_up(slotBytes, 256) + align_up(8ull * (njobs + 1), 256) + align_up(interBytes, 256);
   int rc;
   if ((rc = ensure_arena(ctx, &ctx->persistArena, &ctx->persistArenaBytes, need))) return rc;
   char* base = static_cast<char*>(ctx->persistArena);
@@ -3503,13 +3517,28 @@ int run_eval_persistent(morap_ctx* ctx, int njobs, double eps, int cap) {
   const long long per = (prefix[njobs] + ctx->persistBlocks - 1) / ctx->persistBlocks;
   bool narrow = true;
   for (int j = 0; j < njobs && narrow; ++j) narrow = ctx->hm[ctx->hEvalJobs[j].model].maxRowNnz <= 2;
-  const size_t cacheBytes = static_cast<size_t>((per + 15) & ~15ll) + 24ull * static_cast<size_t>(per);
+  const size_t cacheBytes = static_cast<size_t>((per + 15) & ~15ll) + 24ull * static_cast<size_t>(per) + 16;
   a.cacheStates = (narrow && ctx->usePersistCache && cacheBytes <= kPersistCacheBytes) ? static_cast<int>(per) : 0;
+  // interleaved RHS (k_eval_interleaved) whenever the chains are cached: every job <= 4 RHS here
+  InterArgs ia{a, nullptr, nullptr, R};
+  const bool inter = a.cacheStates > 0 && ctx->useInterleaved;
+  if (inter) {
+    char* ib = base + align_up(slotBytes, 256) + align_up(8ull * (njobs + 1), 256);
+    ia.xi = reinterpret_cast<double*>(ib);
+    ia.rhoI = ia.xi + 2ull * prefix[njobs] * R;
+    CK(cudaMemsetAsync(ia.xi, 0, 2ull * prefix[njobs] * R * sizeof(double), ctx->stream));
+  }
   void* args[] = {&a};
+  void* iargs[] = {&ia};
   const bool timed = ctx->profiling;
   if (timed) CK(cudaEventRecord(ctx->ev0, ctx->stream));
-  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_eval_persistent), dim3(ctx->persistBlocks), dim3(kPersistThreads),
-                                 args, a.cacheStates ? cacheBytes : 0, ctx->stream));
+  if (inter)
+    CK(cudaLaunchCooperativeKernel(R == 2 ? reinterpret_cast<void*>(k_eval_interleaved<2>)
+                                          : reinterpret_cast<void*>(k_eval_interleaved<4>),
+                                   dim3(ctx->persistBlocks), dim3(kPersistThreads), iargs, cacheBytes, ctx->stream));
+  else
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_eval_persistent), dim3(ctx->persistBlocks),
+                                   dim3(kPersistThreads), args, a.cacheStates ? cacheBytes : 0, ctx->stream));
   if (timed) CK(cudaEventRecord(ctx->ev1, ctx->stream));
   ctx->stats[8] += 1;
   CK(d2h(ctx, ctx->hCtl, ctx->dCtl, sizeof(Ctl)));
@@ -3692,6 +3721,15 @@ int morap_cuda_create(int device, morap_ctx** out) {
   int coop = 0;
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
   cudaFuncSetAttribute(k_eval_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, kPersistCacheBytes);
+  cudaFuncSetAttribute(k_eval_interleaved<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPersistCacheBytes);
+  cudaFuncSetAttribute(k_eval_interleaved<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPersistCacheBytes);
+  {
+    int o2 = 0, o4 = 0;  // the interleaved kernel must keep the cooperative grid resident too
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_eval_interleaved<2>, kPersistThreads, kPersistCacheBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k_eval_interleaved<4>, kPersistThreads, kPersistCacheBytes);
+    const char* ie = std::getenv("MORAP_EVAL_INTERLEAVED");  // "0": per-RHS layout (A/B)
+    ctx->useInterleaved = std::min(o2, o4) >= std::max(1, occP) && !(ie && std::string(ie) == "0");
+  }
   {
     int occCache = 0;  // the chain cache must not cost the cooperative grid its residency
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occCache, k_eval_persistent, kPersistThreads, kPersistCacheBytes);
