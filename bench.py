@@ -409,6 +409,7 @@ def run_ours(args):
     cfg, thr, eps, K = workload(args.workload, 1)
     cap = ITER_CAP.get(args.workload, 500)
     streamed = STREAMED.get(args.workload)
+    image_s = None
     solver = Solver(local)
     solver.set_fingerprints(False)  # scheduler hashes are test evidence, not part of paretoPoint
     stream = torch.cuda.Stream()  # the library launches on this stream; the CUDA events below are recorded on it
@@ -422,7 +423,9 @@ def run_ours(args):
         inst = Instance.warehouse(cfg)
         if K > 2:
             inst.add_objectives(K, seed=7)
-        solver.upload(inst)
+        t1 = time.time()
+        solver.upload(inst)  # first upload: the product builder's packed image + its copy
+        image_s = time.time() - t1
     gen_s = time.time() - t0
     for _ in range(max(args.warmup, 0)):
         solver.pareto(inst, thr, eps=eps, iteration_cap=cap)
@@ -461,9 +464,11 @@ def run_ours(args):
                "h2d_bytes_per_step": ecs["upload_bytes"] / args.steps,
                "d2h_bytes_per_step": ecs["d2h_bytes"] / args.steps, "steps": args.steps,
                "ms_per_step": e_ms / args.steps, "pareto_query_ms": e_ms / args.steps,
-               "what": "release + re-upload of the instance's products from host memory (tiling and compact "
-                       "streams built on the host, H2D), the query, and every result read (D2H), per step; "
-                       "bytes counted by the library's copy calls"}
+               "what": "release + re-upload of the instance's products from host memory -- the product "
+                       "builder's packed device image (validated, tiled, compact streams; built once per "
+                       "instance on the host threads, pinned) in one H2D copy -- then the query and every "
+                       "result read (D2H), per step; bytes counted by the library's copy calls",
+               "first_upload_s": round(image_s, 4) if image_s is not None else None}
     else:
         e2e = {"value": None, "unit": UNIT, "note": f"streamed instance: products are built, uploaded lean and "
                                                    f"dropped on the host in chunks of {streamed} "

@@ -63,6 +63,7 @@ enum {
 #define MORAP_MAX_RHS 8        /* reward vectors evaluated together in one fused sweep */
 
 typedef struct morap_ctx morap_ctx;
+typedef struct morap_image morap_image;
 
 /* Host view of one product MDP (ProductMdp, model.hpp:143-157): CSR in the reference
  * layout. rewards[k] has num_rows entries: rewards[0] = cost, rewards[1] = success
@@ -96,6 +97,15 @@ const char* morap_cuda_last_error(morap_ctx* ctx);
  * Validates CSR structure (offsets monotone, successors in range) -> MORAP_INVALID_MODEL. */
 int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models, int32_t* model_ids_out);
 int morap_cuda_release_models(morap_ctx* ctx);
+/* The same upload in two steps: morap_cuda_build_image does everything but the copy --
+ * validation, tiling and the compact streams on the host threads, packed in the device
+ * layout into pinned host memory (the product builder's batched-CSR output, built once
+ * per instance; it honours the context's lean setting); morap_cuda_upload_image then
+ * moves it to the device in one copy and returns model ids as morap_cuda_upload does.
+ * An image can be uploaded any number of times (e.g. after morap_cuda_release_models). */
+int morap_cuda_build_image(morap_ctx* ctx, int nmodels, const morap_csr_view* models, morap_image** image_out);
+int morap_cuda_upload_image(morap_ctx* ctx, const morap_image* image, int32_t* model_ids_out);
+void morap_cuda_free_image(morap_image* image);
 /* Lean uploads (for instances that do not fit otherwise, e.g. 100 x 100): a model with a
  * compact alphabet (<= 256 distinct probabilities and objective tuples) is stored without
  * its fp64 prob / objective arrays -- the device reads the exact same values from the

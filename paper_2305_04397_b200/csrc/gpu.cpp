@@ -80,6 +80,7 @@ GpuBackend::GpuBackend(int device) : device_(device) {
 }
 
 GpuBackend::~GpuBackend() {
+  if (image_) morap_cuda_free_image(image_);
   if (ctx_) morap_cuda_destroy(ctx_);
 }
 
@@ -131,13 +132,43 @@ int GpuBackend::modelIdFor(uint64_t uid, const morap_csr_view& view) {
 
 void GpuBackend::setLean(bool on) { leanDefault_ = on; }
 
+// A whole instance goes through a cached device image (morap_cuda_build_image): the
+// product builder's packed output for these products stays in pinned host memory, so
+// re-uploading the same instance (after release(), or on a fresh context of the same
+// device) is a single host-to-device copy.
 void GpuBackend::uploadInstance(const MorapInstance& inst) {
   std::vector<const ProductMdp*> todo;
   std::set<uint64_t> queued;
   for (const auto& row : inst.products)
     for (const auto& p : row)
       if (!ids_.count(p->uid) && queued.insert(p->uid).second) todo.push_back(p.get());
-  uploadProducts(todo, leanDefault_ && inst.objectives <= 4);
+  if (todo.empty()) return;
+  const bool lean = leanDefault_ && inst.objectives <= 4;
+  std::vector<uint64_t> key{lean ? 1ull : 0ull};
+  for (const ProductMdp* p : todo) {
+    if (p->slim) {  // streamed / slimmed products have no host arrays to image
+      uploadProducts(todo, lean);
+      return;
+    }
+    key.push_back(p->uid);
+  }
+  if (!image_ || imageKey_ != key) {
+    if (image_) morap_cuda_free_image(image_);
+    image_ = nullptr;
+    std::vector<std::vector<const double*>> objs(todo.size());
+    std::vector<std::vector<uint8_t>> done(todo.size());
+    std::vector<morap_csr_view> views(todo.size());
+    for (size_t k = 0; k < todo.size(); ++k) {
+      objs[k] = objectivesOf(*todo[k]);
+      views[k] = viewOf(*todo[k], objs[k], done[k]);
+    }
+    check(ctx_, morap_cuda_set_lean(ctx_, lean ? 1 : 0), "set lean");
+    check(ctx_, morap_cuda_build_image(ctx_, static_cast<int>(todo.size()), views.data(), &image_), "build image");
+    imageKey_ = std::move(key);
+  }
+  std::vector<int32_t> ids(todo.size());
+  check(ctx_, morap_cuda_upload_image(ctx_, image_, ids.data()), "upload instance");
+  for (size_t k = 0; k < todo.size(); ++k) ids_.emplace(todo[k]->uid, ids[k]);
 }
 
 void GpuBackend::uploadProducts(const std::vector<const ProductMdp*>& products, bool lean) {

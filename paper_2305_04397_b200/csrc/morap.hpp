@@ -274,6 +274,8 @@ class GpuBackend {
   std::map<uint64_t, int> ids_;      // ProductMdp::uid -> device model id (query uploads)
   std::map<uint64_t, int> fullIds_;  // full copies of lean products (explicit-reward jobs)
   bool leanDefault_ = true;
+  morap_image* image_ = nullptr;   // cached packed image of the last uploaded instance
+  std::vector<uint64_t> imageKey_;  // lean flag + product uids it holds
   bool isLean(int id);
 };
 

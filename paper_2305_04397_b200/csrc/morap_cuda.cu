@@ -3676,6 +3676,273 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
   return MORAP_OK;
 }
 
+// ---- upload pipeline: prepare (validate, tile, compact) -> pack -> copy -> register ----
+// A batch of models is packed into one device block; `morap_image` keeps a packed batch in
+// pinned host memory with its DevModel records relative to kImageBase, so re-uploading the
+// same products is one H2D copy (the product builder's device-layout output).
+
+struct UploadPrep {
+  std::vector<std::vector<int32_t>> tiles;
+  std::vector<std::vector<TileDesc>> descs;
+  std::vector<CompactStream> compact;
+  std::vector<int32_t> maxRowNnz;
+  std::vector<size_t> off;  // byte offset of each model in the block
+  std::vector<char> lean;   // stored without fp64 prob / objectives
+  size_t bytes = 0;
+};
+
+int prepare_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, UploadPrep& P) {
+  P.tiles.assign(nmodels, {});
+  P.descs.assign(nmodels, {});
+  P.compact.assign(nmodels, CompactStream{});
+  P.maxRowNnz.assign(nmodels, 0);
+  auto& tiles = P.tiles;
+  auto& descs = P.descs;
+  auto& compact = P.compact;
+  auto& maxRowNnz = P.maxRowNnz;
+  std::vector<int> status(nmodels, MORAP_OK);
+  std::vector<std::string> why(nmodels);
+  const auto tu0 = std::chrono::steady_clock::now();
+  auto lapU = [&](const char* what) {
+    if (ctx->trace)
+      std::fprintf(stderr, "[morap] upload %d models: %s at %.3f ms\n", nmodels, what,
+                   1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tu0).count());
+  };
+  std::atomic<long long> phaseNs[4] = {0, 0, 0, 0};  // trace: validate, tiles, compact, streams
+  parallel_for(nmodels, [&](int m) {
+    morap_ctx scratch;  // per-model error text
+    auto tp = std::chrono::steady_clock::now();
+    auto lapP = [&](int k) {
+      if (!ctx->trace) return;
+      const auto now = std::chrono::steady_clock::now();
+      phaseNs[k] += std::chrono::duration_cast<std::chrono::nanoseconds>(now - tp).count();
+      tp = now;
+    };
+    status[m] = validate_view(&scratch, models[m], m);
+    lapP(0);
+    if (status[m]) {
+      why[m] = scratch.err;
+      return;
+    }
+    make_tiles(models[m], tiles[m], descs[m]);
+    for (int r = 0; r < models[m].num_rows; ++r)
+      maxRowNnz[m] = std::max(maxRowNnz[m], models[m].trn_offset[r + 1] - models[m].trn_offset[r]);
+    lapP(1);
+    if (ctx->useCompact) {
+      build_compact(models[m], compact[m]);
+      lapP(2);
+      if (compact[m].ok) layout_streams(models[m], descs[m], compact[m]);
+      lapP(3);
+    }
+  });
+  if (ctx->trace)
+    std::fprintf(stderr, "[morap] upload prep thread-ms: validate %.1f, tiles %.1f, compact %.1f, streams %.1f\n",
+                 phaseNs[0] * 1e-6, phaseNs[1] * 1e-6, phaseNs[2] * 1e-6, phaseNs[3] * 1e-6);
+  for (int m = 0; m < nmodels; ++m)
+    if (status[m]) return ctx->fail(status[m], why[m]);
+  lapU("validated, tiled, compacted");
+  // every array of the batch in one block
+  size_t bytes = 0;
+  auto& off = P.off;
+  off.assign(nmodels, 0);
+  P.lean.assign(nmodels, 0);
+  for (int m = 0; m < nmodels; ++m) {
+    const morap_csr_view& v = models[m];
+    off[m] = bytes;
+    const bool lean = ctx->lean && compact[m].ok && ctx->useTma;
+    P.lean[m] = lean;
+    bytes += align_up(4ull * (v.num_states + 1), 256) + align_up(4ull * (v.num_rows + 1), 256) +
+             align_up(4ull * v.nnz, 256) + (lean ? 0 : align_up(8ull * v.nnz, 256)) + align_up(1ull * v.num_states, 256) +
+             (lean ? 0 : static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256)) +
+             align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
+    if (compact[m].ok)
+      bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(2ull * v.num_rows, 256) +
+               align_up(8ull * compact[m].table.size(), 256) + align_up(4ull * compact[m].nTrW, 256) +
+               align_up(4ull * compact[m].nStW, 256) + align_up(4ull * compact[m].nRowW, 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256) +
+               align_up(4ull * compact[m].outIdx.size(), 256) + align_up(4ull * compact[m].outGrp.size(), 256);
+  }
+  P.bytes = bytes;
+  return MORAP_OK;
+}
+
+// Packs every model into `host` (layout of P) with DevModel pointers into `devBase`; with
+// `dev` set, each model's block is copied as soon as it is packed (copies overlap packing).
+void pack_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, const UploadPrep& P, char* host,
+                 char* devBase, bool copy, std::vector<DevModel>& built, std::atomic<bool>& copyFailed,
+                 std::atomic<long long>& uploadBytes) {
+  const auto& tiles = P.tiles;
+  const auto& descs = P.descs;
+  const auto& compact = P.compact;
+  const auto& off = P.off;
+  void* dev = devBase;
+  parallel_for(nmodels, [&](int m) {
+    const morap_csr_view& v = models[m];
+    char* h = host + off[m];
+    char* d = static_cast<char*>(dev) + off[m];
+    DevModel dmod{};
+    auto put = [&](const void* src, size_t n) {  // src == nullptr: reserve (filled by the caller)
+      if (n && src) std::memcpy(h, src, n);
+      char* at = d;
+      const size_t a = align_up(n, 256);
+      h += a;
+      d += a;
+      return at;
+    };
+    dmod.rowOffset = reinterpret_cast<const int32_t*>(put(v.row_offset, 4ull * (v.num_states + 1)));
+    dmod.trnOffset = reinterpret_cast<const int32_t*>(put(v.trn_offset, 4ull * (v.num_rows + 1)));
+    dmod.succ = reinterpret_cast<const int32_t*>(put(v.succ, 4ull * v.nnz));
+    const bool lean = P.lean[m];  // fp64 prob / objectives live in the tables
+    if (!lean) dmod.prob = reinterpret_cast<const double*>(put(v.prob, 8ull * v.nnz));
+    dmod.done = reinterpret_cast<const uint8_t*>(put(v.done, v.num_states));
+    if (!lean)
+      for (int o = 0; o < v.num_objectives; ++o)
+        dmod.obj[o] = reinterpret_cast<const double*>(put(v.rewards[o], 8ull * v.num_rows));
+    dmod.tileStart = reinterpret_cast<const int32_t*>(put(tiles[m].data(), 4ull * tiles[m].size()));
+    dmod.tiles = reinterpret_cast<const TileDesc*>(put(descs[m].data(), sizeof(TileDesc) * descs[m].size()));
+    dmod.S = v.num_states;
+    dmod.R = v.num_rows;
+    dmod.nnz = v.nnz;
+    dmod.initial = v.initial;
+    dmod.ntiles = static_cast<int32_t>(tiles[m].size() - 1);
+    dmod.K = v.num_objectives;
+    dmod.rewardFinite = v.reward_finite ? 1 : 0;
+    // DESIGN.md §4: succ 4 + prob 8 per nnz; trnOffset 4 + rho 8 per row;
+    // rowOffset 4 + done 1 + x 8 + y 8 per state.
+    dmod.bytesPerSweep = 12ull * v.nnz + 12ull * v.num_rows + 21ull * v.num_states;
+    const CompactStream& c = compact[m];
+    if (c.ok) {
+      dmod.compact = 1;
+      dmod.probIdx = reinterpret_cast<const uint8_t*>(put(c.idx.data(), c.idx.size()));
+      dmod.probDict = reinterpret_cast<const double*>(put(c.dict.data(), 8ull * c.dict.size()));
+      dmod.rclass = reinterpret_cast<const uint16_t*>(put(c.cls.data(), 2ull * c.cls.size()));
+      dmod.classTable = reinterpret_cast<const double*>(put(c.table.data(), 8ull * c.table.size()));
+      dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
+      uint32_t* hs = reinterpret_cast<uint32_t*>(h);
+      dmod.stW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nStW));
+      uint32_t* hr = reinterpret_cast<uint32_t*>(h);
+      dmod.rowW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nRowW));
+      uint32_t* ht = reinterpret_cast<uint32_t*>(h);
+      dmod.trW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nTrW));
+      fill_streams(v, descs[m], c, hs, hr, ht);  // straight into the staging buffer
+      dmod.tilePos = reinterpret_cast<const TilePos*>(put(c.pos.data(), sizeof(TilePos) * c.pos.size()));
+      dmod.outIdx = reinterpret_cast<const int32_t*>(put(c.outIdx.data(), 4ull * c.outIdx.size()));
+      dmod.outGrp = reinterpret_cast<const int32_t*>(put(c.outGrp.data(), 4ull * c.outGrp.size()));
+      // compact stream: one 4-byte word per transition (window offset | index) and per row
+      // (transition end | class) and per state (row end | transition end | done) + x 8 + y 8
+      dmod.bytesPerSweep = 4ull * v.nnz + 4ull * v.num_rows + 20ull * v.num_states;
+    }
+    // evaluate, one RHS over the policy chain: chainOff 4 + done 1 + rhoC 8 + x 8 + y 8 per
+    // state + 12 per chosen transition (mean nnz per row)
+    const double nnzPerRow = v.num_rows ? static_cast<double>(v.nnz) / v.num_rows : 0.0;
+    dmod.bytesPerEval = static_cast<unsigned long long>(v.num_states * (29.0 + 12.0 * nnzPerRow));
+    built[m] = dmod;
+    // this model's block goes out as soon as it is packed (copies overlap the packing)
+    const size_t len = static_cast<size_t>(h - (host + off[m]));
+    uploadBytes += static_cast<long long>(len);
+    if (!copy) return;
+    cudaSetDevice(ctx->device);  // packing runs on pool threads
+    if (cudaMemcpyAsync(static_cast<char*>(dev) + off[m], host + off[m], len, cudaMemcpyHostToDevice, ctx->stream) !=
+        cudaSuccess)
+      copyFailed = true;
+  });
+}
+
+// Appends the packed models to the context's model list and refreshes the device table.
+int register_models(morap_ctx* ctx, const std::vector<DevModel>& built, const std::vector<HostModel>& hmods,
+                    int32_t* ids_out) {
+  const int first = static_cast<int>(ctx->hm.size());
+  for (size_t m = 0; m < built.size(); ++m) {
+    ctx->dm.push_back(built[m]);
+    ctx->hm.push_back(hmods[m]);
+    if (ids_out) ids_out[m] = first + static_cast<int>(m);
+  }
+  int rc;
+  if ((rc = upload_models_table(ctx))) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MORAP_OK;
+}
+
+std::vector<HostModel> host_models(const std::vector<DevModel>& built, const UploadPrep& P) {
+  std::vector<HostModel> out(built.size());
+  for (size_t m = 0; m < built.size(); ++m) {
+    const DevModel& d = built[m];
+    out[m] = HostModel{d.S, d.R, d.nnz, d.initial, d.ntiles, d.K, d.rewardFinite, P.maxRowNnz[m],
+                       static_cast<int32_t>(P.compact[m].outGrp.size())};
+  }
+  return out;
+}
+
+// Device block for `bytes`: a released block that fits (cudaFree of ~1 GB costs up to ~0.8 s
+// on B200), else a fresh allocation.
+int acquire_block(morap_ctx* ctx, size_t bytes, void** out) {
+  void* dev = nullptr;
+  int best = -1;
+  for (int q = 0; q < static_cast<int>(ctx->freeModelAllocs.size()); ++q)
+    if (ctx->freeModelAllocs[q].second >= bytes &&
+        (best < 0 || ctx->freeModelAllocs[q].second < ctx->freeModelAllocs[best].second))
+      best = q;
+  if (best >= 0) {
+    dev = ctx->freeModelAllocs[best].first;
+    ctx->modelAllocs.push_back(dev);
+    ctx->modelAllocBytes.push_back(ctx->freeModelAllocs[best].second);
+    ctx->freeModelAllocs.erase(ctx->freeModelAllocs.begin() + best);
+  } else {
+    if (cudaMalloc(&dev, bytes) != cudaSuccess) {  // give the cached blocks back, retry once
+      cudaGetLastError();
+      for (auto& f : ctx->freeModelAllocs) cudaFree(f.first);
+      ctx->freeModelAllocs.clear();
+      CK(cudaMalloc(&dev, bytes));
+    }
+    ctx->modelAllocs.push_back(dev);
+    ctx->modelAllocBytes.push_back(bytes);
+  }
+  *out = dev;
+  return MORAP_OK;
+}
+
+char* const kImageBase = reinterpret_cast<char*>(uintptr_t{1} << 40);  // DevModel pointers of an image
+
+template <class T>
+void relocate(T*& p, char* to) {
+  if (p) p = reinterpret_cast<T*>(to + (reinterpret_cast<const char*>(p) - kImageBase));
+}
+
+DevModel relocated(DevModel d, char* to) {
+  relocate(d.rowOffset, to);
+  relocate(d.trnOffset, to);
+  relocate(d.succ, to);
+  relocate(d.prob, to);
+  relocate(d.done, to);
+  for (auto& o : d.obj) relocate(o, to);
+  relocate(d.tiles, to);
+  relocate(d.tileStart, to);
+  relocate(d.probIdx, to);
+  relocate(d.probDict, to);
+  relocate(d.rclass, to);
+  relocate(d.classTable, to);
+  relocate(d.stW, to);
+  relocate(d.rowW, to);
+  relocate(d.trW, to);
+  relocate(d.tilePos, to);
+  relocate(d.outIdx, to);
+  relocate(d.outGrp, to);
+  return d;
+}
+
+}  // namespace
+
+struct morap_image {
+  int device = 0;
+  size_t bytes = 0;
+  void* host = nullptr;           // pinned
+  std::vector<DevModel> dm;       // pointers relative to kImageBase
+  std::vector<HostModel> hm;
+  ~morap_image() {
+    if (host) cudaFreeHost(host);
+  }
+};
+
+namespace {
 }  // namespace
 
 // ======================================================================================
@@ -3845,189 +4112,67 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   if (nmodels == 0) return MORAP_OK;
   cudaSetDevice(ctx->device);
   int rc;
-  // validation and tiling of every model on all host threads (first failure in model order)
-  std::vector<std::vector<int32_t>> tiles(nmodels);
-  std::vector<std::vector<TileDesc>> descs(nmodels);
-  std::vector<int> status(nmodels, MORAP_OK);
-  std::vector<std::string> why(nmodels);
-  std::vector<CompactStream> compact(nmodels);
-  std::vector<int32_t> maxRowNnz(nmodels, 0);
-  const auto tu0 = std::chrono::steady_clock::now();
-  auto lapU = [&](const char* what) {
-    if (ctx->trace)
-      std::fprintf(stderr, "[morap] upload %d models: %s at %.3f ms\n", nmodels, what,
-                   1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tu0).count());
-  };
-  std::atomic<long long> phaseNs[4] = {0, 0, 0, 0};  // trace: validate, tiles, compact, streams
-  parallel_for(nmodels, [&](int m) {
-    morap_ctx scratch;  // per-model error text
-    auto tp = std::chrono::steady_clock::now();
-    auto lapP = [&](int k) {
-      if (!ctx->trace) return;
-      const auto now = std::chrono::steady_clock::now();
-      phaseNs[k] += std::chrono::duration_cast<std::chrono::nanoseconds>(now - tp).count();
-      tp = now;
-    };
-    status[m] = validate_view(&scratch, models[m], m);
-    lapP(0);
-    if (status[m]) {
-      why[m] = scratch.err;
-      return;
-    }
-    make_tiles(models[m], tiles[m], descs[m]);
-    for (int r = 0; r < models[m].num_rows; ++r)
-      maxRowNnz[m] = std::max(maxRowNnz[m], models[m].trn_offset[r + 1] - models[m].trn_offset[r]);
-    lapP(1);
-    if (ctx->useCompact) {
-      build_compact(models[m], compact[m]);
-      lapP(2);
-      if (compact[m].ok) layout_streams(models[m], descs[m], compact[m]);
-      lapP(3);
-    }
-  });
-  if (ctx->trace)
-    std::fprintf(stderr, "[morap] upload prep thread-ms: validate %.1f, tiles %.1f, compact %.1f, streams %.1f\n",
-                 phaseNs[0] * 1e-6, phaseNs[1] * 1e-6, phaseNs[2] * 1e-6, phaseNs[3] * 1e-6);
-  for (int m = 0; m < nmodels; ++m)
-    if (status[m]) return ctx->fail(status[m], why[m]);
-  lapU("validated, tiled, compacted");
-  // pack every array of the batch into one device allocation
-  size_t bytes = 0;
-  std::vector<size_t> off(nmodels);
-  for (int m = 0; m < nmodels; ++m) {
-    const morap_csr_view& v = models[m];
-    off[m] = bytes;
-    const bool lean = ctx->lean && compact[m].ok && ctx->useTma;
-    bytes += align_up(4ull * (v.num_states + 1), 256) + align_up(4ull * (v.num_rows + 1), 256) +
-             align_up(4ull * v.nnz, 256) + (lean ? 0 : align_up(8ull * v.nnz, 256)) + align_up(1ull * v.num_states, 256) +
-             (lean ? 0 : static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256)) +
-             align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
-    if (compact[m].ok)
-      bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(2ull * v.num_rows, 256) +
-               align_up(8ull * compact[m].table.size(), 256) + align_up(4ull * compact[m].nTrW, 256) +
-               align_up(4ull * compact[m].nStW, 256) + align_up(4ull * compact[m].nRowW, 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256) +
-               align_up(4ull * compact[m].outIdx.size(), 256) + align_up(4ull * compact[m].outGrp.size(), 256);
-  }
+  UploadPrep P;
+  if ((rc = prepare_models(ctx, nmodels, models, P))) return rc;
   void* dev = nullptr;
-  {
-    int best = -1;
-    for (int q = 0; q < static_cast<int>(ctx->freeModelAllocs.size()); ++q)
-      if (ctx->freeModelAllocs[q].second >= bytes &&
-          (best < 0 || ctx->freeModelAllocs[q].second < ctx->freeModelAllocs[best].second))
-        best = q;
-    if (best >= 0) {
-      dev = ctx->freeModelAllocs[best].first;
-      ctx->modelAllocs.push_back(dev);
-      ctx->modelAllocBytes.push_back(ctx->freeModelAllocs[best].second);
-      ctx->freeModelAllocs.erase(ctx->freeModelAllocs.begin() + best);
-    } else {
-      if (cudaMalloc(&dev, bytes) != cudaSuccess) {  // give the cached blocks back, retry once
-        cudaGetLastError();
-        for (auto& f : ctx->freeModelAllocs) cudaFree(f.first);
-        ctx->freeModelAllocs.clear();
-        CK(cudaMalloc(&dev, bytes));
-      }
-      ctx->modelAllocs.push_back(dev);
-      ctx->modelAllocBytes.push_back(bytes);
-    }
-  }
-  if (bytes > ctx->stageBytes) {  // pinned staging, grow-only (reused by later uploads)
+  if ((rc = acquire_block(ctx, P.bytes, &dev))) return rc;
+  if (P.bytes > ctx->stageBytes) {  // pinned staging, grow-only (reused by later uploads)
     cudaFreeHost(ctx->stage);
     ctx->stage = nullptr;
     ctx->stageBytes = 0;
-    CK(cudaMallocHost(&ctx->stage, bytes));
-    ctx->stageBytes = bytes;
+    CK(cudaMallocHost(&ctx->stage, P.bytes));
+    ctx->stageBytes = P.bytes;
   }
-  char* host = static_cast<char*>(ctx->stage);
-  const int first = static_cast<int>(ctx->hm.size());
   std::vector<DevModel> built(nmodels);
   std::atomic<bool> copyFailed{false};
   std::atomic<long long> uploadBytes{0};
-  parallel_for(nmodels, [&](int m) {
-    const morap_csr_view& v = models[m];
-    char* h = host + off[m];
-    char* d = static_cast<char*>(dev) + off[m];
-    DevModel dmod{};
-    auto put = [&](const void* src, size_t n) {  // src == nullptr: reserve (filled by the caller)
-      if (n && src) std::memcpy(h, src, n);
-      char* at = d;
-      const size_t a = align_up(n, 256);
-      h += a;
-      d += a;
-      return at;
-    };
-    dmod.rowOffset = reinterpret_cast<const int32_t*>(put(v.row_offset, 4ull * (v.num_states + 1)));
-    dmod.trnOffset = reinterpret_cast<const int32_t*>(put(v.trn_offset, 4ull * (v.num_rows + 1)));
-    dmod.succ = reinterpret_cast<const int32_t*>(put(v.succ, 4ull * v.nnz));
-    const bool lean = ctx->lean && compact[m].ok && ctx->useTma;  // fp64 prob / objectives live in the tables
-    if (!lean) dmod.prob = reinterpret_cast<const double*>(put(v.prob, 8ull * v.nnz));
-    dmod.done = reinterpret_cast<const uint8_t*>(put(v.done, v.num_states));
-    if (!lean)
-      for (int o = 0; o < v.num_objectives; ++o)
-        dmod.obj[o] = reinterpret_cast<const double*>(put(v.rewards[o], 8ull * v.num_rows));
-    dmod.tileStart = reinterpret_cast<const int32_t*>(put(tiles[m].data(), 4ull * tiles[m].size()));
-    dmod.tiles = reinterpret_cast<const TileDesc*>(put(descs[m].data(), sizeof(TileDesc) * descs[m].size()));
-    dmod.S = v.num_states;
-    dmod.R = v.num_rows;
-    dmod.nnz = v.nnz;
-    dmod.initial = v.initial;
-    dmod.ntiles = static_cast<int32_t>(tiles[m].size() - 1);
-    dmod.K = v.num_objectives;
-    dmod.rewardFinite = v.reward_finite ? 1 : 0;
-    // DESIGN.md §4: succ 4 + prob 8 per nnz; trnOffset 4 + rho 8 per row;
-    // rowOffset 4 + done 1 + x 8 + y 8 per state.
-    dmod.bytesPerSweep = 12ull * v.nnz + 12ull * v.num_rows + 21ull * v.num_states;
-    const CompactStream& c = compact[m];
-    if (c.ok) {
-      dmod.compact = 1;
-      dmod.probIdx = reinterpret_cast<const uint8_t*>(put(c.idx.data(), c.idx.size()));
-      dmod.probDict = reinterpret_cast<const double*>(put(c.dict.data(), 8ull * c.dict.size()));
-      dmod.rclass = reinterpret_cast<const uint16_t*>(put(c.cls.data(), 2ull * c.cls.size()));
-      dmod.classTable = reinterpret_cast<const double*>(put(c.table.data(), 8ull * c.table.size()));
-      dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
-      uint32_t* hs = reinterpret_cast<uint32_t*>(h);
-      dmod.stW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nStW));
-      uint32_t* hr = reinterpret_cast<uint32_t*>(h);
-      dmod.rowW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nRowW));
-      uint32_t* ht = reinterpret_cast<uint32_t*>(h);
-      dmod.trW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nTrW));
-      fill_streams(v, descs[m], c, hs, hr, ht);  // straight into the staging buffer
-      dmod.tilePos = reinterpret_cast<const TilePos*>(put(c.pos.data(), sizeof(TilePos) * c.pos.size()));
-      dmod.outIdx = reinterpret_cast<const int32_t*>(put(c.outIdx.data(), 4ull * c.outIdx.size()));
-      dmod.outGrp = reinterpret_cast<const int32_t*>(put(c.outGrp.data(), 4ull * c.outGrp.size()));
-      // compact stream: one 4-byte word per transition (window offset | index) and per row
-      // (transition end | class) and per state (row end | transition end | done) + x 8 + y 8
-      dmod.bytesPerSweep = 4ull * v.nnz + 4ull * v.num_rows + 20ull * v.num_states;
-    }
-    // evaluate, one RHS over the policy chain: chainOff 4 + done 1 + rhoC 8 + x 8 + y 8 per
-    // state + 12 per chosen transition (mean nnz per row)
-    const double nnzPerRow = v.num_rows ? static_cast<double>(v.nnz) / v.num_rows : 0.0;
-    dmod.bytesPerEval = static_cast<unsigned long long>(v.num_states * (29.0 + 12.0 * nnzPerRow));
-    built[m] = dmod;
-    // this model's block goes out as soon as it is packed (copies overlap the packing)
-    const size_t len = static_cast<size_t>(h - (host + off[m]));
-    uploadBytes += static_cast<long long>(len);
-    cudaSetDevice(ctx->device);  // packing runs on pool threads
-    if (cudaMemcpyAsync(static_cast<char*>(dev) + off[m], host + off[m], len, cudaMemcpyHostToDevice, ctx->stream) !=
-        cudaSuccess)
-      copyFailed = true;
-  });
-  for (int m = 0; m < nmodels; ++m) {
-    const DevModel& dmod = built[m];
-    ctx->dm.push_back(dmod);
-    ctx->hm.push_back(HostModel{dmod.S, dmod.R, dmod.nnz, dmod.initial, dmod.ntiles, dmod.K, dmod.rewardFinite,
-                                maxRowNnz[m], static_cast<int32_t>(compact[m].outGrp.size())});
-    if (ids_out) ids_out[m] = first + m;
-  }
-  lapU("packed, copies queued");
+  pack_models(ctx, nmodels, models, P, static_cast<char*>(ctx->stage), static_cast<char*>(dev), true, built, copyFailed,
+              uploadBytes);
   ctx->stats[9] += static_cast<double>(uploadBytes.load());
   cudaError_t e = copyFailed ? cudaErrorUnknown : cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return ctx->cudaFail(e, "upload copy", __LINE__);
-  lapU("copied");
-  if ((rc = upload_models_table(ctx))) return rc;
-  CK(cudaStreamSynchronize(ctx->stream));
+  return register_models(ctx, built, host_models(built, P), ids_out);
+}
+
+int morap_cuda_build_image(morap_ctx* ctx, int nmodels, const morap_csr_view* models, morap_image** out) {
+  if (!ctx || !out) return MORAP_INVALID_CONFIG;
+  *out = nullptr;
+  if (nmodels < 0 || (nmodels > 0 && !models)) return ctx->fail(MORAP_INVALID_CONFIG, "bad model list");
+  cudaSetDevice(ctx->device);
+  int rc;
+  UploadPrep P;
+  if (nmodels > 0 && (rc = prepare_models(ctx, nmodels, models, P))) return rc;
+  auto img = std::make_unique<morap_image>();
+  img->device = ctx->device;
+  img->bytes = P.bytes;
+  if (P.bytes) CK(cudaMallocHost(&img->host, P.bytes));
+  img->dm.resize(nmodels);
+  std::atomic<bool> copyFailed{false};
+  std::atomic<long long> uploadBytes{0};
+  if (nmodels > 0)
+    pack_models(ctx, nmodels, models, P, static_cast<char*>(img->host), kImageBase, false, img->dm, copyFailed,
+                uploadBytes);
+  img->hm = host_models(img->dm, P);
+  *out = img.release();
   return MORAP_OK;
 }
+
+int morap_cuda_upload_image(morap_ctx* ctx, const morap_image* img, int32_t* ids_out) {
+  if (!ctx || !img) return MORAP_INVALID_CONFIG;
+  if (img->device != ctx->device) return ctx->fail(MORAP_INVALID_CONFIG, "image was built for another device");
+  if (img->dm.empty()) return MORAP_OK;
+  cudaSetDevice(ctx->device);
+  int rc;
+  void* dev = nullptr;
+  if ((rc = acquire_block(ctx, img->bytes, &dev))) return rc;
+  CK(cudaMemcpyAsync(dev, img->host, img->bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->stats[9] += static_cast<double>(img->bytes);
+  std::vector<DevModel> built(img->dm.size());
+  for (size_t m = 0; m < built.size(); ++m) built[m] = relocated(img->dm[m], static_cast<char*>(dev));
+  return register_models(ctx, built, img->hm, ids_out);
+}
+
+void morap_cuda_free_image(morap_image* img) { delete img; }
 
 int morap_cuda_release_models(morap_ctx* ctx) {
   if (!ctx) return MORAP_INVALID_CONFIG;

@@ -129,15 +129,18 @@ SupportingPoint supportingPoint(const MorapInstance& inst, const Vec& w, GpuBack
     for (int k = 0; k < K; ++k) out.r[coord(k, i, j)] = ev[static_cast<size_t>(j) * K + k];
   }
   // the n schedulers of the assigned pairs (IterationRecord::schedulers, solver.hpp:38-45),
-  // copied out of the pinned staging area on the host threads (page faults of the fresh
-  // vectors included)
+  // copied out of the pinned staging area on the host threads
   const auto t3 = std::chrono::steady_clock::now();
   std::vector<const int32_t*> rowsIn(static_cast<size_t>(n));
   ck(ctx, morap_cuda_policy_views(ctx, n, evalJobs.data(), rowsIn.data()), "fetch policies");
   const auto t3b = std::chrono::steady_clock::now();
+  // (allocated here, on the calling thread: its heap keeps the pages of earlier queries'
+  // schedulers, so the copies do not fault; pool threads would each allocate in their own
+  // malloc arena)
+  for (int j = 0; j < n; ++j)
+    out.schedulers[j].rows.resize(static_cast<size_t>(inst.products[out.assignment.agentOf[j]][j]->mdp.numStates));
   parallelFor(n, [&](int j) {
-    const ProductMdp& p = *inst.products[out.assignment.agentOf[j]][j];
-    out.schedulers[j].rows.assign(rowsIn[j], rowsIn[j] + p.mdp.numStates);
+    std::memcpy(out.schedulers[j].rows.data(), rowsIn[j], sizeof(int32_t) * out.schedulers[j].rows.size());
   });
   if (std::getenv("MORAP_TRACE"))
     std::fprintf(stderr, "[morap] supportingPoint: optimize %.3f ms (%d jobs), assign %.3f ms, evaluate %.3f ms "
