@@ -110,6 +110,32 @@ typedef int (*morap_query_fn)(void* user, const double* w, int d, double* r_out,
 int morap_pareto_core(const double* expanded_thresholds, int d, int n, const double* norm, double eps,
                       int iteration_cap, int verify, morap_query_fn query, void* user, char* json_out, int json_cap);
 
+/* Multi-GPU Pareto query (csrc/shard.cpp). The n x n products are
+ * partitioned over shards by longest-processing-time on nnz (or by the owners of an
+ * instance built with morap_instance_warehouse_shard); per iteration each shard optimizes
+ * its pairs' jobs, the n^2 values are combined (each entry from its owner, exact bits), the
+ * host runs the Hungarian step, each assigned pair is evaluated on its owner and the K*n
+ * values are combined. Results equal morap_pareto's bit for bit.
+ *
+ * One process driving several GPUs (one context and one host thread per device; the
+ * reference's one-engine / several-backend-queues model, engine.hpp:66-72,370-425): */
+typedef struct morap_multi morap_multi;
+int morap_multi_create(const int* devices, int ndevices, morap_multi** out);
+void morap_multi_free(morap_multi* m);
+/* uploads every shard's products to its device (lean when K <= 4) */
+int morap_multi_upload(morap_multi* m, const morap_instance* inst);
+/* owner shard of product (i, j) after morap_multi_upload, -1 if none */
+int morap_multi_owner(const morap_multi* m, int i, int j);
+int morap_multi_pareto(morap_multi* m, const morap_instance* inst, const double* thresholds, int nt, const double* norm,
+                       double eps, int iteration_cap, char* json_out, int json_cap, double* stats_out);
+/* One process per GPU (torch.distributed): `s` holds this rank's shard; `allgather`
+ * (recv[r * count + k] = rank r's send[k], every rank) carries the two exchanges per
+ * iteration -- NCCL over NVLink on GPUs, gloo in the CPU tests. Returns 0 or a status. */
+typedef int (*morap_allgather_fn)(void* user, const double* send, int count, double* recv);
+int morap_shard_pareto(morap_solver* s, const morap_instance* inst, int rank, int world, morap_allgather_fn allgather,
+                       void* user, const double* thresholds, int nt, const double* norm, double eps, int iteration_cap,
+                       char* json_out, int json_cap, double* stats_out);
+
 /* Centralised model (centralised.hpp): buildCentralised (:54-179) with its state guard
  * (MORAP_SIZE_GUARD beyond it), the model's arrays, and centralisedParetoPoint (:216-222)
  * -- one weighted optimize job on the whole model per iteration plus the fused evaluation

@@ -27,6 +27,7 @@ HOST_SO = os.path.join(PKG, "libmorap_host.so")
 
 QUERY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double),
                        C.POINTER(C.c_int32), C.c_int)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double))
 
 _lib = None
 
@@ -70,6 +71,12 @@ def load_host_library() -> C.CDLL:
         "morap_centralised_info": (i32, [p, p]),
         "morap_centralised_export": (i32, [p, p, p, p, p, p, p]),
         "morap_centralised_pareto": (i32, [p, p, p, i32, p, f64, i32, C.c_char_p, i32, p]),
+        "morap_multi_create": (i32, [p, i32, C.POINTER(p)]),
+        "morap_multi_free": (None, [p]),
+        "morap_multi_upload": (i32, [p, p]),
+        "morap_multi_owner": (i32, [p, i32, i32]),
+        "morap_multi_pareto": (i32, [p, p, p, i32, p, f64, i32, C.c_char_p, i32, p]),
+        "morap_shard_pareto": (i32, [p, p, i32, i32, ALLGATHER_FN, p, p, i32, p, f64, i32, C.c_char_p, i32, p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -396,6 +403,84 @@ class Solver:
 
     def verify(self, inst: Instance, thresholds, eps=0.01, norm=None, iteration_cap=500) -> bool:
         return bool(self.pareto(inst, thresholds, eps, norm, iteration_cap, verify=True)["verdict"])
+
+
+_STAT_KEYS = ["optimize_jobs", "optimize_backups", "evaluate_jobs", "evaluate_state_backups", "optimize_s",
+              "evaluate_s", "host_s", "evaluate_batch_s"]
+
+
+class MultiSolver:
+    """One process driving several GPUs (morap_multi_*): one CUDA context and one host
+    thread per device, products sharded by LPT on nnz, results equal Solver.pareto's."""
+
+    def __init__(self, devices):
+        self._lib = load_host_library()
+        devs = np.ascontiguousarray(list(devices), np.int32)
+        h = C.c_void_p()
+        _check(self._lib.morap_multi_create(_ptr(devs), devs.shape[0], C.byref(h)), "multi create")
+        self.h = h
+        self.devices = devs.tolist()
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.morap_multi_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def upload(self, inst: Instance):
+        _check(self._lib.morap_multi_upload(self.h, inst.h), "multi upload")
+
+    def owner(self, i, j) -> int:
+        return int(self._lib.morap_multi_owner(self.h, i, j))
+
+    def pareto(self, inst: Instance, thresholds, eps=0.01, norm=None, iteration_cap=500) -> dict:
+        t = np.ascontiguousarray(thresholds, np.float64)
+        nm = None if norm is None else np.ascontiguousarray(norm, np.float64)
+        buf = C.create_string_buffer(1 << 24)
+        st = np.zeros(8)
+        _check(self._lib.morap_multi_pareto(self.h, inst.h, _ptr(t), t.shape[0], None if nm is None else _ptr(nm), eps,
+                                            iteration_cap, buf, len(buf), _ptr(st)), "multi paretoPoint")
+        out = json.loads(buf.value.decode())
+        out["stats"] = dict(zip(_STAT_KEYS, st[:8].tolist()))
+        return out
+
+
+def shard_pareto(solver: "Solver", inst: Instance, rank: int, world: int, allgather, thresholds, eps=0.01, norm=None,
+                 iteration_cap=500) -> dict:
+    """This rank's part of the multi-GPU query (morap_shard_pareto): allgather(send) -> recv
+    (numpy float64, recv.shape = (world, send.size)) carries the two exchanges per iteration
+    (torch.distributed: NCCL on GPUs, gloo on CPU)."""
+    lib = load_host_library()
+    t = np.ascontiguousarray(thresholds, np.float64)
+    nm = None if norm is None else np.ascontiguousarray(norm, np.float64)
+    err = []
+
+    def cb(user, sp, count, rp):
+        try:
+            send = np.ctypeslib.as_array(sp, shape=(count,)).copy()
+            recv = np.asarray(allgather(send), np.float64).reshape(world * count)
+            np.ctypeslib.as_array(rp, shape=(world * count,))[:] = recv
+            return 0
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+            return 14
+
+    fn = ALLGATHER_FN(cb)
+    buf = C.create_string_buffer(1 << 24)
+    st = np.zeros(8)
+    rc = lib.morap_shard_pareto(solver.h, inst.h, rank, world, fn, None, _ptr(t), t.shape[0],
+                                None if nm is None else _ptr(nm), eps, iteration_cap, buf, len(buf), _ptr(st))
+    if rc != 0 and err:
+        raise err[0]
+    _check(rc, "sharded paretoPoint")
+    out = json.loads(buf.value.decode())
+    out["stats"] = dict(zip(_STAT_KEYS, st[:8].tolist()))
+    return out
 
 
 def pareto_core(thresholds, n, query, eps=0.01, norm=None, iteration_cap=500, verify=False) -> dict:

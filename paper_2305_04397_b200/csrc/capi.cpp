@@ -24,6 +24,12 @@ struct morap_centralised {
   morap::CentralisedMdp c;
 };
 
+struct morap_multi {
+  std::vector<std::unique_ptr<morap::GpuBackend>> gpus;
+  std::vector<std::unique_ptr<morap::Shard>> shards;
+  const morap::MorapInstance* inst = nullptr;
+};
+
 namespace {
 
 thread_local std::string g_error;
@@ -339,6 +345,100 @@ int morap_instance_warehouse_streamed(const char* config_json, int threads, mora
     };
     const std::function<void()> retry = [&] { gpu.release(); };
     *out = new morap_instance{morap::generateInstance(cfg, threads, static_cast<size_t>(chunk), &sink, &retry), {}, {}};
+  });
+}
+
+int morap_multi_create(const int* devices, int ndevices, morap_multi** out) {
+  return guard([&] {
+    if (!out || !devices || ndevices < 1) morap::fail(morap::Errc::InvalidConfig, "need at least one device");
+    auto m = std::make_unique<morap_multi>();
+    for (int d = 0; d < ndevices; ++d) m->gpus.push_back(std::make_unique<morap::GpuBackend>(devices[d]));
+    *out = m.release();
+  });
+}
+
+void morap_multi_free(morap_multi* m) { delete m; }
+
+int morap_multi_upload(morap_multi* m, const morap_instance* p) {
+  return guard([&] {
+    if (!m || !p) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    const int world = static_cast<int>(m->gpus.size());
+    std::vector<int> owner = morap::lptOwners(p->inst, world);
+    m->shards.clear();
+    for (auto& g : m->gpus) g->release();
+    for (int r = 0; r < world; ++r) m->shards.push_back(std::make_unique<morap::Shard>(p->inst, *m->gpus[r], owner, r));
+    std::vector<std::thread> pool;  // one upload thread per device
+    std::vector<std::exception_ptr> err(static_cast<size_t>(world));
+    for (int r = 0; r < world; ++r)
+      pool.emplace_back([&, r] {
+        try {
+          m->shards[r]->upload();
+        } catch (...) {
+          err[r] = std::current_exception();
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
+    m->inst = &p->inst;
+  });
+}
+
+int morap_multi_owner(const morap_multi* m, int i, int j) {
+  if (!m || m->shards.empty() || !m->inst || i < 0 || j < 0 || i >= m->inst->n || j >= m->inst->n) return -1;
+  return m->shards[0]->owners()[static_cast<size_t>(i) * m->inst->n + j];
+}
+
+int morap_multi_pareto(morap_multi* m, const morap_instance* p, const double* thresholds, int nt, const double* norm,
+                       double eps, int iteration_cap, char* json_out, int json_cap, double* stats_out) {
+  return guard([&] {
+    if (!m || !p) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    if (m->inst != &p->inst) morap_multi_upload(m, p) == 0 ? void() : morap::fail(morap::Errc::SolverFailure, g_error);
+    const int d = p->inst.objectives * p->inst.n;
+    morap::NormMatrix M = normOf(norm, d);
+    morap::Vec t(thresholds, thresholds + nt);
+    morap::QueryStats st;
+    std::vector<morap::Shard*> shards;
+    for (auto& s : m->shards) shards.push_back(s.get());
+    morap::ParetoResult res = morap::paretoPointMulti(shards, t, M, eps, iteration_cap, &st);
+    putJson(reportJson(res, false), json_out, json_cap);
+    putStats(st, stats_out);
+  });
+}
+
+int morap_shard_pareto(morap_solver* s, const morap_instance* p, int rank, int world, morap_allgather_fn allgather,
+                       void* user, const double* thresholds, int nt, const double* norm, double eps, int iteration_cap,
+                       char* json_out, int json_cap, double* stats_out) {
+  return guard([&] {
+    if (!s || !p || !allgather) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) morap::fail(morap::Errc::InvalidConfig, "bad shard");
+    const int n = p->inst.n;
+    std::vector<int> owner;
+    if (!p->owner.empty()) {  // built per rank (morap_instance_warehouse_shard): its owners
+      owner.resize(static_cast<size_t>(n) * n);
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+          auto it = p->owner.find(p->inst.products[i][j]->uid);
+          if (it == p->owner.end() || it->second >= world)
+            morap::fail(morap::Errc::InvalidConfig, "instance was sharded for a different world size");
+          owner[static_cast<size_t>(i) * n + j] = it->second;
+        }
+    } else {
+      owner = morap::lptOwners(p->inst, world);
+    }
+    morap::Shard shard(p->inst, *s->gpu, owner, rank);
+    shard.upload();
+    const morap::Exchange ex = [&](const double* send, int count, double* recv) {
+      const int rc = allgather(user, send, count, recv);
+      if (rc != 0) morap::fail(morap::Errc::SolverFailure, "allgather failed (" + std::to_string(rc) + ")");
+    };
+    const int d = p->inst.objectives * n;
+    morap::NormMatrix M = normOf(norm, d);
+    morap::Vec t(thresholds, thresholds + nt);
+    morap::QueryStats st;
+    morap::ParetoResult res = morap::paretoPointSharded(shard, world, ex, t, M, eps, iteration_cap, &st);
+    putJson(reportJson(res, false), json_out, json_cap);
+    putStats(st, stats_out);
   });
 }
 

@@ -138,12 +138,17 @@ void GpuBackend::setLean(bool on) { leanDefault_ = on; }
 // device) is a single host-to-device copy.
 void GpuBackend::uploadInstance(const MorapInstance& inst) {
   std::vector<const ProductMdp*> todo;
-  std::set<uint64_t> queued;
   for (const auto& row : inst.products)
-    for (const auto& p : row)
-      if (!ids_.count(p->uid) && queued.insert(p->uid).second) todo.push_back(p.get());
+    for (const auto& p : row) todo.push_back(p.get());
+  uploadCached(todo, leanDefault_ && inst.objectives <= 4);
+}
+
+void GpuBackend::uploadCached(const std::vector<const ProductMdp*>& products, bool lean) {
+  std::vector<const ProductMdp*> todo;
+  std::set<uint64_t> queued;
+  for (const ProductMdp* p : products)
+    if (!ids_.count(p->uid) && queued.insert(p->uid).second) todo.push_back(p);
   if (todo.empty()) return;
-  const bool lean = leanDefault_ && inst.objectives <= 4;
   std::vector<uint64_t> key{lean ? 1ull : 0ull};
   for (const ProductMdp* p : todo) {
     if (p->slim) {  // streamed / slimmed products have no host arrays to image

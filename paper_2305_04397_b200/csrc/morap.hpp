@@ -261,6 +261,9 @@ class GpuBackend {
   int modelId(const ProductMdp* p, bool full = false);
   void uploadInstance(const MorapInstance& inst);  // all distinct products in one batch
   void uploadProducts(const std::vector<const ProductMdp*>& products, bool lean);  // skips resident ones
+  // the same through a cached packed image: re-uploading the same products (after release())
+  // is one host-to-device copy
+  void uploadCached(const std::vector<const ProductMdp*>& products, bool lean);
   void setLean(bool on);  // default for query uploads (on): compact products without fp64 arrays
   bool lean() const { return leanDefault_; }
   int modelIdFor(uint64_t uid, const morap_csr_view& view);  // any model keyed by a process-unique id
@@ -386,6 +389,41 @@ ParetoResult paretoPoint(const MorapInstance& inst, const Vec& thresholds, const
 bool verifyOnly(const MorapInstance& inst, const Vec& thresholds, const NormMatrix& norm, double eps,
                 GpuBackend& gpu, int iterationCap = 500);
 SynthesisResult synthesize(const ParetoResult& result);
+
+// ---- sharded supporting points (multi-GPU, csrc/shard.cpp) --------------------------------
+// exchange(send, count, recv): recv[r * count + k] = shard r's send[k] for every shard r (an
+// allgather: NCCL / gloo through a callback, or in-process)
+using Exchange = std::function<void(const double* send, int count, double* recv)>;
+// owner shard of every pair i * n + j: distinct products by longest-processing-time on nnz
+std::vector<int> lptOwners(const MorapInstance& inst, int world);
+class Shard {  // the pairs of one shard on one GPU
+ public:
+  Shard(const MorapInstance& inst, GpuBackend& gpu, std::vector<int> owner, int rank);
+  void upload();  // this shard's products (lean when the objectives allow)
+  // initial-state values of the pairs owned here and a mask per pair: 1 owned, 0 not,
+  // 2 + status when the pair's job failed (so every rank raises the same error)
+  void optimize(const Vec& w, double* values, double* mask, QueryStats* stats);
+  // the K values of the assigned pairs owned here (r coordinates), mask per coordinate,
+  // and their schedulers
+  void evaluate(const Assignment& a, double* r, double* mask, std::vector<Scheduler>& schedulers, QueryStats* stats);
+  const MorapInstance& instance() const { return inst_; }
+  int rank() const { return rank_; }
+  const std::vector<int>& owners() const { return owner_; }
+
+ private:
+  const MorapInstance& inst_;
+  GpuBackend& gpu_;
+  std::vector<int> owner_;
+  int rank_;
+  std::vector<int> jobIJ_;  // local optimize job of each owned pair (last optimize)
+};
+SupportingPoint shardedSupportingPoint(Shard& shard, int world, const Exchange& exchange, const Vec& w,
+                                       QueryStats* stats = nullptr);
+ParetoResult paretoPointSharded(Shard& shard, int world, const Exchange& exchange, const Vec& thresholds,
+                                const NormMatrix& norm, double eps, int iterationCap = 500, QueryStats* stats = nullptr);
+SupportingPoint multiSupportingPoint(const std::vector<Shard*>& shards, const Vec& w, QueryStats* stats = nullptr);
+ParetoResult paretoPointMulti(const std::vector<Shard*>& shards, const Vec& thresholds, const NormMatrix& norm,
+                              double eps, int iterationCap = 500, QueryStats* stats = nullptr);
 Json resultToJson(const ParetoResult& result, const SynthesisResult* synthesis = nullptr);
 
 // instance file (cli.hpp:84-117): agents inline or as paths, tasks as LTL strings / DFA JSON.
