@@ -16,7 +16,23 @@ CSRC = os.path.join(PKG, "csrc")
 CUDA_SO = os.path.join(PKG, "libmorap_cuda.so")
 HOST_SO = os.path.join(PKG, "libmorap_host.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-JSON_DIR = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+def _json_dir() -> str:
+    """nlohmann/json (header-only): $MORAP_JSON_DIR, else the copies this image ships."""
+    cands = [os.environ.get("MORAP_JSON_DIR", "")]
+    try:
+        import sysconfig
+        site = sysconfig.get_paths()["purelib"]
+        cands.append(os.path.join(site, "include", "cudnn_frontend", "thirdparty", "nlohmann"))
+    except Exception:  # noqa: BLE001
+        pass
+    cands.append("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann")
+    for c in cands:
+        if c and os.path.exists(os.path.join(c, "json.hpp")):
+            return c
+    raise FileNotFoundError("nlohmann/json.hpp not found: set MORAP_JSON_DIR to the directory holding json.hpp")
+
+
+JSON_DIR = _json_dir()
 
 CUDA_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -48,8 +64,11 @@ def _deps(names):
 
 def build_cuda(force: bool = False, verbose: bool = False) -> str:
     src = os.path.join(CSRC, "morap_cuda.cu")
-    if force or _newer(CUDA_SO, _deps(["morap_cuda.cu"])):
-        cmd = [NVCC, *CUDA_FLAGS, "-o", CUDA_SO, src]
+    diag = os.environ.get("MORAP_BUILD_DIAGNOSTICS") == "1"  # dev probes only (CTA traces, dry runs)
+    checked = os.environ.get("MORAP_BUILD_CHECKED") == "1"  # device bounds checks (test runs)
+    extra = (["-DMORAP_DIAGNOSTICS"] if diag else []) + (["-DMORAP_CHECKED"] if checked else [])
+    if force or extra or _newer(CUDA_SO, _deps(["morap_cuda.cu"])):
+        cmd = [NVCC, *CUDA_FLAGS, *extra, "-o", CUDA_SO, src]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.run(cmd, check=True)

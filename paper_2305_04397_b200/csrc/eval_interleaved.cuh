@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_in
   int k = 0;
   for (;; ++k) {
     const int parity = k & 1;
-    unsigned long long* trace = g_ctaTrace ? g_ctaTrace + (static_cast<size_t>(k % kTraceSlots) * gridDim.x + blockIdx.x) * 4
+    unsigned long long* trace = MORAP_CTA_TRACE() ? MORAP_CTA_TRACE() + (static_cast<size_t>(k % kTraceSlots) * gridDim.x + blockIdx.x) * 4
                                            : nullptr;
     if (trace && tid == 0) trace[0] = global_ns();
     unsigned long long* slot = A.slots + static_cast<size_t>(k % 3) * A.njobs * MORAP_MAX_RHS;
@@ -118,6 +118,8 @@ __global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_in
       const int n = sN[li];
       const int2 sc = sSucc[li];
       const long long base = A.statePrefix[j];
+      MORAP_CHECK(li < C && (n < 1 || (sc.x >= 0 && base + sc.x < A.statePrefix[j + 1])) &&
+                  (n < 2 || (sc.y >= 0 && base + sc.y < A.statePrefix[j + 1])));
       // every load of the state first (x of the batch is read through L1: the grid
       // barrier's fences make the previous sweep's writes visible)
       double2 xs[R / 2], rh[R / 2], x0[R / 2], x1[R / 2];

@@ -3,7 +3,7 @@ CUDA context is created (environment), so each variant runs in its own process:
 
   default            compact streams, 5-stage TMA pipeline (k_greedy_sweep_cmp)
   MORAP_COMPACT=0    fp64 streams, 2-stage TMA pipeline (k_greedy_sweep_tma)
-  MORAP_SWEEP_KERNEL=global   plain global-memory sweep (k_greedy_sweep)
+  MORAP_EVAL_INTERLEAVED=0    per-RHS value layout in the persistent evaluate kernel
   MORAP_GRAPHS=0     sweeps launched one by one instead of CUDA-graph batches
   MORAP_SKIP=0       every tile swept every sweep (no frozen-tile skipping)
 
@@ -57,7 +57,7 @@ print(json.dumps({"hash": h.hexdigest(), "sweeps": sw.tolist(), "eval": ev.tolis
 VARIANTS = {
     "default": {},
     "plain_tma": {"MORAP_COMPACT": "0"},
-    "global": {"MORAP_SWEEP_KERNEL": "global", "MORAP_COMPACT": "0"},
+    "per_rhs_eval": {"MORAP_EVAL_INTERLEAVED": "0"},
     "no_graphs": {"MORAP_GRAPHS": "0"},
     "no_persistent_eval": {"MORAP_PERSISTENT": "0"},
     "no_skip": {"MORAP_SKIP": "0"},
