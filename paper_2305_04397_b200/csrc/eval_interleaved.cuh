@@ -22,6 +22,7 @@ struct InterArgs {
   double* xi;    // 2 x total x R, zeroed (x = 0 at the start, numerics.hpp:141)
   double* rhoI;  // total x R, filled by the prologue from rhoC
   int R;         // 2 or 4
+  int direct;    // 1: the chosen row of each state comes from J.policy (no chain CSR built)
 };
 
 template <int R>
@@ -65,13 +66,31 @@ __global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_in
       while (i >= A.statePrefix[jl + 1]) ++jl;
       const EvalJob& J = A.jobs[jl];
       const int sl = static_cast<int>(i - A.statePrefix[jl]);
-      const int cbl = __ldg(J.chainOff + sl), nl = __ldg(J.chainOff + sl + 1) - cbl;
-      sN[li] = static_cast<uint8_t>(nl);
-      sSucc[li] = make_int2(nl > 0 ? __ldg(J.chainSucc + cbl) : 0, nl > 1 ? __ldg(J.chainSucc + cbl + 1) : 0);
-      sProb[li] = make_double2(nl > 0 ? __ldg(J.chainProb + cbl) : 0.0, nl > 1 ? __ldg(J.chainProb + cbl + 1) : 0.0);
       double r[R];
+      if (IA.direct) {
+        // the policy chain of k_chain_fill, read in place: the chosen row's transitions
+        // (succ, model probability) and its reward per RHS; done states: empty, reward 0
+        const DevModel& M = A.models[J.model];
+        int nl = 0, kb = 0, row = 0;
+        if (!M.done[sl]) {
+          row = J.policy[sl];
+          kb = M.trnOffset[row];
+          nl = M.trnOffset[row + 1] - kb;
+        }
+        sN[li] = static_cast<uint8_t>(nl);
+        sSucc[li] = make_int2(nl > 0 ? M.succ[kb] : 0, nl > 1 ? M.succ[kb + 1] : 0);
+        sProb[li] = make_double2(nl > 0 ? model_prob(M, kb) : 0.0, nl > 1 ? model_prob(M, kb + 1) : 0.0);
 #pragma unroll
-      for (int o = 0; o < R; ++o) r[o] = o < J.nrhs ? __ldg(J.rhoC[o] + sl) : 0.0;
+        for (int o = 0; o < R; ++o)
+          r[o] = o < J.nrhs && nl > 0 ? (J.rho[o] ? J.rho[o][row] : model_obj(M, J.objIdx[o], row)) : 0.0;
+      } else {
+        const int cbl = __ldg(J.chainOff + sl), nl = __ldg(J.chainOff + sl + 1) - cbl;
+        sN[li] = static_cast<uint8_t>(nl);
+        sSucc[li] = make_int2(nl > 0 ? __ldg(J.chainSucc + cbl) : 0, nl > 1 ? __ldg(J.chainSucc + cbl + 1) : 0);
+        sProb[li] = make_double2(nl > 0 ? __ldg(J.chainProb + cbl) : 0.0, nl > 1 ? __ldg(J.chainProb + cbl + 1) : 0.0);
+#pragma unroll
+        for (int o = 0; o < R; ++o) r[o] = o < J.nrhs ? __ldg(J.rhoC[o] + sl) : 0.0;
+      }
       double2* dst = reinterpret_cast<double2*>(IA.rhoI + i * R);
 #pragma unroll
       for (int h = 0; h < R / 2; ++h) dst[h] = make_double2(r[2 * h], r[2 * h + 1]);

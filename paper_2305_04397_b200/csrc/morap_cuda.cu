@@ -187,6 +187,7 @@ struct morap_ctx {
   int persistBlocks = 0;
   bool usePersistCache = false;
   bool useInterleaved = false;  // k_eval_interleaved for cached-chain evaluate batches
+  bool evalDirect = false;      // current evaluate batch: chains read from the policies in-kernel
   unsigned* dBar = nullptr;   // grid-barrier counter + generation
   unsigned* dFinCount = nullptr;  // CTAs done in the current compact sweep (fused finalize)
   void* persistArena = nullptr;
@@ -727,6 +728,21 @@ int prefetch_policies(morap_ctx* ctx, const std::vector<int32_t>& jobs) {
 
 // Whole evaluate batch in one cooperative launch (k_eval_persistent). The policy chains
 // must already be built; dMask / dSweeps / dResidual / dStatus are initialised.
+// States per CTA of the persistent evaluate grid when every job's chains can be cached in
+// shared memory (rows of <= 2 transitions, the CTA's share fits), else 0.
+int eval_cache_states(morap_ctx* ctx, int njobs, size_t* cacheBytesOut = nullptr) {
+  long long total = 0;
+  bool narrow = true;
+  for (int j = 0; j < njobs; ++j) {
+    total += ctx->hm[ctx->hEvalJobs[j].model].S;
+    narrow = narrow && ctx->hm[ctx->hEvalJobs[j].model].maxRowNnz <= 2;
+  }
+  const long long per = (total + ctx->persistBlocks - 1) / ctx->persistBlocks;
+  const size_t cacheBytes = static_cast<size_t>((per + 15) & ~15ll) + 24ull * static_cast<size_t>(per) + 16;
+  if (cacheBytesOut) *cacheBytesOut = cacheBytes;
+  return (narrow && ctx->usePersistCache && cacheBytes <= kPersistCacheBytes) ? static_cast<int>(per) : 0;
+}
+
 int run_eval_persistent(morap_ctx* ctx, int njobs, double eps, int cap) {
   std::vector<long long> prefix(static_cast<size_t>(njobs) + 1, 0);
   for (int j = 0; j < njobs; ++j) prefix[j + 1] = prefix[j] + ctx->hm[ctx->hEvalJobs[j].model].S;
@@ -759,13 +775,12 @@ int run_eval_persistent(morap_ctx* ctx, int njobs, double eps, int cap) {
   a.barCount = ctx->dBar;
   a.barGen = ctx->dBar + 1;
   // shared-memory chains when every job's rows have <= 2 transitions and a CTA's states fit
-  const long long per = (prefix[njobs] + ctx->persistBlocks - 1) / ctx->persistBlocks;
-  bool narrow = true;
-  for (int j = 0; j < njobs && narrow; ++j) narrow = ctx->hm[ctx->hEvalJobs[j].model].maxRowNnz <= 2;
-  const size_t cacheBytes = static_cast<size_t>((per + 15) & ~15ll) + 24ull * static_cast<size_t>(per) + 16;
-  a.cacheStates = (narrow && ctx->usePersistCache && cacheBytes <= kPersistCacheBytes) ? static_cast<int>(per) : 0;
-  // interleaved RHS (k_eval_interleaved) whenever the chains are cached: every job <= 4 RHS here
-  InterArgs ia{a, nullptr, nullptr, R};
+  size_t cacheBytes = 0;
+  a.cacheStates = eval_cache_states(ctx, njobs, &cacheBytes);
+  // interleaved RHS (k_eval_interleaved) whenever the chains are cached: every job <= 4 RHS
+  // here; `direct`: the kernel reads each state's chosen row from the policy itself (the
+  // chain CSR was not built)
+  InterArgs ia{a, nullptr, nullptr, R, ctx->evalDirect ? 1 : 0};
   const bool inter = a.cacheStates > 0 && ctx->useInterleaved;
   if (inter) {
     char* ib = base + align_up(slotBytes, 256) + align_up(8ull * (njobs + 1), 256);
@@ -866,7 +881,10 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
   };
   lap("setup");
   ctx->evalTma = tmaOk;
-  if (tmaOk && !active.empty()) {
+  const bool persistent = tmaOk && ctx->usePersistent && njobs <= kPersistMaxJobs;
+  // the interleaved kernel builds its shared-memory chains from the policies directly
+  ctx->evalDirect = persistent && ctx->useInterleaved && eval_cache_states(ctx, njobs) > 0;
+  if (tmaOk && !active.empty() && !ctx->evalDirect) {
     // policy chains of the active jobs (count, per-job scan, fill)
     const int nl = ctx->hCtl->nactive, tt = ctx->hCtl->totalTiles;
     const EvalJob* ej = static_cast<const EvalJob*>(ctx->dEvalJobsRaw);
@@ -880,7 +898,7 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
   }
   lap("chains");
   if (!active.empty()) {
-    if (tmaOk && ctx->usePersistent && njobs <= kPersistMaxJobs) {
+    if (persistent) {
       if ((rc = run_eval_persistent(ctx, njobs, eps, cap))) return rc;
     } else if ((rc = run_loop(ctx, 1, eps, cap))) {
       return rc;
