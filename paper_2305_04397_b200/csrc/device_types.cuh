@@ -197,3 +197,24 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   __syncthreads();
   return r;  // valid in thread 0
 }
+
+// Software grid barrier of the persistent (cooperative) kernels: every CTA of the grid is
+// resident; fences order the sweep's global writes before the next phase reads them.
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vg = gen;
+    const unsigned g = *vg;
+    __threadfence();
+    if (atomicAdd(count, 1u) == nblocks - 1) {
+      *count = 0;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*vg == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}

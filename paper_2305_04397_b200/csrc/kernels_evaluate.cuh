@@ -327,24 +327,6 @@ __global__ void __launch_bounds__(kTmaThreads, 3) k_eval_sweep_tma(const DevMode
 constexpr int kPersistJobs = 16;   // per-CTA residual accumulators (jobs touched by one CTA)
 constexpr int kPersistMaxJobs = 1024;
 
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* vg = gen;
-    const unsigned g = *vg;
-    __threadfence();
-    if (atomicAdd(count, 1u) == nblocks - 1) {
-      *count = 0;
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      while (*vg == g) {
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
 
 struct PersistArgs {
   const DevModel* models;

@@ -714,6 +714,40 @@ constexpr int kMaxOutGroups = 16;  // out-of-window stamp groups a skippable til
 static_assert((kXWin + 31) / 32 / 4 + 2 <= 15, "successor-window stamp loads overflow 4 bits");
 static_assert((kBlock / 32) / 4 + 2 <= 7, "own-state stamp loads overflow 3 bits");
 static_assert(kMaxOutGroups < 32 && kCandLtBits + 7 + 5 <= 32, "candidate word layout");
+// Latest stamp among the groups candidate c depends on: its successor window, its own states
+// and up to kMaxOutGroups out-of-window groups (the lists k_build_cand packed). Every load is
+// predicated inside fully unrolled loops so a thread has them all in flight at once (the
+// data-dependent loops left up to ~30 dependent L2 round trips on the selection's tail).
+__device__ __forceinline__ int cand_stamp_max(const int4 c, int oo, const int32_t* __restrict__ stampAll,
+                                              const int32_t* __restrict__ candOutG) {
+  const int4* stamp = reinterpret_cast<const int4*>(stampAll);
+  const unsigned u = static_cast<unsigned>(c.y);
+  const int nw = (u >> kCandLtBits) & 15, no = (u >> (kCandLtBits + 4)) & 7, nout = u >> (kCandLtBits + 7);
+  int m = 0;
+#pragma unroll
+  for (int h = 0; h < kMaxOutGroups; h += 8) {  // successors outside the window, 8 groups at a time
+    int g[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) g[q] = h + q < nout ? __ldg(candOutG + oo + h + q) : -1;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (g[q] >= 0) m = max(m, __ldcg(stampAll + g[q]));
+  }
+#pragma unroll
+  for (int q = 0; q < 15; ++q)  // successor window (<= 15 loads of 4 stamps)
+    if (q < nw) {
+      const int4 v = __ldcg(stamp + (c.z >> 2) + q);
+      m = max(m, max(max(v.x, v.y), max(v.z, v.w)));
+    }
+#pragma unroll
+  for (int q = 0; q < 7; ++q)  // own states (<= 7 loads of 4 stamps)
+    if (q < no) {
+      const int4 v = __ldcg(stamp + (c.w >> 2) + q);
+      m = max(m, max(max(v.x, v.y), max(v.z, v.w)));
+    }
+  return m;
+}
+
 __global__ void __launch_bounds__(kSelThreads) k_build_cand(const DevModel* __restrict__ models,
                                                             const OptJob* __restrict__ jobs,
                                                             const int32_t* __restrict__ list,
@@ -804,21 +838,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const DevModel* __restri
       if (run) {
         keep = 1;
         if (k > 0 && c.z >= 0) {
-          const int4* stamp = reinterpret_cast<const int4*>(stampAll);
-          const unsigned u = static_cast<unsigned>(c.y);
-          const int nw = (u >> kCandLtBits) & 15, no = (u >> (kCandLtBits + 4)) & 7, nout = u >> (kCandLtBits + 7);
-          int m = 0;
-          for (int q = 0; q < nout; ++q)  // successors outside the window: their groups one by one
-            m = max(m, __ldcg(stampAll + __ldg(candOutG + oo + q)));
-          for (int q = 0; q < nw; ++q) {  // successor window
-            const int4 v = __ldcg(stamp + (c.z >> 2) + q);
-            m = max(m, max(max(v.x, v.y), max(v.z, v.w)));
-          }
-          for (int q = 0; q < no; ++q) {  // own states
-            const int4 v = __ldcg(stamp + (c.w >> 2) + q);
-            m = max(m, max(max(v.x, v.y), max(v.z, v.w)));
-          }
-          keep = m >= k;  // something it depends on changed in the previous sweep
+          keep = cand_stamp_max(c, oo, stampAll, candOutG) >= k;  // a dependency changed in the previous sweep
         }
       }
       c.y &= (1 << kCandLtBits) - 1;
@@ -1290,3 +1310,4 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
     }
   }
 }
+

@@ -82,9 +82,10 @@ int main() {
   int clk;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const int iters = 2000;
-  for (int threads : {256, 1024})
+  for (int cfg = 0; cfg < 3; ++cfg)
     for (int mode = 0; mode < 4; ++mode) {
-      int nb = 148;
+      const int threads = cfg == 0 ? 256 : cfg == 1 ? 1024 : 288;
+      int nb = cfg == 2 ? 592 : 148;
       void* args[] = {&bar, (void*)&iters, &mode, &slots, &out};
       cudaEvent_t a, b;
       cudaEventCreate(&a);
@@ -96,7 +97,7 @@ int main() {
       cudaEventSynchronize(b);
       float ms;
       cudaEventElapsedTime(&ms, a, b);
-      printf("grid barrier 148x%d mode %d (%s%s): %.3f us per iteration (%s)\n", threads, mode,
+      printf("grid barrier %dx%d mode %d (%s%s): %.3f us per iteration (%s)\n", nb, threads, mode,
              mode & 1 ? "acq/rel PTX" : "threadfence", mode >= 2 ? " + residual atomics/reads" : "",
              ms * 1e3 / iters, cudaGetErrorString(cudaGetLastError()));
     }
