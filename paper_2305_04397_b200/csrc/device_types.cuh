@@ -7,22 +7,20 @@ constexpr int kRowCap = 768;    // max action rows per tile (staged in shared me
 constexpr int kNnzCap = 1024;   // max transitions per multi-state tile (staged)
 constexpr int kFinBlock = 1024; // finalize kernel block
 constexpr bool kFusedStates = true;  // TMA sweep: thread-per-state single pass (else 3 phases)
-// Diagnostics, compiled in only with -DMORAP_DIAGNOSTICS (MORAP_BUILD_DIAGNOSTICS=1 python -m
-// paper_2305_04397_b200.build; the dev probes scripts/probe_cta_trace.py / probe_eval_trace.py):
+// Diagnostics (dev probes scripts/probe_cta_trace.py / probe_eval_trace.py):
 //   MORAP_DEBUG_DRY=1  consumers skip the arithmetic, so the pipeline's pure streaming rate
-//                      can be measured;
+//                      can be measured -- honoured only by -DMORAP_DIAGNOSTICS builds
+//                      (MORAP_BUILD_DIAGNOSTICS=1 python -m paper_2305_04397_b200.build);
 //   morap_cuda_debug_cta_trace  per sweep and CTA, globaltimer stamps {start, first stage
 //                      consumed, all warps done, finalize done}.
-// The shipped library has neither: the macros below are constants there.
-#ifdef MORAP_DIAGNOSTICS
+// The two diagnostics globals are compiled in always (0 / null unless set): ptxas allocates
+// the compact sweep kernel without spills only with the trace stamps present (without them:
+// 104 B of spills and a ~4% slower sweep, C2 A/B). Only the dry-run switch (MORAP_DEBUG_DRY)
+// is limited to diagnostics builds; traces are armed by morap_cuda_debug_cta_trace.
 __device__ int g_dryRun = 0;
 __device__ unsigned long long* g_ctaTrace = nullptr;
 #define MORAP_DRY_RUN() (g_dryRun != 0)
 #define MORAP_CTA_TRACE() (g_ctaTrace)
-#else
-#define MORAP_DRY_RUN() false
-#define MORAP_CTA_TRACE() static_cast<unsigned long long*>(nullptr)
-#endif
 constexpr int kTraceSlots = 128;
 // Device bounds checks, compiled in only with -DMORAP_CHECKED (MORAP_BUILD_CHECKED=1): every
 // staged bulk copy against its shared-memory region and its source array, every gather

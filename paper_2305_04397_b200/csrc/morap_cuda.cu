@@ -1723,12 +1723,6 @@ int morap_cuda_set_lean(morap_ctx* ctx, int on) {
 
 int morap_cuda_debug_cta_trace(morap_ctx* ctx, int enable, uint64_t* out, int64_t n) {
   if (!ctx) return MORAP_INVALID_CONFIG;
-#ifndef MORAP_DIAGNOSTICS
-  (void)enable;
-  (void)out;
-  (void)n;
-  return ctx->fail(MORAP_INVALID_CONFIG, "CTA traces need a diagnostics build (MORAP_BUILD_DIAGNOSTICS=1)");
-#else
   cudaSetDevice(ctx->device);
   const size_t words = static_cast<size_t>(kTraceSlots) * ctx->cmpBlocks * 4;
   if (enable > 0) {
@@ -1745,7 +1739,6 @@ int morap_cuda_debug_cta_trace(morap_ctx* ctx, int enable, uint64_t* out, int64_
     CK(d2h(ctx, out, ctx->dTrace, std::min<size_t>(words, static_cast<size_t>(n)) * 8, true));
   }
   return MORAP_OK;
-#endif
 }
 
 int morap_cuda_set_skip(morap_ctx* ctx, int on) {
