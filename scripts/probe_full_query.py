@@ -15,6 +15,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 cap = int(sys.argv[2]) if len(sys.argv) > 2 else 500
 cfg, thr, eps, K = bench.workload(name)
 s = Solver(0)
+s.set_fingerprints(False)
 t = time.time()
 if name in bench.STREAMED:
     s.set_lean(True)
@@ -35,6 +36,14 @@ print(json.dumps({"workload": name, "query_s": q, "iterations": len(it), "conver
 # the supporting points of every iteration, for an offline replay of the sandwich loop
 # (scripts/replay_sandwich.py: same weight sequence from the reference's geometry)
 import numpy as np  # noqa: E402
+import os  # noqa: E402
+gold = f"tests/golden/replay/{name}_query.npz"  # the round-2 recording (GPU run, replayed on the reference)
+if os.path.exists(gold):
+    z = np.load(gold)
+    same = {k: np.array(v).tobytes() == z[k].tobytes() for k, v in
+            (("w", [x["w"] for x in it]), ("r", [x["r"] for x in it]), ("tUp", r["tUp"]), ("tDown", r["tDown"]),
+             ("lambdaStar", r["lambdaStar"]))}
+    print(json.dumps({"same_as_recorded_query": same}), flush=True)
 np.savez_compressed(f"gpurun_out/report_{name}.npz", thresholds=np.array(r["thresholds"]),
                     w=np.array([x["w"] for x in it]), r=np.array([x["r"] for x in it]),
                     assignment=np.array([x["assignment"] for x in it], dtype=np.int32),
