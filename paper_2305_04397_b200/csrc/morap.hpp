@@ -66,6 +66,29 @@ Vec matVec(const Mat& m, const Vec& x);
 double maxAbs(const Vec& v);
 Vec solveDense(Mat A, Vec b, double pivotTol = 1e-12);
 Vec solveDenseInPlace(Mat& A, Vec& b, double pivotTol = 1e-12);  // A and b are destroyed
+// A recorded elimination of solveDense: the row swap and the nonzero multipliers of every
+// pivot step, and the upper triangle (left in the caller's matrix, row-major, leading
+// dimension lda), so the same system can be solved again for another right-hand side with
+// exactly the arithmetic a fresh elimination performs.
+struct DenseLU {
+  int n = 0, lda = 0;
+  double* U = nullptr;  // caller-owned
+  std::vector<int> piv;
+  std::vector<std::vector<std::pair<int, double>>> steps;  // per step: (row, f), rows ascending
+  void reset(int dim) {
+    n = dim;
+    piv.assign(static_cast<size_t>(dim), 0);
+    if (steps.size() < static_cast<size_t>(dim)) steps.resize(static_cast<size_t>(dim));
+    for (int k = 0; k < dim; ++k) steps[k].clear();
+  }
+  void beginStep(int k, int p) { piv[k] = p; }
+  void log(int k, int r, double f) { steps[k].push_back({r, f}); }
+};
+// solveDenseInPlace on a row-major A (n x n, leading dimension lda) that records `lu`
+Vec solveDenseRecorded(double* A, int n, int lda, Vec& b, DenseLU& lu, double pivotTol = 1e-12);
+// x of the recorded system for another right-hand side (bitwise a fresh solve)
+Vec solveLU(const DenseLU& lu, Vec b);
+
 // 0: blocked + host threads for n >= 128 (bitwise the unblocked elimination), 1: unblocked
 // only (A/B and tests; env MORAP_DENSE=unblocked)
 int& denseSolveMode();

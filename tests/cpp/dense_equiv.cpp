@@ -13,7 +13,7 @@ int main() {
   std::mt19937_64 rng(7);
   std::uniform_real_distribution<double> U(-2.0, 2.0);
   int bad = 0, cases = 0, singular = 0;
-  for (int n : {128, 129, 150, 203, 260, 333}) {
+  for (int n : {20, 61, 127, 128, 129, 150, 203, 260, 333}) {
     for (int rep = 0; rep < 6; ++rep) {
       const double density = rep < 2 ? 0.05 : rep < 4 ? 0.3 : 1.0;
       Mat A(n, n, 0.0);
@@ -37,6 +37,21 @@ int main() {
           x[mode] = solveDense(A, b);
         } catch (const Error& e) {
           err[mode] = 1 + static_cast<int>(e.code());
+        }
+      }
+      // recorded elimination, then a re-solve for another rhs: the bits of a fresh solve
+      if (!err[0]) {
+        Mat Ar = A;
+        Vec br = b;
+        DenseLU lu;
+        const Vec xr = solveDenseRecorded(Ar.a.data(), n, n, br, lu);
+        Vec b2(n);
+        for (int r = 0; r < n; ++r) b2[r] = U(rng);
+        const Vec x2 = solveLU(lu, b2), f2 = solveDense(A, b2);
+        if (std::memcmp(xr.data(), x[0].data(), sizeof(double) * n) != 0 ||
+            std::memcmp(x2.data(), f2.data(), sizeof(double) * n) != 0) {
+          ++bad;
+          std::printf("n=%d rep=%d: recorded elimination / re-solve differs\n", n, rep);
         }
       }
       ++cases;
