@@ -63,6 +63,7 @@ struct HostModel {
   int32_t S, R, nnz, initial, ntiles, K, rewardFinite;
   int32_t maxRowNnz;  // transitions of the widest row
   int32_t nOutGrp;    // entries of the model's out-of-window group lists (frozen-tile skipping)
+  int32_t needB;      // its sweeps read the upload's segment B (non-compact / oversized tiles)
 };
 
 template <class T>
@@ -86,6 +87,8 @@ struct morap_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;           // policy prefetch copies (overlap the evaluate sweeps)
   cudaEvent_t polReady = nullptr, polCopied = nullptr;
+  cudaEvent_t segBReady = nullptr;  // segment B of the last image upload is on the device
+  bool segBPending = false;         // ... and the stream has not waited for it yet
   std::vector<int32_t> polPrefetched;    // jobs whose policies sit in polStage (in this order)
   std::vector<size_t> polOff;
   std::string err;
@@ -219,6 +222,14 @@ cudaError_t d2h(morap_ctx* ctx, void* dst, const void* src, size_t bytes, bool s
   ctx->stats[11] += static_cast<double>(bytes);
   return sync ? cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)
               : cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+}
+
+// The stream waits for the last image upload's segment B before a kernel that reads it.
+int wait_segment_b(morap_ctx* ctx) {
+  if (!ctx->segBPending) return MORAP_OK;
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->segBReady, 0));
+  ctx->segBPending = false;
+  return MORAP_OK;
 }
 
 int ensure_ctl(morap_ctx* ctx, size_t njobs) {
@@ -481,6 +492,13 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
   ctx->polPrefetched.clear();
   ctx->optJobs = 0;
   if (njobs == 0) return MORAP_OK;
+  {
+    bool needB = rhoHost != nullptr;  // explicit rewards: the fp64 arrays
+    for (int j = 0; j < njobs && !needB; ++j)
+      needB = model_ids[j] >= 0 && model_ids[j] < static_cast<int>(ctx->hm.size()) && ctx->hm[model_ids[j]].needB;
+    int rcB;
+    if (needB && (rcB = wait_segment_b(ctx))) return rcB;
+  }
   for (int j = 0; j < njobs; ++j) {
     if (model_ids[j] < 0 || model_ids[j] >= static_cast<int>(ctx->hm.size()))
       return ctx->fail(MORAP_INVALID_CONFIG, "job " + std::to_string(j) + ": unknown model id");
@@ -677,6 +695,8 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
 
 // Computes final-sweep argmax policies for the listed optimize jobs (on the device).
 int extract_policies(morap_ctx* ctx, const std::vector<int32_t>& jobsIn) {
+  int rcB;
+  if ((rcB = wait_segment_b(ctx))) return rcB;
   std::vector<int32_t> jobs;
   for (int j : jobsIn)
     if (!ctx->optPolicyReady[j] && ctx->optSweeps[j] > 0) jobs.push_back(j);
@@ -815,6 +835,7 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
                   double* value_out, int32_t* sweeps_out, double* residual_out, int32_t* status_out,
                   const std::vector<uint32_t>& maskInit, const std::vector<int32_t>& statusInit) {
   int rc;
+  if ((rc = wait_segment_b(ctx))) return rc;
   if ((rc = ensure_ctl(ctx, njobs))) return rc;
   if (static_cast<size_t>(njobs) > ctx->dEvalJobsCap) {
     cudaFree(ctx->dEvalJobsRaw);
@@ -949,9 +970,16 @@ struct UploadPrep {
   std::vector<std::vector<TileDesc>> descs;
   std::vector<CompactStream> compact;
   std::vector<int32_t> maxRowNnz;
-  std::vector<size_t> off;  // byte offset of each model in the block
-  std::vector<char> lean;   // stored without fp64 prob / objectives
-  size_t bytes = 0;
+  // The block has two segments: A = what the compact sweeps read (succ for out-of-window
+  // successors, tiles, dictionaries, the per-tile streams, stamp groups), B = the rest
+  // (rowOffset, trnOffset, done, probIdx, rclass, and the fp64 arrays of full uploads),
+  // needed by the evaluate paths and by non-compact sweeps. An image upload copies A on the
+  // stream and B on the side stream, overlapped with the first optimize batch.
+  std::vector<size_t> offA, offB;  // byte offset of each model in its segment
+  std::vector<size_t> lenA, lenB;
+  std::vector<char> lean;          // stored without fp64 prob / objectives
+  std::vector<char> needB;         // the model's sweeps read segment B (non-compact / oversized tiles)
+  size_t bytesA = 0, bytes = 0;    // segment B starts at bytesA
 };
 
 int prepare_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, UploadPrep& P) {
@@ -1004,27 +1032,42 @@ int prepare_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, Up
   for (int m = 0; m < nmodels; ++m)
     if (status[m]) return ctx->fail(status[m], why[m]);
   lapU("validated, tiled, compacted");
-  // every array of the batch in one block
-  size_t bytes = 0;
-  auto& off = P.off;
-  off.assign(nmodels, 0);
+  // every array of the batch in one block (two segments, see UploadPrep)
+  P.offA.assign(nmodels, 0);
+  P.offB.assign(nmodels, 0);
+  P.lenA.assign(nmodels, 0);
+  P.lenB.assign(nmodels, 0);
   P.lean.assign(nmodels, 0);
+  P.needB.assign(nmodels, 0);
+  size_t totA = 0, totB = 0;
   for (int m = 0; m < nmodels; ++m) {
     const morap_csr_view& v = models[m];
-    off[m] = bytes;
     const bool lean = ctx->lean && compact[m].ok && ctx->useTma;
     P.lean[m] = lean;
-    bytes += align_up(4ull * (v.num_states + 1), 256) + align_up(4ull * (v.num_rows + 1), 256) +
-             align_up(4ull * v.nnz, 256) + (lean ? 0 : align_up(8ull * v.nnz, 256)) + align_up(1ull * v.num_states, 256) +
-             (lean ? 0 : static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256)) +
-             align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
-    if (compact[m].ok)
-      bytes += align_up(v.nnz, 256) + align_up(8ull * compact[m].dict.size(), 256) + align_up(2ull * v.num_rows, 256) +
-               align_up(8ull * compact[m].table.size(), 256) + align_up(4ull * compact[m].nTrW, 256) +
-               align_up(4ull * compact[m].nStW, 256) + align_up(4ull * compact[m].nRowW, 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256) +
-               align_up(4ull * compact[m].outIdx.size(), 256) + align_up(4ull * compact[m].outGrp.size(), 256);
+    bool fitsAll = true;
+    for (const TileDesc& d : descs[m]) fitsAll = fitsAll && (d.fits || d.s0 == v.num_states);
+    P.needB[m] = !compact[m].ok || !fitsAll;
+    size_t a = align_up(4ull * v.nnz, 256) + align_up(4ull * tiles[m].size(), 256) +
+               align_up(sizeof(TileDesc) * descs[m].size(), 256);
+    size_t b = align_up(4ull * (v.num_states + 1), 256) + align_up(4ull * (v.num_rows + 1), 256) +
+               (lean ? 0 : align_up(8ull * v.nnz, 256)) + align_up(1ull * v.num_states, 256) +
+               (lean ? 0 : static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256));
+    if (compact[m].ok) {
+      a += align_up(8ull * compact[m].dict.size(), 256) + align_up(8ull * compact[m].table.size(), 256) +
+           align_up(4ull * compact[m].nTrW, 256) + align_up(4ull * compact[m].nStW, 256) +
+           align_up(4ull * compact[m].nRowW, 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256) +
+           align_up(4ull * compact[m].outIdx.size(), 256) + align_up(4ull * compact[m].outGrp.size(), 256);
+      b += align_up(v.nnz, 256) + align_up(2ull * v.num_rows, 256);
+    }
+    P.offA[m] = totA;
+    P.offB[m] = totB;
+    P.lenA[m] = a;
+    P.lenB[m] = b;
+    totA += a;
+    totB += b;
   }
-  P.bytes = bytes;
+  P.bytesA = totA;
+  P.bytes = totA + totB;
   return MORAP_OK;
 }
 
@@ -1036,14 +1079,18 @@ void pack_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, cons
   const auto& tiles = P.tiles;
   const auto& descs = P.descs;
   const auto& compact = P.compact;
-  const auto& off = P.off;
   void* dev = devBase;
   parallel_for(nmodels, [&](int m) {
     const morap_csr_view& v = models[m];
-    char* h = host + off[m];
-    char* d = static_cast<char*>(dev) + off[m];
+    char* hA = host + P.offA[m];
+    char* dA = static_cast<char*>(dev) + P.offA[m];
+    char* hB = host + P.bytesA + P.offB[m];
+    char* dB = static_cast<char*>(dev) + P.bytesA + P.offB[m];
     DevModel dmod{};
-    auto put = [&](const void* src, size_t n) {  // src == nullptr: reserve (filled by the caller)
+    // src == nullptr: reserve (filled by the caller); seg 0 = A, 1 = B
+    auto put = [&](int seg, const void* src, size_t n) {
+      char*& h = seg ? hB : hA;
+      char*& d = seg ? dB : dA;
       if (n && src) std::memcpy(h, src, n);
       char* at = d;
       const size_t a = align_up(n, 256);
@@ -1051,17 +1098,17 @@ void pack_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, cons
       d += a;
       return at;
     };
-    dmod.rowOffset = reinterpret_cast<const int32_t*>(put(v.row_offset, 4ull * (v.num_states + 1)));
-    dmod.trnOffset = reinterpret_cast<const int32_t*>(put(v.trn_offset, 4ull * (v.num_rows + 1)));
-    dmod.succ = reinterpret_cast<const int32_t*>(put(v.succ, 4ull * v.nnz));
+    dmod.rowOffset = reinterpret_cast<const int32_t*>(put(1, v.row_offset, 4ull * (v.num_states + 1)));
+    dmod.trnOffset = reinterpret_cast<const int32_t*>(put(1, v.trn_offset, 4ull * (v.num_rows + 1)));
+    dmod.succ = reinterpret_cast<const int32_t*>(put(0, v.succ, 4ull * v.nnz));
     const bool lean = P.lean[m];  // fp64 prob / objectives live in the tables
-    if (!lean) dmod.prob = reinterpret_cast<const double*>(put(v.prob, 8ull * v.nnz));
-    dmod.done = reinterpret_cast<const uint8_t*>(put(v.done, v.num_states));
+    if (!lean) dmod.prob = reinterpret_cast<const double*>(put(1, v.prob, 8ull * v.nnz));
+    dmod.done = reinterpret_cast<const uint8_t*>(put(1, v.done, v.num_states));
     if (!lean)
       for (int o = 0; o < v.num_objectives; ++o)
-        dmod.obj[o] = reinterpret_cast<const double*>(put(v.rewards[o], 8ull * v.num_rows));
-    dmod.tileStart = reinterpret_cast<const int32_t*>(put(tiles[m].data(), 4ull * tiles[m].size()));
-    dmod.tiles = reinterpret_cast<const TileDesc*>(put(descs[m].data(), sizeof(TileDesc) * descs[m].size()));
+        dmod.obj[o] = reinterpret_cast<const double*>(put(1, v.rewards[o], 8ull * v.num_rows));
+    dmod.tileStart = reinterpret_cast<const int32_t*>(put(0, tiles[m].data(), 4ull * tiles[m].size()));
+    dmod.tiles = reinterpret_cast<const TileDesc*>(put(0, descs[m].data(), sizeof(TileDesc) * descs[m].size()));
     dmod.S = v.num_states;
     dmod.R = v.num_rows;
     dmod.nnz = v.nnz;
@@ -1075,21 +1122,21 @@ void pack_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, cons
     const CompactStream& c = compact[m];
     if (c.ok) {
       dmod.compact = 1;
-      dmod.probIdx = reinterpret_cast<const uint8_t*>(put(c.idx.data(), c.idx.size()));
-      dmod.probDict = reinterpret_cast<const double*>(put(c.dict.data(), 8ull * c.dict.size()));
-      dmod.rclass = reinterpret_cast<const uint16_t*>(put(c.cls.data(), 2ull * c.cls.size()));
-      dmod.classTable = reinterpret_cast<const double*>(put(c.table.data(), 8ull * c.table.size()));
+      dmod.probIdx = reinterpret_cast<const uint8_t*>(put(1, c.idx.data(), c.idx.size()));
+      dmod.probDict = reinterpret_cast<const double*>(put(0, c.dict.data(), 8ull * c.dict.size()));
+      dmod.rclass = reinterpret_cast<const uint16_t*>(put(1, c.cls.data(), 2ull * c.cls.size()));
+      dmod.classTable = reinterpret_cast<const double*>(put(0, c.table.data(), 8ull * c.table.size()));
       dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
-      uint32_t* hs = reinterpret_cast<uint32_t*>(h);
-      dmod.stW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nStW));
-      uint32_t* hr = reinterpret_cast<uint32_t*>(h);
-      dmod.rowW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nRowW));
-      uint32_t* ht = reinterpret_cast<uint32_t*>(h);
-      dmod.trW = reinterpret_cast<const uint32_t*>(put(nullptr, 4ull * c.nTrW));
+      uint32_t* hs = reinterpret_cast<uint32_t*>(hA);
+      dmod.stW = reinterpret_cast<const uint32_t*>(put(0, nullptr, 4ull * c.nStW));
+      uint32_t* hr = reinterpret_cast<uint32_t*>(hA);
+      dmod.rowW = reinterpret_cast<const uint32_t*>(put(0, nullptr, 4ull * c.nRowW));
+      uint32_t* ht = reinterpret_cast<uint32_t*>(hA);
+      dmod.trW = reinterpret_cast<const uint32_t*>(put(0, nullptr, 4ull * c.nTrW));
       fill_streams(v, descs[m], c, hs, hr, ht);  // straight into the staging buffer
-      dmod.tilePos = reinterpret_cast<const TilePos*>(put(c.pos.data(), sizeof(TilePos) * c.pos.size()));
-      dmod.outIdx = reinterpret_cast<const int32_t*>(put(c.outIdx.data(), 4ull * c.outIdx.size()));
-      dmod.outGrp = reinterpret_cast<const int32_t*>(put(c.outGrp.data(), 4ull * c.outGrp.size()));
+      dmod.tilePos = reinterpret_cast<const TilePos*>(put(0, c.pos.data(), sizeof(TilePos) * c.pos.size()));
+      dmod.outIdx = reinterpret_cast<const int32_t*>(put(0, c.outIdx.data(), 4ull * c.outIdx.size()));
+      dmod.outGrp = reinterpret_cast<const int32_t*>(put(0, c.outGrp.data(), 4ull * c.outGrp.size()));
       // compact stream: one 4-byte word per transition (window offset | index) and per row
       // (transition end | class) and per state (row end | transition end | done) + x 8 + y 8
       dmod.bytesPerSweep = 4ull * v.nnz + 4ull * v.num_rows + 20ull * v.num_states;
@@ -1099,13 +1146,14 @@ void pack_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, cons
     const double nnzPerRow = v.num_rows ? static_cast<double>(v.nnz) / v.num_rows : 0.0;
     dmod.bytesPerEval = static_cast<unsigned long long>(v.num_states * (29.0 + 12.0 * nnzPerRow));
     built[m] = dmod;
-    // this model's block goes out as soon as it is packed (copies overlap the packing)
-    const size_t len = static_cast<size_t>(h - (host + off[m]));
-    uploadBytes += static_cast<long long>(len);
+    // this model's two parts go out as soon as they are packed (copies overlap the packing)
+    uploadBytes += static_cast<long long>(P.lenA[m] + P.lenB[m]);
     if (!copy) return;
     cudaSetDevice(ctx->device);  // packing runs on pool threads
-    if (cudaMemcpyAsync(static_cast<char*>(dev) + off[m], host + off[m], len, cudaMemcpyHostToDevice, ctx->stream) !=
-        cudaSuccess)
+    if (cudaMemcpyAsync(static_cast<char*>(dev) + P.offA[m], host + P.offA[m], P.lenA[m], cudaMemcpyHostToDevice,
+                        ctx->stream) != cudaSuccess ||
+        cudaMemcpyAsync(static_cast<char*>(dev) + P.bytesA + P.offB[m], host + P.bytesA + P.offB[m], P.lenB[m],
+                        cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
       copyFailed = true;
   });
 }
@@ -1130,7 +1178,7 @@ std::vector<HostModel> host_models(const std::vector<DevModel>& built, const Upl
   for (size_t m = 0; m < built.size(); ++m) {
     const DevModel& d = built[m];
     out[m] = HostModel{d.S, d.R, d.nnz, d.initial, d.ntiles, d.K, d.rewardFinite, P.maxRowNnz[m],
-                       static_cast<int32_t>(P.compact[m].outGrp.size())};
+                       static_cast<int32_t>(P.compact[m].outGrp.size()), P.needB[m] ? 1 : 0};
   }
   return out;
 }
@@ -1196,7 +1244,7 @@ DevModel relocated(DevModel d, char* to) {
 
 struct morap_image {
   int device = 0;
-  size_t bytes = 0;
+  size_t bytes = 0, bytesA = 0;  // segment B = [bytesA, bytes)
   void* host = nullptr;           // pinned
   std::vector<DevModel> dm;       // pointers relative to kImageBase
   std::vector<HostModel> hm;
@@ -1305,7 +1353,8 @@ int morap_cuda_create(int device, morap_ctx** out) {
   if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return MORAP_CUDA_ERROR; }
   if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->polReady, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->polCopied, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&ctx->polCopied, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->segBReady, cudaEventDisableTiming) != cudaSuccess) {
     delete ctx;
     return MORAP_CUDA_ERROR;
   }
@@ -1345,6 +1394,7 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   }
   if (ctx->polReady) cudaEventDestroy(ctx->polReady);
   if (ctx->polCopied) cudaEventDestroy(ctx->polCopied);
+  if (ctx->segBReady) cudaEventDestroy(ctx->segBReady);
   cudaFree(ctx->dBar);
   cudaFree(ctx->dFinCount);
   cudaFree(ctx->persistArena);
@@ -1415,6 +1465,7 @@ int morap_cuda_build_image(morap_ctx* ctx, int nmodels, const morap_csr_view* mo
   auto img = std::make_unique<morap_image>();
   img->device = ctx->device;
   img->bytes = P.bytes;
+  img->bytesA = P.bytesA;
   if (P.bytes) CK(cudaMallocHost(&img->host, P.bytes));
   img->dm.resize(nmodels);
   std::atomic<bool> copyFailed{false};
@@ -1435,7 +1486,16 @@ int morap_cuda_upload_image(morap_ctx* ctx, const morap_image* img, int32_t* ids
   int rc;
   void* dev = nullptr;
   if ((rc = acquire_block(ctx, img->bytes, &dev))) return rc;
-  CK(cudaMemcpyAsync(dev, img->host, img->bytes, cudaMemcpyHostToDevice, ctx->stream));
+  // segment A (what the compact sweeps read) on the stream; segment B (evaluate paths) on the
+  // side stream, overlapping the first optimize batch -- the stream waits for it before the
+  // first kernel that reads it (wait_segment_b)
+  CK(cudaMemcpyAsync(dev, img->host, img->bytesA, cudaMemcpyHostToDevice, ctx->stream));
+  if (img->bytes > img->bytesA) {
+    CK(cudaMemcpyAsync(static_cast<char*>(dev) + img->bytesA, static_cast<const char*>(img->host) + img->bytesA,
+                       img->bytes - img->bytesA, cudaMemcpyHostToDevice, ctx->side));
+    CK(cudaEventRecord(ctx->segBReady, ctx->side));
+    ctx->segBPending = true;
+  }
   ctx->stats[9] += static_cast<double>(img->bytes);
   std::vector<DevModel> built(img->dm.size());
   for (size_t m = 0; m < built.size(); ++m) built[m] = relocated(img->dm[m], static_cast<char*>(dev));
@@ -1448,6 +1508,8 @@ int morap_cuda_release_models(morap_ctx* ctx) {
   if (!ctx) return MORAP_INVALID_CONFIG;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  cudaStreamSynchronize(ctx->side);  // an image upload's segment B may still be copying
+  ctx->segBPending = false;
   for (size_t q = 0; q < ctx->modelAllocs.size(); ++q)
     ctx->freeModelAllocs.emplace_back(ctx->modelAllocs[q], ctx->modelAllocBytes[q]);
   ctx->modelAllocs.clear();
