@@ -80,7 +80,9 @@ struct DevModel {
   // tile.r0 and trnOffset[r + 1] - tile.k0 (u16), succW, and copies of probIdx / rclass / done
   const uint32_t* stW;   // per state: row end | transition end << 10 | done << 21 (tile-relative)
   const uint32_t* rowW;  // per row: tile-relative transition end (11 bits) | reward class << 11
-  const uint32_t* trW;   // per transition: window offset (0xFFFF outside) | probability index << 16
+  const uint32_t* trW;   // per transition: window offset | probability index << 16 (outside the
+                         // window: bit 15 + index j into outSucc in bits 0-14, 24-31)
+  const int32_t* outSucc;  // successors of the out-of-window transitions, in transition order
   const TilePos* tilePos;     // ntiles
   // frozen-tile skipping: stamp groups (32 states) of the successors outside each tile's
   // window, outGrp[outIdx[t] .. outIdx[t + 1]) (sorted, distinct; a single -1: too many)

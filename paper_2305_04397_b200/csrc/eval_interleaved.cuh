@@ -22,7 +22,8 @@ struct InterArgs {
   double* xi;    // 2 x total x R, zeroed (x = 0 at the start, numerics.hpp:141)
   double* rhoI;  // total x R, filled by the prologue from rhoC
   int R;         // 2 or 4
-  int direct;    // 1: the chosen row of each state comes from J.policy (no chain CSR built)
+  int direct;    // the chosen row of each state comes from J.policy (no chain CSR built), its
+                 // transitions from the model CSR (1) or from the compact sweep streams (2)
 };
 
 template <int R>
@@ -67,7 +68,48 @@ __global__ void __launch_bounds__(kPersistThreads, MORAP_PERSIST_MINB) k_eval_in
       const EvalJob& J = A.jobs[jl];
       const int sl = static_cast<int>(i - A.statePrefix[jl]);
       double r[R];
-      if (IA.direct) {
+      if (IA.direct == 2) {
+        // the same chain decoded from the sweep streams: the state's tile,
+        // its state word (done), the chosen row's word (transition end, reward class), the
+        // transition words (window offset or out-of-window index, probability index)
+        const DevModel& M = A.models[J.model];
+        int lo = 0, hi = M.ntiles - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (__ldg(M.tileStart + mid) <= sl) lo = mid; else hi = mid - 1;
+        }
+        const TileDesc& d = M.tiles[lo];
+        const TilePos& P = M.tilePos[lo];
+        int nl = 0, cls = 0;
+        int2 sc = make_int2(0, 0);
+        double2 pr = make_double2(0.0, 0.0);
+        if (!(__ldg(M.stW + P.row + (sl - d.s0)) >> 21 & 1u)) {
+          const int lr = J.policy[sl] - d.r0;
+          const uint32_t rw = __ldg(M.rowW + P.trn + lr);
+          const int kb = lr ? static_cast<int>(__ldg(M.rowW + P.trn + lr - 1) & 0x7FFu) : 0;
+          nl = static_cast<int>(rw & 0x7FFu) - kb;
+          cls = static_cast<int>(rw >> 11);
+          auto succOf = [&](uint32_t w) {
+            const unsigned o = w & 0xFFFFu;
+            return o < 0x8000u ? d.wlo + static_cast<int>(o) : __ldg(M.outSucc + ((o & 0x7FFFu) | ((w >> 24) << 15)));
+          };
+          if (nl > 0) {
+            const uint32_t w0 = __ldg(M.trW + P.succ + kb);
+            sc.x = succOf(w0);
+            pr.x = M.probDict[(w0 >> 16) & 0xFFu];
+          }
+          if (nl > 1) {
+            const uint32_t w1 = __ldg(M.trW + P.succ + kb + 1);
+            sc.y = succOf(w1);
+            pr.y = M.probDict[(w1 >> 16) & 0xFFu];
+          }
+        }
+        sN[li] = static_cast<uint8_t>(nl);
+        sSucc[li] = sc;
+        sProb[li] = pr;
+#pragma unroll
+        for (int o = 0; o < R; ++o) r[o] = o < J.nrhs && nl > 0 ? M.classTable[cls * M.K + J.objIdx[o]] : 0.0;
+      } else if (IA.direct) {
         // the policy chain of k_chain_fill, read in place: the chosen row's transitions
         // (succ, model probability) and its reward per RHS; done states: empty, reward 0
         const DevModel& M = A.models[J.model];

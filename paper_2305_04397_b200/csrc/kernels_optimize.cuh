@@ -883,7 +883,7 @@ struct alignas(16) CmpInfo {
   double* y;
   int32_t* policy;
   const DevModel* model;
-  const int32_t* succG;  // absolute successors (out-of-window transitions)
+  const int32_t* succG;  // the model's out-of-window successors (DevModel::outSucc)
   const double* rho;
 };
 
@@ -900,7 +900,7 @@ __device__ __forceinline__ double cmp_tile(const CmpInfo& v, unsigned char* st, 
   } else if (v.fits) {
     // Tile-relative u16 row ends per state: state i owns rows [rowE[i-1], rowE[i]) (0 for
     // i = 0). One u32 word per row: transition end (tile-relative, bits 0-10) and reward
-    // class (bits 11-31); one u32 word per transition: window offset (low 16 bits, 0xFFFF
+    // class (bits 11-31); one u32 word per transition: window offset (low 16 bits, bit 15 set
     // outside the window) and probability index (bits 16-23) -- one shared-memory load
     // each instead of two (the compute warps are bound by shared-memory wavefronts).
     // Padded per-tile streams: every slice starts at offset 0 of its region.
@@ -965,9 +965,9 @@ __device__ __forceinline__ double cmp_tile(const CmpInfo& v, unsigned char* st, 
         } else {
           auto xAt = [&](int q, uint32_t w) {  // window offset staged; absolute successor only outside it
             const unsigned o = w & 0xFFFFu;
-            MORAP_CHECK(o == 0xFFFFu ? v.k0 + q < v.model->nnz && __ldg(v.succG + v.k0 + q) < v.model->S
-                                     : o < static_cast<unsigned>(kXWin + 2));
-            return o != 0xFFFFu ? xwS[o] : __ldg(x + __ldg(v.succG + v.k0 + q));
+            const unsigned j = (o & 0x7FFFu) | ((w >> 24) << 15);  // out-of-window: outSucc index
+            MORAP_CHECK(o & 0x8000u ? __ldg(v.succG + j) < v.model->S : o < static_cast<unsigned>(kXWin + 2));
+            return o < 0x8000u ? xwS[o] : __ldg(x + __ldg(v.succG + j));
           };
           for (int r = rb; r < re; ++r) {
             const uint32_t rw = rowW[r];
@@ -975,7 +975,7 @@ __device__ __forceinline__ double cmp_tile(const CmpInfo& v, unsigned char* st, 
             double acc = __ldg(crho + (rw >> 11));
             for (int q = kb; q < ke; ++q) {
               const uint32_t w = trW[q];
-              acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + (w >> 16)), xAt(q, w)));
+              acc = __dadd_rn(acc, __dmul_rn(__ldg(dict + ((w >> 16) & 0xFFu)), xAt(q, w)));
             }
             kb = ke;
             if (bestRow < 0 || acc > best) {
@@ -1208,7 +1208,7 @@ __global__ void __launch_bounds__(kTmaThreads, MORAP_CMP_CTAS) k_greedy_sweep_cm
           rec.y = curJ->buf[parity ^ 1];
           rec.policy = curJ->policy;
           rec.model = curM;
-          rec.succG = curM->succ;
+          rec.succG = curM->outSucc;  // out-of-window successors of the model
           rec.rho = curJ->rho;
           info[b] = rec;
         }

@@ -87,6 +87,7 @@ struct morap_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;           // policy prefetch copies (overlap the evaluate sweeps)
   cudaEvent_t polReady = nullptr, polCopied = nullptr;
+  cudaStream_t upload = nullptr;    // segment B copies of image uploads (not the policy side stream)
   cudaEvent_t segBReady = nullptr;  // segment B of the last image upload is on the device
   bool segBPending = false;         // ... and the stream has not waited for it yet
   std::vector<int32_t> polPrefetched;    // jobs whose policies sit in polStage (in this order)
@@ -190,7 +191,9 @@ struct morap_ctx {
   int persistBlocks = 0;
   bool usePersistCache = false;
   bool useInterleaved = false;  // k_eval_interleaved for cached-chain evaluate batches
-  bool evalDirect = false;      // current evaluate batch: chains read from the policies in-kernel
+  int evalDirect = 0;  // current evaluate batch builds its chains in-kernel from the policies: 1 via
+                       // the model CSR (segment B), 2 via the sweep streams (segment A only)
+  bool evalModelRewards = false;  // current evaluate batch: rewards are the models' own objectives
   unsigned* dBar = nullptr;   // grid-barrier counter + generation
   unsigned* dFinCount = nullptr;  // CTAs done in the current compact sweep (fused finalize)
   void* persistArena = nullptr;
@@ -695,8 +698,12 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
 
 // Computes final-sweep argmax policies for the listed optimize jobs (on the device).
 int extract_policies(morap_ctx* ctx, const std::vector<int32_t>& jobsIn) {
-  int rcB;
-  if ((rcB = wait_segment_b(ctx))) return rcB;
+  for (int j : jobsIn)  // compact all-fit models: the policy sweep reads segment A only
+    if (!ctx->optCompact || ctx->hm[ctx->optModel[j]].needB) {
+      int rcB;
+      if ((rcB = wait_segment_b(ctx))) return rcB;
+      break;
+    }
   std::vector<int32_t> jobs;
   for (int j : jobsIn)
     if (!ctx->optPolicyReady[j] && ctx->optSweeps[j] > 0) jobs.push_back(j);
@@ -800,7 +807,7 @@ int run_eval_persistent(morap_ctx* ctx, int njobs, double eps, int cap) {
   // interleaved RHS (k_eval_interleaved) whenever the chains are cached: every job <= 4 RHS
   // here; `direct`: the kernel reads each state's chosen row from the policy itself (the
   // chain CSR was not built)
-  InterArgs ia{a, nullptr, nullptr, R, ctx->evalDirect ? 1 : 0};
+  InterArgs ia{a, nullptr, nullptr, R, ctx->evalDirect};
   const bool inter = a.cacheStates > 0 && ctx->useInterleaved;
   if (inter) {
     char* ib = base + align_up(slotBytes, 256) + align_up(8ull * (njobs + 1), 256);
@@ -835,7 +842,6 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
                   double* value_out, int32_t* sweeps_out, double* residual_out, int32_t* status_out,
                   const std::vector<uint32_t>& maskInit, const std::vector<int32_t>& statusInit) {
   int rc;
-  if ((rc = wait_segment_b(ctx))) return rc;
   if ((rc = ensure_ctl(ctx, njobs))) return rc;
   if (static_cast<size_t>(njobs) > ctx->dEvalJobsCap) {
     cudaFree(ctx->dEvalJobsRaw);
@@ -903,8 +909,18 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
   lap("setup");
   ctx->evalTma = tmaOk;
   const bool persistent = tmaOk && ctx->usePersistent && njobs <= kPersistMaxJobs;
-  // the interleaved kernel builds its shared-memory chains from the policies directly
-  ctx->evalDirect = persistent && ctx->useInterleaved && eval_cache_states(ctx, njobs) > 0;
+  // the interleaved kernel builds its shared-memory chains from the policies directly; from
+  // the compact sweep streams when every model has them (and all its tiles fit) and the
+  // rewards are the models' objectives (their class tables) -- then nothing in this batch
+  // reads the upload's segment B
+  ctx->evalDirect = persistent && ctx->useInterleaved && eval_cache_states(ctx, njobs) > 0 ? 1 : 0;
+  if (ctx->evalDirect && ctx->evalModelRewards) {
+    bool streams = true;
+    for (int j = 0; j < njobs && streams; ++j)
+      streams = ctx->dm[proto[j].model].compact && !ctx->hm[proto[j].model].needB;
+    if (streams) ctx->evalDirect = 2;
+  }
+  if (ctx->evalDirect != 2 && (rc = wait_segment_b(ctx))) return rc;
   if (tmaOk && !active.empty() && !ctx->evalDirect) {
     // policy chains of the active jobs (count, per-job scan, fill)
     const int nl = ctx->hCtl->nactive, tt = ctx->hCtl->totalTiles;
@@ -970,11 +986,11 @@ struct UploadPrep {
   std::vector<std::vector<TileDesc>> descs;
   std::vector<CompactStream> compact;
   std::vector<int32_t> maxRowNnz;
-  // The block has two segments: A = what the compact sweeps read (succ for out-of-window
-  // successors, tiles, dictionaries, the per-tile streams, stamp groups), B = the rest
-  // (rowOffset, trnOffset, done, probIdx, rclass, and the fp64 arrays of full uploads),
-  // needed by the evaluate paths and by non-compact sweeps. An image upload copies A on the
-  // stream and B on the side stream, overlapped with the first optimize batch.
+  // The block has two segments: A = what the compact sweeps read (tiles, dictionaries, the
+  // per-tile streams, stamp groups, the out-of-window successors), B = the rest (rowOffset,
+  // trnOffset, succ, done, probIdx, rclass, and the fp64 arrays of full uploads),
+  // needed by the chain-CSR evaluate paths and by non-compact sweeps. An image upload copies
+  // A on the stream and B on the upload stream, overlapped with the query.
   std::vector<size_t> offA, offB;  // byte offset of each model in its segment
   std::vector<size_t> lenA, lenB;
   std::vector<char> lean;          // stored without fp64 prob / objectives
@@ -1047,16 +1063,16 @@ int prepare_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, Up
     bool fitsAll = true;
     for (const TileDesc& d : descs[m]) fitsAll = fitsAll && (d.fits || d.s0 == v.num_states);
     P.needB[m] = !compact[m].ok || !fitsAll;
-    size_t a = align_up(4ull * v.nnz, 256) + align_up(4ull * tiles[m].size(), 256) +
-               align_up(sizeof(TileDesc) * descs[m].size(), 256);
-    size_t b = align_up(4ull * (v.num_states + 1), 256) + align_up(4ull * (v.num_rows + 1), 256) +
+    size_t a = align_up(4ull * tiles[m].size(), 256) + align_up(sizeof(TileDesc) * descs[m].size(), 256);
+    size_t b = align_up(4ull * v.nnz, 256) + align_up(4ull * (v.num_states + 1), 256) + align_up(4ull * (v.num_rows + 1), 256) +
                (lean ? 0 : align_up(8ull * v.nnz, 256)) + align_up(1ull * v.num_states, 256) +
                (lean ? 0 : static_cast<size_t>(v.num_objectives) * align_up(8ull * v.num_rows, 256));
     if (compact[m].ok) {
       a += align_up(8ull * compact[m].dict.size(), 256) + align_up(8ull * compact[m].table.size(), 256) +
            align_up(4ull * compact[m].nTrW, 256) + align_up(4ull * compact[m].nStW, 256) +
            align_up(4ull * compact[m].nRowW, 256) + align_up(sizeof(TilePos) * compact[m].pos.size(), 256) +
-           align_up(4ull * compact[m].outIdx.size(), 256) + align_up(4ull * compact[m].outGrp.size(), 256);
+           align_up(4ull * compact[m].outIdx.size(), 256) + align_up(4ull * compact[m].outGrp.size(), 256) +
+           align_up(4ull * compact[m].outSucc.size(), 256);
       b += align_up(v.nnz, 256) + align_up(2ull * v.num_rows, 256);
     }
     P.offA[m] = totA;
@@ -1100,7 +1116,7 @@ void pack_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, cons
     };
     dmod.rowOffset = reinterpret_cast<const int32_t*>(put(1, v.row_offset, 4ull * (v.num_states + 1)));
     dmod.trnOffset = reinterpret_cast<const int32_t*>(put(1, v.trn_offset, 4ull * (v.num_rows + 1)));
-    dmod.succ = reinterpret_cast<const int32_t*>(put(0, v.succ, 4ull * v.nnz));
+    dmod.succ = reinterpret_cast<const int32_t*>(put(1, v.succ, 4ull * v.nnz));
     const bool lean = P.lean[m];  // fp64 prob / objectives live in the tables
     if (!lean) dmod.prob = reinterpret_cast<const double*>(put(1, v.prob, 8ull * v.nnz));
     dmod.done = reinterpret_cast<const uint8_t*>(put(1, v.done, v.num_states));
@@ -1137,6 +1153,7 @@ void pack_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, cons
       dmod.tilePos = reinterpret_cast<const TilePos*>(put(0, c.pos.data(), sizeof(TilePos) * c.pos.size()));
       dmod.outIdx = reinterpret_cast<const int32_t*>(put(0, c.outIdx.data(), 4ull * c.outIdx.size()));
       dmod.outGrp = reinterpret_cast<const int32_t*>(put(0, c.outGrp.data(), 4ull * c.outGrp.size()));
+      dmod.outSucc = reinterpret_cast<const int32_t*>(put(0, c.outSucc.data(), 4ull * c.outSucc.size()));
       // compact stream: one 4-byte word per transition (window offset | index) and per row
       // (transition end | class) and per state (row end | transition end | done) + x 8 + y 8
       dmod.bytesPerSweep = 4ull * v.nnz + 4ull * v.num_rows + 20ull * v.num_states;
@@ -1237,6 +1254,7 @@ DevModel relocated(DevModel d, char* to) {
   relocate(d.tilePos, to);
   relocate(d.outIdx, to);
   relocate(d.outGrp, to);
+  relocate(d.outSucc, to);
   return d;
 }
 
@@ -1354,7 +1372,8 @@ int morap_cuda_create(int device, morap_ctx** out) {
   if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->polReady, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->polCopied, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->segBReady, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&ctx->segBReady, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->upload, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
     return MORAP_CUDA_ERROR;
   }
@@ -1395,6 +1414,10 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   if (ctx->polReady) cudaEventDestroy(ctx->polReady);
   if (ctx->polCopied) cudaEventDestroy(ctx->polCopied);
   if (ctx->segBReady) cudaEventDestroy(ctx->segBReady);
+  if (ctx->upload) {
+    cudaStreamSynchronize(ctx->upload);
+    cudaStreamDestroy(ctx->upload);
+  }
   cudaFree(ctx->dBar);
   cudaFree(ctx->dFinCount);
   cudaFree(ctx->persistArena);
@@ -1486,14 +1509,14 @@ int morap_cuda_upload_image(morap_ctx* ctx, const morap_image* img, int32_t* ids
   int rc;
   void* dev = nullptr;
   if ((rc = acquire_block(ctx, img->bytes, &dev))) return rc;
-  // segment A (what the compact sweeps read) on the stream; segment B (evaluate paths) on the
-  // side stream, overlapping the first optimize batch -- the stream waits for it before the
-  // first kernel that reads it (wait_segment_b)
+  // segment A (what the compact sweeps read) on the stream; segment B (evaluate paths,
+  // non-compact sweeps) on the upload stream, overlapping the query -- the stream waits for
+  // it before the first kernel that reads it (wait_segment_b)
   CK(cudaMemcpyAsync(dev, img->host, img->bytesA, cudaMemcpyHostToDevice, ctx->stream));
   if (img->bytes > img->bytesA) {
     CK(cudaMemcpyAsync(static_cast<char*>(dev) + img->bytesA, static_cast<const char*>(img->host) + img->bytesA,
-                       img->bytes - img->bytesA, cudaMemcpyHostToDevice, ctx->side));
-    CK(cudaEventRecord(ctx->segBReady, ctx->side));
+                       img->bytes - img->bytesA, cudaMemcpyHostToDevice, ctx->upload));
+    CK(cudaEventRecord(ctx->segBReady, ctx->upload));
     ctx->segBPending = true;
   }
   ctx->stats[9] += static_cast<double>(img->bytes);
@@ -1508,7 +1531,7 @@ int morap_cuda_release_models(morap_ctx* ctx) {
   if (!ctx) return MORAP_INVALID_CONFIG;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  cudaStreamSynchronize(ctx->side);  // an image upload's segment B may still be copying
+  cudaStreamSynchronize(ctx->upload);  // an image upload's segment B may still be copying
   ctx->segBPending = false;
   for (size_t q = 0; q < ctx->modelAllocs.size(); ++q)
     ctx->freeModelAllocs.emplace_back(ctx->modelAllocs[q], ctx->modelAllocBytes[q]);
@@ -1689,6 +1712,7 @@ int morap_cuda_evaluate_optimized(morap_ctx* ctx, int njobs, const int32_t* opt_
     if (!ctx->dm[model].obj[0] && !ctx->useTma)
       return ctx->fail(MORAP_INVALID_CONFIG, "lean models are evaluated through policy chains");
   }
+  ctx->evalModelRewards = true;  // rewards are the models' own objective vectors
   const int rc2 = evaluate_impl(ctx, static_cast<int>(proto.size()), proto, eps, sweep_cap, value_out, sweeps_out,
                                 residual_out, status_out, mask, st);
   ctx->evalSplitG = G;
@@ -1750,6 +1774,7 @@ int morap_cuda_evaluate(morap_ctx* ctx, int njobs, const int32_t* model_ids, con
       st[static_cast<size_t>(j) * MORAP_MAX_RHS] = MORAP_INVALID_MODEL;
     }
   }
+  ctx->evalModelRewards = false;  // explicit reward vectors
   return evaluate_impl(ctx, njobs, proto, eps, sweep_cap, value_out, sweeps_out, residual_out, status_out, mask, st);
 }
 

@@ -80,12 +80,15 @@ struct CompactStream {
                                                // (written straight into the upload staging: fill_streams)
   std::vector<TilePos> pos;
   std::vector<int32_t> outIdx, outGrp;        // out-of-window stamp groups per tile (DevModel)
+  std::vector<int32_t> outSucc;               // out-of-window successors, in transition order
 };
 
 // The sweep streams of a compact model, tile-major: each tile's slice of every stream
 // starts on a 16-byte boundary (padded), so one bulk copy per stream lands at offset 0 of
 // its stage region. u16 window offsets succW = succ - wlo inside the tile's x window
-// (0xFFFF outside), u16 ends relative to the tile, allIn / simple flags per tile.
+// (outside: bit 15 set and j = the model's j-th out-of-window transition, outSucc[j], in
+// bits 0-14 and 24-31 -- allIn tiles have none, so their words keep bits 24-31 clear), u16
+// ends relative to the tile, allIn / simple flags per tile.
 // layout_streams: slice positions, stream sizes, the per-tile flags and out-of-window
 // stamp groups; fill_streams (at packing time) writes the words into the staging buffer.
 void layout_streams(const morap_csr_view& v, std::vector<TileDesc>& desc, CompactStream& c) {
@@ -110,9 +113,14 @@ void layout_streams(const morap_csr_view& v, std::vector<TileDesc>& desc, Compac
   c.nTrW = nSucc;
   c.outIdx.assign(nt + 1, 0);
   c.outGrp.clear();
+  c.outSucc.clear();
   for (size_t t = 0; t < nt; ++t) {
     TileDesc& d = desc[t];
     const TileDesc& e = desc[t + 1];
+    if (d.fits)  // the successors outside the window, in transition order (the sweep reads
+                 // them through outSucc instead of the full succ array)
+      for (int k = d.k0; k < e.k0; ++k)
+        if (static_cast<unsigned>(v.succ[k] - d.wlo) >= static_cast<unsigned>(d.wn)) c.outSucc.push_back(v.succ[k]);
     int simple = 1;
     for (int r = d.r0; r < e.r0; ++r) simple &= v.trn_offset[r + 1] - v.trn_offset[r] <= 2 ? 1 : 0;
     d.simple = simple;
@@ -138,11 +146,13 @@ void layout_streams(const morap_csr_view& v, std::vector<TileDesc>& desc, Compac
     }
     c.outIdx[t + 1] = static_cast<int32_t>(c.outGrp.size());
   }
+  if (c.outSucc.size() >= (1u << 23)) c.ok = false;  // the transition word indexes outSucc with 23 bits
 }
 
 void fill_streams(const morap_csr_view& v, const std::vector<TileDesc>& desc, const CompactStream& c, uint32_t* stW,
                   uint32_t* rowW, uint32_t* trW) {
   const size_t nt = desc.size() - 1;
+  unsigned j = 0;  // out-of-window transitions of the model so far (< 2^23, checked at layout)
   for (size_t t = 0; t < nt; ++t) {
     const TileDesc &d = desc[t], &e = desc[t + 1];
     const TilePos& p = c.pos[t];
@@ -158,7 +168,12 @@ void fill_streams(const morap_csr_view& v, const std::vector<TileDesc>& desc, co
         rowW[b++] = static_cast<uint32_t>(v.trn_offset[r + 1] - d.k0) | (static_cast<uint32_t>(c.cls[r]) << 11);
       for (int k = d.k0; k < e.k0; ++k) {
         const unsigned o = static_cast<unsigned>(v.succ[k] - d.wlo);
-        trW[z++] = (o < static_cast<unsigned>(d.wn) ? o : 0xFFFFu) | (static_cast<uint32_t>(c.idx[k]) << 16);
+        uint32_t word = o;
+        if (o >= static_cast<unsigned>(d.wn)) {  // the model's j-th out-of-window transition
+          word = 0x8000u | (j & 0x7FFFu) | ((j >> 15) << 24);
+          ++j;
+        }
+        trW[z++] = word | (static_cast<uint32_t>(c.idx[k]) << 16);
       }
     }
     for (; a < endRow; ++a) stW[a] = 0u;  // padding (never read)
