@@ -771,19 +771,35 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(const DevModel* __restri
 // value at the initial state of every job's final buffer (OptimizeResult::value,
 // numerics.hpp:120) gathered into one array -> one D2H copy per batch
 
+// Results of a batch packed for ONE device-to-host copy: value (initial state of the final
+// buffer), residual, sweeps, status of m entries -> out[0..m), out[m..2m), then 2 x m int32.
+__device__ __forceinline__ void pack_result(double* out, int m, int q, double value, double residual, int sweeps,
+                                            int status) {
+  out[q] = value;
+  out[m + q] = residual;
+  int32_t* o = reinterpret_cast<int32_t*>(out + 2 * static_cast<size_t>(m));
+  o[q] = sweeps;
+  o[m + q] = status;
+}
+
 __global__ void k_gather_opt(const DevModel* __restrict__ models, const OptJob* __restrict__ jobs, int njobs,
-                             const int32_t* __restrict__ sweeps, double* __restrict__ out) {
+                             const int32_t* __restrict__ sweeps, const int32_t* __restrict__ status,
+                             const double* __restrict__ residual, double* __restrict__ out) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < njobs; j += gridDim.x * blockDim.x) {
     const int sw = sweeps[j];
-    out[j] = sw > 0 ? jobs[j].buf[sw & 1][models[jobs[j].model].initial] : 0.0;
+    pack_result(out, njobs, j, sw > 0 ? jobs[j].buf[sw & 1][models[jobs[j].model].initial] : 0.0, residual[j], sw,
+                status[j]);
   }
 }
 
 __global__ void k_gather_eval(const DevModel* __restrict__ models, const EvalJob* __restrict__ jobs, int njobs,
-                              const int32_t* __restrict__ sweeps, double* __restrict__ out) {
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < njobs * MORAP_MAX_RHS; q += gridDim.x * blockDim.x) {
+                              const int32_t* __restrict__ sweeps, const int32_t* __restrict__ status,
+                              const double* __restrict__ residual, double* __restrict__ out) {
+  const int m = njobs * MORAP_MAX_RHS;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < m; q += gridDim.x * blockDim.x) {
     const int j = q / MORAP_MAX_RHS, o = q % MORAP_MAX_RHS;
     const int sw = sweeps[q];
-    out[q] = (o < jobs[j].nrhs && sw > 0) ? jobs[j].buf[o][sw & 1][models[jobs[j].model].initial] : 0.0;
+    pack_result(out, m, q, (o < jobs[j].nrhs && sw > 0) ? jobs[j].buf[o][sw & 1][models[jobs[j].model].initial] : 0.0,
+                residual[q], sw, status[q]);
   }
 }

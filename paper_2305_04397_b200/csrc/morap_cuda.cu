@@ -136,7 +136,10 @@ struct morap_ctx {
   int32_t* dNrhs = nullptr;
   int32_t* dSweeps = nullptr;
   double* dResidual = nullptr;
-  double* dGather = nullptr;
+  double* dGather = nullptr;   // packed batch results (pack_result), 24 B per entry
+  double* hGather = nullptr;   // pinned twin
+  char* upRing = nullptr;      // pinned ring for the small host-to-device copies (h2d)
+  size_t upRingBytes = 0, upRingPos = 0;
   int32_t* dStatus = nullptr;
   int32_t* dAlive = nullptr;
   void* evalStage = nullptr;
@@ -227,6 +230,36 @@ cudaError_t d2h(morap_ctx* ctx, void* dst, const void* src, size_t bytes, bool s
               : cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream);
 }
 
+// Small host-to-device copies (job tables, lists, masks) through a pinned ring: the driver
+// does not stage pageable memory and the host never waits for the copy. Positions only grow
+// until the ring wraps, and a wrap first drains the stream, so no pending copy is overwritten.
+int h2d(morap_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return MORAP_OK;
+  const size_t need = (bytes + 255) / 256 * 256;
+  if (need > ctx->upRingBytes || ctx->upRingPos + need > ctx->upRingBytes) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->upRingPos = 0;
+    if (need > ctx->upRingBytes) {
+      if (ctx->upRing) cudaFreeHost(ctx->upRing);
+      ctx->upRing = nullptr;
+      ctx->upRingBytes = 0;
+      const size_t cap = std::max<size_t>(need, 8u << 20);
+      CK(cudaMallocHost(&ctx->upRing, cap));
+      ctx->upRingBytes = cap;
+    }
+  }
+  char* at = ctx->upRing + ctx->upRingPos;
+  std::memcpy(at, src, bytes);
+  ctx->upRingPos += need;
+  CK(cudaMemcpyAsync(dst, at, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return MORAP_OK;
+}
+#define H2D(dst, src, bytes)                                   \
+  do {                                                         \
+    const int rcH_ = h2d(ctx, (dst), (src), (bytes));          \
+    if (rcH_) return rcH_;                                     \
+  } while (0)
+
 // The stream waits for the last image upload's segment B before a kernel that reads it.
 int wait_segment_b(morap_ctx* ctx) {
   if (!ctx->segBPending) return MORAP_OK;
@@ -249,7 +282,9 @@ int ensure_ctl(morap_ctx* ctx, size_t njobs) {
   cudaFree(ctx->dStatus);
   cudaFree(ctx->dGather);
   cudaFree(ctx->dAlive);
-  CK(cudaMalloc(&ctx->dGather, cap * MORAP_MAX_RHS * sizeof(double)));
+  CK(cudaMalloc(&ctx->dGather, cap * MORAP_MAX_RHS * 3 * sizeof(double)));
+  if (ctx->hGather) cudaFreeHost(ctx->hGather);
+  CK(cudaMallocHost(&ctx->hGather, cap * MORAP_MAX_RHS * 3 * sizeof(double)));
   CK(cudaMalloc(&ctx->dAlive, cap * sizeof(int32_t)));
   CK(cudaMalloc(&ctx->dList, cap * sizeof(int32_t)));
   CK(cudaMalloc(&ctx->dPrefix, (cap + 1) * sizeof(int32_t)));
@@ -277,8 +312,7 @@ int upload_models_table(morap_ctx* ctx) {
     CK(cudaMalloc(&ctx->dModels, cap * sizeof(DevModel)));
     ctx->dModelsCap = cap;
   }
-  CK(cudaMemcpyAsync(ctx->dModels, ctx->dm.data(), ctx->dm.size() * sizeof(DevModel), cudaMemcpyHostToDevice,
-                     ctx->stream));
+  H2D(ctx->dModels, ctx->dm.data(), ctx->dm.size() * sizeof(DevModel));
   return MORAP_OK;
 }
 
@@ -471,9 +505,9 @@ int run_loop(morap_ctx* ctx, int kind, double eps, int cap) {
 int init_ctl(morap_ctx* ctx, const std::vector<int32_t>& active, const std::vector<int32_t>& jobModel) {
   std::vector<int32_t> prefix(active.size() + 1, 0);
   for (size_t a = 0; a < active.size(); ++a) prefix[a + 1] = prefix[a] + ctx->hm[jobModel[active[a]]].ntiles;
-  if (!active.empty()) CK(cudaMemcpyAsync(ctx->dList, active.data(), active.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->dPrefix, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->dJobModel, jobModel.data(), jobModel.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if (!active.empty()) H2D(ctx->dList, active.data(), active.size() * 4);
+  H2D(ctx->dPrefix, prefix.data(), prefix.size() * 4);
+  H2D(ctx->dJobModel, jobModel.data(), jobModel.size() * 4);
   Ctl c{};
   c.nactive = static_cast<int32_t>(active.size());
   c.totalTiles = prefix.back();
@@ -617,17 +651,16 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
     for (int j = 0; j < njobs; ++j)
       if (!ctx->dm[model_ids[j]].prob)
         return ctx->fail(MORAP_INVALID_CONFIG, "a batch with lean models cannot include non-compact models");
-  CK(cudaMemcpyAsync(ctx->dOptJobs, ctx->hOptJobs.data(), njobs * sizeof(OptJob), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->dStatus, statusInit.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->dSweeps, zeroI.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
+  H2D(ctx->dOptJobs, ctx->hOptJobs.data(), njobs * sizeof(OptJob));
+  H2D(ctx->dStatus, statusInit.data(), njobs * 4);
+  CK(cudaMemsetAsync(ctx->dSweeps, 0, njobs * 4, ctx->stream));
   CK(cudaMemsetAsync(ctx->dDelta, 0, 2 * njobs * sizeof(unsigned long long), ctx->stream));  // two parities
   CK(cudaMemsetAsync(ctx->dResidual, 0, njobs * sizeof(double), ctx->stream));
   if ((rc = init_ctl(ctx, active, ctx->optModel))) return rc;
   if (ctx->optSkip && !active.empty()) {
     std::vector<int32_t> alive(njobs, 0);  // act: 1 while the job iterates
     for (int j : active) alive[j] = 1;
-    CK(cudaMemcpyAsync(ctx->dAlive, alive.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));  // `alive` is a local
+    H2D(ctx->dAlive, alive.data(), njobs * 4);
     int maxTiles = 0;
     for (int j : active) maxTiles = std::max(maxTiles, ctx->hm[model_ids[j]].ntiles);
     for (size_t s0 = 0; s0 < active.size(); s0 += 65535) {  // gridDim.y limit
@@ -664,24 +697,23 @@ int optimize_impl(morap_ctx* ctx, int njobs, const int32_t* model_ids, const dou
                    ctx->lastOptSweeps, ctx->launchedOptSweeps);
   }
 
-  // results: one gather kernel + one copy per array, one synchronisation
+  // results: one gather kernel packs them, one copy into pinned memory, one synchronisation
   ctx->optSweeps.assign(njobs, 0);
   ctx->optStatus.assign(njobs, 0);
-  std::vector<double> resid(njobs), vals(njobs);
   k_gather_opt<<<(njobs + 255) / 256, 256, 0, ctx->stream>>>(ctx->dModels, ctx->dOptJobs, njobs, ctx->dSweeps,
-                                                             ctx->dGather);
+                                                             ctx->dStatus, ctx->dResidual, ctx->dGather);
   CK(cudaGetLastError());
-  CK(d2h(ctx, ctx->optSweeps.data(), ctx->dSweeps, njobs * 4));
-  CK(d2h(ctx, ctx->optStatus.data(), ctx->dStatus, njobs * 4));
-  CK(d2h(ctx, resid.data(), ctx->dResidual, njobs * 8));
-  CK(d2h(ctx, vals.data(), ctx->dGather, njobs * 8));
+  CK(d2h(ctx, ctx->hGather, ctx->dGather, 24ull * njobs));
   CK(d2h(ctx, ctx->hCtl, ctx->dCtl, sizeof(Ctl)));
   CK(cudaStreamSynchronize(ctx->stream));
+  const int32_t* gi = reinterpret_cast<const int32_t*>(ctx->hGather + 2ull * njobs);
   double backups = 0;
   for (int j = 0; j < njobs; ++j) {
-    value_out[j] = vals[j];
+    ctx->optSweeps[j] = gi[j];
+    ctx->optStatus[j] = gi[njobs + j];
+    value_out[j] = ctx->hGather[j];
     if (sweeps_out) sweeps_out[j] = ctx->optSweeps[j];
-    if (residual_out) residual_out[j] = resid[j];
+    if (residual_out) residual_out[j] = ctx->hGather[njobs + j];
     if (status_out) status_out[j] = ctx->optStatus[j];
     backups += static_cast<double>(ctx->optSweeps[j]) * ctx->hm[model_ids[j]].nnz;
   }
@@ -710,7 +742,7 @@ int extract_policies(morap_ctx* ctx, const std::vector<int32_t>& jobsIn) {
   if (jobs.empty()) return MORAP_OK;
   int rc;
   if ((rc = init_ctl(ctx, jobs, ctx->optModel))) return rc;
-  CK(cudaMemcpyAsync(ctx->dSweeps, ctx->optSweeps.data(), ctx->optSweeps.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  H2D(ctx->dSweeps, ctx->optSweeps.data(), ctx->optSweeps.size() * 4);
   if (ctx->optCompact)
     k_greedy_sweep_cmp<true><<<ctx->cmpBlocks, kTmaThreads, kCmpSmemBytes, ctx->stream>>>(
         ctx->dModels, ctx->dOptJobs, ctx->dList, ctx->dPrefix, ctx->dCtl, ctx->dSweeps, nullptr, nullptr, FinArgs{});
@@ -785,7 +817,7 @@ int run_eval_persistent(morap_ctx* ctx, int njobs, double eps, int cap) {
   unsigned long long* slots = reinterpret_cast<unsigned long long*>(base);
   long long* dPrefix = reinterpret_cast<long long*>(base + align_up(slotBytes, 256));
   CK(cudaMemsetAsync(slots, 0, slotBytes, ctx->stream));
-  CK(cudaMemcpyAsync(dPrefix, prefix.data(), 8ull * (njobs + 1), cudaMemcpyHostToDevice, ctx->stream));
+  H2D(dPrefix, prefix.data(), 8ull * (njobs + 1));
   PersistArgs a{};
   a.models = ctx->dModels;
   a.jobs = static_cast<const EvalJob*>(ctx->dEvalJobsRaw);
@@ -891,10 +923,10 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
     if (maskInit[j]) active.push_back(j);
   }
   if (xBytes) CK(cudaMemsetAsync(ctx->evalArena, 0, xBytes, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->dEvalJobsRaw, ctx->hEvalJobs.data(), njobs * sizeof(EvalJob), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->dMask, maskInit.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->dNrhs, nrhs.data(), njobs * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->dStatus, statusInit.data(), njobs * MORAP_MAX_RHS * 4, cudaMemcpyHostToDevice, ctx->stream));
+  H2D(ctx->dEvalJobsRaw, ctx->hEvalJobs.data(), njobs * sizeof(EvalJob));
+  H2D(ctx->dMask, maskInit.data(), njobs * 4);
+  H2D(ctx->dNrhs, nrhs.data(), njobs * 4);
+  H2D(ctx->dStatus, statusInit.data(), njobs * MORAP_MAX_RHS * 4);
   CK(cudaMemsetAsync(ctx->dSweeps, 0, njobs * MORAP_MAX_RHS * 4, ctx->stream));
   CK(cudaMemsetAsync(ctx->dDelta, 0, njobs * MORAP_MAX_RHS * sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->dResidual, 0, njobs * MORAP_MAX_RHS * sizeof(double), ctx->stream));
@@ -943,19 +975,20 @@ int evaluate_impl(morap_ctx* ctx, int njobs, const std::vector<EvalJob>& proto, 
   }
 
   lap("sweeps");
-  ctx->evalSweeps.assign(static_cast<size_t>(njobs) * MORAP_MAX_RHS, 0);
-  std::vector<int32_t> st(static_cast<size_t>(njobs) * MORAP_MAX_RHS);
-  std::vector<double> res(static_cast<size_t>(njobs) * MORAP_MAX_RHS);
-  CK(d2h(ctx, ctx->evalSweeps.data(), ctx->dSweeps, njobs * MORAP_MAX_RHS * 4));
-  CK(d2h(ctx, st.data(), ctx->dStatus, njobs * MORAP_MAX_RHS * 4));
-  CK(d2h(ctx, res.data(), ctx->dResidual, njobs * MORAP_MAX_RHS * 8));
-  std::vector<double> vals(static_cast<size_t>(njobs) * MORAP_MAX_RHS, 0.0);
-  k_gather_eval<<<(njobs * MORAP_MAX_RHS + 255) / 256, 256, 0, ctx->stream>>>(
-      ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw, njobs, ctx->dSweeps, ctx->dGather);
+  const int mres = njobs * MORAP_MAX_RHS;
+  ctx->evalSweeps.assign(static_cast<size_t>(mres), 0);
+  k_gather_eval<<<(mres + 255) / 256, 256, 0, ctx->stream>>>(ctx->dModels, (const EvalJob*)ctx->dEvalJobsRaw, njobs,
+                                                              ctx->dSweeps, ctx->dStatus, ctx->dResidual,
+                                                              ctx->dGather);
   CK(cudaGetLastError());
-  CK(d2h(ctx, vals.data(), ctx->dGather, njobs * MORAP_MAX_RHS * 8));
+  CK(d2h(ctx, ctx->hGather, ctx->dGather, 24ull * mres));
   CK(d2h(ctx, ctx->hCtl, ctx->dCtl, sizeof(Ctl)));
   CK(cudaStreamSynchronize(ctx->stream));
+  const double* vals = ctx->hGather;
+  const double* res = ctx->hGather + mres;
+  const int32_t* gi = reinterpret_cast<const int32_t*>(ctx->hGather + 2ull * mres);
+  const int32_t* st = gi + mres;
+  for (int q2 = 0; q2 < mres; ++q2) ctx->evalSweeps[q2] = gi[q2];
   double backups = 0;
   size_t q = 0;  // outputs: every job's RHS in order (j * nrhs + o for a uniform batch)
   for (int j = 0; j < njobs; ++j) {
@@ -1405,6 +1438,8 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   cudaFree(ctx->dResidual);
   cudaFree(ctx->dStatus);
   cudaFree(ctx->dGather);
+  if (ctx->hGather) cudaFreeHost(ctx->hGather);
+  if (ctx->upRing) cudaFreeHost(ctx->upRing);
   cudaFree(ctx->evalStage);
   cudaFreeHost(ctx->stage);
   if (ctx->side) {
