@@ -138,8 +138,6 @@ struct morap_ctx {
   double* dResidual = nullptr;
   double* dGather = nullptr;   // packed batch results (pack_result), 24 B per entry
   double* hGather = nullptr;   // pinned twin
-  char* upRing = nullptr;      // pinned ring for the small host-to-device copies (h2d)
-  size_t upRingBytes = 0, upRingPos = 0;
   int32_t* dStatus = nullptr;
   int32_t* dAlive = nullptr;
   void* evalStage = nullptr;
@@ -230,28 +228,12 @@ cudaError_t d2h(morap_ctx* ctx, void* dst, const void* src, size_t bytes, bool s
               : cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream);
 }
 
-// Small host-to-device copies (job tables, lists, masks) through a pinned ring: the driver
-// does not stage pageable memory and the host never waits for the copy. Positions only grow
-// until the ring wraps, and a wrap first drains the stream, so no pending copy is overwritten.
+// Small host-to-device copies (job tables, lists, masks) from pageable memory: the driver
+// takes the bytes immediately (the source may be freed on return) and does not wait for the
+// device. (A pinned staging ring was slower: its copies queue behind an image upload's
+// segment-B copy on the copy engine, while small pageable copies travel inline.)
 int h2d(morap_ctx* ctx, void* dst, const void* src, size_t bytes) {
-  if (!bytes) return MORAP_OK;
-  const size_t need = (bytes + 255) / 256 * 256;
-  if (need > ctx->upRingBytes || ctx->upRingPos + need > ctx->upRingBytes) {
-    CK(cudaStreamSynchronize(ctx->stream));
-    ctx->upRingPos = 0;
-    if (need > ctx->upRingBytes) {
-      if (ctx->upRing) cudaFreeHost(ctx->upRing);
-      ctx->upRing = nullptr;
-      ctx->upRingBytes = 0;
-      const size_t cap = std::max<size_t>(need, 8u << 20);
-      CK(cudaMallocHost(&ctx->upRing, cap));
-      ctx->upRingBytes = cap;
-    }
-  }
-  char* at = ctx->upRing + ctx->upRingPos;
-  std::memcpy(at, src, bytes);
-  ctx->upRingPos += need;
-  CK(cudaMemcpyAsync(dst, at, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
   return MORAP_OK;
 }
 #define H2D(dst, src, bytes)                                   \
@@ -1439,7 +1421,6 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   cudaFree(ctx->dStatus);
   cudaFree(ctx->dGather);
   if (ctx->hGather) cudaFreeHost(ctx->hGather);
-  if (ctx->upRing) cudaFreeHost(ctx->upRing);
   cudaFree(ctx->evalStage);
   cudaFreeHost(ctx->stage);
   if (ctx->side) {
