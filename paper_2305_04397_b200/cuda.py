@@ -48,6 +48,9 @@ def load_library(path: str = CUDA_SO) -> C.CDLL:
         "morap_cuda_set_stream": (i32, [p, p]),
         "morap_cuda_last_error": (C.c_char_p, [p]),
         "morap_cuda_upload": (i32, [p, i32, p, p]),
+        "morap_cuda_build_image": (i32, [p, i32, p, C.POINTER(C.c_void_p)]),
+        "morap_cuda_upload_image": (i32, [p, p, p]),
+        "morap_cuda_free_image": (None, [p]),
         "morap_cuda_release_models": (i32, [p]),
         "morap_cuda_num_models": (i32, [p]),
         "morap_cuda_optimize": (i32, [p, i32, p, p, i32, f64, i32, p, p, p, p]),
@@ -121,7 +124,9 @@ class CudaBackend:
         self._check(self.lib.morap_cuda_set_stream(self.h, cuda_stream or None), "set_stream")
 
     # ---- models -------------------------------------------------------------------------
-    def upload(self, models) -> np.ndarray:
+    def upload(self, models, image: bool = False) -> np.ndarray:
+        """morap_cuda_upload; with image=True through morap_cuda_build_image + upload_image
+        (the packed image is uploaded twice, after a release, to exercise the re-upload)."""
         views = (CsrView * len(models))()
         keep = []
         for k, m in enumerate(models):
@@ -141,7 +146,17 @@ class CudaBackend:
             v.row_offset, v.trn_offset, v.succ, v.prob, v.done = [_ptr(a) for a in arrs]
             v.rewards = C.cast(optr, C.c_void_p)
         ids = np.zeros(len(models), np.int32)
-        self._check(self.lib.morap_cuda_upload(self.h, len(models), views, _ptr(ids)), "upload")
+        if image:
+            img = C.c_void_p()
+            self._check(self.lib.morap_cuda_build_image(self.h, len(models), views, C.byref(img)), "build_image")
+            try:
+                self._check(self.lib.morap_cuda_upload_image(self.h, img, _ptr(ids)), "upload_image")
+                self._check(self.lib.morap_cuda_release_models(self.h), "release")
+                self._check(self.lib.morap_cuda_upload_image(self.h, img, _ptr(ids)), "upload_image")
+            finally:
+                self.lib.morap_cuda_free_image(img)
+        else:
+            self._check(self.lib.morap_cuda_upload(self.h, len(models), views, _ptr(ids)), "upload")
         for m in models:
             self._models.append((int(np.asarray(m.rowOffset).shape[0] - 1), int(np.asarray(m.trnOffset).shape[0] - 1),
                                  len(model_objectives(m))))
