@@ -4,6 +4,8 @@
 #include <map>
 #include <set>
 #include <sstream>
+#include <chrono>
+#include <cstdio>
 #include <thread>
 
 #include "morap.h"
@@ -333,8 +335,13 @@ int morap_instance_warehouse_streamed(const char* config_json, int threads, mora
     if (chunk < 1) morap::fail(morap::Errc::InvalidConfig, "chunk must be positive");
     morap::WarehouseConfig cfg = morap::warehouseConfigFromJson(morap::Json::parse(config_json));
     morap::GpuBackend& gpu = *s->gpu;
+    const bool trace = std::getenv("MORAP_TRACE") != nullptr;
     const morap::ProductSink sink = [&](const std::vector<morap::ProductMdp*>& fresh) {
+      const auto t0 = std::chrono::steady_clock::now();
       gpu.uploadProducts(std::vector<const morap::ProductMdp*>(fresh.begin(), fresh.end()), gpu.lean());
+      if (trace)
+        std::fprintf(stderr, "[morap] streamed chunk: upload %.1f ms\n",
+                     1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
       std::vector<std::thread> pool;
       const size_t T = std::max(1u, std::thread::hardware_concurrency());
       for (size_t t = 0; t < T; ++t)

@@ -7,6 +7,9 @@
 // index is a flat int32 table instead of a hash map, and buildInstance builds the n^2
 // products on all host threads before deduplicating them in (i, j) order.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -385,8 +388,14 @@ MorapInstance buildInstance(std::vector<Mdp> agents, std::vector<RewardStructure
   std::map<uint64_t, std::vector<std::shared_ptr<ProductMdp>>> byHash;
   inst.products.assign(static_cast<size_t>(n), std::vector<std::shared_ptr<const ProductMdp>>(static_cast<size_t>(n)));
   const int T = std::min<int>(hostThreads(threads), static_cast<int>(std::min(total, chunk)));
+  const bool trace = std::getenv("MORAP_TRACE") != nullptr;
+  double buildS = 0, dedupS = 0, sinkS = 0;
+  auto since = [](std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count();
+  };
   for (size_t base = 0; base < total; base += chunk) {
     const size_t m = std::min(chunk, total - base);
+    const auto tb = std::chrono::steady_clock::now();
     std::vector<std::unique_ptr<ProductMdp>> built(m);
     std::vector<std::optional<Error>> errs(m);
     std::atomic<size_t> next{0};
@@ -405,6 +414,7 @@ MorapInstance buildInstance(std::vector<Mdp> agents, std::vector<RewardStructure
     for (int t = 1; t < T; ++t) pool.emplace_back(worker);
     worker();
     for (auto& th : pool) th.join();
+    buildS += since(tb);
 
     // reject / deduplicate in (i, j) order, as instance.hpp:445-466 does sequentially
     std::vector<ProductMdp*> fresh;
@@ -430,8 +440,14 @@ MorapInstance buildInstance(std::vector<Mdp> agents, std::vector<RewardStructure
       }
       inst.products[i][j] = share;
     }
+    dedupS += since(tb);
+    const auto ts = std::chrono::steady_clock::now();
     if (sink && !fresh.empty()) (*sink)(fresh);
+    sinkS += since(ts);
   }
+  if (trace)
+    std::fprintf(stderr, "[morap] buildInstance: products %.2f s, dedup %.2f s, sink (upload) %.2f s\n", buildS,
+                 dedupS - buildS, sinkS);
   return inst;
 }
 

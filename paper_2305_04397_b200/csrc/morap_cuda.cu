@@ -1472,25 +1472,39 @@ int morap_cuda_upload(morap_ctx* ctx, int nmodels, const morap_csr_view* models,
   cudaSetDevice(ctx->device);
   int rc;
   UploadPrep P;
+  const auto tu0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (ctx->trace)
+      std::fprintf(stderr, "[morap] upload %d models: %s at %.3f ms\n", nmodels, what,
+                   1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tu0).count());
+  };
   if ((rc = prepare_models(ctx, nmodels, models, P))) return rc;
   void* dev = nullptr;
   if ((rc = acquire_block(ctx, P.bytes, &dev))) return rc;
+  lap("device block");
   if (P.bytes > ctx->stageBytes) {  // pinned staging, grow-only (reused by later uploads)
+    // with headroom: pinning ~1 GB costs ~1 s, and the chunks of a streamed build differ
+    // by a few percent (each new maximum used to re-pin the whole buffer)
+    const size_t cap = P.bytes + P.bytes / 4;
     cudaFreeHost(ctx->stage);
     ctx->stage = nullptr;
     ctx->stageBytes = 0;
-    CK(cudaMallocHost(&ctx->stage, P.bytes));
-    ctx->stageBytes = P.bytes;
+    CK(cudaMallocHost(&ctx->stage, cap));
+    ctx->stageBytes = cap;
   }
   std::vector<DevModel> built(nmodels);
   std::atomic<bool> copyFailed{false};
   std::atomic<long long> uploadBytes{0};
   pack_models(ctx, nmodels, models, P, static_cast<char*>(ctx->stage), static_cast<char*>(dev), true, built, copyFailed,
               uploadBytes);
+  lap("packed, copies queued");
   ctx->stats[9] += static_cast<double>(uploadBytes.load());
   cudaError_t e = copyFailed ? cudaErrorUnknown : cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return ctx->cudaFail(e, "upload copy", __LINE__);
-  return register_models(ctx, built, host_models(built, P), ids_out);
+  lap("copied");
+  rc = register_models(ctx, built, host_models(built, P), ids_out);
+  lap("registered");
+  return rc;
 }
 
 int morap_cuda_build_image(morap_ctx* ctx, int nmodels, const morap_csr_view* models, morap_image** out) {
