@@ -88,6 +88,13 @@ int morap_solver_set_fingerprints(morap_solver* s, int on);
 int morap_instance_warehouse_streamed(const char* config_json, int threads, morap_solver* s, int chunk,
                                       morap_instance** out);
 
+/* generateInstance with every product built on the GPU of `s` (morap_cuda_build_products:
+ * the BFS of buildProduct, checkRewardFinite and the compact upload layout run on the
+ * device; the host never holds a product array). Same products, same errors and the same
+ * seeded retries as morap_instance_warehouse; the instance then answers queries on `s` only
+ * (as a streamed one). Deduplication compares (identity hash, S, R, nnz). */
+int morap_instance_warehouse_device(const char* config_json, morap_solver* s, morap_instance** out);
+
 /* supportingPoint (solver.hpp:103-184): w has K*n entries (unit 1-norm). Writes r (K*n)
  * and the assignment agent_of[n]. stats_out (nullable, 8 doubles): optimize jobs,
  * optimize nnz backups, evaluate jobs, evaluate state backups, optimize s, evaluate s,

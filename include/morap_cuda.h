@@ -124,6 +124,52 @@ int morap_cuda_set_skip(morap_ctx* ctx, int on);
  * index mod 128) x sweep CTAs x 4 globaltimer ns {start, first stage consumed, all warps
  * done, finalize done (last CTA only)}. */
 int morap_cuda_debug_cta_trace(morap_ctx* ctx, int enable, uint64_t* out, int64_t n);
+
+/* Device product builder: buildProduct (model.hpp:230-321) + checkRewardFinite
+ * (model.hpp:163-206) + the upload preparation, on the GPU. Builds the products of `npairs`
+ * (agent, task) pairs straight into device memory as lean compact models (two objectives:
+ * cost, success) -- the host never holds their arrays. Agents come as CSR MDPs whose
+ * probabilities / costs are indices into a shared alphabet (exact fp64 bit patterns), tasks
+ * as DFAs with pre-sinks already inserted (insertPreSinks) and their letters per label set. */
+typedef struct {
+  int32_t num_states, num_rows, nnz, initial;
+  const int32_t* row_offset; /* num_states + 1 */
+  const int32_t* trn_offset; /* num_rows + 1 */
+  const int32_t* succ;       /* nnz */
+  const int32_t* prob_cand;  /* nnz: index into morap_build_alphabet.probs */
+  const int32_t* cost_cand;  /* num_rows: index into morap_build_alphabet.costs */
+  const int32_t* name_id;    /* num_rows: action-name id (product identity only) */
+  const int32_t* label_set;  /* num_states: label-set id */
+} morap_build_agent;
+typedef struct {
+  int32_t num_locations, num_letters, initial;
+  const int32_t* delta;         /* num_locations x num_letters */
+  const uint8_t* flags;         /* per location: 1 accepting, 2 trap, 4 pre-sink */
+  const int32_t* letter_of_set; /* per label-set id: the letter (bitmask over the task's atoms) */
+} morap_build_task;
+typedef struct {
+  int32_t num_probs, num_costs, internal_name; /* <= 1024 probabilities, < 1024 costs */
+  int32_t num_label_sets;
+  const double* probs;                         /* distinct bit patterns, must contain 1.0 */
+  const double* costs;                         /* distinct bit patterns */
+} morap_build_alphabet;
+typedef struct {
+  int32_t status; /* MORAP_OK, or MORAP_INVALID_CONFIG: not compact (> 256 probabilities ...) */
+  int32_t num_states, num_rows, nnz;
+  int32_t reward_finite;
+  int32_t ntiles;
+  uint64_t hash;  /* identity of the product's arrays (equal products, equal hash) */
+  uint64_t bytes; /* device bytes of the built model */
+} morap_build_info;
+/* write == 0 (measure): fills info[] only. write == 1: builds and registers the models
+ * (model_ids_out[k]); info[] must hold the measure results of the same pairs (sizes). */
+int morap_cuda_build_products(morap_ctx* ctx, int nagents, const morap_build_agent* agents, int ntasks,
+                              const morap_build_task* tasks, const morap_build_alphabet* alphabet, int npairs,
+                              const int32_t* pairs, int write, morap_build_info* info, int32_t* model_ids_out);
+/* Test support: 17 FNV digests of a device model's arrays (rowOffset, trnOffset, succ, done,
+ * probIdx, rclass, tileStart, tiles, probDict, classTable, stW, rowW, trW, tilePos, outIdx,
+ * outGrp, outSucc), so a device-built model can be compared with the host-prepared upload. */
+int morap_cuda_debug_model_digest(morap_ctx* ctx, int model_id, uint64_t* out17);
 int morap_cuda_num_models(morap_ctx* ctx);
 /* out[6] = {S, R, nnz, number of objectives, compact (0/1), lean (0/1)} of a device model. */
 int morap_cuda_model_info(morap_ctx* ctx, int model_id, int32_t* out);

@@ -61,6 +61,7 @@ def load_host_library() -> C.CDLL:
         "morap_instance_warehouse_shard": (i32, [C.c_char_p, i32, i32, i32, i32, C.POINTER(p)]),
         "morap_instance_product_owner": (i32, [p, i32, i32]),
         "morap_instance_warehouse_streamed": (i32, [C.c_char_p, i32, p, i32, C.POINTER(p)]),
+        "morap_instance_warehouse_device": (i32, [C.c_char_p, p, C.POINTER(p)]),
         "morap_supporting_point": (i32, [p, p, p, i32, p, p, p]),
         "morap_pareto": (i32, [p, p, p, i32, p, f64, i32, i32, C.c_char_p, i32, p]),
         "morap_pareto_core": (i32, [p, i32, i32, p, f64, i32, i32, QUERY_FN, p, C.c_char_p, i32]),
@@ -142,6 +143,19 @@ class Instance:
         h = C.c_void_p()
         _check(lib.morap_instance_warehouse_streamed(json.dumps(config).encode(), threads, solver.h, chunk,
                                                      C.byref(h)), "generateInstance (streamed)")
+        inst = cls(h)
+        inst.streamed = True
+        return inst
+
+    @classmethod
+    def warehouse_device(cls, config: dict, solver: "Solver") -> "Instance":
+        """generateInstance with the products built on `solver`'s GPU (morap.h,
+        morap_cuda_build_products): the host never holds a product array, so the instance
+        only answers queries on that solver, like a streamed one."""
+        lib = load_host_library()
+        h = C.c_void_p()
+        _check(lib.morap_instance_warehouse_device(json.dumps(config).encode(), solver.h, C.byref(h)),
+               "generateInstance (device)")
         inst = cls(h)
         inst.streamed = True
         return inst

@@ -45,7 +45,7 @@ CUDA_FLAGS = [
 ]
 
 HOST_SOURCES = ["linalg.cpp", "logic.cpp", "model.cpp", "warehouse.cpp", "assignment.cpp", "geometry.cpp",
-                "gpu.cpp", "solver.cpp", "shard.cpp", "centralised.cpp", "capi.cpp"]
+                "gpu.cpp", "device_build.cpp", "solver.cpp", "shard.cpp", "centralised.cpp", "capi.cpp"]
 
 
 def _newer(target: str, sources: list[str]) -> bool:

@@ -355,6 +355,20 @@ int morap_instance_warehouse_streamed(const char* config_json, int threads, mora
   });
 }
 
+int morap_instance_warehouse_device(const char* config_json, morap_solver* s, morap_instance** out) {
+  return guard([&] {
+    if (!out || !config_json || !s) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    morap::WarehouseConfig cfg = morap::warehouseConfigFromJson(morap::Json::parse(config_json));
+    morap::GpuBackend& gpu = *s->gpu;
+    const morap::InstanceBuilder build = [&](std::vector<morap::Mdp> agents, std::vector<morap::RewardStructure> costs,
+                                             std::vector<morap::Dfa> tasks) {
+      return morap::buildInstanceOnDevice(gpu, std::move(agents), std::move(costs), std::move(tasks));
+    };
+    const std::function<void()> retry = [&] { gpu.release(); };
+    *out = new morap_instance{morap::generateInstanceWith(cfg, build, &retry), {}, {}};
+  });
+}
+
 int morap_multi_create(const int* devices, int ndevices, morap_multi** out) {
   return guard([&] {
     if (!out || !devices || ndevices < 1) morap::fail(morap::Errc::InvalidConfig, "need at least one device");

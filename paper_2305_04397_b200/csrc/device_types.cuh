@@ -89,7 +89,8 @@ struct DevModel {
   const int32_t* outIdx;      // ntiles + 1
   const int32_t* outGrp;
   int32_t S, R, nnz, initial, ntiles, K, rewardFinite, compact;
-  int32_t nclass, pad2;
+  int32_t nclass, nOutSucc;  // reward classes; out-of-window transitions (outSucc entries)
+  int32_t nDict, nStW, nRowW, nTrW;  // probability dictionary entries; stream words (padded)
   unsigned long long bytesPerSweep;  // algorithmic bytes of one greedy sweep
   unsigned long long bytesPerEval;   // per evaluate sweep, one RHS
 };

@@ -209,10 +209,8 @@ uint64_t productHash(const ProductMdp& p) {
   return f.digest();
 }
 
-ProductMdp buildProduct(const Mdp& agent, const RewardStructure& agentCost, const Dfa& task, int agentId, int taskId) {
-  if (static_cast<int>(agentCost.size()) != agent.numActions())
-    fail(Errc::DimensionMismatch, "cost structure does not match the model's action rows");
-  // every acceptance must be entered through a pre-sink step (model.hpp:234-243)
+// every acceptance must be entered through a pre-sink step (model.hpp:234-243)
+void checkPreSinks(const Dfa& task) {
   if (task.accepting[task.initial]) fail(Errc::InvalidDfa, "task automaton lacks pre-sinks: initial location is accepting");
   const int L = task.numLetters(), Q = task.numLocations;
   for (int q = 0; q < Q; ++q) {
@@ -221,6 +219,13 @@ ProductMdp buildProduct(const Mdp& agent, const RewardStructure& agentCost, cons
       if (task.accepting[task.step(q, w)])
         fail(Errc::InvalidDfa, "task automaton lacks pre-sinks: acceptance without a pre-sink step");
   }
+}
+
+ProductMdp buildProduct(const Mdp& agent, const RewardStructure& agentCost, const Dfa& task, int agentId, int taskId) {
+  if (static_cast<int>(agentCost.size()) != agent.numActions())
+    fail(Errc::DimensionMismatch, "cost structure does not match the model's action rows");
+  checkPreSinks(task);
+  const int L = task.numLetters(), Q = task.numLocations;
   ProductMdp p;
   p.agentId = agentId;
   p.taskId = taskId;

@@ -187,6 +187,7 @@ std::vector<int> maximalAvoidSet(const Mdp& m, const std::vector<char>& done);
 bool checkRewardFinite(const Mdp& m, const std::vector<char>& done);
 bool checkRewardFinite(const ProductMdp& p);
 uint64_t productHash(const ProductMdp& p);
+void checkPreSinks(const Dfa& task);  // buildProduct's InvalidDfa checks (model.hpp:234-243)
 ProductMdp buildProduct(const Mdp& agent, const RewardStructure& agentCost, const Dfa& task, int agentId = -1,
                         int taskId = -1);
 
@@ -227,6 +228,11 @@ Formula generateTask(const WarehouseConfig& cfg, int rackIndex);
 Dfa taskAutomaton(const WarehouseConfig& cfg, int rackIndex);
 MorapInstance generateInstance(const WarehouseConfig& cfg, int threads = 0, size_t chunk = 0,
                                const ProductSink* sink = nullptr, const std::function<void()>* onRetry = nullptr);
+// the seeded retry loop of generateInstance (warehouse.hpp) around any instance builder
+using InstanceBuilder =
+    std::function<MorapInstance(std::vector<Mdp>, std::vector<RewardStructure>, std::vector<Dfa>)>;
+MorapInstance generateInstanceWith(const WarehouseConfig& cfg, const InstanceBuilder& build,
+                                   const std::function<void()>* onRetry = nullptr);
 WarehouseConfig warehouseConfigFromJson(const Json& j);
 
 // ---- per-model solve on the GPU (numerics.hpp, engine.hpp) --------------------------------
@@ -293,6 +299,7 @@ class GpuBackend {
   morap_ctx* ctx() const { return ctx_; }
   int device() const { return device_; }
   void release();
+  void adopt(uint64_t uid, int id) { ids_[uid] = id; }  // a model built on the device for product uid
 
  private:
   morap_ctx* ctx_ = nullptr;
@@ -304,6 +311,12 @@ class GpuBackend {
   std::vector<uint64_t> imageKey_;  // lean flag + product uids it holds
   bool isLean(int id);
 };
+
+// buildInstance (instance.hpp:42-91) with every product built on the GPU (morap_cuda_build_products):
+// the products stay device-resident as lean compact models, the instance holds slim products
+// (dimensions, reward finiteness, identity hash). Two objectives only (cost, success).
+MorapInstance buildInstanceOnDevice(GpuBackend& gpu, std::vector<Mdp> agents, std::vector<RewardStructure> costs,
+                                    std::vector<Dfa> tasks);
 
 OptimizeResult optimalScheduler(GpuBackend& gpu, const ProductMdp& p, const RewardStructure& rho, double eps = 1e-6,
                                 int sweepCap = 100000);

@@ -199,6 +199,8 @@ struct morap_ctx {
   unsigned* dFinCount = nullptr;  // CTAs done in the current compact sweep (fused finalize)
   void* persistArena = nullptr;
   size_t persistArenaBytes = 0;
+  void* buildWs = nullptr;  // device product builder: per-CTA workspaces
+  size_t buildWsBytes = 0;
   void* polStage = nullptr;  // pinned staging for batched policy reads
   size_t polStageBytes = 0;
   Ctl* dCtl = nullptr;
@@ -286,10 +288,12 @@ int ensure_ctl(morap_ctx* ctx, size_t njobs) {
 }
 
 #include "upload_prep.cuh"
+#include "kernels_build.cuh"
 
 int upload_models_table(morap_ctx* ctx) {
   if (ctx->dm.size() > ctx->dModelsCap) {
     cudaFree(ctx->dModels);
+  cudaFree(ctx->buildWs);
     size_t cap = std::max<size_t>(ctx->dm.size() * 2, 16);
     CK(cudaMalloc(&ctx->dModels, cap * sizeof(DevModel)));
     ctx->dModelsCap = cap;
@@ -1158,6 +1162,11 @@ void pack_models(morap_ctx* ctx, int nmodels, const morap_csr_view* models, cons
       dmod.rclass = reinterpret_cast<const uint16_t*>(put(1, c.cls.data(), 2ull * c.cls.size()));
       dmod.classTable = reinterpret_cast<const double*>(put(0, c.table.data(), 8ull * c.table.size()));
       dmod.nclass = static_cast<int32_t>(c.table.size() / std::max(1, v.num_objectives));
+      dmod.nOutSucc = static_cast<int32_t>(c.outSucc.size());
+      dmod.nDict = static_cast<int32_t>(c.dict.size());
+      dmod.nStW = static_cast<int32_t>(c.nStW);
+      dmod.nRowW = static_cast<int32_t>(c.nRowW);
+      dmod.nTrW = static_cast<int32_t>(c.nTrW);
       uint32_t* hs = reinterpret_cast<uint32_t*>(hA);
       dmod.stW = reinterpret_cast<const uint32_t*>(put(0, nullptr, 4ull * c.nStW));
       uint32_t* hr = reinterpret_cast<uint32_t*>(hA);
@@ -1573,6 +1582,270 @@ int morap_cuda_release_models(morap_ctx* ctx) {
   ctx->evalJobs = 0;
   ctx->evalSplitG = 1;
   ctx->evalSplitChunk = 0;
+  return MORAP_OK;
+}
+
+int morap_cuda_build_products(morap_ctx* ctx, int nagents, const morap_build_agent* agents, int ntasks,
+                              const morap_build_task* tasks, const morap_build_alphabet* alpha, int npairs,
+                              const int32_t* pairs, int write, morap_build_info* info, int32_t* model_ids_out) {
+  if (!ctx) return MORAP_INVALID_CONFIG;
+  if (npairs < 0 || (npairs && (!agents || !tasks || !alpha || !pairs || !info)) || (write && npairs && !model_ids_out))
+    return ctx->fail(MORAP_INVALID_CONFIG, "build_products: null argument");
+  if (npairs == 0) return MORAP_OK;
+  cudaSetDevice(ctx->device);
+  const auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (ctx->trace)
+      std::fprintf(stderr, "[morap] build_products (%d pairs, %s): %s at %.1f ms\n", npairs, write ? "write" : "measure",
+                   what, 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  };
+  if (alpha->num_probs < 1 || alpha->num_probs > kBuildMaxCand || alpha->num_costs < 0 ||
+      alpha->num_costs >= kBuildMaxCand || alpha->num_label_sets < 1 || !alpha->probs ||
+      (alpha->num_costs && !alpha->costs))
+    return ctx->fail(MORAP_INVALID_CONFIG, "build_products: alphabet sizes out of range");
+  int probOne = -1;
+  {
+    const double d1 = 1.0;
+    uint64_t one;
+    std::memcpy(&one, &d1, 8);
+    for (int c = 0; c < alpha->num_probs; ++c) {
+      uint64_t b;
+      std::memcpy(&b, &alpha->probs[c], 8);
+      if (b == one) probOne = c;
+    }
+  }
+  if (probOne < 0) return ctx->fail(MORAP_INVALID_CONFIG, "build_products: the probability alphabet lacks 1.0");
+  // per agent: the widest state (rows, transitions); validation of the index arrays
+  std::vector<int64_t> maxRows(nagents, 1), maxEdges(nagents, 1);
+  for (int a = 0; a < nagents; ++a) {
+    const morap_build_agent& g = agents[a];
+    const std::string who = "build_products: agent " + std::to_string(a);
+    if (g.num_states < 1 || g.num_rows < 0 || g.nnz < 0 || g.initial < 0 || g.initial >= g.num_states ||
+        !g.row_offset || !g.trn_offset || !g.label_set || (g.num_rows && (!g.cost_cand || !g.name_id)) ||
+        (g.nnz && (!g.succ || !g.prob_cand)) || g.row_offset[0] != 0 || g.row_offset[g.num_states] != g.num_rows ||
+        g.trn_offset[0] != 0 || g.trn_offset[g.num_rows] != g.nnz)
+      return ctx->fail(MORAP_INVALID_MODEL, who + " is not a valid CSR");
+    for (int s = 0; s < g.num_states; ++s) {
+      const int r0 = g.row_offset[s], r1 = g.row_offset[s + 1];
+      if (r1 < r0 || g.label_set[s] < 0 || g.label_set[s] >= alpha->num_label_sets)
+        return ctx->fail(MORAP_INVALID_MODEL, who + ": row offsets / label sets");
+      maxRows[a] = std::max<int64_t>(maxRows[a], r1 - r0);
+      maxEdges[a] = std::max<int64_t>(maxEdges[a], g.trn_offset[r1] - g.trn_offset[r0]);
+    }
+    for (int r = 0; r < g.num_rows; ++r)
+      if (g.trn_offset[r + 1] < g.trn_offset[r] || g.cost_cand[r] < 0 || g.cost_cand[r] >= alpha->num_costs)
+        return ctx->fail(MORAP_INVALID_MODEL, who + ": rows");
+    for (int k = 0; k < g.nnz; ++k)
+      if (g.succ[k] < 0 || g.succ[k] >= g.num_states || g.prob_cand[k] < 0 || g.prob_cand[k] >= alpha->num_probs)
+        return ctx->fail(MORAP_INVALID_MODEL, who + ": transitions");
+  }
+  for (int t = 0; t < ntasks; ++t) {
+    const morap_build_task& d = tasks[t];
+    const std::string who = "build_products: task " + std::to_string(t);
+    if (d.num_locations < 1 || d.num_letters < 1 || d.initial < 0 || d.initial >= d.num_locations || !d.delta ||
+        !d.flags || !d.letter_of_set)
+      return ctx->fail(MORAP_INVALID_DFA, who + " is not a valid DFA");
+    for (int64_t i = 0; i < static_cast<int64_t>(d.num_locations) * d.num_letters; ++i)
+      if (d.delta[i] < 0 || d.delta[i] >= d.num_locations) return ctx->fail(MORAP_INVALID_DFA, who + ": transition out of range");
+    for (int l = 0; l < alpha->num_label_sets; ++l)
+      if (d.letter_of_set[l] < 0 || d.letter_of_set[l] >= d.num_letters)
+        return ctx->fail(MORAP_INVALID_DFA, who + ": letter out of range");
+  }
+  int64_t SQmax = 1, Rmax = 1, Nmax = 1, SAmax = 1;
+  for (int k = 0; k < npairs; ++k) {
+    const int a = pairs[2 * k], t = pairs[2 * k + 1];
+    if (a < 0 || a >= nagents || t < 0 || t >= ntasks)
+      return ctx->fail(MORAP_INVALID_CONFIG, "build_products: pair " + std::to_string(k) + " out of range");
+    const int64_t SQ = static_cast<int64_t>(agents[a].num_states) * tasks[t].num_locations;
+    SQmax = std::max(SQmax, SQ);
+    Rmax = std::max(Rmax, SQ * maxRows[a]);
+    Nmax = std::max(Nmax, SQ * maxEdges[a]);
+    SAmax = std::max<int64_t>(SAmax, agents[a].num_states);
+  }
+  if (Nmax >= (int64_t{1} << 31) - 2 || Rmax >= (int64_t{1} << 31) - 2)
+    return ctx->fail(MORAP_SIZE_GUARD, "build_products: a product could exceed 2^31 transitions");
+
+  // agents, tasks, alphabet, pairs and the outputs in one device block
+  std::vector<char> blob;
+  auto add = [&](const void* src, size_t bytes) {
+    const size_t at = blob.size();
+    blob.resize(at + align_up(std::max<size_t>(bytes, 1), 256));
+    if (bytes && src) std::memcpy(blob.data() + at, src, bytes);
+    return at;
+  };
+  struct AgentOff {
+    size_t row, trn, succ, pc, cc, name, lset;
+  };
+  struct TaskOff {
+    size_t delta, flags, letter;
+  };
+  std::vector<AgentOff> ao(nagents);
+  std::vector<TaskOff> tof(ntasks);
+  const size_t offAgents = add(nullptr, sizeof(BAgent) * nagents);
+  const size_t offTasks = add(nullptr, sizeof(BTask) * ntasks);
+  for (int a = 0; a < nagents; ++a) {
+    const morap_build_agent& g = agents[a];
+    ao[a].row = add(g.row_offset, 4ull * (g.num_states + 1));
+    ao[a].trn = add(g.trn_offset, 4ull * (g.num_rows + 1));
+    ao[a].succ = add(g.succ, 4ull * g.nnz);
+    ao[a].pc = add(g.prob_cand, 4ull * g.nnz);
+    ao[a].cc = add(g.cost_cand, 4ull * g.num_rows);
+    ao[a].name = add(g.name_id, 4ull * g.num_rows);
+    ao[a].lset = add(g.label_set, 4ull * g.num_states);
+  }
+  for (int t = 0; t < ntasks; ++t) {
+    const morap_build_task& d = tasks[t];
+    tof[t].delta = add(d.delta, 4ull * d.num_locations * d.num_letters);
+    tof[t].flags = add(d.flags, d.num_locations);
+    tof[t].letter = add(d.letter_of_set, 4ull * alpha->num_label_sets);
+  }
+  const size_t offProbs = add(alpha->probs, 8ull * alpha->num_probs);
+  const size_t offCosts = add(alpha->costs, 8ull * alpha->num_costs);
+  const size_t offPairs = add(pairs, 8ull * npairs);
+  const size_t offOffsets = add(nullptr, 8ull * npairs);
+  const size_t offNext = add(nullptr, 4);
+  const size_t upBytes = blob.size();  // the outputs are not uploaded
+  const size_t offOut = add(nullptr, sizeof(BuildOut) * npairs);
+  char* dBlob = nullptr;
+  CK(cudaMalloc(&dBlob, blob.size()));
+  struct Free {
+    char* p;
+    ~Free() { cudaFree(p); }
+  } freeBlob{dBlob};
+  auto dptr = [&](size_t off) { return reinterpret_cast<const int32_t*>(dBlob + off); };
+  for (int a = 0; a < nagents; ++a) {
+    const morap_build_agent& g = agents[a];
+    const BAgent b{g.num_states, g.num_rows, g.nnz, g.initial, dptr(ao[a].row), dptr(ao[a].trn), dptr(ao[a].succ),
+                   dptr(ao[a].pc), dptr(ao[a].cc), dptr(ao[a].name), dptr(ao[a].lset)};
+    std::memcpy(blob.data() + offAgents + sizeof(BAgent) * a, &b, sizeof b);
+  }
+  for (int t = 0; t < ntasks; ++t) {
+    const morap_build_task& d = tasks[t];
+    const BTask b{d.num_locations, d.num_letters, d.initial, 0, dptr(tof[t].delta),
+                  reinterpret_cast<const uint8_t*>(dBlob + tof[t].flags), dptr(tof[t].letter)};
+    std::memcpy(blob.data() + offTasks + sizeof(BTask) * t, &b, sizeof b);
+  }
+  // write: each product's block at the prefix of the measured sizes
+  size_t arenaBytes = 0;
+  if (write) {
+    std::vector<unsigned long long> offs(npairs);
+    for (int k = 0; k < npairs; ++k) {
+      if (info[k].status != MORAP_OK || info[k].bytes == 0)
+        return ctx->fail(MORAP_INVALID_CONFIG, "build_products: write needs the measure results of every pair");
+      offs[k] = arenaBytes;
+      arenaBytes += align_up(info[k].bytes, 256);
+    }
+    std::memcpy(blob.data() + offOffsets, offs.data(), 8ull * npairs);
+  }
+  CK(cudaMemcpyAsync(dBlob, blob.data(), upBytes, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // the pageable blob is freed on return
+  lap("inputs uploaded");
+
+  // per-CTA workspaces: one CTA per SM, fewer when they would not fit in a quarter of free memory
+  const size_t wsBytes = align_up(build_ws_layout(nullptr, static_cast<int>(SQmax), static_cast<int>(SQmax),
+                                                  static_cast<int>(Rmax), static_cast<int>(Nmax),
+                                                  static_cast<int>(SAmax), nullptr),
+                                  256);
+  int grid = std::min(npairs, ctx->numSMs);
+  if (ctx->buildWsBytes < wsBytes * grid) {
+    cudaFree(ctx->buildWs);
+    ctx->buildWs = nullptr;
+    ctx->buildWsBytes = 0;
+    size_t freeB = 0, totalB = 0;
+    CK(cudaMemGetInfo(&freeB, &totalB));
+    grid = static_cast<int>(std::min<size_t>(grid, std::max<size_t>(1, freeB / 4 / wsBytes)));
+    CK(cudaMalloc(&ctx->buildWs, wsBytes * grid));
+    ctx->buildWsBytes = wsBytes * grid;
+  }
+  grid = static_cast<int>(std::min<size_t>(grid, ctx->buildWsBytes / wsBytes));
+  void* arena = nullptr;
+  if (write) {
+    const int rc = acquire_block(ctx, arenaBytes, &arena);
+    if (rc) return rc;
+  }
+  CK(cudaMemsetAsync(dBlob + offNext, 0, 4, ctx->stream));
+  BuildArgs A{};
+  A.agents = reinterpret_cast<const BAgent*>(dBlob + offAgents);
+  A.tasks = reinterpret_cast<const BTask*>(dBlob + offTasks);
+  A.pairs = dptr(offPairs);
+  A.npairs = npairs;
+  A.probs = reinterpret_cast<const double*>(dBlob + offProbs);
+  A.costs = reinterpret_cast<const double*>(dBlob + offCosts);
+  A.nProbs = alpha->num_probs;
+  A.nCosts = alpha->num_costs;
+  A.probOne = probOne;
+  A.internalName = alpha->internal_name;
+  A.mode = write ? 1 : 0;
+  A.ws = static_cast<char*>(ctx->buildWs);
+  A.wsBytes = wsBytes;
+  A.SQmax = static_cast<int32_t>(SQmax);
+  A.Smax = static_cast<int32_t>(SQmax);
+  A.Rmax = static_cast<int32_t>(Rmax);
+  A.Nmax = static_cast<int32_t>(Nmax);
+  A.SAmax = static_cast<int32_t>(SAmax);
+  A.arena = static_cast<char*>(arena);
+  A.offsets = reinterpret_cast<const unsigned long long*>(dBlob + offOffsets);
+  A.out = reinterpret_cast<BuildOut*>(dBlob + offOut);
+  A.next = reinterpret_cast<int*>(dBlob + offNext);
+  k_build_products<<<grid, kBT, 0, ctx->stream>>>(A);
+  CK(cudaGetLastError());
+  std::vector<BuildOut> out(npairs);
+  CK(d2h(ctx, out.data(), dBlob + offOut, sizeof(BuildOut) * npairs));
+  CK(cudaStreamSynchronize(ctx->stream));
+  lap("kernel done");
+  for (int k = 0; k < npairs; ++k) {
+    const BuildOut& o = out[k];
+    if (write && (o.bytes != info[k].bytes || o.status != MORAP_OK))
+      return ctx->fail(MORAP_SOLVER_FAILURE,
+                       "build_products: product " + std::to_string(k) + " differs between the measure and write passes");
+    info[k] = morap_build_info{o.status, o.S, o.R, o.nnz, o.rewardFinite, o.ntiles, o.hash, o.bytes};
+  }
+  if (!write) return MORAP_OK;
+  std::vector<DevModel> built(npairs);
+  std::vector<HostModel> hmods(npairs);
+  for (int k = 0; k < npairs; ++k) {
+    const BuildOut& o = out[k];
+    built[k] = o.dm;
+    hmods[k] = HostModel{o.S, o.R, o.nnz, 0, o.ntiles, 2, o.rewardFinite, o.maxRowNnz, o.nOutGrp, o.needB};
+  }
+  return register_models(ctx, built, hmods, model_ids_out);
+}
+
+int morap_cuda_debug_model_digest(morap_ctx* ctx, int id, uint64_t* out) {
+  if (!ctx || !out) return MORAP_INVALID_CONFIG;
+  if (id < 0 || id >= static_cast<int>(ctx->hm.size())) return ctx->fail(MORAP_INVALID_CONFIG, "unknown model id");
+  cudaSetDevice(ctx->device);
+  CK(cudaDeviceSynchronize());
+  const DevModel& d = ctx->dm[static_cast<size_t>(id)];
+  if (!d.compact) return ctx->fail(MORAP_INVALID_CONFIG, "digest: not a compact model");
+  const size_t nt = static_cast<size_t>(d.ntiles);
+  int32_t nGrp = 0;
+  CK(cudaMemcpy(&nGrp, d.outIdx + nt, 4, cudaMemcpyDeviceToHost));
+  const std::pair<const void*, size_t> arrays[17] = {{d.rowOffset, 4ull * (d.S + 1)},
+                                                     {d.trnOffset, 4ull * (d.R + 1)},
+                                                     {d.succ, 4ull * d.nnz},
+                                                     {d.done, 1ull * d.S},
+                                                     {d.probIdx, 1ull * d.nnz},
+                                                     {d.rclass, 2ull * d.R},
+                                                     {d.tileStart, 4 * (nt + 1)},
+                                                     {d.tiles, sizeof(TileDesc) * (nt + 1)},
+                                                     {d.probDict, 8ull * d.nDict},
+                                                     {d.classTable, 8ull * d.K * d.nclass},
+                                                     {d.stW, 4ull * d.nStW},
+                                                     {d.rowW, 4ull * d.nRowW},
+                                                     {d.trW, 4ull * d.nTrW},
+                                                     {d.tilePos, sizeof(TilePos) * nt},
+                                                     {d.outIdx, 4 * (nt + 1)},
+                                                     {d.outGrp, 4ull * nGrp},
+                                                     {d.outSucc, 4ull * d.nOutSucc}};
+  std::vector<unsigned char> v;
+  for (int i = 0; i < 17; ++i) {
+    v.resize(arrays[i].second);
+    if (!v.empty()) CK(cudaMemcpy(v.data(), arrays[i].first, v.size(), cudaMemcpyDeviceToHost));
+    uint64_t h = 1469598103934665603ull ^ v.size();
+    for (unsigned char c : v) h = (h ^ c) * 1099511628211ull;
+    out[i] = h;
+  }
   return MORAP_OK;
 }
 

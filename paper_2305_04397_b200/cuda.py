@@ -66,6 +66,8 @@ def load_library(path: str = CUDA_SO) -> C.CDLL:
         "morap_cuda_set_skip": (i32, [p, i32]),
         "morap_cuda_debug_cta_trace": (i32, [p, i32, p, C.c_int64]),
         "morap_cuda_model_info": (i32, [p, i32, p]),
+        "morap_cuda_debug_model_digest": (i32, [p, i32, p]),
+        "morap_cuda_build_products": (i32, [p, i32, p, i32, p, p, i32, p, i32, p, p]),
         "morap_cuda_stats": (i32, [p, p, i32]),
         "morap_cuda_reset_stats": (i32, [p]),
         "morap_cuda_device_bytes": (i32, [p, p]),

@@ -1,0 +1,109 @@
+"""Device product builder (morap_cuda_build_products): products built on the GPU
+must be the very models the host path uploads -- every array of the device model (CSR,
+done flags, probability indices, reward classes, tiles, successor windows, the compact
+sweep streams, out-of-window lists) bit for bit against buildProduct (model.hpp:230-321)
++ the host upload preparation -- and the Pareto query on the device-built instance must
+return the host-built instance's report exactly. Errors and seeded retries follow
+generateInstance (warehouse.hpp)."""
+import ctypes as C
+
+import pytest
+
+from paper_2305_04397_b200 import cuda
+from paper_2305_04397_b200.api import Instance, Solver
+from paper_2305_04397_b200.errors import Errc, MorapError
+from tests.helpers import SUITE_5x5, SUITE_6x6, warehouse_config
+
+pytestmark = pytest.mark.gpu
+
+ARRAYS = ["rowOffset", "trnOffset", "succ", "done", "probIdx", "rclass", "tileStart", "tiles", "probDict",
+          "classTable", "stW", "rowW", "trW", "tilePos", "outIdx", "outGrp", "outSucc"]
+
+C4_RACKS = [[9 - (k % 10), 9 - (k // 10)] for k in range(100)]
+CONFIGS = {
+    "suite6x6_n3": {**SUITE_6x6, "n": 3},
+    "suite5x5_n2": {**SUITE_5x5, "n": 2},
+    "c2_10x10_n10": warehouse_config(10, 10, 10),
+    "slip0_8x8_n4": warehouse_config(8, 8, 4, slip=0.0),
+    "deadline7_6x6_n3": warehouse_config(6, 6, 3, deadline=7),
+    # the (i, j < 4) products of C4 (10 x 10, 100 racks): ~9.5e4 states, ~4.6e5 transitions each
+    "c4_sub_n4": {"W": 10, "H": 10, "n": 4, "slip": 0.05, "racks": C4_RACKS, "feed": [0, 0], "seed": 42},
+}
+
+
+def digests(solver):
+    lib = cuda.load_library()
+    ctx = solver.cuda_ctx
+    out = []
+    for m in range(lib.morap_cuda_num_models(ctx)):
+        d = (C.c_uint64 * 17)()
+        assert lib.morap_cuda_debug_model_digest(ctx, m, d) == 0, lib.morap_cuda_last_error(ctx)
+        out.append(list(d))
+    return out
+
+
+def host_and_device(cfg):
+    host = Instance.warehouse(cfg)
+    hs = Solver(0)
+    hs.set_lean(True)
+    hs.upload(host)
+    ds = Solver(0)
+    dev = Instance.warehouse_device(cfg, ds)
+    return host, hs, dev, ds
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_device_models_bitwise(name):
+    host, hs, dev, ds = host_and_device(CONFIGS[name])
+    assert (dev.n, dev.distinct, dev.total_states, dev.total_rows, dev.total_nnz) == \
+           (host.n, host.distinct, host.total_states, host.total_rows, host.total_nnz)
+    for i in range(host.n):
+        for j in range(host.n):
+            # S, R, nnz, initial, rewardFinite, first slot of the product (dedup)
+            assert dev.product_dims(i, j)[0].tolist() == host.product_dims(i, j)[0].tolist(), (i, j)
+    want, got = digests(hs), digests(ds)
+    assert len(got) == len(want) == host.distinct
+    for m, (a, b) in enumerate(zip(want, got)):
+        bad = [ARRAYS[k] for k in range(17) if a[k] != b[k]]
+        assert not bad, f"model {m}: {bad}"
+
+
+def _strip(rep):
+    rep = dict(rep)
+    rep.pop("stats", None)
+    return rep
+
+
+@pytest.mark.parametrize("name,thr", [
+    ("suite6x6_n3", [-25.0] * 3 + [0.9] * 3),
+    ("c2_10x10_n10", [-20.0] * 10 + [0.99] * 10),
+])
+def test_device_built_query_bitwise(name, thr):
+    cfg = CONFIGS[name]
+    want = _strip(Solver(0).pareto(Instance.warehouse(cfg), thr, eps=0.01, iteration_cap=40))
+    s = Solver(0)
+    got = _strip(s.pareto(Instance.warehouse_device(cfg, s), thr, eps=0.01, iteration_cap=40))
+    assert got == want
+
+
+def test_device_build_errors_follow_generate_instance():
+    # deadline 0: no product is reward-finite, 10 seeded attempts, GenerationFailure
+    cfg = warehouse_config(6, 6, 2, deadline=0)
+    with pytest.raises(MorapError) as host_err:
+        Instance.warehouse(cfg)
+    s = Solver(0)
+    with pytest.raises(MorapError) as dev_err:
+        Instance.warehouse_device(cfg, s)
+    assert dev_err.value.code == host_err.value.code == Errc.GenerationFailure
+    assert str(dev_err.value).split(": ", 1)[1] == str(host_err.value).split(": ", 1)[1]
+    # the failed attempts left nothing registered on the solver
+    assert cuda.load_library().morap_cuda_num_models(s.cuda_ctx) == 0
+
+
+def test_device_products_have_no_host_copy():
+    s = Solver(0)
+    inst = Instance.warehouse_device(CONFIGS["suite6x6_n3"], s)
+    with pytest.raises(MorapError):
+        inst.product(0, 0)
+    with pytest.raises(MorapError):
+        Solver(0).pareto(inst, [-25.0] * 3 + [0.9] * 3, eps=0.01, iteration_cap=2)
