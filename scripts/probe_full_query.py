@@ -1,7 +1,8 @@
 """Dev probe: one full point-oriented query (to convergence or a cap) on a large workload,
 printing per-iteration progress, the verdict and the phase split.
 
-    python scripts/probe_full_query.py c4 [cap]
+    python scripts/probe_full_query.py c4 [cap] [device]
+(device: products built by the device product builder instead of the host)
 """
 import json
 import sys
@@ -17,7 +18,9 @@ cfg, thr, eps, K = bench.workload(name)
 s = Solver(0)
 s.set_fingerprints(False)
 t = time.time()
-if name in bench.STREAMED:
+if len(sys.argv) > 3 and sys.argv[3] == "device":
+    inst = Instance.warehouse_device(cfg, s)
+elif name in bench.STREAMED:
     s.set_lean(True)
     inst = Instance.warehouse_streamed(cfg, s, chunk=bench.STREAMED[name])
 else:
@@ -43,7 +46,8 @@ if os.path.exists(gold):
     same = {k: np.array(v).tobytes() == z[k].tobytes() for k, v in
             (("w", [x["w"] for x in it]), ("r", [x["r"] for x in it]), ("tUp", r["tUp"]), ("tDown", r["tDown"]),
              ("lambdaStar", r["lambdaStar"]))}
-    print(json.dumps({"same_as_recorded_query": same}), flush=True)
+    print(json.dumps({"same_as_recorded_query": same, "builder": sys.argv[3] if len(sys.argv) > 3 else "host"}),
+          flush=True)
 np.savez_compressed(f"gpurun_out/report_{name}.npz", thresholds=np.array(r["thresholds"]),
                     w=np.array([x["w"] for x in it]), r=np.array([x["r"] for x in it]),
                     assignment=np.array([x["assignment"] for x in it], dtype=np.int32),
