@@ -95,6 +95,14 @@ int morap_instance_warehouse_streamed(const char* config_json, int threads, mora
  * (as a streamed one). Deduplication compares (identity hash, S, R, nnz). */
 int morap_instance_warehouse_device(const char* config_json, morap_solver* s, morap_instance** out);
 
+/* Sharded device builds. _device_shard: the per-rank build for morap_shard_pareto -- every
+ * rank measures every pair on its GPU, takes the owners morap_instance_warehouse_shard takes
+ * and builds only its own products there. morap_multi_warehouse_device: one process, the
+ * products built on the devices of `m` that own them (the owners morap_multi_upload takes);
+ * the instance is then queried with morap_multi_pareto. */
+int morap_instance_warehouse_device_shard(const char* config_json, morap_solver* s, int rank, int world,
+                                          morap_instance** out);
+
 /* supportingPoint (solver.hpp:103-184): w has K*n entries (unit 1-norm). Writes r (K*n)
  * and the assignment agent_of[n]. stats_out (nullable, 8 doubles): optimize jobs,
  * optimize nnz backups, evaluate jobs, evaluate state backups, optimize s, evaluate s,
@@ -135,6 +143,7 @@ int morap_multi_upload(morap_multi* m, const morap_instance* inst);
 int morap_multi_owner(const morap_multi* m, int i, int j);
 int morap_multi_pareto(morap_multi* m, const morap_instance* inst, const double* thresholds, int nt, const double* norm,
                        double eps, int iteration_cap, char* json_out, int json_cap, double* stats_out);
+int morap_multi_warehouse_device(morap_multi* m, const char* config_json, morap_instance** out);
 /* One process per GPU (torch.distributed): `s` holds this rank's shard; `allgather`
  * (recv[r * count + k] = rank r's send[k], every rank) carries the two exchanges per
  * iteration -- NCCL over NVLink on GPUs, gloo in the CPU tests. Returns 0 or a status. */

@@ -62,6 +62,8 @@ def load_host_library() -> C.CDLL:
         "morap_instance_product_owner": (i32, [p, i32, i32]),
         "morap_instance_warehouse_streamed": (i32, [C.c_char_p, i32, p, i32, C.POINTER(p)]),
         "morap_instance_warehouse_device": (i32, [C.c_char_p, p, C.POINTER(p)]),
+        "morap_instance_warehouse_device_shard": (i32, [C.c_char_p, p, i32, i32, C.POINTER(p)]),
+        "morap_multi_warehouse_device": (i32, [p, C.c_char_p, C.POINTER(p)]),
         "morap_supporting_point": (i32, [p, p, p, i32, p, p, p]),
         "morap_pareto": (i32, [p, p, p, i32, p, f64, i32, i32, C.c_char_p, i32, p]),
         "morap_pareto_core": (i32, [p, i32, i32, p, f64, i32, i32, QUERY_FN, p, C.c_char_p, i32]),
@@ -156,6 +158,18 @@ class Instance:
         h = C.c_void_p()
         _check(lib.morap_instance_warehouse_device(json.dumps(config).encode(), solver.h, C.byref(h)),
                "generateInstance (device)")
+        inst = cls(h)
+        inst.streamed = True
+        return inst
+
+    @classmethod
+    def warehouse_device_shard(cls, config: dict, solver: "Solver", rank: int, world: int) -> "Instance":
+        """Per-rank device build for shard_pareto: the owners warehouse_shard takes, only this
+        rank's products built on `solver`'s GPU (morap.h)."""
+        lib = load_host_library()
+        h = C.c_void_p()
+        _check(lib.morap_instance_warehouse_device_shard(json.dumps(config).encode(), solver.h, rank, world,
+                                                         C.byref(h)), "generateInstance (device shard)")
         inst = cls(h)
         inst.streamed = True
         return inst
@@ -448,6 +462,16 @@ class MultiSolver:
 
     def upload(self, inst: Instance):
         _check(self._lib.morap_multi_upload(self.h, inst.h), "multi upload")
+
+    def warehouse_device(self, config: dict) -> Instance:
+        """generateInstance with every product built on the device that owns it (morap.h:
+        morap_multi_warehouse_device); query it with pareto()."""
+        h = C.c_void_p()
+        _check(self._lib.morap_multi_warehouse_device(self.h, json.dumps(config).encode(), C.byref(h)),
+               "generateInstance (multi device)")
+        inst = Instance(h)
+        inst.streamed = True
+        return inst
 
     def owner(self, i, j) -> int:
         return int(self._lib.morap_multi_owner(self.h, i, j))

@@ -369,6 +369,84 @@ int morap_instance_warehouse_device(const char* config_json, morap_solver* s, mo
   });
 }
 
+int morap_instance_warehouse_device_shard(const char* config_json, morap_solver* s, int rank, int world,
+                                          morap_instance** out) {
+  return guard([&] {
+    if (!out || !config_json || !s) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) morap::fail(morap::Errc::InvalidConfig, "bad shard");
+    morap::WarehouseConfig cfg = morap::warehouseConfigFromJson(morap::Json::parse(config_json));
+    morap::GpuBackend& gpu = *s->gpu;
+    std::map<uint64_t, int> owner;
+    // every rank measures every pair (a fraction of a second at C4) and so takes the same
+    // owners as morap_instance_warehouse_shard: distinct products in first-occurrence order,
+    // each to the least loaded rank by nnz; it then builds only its own
+    const morap::InstanceBuilder build = [&](std::vector<morap::Mdp> agents, std::vector<morap::RewardStructure> costs,
+                                             std::vector<morap::Dfa> tasks) {
+      auto plan = morap::planDeviceBuild(gpu, std::move(agents), std::move(costs), std::move(tasks));
+      std::vector<double> load(static_cast<size_t>(world), 0.0);
+      std::vector<size_t> mine;
+      owner.clear();
+      for (size_t k = 0; k < plan->distinct.size(); ++k) {
+        const morap::ProductMdp* p = plan->distinct[k];
+        const int r = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+        load[static_cast<size_t>(r)] += static_cast<double>(morap::productNnz(*p));
+        owner[p->uid] = r;
+        if (r == rank) mine.push_back(k);
+      }
+      plan->write(gpu, mine);
+      return std::move(plan->inst);
+    };
+    morap::MorapInstance inst = morap::generateInstanceWith(cfg, build);
+    *out = new morap_instance{std::move(inst), {}, std::move(owner)};
+  });
+}
+
+int morap_multi_warehouse_device(morap_multi* m, const char* config_json, morap_instance** out) {
+  return guard([&] {
+    if (!m || !out || !config_json) morap::fail(morap::Errc::InvalidConfig, "null argument");
+    morap::WarehouseConfig cfg = morap::warehouseConfigFromJson(morap::Json::parse(config_json));
+    const int world = static_cast<int>(m->gpus.size());
+    for (auto& g : m->gpus) g->release();
+    m->shards.clear();
+    m->inst = nullptr;
+    std::unique_ptr<morap::DeviceBuild> plan;
+    const morap::InstanceBuilder build = [&](std::vector<morap::Mdp> agents, std::vector<morap::RewardStructure> costs,
+                                             std::vector<morap::Dfa> tasks) {
+      plan = morap::planDeviceBuild(*m->gpus[0], std::move(agents), std::move(costs), std::move(tasks));
+      return morap::MorapInstance{};
+    };
+    morap::generateInstanceWith(cfg, build);
+    auto mi = std::make_unique<morap_instance>(morap_instance{std::move(plan->inst), {}, {}});
+    const morap::MorapInstance& inst = mi->inst;
+    // the owners morap_multi_upload would take (LPT by nnz); each device builds its own
+    const std::vector<int> owner = morap::lptOwners(inst, world);
+    std::map<const morap::ProductMdp*, int> ownerOf;
+    for (int i = 0; i < inst.n; ++i)
+      for (int j = 0; j < inst.n; ++j) ownerOf[inst.products[i][j].get()] = owner[static_cast<size_t>(i) * inst.n + j];
+    std::vector<std::vector<size_t>> mine(static_cast<size_t>(world));
+    for (size_t k = 0; k < plan->distinct.size(); ++k) mine[ownerOf.at(plan->distinct[k])].push_back(k);
+    std::vector<std::thread> pool;  // one build thread per device
+    std::vector<std::exception_ptr> err(static_cast<size_t>(world));
+    for (int r = 0; r < world; ++r)
+      pool.emplace_back([&, r] {
+        try {
+          plan->write(*m->gpus[r], mine[r]);
+        } catch (...) {
+          err[r] = std::current_exception();
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
+    for (int r = 0; r < world; ++r) {
+      m->shards.push_back(std::make_unique<morap::Shard>(inst, *m->gpus[r], owner, r));
+      m->shards.back()->upload();  // registers nothing new: every owned product is resident
+    }
+    m->inst = &mi->inst;
+    *out = mi.release();
+  });
+}
+
 int morap_multi_create(const int* devices, int ndevices, morap_multi** out) {
   return guard([&] {
     if (!out || !devices || ndevices < 1) morap::fail(morap::Errc::InvalidConfig, "need at least one device");

@@ -315,6 +315,20 @@ class GpuBackend {
 // buildInstance (instance.hpp:42-91) with every product built on the GPU (morap_cuda_build_products):
 // the products stay device-resident as lean compact models, the instance holds slim products
 // (dimensions, reward finiteness, identity hash). Two objectives only (cost, success).
+// In two steps for sharded builds: planDeviceBuild validates, measures every pair on `gpu`
+// and rejects / deduplicates (the instance and its distinct products, nothing registered
+// yet); DeviceBuild::write builds a subset of the distinct products on any device.
+struct DeviceBuild {
+  MorapInstance inst;
+  std::vector<ProductMdp*> distinct;  // first-occurrence order
+  struct Inputs;                      // agents / tasks / alphabets in the ABI layout
+  std::unique_ptr<Inputs> in;
+  void write(GpuBackend& gpu, const std::vector<size_t>& which) const;  // indices into `distinct`
+  DeviceBuild();
+  ~DeviceBuild();
+};
+std::unique_ptr<DeviceBuild> planDeviceBuild(GpuBackend& gpu, std::vector<Mdp> agents,
+                                             std::vector<RewardStructure> costs, std::vector<Dfa> tasks);
 MorapInstance buildInstanceOnDevice(GpuBackend& gpu, std::vector<Mdp> agents, std::vector<RewardStructure> costs,
                                     std::vector<Dfa> tasks);
 

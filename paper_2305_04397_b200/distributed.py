@@ -246,7 +246,8 @@ def pareto_sharded(inst: Instance, thresholds, eps: float, rank: int, world: int
 # ------------------------------------------------------------------------------------------
 def bench_main(args, rank: int, world: int, local: int):
     """bench.py --gpus N under torchrun: sharded C2-family query, max-over-ranks timing.
-    Every rank builds only its own products (Instance.warehouse_shard)."""
+    Every rank builds only its own products (Instance.warehouse_shard; for --workload c4 on its
+    GPU, Instance.warehouse_device_shard -- then there is no host copy and no e2e leg)."""
     import json
 
     import torch
@@ -258,10 +259,14 @@ def bench_main(args, rank: int, world: int, local: int):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg, thr, eps, K = B.workload(args.workload, world)
     threads = max(1, (os.cpu_count() or 1) // world)  # ranks share the host cores
-    inst = Instance.warehouse_shard(cfg, rank, world, threads=threads)
     from .api import Solver, shard_pareto
     solver = Solver(local)
     solver.set_fingerprints(False)
+    device_built = args.workload == "c4"  # C4 sharded: each rank builds its own products on its GPU
+    if device_built:
+        inst = Instance.warehouse_device_shard(cfg, solver, rank, world)
+    else:
+        inst = Instance.warehouse_shard(cfg, rank, world, threads=threads)
     stream = torch.cuda.current_stream()
     solver.set_stream(stream.cuda_stream)
     allgather = torch_allgather(world, torch.device("cuda", local))
@@ -295,7 +300,10 @@ def bench_main(args, rank: int, world: int, local: int):
     with B.ClockSampler(local) as clk:
         ms, (bk, kernels, _, _), rep = timed(args.steps, False)
     e2e_steps = max(1, args.steps)
-    e_ms, (e_bk, _, h2d, d2h), _ = timed(e2e_steps, True)
+    if device_built:  # no host copy of the products to re-upload: no end-to-end leg
+        e_ms, e_bk, h2d, d2h = None, None, None, None
+    else:
+        e_ms, (e_bk, _, h2d, d2h), _ = timed(e2e_steps, True)
     if rank == 0:
         n = inst.n
         print(json.dumps({
@@ -309,11 +317,11 @@ def bench_main(args, rank: int, world: int, local: int):
                        "pareto_iterations": len(rep["iterations"]), "feasible": rep["feasible"],
                        "products": inst.distinct, "nnz": inst.total_nnz,
                        "value_counts": "optimize + evaluate backups summed over ranks / max-over-ranks device time"},
-            "e2e": {"value": e_bk / (e_ms * 1e-3), "unit": B.UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
-                    "d2h_bytes_per_step": d2h / e2e_steps,
-                    "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps,
-                    "note": "every rank re-uploads its products from host memory each step (the library's "
-                            "copy calls, summed over ranks); exchanges through NCCL allgather"},
+            "e2e": None if device_built else {
+                "value": e_bk / (e_ms * 1e-3), "unit": B.UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
+                "d2h_bytes_per_step": d2h / e2e_steps, "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps,
+                "note": "every rank re-uploads its products from host memory each step (the library's "
+                        "copy calls, summed over ranks); exchanges through NCCL allgather"},
             "gpu_launches": int(kernels),
             "clocks": clk.summary(),
         }))

@@ -107,3 +107,64 @@ def test_device_products_have_no_host_copy():
         inst.product(0, 0)
     with pytest.raises(MorapError):
         Solver(0).pareto(inst, [-25.0] * 3 + [0.9] * 3, eps=0.01, iteration_cap=2)
+
+
+def test_multi_device_build_matches_reference():
+    """One process, two contexts on device 0: each builds the products it owns."""
+    from paper_2305_04397_b200.api import MultiSolver
+    from tests.helpers import load_golden
+    g = load_golden("c2.json")
+    case = g["pareto"]
+    m = MultiSolver([0, 0])
+    inst = m.warehouse_device(g["config"])
+    owners = {m.owner(i, j) for i in range(inst.n) for j in range(inst.n)}
+    assert owners == {0, 1}
+    rep = m.pareto(inst, case["thresholds"], eps=case["eps"])
+    keys = ("feasible", "converged", "tUp", "tDown", "lambdaStar", "iterations")
+    assert {k: rep.get(k) for k in keys} == {k: case["result"].get(k) for k in keys}
+    m.close()
+
+
+def test_device_shard_ranks_match_reference():
+    """world 2 as two host threads, each rank building only its own products on its GPU."""
+    import threading
+
+    import numpy as np
+
+    from paper_2305_04397_b200.api import shard_pareto
+    from tests.helpers import load_golden
+    g = load_golden("c2.json")
+    case = g["pareto"]
+    world = 2
+    slots = [None] * world
+    bar = threading.Barrier(world)
+    reps, errs = [None] * world, []
+
+    def run(rank):
+        try:
+            s = Solver(0)
+            inst = Instance.warehouse_device_shard(g["config"], s, rank, world)
+            mine = sum(inst.product_owner(i, j) == rank for i in range(inst.n) for j in range(inst.n))
+            assert 0 < mine < inst.n * inst.n
+
+            def allgather(send):
+                slots[rank] = send
+                bar.wait()
+                out = np.stack([slots[r] for r in range(world)])
+                bar.wait()
+                return out
+            reps[rank] = shard_pareto(s, inst, rank, world, allgather, case["thresholds"], eps=case["eps"])
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    keys = ("feasible", "converged", "tUp", "tDown", "lambdaStar", "iterations")
+    for rep in reps:
+        assert {k: rep.get(k) for k in keys} == {k: case["result"].get(k) for k in keys}
+    assert reps[0]["stats"]["optimize_jobs"] + reps[1]["stats"]["optimize_jobs"] == 13 * 100
