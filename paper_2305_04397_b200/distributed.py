@@ -271,8 +271,9 @@ def bench_main(args, rank: int, world: int, local: int):
     solver.set_stream(stream.cuda_stream)
     allgather = torch_allgather(world, torch.device("cuda", local))
     thr = np.array(thr, np.float64)
+    cap = B.ITER_CAP.get(args.workload, 500)
     for _ in range(max(args.warmup, 0)):
-        shard_pareto(solver, inst, rank, world, allgather, thr, eps=eps)
+        shard_pareto(solver, inst, rank, world, allgather, thr, eps=eps, iteration_cap=cap)
 
     def timed(steps, reupload):
         solver.reset_cuda_stats()
@@ -284,7 +285,7 @@ def bench_main(args, rank: int, world: int, local: int):
         for _ in range(steps):
             if reupload:
                 solver.release()  # the next query re-uploads this rank's products (host image)
-            rep = shard_pareto(solver, inst, rank, world, allgather, thr, eps=eps)
+            rep = shard_pareto(solver, inst, rank, world, allgather, thr, eps=eps, iteration_cap=cap)
             backups += rep["stats"]["optimize_backups"] + rep["stats"]["evaluate_state_backups"]
         e1.record(stream)
         torch.cuda.synchronize()
