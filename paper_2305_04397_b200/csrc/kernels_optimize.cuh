@@ -800,6 +800,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const DevModel* __restri
                                                         double eps, int cap, int32_t* sweeps, double* residual,
                                                         int32_t* status) {
   __shared__ unsigned long long sB[kSelThreads / 32], sK[kSelThreads / 32];
+  __shared__ int sCnt[kSelThreads / 32], sOff[kSelThreads / 32], sBase;
   const int k = ctl->sweepsDone;
   if (ctl->nactive == 0) return;
   const int per = ((ncand + gridDim.x - 1) / gridDim.x + kSelThreads - 1) / kSelThreads * kSelThreads;
@@ -843,12 +844,21 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const DevModel* __restri
       }
       c.y &= (1 << kCandLtBits) - 1;
     }
-    // compaction per warp: one atomic per warp with a kept tile, order kept within the warp
+    // compaction per CTA: one atomic per CTA with a kept tile (same-address atomics from every
+    // warp of the grid serialise in L2), order kept within the CTA
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    int at = 0;
-    if (lane == 0 && bal) at = atomicAdd(&ctl->nsel, __popc(bal));
-    at = __shfl_sync(0xffffffffu, at, 0);
-    if (keep) sel[at + __popc(bal & ((1u << lane) - 1u))] = make_int2(c.x, c.y);
+    if (lane == 0) sCnt[wid] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < kSelThreads / 32; ++w) {
+        sOff[w] = tot;
+        tot += sCnt[w];
+      }
+      sBase = tot ? atomicAdd(&ctl->nsel, tot) : 0;
+    }
+    __syncthreads();
+    if (keep) sel[sBase + sOff[wid] + __popc(bal & ((1u << lane) - 1u))] = make_int2(c.x, c.y);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
