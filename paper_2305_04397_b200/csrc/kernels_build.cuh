@@ -4,8 +4,8 @@
 // (upload_prep.cuh: tiles, successor windows, compact streams, out-of-window lists) on the GPU.
 // Included by morap_cuda.cu inside its anonymous namespace.
 //
-// One CTA builds one product at a time (persistent CTAs claim products from a counter), with
-// every intermediate array in a per-CTA global workspace:
+// One CTA builds one product at a time (persistent CTAs, two per SM, claim products from a
+// counter), with every intermediate array in a per-CTA global workspace:
 //   BFS       level-synchronous. The reference numbers product states in FIFO discovery order
 //             (model.hpp:262-300); level by level that order is "by the first discovering edge",
 //             edges ordered by (state, row, transition): pass A takes atomicMin of the edge index
@@ -25,7 +25,11 @@
 // Mode 0 ("measure") stops before the write and reports sizes, reward finiteness and an
 // identity hash; the host deduplicates on those and builds only the distinct products.
 
-constexpr int kBT = 1024;           // builder CTA threads
+#ifndef MORAP_BUILD_THREADS
+#define MORAP_BUILD_THREADS 512
+#endif
+constexpr int kBT = MORAP_BUILD_THREADS;  // builder CTA threads (two CTAs per SM: A/B in DESIGN.md §9)
+constexpr int kBuildCtasPerSm = 1024 / kBT;
 constexpr int kBW = kBT / 32;
 constexpr int kBuildMaxCand = 1024; // distinct probabilities / costs over all agents
 
@@ -64,7 +68,7 @@ struct BuildArgs {
   int mode;             // 0 measure, 1 write
   char* ws;
   size_t wsBytes;       // per CTA
-  int32_t SQmax, Smax, Rmax, Nmax, SAmax;
+  int32_t SQmax, Smax, Rmax, Nmax, SAmax, Tmax;  // workspace bounds (Tmax: tiles)
   char* arena;
   const unsigned long long* offsets;  // mode 1: arena offset of each product
   BuildOut* out;
@@ -85,7 +89,8 @@ struct BuildWs {
 __host__ __device__ constexpr int kBinsPerWarp(int Smax) { return Smax / 64 + 2; }
 
 // Carves one CTA's workspace (base == nullptr: just the size).
-__host__ __device__ inline size_t build_ws_layout(char* base, int SQ, int S, int R, int N, int SA, BuildWs* W) {
+__host__ __device__ inline size_t build_ws_layout(char* base, int SQ, int S, int R, int N, int SA, int T,
+                                                  BuildWs* W) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     char* p = base ? base + off : nullptr;
@@ -115,13 +120,13 @@ __host__ __device__ inline size_t build_ws_layout(char* base, int SQ, int S, int
   w.closed = reinterpret_cast<int32_t*>(take(4ull * S));
   w.F1 = reinterpret_cast<int32_t*>(take(4ull * S));
   w.F2 = reinterpret_cast<int32_t*>(take(4ull * S));
-  w.tileStart = reinterpret_cast<int32_t*>(take(4ull * (S + 1)));
-  w.desc = reinterpret_cast<TileDesc*>(take(sizeof(TileDesc) * (S + 1ull)));
-  w.tcnt = reinterpret_cast<int4*>(take(sizeof(int4) * (S + 1ull)));
-  w.tbase = reinterpret_cast<int4*>(take(sizeof(int4) * (S + 1ull)));
-  w.grpCnt = reinterpret_cast<int32_t*>(take(4ull * (S + 1)));
-  w.outIdx = reinterpret_cast<int32_t*>(take(4ull * (S + 1)));
-  w.tileGrp = reinterpret_cast<int32_t*>(take(4ull * kMaxOutGroups * S));
+  w.tileStart = reinterpret_cast<int32_t*>(take(4ull * (T + 1)));
+  w.desc = reinterpret_cast<TileDesc*>(take(sizeof(TileDesc) * (T + 1ull)));
+  w.tcnt = reinterpret_cast<int4*>(take(sizeof(int4) * (T + 1ull)));
+  w.tbase = reinterpret_cast<int4*>(take(sizeof(int4) * (T + 1ull)));
+  w.grpCnt = reinterpret_cast<int32_t*>(take(4ull * (T + 1)));
+  w.outIdx = reinterpret_cast<int32_t*>(take(4ull * (T + 1)));
+  w.tileGrp = reinterpret_cast<int32_t*>(take(4ull * kMaxOutGroups * T));
   w.bins = reinterpret_cast<int32_t*>(take(4ull * kBW * kBinsPerWarp(S)));
   if (W) *W = w;
   return off;
@@ -204,7 +209,91 @@ __device__ __forceinline__ unsigned long long dbits(double d) {
 
 __device__ __forceinline__ size_t up256(size_t n) { return (n + 255) / 256 * 256; }
 
-__global__ void __launch_bounds__(kBT, 1) k_build_products(BuildArgs A) {
+// The maximal avoid set of a product in the workspace (model.cpp maximalAvoidSet): reverse
+// edges by counting sort, then the removal worklist in parallel rounds. True iff it is empty.
+__device__ bool build_reward_finite(const BuildWs& W, int S, int* sh, int& sCount, int& sCount2) {
+  const int tid = threadIdx.x;
+  for (int x = tid; x < S + 2; x += kBT) W.head[x] = 0;
+  for (int x = tid; x < S; x += kBT) {
+    W.inF[x] = W.done[x] ? 0 : 1;
+    W.fillc[x] = 0;
+  }
+  if (tid == 0) {
+    sCount = 0;
+    sCount2 = 0;
+  }
+  __syncthreads();
+  int inCount = 0;
+  for (int x = tid; x < S; x += kBT) {
+    if (!W.inF[x]) continue;
+    ++inCount;
+    int closed = 0;
+    for (int r = W.ro[x]; r < W.ro[x + 1]; ++r) {
+      W.owner[r] = x;
+      int lv = 0;
+      for (int k = W.to[r]; k < W.to[r + 1]; ++k) {
+        const int t = W.succ[k];
+        atomicAdd(&W.head[t + 1], 1);
+        lv += W.inF[t] ? 0 : 1;
+      }
+      W.leaving[r] = lv;
+      closed += lv == 0 ? 1 : 0;
+    }
+    W.closed[x] = closed;
+  }
+  inCount = breduce_sum(inCount, sh);
+  {
+    int run = 0;
+    for (int base = 0; base <= S; base += kBT) {  // head[t] = first reverse edge of t
+      const int x = base + tid;
+      const int v = x <= S ? W.head[x + 1] : 0;
+      int tot;
+      const int ex = run + bscan_excl(v, sh, tot);
+      if (x <= S) W.head[x] = ex;
+      run += tot;
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x < S; x += kBT) {
+    if (!W.inF[x]) continue;
+    for (int r = W.ro[x]; r < W.ro[x + 1]; ++r)
+      for (int k = W.to[r]; k < W.to[r + 1]; ++k) {
+        const int t = W.succ[k];
+        W.rev[W.head[t] + atomicAdd(&W.fillc[t], 1)] = r;
+      }
+    if (W.closed[x] == 0) W.F1[atomicAdd(&sCount, 1)] = x;
+  }
+  __syncthreads();
+  int removed = 0;
+  {
+    int* F = W.F1;
+    int* G = W.F2;
+    int nF = sCount;
+    __syncthreads();
+    while (nF > 0) {
+      removed += nF;
+      if (tid == 0) sCount2 = 0;
+      __syncthreads();
+      for (int i = tid; i < nF; i += kBT) {
+        const int s = F[i];
+        for (int e = W.head[s]; e < W.head[s + 1]; ++e) {
+          const int r = W.rev[e];
+          const int o = W.owner[r];
+          if (atomicAdd(&W.leaving[r], 1) == 0 && atomicSub(&W.closed[o], 1) == 1) G[atomicAdd(&sCount2, 1)] = o;
+        }
+      }
+      __syncthreads();
+      nF = sCount2;
+      int* tmp = F;
+      F = G;
+      G = tmp;
+      __syncthreads();
+    }
+  }
+  return removed == inCount;
+}
+
+__global__ void __launch_bounds__(kBT, kBuildCtasPerSm) k_build_products(BuildArgs A) {
   __shared__ int sh[kBW];
   __shared__ unsigned long long sh64[kBW];
   __shared__ int sFirstP[kBuildMaxCand], sFirstC[kBuildMaxCand + 1];
@@ -212,7 +301,7 @@ __global__ void __launch_bounds__(kBT, 1) k_build_products(BuildArgs A) {
   __shared__ int sProd, sCount, sCount2, sNt;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   BuildWs W;
-  build_ws_layout(A.ws + blockIdx.x * A.wsBytes, A.SQmax, A.Smax, A.Rmax, A.Nmax, A.SAmax, &W);
+  build_ws_layout(A.ws + blockIdx.x * A.wsBytes, A.SQmax, A.Smax, A.Rmax, A.Nmax, A.SAmax, A.Tmax, &W);
   const int binsPerWarp = kBinsPerWarp(A.Smax);
 
   for (;;) {
@@ -422,90 +511,14 @@ __global__ void __launch_bounds__(kBT, 1) k_build_products(BuildArgs A) {
     maxRow = breduce_max(maxRow, sh);
 
     // ---- reward finiteness: the maximal avoid set (model.cpp maximalAvoidSet) ------------
-    for (int x = tid; x < S + 2; x += kBT) W.head[x] = 0;
-    for (int x = tid; x < S; x += kBT) {
-      W.inF[x] = W.done[x] ? 0 : 1;
-      W.fillc[x] = 0;
-    }
-    if (tid == 0) {
-      sCount = 0;
-      sCount2 = 0;
-    }
-    __syncthreads();
-    int inCount = 0;
-    for (int x = tid; x < S; x += kBT) {
-      if (!W.inF[x]) continue;
-      ++inCount;
-      int closed = 0;
-      for (int r = W.ro[x]; r < W.ro[x + 1]; ++r) {
-        W.owner[r] = x;
-        int lv = 0;
-        for (int k = W.to[r]; k < W.to[r + 1]; ++k) {
-          const int t = W.succ[k];
-          atomicAdd(&W.head[t + 1], 1);
-          lv += W.inF[t] ? 0 : 1;
-        }
-        W.leaving[r] = lv;
-        closed += lv == 0 ? 1 : 0;
-      }
-      W.closed[x] = closed;
-    }
-    inCount = breduce_sum(inCount, sh);
-    {
-      int run = 0;
-      for (int base = 0; base <= S; base += kBT) {  // head[t] = first reverse edge of t
-        const int x = base + tid;
-        const int v = x <= S ? W.head[x + 1] : 0;
-        int tot;
-        const int ex = run + bscan_excl(v, sh, tot);
-        if (x <= S) W.head[x] = ex;
-        run += tot;
-      }
-    }
-    __syncthreads();
-    for (int x = tid; x < S; x += kBT) {
-      if (!W.inF[x]) continue;
-      for (int r = W.ro[x]; r < W.ro[x + 1]; ++r)
-        for (int k = W.to[r]; k < W.to[r + 1]; ++k) {
-          const int t = W.succ[k];
-          W.rev[W.head[t] + atomicAdd(&W.fillc[t], 1)] = r;
-        }
-      if (W.closed[x] == 0) W.F1[atomicAdd(&sCount, 1)] = x;
-    }
-    __syncthreads();
-    int removed = 0;
-    {
-      int* F = W.F1;
-      int* G = W.F2;
-      int nF = sCount;
-      __syncthreads();
-      while (nF > 0) {
-        removed += nF;
-        if (tid == 0) sCount2 = 0;
-        __syncthreads();
-        for (int i = tid; i < nF; i += kBT) {
-          const int s = F[i];
-          for (int e = W.head[s]; e < W.head[s + 1]; ++e) {
-            const int r = W.rev[e];
-            const int o = W.owner[r];
-            if (atomicAdd(&W.leaving[r], 1) == 0 && atomicSub(&W.closed[o], 1) == 1) G[atomicAdd(&sCount2, 1)] = o;
-          }
-        }
-        __syncthreads();
-        nF = sCount2;
-        int* tmp = F;
-        F = G;
-        G = tmp;
-        __syncthreads();
-      }
-    }
-    res.rewardFinite = removed == inCount ? 1 : 0;
+    // (measure pass only: the write pass builds products the host accepted as reward-finite)
+    res.rewardFinite = A.mode == 0 ? (build_reward_finite(W, S, sh, sCount, sCount2) ? 1 : 0) : 1;
 
     // ---- tiles (make_tiles), one warp ---------------------------------------------------
     if (wid == 0) {
       int s = 0, nt = 0;
       if (lane == 0) W.tileStart[0] = 0;
-      while (s < S) {
+      while (s < S && nt < A.Tmax) {  // (Tmax is a bound, never reached: checked below)
         const int rs = W.ro[s], ks = W.eb[s];
         int cnt = 0;
 #pragma unroll
@@ -527,11 +540,12 @@ __global__ void __launch_bounds__(kBT, 1) k_build_products(BuildArgs A) {
       }
       if (lane == 0) {
         W.desc[nt] = TileDesc{S, R, nnz, 0, 0, 0, 0, 0};
-        sNt = nt;
+        sNt = s < S ? -nt : nt;
       }
     }
     __syncthreads();
-    const int nt = sNt;
+    if (sNt < 0) res.status = MORAP_SIZE_GUARD;  // the tile workspace bound was wrong: no model
+    const int nt = sNt < 0 ? -sNt : sNt;
 
     // ---- per tile: successor window, flags, out-of-window lists (warp per tile) ---------
     for (int t = wid; t < nt; t += kBW) {

@@ -1651,7 +1651,10 @@ int morap_cuda_build_products(morap_ctx* ctx, int nagents, const morap_build_age
       if (d.letter_of_set[l] < 0 || d.letter_of_set[l] >= d.num_letters)
         return ctx->fail(MORAP_INVALID_DFA, who + ": letter out of range");
   }
-  int64_t SQmax = 1, Rmax = 1, Nmax = 1, SAmax = 1;
+  // tiles: every tile but the last ends because the next state would overflow one of its caps
+  // (kBlock states, kRowCap rows, kNnzCap transitions), so it holds at least kBlock states,
+  // kRowCap - (widest state's rows) rows or kNnzCap - (widest state's transitions) transitions
+  int64_t SQmax = 1, Rmax = 1, Nmax = 1, SAmax = 1, Tmax = 1;
   for (int k = 0; k < npairs; ++k) {
     const int a = pairs[2 * k], t = pairs[2 * k + 1];
     if (a < 0 || a >= nagents || t < 0 || t >= ntasks)
@@ -1661,6 +1664,11 @@ int morap_cuda_build_products(morap_ctx* ctx, int nagents, const morap_build_age
     Rmax = std::max(Rmax, SQ * maxRows[a]);
     Nmax = std::max(Nmax, SQ * maxEdges[a]);
     SAmax = std::max<int64_t>(SAmax, agents[a].num_states);
+    int64_t T = SQ;
+    if (maxRows[a] < kRowCap && maxEdges[a] < kNnzCap)
+      T = std::min(SQ, 2 + SQ / kBlock + SQ * maxRows[a] / (kRowCap - maxRows[a]) +
+                            SQ * maxEdges[a] / (kNnzCap - maxEdges[a]));
+    Tmax = std::max(Tmax, T);
   }
   if (Nmax >= (int64_t{1} << 31) - 2 || Rmax >= (int64_t{1} << 31) - 2)
     return ctx->fail(MORAP_SIZE_GUARD, "build_products: a product could exceed 2^31 transitions");
@@ -1744,9 +1752,9 @@ int morap_cuda_build_products(morap_ctx* ctx, int nagents, const morap_build_age
   // per-CTA workspaces: one CTA per SM, fewer when they would not fit in a quarter of free memory
   const size_t wsBytes = align_up(build_ws_layout(nullptr, static_cast<int>(SQmax), static_cast<int>(SQmax),
                                                   static_cast<int>(Rmax), static_cast<int>(Nmax),
-                                                  static_cast<int>(SAmax), nullptr),
+                                                  static_cast<int>(SAmax), static_cast<int>(Tmax), nullptr),
                                   256);
-  int grid = std::min(npairs, ctx->numSMs);
+  int grid = std::min(npairs, ctx->numSMs * kBuildCtasPerSm);
   if (ctx->buildWsBytes < wsBytes * grid) {
     cudaFree(ctx->buildWs);
     ctx->buildWs = nullptr;
@@ -1783,6 +1791,7 @@ int morap_cuda_build_products(morap_ctx* ctx, int nagents, const morap_build_age
   A.Rmax = static_cast<int32_t>(Rmax);
   A.Nmax = static_cast<int32_t>(Nmax);
   A.SAmax = static_cast<int32_t>(SAmax);
+  A.Tmax = static_cast<int32_t>(Tmax);
   A.arena = static_cast<char*>(arena);
   A.offsets = reinterpret_cast<const unsigned long long*>(dBlob + offOffsets);
   A.out = reinterpret_cast<BuildOut*>(dBlob + offOut);
