@@ -38,6 +38,10 @@ int morap_instance_warehouse(const char* config_json, int threads, morap_instanc
  * and *has_norm is set. */
 int morap_instance_from_json(const char* json_text, const char* base_dir, morap_instance** out, double* norm_out,
                              int norm_cap, int* has_norm);
+/* instanceFromJson with the products built on the GPU of `s` (morap_cuda_build_products); the
+ * instance then answers queries on `s` only (two objectives; see morap_instance_warehouse_device). */
+int morap_instance_from_json_device(const char* json_text, const char* base_dir, morap_solver* s,
+                                    morap_instance** out, double* norm_out, int norm_cap, int* has_norm);
 void morap_instance_free(morap_instance* inst);
 
 /* out[8] = {n, realTasks, distinctProducts, K, sum states, sum rows, sum nnz over the n^2

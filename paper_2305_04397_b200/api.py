@@ -45,6 +45,8 @@ def load_host_library() -> C.CDLL:
         "morap_last_error": (C.c_char_p, []),
         "morap_instance_warehouse": (i32, [C.c_char_p, i32, C.POINTER(p)]),
         "morap_instance_from_json": (i32, [C.c_char_p, C.c_char_p, C.POINTER(p), p, i32, C.POINTER(C.c_int)]),
+        "morap_instance_from_json_device": (i32, [C.c_char_p, C.c_char_p, p, C.POINTER(p), p, i32,
+                                                  C.POINTER(C.c_int)]),
         "morap_instance_free": (None, [p]),
         "morap_instance_info": (i32, [p, p]),
         "morap_instance_product_dims": (i32, [p, i32, i32, p, C.POINTER(u64)]),
@@ -197,6 +199,20 @@ class Instance:
                                             C.byref(has)), "instanceFromJson")
         d = has.value
         return cls(h, norm[: d * d].reshape(d, d).copy() if d else None)
+
+    @classmethod
+    def from_json_device(cls, text: str, solver: "Solver", base_dir: str = ".") -> "Instance":
+        """from_json with the products built on `solver`'s GPU (morap.h)."""
+        lib = load_host_library()
+        h = C.c_void_p()
+        norm = np.zeros(4096, np.float64)
+        has = C.c_int(0)
+        _check(lib.morap_instance_from_json_device(text.encode(), base_dir.encode(), solver.h, C.byref(h), _ptr(norm),
+                                                   norm.shape[0], C.byref(has)), "instanceFromJson (device)")
+        d = has.value
+        inst = cls(h, norm[: d * d].reshape(d, d).copy() if d else None)
+        inst.streamed = True
+        return inst
 
     def close(self):
         if getattr(self, "h", None):

@@ -147,8 +147,9 @@ int morap_instance_warehouse(const char* config_json, int threads, morap_instanc
   });
 }
 
-int morap_instance_from_json(const char* text, const char* base_dir, morap_instance** out, double* norm_out,
-                             int norm_cap, int* has_norm) {
+namespace {
+int fromJson(const char* text, const char* base_dir, morap_instance** out, double* norm_out, int norm_cap,
+             int* has_norm, const morap::InstanceBuilder* build) {
   return guard([&] {
     if (!out || !text) morap::fail(morap::Errc::InvalidConfig, "null argument");
     morap::Json j;
@@ -158,7 +159,7 @@ int morap_instance_from_json(const char* text, const char* base_dir, morap_insta
       morap::fail(morap::Errc::Io, e.what());
     }
     const std::string base = base_dir ? base_dir : ".";
-    auto inst = std::make_unique<morap_instance>(morap_instance{morap::instanceFromJson(j, base), {}, {}});
+    auto inst = std::make_unique<morap_instance>(morap_instance{morap::instanceFromJson(j, base, build), {}, {}});
     if (has_norm) *has_norm = 0;
     if (j.contains("norm") && norm_out) {
       morap::Json nj = j.at("norm");
@@ -182,6 +183,23 @@ int morap_instance_from_json(const char* text, const char* base_dir, morap_insta
     }
     *out = inst.release();
   });
+}
+}  // namespace
+
+int morap_instance_from_json(const char* text, const char* base_dir, morap_instance** out, double* norm_out,
+                             int norm_cap, int* has_norm) {
+  return fromJson(text, base_dir, out, norm_out, norm_cap, has_norm, nullptr);
+}
+
+int morap_instance_from_json_device(const char* text, const char* base_dir, morap_solver* s, morap_instance** out,
+                                    double* norm_out, int norm_cap, int* has_norm) {
+  if (!s) return guard([&] { morap::fail(morap::Errc::InvalidConfig, "null solver"); });
+  morap::GpuBackend& gpu = *s->gpu;
+  const morap::InstanceBuilder build = [&](std::vector<morap::Mdp> agents, std::vector<morap::RewardStructure> costs,
+                                           std::vector<morap::Dfa> tasks) {
+    return morap::buildInstanceOnDevice(gpu, std::move(agents), std::move(costs), std::move(tasks));
+  };
+  return fromJson(text, base_dir, out, norm_out, norm_cap, has_norm, &build);
 }
 
 void morap_instance_free(morap_instance* inst) { delete inst; }

@@ -477,7 +477,8 @@ ParetoResult paretoPointMulti(const std::vector<Shard*>& shards, const Vec& thre
 Json resultToJson(const ParetoResult& result, const SynthesisResult* synthesis = nullptr);
 
 // instance file (cli.hpp:84-117): agents inline or as paths, tasks as LTL strings / DFA JSON.
-MorapInstance instanceFromJson(const Json& j, const std::string& baseDir = ".");
+// `build` (optional): the instance builder to use instead of buildInstance (device builds)
+MorapInstance instanceFromJson(const Json& j, const std::string& baseDir = ".", const InstanceBuilder* build = nullptr);
 
 // ---- centralised model (centralised.hpp) -------------------------------------------------
 // One MDP over (agent block i, task j, product state, assigned-agent mask) with the control

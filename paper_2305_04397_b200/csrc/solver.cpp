@@ -306,7 +306,7 @@ Json resultToJson(const ParetoResult& result, const SynthesisResult* synthesis) 
   return j;
 }
 
-MorapInstance instanceFromJson(const Json& j, const std::string& baseDir) {
+MorapInstance instanceFromJson(const Json& j, const std::string& baseDir, const InstanceBuilder* build) {
   if (!j.is_object() || !j.contains("agents") || !j.contains("tasks"))
     fail(Errc::InvalidConfig, "instance file needs agents and tasks");
   auto readFile = [&](const std::string& rel) {
@@ -336,6 +336,7 @@ MorapInstance instanceFromJson(const Json& j, const std::string& baseDir) {
     if (s.size() > 5 && s.compare(s.size() - 5, 5, ".json") == 0) tasks.push_back(dfaFromJson(readFile(s)));
     else tasks.push_back(insertPreSinks(formulaToDfa(parseCoSafe(s))));
   }
+  if (build) return (*build)(std::move(agents), std::move(costs), std::move(tasks));
   return buildInstance(std::move(agents), std::move(costs), std::move(tasks));
 }
 

@@ -168,3 +168,20 @@ def test_device_shard_ranks_match_reference():
     for rep in reps:
         assert {k: rep.get(k) for k in keys} == {k: case["result"].get(k) for k in keys}
     assert reps[0]["stats"]["optimize_jobs"] + reps[1]["stats"]["optimize_jobs"] == 13 * 100
+
+
+def test_json_instance_built_on_device_matches_reference():
+    """instanceFromJson with the device builder: the fig2 instance (hand-written agent MDP and
+    formulas) answers every recorded query of the reference bit for bit, schedulers included."""
+    from tests.helpers import GOLDEN, load_golden
+    gold = load_golden("pareto.json")
+    s = Solver(0)
+    inst = Instance.from_json_device(open(f"{GOLDEN}/fig2.json").read(), s)
+    host = Instance.from_json(open(f"{GOLDEN}/fig2.json").read())
+    assert (inst.n, inst.distinct, inst.total_states, inst.total_nnz) == \
+           (host.n, host.distinct, host.total_states, host.total_nnz)
+    for case in gold["fig2"]:
+        got = s.pareto(inst, case["thresholds"], eps=case["eps"])
+        for key in ("feasible", "converged", "tUp", "tDown", "lambdaStar", "thresholds", "iterations", "synthesis",
+                    "records"):
+            assert got[key] == case["result"][key], key
