@@ -75,8 +75,11 @@ def _read(path: str) -> str:
         _fail(Errc.Io, f"cannot read {path}: {e.strerror}")
 
 
-def _load_instance(path: str):
+def _load_instance(path: str, solver=None):
+    """instanceFromJson; with `solver`, the products are built on its GPU (--device-build)."""
     from .api import Instance
+    if solver is not None:
+        return Instance.from_json_device(_read(path), solver, os.path.dirname(os.path.abspath(path)))
     return Instance.from_json(_read(path), os.path.dirname(os.path.abspath(path)))
 
 
@@ -121,13 +124,17 @@ def _write(path: str, text: str):
 
 def cmd_solve(a, verb: str) -> int:
     """runSolve + the pareto / verify / synth branch of runCli (cli.hpp:230-250, 387-405)."""
-    inst = _load_instance(a.instance)
+    from .api import Centralised, Solver
+    device_build = getattr(a, "device_build", False)
+    if device_build and getattr(a, "centralised", False):
+        _fail(Errc.InvalidConfig, "--device-build keeps the products on the device; --centralised needs them on the host")
+    solver = Solver(a.device) if device_build else None
+    inst = _load_instance(a.instance, solver)
     thr = _thresholds(a.thresholds)
     if len(thr) != inst.objectives * inst.n:  # paretoPoint's dimension check, before any device work
         _fail(Errc.DimensionMismatch, f"{len(thr)} thresholds for {inst.objectives * inst.n} objectives")
     norm = np.asarray(json.loads(_read(a.norm)), np.float64) if a.norm else inst.norm
-    from .api import Centralised, Solver
-    solver = Solver(a.device)
+    solver = solver or Solver(a.device)
     if getattr(a, "centralised", False):
         rep = solver.centralised_pareto(Centralised(inst), thr, eps=a.eps, norm=norm, iteration_cap=a.max_iters)
     else:
@@ -154,7 +161,11 @@ def cmd_bench(a) -> int:
             wc["seed"] = a.seed
         eps = run.get("eps", 0.01)
         t0 = time.perf_counter()
-        inst = Instance.warehouse(wc)
+        if a.device_build and not a.centralised:
+            solver.release()
+            inst = Instance.warehouse_device(wc, solver)  # products built on the GPU, resident
+        else:
+            inst = Instance.warehouse(wc)
         t1 = time.perf_counter()
         entry = {"config": wc, "agents": inst.n, "totalProductStates": inst.total_states,
                  "distinctProducts": inst.distinct, "generateSeconds": t1 - t0}
@@ -164,7 +175,8 @@ def cmd_bench(a) -> int:
             entry["centralisedStates"] = c.S
             rep = solver.centralised_pareto(c, run["thresholds"], eps=eps)
         else:
-            solver.release()
+            if not a.device_build:
+                solver.release()
             rep = solver.pareto(inst, run["thresholds"], eps=eps)
         entry["solveSeconds"] = time.perf_counter() - t2
         entry.update(feasible=rep["feasible"], converged=rep["converged"], iterations=len(rep["iterations"]),
@@ -194,6 +206,7 @@ def _parser() -> argparse.ArgumentParser:
         p.add_argument("--max-iters", type=int, default=500)
         p.add_argument("--workers", type=int, default=0, help="accepted for compatibility (device batches)")
         p.add_argument("--device", type=int, default=0)
+        p.add_argument("--device-build", action="store_true", help="build the products on the GPU")
         p.add_argument("--out")
         if verb != "synth":
             p.add_argument("--centralised", action="store_true")
@@ -204,6 +217,7 @@ def _parser() -> argparse.ArgumentParser:
     p.add_argument("--workers", type=int, default=0)
     p.add_argument("--out")
     p.add_argument("--device", type=int, default=0)
+    p.add_argument("--device-build", action="store_true", help="build the products on the GPU (decentralised runs)")
     return ap
 
 

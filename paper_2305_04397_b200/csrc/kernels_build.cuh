@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(kBT, kBuildCtasPerSm) k_build_products(BuildAr
         int tot;
         const int e0 = ecur + levelEdges + bscan_excl(ne, sh, tot);
         if (x < fb) {
+          MORAP_CHECK(e0 + ne <= A.Nmax);
           W.eb[x] = e0;
           for (int i = 0; i < ne; ++i) {
             const int t = ps ? s : ag.succ[kb + i];
@@ -386,6 +387,7 @@ __global__ void __launch_bounds__(kBT, kBuildCtasPerSm) k_build_products(BuildAr
             const int qq = tk.delta[q * L + W.let[t]];
             const int slot = t * Q + qq;
             if (W.id[slot] < 0 && W.minE[slot] == e0 + i) {
+              MORAP_CHECK(nid < A.Smax && slot < SQ);
               W.id[slot] = nid;
               W.as[nid] = t;
               W.qs[nid] = qq;
@@ -443,6 +445,7 @@ __global__ void __launch_bounds__(kBT, kBuildCtasPerSm) k_build_products(BuildAr
       const uint8_t f = tk.flags[q];
       const bool ps = (f & 4) != 0;
       const int r0 = W.ro[x], e0 = W.eb[x];
+      MORAP_CHECK(r0 + (ps ? 1 : ag.row[s + 1] - ag.row[s]) <= A.Rmax);
       W.done[x] = (f & 3) ? 1 : 0;
       h += hterm(1, x, (static_cast<unsigned long long>(r0) << 32) | static_cast<unsigned>(e0));
       h += hterm(2, x, f & 7);

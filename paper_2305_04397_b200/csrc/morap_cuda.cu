@@ -293,7 +293,6 @@ int ensure_ctl(morap_ctx* ctx, size_t njobs) {
 int upload_models_table(morap_ctx* ctx) {
   if (ctx->dm.size() > ctx->dModelsCap) {
     cudaFree(ctx->dModels);
-  cudaFree(ctx->buildWs);
     size_t cap = std::max<size_t>(ctx->dm.size() * 2, 16);
     CK(cudaMalloc(&ctx->dModels, cap * sizeof(DevModel)));
     ctx->dModelsCap = cap;
@@ -1415,6 +1414,7 @@ int morap_cuda_destroy(morap_ctx* ctx) {
   for (void* p : ctx->modelAllocs) cudaFree(p);
   for (auto& f : ctx->freeModelAllocs) cudaFree(f.first);
   cudaFree(ctx->dModels);
+  cudaFree(ctx->buildWs);
   cudaFree(ctx->optArena);
   cudaFree(ctx->evalArena);
   cudaFree(ctx->dOptJobs);
@@ -1593,6 +1593,10 @@ int morap_cuda_build_products(morap_ctx* ctx, int nagents, const morap_build_age
     return ctx->fail(MORAP_INVALID_CONFIG, "build_products: null argument");
   if (npairs == 0) return MORAP_OK;
   cudaSetDevice(ctx->device);
+  {
+    const cudaError_t stale = cudaPeekAtLastError();
+    if (stale != cudaSuccess) return ctx->cudaFail(stale, "stale error before build_products", __LINE__);
+  }
   const auto t0 = std::chrono::steady_clock::now();
   auto lap = [&](const char* what) {
     if (ctx->trace)
@@ -1756,7 +1760,7 @@ int morap_cuda_build_products(morap_ctx* ctx, int nagents, const morap_build_age
                                   256);
   int grid = std::min(npairs, ctx->numSMs * kBuildCtasPerSm);
   if (ctx->buildWsBytes < wsBytes * grid) {
-    cudaFree(ctx->buildWs);
+    if (ctx->buildWs) CK(cudaFree(ctx->buildWs));
     ctx->buildWs = nullptr;
     ctx->buildWsBytes = 0;
     size_t freeB = 0, totalB = 0;

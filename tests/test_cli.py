@@ -120,3 +120,20 @@ def test_cli_solve_fig2_matches_reference(tmp_path):
     assert got["tDown"] == res["tDown"] and got["feasible"] == res["feasible"]
     assert got["iterationCount"] == len(res["iterations"]) and got["eps"] == case["eps"]
     assert [it["w"] for it in got["iterations"]] == [it["w"] for it in res["iterations"]]
+
+
+@pytest.mark.gpu
+def test_cli_device_build_same_output(tmp_path):
+    case = load_golden("pareto.json")["fig2"][0]
+    args = ["pareto", "--instance", FIG2, "--thresholds=" + ",".join(map(str, case["thresholds"])), "--eps",
+            str(case["eps"])]
+    host, dev = _run(*args), _run(*args, "--device-build")
+    assert dev.returncode == host.returncode, dev.stderr
+    assert dev.stdout == host.stdout
+    b_host = _run("bench", "--config", f"{GOLDEN}/warehouse_suite.json")
+    b_dev = _run("bench", "--config", f"{GOLDEN}/warehouse_suite.json", "--device-build")
+    assert b_dev.returncode == 0, b_dev.stderr
+    strip = ("generateSeconds", "solveSeconds")
+    got = [{k: v for k, v in r.items() if k not in strip} for r in json.loads(b_dev.stdout)["runs"]]
+    want = [{k: v for k, v in r.items() if k not in strip} for r in json.loads(b_host.stdout)["runs"]]
+    assert got == want
