@@ -21,3 +21,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 1 --no-north-star --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
 echo "ncu launches rc=$?"
 python scripts/launch_summary.py gpurun_out/launches.csv "ncu launch list of python bench.py --steps 2 --warmup 1 --no-north-star --no-cpu-baseline (C2)" > gpurun_out/launches.txt 2>&1; head -20 gpurun_out/launches.txt
+# device product builder: C4 build trace, and one ncu --set full capture of the builder kernel (C2 measure pass)
+MORAP_TRACE=1 timeout 300 python scripts/probe_device_build.py c4 0 > gpurun_out/devc4.json 2> gpurun_out/devc4.err; echo "device build rc=$?"
+tail -1 gpurun_out/devc4.json; grep "build_products\|planDevice\|DeviceBuild" gpurun_out/devc4.err
+timeout 600 ncu --kernel-name regex:k_build_products --launch-count 1 --set full --clock-control none --import-source on \
+  -f -o gpurun_out/build_c2 python scripts/probe_device_build.py c2 0 > gpurun_out/ncu_build.log 2>&1; echo "ncu build rc=$?"
