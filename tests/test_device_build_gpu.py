@@ -185,3 +185,28 @@ def test_json_instance_built_on_device_matches_reference():
         for key in ("feasible", "converged", "tUp", "tDown", "lambdaStar", "thresholds", "iterations", "synthesis",
                     "records"):
             assert got[key] == case["result"][key], key
+
+
+def _chain_instance(nstates):
+    """A chain agent whose every state has its own pair of probabilities: 2 * nstates distinct
+    values -- no compact layout above 256 (the host path falls back to fp64 arrays)."""
+    import json
+    acts = []
+    for s in range(nstates):
+        p = 0.5 + 1e-4 * (s + 1)
+        acts.append({"state": s, "name": "go", "to": [{"s": s + 1, "p": p}, {"s": s, "p": 1.0 - p}], "reward": -1})
+    acts.append({"state": nstates, "name": "stay", "to": [{"s": nstates, "p": 1.0}], "reward": -1})
+    agent = {"states": nstates + 1, "initial": 0, "labels": {str(nstates): ["goal"]}, "actions": acts}
+    return json.dumps({"agents": [agent], "tasks": ["F goal"]})
+
+
+@pytest.mark.parametrize("nstates,msg", [(200, "compact"), (600, "alphabet")])
+def test_device_build_rejects_what_it_cannot_lay_out(nstates, msg):
+    text = _chain_instance(nstates)
+    host = Instance.from_json(text)  # the host path takes any product
+    rep = Solver(0).pareto(host, [-2000.0, 0.5], eps=0.01)
+    assert rep["converged"]
+    with pytest.raises(MorapError) as err:
+        Instance.from_json_device(text, Solver(0))
+    assert err.value.code == Errc.InvalidConfig
+    assert msg in str(err.value)
