@@ -44,6 +44,7 @@ assert lib.morap_cuda_debug_cta_trace(be.h, 0, buf.ctypes.data_as(C.c_void_p), n
 blocks = int(sys.argv[2]) if len(sys.argv) > 2 else 148 * 4  # the compact sweep's grid
 T = buf[: 128 * blocks * 4].reshape(128, blocks, 4).astype(np.int64)
 rows = []
+starts = []
 nsw = int(sw.max())
 for k in range(max(0, nsw - 128), nsw):  # the slots keep the last 128 sweeps
     t = T[k % 128]
@@ -58,9 +59,15 @@ for k in range(max(0, nsw - 128), nsw):  # the slots keep the last 128 sweeps
     end = (t[:, 2] - t0) / 1e3
     rows.append((k + 1, fin / 1e3, (t[:, 0] - t0).max() / 1e3, np.median(first), np.median(end), end.max(),
                  fin / 1e3 - end.max()))
+    starts.append((t0, t0 + fin))
 print(f"{mode}: CTAs {T.shape[1]}")
 print("sweep  span_us  start_spread  first_stage_med  work_end_med  work_end_max  finalize_us")
 for r in rows[:: max(1, len(rows) // 12)]:
     print("%5d  %7.1f  %12.1f  %15.1f  %12.1f  %12.1f  %11.1f" % r)
 a = np.array(rows)[:, 1:]
 print("mean   %7.1f  %12.1f  %15.1f  %12.1f  %12.1f  %11.1f" % tuple(a.mean(0)))
+# start-to-start: the sweep plus the k_select launch and the gaps before the next sweep
+gaps = [(starts[q + 1][0] - starts[q][1]) / 1e3 for q in range(len(starts) - 1)]
+print("per sweep: span_us, then gap to the next sweep's first CTA (k_select + launch gaps)")
+print(" ".join("%d:%.1f/%.1f" % (rows[q][0], rows[q][1], gaps[q]) for q in range(len(gaps))))
+print("sum span %.1f us, sum gaps %.1f us over %d sweeps" % (sum(r[1] for r in rows), sum(gaps), len(rows)))
