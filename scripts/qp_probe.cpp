@@ -60,6 +60,8 @@ int main(int argc, char** argv) {
 #ifdef MORAP_QP_PROFILE
     std::printf("  blocked solve: panel %.3f  list %.3f  pivot rows %.3f  trailing %.3f  back-subst %.3f  KKT assembly %.3f s\n",
                 g_qpProf[0], g_qpProf[1], g_qpProf[2], g_qpProf[3], g_qpProf[4], g_qpProf[5]);
+    std::printf("  per projection: eliminations %.1f G row updates (sum dim^3/3), re-solves %.0f\n",
+                g_qpProf[6] / 2e3, g_qpProf[7] / 2);
     std::fill_n(g_qpProf, 8, 0.0);
 #endif
     std::printf("D=%d points=%d unblocked %.3f s  blocked %.3f s  (x%.2f)  bits %s\n", d, k, sec[1], sec[0],
