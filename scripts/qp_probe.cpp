@@ -51,6 +51,9 @@ int main(int argc, char** argv) {
     unsigned long long h[2];
     for (int mode = 1; mode >= 0; --mode) {
       denseSolveMode() = mode;
+#ifdef MORAP_QP_PROFILE
+      std::fill_n(g_qpProf, 8, 0.0);  // the profile is the blocked run's
+#endif
       const auto t0 = std::chrono::steady_clock::now();
       const ProjectionResult p = projectToLowerApprox(t, phi, NormMatrix::identity(d));
       sec[mode] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -58,10 +61,12 @@ int main(int argc, char** argv) {
     }
     bad += h[0] != h[1];
 #ifdef MORAP_QP_PROFILE
-    std::printf("  blocked solve: panel %.3f  list %.3f  pivot rows %.3f  trailing %.3f  back-subst %.3f  KKT assembly %.3f s\n",
-                g_qpProf[0], g_qpProf[1], g_qpProf[2], g_qpProf[3], g_qpProf[4], g_qpProf[5]);
+    std::printf("  blocked solve: panel %.3f  list %.3f  pivot rows %.3f  trailing + lookahead %.3f  re-solves %.3f  "
+                "KKT assembly %.3f  rest of the QP %.3f s\n",
+                g_qpProf[0], g_qpProf[1], g_qpProf[2], g_qpProf[3], g_qpProf[4], g_qpProf[5],
+                sec[0] - (g_qpProf[0] + g_qpProf[1] + g_qpProf[2] + g_qpProf[3] + g_qpProf[4] + g_qpProf[5]));
     std::printf("  per projection: eliminations %.1f G row updates (sum dim^3/3), re-solves %.0f\n",
-                g_qpProf[6] / 2e3, g_qpProf[7] / 2);
+                g_qpProf[6] / 1e3, g_qpProf[7]);
     std::fill_n(g_qpProf, 8, 0.0);
 #endif
     std::printf("D=%d points=%d unblocked %.3f s  blocked %.3f s  (x%.2f)  bits %s\n", d, k, sec[1], sec[0],
