@@ -836,9 +836,7 @@ __global__ void __launch_bounds__(kBT, kBuildCtasPerSm) k_build_products(BuildAr
       dm.nRowW = nRowW;
       dm.nTrW = nTrW;
       dm.bytesPerSweep = 4ull * nnz + 4ull * R + 20ull * S;
-      const double nnzPerRow = R ? __ddiv_rn(static_cast<double>(nnz), static_cast<double>(R)) : 0.0;
-      dm.bytesPerEval = static_cast<unsigned long long>(
-          __dmul_rn(static_cast<double>(S), __dadd_rn(29.0, __dmul_rn(12.0, nnzPerRow))));
+      dm.bytesPerEval = 0;  // set on the host (the same formula as pack_models)
       res.dm = dm;
     }
     __syncthreads();

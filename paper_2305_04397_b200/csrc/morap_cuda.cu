@@ -1819,6 +1819,8 @@ int morap_cuda_build_products(morap_ctx* ctx, int nagents, const morap_build_age
   for (int k = 0; k < npairs; ++k) {
     const BuildOut& o = out[k];
     built[k] = o.dm;
+    const double nnzPerRow = o.R ? static_cast<double>(o.nnz) / o.R : 0.0;  // as pack_models
+    built[k].bytesPerEval = static_cast<unsigned long long>(o.S * (29.0 + 12.0 * nnzPerRow));
     hmods[k] = HostModel{o.S, o.R, o.nnz, 0, o.ntiles, 2, o.rewardFinite, o.maxRowNnz, o.nOutGrp, o.needB};
   }
   return register_models(ctx, built, hmods, model_ids_out);
