@@ -210,3 +210,33 @@ def test_device_build_rejects_what_it_cannot_lay_out(nstates, msg):
         Instance.from_json_device(text, Solver(0))
     assert err.value.code == Errc.InvalidConfig
     assert msg in str(err.value)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_device_models_bitwise_random_configs(seed):
+    """Random warehouse layouts (grid, racks, feed, slip, deadline, seed): the device models
+    equal the host-prepared ones array for array."""
+    import random
+    rng = random.Random(1000 + seed)
+    W, H = rng.randint(3, 8), rng.randint(3, 8)
+    n = rng.randint(1, 4)
+    cells = [[x, y] for x in range(W) for y in range(H)]
+    rng.shuffle(cells)
+    racks = cells[: max(n, rng.randint(n, n + 3))]
+    cfg = {"W": W, "H": H, "n": n, "slip": rng.choice([0.0, 0.05, 0.1, 0.25]), "racks": racks,
+           "feed": cells[-1], "seed": rng.randint(0, 10000)}
+    if rng.random() < 0.5:
+        cfg["deadline"] = rng.randint(W + H, 3 * (W + H))
+    try:
+        host, hs, dev, ds = host_and_device(cfg)
+    except MorapError as e:  # the host path rejects it too (e.g. no reward-finite seed)
+        with pytest.raises(MorapError) as err:
+            Instance.warehouse(cfg)
+        assert err.value.code == e.code
+        return
+    assert (dev.n, dev.distinct, dev.total_states, dev.total_nnz) == (host.n, host.distinct, host.total_states,
+                                                                       host.total_nnz)
+    want, got = digests(hs), digests(ds)
+    for m, (a, b) in enumerate(zip(want, got)):
+        bad = [ARRAYS[k] for k in range(17) if a[k] != b[k]]
+        assert not bad, f"{cfg}: model {m}: {bad}"
