@@ -74,15 +74,29 @@ struct DenseLU {
   int n = 0, lda = 0;
   double* U = nullptr;  // caller-owned
   std::vector<int> piv;
-  std::vector<std::vector<std::pair<int, double>>> steps;  // per step: (row, f), rows ascending
+  // step k's multipliers: (rows[i], f[i]) for i in [stepOff[k], stepOff[k + 1]), rows ascending
+  std::vector<int> stepOff, rows;
+  std::vector<double> f;
   void reset(int dim) {
     n = dim;
     piv.assign(static_cast<size_t>(dim), 0);
-    if (steps.size() < static_cast<size_t>(dim)) steps.resize(static_cast<size_t>(dim));
-    for (int k = 0; k < dim; ++k) steps[k].clear();
+    stepOff.assign(static_cast<size_t>(dim) + 1, 0);
+    rows.clear();
+    f.clear();
   }
-  void beginStep(int k, int p) { piv[k] = p; }
-  void log(int k, int r, double f) { steps[k].push_back({r, f}); }
+  void beginStep(int k, int p) {
+    piv[k] = p;
+    stepOff[k] = static_cast<int>(rows.size());
+  }
+  void log(int, int r, double fv) {
+    rows.push_back(r);
+    f.push_back(fv);
+  }
+  void logMany(const int* r, const double* fv, int m) {
+    rows.insert(rows.end(), r, r + m);
+    f.insert(f.end(), fv, fv + m);
+  }
+  void finish() { stepOff[n] = static_cast<int>(rows.size()); }
 };
 // solveDenseInPlace on a row-major A (n x n, leading dimension lda) that records `lu`
 Vec solveDenseRecorded(double* A, int n, int lda, Vec& b, DenseLU& lu, double pivotTol = 1e-12);

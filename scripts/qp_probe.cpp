@@ -61,10 +61,10 @@ int main(int argc, char** argv) {
     }
     bad += h[0] != h[1];
 #ifdef MORAP_QP_PROFILE
-    std::printf("  blocked solve: panel %.3f  list %.3f  pivot rows %.3f  trailing + lookahead %.3f  re-solves %.3f  "
-                "KKT assembly %.3f  rest of the QP %.3f s\n",
+    std::printf("  blocked solve: panels %.3f (inside the next region)  list %.3f  pivot rows %.3f  lookahead + "
+                "overlapped region %.3f  re-solves %.3f  KKT assembly %.3f  rest of the QP %.3f s\n",
                 g_qpProf[0], g_qpProf[1], g_qpProf[2], g_qpProf[3], g_qpProf[4], g_qpProf[5],
-                sec[0] - (g_qpProf[0] + g_qpProf[1] + g_qpProf[2] + g_qpProf[3] + g_qpProf[4] + g_qpProf[5]));
+                sec[0] - (g_qpProf[1] + g_qpProf[2] + g_qpProf[3] + g_qpProf[4] + g_qpProf[5]));
     std::printf("  per projection: eliminations %.1f G row updates (sum dim^3/3), re-solves %.0f\n",
                 g_qpProf[6] / 1e3, g_qpProf[7]);
     std::fill_n(g_qpProf, 8, 0.0);
