@@ -23,7 +23,7 @@ from .cuda import load_library as _load_cuda
 from .errors import MorapError
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-HOST_SO = os.path.join(PKG, "libmorap_host.so")
+HOST_SO = os.environ.get("MORAP_HOST_SO", os.path.join(PKG, "libmorap_host.so"))  # (A/B builds: scripts/)
 
 QUERY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double),
                        C.POINTER(C.c_int32), C.c_int)
