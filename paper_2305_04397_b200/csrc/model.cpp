@@ -225,7 +225,7 @@ ProductMdp buildProduct(const Mdp& agent, const RewardStructure& agentCost, cons
   if (static_cast<int>(agentCost.size()) != agent.numActions())
     fail(Errc::DimensionMismatch, "cost structure does not match the model's action rows");
   checkPreSinks(task);
-  const int L = task.numLetters(), Q = task.numLocations;
+  const int Q = task.numLocations;
   ProductMdp p;
   p.agentId = agentId;
   p.taskId = taskId;
